@@ -1,0 +1,121 @@
+/* C ABI of the B200-native BDDC-SO operator (libbddcso_b200.so).
+ *
+ * The reference (arXiv 2001.07289 package `bddcso`, pure Python) has no native FFI; its
+ * operator interface for this path is the set of Python callables below. Each entry
+ * point here replaces one of them; the ctypes binding that a maintainer adds on the
+ * reference side is shown in INTEGRATION.md (and lives in paper_2001_07289_b200/_capi.py).
+ *
+ *   bddc_setup     <- build_bddc(system, pair, objects, recipe, weights)  bddc.py:393-523
+ *   bddc_refactor  <- build_bddc numeric phase on resident inputs         bddc.py:419-511
+ *   bddc_apply     <- BddcOperator.apply(r) / apply_bddc(bddc, r)          bddc.py:336-380, 526
+ *   bddc_harmonic  <- harmonic_extension(bddc, g) / BddcOperator._harmonic bddc.py:382-390, 530
+ *   bddc_spmv      <- SparseSym.matvec / `A @ v` in run()                   linalg.py:79, experiments.py:232
+ *   bddc_pcg       <- pcg(lambda v: A @ v, op.apply, b, tol, max_iters)    krylov.py:31-92
+ *   bddc_dense_*   <- spd_factor / saddle_factor / their solves            linalg.py:117-212
+ *
+ * Conventions: plain pointers and sizes only; all vectors are float64 over free dofs in
+ * the reference's numbering (mesh.py:97-102). Device pointers where marked; host arrays
+ * in bddc_setup_desc are read during the call only. Return codes:
+ *   0 ok, 1 invalid argument, 2 not SPD (NotSpdError), 3 underconstrained
+ *   (UnderconstrainedError), 4 coarse matrix not SPD (NotSpdError), 5 operator / preconditioner
+ *   not SPD inside PCG (NotSpdOperatorError), 6 CUDA error.
+ * The message buffer `err` (may be NULL) receives the reference-style text.
+ */
+#ifndef BDDCSO_B200_H
+#define BDDCSO_B200_H
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bddc_ctx bddc_ctx;
+
+typedef struct {
+  /* geometry (uniform box partition of the unit box, mesh.py:73 + partition.py:134) */
+  int dim;
+  int cells[3];
+  int subs[3];
+  int element;        /* 0 Q1, 1 P1-Kuhn (informational; elem_K carries the numbers) */
+  int coarse_scaling; /* 0 "reference" (Psi = Phi / s_i^2), 1 "spec" (Psi = Phi) */
+  const double* alpha;  /* [prod(cells)] coefficient per cell */
+  const double* elem_K; /* [2^dim * 2^dim] row-major element matrix for alpha = 1 */
+  /* local layout (identical for all subdomains) */
+  int nloc_nodes, nG, nG_pad, m, m_pad, nblk, nI_pad, nc_pad;
+  const int* node_code; /* [nloc_nodes] >=0 interior row, <0 -(slot+1) */
+  const int* slot_node; /* [nG] */
+  const int* irow_node; /* [nI_pad] -1 on padding rows */
+  /* per-subdomain slots [nsub * nG_pad] and constraints [nsub * nc_pad] */
+  const int* slot_gamma;
+  const double* slot_w;
+  const int* slot_con;
+  const double* slot_coef;
+  const int* con_coarse; /* coarse index in elimination order, -1 on padding */
+  /* interface: global position -> free dof, owner slots (ascending subdomain) */
+  int n_gamma;
+  const long long* gamma_dof;
+  const int* gamma_slots; /* [n_gamma * 2^dim] sub*nG_pad + slot, -1 pad */
+  /* coarse problem */
+  int n_coarse;
+  const int* coarse_slots; /* [n_coarse * 2^dim] sub*nc_pad + k (elimination order), -1 pad */
+  int nnodes;              /* nested-dissection fronts, children before parents */
+  const int* node_sep_start;
+  const int* node_sep_size;
+  const int* node_level;
+  const int* node_parent; /* -1 for roots */
+  const int* bnd_ptr;     /* [nnodes + 1] */
+  const int* bnd_idx;     /* boundary dofs of each front (elimination order, ascending) */
+  const int* rmap;        /* aligned with bnd_idx: position in the parent front */
+  long long nnz;          /* lower-triangular coarse CSR entries */
+  const int* csr_node;    /* front receiving each entry */
+  const int* csr_row;     /* row position in that front */
+  const int* csr_col;     /* column position in that front */
+  const long long* seg_ptr; /* [nnz + 1] contributions per entry */
+  long long ncontrib;
+  const int* contrib; /* index into the local coarse blocks [nsub * nc_pad * nc_pad] */
+} bddc_setup_desc;
+
+typedef struct {
+  int iterations;
+  int converged;
+  double bad_value; /* offending inner product when the return code is 5 */
+  int bad_kind;     /* 0 <r,Br> initial, 1 <p,Ap>, 2 <r,Br> */
+} bddc_pcg_report;
+
+typedef struct {
+  double t_upload_ms, t_local_ms, t_coarse_ms; /* last setup, CUDA events */
+  long long n, n_gamma, n_coarse, nsub;
+  long long factor_bytes, front_bytes, workspace_bytes;
+  int nG_pad, nI_pad, m_pad, nblk, nc_pad, nlevels, max_front;
+} bddc_stats;
+
+int bddc_create(int device, bddc_ctx** out);
+void bddc_destroy(bddc_ctx* ctx);
+int bddc_setup(bddc_ctx* ctx, const bddc_setup_desc* desc, char* err, size_t errlen);
+int bddc_refactor(bddc_ctx* ctx, const double* alpha_host, char* err, size_t errlen);
+int bddc_apply(bddc_ctx* ctx, const double* r_dev, double* z_dev, void* stream);
+int bddc_harmonic(bddc_ctx* ctx, const double* gamma_dev, double* out_dev, void* stream);
+int bddc_spmv(bddc_ctx* ctx, const double* x_dev, double* y_dev, void* stream);
+int bddc_pcg(bddc_ctx* ctx, const double* b_dev, double* x_dev, double tol, int max_iters,
+             double* alphas, double* betas, double* resid, bddc_pcg_report* rep, char* err,
+             size_t errlen);
+int bddc_pcg_host(bddc_ctx* ctx, const double* b_host, double* x_host, double tol, int max_iters,
+                  double* alphas, double* betas, double* resid, bddc_pcg_report* rep, char* err,
+                  size_t errlen);
+int bddc_get_stats(bddc_ctx* ctx, bddc_stats* out);
+int bddc_sync(bddc_ctx* ctx);
+int bddc_kernel_launches_per_apply(bddc_ctx* ctx);
+
+/* dense FP64 batched kernels (column-major, even leading dimensions, device pointers) */
+int bddc_dense_potrf(double* A, int n, int lda, long long stride, int count, int* info_host,
+                     void* stream);
+int bddc_dense_trsm(int kind, const double* L, int n, int ldl, long long sL, double* B,
+                    int nother, int ldb, long long sB, int count, void* stream);
+int bddc_dense_gemm(int transA, int transB, int M, int N, int K, double alpha, const double* A,
+                    int lda, long long sA, const double* B, int ldb, long long sB, double beta,
+                    double* C, int ldc, long long sC, int count, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

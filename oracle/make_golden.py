@@ -1,0 +1,183 @@
+"""TEST INFRASTRUCTURE ONLY — generate golden fixtures from the REFERENCE implementation.
+
+Run in the build container (where /root/reference exists):
+
+    python oracle/make_golden.py
+
+It imports the unmodified reference package ``bddcso`` from /root/reference/pkg/src and
+runs each case through the reference's own public API (build_mesh → partition_uniform →
+refine_uniform → assemble → classify_objects → compute_weights → build_bddc → apply → pcg).
+Two documented extensions are applied by patching, never by editing reference files:
+
+* P1 cases swap ``bddcso.mesh._element_stiffness_box`` (mesh.py:132, its only element
+  hook, used by assemble_cells mesh.py:189) for the P1-Kuhn macro element;
+* "spec" coarse-scaling cases replace ``SaddleFactorization.solve`` (linalg.py:158-172) by
+  the one-line corrected version that scales g and λ by s instead of 1/s;
+* random sources and block coefficients are passed through ``pcg(b=...)`` and the
+  ``CoefficientField`` (the reference takes any b and any α, krylov.py:31, mesh.py:52).
+
+Outputs: tests/golden/<case>.npz (index sets, weights, coarse matrix, B·r on seeded r,
+PCG iterations / α / β / κ / x). The oracle is then pinned against these files by
+tests/test_oracle_golden.py; the GPU path is checked against the oracle.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, ROOT)
+
+import bddcso  # noqa: E402  (reference, read-only)
+import bddcso.linalg as rlin  # noqa: E402
+import bddcso.mesh as rmesh  # noqa: E402
+
+from oracle import bddc_oracle as orc  # noqa: E402
+
+OUT = os.path.join(ROOT, "tests", "golden")
+
+_Q1 = rmesh._element_stiffness_box
+_SOLVE = rlin.SaddleFactorization.solve
+
+
+def _p1_box(lengths, alpha):
+    return alpha * orc.p1_kuhn_element([float(x) for x in lengths])
+
+
+def _spec_solve(self, f, g):
+    f = np.asarray(f, dtype=float)
+    g = np.asarray(g, dtype=float)
+    if self.m == 0:
+        return self._lu.solve(f), np.zeros((0,) + f.shape[1:])
+    s = 1.0 / self._scale  # reference stores 1/s; the corrected solve multiplies by s
+    sol = self._lu.solve(np.concatenate([f, s * g], axis=0))
+    return sol[: self.n], s * sol[self.n:]
+
+
+# (name, dim, cells, subs, split, recipe, weighting, element, coeff, rhs, mode, tol, full)
+CASES = [
+    ("cfg1_p1_ref", 2, (64, 64), (4, 4), 4, "ve", "cardinality", "p1", "const", "one", "reference", 1e-8, False),
+    ("cfg1_p1_spec", 2, (64, 64), (4, 4), 4, "ve", "cardinality", "p1", "const", "one", "spec", 1e-8, False),
+    ("cfg1_q1_ref", 2, (64, 64), (4, 4), 4, "ve", "cardinality", "q1", "const", "one", "reference", 1e-8, False),
+    ("cfg2a_p1_L4h", 2, (128, 128), (4, 4), 8, "ve", "cardinality", "p1", "const", "uniform", "reference", 1e-8, False),
+    ("cfg2a_p1_Lh", 2, (64, 64), (2, 2), 32, "ve", "cardinality", "p1", "const", "uniform", "reference", 1e-8, False),
+    ("cfg2a_p1_LH", 2, (128, 128), (4, 4), 1, "ve", "counting", "p1", "const", "uniform", "reference", 1e-8, False),
+    ("cfg3a_p1_ref", 3, (16, 16, 16), (2, 2, 2), 2, "vef", "cardinality", "p1", "const", "one", "reference", 1e-8, False),
+    ("cfg3b_p1_ref", 3, (24, 24, 24), (3, 3, 3), 2, "vef", "cardinality", "p1", "const", "one", "reference", 1e-8, False),
+    ("cfg4a_p1_spec", 3, (16, 16, 16), (2, 2, 2), 2, "vef", "coefficient", "p1", "blocks", "one", "spec", 1e-8, False),
+    ("cfg4a_p1_ref", 3, (16, 16, 16), (2, 2, 2), 2, "vef", "coefficient", "p1", "blocks", "one", "reference", 1e-8, False),
+    ("q1_3d_vf", 3, (12, 12, 12), (3, 3, 3), 2, "vf", "cardinality", "q1", "const", "one", "reference", 1e-8, False),
+    ("full_p1_2d", 2, (32, 32), (4, 4), 2, "vef", "cardinality", "p1", "const", "one", "spec", 1e-8, True),
+]
+
+
+def _set_element(element):
+    rmesh._element_stiffness_box = _p1_box if element == "p1" else _Q1
+
+
+def _set_mode(mode):
+    rlin.SaddleFactorization.solve = _spec_solve if mode == "spec" else _SOLVE
+
+
+def run_case(case):
+    (name, dim, cells, subs, split, recipe, wmode, element, coeff, rhs, mode, tol, full) = case
+    _set_element(element)
+    _set_mode(mode)
+    mesh = bddcso.build_mesh(dim, cells)
+    if coeff == "const":
+        cf = bddcso.make_constant(mesh, 1.0)
+    else:
+        cf = bddcso.CoefficientField(orc.block_alpha(cells, 4, seed=0))
+    theta = bddcso.partition_uniform(mesh, subs)
+    pair = bddcso.refine_uniform(mesh, theta, split)
+    system = bddcso.assemble(mesh, cf, 1.0)
+    objects = bddcso.classify_objects(pair)
+    weights = bddcso.compute_weights(pair, wmode, cf)
+    recipe_obj = bddcso.Recipe.full() if full else recipe
+    t0 = time.perf_counter()
+    op = bddcso.build_bddc(system, pair, objects, recipe_obj, weights)
+    t_build = time.perf_counter() - t0
+    n = mesh.free_count
+    if rhs == "one":
+        b = system.rhs
+    else:
+        b = orc.load(orc.make_mesh(dim, cells, element), orc.uniform_f(n, seed=0))
+    rng = np.random.default_rng(1234)
+    r = rng.standard_normal(n)
+    Br = op.apply(r)
+    A = system.matrix.tocsr()
+    t0 = time.perf_counter()
+    x, rep = bddcso.pcg(lambda v: A @ v, op.apply, b, tol=tol, max_iters=2000)
+    t_pcg = time.perf_counter() - t0
+
+    # index sets
+    W = 2**dim
+    sig = -np.ones((len(objects), W), dtype=np.int64)
+    own = -np.ones((len(objects), W), dtype=np.int64)
+    kinds = np.array([("vertex", "edge", "face").index(o.kind) for o in objects], dtype=np.int8)
+    dptr = np.zeros(len(objects) + 1, dtype=np.int64)
+    dl = []
+    for i, o in enumerate(objects):
+        sig[i, : len(o.signature)] = o.signature
+        own[i, : len(o.owners)] = o.owners
+        dptr[i + 1] = dptr[i] + len(o.dofs)
+        dl.append(np.asarray(o.dofs))
+    dlist = np.concatenate(dl) if dl else np.zeros(0, np.int64)
+    cons = op.constraints
+    con_obj = np.array([c.object_id for c in cons], dtype=np.int64)
+    con_coeff = np.concatenate([c.coeffs for c in cons]) if len(cons) else np.zeros(0)
+    con_ptr = np.concatenate([[0], np.cumsum([len(c.dofs) for c in cons])]).astype(np.int64)
+    con_dofs = np.concatenate([c.dofs for c in cons]) if len(cons) else np.zeros(0, np.int64)
+    # weights per (gamma dof, member)
+    wsub, wdof, wval = [], [], []
+    for d in pair.membership.gamma_dofs:
+        for s in weights.members(int(d)):
+            wsub.append(s)
+            wdof.append(int(d))
+            wval.append(weights.weight(s, int(d)))
+    cm = op.coarse_matrix.tocsr() if op.coarse_matrix is not None else None
+    out = dict(
+        dim=dim, cells=np.array(cells), subs=np.array(subs), split=split, recipe=recipe,
+        weighting=wmode, element=element, coeff=coeff, rhs_kind=rhs, mode=mode, tol=tol,
+        full=full, n=n, coarse_size=op.coarse_size, gamma_dofs=pair.membership.gamma_dofs,
+        obj_sig=sig, obj_owners=own, obj_kind=kinds, obj_dof_ptr=dptr, obj_dofs=dlist,
+        con_obj=con_obj, con_ptr=con_ptr, con_dofs=con_dofs, con_coeff=con_coeff,
+        w_sub=np.array(wsub), w_dof=np.array(wdof), w_val=np.array(wval),
+        b=b, r=r, Br=Br, x=x, iterations=rep.iterations, converged=rep.converged,
+        kappa=rep.kappa_estimate, ritz=np.array(rep.ritz_extremes),
+        residual_history=np.array(rep.residual_history),
+        t_build=t_build, t_pcg=t_pcg,
+    )
+    if cm is not None and cm.shape[0] <= 4000:
+        out.update(coarse_data=cm.data, coarse_indices=cm.indices, coarse_indptr=cm.indptr)
+    return out
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    names = sys.argv[1:]
+    for case in CASES:
+        if names and case[0] not in names:
+            continue
+        t0 = time.perf_counter()
+        res = run_case(case)
+        np.savez_compressed(os.path.join(OUT, case[0] + ".npz"), **res)
+        print(f"{case[0]:16s} n={res['n']:6d} coarse={res['coarse_size']:5d} "
+              f"its={res['iterations']:4d} kappa={res['kappa']:.10g} "
+              f"({time.perf_counter() - t0:.1f}s)")
+    # SPEC KATs for the combinatorial counter
+    kat = {f"{s}": bddcso.count_coarse_dofs((10, 10, 10), s, "vef") for s in (1, 2, 4, 6, 8)}
+    np.savez(os.path.join(OUT, "count_kat.npz"), **{k: np.array(v) for k, v in kat.items()})
+    print("count KAT", kat)
+    _set_element("q1")
+    _set_mode("reference")
+
+
+if __name__ == "__main__":
+    main()

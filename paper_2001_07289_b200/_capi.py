@@ -1,0 +1,103 @@
+"""ctypes binding of the C ABI in include/bddcso_b200.h (libbddcso_b200.so, built in-tree).
+
+There is no fallback: if the CUDA library is missing or no GPU is present, the device
+operator raises. This is the binding a reference-side maintainer would add.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbddcso_b200.so")
+
+_i = C.c_int
+_ll = C.c_longlong
+_d = C.c_double
+_pi = C.POINTER(C.c_int)
+_pll = C.POINTER(C.c_longlong)
+_pd = C.POINTER(C.c_double)
+_vp = C.c_void_p
+
+EXPORTS = (
+    "bddc_create", "bddc_destroy", "bddc_setup", "bddc_refactor", "bddc_apply", "bddc_harmonic",
+    "bddc_spmv", "bddc_pcg", "bddc_pcg_host", "bddc_get_stats", "bddc_sync",
+    "bddc_kernel_launches_per_apply", "bddc_dense_potrf", "bddc_dense_trsm", "bddc_dense_gemm",
+)
+
+
+class SetupDesc(C.Structure):
+    _fields_ = [
+        ("dim", _i), ("cells", _i * 3), ("subs", _i * 3), ("element", _i), ("coarse_scaling", _i),
+        ("alpha", _pd), ("elem_K", _pd),
+        ("nloc_nodes", _i), ("nG", _i), ("nG_pad", _i), ("m", _i), ("m_pad", _i), ("nblk", _i),
+        ("nI_pad", _i), ("nc_pad", _i),
+        ("node_code", _pi), ("slot_node", _pi), ("irow_node", _pi),
+        ("slot_gamma", _pi), ("slot_w", _pd), ("slot_con", _pi), ("slot_coef", _pd),
+        ("con_coarse", _pi),
+        ("n_gamma", _i), ("gamma_dof", _pll), ("gamma_slots", _pi),
+        ("n_coarse", _i), ("coarse_slots", _pi),
+        ("nnodes", _i), ("node_sep_start", _pi), ("node_sep_size", _pi), ("node_level", _pi),
+        ("node_parent", _pi), ("bnd_ptr", _pi), ("bnd_idx", _pi), ("rmap", _pi),
+        ("nnz", _ll), ("csr_node", _pi), ("csr_row", _pi), ("csr_col", _pi), ("seg_ptr", _pll),
+        ("ncontrib", _ll), ("contrib", _pi),
+    ]
+
+
+class PcgReport(C.Structure):
+    _fields_ = [("iterations", _i), ("converged", _i), ("bad_value", _d), ("bad_kind", _i)]
+
+
+class Stats(C.Structure):
+    _fields_ = [
+        ("t_upload_ms", _d), ("t_local_ms", _d), ("t_coarse_ms", _d),
+        ("n", _ll), ("n_gamma", _ll), ("n_coarse", _ll), ("nsub", _ll),
+        ("factor_bytes", _ll), ("front_bytes", _ll), ("workspace_bytes", _ll),
+        ("nG_pad", _i), ("nI_pad", _i), ("m_pad", _i), ("nblk", _i), ("nc_pad", _i),
+        ("nlevels", _i), ("max_front", _i),
+    ]
+
+
+_lib = None
+
+
+def load(required: bool = True):
+    """Load the library (no GPU needed to load); raise if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        if required:
+            raise RuntimeError(
+                f"CUDA library {LIB_PATH} not built; run `make` or __graft_entry__.build() "
+                "(there is no CPU fallback)")
+        return None
+    lib = C.CDLL(LIB_PATH)
+    lib.bddc_create.argtypes = [_i, C.POINTER(_vp)]
+    lib.bddc_destroy.argtypes = [_vp]
+    lib.bddc_destroy.restype = None
+    lib.bddc_setup.argtypes = [_vp, C.POINTER(SetupDesc), C.c_char_p, C.c_size_t]
+    lib.bddc_refactor.argtypes = [_vp, _pd, C.c_char_p, C.c_size_t]
+    lib.bddc_apply.argtypes = [_vp, _vp, _vp, _vp]
+    lib.bddc_harmonic.argtypes = [_vp, _vp, _vp, _vp]
+    lib.bddc_spmv.argtypes = [_vp, _vp, _vp, _vp]
+    lib.bddc_pcg.argtypes = [_vp, _vp, _vp, _d, _i, _pd, _pd, _pd, C.POINTER(PcgReport),
+                             C.c_char_p, C.c_size_t]
+    lib.bddc_pcg_host.argtypes = [_vp, _pd, _pd, _d, _i, _pd, _pd, _pd, C.POINTER(PcgReport),
+                                  C.c_char_p, C.c_size_t]
+    lib.bddc_get_stats.argtypes = [_vp, C.POINTER(Stats)]
+    lib.bddc_sync.argtypes = [_vp]
+    lib.bddc_kernel_launches_per_apply.argtypes = [_vp]
+    lib.bddc_dense_potrf.argtypes = [_vp, _i, _i, _ll, _i, _pi, _vp]
+    lib.bddc_dense_trsm.argtypes = [_i, _vp, _i, _i, _ll, _vp, _i, _i, _ll, _i, _vp]
+    lib.bddc_dense_gemm.argtypes = [_i, _i, _i, _i, _i, _d, _vp, _i, _ll, _vp, _i, _ll, _d, _vp,
+                                    _i, _ll, _i, _vp]
+    _lib = lib
+    return lib
+
+
+def ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))

@@ -1,0 +1,197 @@
+// Internal structures of the BDDC-SO device operator.
+//
+// Local layout of every subdomain (all subdomains of a uniform box partition share it):
+//   * interior nodes: (b0-1)(b1-1)[(b2-1)] in x-fastest order, grouped in nblk "planes"
+//     along the slowest axis, each plane padded to m_pad rows -> block-tridiagonal A_II;
+//   * surface slots: the box-surface nodes in x-fastest order (= ascending global dof,
+//     the reference's gamma_local order, bddc.py:429-433), padded to nG_pad; Dirichlet
+//     surface nodes keep their slot as a decoupled identity row.
+#pragma once
+#include <vector>
+
+#include "common.cuh"
+#include "dense_f64.cuh"
+
+namespace bddc {
+
+struct Geometry {
+  int dim;
+  int cells[3];
+  int subs[3];
+  int blk[3];
+  int nfree[3];  // free nodes per axis = cells - 1
+  long long n;   // free dofs
+  int nsub;
+  int nloc_nodes;  // prod(blk+1)
+  int m, m_pad, nblk, nI_pad;
+  int nG, nG_pad;
+  int nc_pad;
+  int npe;      // nodes per element = 2^dim
+  double K[64]; // reference element matrix (alpha = 1), row-major npe x npe
+};
+
+// Decoded local node information (host-built tables, device copies).
+struct LocalTables {
+  int* node_code = nullptr;  // [nloc_nodes]: >=0 interior row (j*m_pad+r); <0: -(slot+1)
+  int* slot_node = nullptr;  // [nG]
+  int* irow_node = nullptr;  // [nI_pad] local node of interior row, -1 for pad rows
+};
+
+// Per-subdomain index data (device), shapes [nsub x nG_pad] / [nsub x nc_pad].
+struct SubTables {
+  int* slot_gamma = nullptr;    // global interface index, -1 (Dirichlet / pad)
+  double* slot_w = nullptr;     // weight delta_i(xi)
+  int* slot_con = nullptr;      // local constraint index or -1
+  double* slot_coef = nullptr;  // constraint coefficient (1 or 1/|obj|)
+  int* con_coarse = nullptr;    // coarse index (elimination order) or -1
+};
+
+// Device view of the multifrontal plan (POD: passed by value to kernels).
+struct FrontDev {
+  double* fronts = nullptr;
+  double* upd = nullptr;        // per-node update vectors (solve)
+  int* sep_start = nullptr;
+  int* sep_size = nullptr;
+  int* bnd_size = nullptr;
+  int* ld = nullptr;
+  long long* front_off = nullptr;
+  long long* upd_off = nullptr;
+  int* child_ptr = nullptr;
+  int* child_list = nullptr;
+  int* rmap = nullptr;          // per node: positions of its boundary dofs in the parent front
+  int* rmap_ptr = nullptr;
+  int* bnd_idx = nullptr;       // per node: boundary dofs (elimination order)
+  int* bnd_ptr = nullptr;
+};
+
+// Coarse multifrontal plan (device data + host schedule).
+struct FrontPlan {
+  int n_coarse = 0;
+  int nnodes = 0;
+  int nlevels = 0;
+  // host copies
+  std::vector<int> level_ptr;     // nodes sorted by level: [level_ptr[l], level_ptr[l+1])
+  std::vector<int> sep_start, sep_size, bnd_size, ld;
+  std::vector<long long> front_off, upd_off;
+  std::vector<int> child_ptr, child_list;  // CSR children per node
+  std::vector<int> rmap_off;               // offset of node's rmap into its parent's front
+  std::vector<int> bnd_ptr;                // CSR offsets into bnd_idx
+  std::vector<int> parent;
+  long long front_pool = 0, upd_pool = 0;
+  int max_front = 0;
+  FrontDev d;  // device pointers (POD, passed to kernels)
+  // CSR of the assembled coarse operator (elimination order, lower triangle) + maps
+  long long nnz = 0;
+  long long* csr_front_pos = nullptr;  // [nnz] offset into the front pool
+  long long ncontrib = 0;
+  long long* seg_ptr = nullptr;        // [nnz+1] contributions of each CSR entry
+  int* contrib = nullptr;              // [ncontrib] index into local coarse blocks
+  double* csr_val = nullptr;           // [nnz]
+  int* coarse_slots = nullptr;         // [n_coarse x W] (sub*nc_pad + k), -1 pad
+  int W = 0;
+  std::vector<int> level_list;         // nodes sorted by level (see level_ptr)
+  int* info = nullptr;                 // per node pivot failure (global coarse index)
+};
+
+// Plan-time schedule of the multifrontal factorization: per level, per 64-column panel
+// step, device task arrays for the tile Cholesky / tile TRSM / lower GEMM launches.
+struct LevelSchedule {
+  struct Step {
+    TileTask* potrf = nullptr;
+    int n_potrf = 0;
+    TileTask* trsm = nullptr;
+    int n_trsm = 0, max_trsm = 0;
+    GemmTask* gemm = nullptr;
+    int n_gemm = 0, max_gemm = 0;
+  };
+  std::vector<std::vector<Step>> steps;  // [level][step]
+  int* d_nodes = nullptr;                // level node lists concatenated
+  std::vector<int> nodes_off;
+  int max_children = 0;
+  size_t max_fwd_smem = 0;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  Geometry geo{};
+  int element = 0;
+  int coarse_scaling = 0;  // 0 reference (Psi = Phi / s^2), 1 spec (Psi = Phi)
+  bool setup_done = false;
+  // inputs (device)
+  double* alpha = nullptr;  // [ncells]
+  LocalTables lt;
+  SubTables st;
+  int n_gamma = 0;
+  long long* gamma_dof = nullptr;  // [n_gamma]
+  int* gamma_slots = nullptr;      // [n_gamma x W]
+  // factors (device)
+  double* LI = nullptr;      // [nsub x nblk x 2 x m_pad^2] block-tridiagonal interior factor
+  double* LS = nullptr;      // [nsub x nG_pad^2] Cholesky of S_K = S_Gamma + rho C^T C
+  double* Phi = nullptr;     // [nsub x nG_pad x nc_pad] energy-minimal coarse basis on Gamma
+  double* cscale = nullptr;  // [nsub] c_i (1/s_i^2 reference, 1 spec)
+  double* diag_s = nullptr;  // [nsub] s_i = mean |diag A_i|
+  double* Sloc = nullptr;    // [nsub x nc_pad^2] local coarse blocks (kept for assembly)
+  int* info = nullptr;       // [nsub] interior (A_II) pivot failure per subdomain
+  int* info_k = nullptr;     // [nsub] S_K pivot failure (underconstrained) per subdomain
+  FrontPlan fp;
+  LevelSchedule sched;
+  // apply workspaces (device)
+  double *v1 = nullptr, *v2 = nullptr;    // [n]
+  double* rpg = nullptr;                  // [n_gamma]
+  double *qloc = nullptr, *tloc = nullptr;  // [nsub x nc_pad]
+  double *uloc = nullptr, *wloc = nullptr;  // [nsub x nG_pad]
+  double *crhs = nullptr, *csol = nullptr;  // [n_coarse]
+  // pcg workspaces
+  double *r = nullptr, *z = nullptr, *p = nullptr, *Ap = nullptr;
+  double* red = nullptr;     // reduction partials
+  double* scal = nullptr;    // device scalars
+  double* h_scal = nullptr;  // pinned host mirror
+  // timing of the last setup (ms) per phase
+  float t_local_ms = 0, t_coarse_ms = 0, t_upload_ms = 0;
+  std::vector<void*> allocations;
+
+  template <class T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    BDDC_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    allocations.push_back(p);
+    return (T*)p;
+  }
+  template <class T>
+  T* upload(const T* host, size_t count) {
+    T* d = alloc<T>(count);
+    if (count && host) BDDC_CUDA(cudaMemcpyAsync(d, host, count * sizeof(T), cudaMemcpyHostToDevice, stream));
+    return d;
+  }
+  void free_all() {
+    for (void* p : allocations) cudaFree(p);
+    allocations.clear();
+  }
+};
+
+// local_setup.cu
+void local_setup(Ctx& c, double* workspace, size_t ws_doubles);
+size_t local_setup_workspace(const Geometry& g, int chunk);
+// coarse.cu
+void build_level_schedule(Ctx& c);
+void coarse_assemble_and_factor(Ctx& c);
+void coarse_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s);
+// apply.cu
+void apply_bddc(Ctx& c, const double* r, double* z, cudaStream_t s);
+void spmv(Ctx& c, const double* x, double* y, cudaStream_t s);
+void harmonic_interior(Ctx& c, double* out, cudaStream_t s);
+// pcg.cu
+struct PcgResult {
+  int iterations;
+  int converged;
+  int status;  // 0 ok, 5 not SPD operator
+  double bad_value;
+  int bad_kind;  // 0 <r,Br> (initial), 1 <p,Ap>, 2 <r,Br>
+};
+PcgResult pcg_solve(Ctx& c, const double* b, double* x, double tol, int max_iters, double* alphas,
+                    double* betas, double* resid);
+double dot(Ctx& c, const double* a, const double* b, long long n, cudaStream_t s);
+
+}  // namespace bddc

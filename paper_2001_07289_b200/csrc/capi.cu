@@ -1,0 +1,498 @@
+// C ABI (include/bddcso_b200.h): context, setup upload, numeric factorization, apply, PCG.
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <string>
+
+#include "../../include/bddcso_b200.h"
+#include "bddc_internal.cuh"
+#include "stencil.cuh"
+
+using namespace bddc;
+
+struct bddc_ctx {
+  Ctx c;
+  double* ws = nullptr;
+  size_t ws_doubles = 0;
+  double* alpha_host_shadow = nullptr;
+  long long ncells = 0;
+};
+
+namespace {
+
+constexpr int kNoFail = 0x7f7f7f7f;
+
+void set_err(char* err, size_t len, const std::string& msg) {
+  if (!err || len == 0) return;
+  size_t n = std::min(len - 1, msg.size());
+  memcpy(err, msg.data(), n);
+  err[n] = 0;
+}
+
+struct ApiError {
+  int code;
+  std::string msg;
+};
+
+template <class F>
+int guarded(char* err, size_t len, F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const ApiError& e) {
+    set_err(err, len, e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    set_err(err, len, e.what());
+    return 6;
+  }
+}
+
+__global__ void scatter_gamma_kernel(int n_gamma, const long long* gdof, const double* g, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n_gamma) out[gdof[i]] = g[i];
+}
+
+// numeric setup: local batched factorizations + coarse assembly / multifrontal factor
+void numeric_setup(bddc_ctx* h) {
+  Ctx& c = h->c;
+  cudaStream_t s = c.stream;
+  cudaEvent_t e0, e1, e2;
+  BDDC_CUDA(cudaEventCreate(&e0));
+  BDDC_CUDA(cudaEventCreate(&e1));
+  BDDC_CUDA(cudaEventCreate(&e2));
+  BDDC_CUDA(cudaMemsetAsync(c.info, 0x7f, sizeof(int) * c.geo.nsub, s));
+  BDDC_CUDA(cudaMemsetAsync(c.info_k, 0x7f, sizeof(int) * c.geo.nsub, s));
+  if (c.fp.nnodes) BDDC_CUDA(cudaMemsetAsync(c.fp.info, 0x7f, sizeof(int) * c.fp.nnodes, s));
+  BDDC_CUDA(cudaEventRecord(e0, s));
+  local_setup(c, h->ws, h->ws_doubles);
+  BDDC_CUDA(cudaEventRecord(e1, s));
+  coarse_assemble_and_factor(c);
+  BDDC_CUDA(cudaEventRecord(e2, s));
+  BDDC_CUDA(cudaEventSynchronize(e2));
+  BDDC_CUDA(cudaEventElapsedTime(&c.t_local_ms, e0, e1));
+  BDDC_CUDA(cudaEventElapsedTime(&c.t_coarse_ms, e1, e2));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  const int nsub = c.geo.nsub;
+  std::vector<int> info(nsub), info_k(nsub);
+  BDDC_CUDA(cudaMemcpy(info.data(), c.info, sizeof(int) * nsub, cudaMemcpyDeviceToHost));
+  BDDC_CUDA(cudaMemcpy(info_k.data(), c.info_k, sizeof(int) * nsub, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < nsub; ++i)
+    if (info[i] != kNoFail)
+      throw ApiError{2, "subdomain " + std::to_string(i) +
+                            ": matrix not SPD: nonpositive pivot at index " + std::to_string(info[i])};
+  for (int i = 0; i < nsub; ++i)
+    if (info_k[i] != kNoFail)
+      throw ApiError{3, "subdomain " + std::to_string(i) +
+                            ": saddle system numerically singular (floating subdomain "
+                            "underconstrained or rank-deficient constraints)"};
+  if (c.fp.nnodes) {
+    std::vector<int> fi(c.fp.nnodes);
+    BDDC_CUDA(cudaMemcpy(fi.data(), c.fp.info, sizeof(int) * c.fp.nnodes, cudaMemcpyDeviceToHost));
+    int bad = kNoFail;
+    for (int v : fi) bad = std::min(bad, v);
+    if (bad != kNoFail)
+      throw ApiError{4, "matrix not SPD: nonpositive pivot at index " + std::to_string(bad)};
+  }
+  c.setup_done = true;
+}
+
+void build_plan(Ctx& c, const bddc_setup_desc* d) {
+  FrontPlan& fp = c.fp;
+  fp.n_coarse = d->n_coarse;
+  fp.nnodes = d->nnodes;
+  fp.W = c.geo.npe;
+  if (fp.n_coarse == 0) return;
+  const int N = fp.nnodes;
+  fp.sep_start.assign(d->node_sep_start, d->node_sep_start + N);
+  fp.sep_size.assign(d->node_sep_size, d->node_sep_size + N);
+  fp.parent.assign(d->node_parent, d->node_parent + N);
+  fp.bnd_ptr.assign(d->bnd_ptr, d->bnd_ptr + N + 1);
+  fp.bnd_size.resize(N);
+  fp.ld.resize(N);
+  fp.front_off.resize(N);
+  fp.upd_off.resize(N);
+  int nlev = 0;
+  for (int i = 0; i < N; ++i) nlev = std::max(nlev, d->node_level[i] + 1);
+  fp.nlevels = nlev;
+  long long off = 0, uoff = 0;
+  fp.max_front = 0;
+  for (int i = 0; i < N; ++i) {
+    fp.bnd_size[i] = fp.bnd_ptr[i + 1] - fp.bnd_ptr[i];
+    const int f = fp.sep_size[i] + fp.bnd_size[i];
+    fp.ld[i] = (int)round_up(std::max(f, 2), 2);
+    fp.front_off[i] = off;
+    off += (long long)fp.ld[i] * f;
+    off = round_up(off, 2);
+    fp.upd_off[i] = uoff;
+    uoff += fp.bnd_size[i];
+    fp.max_front = std::max(fp.max_front, f);
+  }
+  fp.front_pool = off;
+  fp.upd_pool = uoff;
+  // children CSR (in node order) and level lists
+  fp.child_ptr.assign(N + 1, 0);
+  for (int i = 0; i < N; ++i)
+    if (fp.parent[i] >= 0) fp.child_ptr[fp.parent[i] + 1]++;
+  for (int i = 0; i < N; ++i) fp.child_ptr[i + 1] += fp.child_ptr[i];
+  fp.child_list.assign(fp.child_ptr[N], 0);
+  {
+    std::vector<int> fill(fp.child_ptr.begin(), fp.child_ptr.end() - 1);
+    for (int i = 0; i < N; ++i)
+      if (fp.parent[i] >= 0) fp.child_list[fill[fp.parent[i]]++] = i;
+  }
+  fp.level_ptr.assign(nlev + 1, 0);
+  for (int i = 0; i < N; ++i) fp.level_ptr[d->node_level[i] + 1]++;
+  for (int l = 0; l < nlev; ++l) fp.level_ptr[l + 1] += fp.level_ptr[l];
+  fp.level_list.assign(N, 0);
+  {
+    std::vector<int> fill(fp.level_ptr.begin(), fp.level_ptr.end() - 1);
+    for (int i = 0; i < N; ++i) fp.level_list[fill[d->node_level[i]]++] = i;
+  }
+  // device copies
+  FrontDev& fd = fp.d;
+  fd.fronts = c.alloc<double>(fp.front_pool);
+  fd.upd = c.alloc<double>(std::max<long long>(fp.upd_pool, 1));
+  fd.sep_start = c.upload(fp.sep_start.data(), N);
+  fd.sep_size = c.upload(fp.sep_size.data(), N);
+  fd.bnd_size = c.upload(fp.bnd_size.data(), N);
+  fd.ld = c.upload(fp.ld.data(), N);
+  fd.front_off = c.upload(fp.front_off.data(), N);
+  fd.upd_off = c.upload(fp.upd_off.data(), N);
+  fd.child_ptr = c.upload(fp.child_ptr.data(), N + 1);
+  fd.child_list = c.upload(fp.child_list.data(), fp.child_list.size());
+  fd.bnd_ptr = c.upload(fp.bnd_ptr.data(), N + 1);
+  fd.bnd_idx = c.upload(d->bnd_idx, fp.bnd_ptr[N]);
+  fd.rmap = c.upload(d->rmap, fp.bnd_ptr[N]);
+  fd.rmap_ptr = fd.bnd_ptr;
+  fp.info = c.alloc<int>(N);
+  // CSR -> front positions
+  fp.nnz = d->nnz;
+  std::vector<long long> pos(d->nnz);
+  for (long long e = 0; e < d->nnz; ++e) {
+    const int nd = d->csr_node[e];
+    pos[e] = fp.front_off[nd] + d->csr_row[e] + (long long)d->csr_col[e] * fp.ld[nd];
+  }
+  fp.csr_front_pos = c.upload(pos.data(), pos.size());
+  fp.seg_ptr = c.upload(d->seg_ptr, d->nnz + 1);
+  fp.ncontrib = d->ncontrib;
+  fp.contrib = c.upload(d->contrib, d->ncontrib);
+  fp.csr_val = c.alloc<double>(d->nnz);
+  fp.coarse_slots = c.upload(d->coarse_slots, (size_t)d->n_coarse * fp.W);
+  build_level_schedule(c);
+}
+
+void do_setup(bddc_ctx* h, const bddc_setup_desc* d) {
+  Ctx& c = h->c;
+  if (!d) throw ApiError{1, "null descriptor"};
+  if (d->dim != 2 && d->dim != 3) throw ApiError{1, "dim must be 2 or 3"};
+  c.free_all();
+  c.setup_done = false;
+  Geometry& G = c.geo;
+  G = Geometry{};
+  G.dim = d->dim;
+  G.npe = 1 << d->dim;
+  long long ncells = 1, n = 1;
+  G.nsub = 1;
+  for (int a = 0; a < 3; ++a) {
+    const bool used = a < d->dim;
+    G.cells[a] = used ? d->cells[a] : 1;
+    G.subs[a] = used ? d->subs[a] : 1;
+    if (used && (G.subs[a] < 1 || G.cells[a] % G.subs[a]))
+      throw ApiError{1, "subdomains must divide the cell grid"};
+    G.blk[a] = G.cells[a] / G.subs[a];
+    G.nfree[a] = used ? G.cells[a] - 1 : 1;
+    ncells *= G.cells[a];
+    if (used) n *= G.nfree[a];
+    G.nsub *= G.subs[a];
+  }
+  G.n = n;
+  G.nloc_nodes = d->nloc_nodes;
+  G.nG = d->nG;
+  G.nG_pad = d->nG_pad;
+  G.m = d->m;
+  G.m_pad = d->m_pad;
+  G.nblk = d->nblk;
+  G.nI_pad = d->nI_pad;
+  G.nc_pad = d->nc_pad;
+  if (G.m_pad > 64 || G.m_pad % 8 || G.nI_pad != G.m_pad * G.nblk)
+    throw ApiError{1, "interior planes must fit one 64-row tile (m_pad <= 64, multiple of 8)"};
+  if (G.nG_pad > 1024 || G.nG_pad % 8 || G.nc_pad > 1024 || G.nc_pad % 8)
+    throw ApiError{1, "interface / constraint padding out of range"};
+  for (int i = 0; i < G.npe * G.npe; ++i) G.K[i] = d->elem_K[i];
+  c.element = d->element;
+  c.coarse_scaling = d->coarse_scaling;
+  h->ncells = ncells;
+
+  cudaEvent_t e0, e1;
+  BDDC_CUDA(cudaEventCreate(&e0));
+  BDDC_CUDA(cudaEventCreate(&e1));
+  BDDC_CUDA(cudaEventRecord(e0, c.stream));
+  c.alpha = c.upload(d->alpha, ncells);
+  c.lt.node_code = c.upload(d->node_code, G.nloc_nodes);
+  c.lt.slot_node = c.upload(d->slot_node, G.nG);
+  c.lt.irow_node = c.upload(d->irow_node, G.nI_pad);
+  const size_t ns = (size_t)G.nsub * G.nG_pad, nc = (size_t)G.nsub * G.nc_pad;
+  c.st.slot_gamma = c.upload(d->slot_gamma, ns);
+  c.st.slot_w = c.upload(d->slot_w, ns);
+  c.st.slot_con = c.upload(d->slot_con, ns);
+  c.st.slot_coef = c.upload(d->slot_coef, ns);
+  c.st.con_coarse = c.upload(d->con_coarse, nc);
+  c.n_gamma = d->n_gamma;
+  c.gamma_dof = c.upload(d->gamma_dof, d->n_gamma);
+  c.gamma_slots = c.upload(d->gamma_slots, (size_t)d->n_gamma * G.npe);
+  build_plan(c, d);
+  BDDC_CUDA(cudaEventRecord(e1, c.stream));
+  BDDC_CUDA(cudaEventSynchronize(e1));
+  BDDC_CUDA(cudaEventElapsedTime(&c.t_upload_ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+
+  // persistent factors and workspaces
+  const long long mm = (long long)G.m_pad * G.m_pad;
+  c.LI = c.alloc<double>((size_t)G.nsub * G.nblk * 2 * mm);
+  c.LS = c.alloc<double>((size_t)G.nsub * G.nG_pad * G.nG_pad);
+  c.Phi = c.alloc<double>((size_t)G.nsub * G.nG_pad * G.nc_pad);
+  c.Sloc = c.alloc<double>((size_t)G.nsub * G.nc_pad * G.nc_pad);
+  c.cscale = c.alloc<double>(G.nsub);
+  c.diag_s = c.alloc<double>(G.nsub);
+  c.info = c.alloc<int>(G.nsub);
+  c.info_k = c.alloc<int>(G.nsub);
+  c.v1 = c.alloc<double>(G.n);
+  c.v2 = c.alloc<double>(G.n);
+  c.rpg = c.alloc<double>(std::max(c.n_gamma, 1));
+  c.qloc = c.alloc<double>(nc);
+  c.tloc = c.alloc<double>(nc);
+  c.uloc = c.alloc<double>(ns);
+  c.wloc = c.alloc<double>(ns);
+  c.crhs = c.alloc<double>(std::max(c.fp.n_coarse, 1));
+  c.csol = c.alloc<double>(std::max(c.fp.n_coarse, 1));
+  c.r = c.alloc<double>(G.n);
+  c.z = c.alloc<double>(G.n);
+  c.p = c.alloc<double>(G.n);
+  c.Ap = c.alloc<double>(G.n);
+  c.red = c.alloc<double>(4096);
+  c.scal = c.alloc<double>(16);
+  BDDC_CUDA(cudaMemsetAsync(c.scal, 0, 16 * sizeof(double), c.stream));
+  // setup workspace: all subdomains at once if it fits in ~60% of the free memory
+  size_t free_b = 0, total_b = 0;
+  BDDC_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const size_t per = local_setup_workspace(G, 1);
+  size_t want = per * G.nsub;
+  size_t cap = (size_t)(0.6 * free_b) / sizeof(double);
+  size_t use = std::min(want, std::max(cap - cap % per, per));
+  h->ws = c.alloc<double>(use);
+  h->ws_doubles = use;
+  numeric_setup(h);
+}
+
+}  // namespace
+
+extern "C" {
+
+int bddc_create(int device, bddc_ctx** out) {
+  if (!out) return 1;
+  try {
+    BDDC_CUDA(cudaSetDevice(device));
+    auto* h = new bddc_ctx();
+    h->c.device = device;
+    BDDC_CUDA(cudaStreamCreateWithFlags(&h->c.stream, cudaStreamNonBlocking));
+    BDDC_CUDA(cudaMallocHost(&h->c.h_scal, 16 * sizeof(double)));
+    *out = h;
+    return 0;
+  } catch (const std::exception&) {
+    return 6;
+  }
+}
+
+void bddc_destroy(bddc_ctx* h) {
+  if (!h) return;
+  cudaSetDevice(h->c.device);
+  cudaStreamSynchronize(h->c.stream);
+  h->c.free_all();
+  if (h->c.h_scal) cudaFreeHost(h->c.h_scal);
+  cudaStreamDestroy(h->c.stream);
+  delete h;
+}
+
+int bddc_setup(bddc_ctx* h, const bddc_setup_desc* d, char* err, size_t errlen) {
+  if (!h) return 1;
+  return guarded(err, errlen, [&] {
+    BDDC_CUDA(cudaSetDevice(h->c.device));
+    do_setup(h, d);
+  });
+}
+
+int bddc_refactor(bddc_ctx* h, const double* alpha_host, char* err, size_t errlen) {
+  if (!h) return 1;
+  return guarded(err, errlen, [&] {
+    if (!h->c.alpha) throw ApiError{1, "bddc_refactor before bddc_setup"};
+    BDDC_CUDA(cudaSetDevice(h->c.device));
+    if (alpha_host)
+      BDDC_CUDA(cudaMemcpyAsync(h->c.alpha, alpha_host, sizeof(double) * h->ncells,
+                                cudaMemcpyHostToDevice, h->c.stream));
+    numeric_setup(h);
+  });
+}
+
+int bddc_apply(bddc_ctx* h, const double* r, double* z, void* stream) {
+  if (!h || !h->c.setup_done) return 1;
+  return guarded(nullptr, 0, [&] {
+    cudaStream_t s = stream ? (cudaStream_t)stream : h->c.stream;
+    if (s != h->c.stream) {  // order after any pending work of the context stream
+      cudaEvent_t e;
+      BDDC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      BDDC_CUDA(cudaEventRecord(e, h->c.stream));
+      BDDC_CUDA(cudaStreamWaitEvent(s, e, 0));
+      cudaEventDestroy(e);
+    }
+    apply_bddc(h->c, r, z, s);
+  });
+}
+
+int bddc_harmonic(bddc_ctx* h, const double* g, double* out, void* stream) {
+  if (!h || !h->c.setup_done) return 1;
+  return guarded(nullptr, 0, [&] {
+    Ctx& c = h->c;
+    cudaStream_t s = stream ? (cudaStream_t)stream : c.stream;
+    const Geometry& G = c.geo;
+    // out_Gamma = g; out_I = A_II^{-1} (0 - A g_ext)_I
+    BDDC_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * G.n, s));
+    BDDC_CUDA(cudaMemsetAsync(c.v1, 0, sizeof(double) * G.n, s));
+    if (c.n_gamma)
+      scatter_gamma_kernel<<<ceil_div(c.n_gamma, 256), 256, 0, s>>>(c.n_gamma, c.gamma_dof, g, out);
+    BDDC_LAUNCH_CHECK();
+    harmonic_interior(c, out, s);
+  });
+}
+
+int bddc_spmv(bddc_ctx* h, const double* x, double* y, void* stream) {
+  if (!h || !h->c.alpha) return 1;
+  return guarded(nullptr, 0, [&] { spmv(h->c, x, y, stream ? (cudaStream_t)stream : h->c.stream); });
+}
+
+int bddc_pcg(bddc_ctx* h, const double* b, double* x, double tol, int max_iters, double* alphas,
+             double* betas, double* resid, bddc_pcg_report* rep, char* err, size_t errlen) {
+  if (!h || !h->c.setup_done) return 1;
+  return guarded(err, errlen, [&] {
+    PcgResult r = pcg_solve(h->c, b, x, tol, max_iters, alphas, betas, resid);
+    if (rep) {
+      rep->iterations = r.iterations;
+      rep->converged = r.converged;
+      rep->bad_value = r.bad_value;
+      rep->bad_kind = r.bad_kind;
+    }
+    if (r.status == 5) {
+      char buf[128];
+      snprintf(buf, sizeof buf, r.bad_kind == 1 ? "operator not SPD: <p, Ap> = %.17g"
+                                                : "preconditioner not SPD: <r, Br> = %.17g",
+               r.bad_value);
+      throw ApiError{5, buf};
+    }
+  });
+}
+
+int bddc_pcg_host(bddc_ctx* h, const double* b_host, double* x_host, double tol, int max_iters,
+                  double* alphas, double* betas, double* resid, bddc_pcg_report* rep, char* err,
+                  size_t errlen) {
+  if (!h || !h->c.setup_done) return 1;
+  int code = 0;
+  code = guarded(err, errlen, [&] {
+    Ctx& c = h->c;
+    const size_t bytes = sizeof(double) * c.geo.n;
+    BDDC_CUDA(cudaMemcpyAsync(c.v2, b_host, bytes, cudaMemcpyHostToDevice, c.stream));
+  });
+  if (code) return code;
+  code = bddc_pcg(h, h->c.v2, h->c.Ap, tol, max_iters, alphas, betas, resid, rep, err, errlen);
+  int code2 = guarded(err, code ? 0 : errlen, [&] {
+    BDDC_CUDA(cudaMemcpyAsync(x_host, h->c.Ap, sizeof(double) * h->c.geo.n, cudaMemcpyDeviceToHost,
+                              h->c.stream));
+    BDDC_CUDA(cudaStreamSynchronize(h->c.stream));
+  });
+  return code ? code : code2;
+}
+
+int bddc_get_stats(bddc_ctx* h, bddc_stats* o) {
+  if (!h || !o) return 1;
+  const Ctx& c = h->c;
+  const Geometry& G = c.geo;
+  memset(o, 0, sizeof(*o));
+  o->t_upload_ms = c.t_upload_ms;
+  o->t_local_ms = c.t_local_ms;
+  o->t_coarse_ms = c.t_coarse_ms;
+  o->n = G.n;
+  o->n_gamma = c.n_gamma;
+  o->n_coarse = c.fp.n_coarse;
+  o->nsub = G.nsub;
+  o->factor_bytes = 8LL * G.nsub * (2LL * G.nblk * G.m_pad * G.m_pad + (long long)G.nG_pad * G.nG_pad +
+                                    (long long)G.nG_pad * G.nc_pad);
+  o->front_bytes = 8LL * c.fp.front_pool;
+  o->workspace_bytes = 8LL * h->ws_doubles;
+  o->nG_pad = G.nG_pad;
+  o->nI_pad = G.nI_pad;
+  o->m_pad = G.m_pad;
+  o->nblk = G.nblk;
+  o->nc_pad = G.nc_pad;
+  o->nlevels = c.fp.nlevels;
+  o->max_front = c.fp.max_front;
+  return 0;
+}
+
+int bddc_sync(bddc_ctx* h) {
+  if (!h) return 1;
+  return cudaStreamSynchronize(h->c.stream) == cudaSuccess ? 0 : 6;
+}
+
+int bddc_kernel_launches_per_apply(bddc_ctx* h) {
+  if (!h) return -1;
+  const Ctx& c = h->c;
+  // bt_solve x2, gamma residual, local_gamma1, coarse gather, fwd/bwd per level,
+  // local_gamma2, gamma gather, residual (memsets are copy-engine ops, not kernels)
+  int n = 2 + 1 + 1 + 1 + 1 + 1;
+  if (c.fp.n_coarse) n += 1 + 2 * c.fp.nlevels;
+  return n;
+}
+
+int bddc_dense_potrf(double* A, int n, int lda, long long stride, int count, int* info_host,
+                     void* stream) {
+  if (!A || n <= 0 || lda < n || (lda & 1) || count <= 0) return 1;
+  return guarded(nullptr, 0, [&] {
+    cudaStream_t s = (cudaStream_t)stream;
+    int* info = nullptr;
+    BDDC_CUDA(cudaMallocAsync((void**)&info, sizeof(int) * count, s));
+    BDDC_CUDA(cudaMemsetAsync(info, 0x7f, sizeof(int) * count, s));
+    potrf_batched(BMat{A, stride, lda}, n, n, count, info, s);
+    if (info_host) {
+      BDDC_CUDA(cudaMemcpyAsync(info_host, info, sizeof(int) * count, cudaMemcpyDeviceToHost, s));
+      BDDC_CUDA(cudaStreamSynchronize(s));
+      for (int i = 0; i < count; ++i)
+        if (info_host[i] == kNoFail) info_host[i] = -1;
+    }
+    BDDC_CUDA(cudaFreeAsync(info, s));
+  });
+}
+
+int bddc_dense_trsm(int kind, const double* L, int n, int ldl, long long sL, double* B, int nother,
+                    int ldb, long long sB, int count, void* stream) {
+  if (!L || !B || kind < 0 || kind > 3 || (ldl & 1) || (ldb & 1)) return 1;
+  return guarded(nullptr, 0, [&] {
+    trsm_batched((TrsmKind)kind, BMat{(double*)L, sL, ldl}, n, BMat{B, sB, ldb}, nother, count,
+                 (cudaStream_t)stream);
+  });
+}
+
+int bddc_dense_gemm(int tA, int tB, int M, int N, int K, double alpha, const double* A, int lda,
+                    long long sA, const double* B, int ldb, long long sB, double beta, double* C,
+                    int ldc, long long sC, int count, void* stream) {
+  if ((lda & 1) || (ldb & 1)) return 1;
+  return guarded(nullptr, 0, [&] {
+    gemm_batched(tA != 0, tB != 0, M, N, K, alpha, BMat{(double*)A, sA, lda}, BMat{(double*)B, sB, ldb},
+                 beta, BMat{C, sC, ldc}, count, (cudaStream_t)stream);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,423 @@
+// Batched FP64 dense kernels (sm_100a). See dense_f64.cuh.
+//
+// GEMM: 64x64x16 CTA tile, 4 warps (2x2), 32x32 warp tile = 4x4 DMMA.8x8x4 accumulators,
+// cp.async double-buffered shared-memory staging. Shared-memory pitches are chosen so the
+// 64-bit fragment reads are bank-conflict free (pitch ≡ 4 mod 16 doubles).
+#include <climits>
+
+#include "dense_f64.cuh"
+
+namespace bddc {
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16;
+constexpr int LDW = BM + 4;  // pitch of [k][m] / [k][n] tiles (m or n contiguous)
+constexpr int LDK = BK + 4;  // pitch of [m][k] / [n][k] tiles (k contiguous)
+constexpr int TILE_A = BK * LDW > BM * LDK ? BK * LDW : BM * LDK;
+constexpr int TILE_B = TILE_A;
+
+struct TaskView {
+  const double* A;
+  const double* B;
+  double* C;
+  int M, N, K, lda, ldb, ldc;
+};
+
+__device__ __forceinline__ TaskView gemm_task(const GemmArgs& a, int b) {
+  if (a.tasks) {
+    const GemmTask& t = a.tasks[b];
+    return TaskView{t.A, t.B, t.C, t.M, t.N, t.K, t.lda, t.ldb, t.ldc};
+  }
+  return TaskView{a.A + b * a.sA, a.B + b * a.sB, a.C + b * a.sC, a.M, a.N, a.K,
+                  a.lda,          a.ldb,          a.ldc};
+}
+
+// Load a BM x BK slice of op(A) (rows m0.., k0..) into shared memory.
+//   !TA: A(m,k) = A[m + k*lda]  -> sm[k*LDW + m]
+//    TA: A(m,k) = A[k + m*lda]  -> sm[m*LDK + k]
+template <bool TA>
+__device__ __forceinline__ void load_a(double* sm, const double* A, int lda, int M, int K, int m0,
+                                       int k0, int tid) {
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    int c = tid + it * 128;
+    if (!TA) {
+      int k = c >> 5, m = (c & 31) * 2;
+      int gm = m0 + m, gk = k0 + k;
+      int valid = (gk < K) ? max(0, min(2, M - gm)) : 0;
+      const double* src = valid ? A + gm + (long long)gk * lda : A;
+      cp_async16(sm + k * LDW + m, src, valid * 8);
+    } else {
+      int m = c >> 3, k = (c & 7) * 2;
+      int gm = m0 + m, gk = k0 + k;
+      int valid = (gm < M) ? max(0, min(2, K - gk)) : 0;
+      const double* src = valid ? A + gk + (long long)gm * lda : A;
+      cp_async16(sm + m * LDK + k, src, valid * 8);
+    }
+  }
+}
+
+// Load a BK x BN slice of op(B) (k0.., cols n0..).
+//   !TB: B(k,n) = B[k + n*ldb]  -> sm[n*LDK + k]
+//    TB: B(k,n) = B[n + k*ldb]  -> sm[k*LDW + n]
+template <bool TB>
+__device__ __forceinline__ void load_b(double* sm, const double* B, int ldb, int N, int K, int n0,
+                                       int k0, int tid) {
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    int c = tid + it * 128;
+    if (!TB) {
+      int n = c >> 3, k = (c & 7) * 2;
+      int gn = n0 + n, gk = k0 + k;
+      int valid = (gn < N) ? max(0, min(2, K - gk)) : 0;
+      const double* src = valid ? B + gk + (long long)gn * ldb : B;
+      cp_async16(sm + n * LDK + k, src, valid * 8);
+    } else {
+      int k = c >> 5, n = (c & 31) * 2;
+      int gn = n0 + n, gk = k0 + k;
+      int valid = (gk < K) ? max(0, min(2, N - gn)) : 0;
+      const double* src = valid ? B + gn + (long long)gk * ldb : B;
+      cp_async16(sm + k * LDW + n, src, valid * 8);
+    }
+  }
+}
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(128) gemm_f64_kernel(GemmArgs args) {
+  __shared__ __align__(16) double As[2][TILE_A];
+  __shared__ __align__(16) double Bs[2][TILE_B];
+  const TaskView t = gemm_task(args, blockIdx.y);
+  const int tiles_m = (t.M + BM - 1) / BM;
+  const int tiles_n = (t.N + BN - 1) / BN;
+  if ((int)blockIdx.x >= tiles_m * tiles_n) return;
+  const int tm = blockIdx.x % tiles_m, tn = blockIdx.x / tiles_m;
+  const int m0 = tm * BM, n0 = tn * BN;
+  if (args.lower && n0 > m0 + BM - 1) return;  // tile strictly above the diagonal
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int g = lane >> 2, q = lane & 3;
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int nk = (t.K + BK - 1) / BK;
+  if (nk > 0) {
+    load_a<TA>(As[0], t.A, t.lda, t.M, t.K, m0, 0, tid);
+    load_b<TB>(Bs[0], t.B, t.ldb, t.N, t.K, n0, 0, tid);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    const int st = kt & 1;
+    if (kt + 1 < nk) {
+      load_a<TA>(As[st ^ 1], t.A, t.lda, t.M, t.K, m0, (kt + 1) * BK, tid);
+      load_b<TB>(Bs[st ^ 1], t.B, t.ldb, t.N, t.K, n0, (kt + 1) * BK, tid);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* as = As[st];
+    const double* bs = Bs[st];
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        int m = wm * 32 + i * 8 + g;
+        af[i] = TA ? as[m * LDK + kk + q] : as[(kk + q) * LDW + m];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        int n = wn * 32 + j * 8 + g;
+        bf[j] = TB ? bs[(kk + q) * LDW + n] : bs[n * LDK + kk + q];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+
+  const double alpha = args.alpha, beta = args.beta;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = m0 + wm * 32 + i * 8 + g;
+    if (row >= t.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = n0 + wn * 32 + j * 8 + 2 * q + e;
+        if (col >= t.N || (args.lower && col > row)) continue;
+        double* cp = t.C + row + (long long)col * t.ldc;
+        double v = alpha * acc[i][j][e];
+        if (beta != 0.0) v += beta * *cp;
+        *cp = v;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// tile kernels (n <= 64)
+// ---------------------------------------------------------------------------------------
+constexpr int TP = kTile + 1;  // odd pitch: conflict-free per-thread vectors
+
+struct TileView {
+  double* L;
+  double* B;
+  int n, ldl, ldb, nvec, id, offset;
+};
+
+__device__ __forceinline__ TileView tile_task(const TileArgs& a, int b) {
+  if (a.tasks) {
+    const TileTask& t = a.tasks[b];
+    return TileView{t.L, t.B, t.n, t.ldl, t.ldb, t.nvec, t.id, t.offset};
+  }
+  return TileView{a.L + b * a.sL, a.B ? a.B + b * a.sB : nullptr, a.n, a.ldl, a.ldb, a.nvec, b,
+                  a.offset};
+}
+
+__global__ void __launch_bounds__(128) potrf_tile_kernel(TileArgs args) {
+  __shared__ double S[kTile * TP];
+  const TileView t = tile_task(args, blockIdx.x);
+  const int n = t.n, tid = threadIdx.x;
+  if (n <= 0) return;
+  for (int idx = tid; idx < n * n; idx += blockDim.x) {
+    int i = idx % n, j = idx / n;
+    if (i >= j) S[i + j * TP] = t.L[i + (long long)j * t.ldl];
+  }
+  __syncthreads();
+  __shared__ int failed;
+  if (tid == 0) failed = INT_MAX;
+  for (int j = 0; j < n; ++j) {
+    if (tid == 0) {
+      double d = S[j + j * TP];
+      if (!(d > 0.0)) {
+        if (failed == INT_MAX) failed = t.offset + j;
+        d = 1.0;
+      }
+      S[j + j * TP] = sqrt(d);
+    }
+    __syncthreads();
+    const double inv = 1.0 / S[j + j * TP];
+    for (int i = j + 1 + tid; i < n; i += blockDim.x) S[i + j * TP] *= inv;
+    __syncthreads();
+    const int r = n - j - 1;
+    for (int idx = tid; idx < r * r; idx += blockDim.x) {
+      int ii = idx % r, kk = idx / r;
+      if (ii >= kk) {
+        int i = j + 1 + ii, k = j + 1 + kk;
+        S[i + k * TP] -= S[i + j * TP] * S[k + j * TP];
+      }
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < n * n; idx += blockDim.x) {
+    int i = idx % n, j = idx / n;
+    if (i >= j) t.L[i + (long long)j * t.ldl] = S[i + j * TP];
+  }
+  if (tid == 0 && failed != INT_MAX && args.info) atomicMin(&args.info[t.id], failed);
+}
+
+// Each thread owns one right-hand-side vector (a row of B for right-side solves, a column
+// for left-side solves); vectors are staged through shared memory with coalesced loads.
+//   FORWARD  (LLN, RLT): x_j = (b_j - sum_{k<j} L[j][k] x_k) / L[j][j]
+//   BACKWARD (LLT, RLN): x_j = (b_j - sum_{k>j} L[k][j] x_k) / L[j][j]
+template <bool RIGHT, bool FORWARD>
+__global__ void __launch_bounds__(64) trsm_tile_kernel(TileArgs args) {
+  extern __shared__ double smem[];
+  double* Ls = smem;              // kTile * TP
+  double* V = smem + kTile * TP;  // 64 vectors * TP
+  const TileView t = tile_task(args, blockIdx.y);
+  const int n = t.n, tid = threadIdx.x;
+  const int v0 = blockIdx.x * 64;
+  if (v0 >= t.nvec || n <= 0) return;
+  const int nv = min(64, t.nvec - v0);
+  for (int idx = tid; idx < n * n; idx += 64) {
+    int i = idx % n, j = idx / n;
+    if (i >= j) Ls[i + j * TP] = t.L[i + (long long)j * t.ldl];
+  }
+  if (RIGHT) {  // B is nvec x n: vector r = row r
+    for (int idx = tid; idx < 64 * n; idx += 64) {
+      int r = idx % 64, k = idx / 64;
+      if (r < nv) V[r * TP + k] = t.B[(v0 + r) + (long long)k * t.ldb];
+    }
+  } else {  // B is n x nvec: vector c = column c
+    for (int idx = tid; idx < 64 * n; idx += 64) {
+      int k = idx % n, c = idx / n;
+      if (c < nv) V[c * TP + k] = t.B[k + (long long)(v0 + c) * t.ldb];
+    }
+  }
+  __syncthreads();
+  if (tid < nv) {
+    double* x = V + tid * TP;
+    if (FORWARD) {
+      for (int j = 0; j < n; ++j) {
+        double s0 = x[j], s1 = 0.0;
+        int k = 0;
+        for (; k + 1 < j; k += 2) {
+          s0 -= Ls[j + k * TP] * x[k];
+          s1 -= Ls[j + (k + 1) * TP] * x[k + 1];
+        }
+        if (k < j) s0 -= Ls[j + k * TP] * x[k];
+        x[j] = (s0 + s1) / Ls[j + j * TP];
+      }
+    } else {
+      for (int j = n - 1; j >= 0; --j) {
+        double s0 = x[j], s1 = 0.0;
+        int k = j + 1;
+        for (; k + 1 < n; k += 2) {
+          s0 -= Ls[k + j * TP] * x[k];
+          s1 -= Ls[k + 1 + j * TP] * x[k + 1];
+        }
+        if (k < n) s0 -= Ls[k + j * TP] * x[k];
+        x[j] = (s0 + s1) / Ls[j + j * TP];
+      }
+    }
+  }
+  __syncthreads();
+  if (RIGHT) {
+    for (int idx = tid; idx < 64 * n; idx += 64) {
+      int r = idx % 64, k = idx / 64;
+      if (r < nv) t.B[(v0 + r) + (long long)k * t.ldb] = V[r * TP + k];
+    }
+  } else {
+    for (int idx = tid; idx < 64 * n; idx += 64) {
+      int k = idx % n, c = idx / n;
+      if (c < nv) t.B[k + (long long)(v0 + c) * t.ldb] = V[c * TP + k];
+    }
+  }
+}
+
+constexpr int kTrsmSmem = 2 * kTile * TP * (int)sizeof(double);
+
+template <bool R, bool F>
+void launch_trsm(const TileArgs& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    BDDC_CUDA(cudaFuncSetAttribute(trsm_tile_kernel<R, F>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmem));
+    attr = true;
+  }
+  int nvec = a.tasks ? a.max_nvec : a.nvec;
+  if (nvec <= 0 || a.count <= 0) return;
+  dim3 grid(ceil_div(nvec, 64), a.count);
+  trsm_tile_kernel<R, F><<<grid, 64, kTrsmSmem, s>>>(a);
+  BDDC_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+void gemm(const GemmArgs& a, bool tA, bool tB, cudaStream_t s) {
+  int M = a.tasks ? a.max_M : a.M, N = a.tasks ? a.max_N : a.N;
+  if (M <= 0 || N <= 0 || a.count <= 0) return;
+  dim3 grid(ceil_div(M, BM) * ceil_div(N, BN), a.count);
+  if (!tA && !tB) gemm_f64_kernel<false, false><<<grid, 128, 0, s>>>(a);
+  else if (!tA && tB) gemm_f64_kernel<false, true><<<grid, 128, 0, s>>>(a);
+  else if (tA && !tB) gemm_f64_kernel<true, false><<<grid, 128, 0, s>>>(a);
+  else gemm_f64_kernel<true, true><<<grid, 128, 0, s>>>(a);
+  BDDC_LAUNCH_CHECK();
+}
+
+void potrf_tile(const TileArgs& a, cudaStream_t s) {
+  if (a.count <= 0) return;
+  potrf_tile_kernel<<<a.count, 128, 0, s>>>(a);
+  BDDC_LAUNCH_CHECK();
+}
+
+void trsm_tile(const TileArgs& a, TrsmKind kind, cudaStream_t s) {
+  switch (kind) {
+    case TRSM_LLN: launch_trsm<false, true>(a, s); break;
+    case TRSM_LLT: launch_trsm<false, false>(a, s); break;
+    case TRSM_RLT: launch_trsm<true, true>(a, s); break;
+    case TRSM_RLN: launch_trsm<true, false>(a, s); break;
+  }
+}
+
+void gemm_batched(bool tA, bool tB, int M, int N, int K, double alpha, BMat A, BMat B,
+                  double beta, BMat C, int count, cudaStream_t s, bool lower) {
+  if (M <= 0 || N <= 0) return;
+  GemmArgs g;
+  g.A = A.p; g.sA = A.stride; g.lda = A.ld;
+  g.B = B.p; g.sB = B.stride; g.ldb = B.ld;
+  g.C = C.p; g.sC = C.stride; g.ldc = C.ld;
+  g.M = M; g.N = N; g.K = K; g.count = count;
+  g.alpha = alpha; g.beta = beta; g.lower = lower ? 1 : 0;
+  if (K <= 0) {
+    if (beta == 1.0) return;
+  }
+  gemm(g, tA, tB, s);
+}
+
+void potrf_batched(BMat A, int n, int npiv, int count, int* info, cudaStream_t s) {
+  for (int k = 0; k < npiv; k += kTile) {
+    const int nb = std::min(kTile, npiv - k);
+    TileArgs t;
+    t.L = A.p + k + (long long)k * A.ld; t.sL = A.stride; t.ldl = A.ld;
+    t.n = nb; t.count = count; t.offset = k; t.info = info;
+    potrf_tile(t, s);
+    const int rest = n - k - nb;
+    if (rest <= 0) continue;
+    TileArgs r = t;
+    r.B = A.p + (k + nb) + (long long)k * A.ld; r.sB = A.stride; r.ldb = A.ld; r.nvec = rest;
+    trsm_tile(r, TRSM_RLT, s);
+    // trailing update A22 -= L21 L21^T (lower tiles only)
+    BMat L21 = A.at(k + nb, k);
+    BMat A22 = A.at(k + nb, k + nb);
+    gemm_batched(false, true, rest, rest, nb, -1.0, L21, L21, 1.0, A22, count, s, true);
+  }
+}
+
+void trsm_batched(TrsmKind kind, BMat L, int n, BMat B, int nother, int count, cudaStream_t s) {
+  const int nblk = ceil_div(n, kTile);
+  auto tile = [&](int kb, BMat Bv) {
+    const int k = kb * kTile, nb = std::min(kTile, n - k);
+    TileArgs t;
+    t.L = L.p + k + (long long)k * L.ld; t.sL = L.stride; t.ldl = L.ld; t.n = nb;
+    t.B = Bv.p; t.sB = Bv.stride; t.ldb = Bv.ld; t.nvec = nother; t.count = count;
+    trsm_tile(t, kind, s);
+  };
+  if (kind == TRSM_LLN) {  // forward over row blocks
+    for (int kb = 0; kb < nblk; ++kb) {
+      const int k = kb * kTile, nb = std::min(kTile, n - k), rest = n - k - nb;
+      tile(kb, B.at(k, 0));
+      if (rest > 0)
+        gemm_batched(false, false, rest, nother, nb, -1.0, L.at(k + nb, k), B.at(k, 0), 1.0,
+                     B.at(k + nb, 0), count, s);
+    }
+  } else if (kind == TRSM_LLT) {  // backward over row blocks
+    for (int kb = nblk - 1; kb >= 0; --kb) {
+      const int k = kb * kTile;
+      tile(kb, B.at(k, 0));
+      if (k > 0)  // B[0:k] -= L[k:k+nb, 0:k]^T X_k
+        gemm_batched(true, false, k, nother, std::min(kTile, n - k), -1.0, L.at(k, 0),
+                     B.at(k, 0), 1.0, B.at(0, 0), count, s);
+    }
+  } else if (kind == TRSM_RLT) {  // forward over column blocks: X L^T = B
+    for (int kb = 0; kb < nblk; ++kb) {
+      const int k = kb * kTile, nb = std::min(kTile, n - k), rest = n - k - nb;
+      tile(kb, B.at(0, k));
+      if (rest > 0)  // B[:, k+nb:] -= X_k L[k+nb:, k]^T
+        gemm_batched(false, true, nother, rest, nb, -1.0, B.at(0, k), L.at(k + nb, k), 1.0,
+                     B.at(0, k + nb), count, s);
+    }
+  } else {  // RLN: backward over column blocks: X L = B
+    for (int kb = nblk - 1; kb >= 0; --kb) {
+      const int k = kb * kTile, nb = std::min(kTile, n - k);
+      tile(kb, B.at(0, k));
+      if (k > 0)  // B[:, 0:k] -= X_k L[k:k+nb, 0:k]
+        gemm_batched(false, false, nother, k, nb, -1.0, B.at(0, k), L.at(k, 0), 1.0,
+                     B.at(0, 0), count, s);
+    }
+  }
+}
+
+}  // namespace bddc

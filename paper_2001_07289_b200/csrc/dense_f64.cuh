@@ -1,0 +1,83 @@
+// Batched FP64 dense kernels for sm_100a: DMMA (mma.sync m8n8k4 f64) grouped GEMM,
+// tile Cholesky and tile triangular solves, plus blocked host drivers.
+//
+// All matrices are column-major. A batch is either strided (base + b*stride, uniform
+// sizes) or an explicit device task array (variable sizes: multifrontal fronts).
+#pragma once
+#include "common.cuh"
+
+namespace bddc {
+
+struct GemmTask {
+  const double* A;
+  const double* B;
+  double* C;
+  int M, N, K, lda, ldb, ldc;
+};
+
+// C = alpha * op(A) op(B) + beta * C; lower != 0 writes only C(i,j) with i >= j.
+struct GemmArgs {
+  const double* A = nullptr;
+  const double* B = nullptr;
+  double* C = nullptr;
+  long long sA = 0, sB = 0, sC = 0;
+  int M = 0, N = 0, K = 0, lda = 0, ldb = 0, ldc = 0;
+  int count = 0;
+  const GemmTask* tasks = nullptr;  // device array; overrides the strided fields
+  int max_M = 0, max_N = 0;         // grid sizing when tasks != nullptr
+  double alpha = 1.0, beta = 1.0;
+  int lower = 0;
+};
+
+struct TileTask {
+  double* L;  // n x n lower tile
+  double* B;  // right-hand sides (see kernels)
+  int n, ldl, ldb, nvec;  // nvec: rows (right side) or columns (left side) of B
+  int id, offset;         // batch entry id and global index of the tile's first row
+};
+
+struct TileArgs {
+  double* L = nullptr;
+  double* B = nullptr;
+  long long sL = 0, sB = 0;
+  int n = 0, ldl = 0, ldb = 0, nvec = 0;
+  int count = 0;
+  const TileTask* tasks = nullptr;
+  int max_nvec = 0;
+  int offset = 0;      // global index of first row (pivot reporting)
+  int* info = nullptr; // per batch entry: first failing pivot (INT_MAX if none)
+};
+
+enum TrsmKind {
+  // side, uplo=lower always
+  TRSM_LLN = 0,  // X = L^{-1} B      (left, no-trans)
+  TRSM_LLT = 1,  // X = L^{-T} B      (left, trans)
+  TRSM_RLT = 2,  // X = B L^{-T}      (right, trans)
+  TRSM_RLN = 3,  // X = B L^{-1}      (right, no-trans)
+};
+
+void gemm(const GemmArgs& a, bool transA, bool transB, cudaStream_t s);
+void potrf_tile(const TileArgs& a, cudaStream_t s);
+void trsm_tile(const TileArgs& a, TrsmKind kind, cudaStream_t s);
+
+// Strided uniform batch view of n x n (or rows x cols) matrices.
+struct BMat {
+  double* p;
+  long long stride;
+  int ld;
+  BMat at(int i, int j) const { return BMat{p + i + (long long)j * ld, stride, ld}; }
+};
+
+// Blocked in-place lower Cholesky of `count` n x n matrices; factors the leading npiv
+// columns only (npiv < n: partial factorization, trailing block becomes the Schur complement).
+void potrf_batched(BMat A, int n, int npiv, int count, int* info, cudaStream_t s);
+// Blocked triangular solves with a batch of n x n lower factors L:
+//   left kinds: B is n x ncol; right kinds: B is nrow x n.
+void trsm_batched(TrsmKind kind, BMat L, int n, BMat B, int nother, int count, cudaStream_t s);
+// C = alpha op(A) op(B) + beta C over a strided batch.
+void gemm_batched(bool tA, bool tB, int M, int N, int K, double alpha, BMat A, BMat B,
+                  double beta, BMat C, int count, cudaStream_t s, bool lower = false);
+
+constexpr int kTile = 64;
+
+}  // namespace bddc

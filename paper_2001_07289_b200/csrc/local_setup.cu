@@ -1,0 +1,323 @@
+// Per-subdomain setup (the batched half of build_bddc, bddc.py:419-492).
+//
+// For every subdomain i (all at once, in chunks that fit the workspace):
+//   1. assemble the local Neumann pieces from alpha (bddc.py:427): block-tridiagonal A_II,
+//      dense A_I,Gamma (into E), dense A_Gamma,Gamma (into LS), s_i = mean|diag A_i|
+//   2. block-tridiagonal Cholesky of A_II (interior factor, bddc.py:436-440)
+//   3. E = L_I^{-1} A_I,Gamma;  S_Gamma = A_GammaGamma - E^T E  (DMMA GEMM)
+//   4. S_K = S_Gamma + s_i C^T C, Cholesky (replaces the KKT LU of linalg.py:175-208;
+//      same constrained solution because C u = 0 there)
+//   5. G = L_S^{-1} C^T, S_C = G^T G, Phi = L_S^{-T} G S_C^{-1}  (energy-minimal basis,
+//      C Phi = I);  Psi = c_i Phi with c_i = 1/s_i^2 ("reference", reproducing
+//      linalg.py:165-171 + bddc.py:457) or 1 ("spec")
+//   6. local coarse block c_i^2 * sym(Phi^T S_Gamma Phi)  (= Psi^T A Psi, bddc.py:464-466)
+#include "stencil.cuh"
+
+namespace bddc {
+
+namespace {
+
+template <int DIM>
+__global__ void __launch_bounds__(256) assemble_local_kernel(Geometry G, const double* __restrict__ alpha,
+                                                             LocalTables lt, int sub0, double* LI,
+                                                             double* E, double* LS,
+                                                             double* diag_s) {
+  const int sub = sub0 + blockIdx.x;
+  const long long b = blockIdx.x;
+  int p[3];
+  sub_coords(G, sub, p);
+  const long long mm = (long long)G.m_pad * G.m_pad;
+  double* li = LI + (long long)sub * G.nblk * 2 * mm;
+  double* e = E + b * (long long)G.nI_pad * G.nG_pad;
+  double* ls = LS + (long long)sub * G.nG_pad * G.nG_pad;
+  constexpr int NOFF = DIM == 3 ? 27 : 9;
+  double dsum = 0.0;
+  int nfree_loc = 0;
+  const int total = G.nloc_nodes * NOFF;
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    const int node = idx / NOFF, o = idx % NOFF;
+    int a[3], d[3] = {o % 3 - 1, (o / 3) % 3 - 1, DIM == 3 ? o / 9 - 1 : 0};
+    local_coords(G, node, a);
+    int bn[3] = {a[0] + d[0], a[1] + d[1], a[2] + d[2]};
+    if (bn[0] < 0 || bn[0] > G.blk[0] || bn[1] < 0 || bn[1] > G.blk[1]) continue;
+    if (DIM == 3 && (bn[2] < 0 || bn[2] > G.blk[2])) continue;
+    const int nb = bn[0] + (G.blk[0] + 1) * (bn[1] + (G.blk[1] + 1) * bn[2]);
+    const bool dir_a = local_to_free(G, p, a) < 0;
+    const bool dir_b = local_to_free(G, p, bn) < 0;
+    const int ca = lt.node_code[node], cb = lt.node_code[nb];
+    if (dir_a || dir_b) {
+      if (node == nb && ca < 0) {
+        const int s = -ca - 1;
+        ls[s + (long long)s * G.nG_pad] = 1.0;
+      }
+      continue;
+    }
+    const double v = local_coef<DIM>(G, alpha, p, a, d);
+    if (node == nb) {
+      dsum += fabs(v);
+      nfree_loc += 1;
+    }
+    if (ca >= 0 && cb >= 0) {
+      const int ja = ca / G.m_pad, jb = cb / G.m_pad, ra = ca % G.m_pad, rb = cb % G.m_pad;
+      if (ja == jb) li[(2LL * ja) * mm + ra + (long long)rb * G.m_pad] = v;
+      else if (ja == jb + 1) li[(2LL * ja + 1) * mm + ra + (long long)rb * G.m_pad] = v;
+    } else if (ca >= 0 && cb < 0) {
+      e[ca + (long long)(-cb - 1) * G.nI_pad] = v;
+    } else if (ca < 0 && cb < 0) {
+      ls[(-ca - 1) + (long long)(-cb - 1) * G.nG_pad] = v;
+    }
+  }
+  // identity on padding
+  for (int idx = threadIdx.x; idx < G.nblk * (G.m_pad - G.m); idx += blockDim.x) {
+    const int j = idx / (G.m_pad - G.m), r = G.m + idx % (G.m_pad - G.m);
+    li[(2LL * j) * mm + r + (long long)r * G.m_pad] = 1.0;
+  }
+  for (int s = G.nG + threadIdx.x; s < G.nG_pad; s += blockDim.x) ls[s + (long long)s * G.nG_pad] = 1.0;
+  // s_i = mean |diag A_i| over local free nodes
+  __shared__ double red[256];
+  __shared__ int cnt[256];
+  red[threadIdx.x] = dsum;
+  cnt[threadIdx.x] = nfree_loc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) {
+      red[threadIdx.x] += red[threadIdx.x + w];
+      cnt[threadIdx.x] += cnt[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) diag_s[sub] = cnt[0] ? red[0] / cnt[0] : 1.0;
+}
+
+// Block-tridiagonal Cholesky of A_II, one CTA per subdomain (blocks of m_pad <= 64):
+//   Lo_j <- Lo_j Ld_{j-1}^{-T};  Ld_j <- chol(T_j - Lo_j Lo_j^T)
+__global__ void __launch_bounds__(128) btchol_kernel(Geometry G, int sub0, double* LI, int* info) {
+  extern __shared__ double sm[];
+  const int M = G.m_pad, P = M + 1;  // odd pitch
+  double* prev = sm;
+  double* cur = sm + M * P;
+  double* off = sm + 2 * M * P;
+  const int sub = sub0 + blockIdx.x;
+  const long long mm = (long long)M * M;
+  double* li = LI + (long long)sub * G.nblk * 2 * mm;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  __shared__ int failed;
+  if (tid == 0) failed = -1;
+  for (int j = 0; j < G.nblk; ++j) {
+    const double* dsrc = li + 2LL * j * mm;
+    for (int idx = tid; idx < M * M; idx += nt) cur[idx % M + (idx / M) * P] = dsrc[idx];
+    if (j > 0) {
+      const double* osrc = li + (2LL * j + 1) * mm;
+      for (int idx = tid; idx < M * M; idx += nt) off[idx % M + (idx / M) * P] = osrc[idx];
+    }
+    __syncthreads();
+    if (j > 0) {
+      // off <- off * prev^{-T}: row r of off solves x prev^T = b (forward)
+      for (int r = tid; r < M; r += nt) {
+        for (int c = 0; c < M; ++c) {
+          double s = off[r + c * P];
+          for (int k = 0; k < c; ++k) s -= off[r + k * P] * prev[c + k * P];
+          off[r + c * P] = s / prev[c + c * P];
+        }
+      }
+      __syncthreads();
+      // cur -= off off^T (lower)
+      for (int idx = tid; idx < M * M; idx += nt) {
+        const int r = idx % M, c = idx / M;
+        if (r < c) continue;
+        double s = 0.0;
+        for (int k = 0; k < M; ++k) s += off[r + k * P] * off[c + k * P];
+        cur[r + c * P] -= s;
+      }
+      __syncthreads();
+    }
+    for (int c = 0; c < M; ++c) {
+      if (tid == 0) {
+        double d = cur[c + c * P];
+        if (!(d > 0.0)) {
+          if (failed < 0) failed = j * M + c;
+          d = 1.0;
+        }
+        cur[c + c * P] = sqrt(d);
+      }
+      __syncthreads();
+      const double inv = 1.0 / cur[c + c * P];
+      for (int r = c + 1 + tid; r < M; r += nt) cur[r + c * P] *= inv;
+      __syncthreads();
+      const int rr = M - c - 1;
+      for (int idx = tid; idx < rr * rr; idx += nt) {
+        const int i = c + 1 + idx % rr, k = c + 1 + idx / rr;
+        if (i >= k) cur[i + k * P] -= cur[i + c * P] * cur[k + c * P];
+      }
+      __syncthreads();
+    }
+    double* ddst = li + 2LL * j * mm;
+    for (int idx = tid; idx < M * M; idx += nt) {
+      const int r = idx % M, c = idx / M;
+      ddst[idx] = r >= c ? cur[r + c * P] : 0.0;
+    }
+    if (j > 0) {
+      double* odst = li + (2LL * j + 1) * mm;
+      for (int idx = tid; idx < M * M; idx += nt) odst[idx] = off[idx % M + (idx / M) * P];
+    }
+    __syncthreads();
+    double* t = prev;
+    prev = cur;
+    cur = t;
+  }
+  if (tid == 0 && failed >= 0) atomicMin(info + sub, failed);
+}
+
+// S += s_i C^T C (one CTA per subdomain): entries of slots sharing a constraint.
+__global__ void add_ctc_kernel(Geometry G, int sub0, SubTables st, const double* diag_s, double* LS) {
+  const int sub = sub0 + blockIdx.x;
+  __shared__ int con[1024];
+  __shared__ double coef[1024];
+  for (int s = threadIdx.x; s < G.nG_pad; s += blockDim.x) {
+    con[s] = st.slot_con[(long long)sub * G.nG_pad + s];
+    coef[s] = st.slot_coef[(long long)sub * G.nG_pad + s];
+  }
+  __syncthreads();
+  const double rho = diag_s[sub];
+  double* ls = LS + (long long)sub * G.nG_pad * G.nG_pad;
+  for (int a = threadIdx.x; a < G.nG_pad; a += blockDim.x) {
+    const int ka = con[a];
+    if (ka < 0) continue;
+    for (int b = 0; b < G.nG_pad; ++b)
+      if (con[b] == ka) ls[a + (long long)b * G.nG_pad] += rho * coef[a] * coef[b];
+  }
+}
+
+// G = C^T (dense nG_pad x nc_pad)
+__global__ void build_ct_kernel(Geometry G, int sub0, SubTables st, double* Gm) {
+  const int sub = sub0 + blockIdx.x;
+  double* g = Gm + (long long)sub * G.nG_pad * G.nc_pad;
+  for (int s = threadIdx.x; s < G.nG_pad; s += blockDim.x) {
+    const int k = st.slot_con[(long long)sub * G.nG_pad + s];
+    if (k >= 0) g[s + (long long)k * G.nG_pad] = st.slot_coef[(long long)sub * G.nG_pad + s];
+  }
+}
+
+// identity on padded constraints of S_C
+__global__ void sc_pad_kernel(Geometry G, int sub0, SubTables st, double* SC) {
+  const int b = blockIdx.x, sub = sub0 + b;
+  double* sc = SC + (long long)b * G.nc_pad * G.nc_pad;
+  for (int k = threadIdx.x; k < G.nc_pad; k += blockDim.x)
+    if (st.con_coarse[(long long)sub * G.nc_pad + k] < 0) sc[k + (long long)k * G.nc_pad] = 1.0;
+}
+
+// Sloc = c^2 * 0.5 (P + P^T);  cscale = c
+__global__ void finish_local_kernel(Geometry G, int sub0, int spec, const double* diag_s,
+                                    double* cscale, const double* P, double* Sloc) {
+  const int b = blockIdx.x, sub = sub0 + b;
+  const double s = diag_s[sub];
+  const double c = spec ? 1.0 : 1.0 / (s * s);
+  if (threadIdx.x == 0) cscale[sub] = c;
+  const int n = G.nc_pad;
+  const double* pp = P + (long long)b * n * n;
+  double* out = Sloc + (long long)sub * n * n;
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    const int i = idx % n, j = idx / n;
+    const double v = 0.5 * (pp[i + j * n] + pp[j + i * n]);
+    out[idx] = (c * c) * v;
+  }
+}
+
+}  // namespace
+
+size_t local_setup_workspace(const Geometry& g, int chunk) {
+  const size_t E = (size_t)g.nI_pad * g.nG_pad;
+  const size_t SG = (size_t)g.nG_pad * g.nG_pad;
+  const size_t X = (size_t)g.nG_pad * g.nc_pad;
+  const size_t SC = (size_t)g.nc_pad * g.nc_pad;
+  return (size_t)chunk * (E + SG + X + 2 * SC);
+}
+
+void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
+  const Geometry& G = c.geo;
+  cudaStream_t s = c.stream;
+  const size_t per = local_setup_workspace(G, 1);
+  int chunk = (int)std::min<size_t>(G.nsub, ws_doubles / per);
+  if (chunk <= 0) throw CudaError("local setup workspace too small");
+  const long long mm = (long long)G.m_pad * G.m_pad;
+  const long long liS = (long long)G.nblk * 2 * mm;
+  const long long lsS = (long long)G.nG_pad * G.nG_pad;
+  const long long phS = (long long)G.nG_pad * G.nc_pad;
+  const long long scS = (long long)G.nc_pad * G.nc_pad;
+  const long long eS = (long long)G.nI_pad * G.nG_pad;
+  const int btchol_smem = 3 * G.m_pad * (G.m_pad + 1) * (int)sizeof(double);
+  BDDC_CUDA(cudaFuncSetAttribute(btchol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, btchol_smem));
+
+  for (int sub0 = 0; sub0 < G.nsub; sub0 += chunk) {
+    const int cnt = std::min(chunk, G.nsub - sub0);
+    double* E = ws;
+    double* SG = E + (size_t)chunk * eS;
+    double* X = SG + (size_t)chunk * lsS;
+    double* SC = X + (size_t)chunk * phS;
+    double* P = SC + (size_t)chunk * scS;
+    double* LI = c.LI;  // indexed by global sub inside kernels
+    double* LS = c.LS + sub0 * lsS;
+    double* PH = c.Phi + sub0 * phS;
+    BDDC_CUDA(cudaMemsetAsync(c.LI + sub0 * liS, 0, sizeof(double) * cnt * liS, s));
+    BDDC_CUDA(cudaMemsetAsync(E, 0, sizeof(double) * cnt * eS, s));
+    BDDC_CUDA(cudaMemsetAsync(LS, 0, sizeof(double) * cnt * lsS, s));
+    BDDC_CUDA(cudaMemsetAsync(PH, 0, sizeof(double) * cnt * phS, s));
+    // 1. assembly
+    if (G.dim == 2)
+      assemble_local_kernel<2><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, LI, E, c.LS, c.diag_s);
+    else
+      assemble_local_kernel<3><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, LI, E, c.LS, c.diag_s);
+    BDDC_LAUNCH_CHECK();
+    // 2. interior block-tridiagonal Cholesky
+    btchol_kernel<<<cnt, 128, btchol_smem, s>>>(G, sub0, LI, c.info);
+    BDDC_LAUNCH_CHECK();
+    // 3. E <- L_I^{-1} E, block forward substitution over planes
+    for (int j = 0; j < G.nblk; ++j) {
+      BMat Ej{E + (long long)j * G.m_pad, eS, G.nI_pad};
+      if (j > 0) {
+        BMat Lo{c.LI + sub0 * liS + (2LL * j + 1) * mm, liS, G.m_pad};
+        BMat Ejm{E + (long long)(j - 1) * G.m_pad, eS, G.nI_pad};
+        gemm_batched(false, false, G.m_pad, G.nG_pad, G.m_pad, -1.0, Lo, Ejm, 1.0, Ej, cnt, s);
+      }
+      TileArgs t;
+      t.L = c.LI + sub0 * liS + 2LL * j * mm; t.sL = liS; t.ldl = G.m_pad; t.n = G.m_pad;
+      t.B = Ej.p; t.sB = eS; t.ldb = G.nI_pad; t.nvec = G.nG_pad; t.count = cnt;
+      trsm_tile(t, TRSM_LLN, s);
+    }
+    // S_Gamma = A_GG - E^T E  (in LS)
+    BMat Eb{E, eS, G.nI_pad};
+    BMat LSb{LS, lsS, G.nG_pad};
+    gemm_batched(true, false, G.nG_pad, G.nG_pad, G.nI_pad, -1.0, Eb, Eb, 1.0, LSb, cnt, s);
+    BDDC_CUDA(cudaMemcpyAsync(SG, LS, sizeof(double) * cnt * lsS, cudaMemcpyDeviceToDevice, s));
+    // 4. S_K = S_Gamma + s C^T C; Cholesky
+    add_ctc_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, c.diag_s, c.LS);
+    BDDC_LAUNCH_CHECK();
+    potrf_batched(LSb, G.nG_pad, G.nG_pad, cnt, c.info_k + sub0, s);
+    if (G.nc_pad > 0) {
+      // 5. G = L_S^{-1} C^T ; S_C = G^T G ; Phi = L_S^{-T} G S_C^{-1}
+      build_ct_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, c.Phi);
+      BDDC_LAUNCH_CHECK();
+      BMat PHb{PH, phS, G.nG_pad};
+      BMat SCb{SC, scS, G.nc_pad};
+      trsm_batched(TRSM_LLN, LSb, G.nG_pad, PHb, G.nc_pad, cnt, s);
+      gemm_batched(true, false, G.nc_pad, G.nc_pad, G.nG_pad, 1.0, PHb, PHb, 0.0, SCb, cnt, s);
+      sc_pad_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, SC);
+      BDDC_LAUNCH_CHECK();
+      potrf_batched(SCb, G.nc_pad, G.nc_pad, cnt, nullptr, s);
+      trsm_batched(TRSM_RLT, SCb, G.nc_pad, PHb, G.nG_pad, cnt, s);
+      trsm_batched(TRSM_RLN, SCb, G.nc_pad, PHb, G.nG_pad, cnt, s);
+      trsm_batched(TRSM_LLT, LSb, G.nG_pad, PHb, G.nc_pad, cnt, s);
+      // 6. P = Phi^T (S_Gamma Phi)
+      BMat SGb{SG, lsS, G.nG_pad};
+      BMat Xb{X, phS, G.nG_pad};
+      BMat Pb{P, scS, G.nc_pad};
+      gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nG_pad, 1.0, SGb, PHb, 0.0, Xb, cnt, s);
+      gemm_batched(true, false, G.nc_pad, G.nc_pad, G.nG_pad, 1.0, PHb, Xb, 0.0, Pb, cnt, s);
+      finish_local_kernel<<<cnt, 256, 0, s>>>(G, sub0, c.coarse_scaling, c.diag_s, c.cscale, P,
+                                              c.Sloc);
+      BDDC_LAUNCH_CHECK();
+    }
+  }
+}
+
+}  // namespace bddc

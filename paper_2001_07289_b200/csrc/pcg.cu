@@ -1,0 +1,194 @@
+// Device PCG (krylov.py:31-92): x0 = 0, recurrence residual, stop at ||r|| <= tol ||b||.
+// SpMV is fused with <p, Ap>; the x / r update is fused with ||r||^2; all reductions are
+// two-pass over a fixed grid, hence deterministic. One host synchronisation per
+// iteration reads {rz, pAp, rr} for the stopping test, the SPD guards and the Lanczos
+// coefficients (alpha_k, beta_k).
+#include "stencil.cuh"
+
+namespace bddc {
+
+namespace {
+
+constexpr int kRedBlocks = 592;  // 4 x 148 SMs
+constexpr int kRedThreads = 256;
+
+__device__ __forceinline__ void block_partial(double v, double* partial) {
+  __shared__ double red[kRedThreads / 32];
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < kRedThreads / 32; ++i) s += red[i];
+    partial[blockIdx.x] = s;
+  }
+}
+
+__global__ void __launch_bounds__(kRedThreads) dot_partial_kernel(const double* __restrict__ a,
+                                                                  const double* __restrict__ b,
+                                                                  long long n, double* partial) {
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    acc += a[i] * b[i];
+  block_partial(acc, partial);
+}
+
+__global__ void reduce_final_kernel(const double* __restrict__ partial, int np, double* out) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) acc += partial[i];
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+    *out = s;
+  }
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(kRedThreads) spmv_dot_kernel(Geometry G, const double* __restrict__ alpha,
+                                                               const double* __restrict__ p,
+                                                               double* __restrict__ Ap, double* partial) {
+  double acc = 0.0;
+  for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < G.n;
+       f += (long long)gridDim.x * blockDim.x) {
+    int g0, g1, g2;
+    free_coords(G, f, g0, g1, g2);
+    const double v = stencil_row<DIM>(G, alpha, p, g0, g1, g2);
+    Ap[f] = v;
+    acc += p[f] * v;
+  }
+  block_partial(acc, partial);
+}
+
+// alpha = rz / pAp; x += alpha p; r -= alpha Ap; partial ||r||^2
+__global__ void __launch_bounds__(kRedThreads) update_xr_kernel(double* __restrict__ x, double* __restrict__ r,
+                                                                const double* __restrict__ p,
+                                                                const double* __restrict__ Ap,
+                                                                const double* __restrict__ scal,
+                                                                long long n, double* partial) {
+  const double a = scal[0] / scal[1];
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    x[i] += a * p[i];
+    const double ri = r[i] - a * Ap[i];
+    r[i] = ri;
+    acc += ri * ri;
+  }
+  block_partial(acc, partial);
+}
+
+// beta = rz_new / rz; p = z + beta p
+__global__ void xpay_kernel(double* __restrict__ p, const double* __restrict__ z,
+                            const double* __restrict__ scal, long long n) {
+  const double b = scal[3] / scal[0];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    p[i] = z[i] + b * p[i];
+}
+
+__global__ void copy_scalar_kernel(double* dst, const double* src) { *dst = *src; }
+
+}  // namespace
+
+double dot(Ctx& c, const double* a, const double* b, long long n, cudaStream_t s) {
+  dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(a, b, n, c.red);
+  reduce_final_kernel<<<1, 1024, 0, s>>>(c.red, kRedBlocks, c.scal + 7);
+  BDDC_LAUNCH_CHECK();
+  BDDC_CUDA(cudaMemcpyAsync(c.h_scal + 7, c.scal + 7, sizeof(double), cudaMemcpyDeviceToHost, s));
+  BDDC_CUDA(cudaStreamSynchronize(s));
+  return c.h_scal[7];
+}
+
+static void dot_to(Ctx& c, const double* a, const double* b, long long n, double* out, cudaStream_t s) {
+  dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(a, b, n, c.red);
+  reduce_final_kernel<<<1, 1024, 0, s>>>(c.red, kRedBlocks, out);
+  BDDC_LAUNCH_CHECK();
+}
+
+PcgResult pcg_solve(Ctx& c, const double* b, double* x, double tol, int max_iters, double* alphas,
+                    double* betas, double* resid) {
+  const Geometry& G = c.geo;
+  cudaStream_t s = c.stream;
+  const long long n = G.n;
+  PcgResult res{0, 0, 0, 0.0, 0};
+  double* sc = c.scal;
+  double* hs = c.h_scal;
+  BDDC_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
+  BDDC_CUDA(cudaMemcpyAsync(c.r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  dot_to(c, c.r, c.r, n, sc + 4, s);
+  apply_bddc(c, c.r, c.z, s);
+  dot_to(c, c.r, c.z, n, sc + 0, s);
+  BDDC_CUDA(cudaMemcpyAsync(hs, sc, sizeof(double) * 8, cudaMemcpyDeviceToHost, s));
+  BDDC_CUDA(cudaStreamSynchronize(s));
+  const double norm0 = sqrt(hs[4]);
+  resid[0] = norm0;
+  if (norm0 == 0.0) {
+    res.converged = 1;
+    return res;
+  }
+  double rz = hs[0];
+  if (!(rz > 0.0)) {
+    res.status = 5; res.bad_value = rz; res.bad_kind = 0;
+    return res;
+  }
+  BDDC_CUDA(cudaMemcpyAsync(c.p, c.z, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  int nbeta = 0;
+  for (int it = 0; it < max_iters; ++it) {
+    if (G.dim == 2) spmv_dot_kernel<2><<<kRedBlocks, kRedThreads, 0, s>>>(G, c.alpha, c.p, c.Ap, c.red);
+    else spmv_dot_kernel<3><<<kRedBlocks, kRedThreads, 0, s>>>(G, c.alpha, c.p, c.Ap, c.red);
+    reduce_final_kernel<<<1, 1024, 0, s>>>(c.red, kRedBlocks, sc + 1);
+    update_xr_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(x, c.r, c.p, c.Ap, sc, n, c.red);
+    reduce_final_kernel<<<1, 1024, 0, s>>>(c.red, kRedBlocks, sc + 2);
+    BDDC_LAUNCH_CHECK();
+    BDDC_CUDA(cudaMemcpyAsync(hs, sc, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
+    BDDC_CUDA(cudaStreamSynchronize(s));
+    if (it > 0) {  // rz_new of the previous iteration is now in hs[0]
+      const double rz_new = hs[0];
+      if (!(rz_new > 0.0)) {
+        res.status = 5; res.bad_value = rz_new; res.bad_kind = 2;
+        res.iterations = it;
+        return res;
+      }
+      betas[nbeta++] = rz_new / rz;
+      rz = rz_new;
+    }
+    const double pAp = hs[1];
+    if (!(pAp > 0.0)) {
+      res.status = 5; res.bad_value = pAp; res.bad_kind = 1;
+      res.iterations = it;
+      return res;
+    }
+    alphas[it] = hs[0] / pAp;
+    const double rn = sqrt(hs[2]);
+    resid[it + 1] = rn;
+    res.iterations = it + 1;
+    if (rn <= tol * norm0) {
+      res.converged = 1;
+      break;
+    }
+    if (it + 1 == max_iters) {
+      // the reference computes one more B-apply and beta that the Lanczos step ignores
+      apply_bddc(c, c.r, c.z, s);
+      dot_to(c, c.r, c.z, n, sc + 3, s);
+      BDDC_CUDA(cudaMemcpyAsync(hs + 3, sc + 3, sizeof(double), cudaMemcpyDeviceToHost, s));
+      BDDC_CUDA(cudaStreamSynchronize(s));
+      if (!(hs[3] > 0.0)) {
+        res.status = 5; res.bad_value = hs[3]; res.bad_kind = 2;
+      }
+      break;
+    }
+    apply_bddc(c, c.r, c.z, s);
+    dot_to(c, c.r, c.z, n, sc + 3, s);
+    xpay_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(c.p, c.z, sc, n);
+    copy_scalar_kernel<<<1, 1, 0, s>>>(sc + 0, sc + 3);
+    BDDC_LAUNCH_CHECK();
+  }
+  return res;
+}
+
+}  // namespace bddc

@@ -1,0 +1,120 @@
+// Matrix-free element-by-element operator on the structured grid.
+//
+// (A x)[g] = sum over the 2^d cells c containing node g of alpha_c * sum_t K[s][t] x[c + t],
+// with s = g - c the node's corner in c and x = 0 on Dirichlet nodes. This is the
+// assembled operator of mesh.py:172-198 applied without storing it: 8 B of alpha per cell
+// plus the x / y streams, instead of 12 B per CSR nonzero.
+#pragma once
+#include "bddc_internal.cuh"
+
+namespace bddc {
+
+__device__ __forceinline__ long long free_id(const Geometry& G, int g0, int g1, int g2) {
+  return (long long)(g0 - 1) + (long long)G.nfree[0] * ((g1 - 1) + (long long)G.nfree[1] * (g2 - 1));
+}
+
+__device__ __forceinline__ long long cell_id(const Geometry& G, int c0, int c1, int c2) {
+  return (long long)c0 + (long long)G.cells[0] * (c1 + (long long)G.cells[1] * c2);
+}
+
+__device__ __forceinline__ void free_coords(const Geometry& G, long long f, int& g0, int& g1,
+                                            int& g2) {
+  g0 = (int)(f % G.nfree[0]) + 1;
+  f /= G.nfree[0];
+  if (G.dim == 3) {
+    g1 = (int)(f % G.nfree[1]) + 1;
+    g2 = (int)(f / G.nfree[1]) + 1;
+  } else {
+    g1 = (int)f + 1;
+    g2 = 0;
+  }
+}
+
+// Row g of A applied to x (g is a free node).
+template <int DIM>
+__device__ __forceinline__ double stencil_row(const Geometry& G, const double* __restrict__ alpha,
+                                              const double* __restrict__ x, int g0, int g1,
+                                              int g2) {
+  constexpr int NPE = 1 << DIM;
+  double acc = 0.0;
+#pragma unroll
+  for (int s = 0; s < NPE; ++s) {
+    const int c0 = g0 - (s & 1), c1 = g1 - ((s >> 1) & 1), c2 = DIM == 3 ? g2 - ((s >> 2) & 1) : 0;
+    const double a = __ldg(alpha + cell_id(G, c0, c1, c2));
+    double part = 0.0;
+#pragma unroll
+    for (int t = 0; t < NPE; ++t) {
+      const double k = G.K[s * NPE + t];
+      if (k == 0.0) continue;
+      const int n0 = c0 + (t & 1), n1 = c1 + ((t >> 1) & 1), n2 = DIM == 3 ? c2 + ((t >> 2) & 1) : 1;
+      if (n0 == 0 || n0 == G.cells[0] || n1 == 0 || n1 == G.cells[1]) continue;
+      if (DIM == 3 && (n2 == 0 || n2 == G.cells[2])) continue;
+      part += k * __ldg(x + free_id(G, n0, n1, DIM == 3 ? n2 : 1));
+    }
+    acc += a * part;
+  }
+  return acc;
+}
+
+// Coefficient A_i(a, a + d) of subdomain p's local Neumann matrix (local node coords a),
+// summing only cells of the subdomain box (bddc.py:427 via assemble_cells).
+template <int DIM>
+__device__ __forceinline__ double local_coef(const Geometry& G, const double* __restrict__ alpha,
+                                             const int p[3], const int a[3], const int d[3]) {
+  constexpr int NPE = 1 << DIM;
+  double acc = 0.0;
+  // candidate cell offsets per axis: d=0 -> {a-1, a}; d=1 -> {a}; d=-1 -> {a-1}
+#pragma unroll
+  for (int s = 0; s < NPE; ++s) {
+    int cc[3] = {0, 0, 0};
+    bool ok = true;
+#pragma unroll
+    for (int ax = 0; ax < DIM; ++ax) {
+      const int bit = (s >> ax) & 1;  // 1: cell below the node on this axis
+      if (d[ax] == 1 && bit) ok = false;
+      if (d[ax] == -1 && !bit) ok = false;
+      cc[ax] = a[ax] - bit;
+      if (cc[ax] < 0 || cc[ax] >= G.blk[ax]) ok = false;
+    }
+    if (!ok) continue;
+    int ca = 0, cb = 0;
+#pragma unroll
+    for (int ax = 0; ax < DIM; ++ax) {
+      ca |= ((s >> ax) & 1) << ax;
+      cb |= (a[ax] + d[ax] - cc[ax]) << ax;
+    }
+    const double k = G.K[ca * NPE + cb];
+    if (k == 0.0) continue;
+    const long long cid = cell_id(G, p[0] * G.blk[0] + cc[0], p[1] * G.blk[1] + cc[1],
+                                  DIM == 3 ? p[2] * G.blk[2] + cc[2] : 0);
+    acc += __ldg(alpha + cid) * k;
+  }
+  return acc;
+}
+
+__device__ __forceinline__ void sub_coords(const Geometry& G, int sub, int p[3]) {
+  p[0] = sub % G.subs[0];
+  p[1] = (sub / G.subs[0]) % G.subs[1];
+  p[2] = G.dim == 3 ? sub / (G.subs[0] * G.subs[1]) : 0;
+}
+
+__device__ __forceinline__ void local_coords(const Geometry& G, int node, int a[3]) {
+  a[0] = node % (G.blk[0] + 1);
+  a[1] = (node / (G.blk[0] + 1)) % (G.blk[1] + 1);
+  a[2] = G.dim == 3 ? node / ((G.blk[0] + 1) * (G.blk[1] + 1)) : 0;
+}
+
+// Global free dof of local node a of subdomain p, or -1 if it is a Dirichlet node.
+__device__ __forceinline__ long long local_to_free(const Geometry& G, const int p[3],
+                                                   const int a[3]) {
+  const int g0 = p[0] * G.blk[0] + a[0], g1 = p[1] * G.blk[1] + a[1];
+  if (g0 == 0 || g0 == G.cells[0] || g1 == 0 || g1 == G.cells[1]) return -1;
+  int g2 = 1;
+  if (G.dim == 3) {
+    g2 = p[2] * G.blk[2] + a[2];
+    if (g2 == 0 || g2 == G.cells[2]) return -1;
+  }
+  return free_id(G, g0, g1, g2);
+}
+
+}  // namespace bddc

@@ -1,0 +1,228 @@
+"""Host construction of the device operator's index tables (integer work, bit-exact).
+
+Everything the CUDA setup needs besides the coefficient: the local layout shared by all
+subdomains of a uniform box partition, per-subdomain interface slots with weights and
+constraint membership, interface / coarse gather tables, and the coarse symbolic plan.
+Reference correspondence (bddc.py:404-492):
+
+* local dofs ascending, gamma_local / interior_local split       bddc.py:420-433
+* constraint rows in coarse_id order of the constraints owned   bddc.py:411-414, 441-450
+* gamma_weights aligned with gamma_global                        bddc.py:472
+* gamma_positions / coarse_ids scatter targets                   bddc.py:360, 371, 490
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import symbolic
+from .partition import PartitionPair
+from .weights import ConstraintTable, WeightingOperator
+
+
+def _round(x: int, m: int) -> int:
+    return (x + m - 1) // m * m
+
+
+@dataclass
+class LocalLayout:
+    dim: int
+    blk: tuple
+    nloc_nodes: int
+    nG: int
+    nG_pad: int
+    m: int
+    m_pad: int
+    nblk: int
+    nI_pad: int
+    node_code: np.ndarray   # >=0 interior row j*m_pad + r; <0 −(slot+1)
+    slot_node: np.ndarray   # [nG]
+    irow_node: np.ndarray   # [nI_pad], −1 on padding
+    slot_coords: np.ndarray  # [nG, dim] local node coordinates
+
+
+def local_layout(dim: int, blk: tuple) -> LocalLayout:
+    npd = [b + 1 for b in blk]
+    nloc = int(np.prod(npd))
+    ids = np.arange(nloc)
+    coords = np.zeros((nloc, dim), dtype=np.int64)
+    rem = ids.copy()
+    for d in range(dim):
+        coords[:, d] = rem % npd[d]
+        rem //= npd[d]
+    interior = np.all((coords >= 1) & (coords <= np.asarray(blk) - 1), axis=1)
+    m = int(np.prod([b - 1 for b in blk[:-1]]))
+    nblk = blk[-1] - 1
+    m_pad = _round(max(m, 1), 8)
+    nI_pad = m_pad * max(nblk, 0)
+    code = np.zeros(nloc, dtype=np.int32)
+    # interior row: plane j = last coord − 1, row r = x-fastest index over the other coords
+    r = np.zeros(nloc, dtype=np.int64)
+    st = 1
+    for d in range(dim - 1):
+        r += (coords[:, d] - 1) * st
+        st *= blk[d] - 1
+    j = coords[:, dim - 1] - 1
+    row = j * m_pad + r
+    code[interior] = row[interior]
+    surf = np.flatnonzero(~interior)
+    code[surf] = -(np.arange(len(surf)) + 1)
+    nG = len(surf)
+    irow = -np.ones(nI_pad, dtype=np.int32)
+    irow[row[interior]] = np.flatnonzero(interior)
+    return LocalLayout(dim, tuple(blk), nloc, nG, _round(nG, 8), m, m_pad, max(nblk, 0), nI_pad,
+                       code, surf.astype(np.int32), irow, coords[surf])
+
+
+@dataclass
+class DevicePlan:
+    layout: LocalLayout
+    nsub: int
+    nc_pad: int
+    slot_gamma: np.ndarray
+    slot_w: np.ndarray
+    slot_con: np.ndarray
+    slot_coef: np.ndarray
+    con_coarse: np.ndarray
+    gamma_dof: np.ndarray
+    gamma_slots: np.ndarray
+    coarse_slots: np.ndarray
+    coarse: symbolic.CoarsePlan | None
+    n_con_local: np.ndarray
+
+
+def build_device_plan(pair: PartitionPair, cons: ConstraintTable,
+                      weights: WeightingOperator) -> DevicePlan:
+    mesh = pair.mesh
+    layout_info = pair.box_layout
+    if layout_info is None:
+        raise ValueError("the device operator needs a uniform box partition (partition_uniform)")
+    subs, blk = layout_info
+    dim = mesh.dim
+    lay = local_layout(dim, blk)
+    nsub = int(np.prod(subs))
+    W = 2**dim
+    objects = cons.objects
+    ms = pair.membership
+    gamma = ms.gamma_dofs
+    nfree = mesh.free_count
+    gidx = -np.ones(nfree, dtype=np.int64)
+    gidx[gamma] = np.arange(len(gamma))
+
+    # subdomain lattice coordinates (x-fastest ids, partition.py:146-153)
+    pid = np.arange(nsub)
+    pc = np.zeros((nsub, dim), dtype=np.int64)
+    rem = pid.copy()
+    for d in range(dim):
+        pc[:, d] = rem % subs[d]
+        rem //= subs[d]
+
+    # global free dof of every (sub, slot)
+    gcoords = pc[:, None, :] * np.asarray(blk)[None, None, :] + lay.slot_coords[None, :, :]
+    cells = np.asarray(mesh.cells_per_dim)
+    dirichlet = np.any((gcoords == 0) | (gcoords == cells), axis=2)
+    nf = cells - 1
+    fid = np.zeros(gcoords.shape[:2], dtype=np.int64)
+    st = 1
+    for d in range(dim):
+        fid += (gcoords[:, :, d] - 1) * st
+        st *= int(nf[d])
+    fid[dirichlet] = -1
+    nG, nG_pad = lay.nG, lay.nG_pad
+
+    # constraint of each free dof
+    n_con = len(cons)
+    con_of = -np.ones(nfree, dtype=np.int64)
+    coef_of = np.zeros(nfree)
+    cnt = np.diff(cons.dof_ptr)
+    con_of[cons.dof_list] = np.repeat(np.arange(n_con), cnt)
+    coef_of[cons.dof_list] = cons.coeff
+
+    # local constraint numbering: constraints owned by p in coarse-id order
+    con_owners = objects.owners[cons.con_obj] if n_con else np.zeros((0, W), np.int64)
+    pv = con_owners >= 0
+    pair_sub = con_owners[pv]
+    pair_con = np.broadcast_to(np.arange(n_con)[:, None], con_owners.shape)[pv]
+    order = np.lexsort((pair_con, pair_sub))
+    pair_sub, pair_con = pair_sub[order], pair_con[order]
+    n_local = np.bincount(pair_sub, minlength=nsub)
+    sub_con_ptr = np.concatenate([[0], np.cumsum(n_local)]).astype(np.int64)
+    local_k = np.arange(len(pair_sub)) - sub_con_ptr[pair_sub]
+    nc_max = int(n_local.max()) if nsub else 0
+    nc_pad = _round(max(nc_max, 1), 8)
+    pair_key = pair_sub * max(n_con, 1) + pair_con
+
+    def lookup_k(sub, con):
+        key = sub * max(n_con, 1) + con
+        pos = np.searchsorted(pair_key, key)
+        return local_k[pos]
+
+    valid = fid >= 0
+    slot_gamma = -np.ones((nsub, nG_pad), dtype=np.int32)
+    slot_w = np.zeros((nsub, nG_pad))
+    slot_con = -np.ones((nsub, nG_pad), dtype=np.int32)
+    slot_coef = np.zeros((nsub, nG_pad))
+    sub_idx = np.broadcast_to(pid[:, None], fid.shape)
+    fv = fid[valid]
+    sv = sub_idx[valid]
+    sg = slot_gamma[:, :nG]
+    sg[valid] = gidx[fv]
+    if np.any(gidx[fv] < 0):
+        raise AssertionError("a free surface node is not on the interface")
+    slot_gamma[:, :nG] = sg
+    sw = slot_w[:, :nG]
+    sw[valid] = weights.weights_for(sv, fv)
+    slot_w[:, :nG] = sw
+    cv = con_of[fv]
+    has = cv >= 0
+    sc = slot_con[:, :nG]
+    tmp = -np.ones(len(fv), dtype=np.int64)
+    tmp[has] = lookup_k(sv[has], cv[has])
+    sc[valid] = tmp
+    slot_con[:, :nG] = sc
+    sco = slot_coef[:, :nG]
+    sco[valid] = np.where(has, coef_of[fv], 0.0)
+    slot_coef[:, :nG] = sco
+
+    # coarse plan (elimination order) and the constraint maps
+    plan = None
+    con_coarse = -np.ones((nsub, nc_pad), dtype=np.int32)
+    coarse_slots = -np.ones((max(n_con, 0), W), dtype=np.int32)
+    if n_con:
+        plan = symbolic.analyze(n_con, con_owners, pc, tuple(subs), sub_con_ptr=sub_con_ptr,
+                                sub_con_ids=pair_con)
+        symbolic.coarse_csr(plan, sub_con_ptr, pair_con, nc_pad)
+        con_coarse[pair_sub, local_k] = plan.iperm[pair_con]
+        # owners of each constraint (ascending) -> slot sub*nc_pad + k, rows in elimination order
+        ks = np.where(pv, 0, -1).astype(np.int64)
+        ks[pv] = lookup_k(con_owners[pv], np.broadcast_to(np.arange(n_con)[:, None], con_owners.shape)[pv])
+        slots = np.where(pv, con_owners * nc_pad + ks, -1)
+        coarse_slots = slots[plan.perm].astype(np.int32)
+
+    # interface gather: owner slots of each gamma dof, ascending subdomain
+    gobj = objects.dof_obj[gamma]
+    gown = objects.owners[gobj]  # (n_gamma, W) ascending, −1 padded
+    gv = gown >= 0
+    gcoord = np.zeros((len(gamma), dim), dtype=np.int64)
+    rem = gamma.copy()
+    for d in range(dim):
+        gcoord[:, d] = rem % nf[d] + 1
+        rem //= nf[d]
+    slot_of_node = np.full(lay.nloc_nodes, -1, dtype=np.int64)
+    slot_of_node[lay.slot_node] = np.arange(nG)
+    npd = np.asarray(blk) + 1
+    loc = gcoord[:, None, :] - pc[np.maximum(gown, 0)] * np.asarray(blk)[None, None, :]
+    lnode = np.zeros(gown.shape, dtype=np.int64)
+    st = 1
+    for d in range(dim):
+        lnode += loc[:, :, d] * st
+        st *= int(npd[d])
+    sl = slot_of_node[np.where(gv, lnode, 0)]
+    if np.any(gv & (sl < 0)):
+        raise AssertionError("interface dof does not map to a surface slot")
+    gamma_slots = np.where(gv, gown * nG_pad + sl, -1).astype(np.int32)
+
+    return DevicePlan(lay, nsub, nc_pad, slot_gamma, slot_w, slot_con, slot_coef, con_coarse,
+                      gamma.astype(np.int64), gamma_slots, coarse_slots, plan, n_local)

@@ -1,0 +1,500 @@
+"""Subdomain partitions, refinements, membership and interface-object classification.
+
+Vectorised, bit-exact restatement of ``bddcso.partition`` (reference
+``pkg/src/bddcso/partition.py``). The reference loops over parts and runs one
+``ndimage.label`` over the whole grid per part (partition.py:63-73, 106-114), which is
+O(N̂·cells); here every step is O(cells) array work so cfg5 (16.6M dofs, 262k
+subsubdomains) classifies in seconds.
+
+Index-set contract (SURVEY §8(a′)), reproduced exactly:
+* Θ: Σ_d (i_d // block_d)·stride_d, x-fastest over the subdomain grid (partition.py:134-153)
+* Θ̂ (uniform): p·s^d + Σ_d ((i_d − lo_d)//(block_d/s))·s^d (partition.py:171-199)
+* membership: sorted distinct labels of the cells containing each free dof (partition.py:117-131)
+* objects: Γ dofs grouped by Θ̂-signature, ordered like Python tuples (proper prefix first),
+  dofs ascending; kind vertex / face(3D)·edge(2D) / edge; owners = sorted parents
+  (partition.py:223-250)
+
+Signatures are stored as fixed-width int rows padded with −1 *after* the labels; a
+lexicographic row sort then equals Python tuple order, because −1 sorts below every
+label exactly where a shorter tuple would.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from functools import cached_property
+from typing import Sequence
+
+import numpy as np
+import scipy.sparse as sp
+from scipy.sparse.csgraph import connected_components
+
+from .mesh import CoefficientField, StructuredMesh
+
+KINDS = ("vertex", "edge", "face")
+_KIND_CODE = {k: i for i, k in enumerate(KINDS)}
+
+
+# --------------------------------------------------------------------------------------
+# membership tables
+# --------------------------------------------------------------------------------------
+
+def _node_cells(mesh: StructuredMesh) -> np.ndarray:
+    """(free_count, 2^d) ids of the cells containing each free node (all exist for free nodes)."""
+    dim = mesh.dim
+    npd = mesh.nodes_per_dim
+    free = mesh.free_nodes
+    coords = np.empty((len(free), dim), dtype=np.int64)
+    rem = free.copy()
+    for d in range(dim):
+        coords[:, d] = rem % npd[d]
+        rem //= npd[d]
+    cstrides = np.cumprod((1,) + tuple(mesh.cells_per_dim[:-1])).astype(np.int64)
+    out = np.empty((len(free), 2**dim), dtype=np.int64)
+    for c in range(2**dim):
+        cid = np.zeros(len(free), dtype=np.int64)
+        for d in range(dim):
+            cid += (coords[:, d] - ((c >> d) & 1)) * cstrides[d]
+        out[:, c] = cid
+    return out
+
+
+def _sorted_unique_rows(labels: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """Per row: sorted distinct values, padded with −1 at the end; and the distinct count."""
+    s = np.sort(labels, axis=1)
+    dup = np.zeros_like(s, dtype=bool)
+    dup[:, 1:] = s[:, 1:] == s[:, :-1]
+    big = np.iinfo(s.dtype).max
+    s = np.where(dup, big, s)
+    s.sort(axis=1)
+    count = (s != big).sum(axis=1)
+    s[s == big] = -1
+    return s, count
+
+
+class _TupleView:
+    """Read-only list-like view of padded signature rows as Python tuples."""
+
+    def __init__(self, rows: np.ndarray, counts: np.ndarray):
+        self._rows = rows
+        self._counts = counts
+
+    def __len__(self):
+        return len(self._rows)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        i = int(i)
+        return tuple(int(v) for v in self._rows[i, : self._counts[i]])
+
+    def __iter__(self):
+        for i in range(len(self)):
+            yield self[i]
+
+
+@dataclass(frozen=True)
+class MembershipSets:
+    """Per free dof, the subdomains / subsubdomains whose closure contains it (partition.py:21-28).
+
+    ``on_gamma`` / ``on_gamma_hat`` behave like the reference's lists of tuples; the
+    array forms (``theta_rows``/``hat_rows`` padded with −1, and counts) are what the
+    vectorised code uses.
+    """
+
+    on_gamma: _TupleView
+    on_gamma_hat: _TupleView
+    gamma_dofs: np.ndarray
+    gamma_hat_dofs: np.ndarray
+    theta_rows: np.ndarray
+    theta_counts: np.ndarray
+    hat_rows: np.ndarray
+    hat_counts: np.ndarray
+
+
+@dataclass(frozen=True)
+class InterfaceObject:
+    """partition.py:31-37."""
+
+    id: int
+    kind: str
+    dofs: np.ndarray
+    signature: tuple
+    owners: tuple
+
+
+class ObjectTable:
+    """Array form of the classified objects, list-like over :class:`InterfaceObject`.
+
+    Fields (n_obj objects, W = 2^d):
+      signature (n_obj, W) int64, −1 padded;  sig_len (n_obj,)
+      owners    (n_obj, W) int64, −1 padded;  owner_len (n_obj,)
+      kind      (n_obj,) int8 code into KINDS
+      dof_ptr   (n_obj+1,) CSR into dof_list (ascending free-dof ids per object)
+      dof_obj   (free_count,) object id per free dof, −1 off Γ
+    """
+
+    def __init__(self, dim, signature, sig_len, owners, owner_len, kind, dof_ptr, dof_list,
+                 dof_obj):
+        self.dim = dim
+        self.signature = signature
+        self.sig_len = sig_len
+        self.owners = owners
+        self.owner_len = owner_len
+        self.kind = kind
+        self.dof_ptr = dof_ptr
+        self.dof_list = dof_list
+        self.dof_obj = dof_obj
+
+    def __len__(self):
+        return len(self.kind)
+
+    def dof_count(self) -> np.ndarray:
+        return np.diff(self.dof_ptr)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        i = int(i)
+        if i < 0:
+            i += len(self)
+        if not 0 <= i < len(self):
+            raise IndexError(i)
+        return InterfaceObject(
+            id=i,
+            kind=KINDS[int(self.kind[i])],
+            dofs=self.dof_list[self.dof_ptr[i]: self.dof_ptr[i + 1]].copy(),
+            signature=tuple(int(v) for v in self.signature[i, : self.sig_len[i]]),
+            owners=tuple(int(v) for v in self.owners[i, : self.owner_len[i]]),
+        )
+
+    def __iter__(self):
+        for i in range(len(self)):
+            yield self[i]
+
+
+# --------------------------------------------------------------------------------------
+# partitions
+# --------------------------------------------------------------------------------------
+
+def _face_components(mesh: StructuredMesh, labels: np.ndarray) -> np.ndarray:
+    """Number of face-connected components per label (one O(cells) graph pass)."""
+    grid = mesh.cells_grid(np.arange(mesh.cell_count))
+    lab = mesh.cells_grid(labels)
+    rows, cols = [], []
+    for ax in range(mesh.dim):
+        a = np.take(grid, np.arange(grid.shape[ax] - 1), axis=ax).ravel()
+        b = np.take(grid, np.arange(1, grid.shape[ax]), axis=ax).ravel()
+        la = np.take(lab, np.arange(lab.shape[ax] - 1), axis=ax).ravel()
+        lb = np.take(lab, np.arange(1, lab.shape[ax]), axis=ax).ravel()
+        keep = la == lb
+        rows.append(a[keep])
+        cols.append(b[keep])
+    rows = np.concatenate(rows)
+    cols = np.concatenate(cols)
+    g = sp.coo_matrix((np.ones(len(rows), dtype=np.int8), (rows, cols)),
+                      shape=(mesh.cell_count, mesh.cell_count))
+    _, comp = connected_components(g, directed=False)
+    count = int(labels.max()) + 1
+    # distinct (label, component) pairs per label
+    pairs = np.unique(labels.astype(np.int64) * (comp.max() + 1) + comp)
+    return np.bincount(pairs // (comp.max() + 1), minlength=count)
+
+
+class PartitionPair:
+    """Coarse partition Θ and nested refinement Θ̂ over mesh cells (partition.py:40-91)."""
+
+    def __init__(self, mesh: StructuredMesh, theta: np.ndarray, theta_hat: np.ndarray,
+                 validate: bool = True):
+        theta = np.asarray(theta, dtype=np.int64)
+        theta_hat = np.asarray(theta_hat, dtype=np.int64)
+        if theta.shape != (mesh.cell_count,) or theta_hat.shape != (mesh.cell_count,):
+            raise ValueError("partition arrays must have one entry per cell")
+        self.mesh = mesh
+        self.theta = theta
+        self.theta_hat = theta_hat
+        self.subdomain_count = int(theta.max()) + 1
+        self.subsubdomain_count = int(theta_hat.max()) + 1
+        self.parent = _parent_map(theta, theta_hat, self.subsubdomain_count)
+        if validate:
+            self._validate()
+
+    def _validate(self):
+        """partition.py:63-73: contiguous, nonempty, face-connected parts."""
+        for name, labels, count in (
+            ("subdomain", self.theta, self.subdomain_count),
+            ("subsubdomain", self.theta_hat, self.subsubdomain_count),
+        ):
+            sizes = np.bincount(labels, minlength=count)
+            if np.any(sizes == 0):
+                raise ValueError(f"{name} ids must be contiguous and nonempty")
+            ncomp = _face_components(self.mesh, labels)
+            bad = np.flatnonzero(ncomp != 1)
+            if bad.size:
+                raise ValueError(f"{name} {int(bad[0])} is not face-connected")
+
+    @cached_property
+    def membership(self) -> MembershipSets:
+        """partition.py:75-83 with _node_membership (117-131) as array work."""
+        cells = _node_cells(self.mesh)
+        th_rows, th_cnt = _sorted_unique_rows(self.theta[cells])
+        hat_rows, hat_cnt = _sorted_unique_rows(self.theta_hat[cells])
+        return MembershipSets(
+            on_gamma=_TupleView(th_rows, th_cnt),
+            on_gamma_hat=_TupleView(hat_rows, hat_cnt),
+            gamma_dofs=np.flatnonzero(th_cnt >= 2).astype(np.int64),
+            gamma_hat_dofs=np.flatnonzero(hat_cnt >= 2).astype(np.int64),
+            theta_rows=th_rows,
+            theta_counts=th_cnt,
+            hat_rows=hat_rows,
+            hat_counts=hat_cnt,
+        )
+
+    @cached_property
+    def grounded_subdomains(self) -> np.ndarray:
+        """partition.py:85-91: subdomains whose closure meets the Dirichlet boundary."""
+        touches = np.zeros(self.subdomain_count, dtype=bool)
+        cell_on_boundary = self.mesh.boundary_mask[self.mesh.cell_nodes].any(axis=1)
+        touches[np.unique(self.theta[cell_on_boundary])] = True
+        return touches
+
+    @cached_property
+    def box_layout(self):
+        """Uniform box structure of Θ if it has one: (subs_per_dim, block) else None."""
+        return _uniform_box_layout(self.mesh, self.theta)
+
+
+def _parent_map(theta, theta_hat, hat_count) -> np.ndarray:
+    """partition.py:94-103: parent subdomain of each subsubdomain; error if one spans two."""
+    first = np.full(hat_count, len(theta_hat), dtype=np.int64)
+    np.minimum.at(first, theta_hat, np.arange(len(theta_hat)))
+    parent = np.full(hat_count, -1, dtype=np.int64)
+    seen = first < len(theta_hat)
+    parent[seen] = theta[first[seen]]
+    bad = np.flatnonzero(parent[theta_hat] != theta)
+    if bad.size:
+        c = int(bad[0])
+        hat = int(theta_hat[c])
+        raise ValueError(
+            f"subsubdomain {hat} spans subdomains {int(parent[hat])} and {int(theta[c])}"
+        )
+    return parent
+
+
+def partition_uniform(mesh: StructuredMesh, subdomains_per_dim: Sequence[int]) -> np.ndarray:
+    """Block partition, lexicographic subdomain ids (partition.py:134-153)."""
+    subs = tuple(int(s) for s in subdomains_per_dim)
+    if len(subs) != mesh.dim:
+        raise ValueError(f"expected {mesh.dim} subdomain counts, got {len(subs)}")
+    if any(s < 1 for s in subs):
+        raise ValueError("subdomain counts must be positive")
+    for d in range(mesh.dim):
+        if mesh.cells_per_dim[d] % subs[d] != 0:
+            raise ValueError(
+                f"{subs[d]} subdomains do not divide {mesh.cells_per_dim[d]} cells on axis {d}"
+            )
+    blocks = [mesh.cells_per_dim[d] // subs[d] for d in range(mesh.dim)]
+    multi = mesh.cell_multi_indices()
+    theta = np.zeros(mesh.cell_count, dtype=np.int64)
+    stride = 1
+    for d in range(mesh.dim):
+        theta += (multi[:, d] // blocks[d]) * stride
+        stride *= subs[d]
+    return theta
+
+
+def _subdomain_boxes(mesh: StructuredMesh, theta: np.ndarray):
+    """Bounding cell box per part (partition.py:156-168); error if a part is not a box."""
+    multi = mesh.cell_multi_indices()
+    count = int(theta.max()) + 1
+    lo = np.full((count, mesh.dim), np.iinfo(np.int64).max, dtype=np.int64)
+    hi = np.full((count, mesh.dim), -1, dtype=np.int64)
+    for d in range(mesh.dim):
+        np.minimum.at(lo[:, d], theta, multi[:, d])
+        np.maximum.at(hi[:, d], theta, multi[:, d])
+    sizes = np.bincount(theta, minlength=count)
+    vol = np.prod(hi - lo + 1, axis=1)
+    bad = np.flatnonzero(sizes != vol)
+    if bad.size:
+        raise ValueError(f"subdomain {int(bad[0])} is not a box; uniform refinement undefined")
+    return lo, hi
+
+
+def _uniform_box_layout(mesh: StructuredMesh, theta: np.ndarray):
+    """(subs_per_dim, block) if Θ equals partition_uniform(mesh, subs_per_dim), else None."""
+    try:
+        lo, hi = _subdomain_boxes(mesh, theta)
+    except ValueError:
+        return None
+    block = tuple(int(b) for b in (hi[0] - lo[0] + 1))
+    if any(mesh.cells_per_dim[d] % block[d] for d in range(mesh.dim)):
+        return None
+    subs = tuple(mesh.cells_per_dim[d] // block[d] for d in range(mesh.dim))
+    if int(np.prod(subs)) != len(lo):
+        return None
+    if not np.array_equal(theta, partition_uniform(mesh, subs)):
+        return None
+    return subs, block
+
+
+def refine_uniform(mesh: StructuredMesh, theta: np.ndarray, split: int,
+                   validate: bool = True) -> PartitionPair:
+    """Split every box subdomain into split^dim equal blocks (partition.py:171-199)."""
+    split = int(split)
+    if split < 1:
+        raise ValueError("split must be a positive integer")
+    theta = np.asarray(theta, dtype=np.int64)
+    if split == 1:
+        return PartitionPair(mesh, theta, theta.copy(), validate=validate)
+    lo, hi = _subdomain_boxes(mesh, theta)
+    size = hi - lo + 1
+    bad = np.flatnonzero(np.any(size % split != 0, axis=1))
+    if bad.size:
+        p = int(bad[0])
+        raise ValueError(
+            f"split {split} does not divide subdomain {p} of size {tuple(int(v) for v in size[p])}"
+        )
+    block = size // split
+    multi = mesh.cell_multi_indices()
+    local = (multi - lo[theta]) // block[theta]
+    sub_id = np.zeros(mesh.cell_count, dtype=np.int64)
+    stride = 1
+    for d in range(mesh.dim):
+        sub_id += local[:, d] * stride
+        stride *= split
+    theta_hat = theta * split**mesh.dim + sub_id
+    return PartitionPair(mesh, theta, theta_hat, validate=validate)
+
+
+def refine_by_coefficient(mesh: StructuredMesh, theta: np.ndarray, coeff: CoefficientField,
+                          validate: bool = True) -> PartitionPair:
+    """Face-connected components of equal coefficient inside each subdomain (partition.py:202-220).
+
+    Numbering follows the reference: parts in id order, then coefficient values ascending,
+    then components in ``ndimage.label`` order (first cell in C/grid order, i.e. the
+    reversed-axis raster = x-fastest cell id order).
+    """
+    theta = np.asarray(theta, dtype=np.int64)
+    alpha = np.asarray(coeff.alpha, dtype=float)
+    # key cells by (part, value rank); components of equal key via face adjacency
+    _, vrank = np.unique(alpha, return_inverse=True)
+    key = theta * (int(vrank.max()) + 1) + vrank
+    grid = mesh.cells_grid(np.arange(mesh.cell_count))
+    kg = mesh.cells_grid(key)
+    rows, cols = [], []
+    for ax in range(mesh.dim):
+        a = np.take(grid, np.arange(grid.shape[ax] - 1), axis=ax).ravel()
+        b = np.take(grid, np.arange(1, grid.shape[ax]), axis=ax).ravel()
+        ka = np.take(kg, np.arange(kg.shape[ax] - 1), axis=ax).ravel()
+        kb = np.take(kg, np.arange(1, kg.shape[ax]), axis=ax).ravel()
+        keep = ka == kb
+        rows.append(a[keep])
+        cols.append(b[keep])
+    rows = np.concatenate(rows)
+    cols = np.concatenate(cols)
+    g = sp.coo_matrix((np.ones(len(rows), dtype=np.int8), (rows, cols)),
+                      shape=(mesh.cell_count, mesh.cell_count))
+    _, comp = connected_components(g, directed=False)
+    # order components by (key, first cell id)
+    first = np.full(comp.max() + 1, mesh.cell_count, dtype=np.int64)
+    np.minimum.at(first, comp, np.arange(mesh.cell_count))
+    comp_key = key[first]
+    order = np.lexsort((first, comp_key))
+    new_id = np.empty_like(order)
+    new_id[order] = np.arange(len(order))
+    return PartitionPair(mesh, theta, new_id[comp], validate=validate)
+
+
+# --------------------------------------------------------------------------------------
+# objects
+# --------------------------------------------------------------------------------------
+
+def _lexsort_rows(rows: np.ndarray) -> np.ndarray:
+    """Stable lexicographic order of int rows (column 0 primary)."""
+    return np.lexsort(tuple(rows[:, k] for k in range(rows.shape[1] - 1, -1, -1)))
+
+
+def classify_objects(pair: PartitionPair) -> ObjectTable:
+    """Group Γ dofs into objects by Θ̂-signature (partition.py:223-250).
+
+    Returns an :class:`ObjectTable`, which indexes and iterates like the reference's
+    list of ``InterfaceObject``.
+    """
+    ms = pair.membership
+    mesh = pair.mesh
+    gamma = ms.gamma_dofs
+    W = ms.hat_rows.shape[1]
+    sig_rows = ms.hat_rows[gamma]
+    sig_cnt = ms.hat_counts[gamma]
+    dof_obj = np.full(mesh.free_count, -1, dtype=np.int64)
+    if len(gamma) == 0:
+        empty = np.zeros((0, W), dtype=np.int64)
+        return ObjectTable(mesh.dim, empty, np.zeros(0, np.int64), empty.copy(),
+                           np.zeros(0, np.int64), np.zeros(0, np.int8),
+                           np.zeros(1, np.int64), np.zeros(0, np.int64), dof_obj)
+    order = _lexsort_rows(sig_rows)  # stable: dofs stay ascending within a signature
+    srt = sig_rows[order]
+    new = np.ones(len(srt), dtype=bool)
+    new[1:] = np.any(srt[1:] != srt[:-1], axis=1)
+    starts = np.flatnonzero(new)
+    n_obj = len(starts)
+    dof_ptr = np.append(starts, len(srt)).astype(np.int64)
+    dof_list = gamma[order]
+    obj_of = np.cumsum(new) - 1
+    dof_obj[dof_list] = obj_of
+    signature = srt[starts]
+    sig_len = sig_cnt[order][starts].astype(np.int64)
+    ndofs = np.diff(dof_ptr)
+    kind = np.where(ndofs == 1, _KIND_CODE["vertex"],
+                    np.where(sig_len == 2, _KIND_CODE["face" if mesh.dim == 3 else "edge"],
+                             _KIND_CODE["edge"])).astype(np.int8)
+    par = np.where(signature >= 0, pair.parent[np.maximum(signature, 0)], -1)
+    owners, owner_len = _sorted_unique_rows(par)
+    # _sorted_unique_rows treats −1 as a value: drop it (it sorts first)
+    has_pad = owners[:, 0] == -1
+    owners = np.where(has_pad[:, None], np.roll(owners, -1, axis=1), owners)
+    owners[has_pad, -1] = -1
+    owner_len = owner_len - has_pad
+    return ObjectTable(mesh.dim, signature, sig_len, owners, owner_len.astype(np.int64), kind,
+                       dof_ptr, dof_list, dof_obj)
+
+
+def _kind_flags(recipe) -> dict:
+    if hasattr(recipe, "selects"):
+        return {k: recipe.selects(k) for k in ("vertex", "edge", "face")}
+    letters = set(str(recipe))
+    if not letters <= {"v", "e", "f"}:
+        raise ValueError(f"unknown recipe {recipe!r}; use letters from 'vef'")
+    return {"vertex": "v" in letters, "edge": "e" in letters, "face": "f" in letters}
+
+
+def count_coarse_dofs(subdomains_per_dim: Sequence[int], split: int, recipe="vef") -> int:
+    """Closed-form coarse size of a uniformly split box partition (partition.py:262-296).
+
+    Counts the vertices / edges / faces of the refined subsubdomain grid that lie on the
+    coarse interface; valid when every subsubdomain is ≥ 2 cells wide.
+    """
+    subs = tuple(int(s) for s in subdomains_per_dim)
+    split = int(split)
+    if split < 1 or any(s < 1 for s in subs):
+        raise ValueError("subdomain counts and split must be positive")
+    flags = _kind_flags(recipe)
+    dim = len(subs)
+    m = [s * split for s in subs]       # subsubdomains per axis
+    fine = [mi - 1 for mi in m]         # interior subsubdomain planes per axis
+    coarse = [s - 1 for s in subs]      # interior subdomain planes per axis
+    only_fine = [a - c for a, c in zip(fine, coarse)]
+    total = 0
+    if flags["vertex"]:
+        total += int(np.prod(fine)) - int(np.prod(only_fine))
+    if dim == 2:
+        if flags["edge"]:
+            total += m[0] * coarse[1] + m[1] * coarse[0]
+        return total
+    for d in range(3):
+        e, f = [ax for ax in range(3) if ax != d]
+        if flags["edge"]:
+            total += m[d] * (fine[e] * fine[f] - only_fine[e] * only_fine[f])
+        if flags["face"]:
+            total += coarse[d] * m[e] * m[f]
+    return total
