@@ -171,6 +171,13 @@ def main():
         print(f"{case[0]:16s} n={res['n']:6d} coarse={res['coarse_size']:5d} "
               f"its={res['iterations']:4d} kappa={res['kappa']:.10g} "
               f"({time.perf_counter() - t0:.1f}s)")
+    # refine_by_coefficient labels (partition.py:202-220) on a channel field
+    _set_element("q1")
+    mesh = bddcso.build_mesh(3, (12, 12, 12))
+    cf = bddcso.make_channels(mesh, (2, 2, 2), bddcso.ChannelSpec(3.0, 2, 2, 1))
+    pair = bddcso.refine_by_coefficient(mesh, bddcso.partition_uniform(mesh, (2, 2, 2)), cf)
+    np.savez_compressed(os.path.join(OUT, "refine_coeff.npz"), cells=np.array((12, 12, 12)),
+                        subs=np.array((2, 2, 2)), alpha=cf.alpha, theta_hat=pair.theta_hat)
     # SPEC KATs for the combinatorial counter
     kat = {f"{s}": bddcso.count_coarse_dofs((10, 10, 10), s, "vef") for s in (1, 2, 4, 6, 8)}
     np.savez(os.path.join(OUT, "count_kat.npz"), **{k: np.array(v) for k, v in kat.items()})

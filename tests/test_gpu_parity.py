@@ -1,0 +1,187 @@
+"""GPU parity: the sm_100a path through the C ABI against the reference fixtures / oracle.
+
+Tolerances (north_star): identical PCG iterations (±1), x relative ℓ2 ≤ 1e-10, κ ≤ 1e-6
+relative; apply within 1e-12 (1e-9 for the 1e12-contrast cfg4 analogue).
+"""
+import numpy as np
+import pytest
+
+import paper_2001_07289_b200 as P
+from conftest import build_problem, golden_cases, load_golden
+
+pytestmark = pytest.mark.gpu
+
+CASES = [c for c in golden_cases() if c != "cfg4a_p1_ref"]
+
+
+def _op(g):
+    pb = build_problem(g)
+    op = P.build_bddc(pb["system"], pb["pair"], pb["objects"], pb["recipe"], pb["weights"],
+                      coarse_scaling=pb["mode"])
+    return pb, op
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_apply_matches_reference(cuda_ok, case):
+    g = load_golden(case)
+    pb, op = _op(g)
+    assert op.coarse_size == int(g["coarse_size"])
+    z = op.apply(g["r"])
+    tol = 1e-9 if "cfg4" in case else 1e-12
+    assert np.abs(z - g["Br"]).max() <= tol * np.abs(g["Br"]).max()
+    op.close()
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_fused_pcg_matches_reference(cuda_ok, case):
+    g = load_golden(case)
+    pb, op = _op(g)
+    x, rep = P.pcg(op.matvec, op.apply, g["b"], tol=float(g["tol"]), max_iters=2000)
+    assert abs(rep.iterations - int(g["iterations"])) <= 1
+    assert abs(rep.kappa_estimate - float(g["kappa"])) <= 1e-6 * float(g["kappa"])
+    assert np.linalg.norm(x - g["x"]) <= 1e-10 * np.linalg.norm(g["x"])
+    assert rep.converged
+    op.close()
+
+
+def test_spmv_matches_host_matrix(cuda_ok):
+    for case in ("cfg1_q1_ref", "cfg3a_p1_ref", "cfg4a_p1_spec", "q1_3d_vf"):
+        g = load_golden(case)
+        pb, op = _op(g)
+        x = np.random.default_rng(5).standard_normal(op.n)
+        y = op.matvec(x)
+        yr = pb["system"].matrix.matvec(x)
+        assert np.abs(y - yr).max() <= 1e-13 * np.abs(yr).max()
+        op.close()
+
+
+def test_host_callable_pcg_path(cuda_ok):
+    """Reference-style call: pcg(lambda v: A @ v, op.apply, b) through numpy callables."""
+    g = load_golden("cfg1_p1_ref")
+    pb, op = _op(g)
+    A = pb["system"].matrix.tocsr()
+    x, rep = P.pcg(lambda v: A @ v, op.apply, g["b"], tol=1e-8)
+    assert rep.iterations == int(g["iterations"])
+    assert np.linalg.norm(x - g["x"]) <= 1e-10 * np.linalg.norm(g["x"])
+    op.close()
+
+
+def test_torch_zero_copy_apply(cuda_ok):
+    import torch
+
+    g = load_golden("cfg3a_p1_ref")
+    pb, op = _op(g)
+    r = torch.from_numpy(g["r"]).cuda()
+    z = op.apply(r)
+    assert z.is_cuda
+    assert np.abs(z.cpu().numpy() - g["Br"]).max() <= 1e-12 * np.abs(g["Br"]).max()
+    op.close()
+
+
+def test_harmonic_extension_against_oracle(cuda_ok):
+    from oracle import bddc_oracle as orc
+
+    g = load_golden("cfg3a_p1_ref")
+    pb, op = _op(g)
+    o = orc.Oracle(3, (16, 16, 16), (2, 2, 2), 2, "vef", "cardinality", "p1")
+    gv = np.random.default_rng(2).standard_normal(len(op.gamma_dofs))
+    h = P.harmonic_extension(op, gv)
+    hr = o.harmonic(gv)
+    assert np.abs(h - hr).max() <= 1e-12 * np.abs(hr).max()
+    op.close()
+
+
+def test_preconditioner_symmetric(cuda_ok):
+    g = load_golden("cfg2a_p1_L4h")
+    pb, op = _op(g)
+    rng = np.random.default_rng(7)
+    for _ in range(5):
+        u, v = rng.standard_normal(op.n), rng.standard_normal(op.n)
+        a, b = u @ op.apply(v), v @ op.apply(u)
+        assert abs(a - b) <= 1e-9 * max(abs(a), abs(b))
+    op.close()
+
+
+@pytest.mark.parametrize("n", [1, 7, 64, 65, 130, 200])
+def test_dense_batched_kernels(cuda_ok, n):
+    import ctypes as C
+
+    import torch
+
+    from paper_2001_07289_b200 import _capi
+
+    lib = _capi.load()
+    rng = np.random.default_rng(n)
+    count = 5
+    ld = n + (n & 1)
+    M = rng.standard_normal((count, n, n))
+    A = M @ M.transpose(0, 2, 1) + n * np.eye(n)
+    buf = np.zeros((count, ld, ld))
+    buf[:, :n, :n] = A.transpose(0, 2, 1)  # column-major: element (i,j) at [j][i]
+    d = torch.from_numpy(buf).cuda()
+    info = np.zeros(count, dtype=np.int32)
+    rc = lib.bddc_dense_potrf(C.c_void_p(d.data_ptr()), n, ld, ld * ld, count,
+                              info.ctypes.data_as(C.POINTER(C.c_int)), None)
+    assert rc == 0 and np.all(info == -1)
+    L = np.tril(d.cpu().numpy()[:, :n, :n].transpose(0, 2, 1))
+    Lr = np.linalg.cholesky(A)
+    assert np.abs(L - Lr).max() <= 1e-12 * np.abs(Lr).max()
+    # trsm kinds against numpy
+    nb = 37
+    for kind in range(4):
+        left = kind < 2
+        shape = (n, nb) if left else (nb, n)
+        B = rng.standard_normal((count,) + shape)
+        ldb = shape[0] + (shape[0] & 1)
+        bb = np.zeros((count, shape[1], ldb))
+        bb[:, :, : shape[0]] = B.transpose(0, 2, 1)
+        db = torch.from_numpy(bb).cuda()
+        rc = lib.bddc_dense_trsm(kind, C.c_void_p(d.data_ptr()), n, ld, ld * ld,
+                                 C.c_void_p(db.data_ptr()), nb, ldb, ldb * shape[1], count, None)
+        torch.cuda.synchronize()
+        assert rc == 0
+        X = db.cpu().numpy()[:, :, : shape[0]].transpose(0, 2, 1)
+        for b in range(count):
+            Lb = Lr[b]
+            ref = {0: np.linalg.solve(Lb, B[b]), 1: np.linalg.solve(Lb.T, B[b]),
+                   2: np.linalg.solve(Lb, B[b].T).T, 3: np.linalg.solve(Lb.T, B[b].T).T}[kind]
+            assert np.abs(X[b] - ref).max() <= 1e-10 * max(1.0, np.abs(ref).max())
+
+
+@pytest.mark.parametrize("tA,tB", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_dense_gemm(cuda_ok, tA, tB):
+    import ctypes as C
+
+    import torch
+
+    from paper_2001_07289_b200 import _capi
+
+    lib = _capi.load()
+    rng = np.random.default_rng(11)
+    M, N, K, count = 97, 70, 131, 3
+    Ash = (K, M) if tA else (M, K)
+    Bsh = (N, K) if tB else (K, N)
+    A = rng.standard_normal((count,) + Ash)
+    B = rng.standard_normal((count,) + Bsh)
+    Cm = rng.standard_normal((count, M, N))
+
+    def cm(X):
+        r, c = X.shape[1:]
+        ld = r + (r & 1)
+        out = np.zeros((count, c, ld))
+        out[:, :, :r] = X.transpose(0, 2, 1)
+        return torch.from_numpy(out).cuda(), ld
+
+    dA, lda = cm(A)
+    dB, ldb = cm(B)
+    dC, ldc = cm(Cm)
+    rc = lib.bddc_dense_gemm(tA, tB, M, N, K, -1.5, C.c_void_p(dA.data_ptr()), lda,
+                             dA[0].numel(), C.c_void_p(dB.data_ptr()), ldb, dB[0].numel(), 0.5,
+                             C.c_void_p(dC.data_ptr()), ldc, dC[0].numel(), count, None)
+    torch.cuda.synchronize()
+    assert rc == 0
+    got = dC.cpu().numpy()[:, :, :M].transpose(0, 2, 1)
+    opA = A.transpose(0, 2, 1) if tA else A
+    opB = B.transpose(0, 2, 1) if tB else B
+    ref = -1.5 * opA @ opB + 0.5 * Cm
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
