@@ -13,6 +13,8 @@
  *   bddc_pcg       <- pcg(lambda v: A @ v, op.apply, b, tol, max_iters)    krylov.py:31-92
  *   bddc_dense_*   <- spd_factor / saddle_factor / their solves            linalg.py:117-212
  *
+ * Streams: `stream` is a cudaStream_t (NULL = the legacy default stream); work is ordered
+ * after earlier calls on the context and before later ones.
  * Conventions: plain pointers and sizes only; all vectors are float64 over free dofs in
  * the reference's numbering (mesh.py:97-102). Device pointers where marked; host arrays
  * in bddc_setup_desc are read during the call only. Return codes:
@@ -105,6 +107,9 @@ int bddc_pcg_host(bddc_ctx* ctx, const double* b_host, double* x_host, double to
 int bddc_get_stats(bddc_ctx* ctx, bddc_stats* out);
 int bddc_sync(bddc_ctx* ctx);
 int bddc_kernel_launches_per_apply(bddc_ctx* ctx);
+/* diagnostics: copy an internal buffer ("LI", "LS", "Phi", "Sloc", "cscale", "diag_s",
+   "csr_val", "fronts") to host; returns the element count (or -1) */
+long long bddc_debug_copy(bddc_ctx* ctx, const char* name, double* host, long long capacity);
 
 /* dense FP64 batched kernels (column-major, even leading dimensions, device pointers) */
 int bddc_dense_potrf(double* A, int n, int lda, long long stride, int count, int* info_host,

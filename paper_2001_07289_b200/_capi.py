@@ -25,7 +25,7 @@ _vp = C.c_void_p
 EXPORTS = (
     "bddc_create", "bddc_destroy", "bddc_setup", "bddc_refactor", "bddc_apply", "bddc_harmonic",
     "bddc_spmv", "bddc_pcg", "bddc_pcg_host", "bddc_get_stats", "bddc_sync",
-    "bddc_kernel_launches_per_apply", "bddc_dense_potrf", "bddc_dense_trsm", "bddc_dense_gemm",
+    "bddc_kernel_launches_per_apply", "bddc_debug_copy", "bddc_dense_potrf", "bddc_dense_trsm", "bddc_dense_gemm",
 )
 
 
@@ -91,6 +91,8 @@ def load(required: bool = True):
     lib.bddc_get_stats.argtypes = [_vp, C.POINTER(Stats)]
     lib.bddc_sync.argtypes = [_vp]
     lib.bddc_kernel_launches_per_apply.argtypes = [_vp]
+    lib.bddc_debug_copy.argtypes = [_vp, C.c_char_p, _pd, _ll]
+    lib.bddc_debug_copy.restype = _ll
     lib.bddc_dense_potrf.argtypes = [_vp, _i, _i, _ll, _i, _pi, _vp]
     lib.bddc_dense_trsm.argtypes = [_i, _vp, _i, _i, _ll, _vp, _i, _i, _ll, _i, _vp]
     lib.bddc_dense_gemm.argtypes = [_i, _i, _i, _i, _i, _d, _vp, _i, _ll, _vp, _i, _ll, _d, _vp,

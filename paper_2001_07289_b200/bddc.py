@@ -13,6 +13,7 @@ gives the documented C Ψ = I.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 from dataclasses import dataclass
 
@@ -156,6 +157,9 @@ class BddcOperator:
         d = self._descriptor()
         err = C.create_string_buffer(1024)
         rc = self._lib.bddc_setup(self._ctx, C.byref(d), err, len(err))
+        self.setup_code = rc
+        if rc and os.environ.get("BDDC_DEBUG_KEEP"):
+            return
         raise_for(rc, err.value.decode(errors="replace"), self.recipe)
         self._read_times()
 
@@ -258,6 +262,17 @@ class BddcOperator:
         raise_for(rc, err.value.decode(errors="replace"))
         k = rep.iterations
         return x, alphas[:k].copy(), betas[: max(k - 1, 0)].copy(), resid[: k + 1].copy(), k, bool(rep.converged)
+
+    def debug_buffer(self, name: str) -> np.ndarray:
+        """Copy an internal device buffer to host (diagnostics / kernel-level tests)."""
+        n = self._lib.bddc_debug_copy(self._ctx, name.encode(), None, 0)
+        if n < 0:
+            raise KeyError(name)
+        out = np.empty(max(n, 0))
+        got = self._lib.bddc_debug_copy(self._ctx, name.encode(), _capi.ptr(out, C.c_double), n)
+        if got != n:
+            raise RuntimeError(f"debug copy of {name} failed")
+        return out
 
     def sync(self):
         self._lib.bddc_sync(self._ctx)

@@ -144,6 +144,7 @@ struct Ctx {
   double *crhs = nullptr, *csol = nullptr;  // [n_coarse]
   // pcg workspaces
   double *r = nullptr, *z = nullptr, *p = nullptr, *Ap = nullptr;
+  double *bbuf = nullptr, *xbuf = nullptr;  // host-facing PCG staging
   double* red = nullptr;     // reduction partials
   double* scal = nullptr;    // device scalars
   double* h_scal = nullptr;  // pinned host mirror

@@ -275,6 +275,8 @@ void do_setup(bddc_ctx* h, const bddc_setup_desc* d) {
   c.z = c.alloc<double>(G.n);
   c.p = c.alloc<double>(G.n);
   c.Ap = c.alloc<double>(G.n);
+  c.bbuf = c.alloc<double>(G.n);
+  c.xbuf = c.alloc<double>(G.n);
   c.red = c.alloc<double>(4096);
   c.scal = c.alloc<double>(16);
   BDDC_CUDA(cudaMemsetAsync(c.scal, 0, 16 * sizeof(double), c.stream));
@@ -288,6 +290,25 @@ void do_setup(bddc_ctx* h, const bddc_setup_desc* d) {
   h->ws = c.alloc<double>(use);
   h->ws_doubles = use;
   numeric_setup(h);
+}
+
+// Run f on the caller's stream (NULL = legacy default stream), ordered after pending work
+// of the context stream and before later context-stream work (shared workspaces).
+template <class F>
+void on_stream(bddc_ctx* h, void* stream, F&& f) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (s == h->c.stream) {
+    f(s);
+    return;
+  }
+  cudaEvent_t e;
+  BDDC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  BDDC_CUDA(cudaEventRecord(e, h->c.stream));
+  BDDC_CUDA(cudaStreamWaitEvent(s, e, 0));
+  f(s);
+  BDDC_CUDA(cudaEventRecord(e, s));
+  BDDC_CUDA(cudaStreamWaitEvent(h->c.stream, e, 0));
+  BDDC_CUDA(cudaEventDestroy(e));
 }
 
 }  // namespace
@@ -341,24 +362,13 @@ int bddc_refactor(bddc_ctx* h, const double* alpha_host, char* err, size_t errle
 
 int bddc_apply(bddc_ctx* h, const double* r, double* z, void* stream) {
   if (!h || !h->c.setup_done) return 1;
-  return guarded(nullptr, 0, [&] {
-    cudaStream_t s = stream ? (cudaStream_t)stream : h->c.stream;
-    if (s != h->c.stream) {  // order after any pending work of the context stream
-      cudaEvent_t e;
-      BDDC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      BDDC_CUDA(cudaEventRecord(e, h->c.stream));
-      BDDC_CUDA(cudaStreamWaitEvent(s, e, 0));
-      cudaEventDestroy(e);
-    }
-    apply_bddc(h->c, r, z, s);
-  });
+  return guarded(nullptr, 0, [&] { on_stream(h, stream, [&](cudaStream_t s) { apply_bddc(h->c, r, z, s); }); });
 }
 
 int bddc_harmonic(bddc_ctx* h, const double* g, double* out, void* stream) {
   if (!h || !h->c.setup_done) return 1;
-  return guarded(nullptr, 0, [&] {
+  return guarded(nullptr, 0, [&] { on_stream(h, stream, [&](cudaStream_t s) {
     Ctx& c = h->c;
-    cudaStream_t s = stream ? (cudaStream_t)stream : c.stream;
     const Geometry& G = c.geo;
     // out_Gamma = g; out_I = A_II^{-1} (0 - A g_ext)_I
     BDDC_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * G.n, s));
@@ -367,12 +377,12 @@ int bddc_harmonic(bddc_ctx* h, const double* g, double* out, void* stream) {
       scatter_gamma_kernel<<<ceil_div(c.n_gamma, 256), 256, 0, s>>>(c.n_gamma, c.gamma_dof, g, out);
     BDDC_LAUNCH_CHECK();
     harmonic_interior(c, out, s);
-  });
+  }); });
 }
 
 int bddc_spmv(bddc_ctx* h, const double* x, double* y, void* stream) {
   if (!h || !h->c.alpha) return 1;
-  return guarded(nullptr, 0, [&] { spmv(h->c, x, y, stream ? (cudaStream_t)stream : h->c.stream); });
+  return guarded(nullptr, 0, [&] { on_stream(h, stream, [&](cudaStream_t s) { spmv(h->c, x, y, s); }); });
 }
 
 int bddc_pcg(bddc_ctx* h, const double* b, double* x, double tol, int max_iters, double* alphas,
@@ -404,12 +414,12 @@ int bddc_pcg_host(bddc_ctx* h, const double* b_host, double* x_host, double tol,
   code = guarded(err, errlen, [&] {
     Ctx& c = h->c;
     const size_t bytes = sizeof(double) * c.geo.n;
-    BDDC_CUDA(cudaMemcpyAsync(c.v2, b_host, bytes, cudaMemcpyHostToDevice, c.stream));
+    BDDC_CUDA(cudaMemcpyAsync(c.bbuf, b_host, bytes, cudaMemcpyHostToDevice, c.stream));
   });
   if (code) return code;
-  code = bddc_pcg(h, h->c.v2, h->c.Ap, tol, max_iters, alphas, betas, resid, rep, err, errlen);
+  code = bddc_pcg(h, h->c.bbuf, h->c.xbuf, tol, max_iters, alphas, betas, resid, rep, err, errlen);
   int code2 = guarded(err, code ? 0 : errlen, [&] {
-    BDDC_CUDA(cudaMemcpyAsync(x_host, h->c.Ap, sizeof(double) * h->c.geo.n, cudaMemcpyDeviceToHost,
+    BDDC_CUDA(cudaMemcpyAsync(x_host, h->c.xbuf, sizeof(double) * h->c.geo.n, cudaMemcpyDeviceToHost,
                               h->c.stream));
     BDDC_CUDA(cudaStreamSynchronize(h->c.stream));
   });
@@ -454,6 +464,38 @@ int bddc_kernel_launches_per_apply(bddc_ctx* h) {
   // local_gamma2, gamma gather, residual (memsets are copy-engine ops, not kernels)
   int n = 2 + 1 + 1 + 1 + 1 + 1;
   if (c.fp.n_coarse) n += 1 + 2 * c.fp.nlevels;
+  return n;
+}
+
+long long bddc_debug_copy(bddc_ctx* h, const char* name, double* host, long long cap) {
+  if (!h || !name) return -1;
+  const Ctx& c = h->c;
+  const Geometry& G = c.geo;
+  const double* src = nullptr;
+  long long n = 0;
+  std::string nm(name);
+  if (nm == "LI") { src = c.LI; n = (long long)G.nsub * G.nblk * 2 * G.m_pad * G.m_pad; }
+  else if (nm == "LS") { src = c.LS; n = (long long)G.nsub * G.nG_pad * G.nG_pad; }
+  else if (nm == "Phi") { src = c.Phi; n = (long long)G.nsub * G.nG_pad * G.nc_pad; }
+  else if (nm == "Sloc") { src = c.Sloc; n = (long long)G.nsub * G.nc_pad * G.nc_pad; }
+  else if (nm == "cscale") { src = c.cscale; n = G.nsub; }
+  else if (nm == "diag_s") { src = c.diag_s; n = G.nsub; }
+  else if (nm == "csr_val") { src = c.fp.csr_val; n = c.fp.nnz; }
+  else if (nm == "fronts") { src = c.fp.d.fronts; n = c.fp.front_pool; }
+  else if (nm == "v1") { src = c.v1; n = G.n; }
+  else if (nm == "v2") { src = c.v2; n = G.n; }
+  else if (nm == "rpg") { src = c.rpg; n = c.n_gamma; }
+  else if (nm == "qloc") { src = c.qloc; n = (long long)G.nsub * G.nc_pad; }
+  else if (nm == "tloc") { src = c.tloc; n = (long long)G.nsub * G.nc_pad; }
+  else if (nm == "uloc") { src = c.uloc; n = (long long)G.nsub * G.nG_pad; }
+  else if (nm == "wloc") { src = c.wloc; n = (long long)G.nsub * G.nG_pad; }
+  else if (nm == "crhs") { src = c.crhs; n = c.fp.n_coarse; }
+  else if (nm == "csol") { src = c.csol; n = c.fp.n_coarse; }
+  else return -1;
+  if (!host) return n;
+  if (cap < n || !src) return -1;
+  if (cudaStreamSynchronize(c.stream) != cudaSuccess) return -1;
+  if (cudaMemcpy(host, src, sizeof(double) * n, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
   return n;
 }
 

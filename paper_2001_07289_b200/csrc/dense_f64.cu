@@ -33,12 +33,22 @@ __device__ __forceinline__ TaskView gemm_task(const GemmArgs& a, int b) {
                   a.lda,          a.ldb,          a.ldc};
 }
 
+// Copy a pair of consecutive doubles (valid = 0, 1 or 2 of them) into shared memory.
+__device__ __forceinline__ void copy_pair(double* dst, const double* src, int valid, bool al16) {
+  if (al16) {
+    cp_async16(dst, src, valid * 8);
+  } else {
+    cp_async8(dst, src, valid > 0 ? 8 : 0);
+    cp_async8(dst + 1, valid > 1 ? src + 1 : src, valid > 1 ? 8 : 0);
+  }
+}
+
 // Load a BM x BK slice of op(A) (rows m0.., k0..) into shared memory.
 //   !TA: A(m,k) = A[m + k*lda]  -> sm[k*LDW + m]
 //    TA: A(m,k) = A[k + m*lda]  -> sm[m*LDK + k]
 template <bool TA>
 __device__ __forceinline__ void load_a(double* sm, const double* A, int lda, int M, int K, int m0,
-                                       int k0, int tid) {
+                                       int k0, int tid, bool al) {
 #pragma unroll
   for (int it = 0; it < 4; ++it) {
     int c = tid + it * 128;
@@ -47,13 +57,13 @@ __device__ __forceinline__ void load_a(double* sm, const double* A, int lda, int
       int gm = m0 + m, gk = k0 + k;
       int valid = (gk < K) ? max(0, min(2, M - gm)) : 0;
       const double* src = valid ? A + gm + (long long)gk * lda : A;
-      cp_async16(sm + k * LDW + m, src, valid * 8);
+      copy_pair(sm + k * LDW + m, src, valid, al);
     } else {
       int m = c >> 3, k = (c & 7) * 2;
       int gm = m0 + m, gk = k0 + k;
       int valid = (gm < M) ? max(0, min(2, K - gk)) : 0;
       const double* src = valid ? A + gk + (long long)gm * lda : A;
-      cp_async16(sm + m * LDK + k, src, valid * 8);
+      copy_pair(sm + m * LDK + k, src, valid, al);
     }
   }
 }
@@ -63,7 +73,7 @@ __device__ __forceinline__ void load_a(double* sm, const double* A, int lda, int
 //    TB: B(k,n) = B[n + k*ldb]  -> sm[k*LDW + n]
 template <bool TB>
 __device__ __forceinline__ void load_b(double* sm, const double* B, int ldb, int N, int K, int n0,
-                                       int k0, int tid) {
+                                       int k0, int tid, bool al) {
 #pragma unroll
   for (int it = 0; it < 4; ++it) {
     int c = tid + it * 128;
@@ -72,13 +82,13 @@ __device__ __forceinline__ void load_b(double* sm, const double* B, int ldb, int
       int gn = n0 + n, gk = k0 + k;
       int valid = (gn < N) ? max(0, min(2, K - gk)) : 0;
       const double* src = valid ? B + gk + (long long)gn * ldb : B;
-      cp_async16(sm + n * LDK + k, src, valid * 8);
+      copy_pair(sm + n * LDK + k, src, valid, al);
     } else {
       int k = c >> 5, n = (c & 31) * 2;
       int gn = n0 + n, gk = k0 + k;
       int valid = (gk < K) ? max(0, min(2, N - gn)) : 0;
       const double* src = valid ? B + gn + (long long)gk * ldb : B;
-      cp_async16(sm + k * LDW + n, src, valid * 8);
+      copy_pair(sm + k * LDW + n, src, valid, al);
     }
   }
 }
@@ -106,16 +116,19 @@ __global__ void __launch_bounds__(128) gemm_f64_kernel(GemmArgs args) {
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int nk = (t.K + BK - 1) / BK;
+  // 16-byte copies need 16-byte aligned pairs: base pointers aligned and even pitches
+  const bool al_a = ((((unsigned long long)t.A) & 15) == 0) && ((t.lda & 1) == 0);
+  const bool al_b = ((((unsigned long long)t.B) & 15) == 0) && ((t.ldb & 1) == 0);
   if (nk > 0) {
-    load_a<TA>(As[0], t.A, t.lda, t.M, t.K, m0, 0, tid);
-    load_b<TB>(Bs[0], t.B, t.ldb, t.N, t.K, n0, 0, tid);
+    load_a<TA>(As[0], t.A, t.lda, t.M, t.K, m0, 0, tid, al_a);
+    load_b<TB>(Bs[0], t.B, t.ldb, t.N, t.K, n0, 0, tid, al_b);
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
     const int st = kt & 1;
     if (kt + 1 < nk) {
-      load_a<TA>(As[st ^ 1], t.A, t.lda, t.M, t.K, m0, (kt + 1) * BK, tid);
-      load_b<TB>(Bs[st ^ 1], t.B, t.ldb, t.N, t.K, n0, (kt + 1) * BK, tid);
+      load_a<TA>(As[st ^ 1], t.A, t.lda, t.M, t.K, m0, (kt + 1) * BK, tid, al_a);
+      load_b<TB>(Bs[st ^ 1], t.B, t.ldb, t.N, t.K, n0, (kt + 1) * BK, tid, al_b);
       cp_async_commit();
       cp_async_wait<1>();
     } else {

@@ -143,6 +143,7 @@ class Emulator:
             if len(fI):
                 u1[fI] = np.linalg.solve(L["AII"], r[fI])
         rp = r - A @ u1
+        self.dbg = dict(u1=u1.copy(), rp=rp.copy())
         ncoarse = self.cp.n if self.cp is not None else 0
         crhs = np.zeros(ncoarse)
         st = []
@@ -155,6 +156,7 @@ class Emulator:
             np.add.at(crhs, L["cc"], q)
             st.append((u, t))
         csol = self.coarse_solve(crhs) if ncoarse else crhs
+        self.dbg.update(crhs=crhs.copy(), csol=csol.copy(), st=st)
         z = np.zeros(self.n)
         for L, (u, t) in zip(self.loc, st):
             e = L["c"] * csol[L["cc"]] - t

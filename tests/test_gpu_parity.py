@@ -143,8 +143,14 @@ def test_dense_batched_kernels(cuda_ok, n):
         X = db.cpu().numpy()[:, :, : shape[0]].transpose(0, 2, 1)
         for b in range(count):
             Lb = Lr[b]
-            ref = {0: np.linalg.solve(Lb, B[b]), 1: np.linalg.solve(Lb.T, B[b]),
-                   2: np.linalg.solve(Lb, B[b].T).T, 3: np.linalg.solve(Lb.T, B[b].T).T}[kind]
+            if kind == 0:
+                ref = np.linalg.solve(Lb, B[b])
+            elif kind == 1:
+                ref = np.linalg.solve(Lb.T, B[b])
+            elif kind == 2:
+                ref = np.linalg.solve(Lb, B[b].T).T
+            else:
+                ref = np.linalg.solve(Lb.T, B[b].T).T
             assert np.abs(X[b] - ref).max() <= 1e-10 * max(1.0, np.abs(ref).max())
 
 
