@@ -1,0 +1,484 @@
+#!/usr/bin/env python
+"""BDDC-SO setup + PCG solve throughput on B200 (BASELINE.json metric: Mdof/s, applies/s,
+fraction of roofline).
+
+Workload (BASELINE.json configs[1], the metric's config that fits one GPU): 2D Poisson,
+2048x2048 cells split into P1 triangles (4,190,209 dofs), 64x64 subdomains of 32x32 cells,
+subedges of L = 4h (split 8) + vertices between them ('ve'), cardinality weights,
+f ~ U[-1,1] per dof (seed 0), PCG rtol 1e-8 from x0 = 0, FP64, reference coarse scaling.
+
+One step = numeric BDDC-SO setup on device-resident inputs (local factorizations, coarse
+basis, coarse assembly + multifrontal factorization) + the PCG solve to rtol 1e-8.
+`value` = dofs solved per second over the timed steps (CUDA events on the library stream);
+`e2e` = the same through the C ABI with host buffers (alpha and b uploaded from pinned
+memory, x downloaded) every step. Host index tables / symbolic analysis are one-time prep
+(reported as prep_s). Inputs (factors ~3.5 GB) exceed the 126 MB L2 between steps.
+
+--impl reference times the CPU oracle port (oracle/bddc_oracle.py: SuperLU factorizations,
+three-step apply, the reference algorithm) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK = 6650.0
+FP64_PEAK_TFLOPS = 35.43  # cuBLAS (torch.matmul) FP64 8192^3 measured on this pool, profiles/r01_fp64_peak_probe.log
+FP64_DMMA_ISSUE_TFLOPS = 37.07  # mma.sync m8n8k4 issue-bound loop, same probe
+
+WORKLOADS = {
+    # name: (dim, cells, subs, split, recipe, weighting, source)
+    "cfg2_L4h": (2, (2048, 2048), (64, 64), 8, "ve", "cardinality", "uniform"),
+    "cfg2_Lh": (2, (2048, 2048), (64, 64), 32, "ve", "cardinality", "uniform"),
+    "cfg2_L16h": (2, (2048, 2048), (64, 64), 2, "ve", "cardinality", "uniform"),
+    "cfg2_LH": (2, (2048, 2048), (64, 64), 1, "ve", "cardinality", "uniform"),
+    "cfg3": (3, (128, 128, 128), (16, 16, 16), 2, "vef", "cardinality", "one"),
+    "cfg1": (2, (64, 64), (4, 4), 4, "ve", "cardinality", "one"),
+}
+SAMPLE = {  # bounded CPU sample with the same local geometry (subdomain size, split, recipe)
+    "cfg2_L4h": (2, (128, 128), (4, 4), 8),
+    "cfg2_Lh": (2, (128, 128), (4, 4), 32),
+    "cfg2_L16h": (2, (128, 128), (4, 4), 2),
+    "cfg2_LH": (2, (128, 128), (4, 4), 1),
+    "cfg3": (3, (24, 24, 24), (3, 3, 3), 2),
+    "cfg1": (2, (64, 64), (4, 4), 4),
+}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return HBM_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def build_host_problem(name):
+    import paper_2001_07289_b200 as P
+
+    dim, cells, subs, split, recipe, wmode, source = WORKLOADS[name]
+    t0 = time.perf_counter()
+    mesh = P.build_mesh(dim, cells, "p1")
+    cf = P.make_constant(mesh, 1.0)
+    pair = P.refine_uniform(mesh, P.partition_uniform(mesh, subs), split, validate=False)
+    objs = P.classify_objects(pair)
+    w = P.compute_weights(pair, wmode, cf, objs)
+    system = P.assemble(mesh, cf)
+    if source == "uniform":
+        b = P.mesh.load_vector(mesh, P.uniform_source(mesh, 0))
+    else:
+        b = system.rhs
+    prep = time.perf_counter() - t0
+    return dict(P=P, mesh=mesh, cf=cf, pair=pair, objs=objs, w=w, system=system, b=b,
+                recipe=recipe, prep=prep)
+
+
+def phase_work(op, pb, its):
+    """Algorithmic bytes / flops per launch of each timed phase."""
+    st = op.stats()
+    lay = op.plan.layout
+    nsub = int(st.nsub)
+    m, nblk, nG, nI = lay.m, lay.nblk, lay.nG, lay.m * lay.nblk
+    nc = op.plan.n_con_local
+    n = int(st.n)
+    T = lambda k: k * (k + 1) / 2  # noqa: E731
+    w = {}
+    # interior solve: Ld_j lower + Lo_j dense, forward and backward, + vector in/out
+    li = nblk * T(m) + max(nblk - 1, 0) * m * m
+    w["apply.bt_solve"] = ("hbm", 8.0 * (2 * nsub * li + 2 * nsub * nI))
+    # local Gamma phase 1: L_S forward + backward (lower), Phi^T rho
+    w["apply.gamma1"] = ("hbm", 8.0 * float(np.sum(2 * T(nG) + nG * nc)))
+    w["apply.gamma2"] = ("hbm", 8.0 * float(np.sum(nG * nc)))
+    cp = op.plan.coarse
+    if cp is not None:
+        w["apply.coarse"] = ("hbm", 8.0 * 2 * cp.factor_entries())
+        w["setup.coarse"] = ("fp64", cp.factor_flops())
+    # pcg SpMV + dot: x, y, alpha (cells ~ n)
+    w["pcg.spmv_dot"] = ("hbm", 8.0 * 3 * n)
+    # setup: E = L_I^{-1} A_IG (block forward, dense n_G RHS), S_G = A_GG - E^T E (SYRK),
+    # S_K Cholesky, Phi (TRSMs with n_c RHS, S_C), P = Phi^T S_G Phi
+    w["setup.E"] = ("fp64", nsub * (max(nblk - 1, 0) * 2 * m * m * nG + nblk * m * m * nG))
+    w["setup.SG"] = ("fp64", nsub * nG * (nG + 1) * nI)
+    w["setup.SK"] = ("fp64", nsub * nG**3 / 3)
+    w["setup.Phi"] = ("fp64", float(np.sum(2 * nG * nG * nc + 2 * nG * nc * nc + nc**3 / 3
+                                           + 2 * nG * nG * nc + 2 * nG * nc * nc)))
+    w["setup.btchol"] = ("fp64", nsub * nblk * (m**3 / 3 + 2 * m**3))
+    return w
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_2001_07289_b200 import _capi
+
+    torch.cuda.set_device(local_rank)
+    pb = build_host_problem(args.workload)
+    P = pb["P"]
+    t0 = time.perf_counter()
+    op = P.build_bddc(pb["system"], pb["pair"], pb["objs"], pb["recipe"], pb["w"],
+                      coarse_scaling="reference", device=local_rank)
+    first_setup_s = time.perf_counter() - t0
+    lib = _capi.load()
+    ctx = op._ctx
+    n = op.n
+    b_host = np.ascontiguousarray(pb["b"])
+    b_dev = torch.from_numpy(b_host).cuda()
+    x_dev = torch.empty_like(b_dev)
+    alpha_pin = torch.from_numpy(np.ascontiguousarray(pb["cf"].alpha)).pin_memory()
+    b_pin = torch.from_numpy(b_host).pin_memory()
+    x_pin = torch.empty(n, dtype=torch.float64).pin_memory()
+    tol, maxit = 1e-8, 2000
+
+    def step_device():
+        op.refactor()
+        return op.pcg(b_dev, tol=tol, max_iters=maxit, x_out=x_dev)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        res = step_device()
+    iters = res[4]
+    # ---- timed region (device-resident inputs) ----
+    sampler = ClockSampler(local_rank)
+    lib.bddc_profile(ctx, 1)
+    barrier()
+    sampler.start()
+    l0 = lib.bddc_launch_count()
+    lib.bddc_event_record(ctx, 0)
+    setup_ms = solve_ms = 0.0
+    for _ in range(args.steps):
+        lib.bddc_event_record(ctx, 2)
+        op.refactor()
+        lib.bddc_event_record(ctx, 3)
+        res = op.pcg(b_dev, tol=tol, max_iters=maxit, x_out=x_dev)
+        lib.bddc_event_record(ctx, 4)
+        setup_ms += lib.bddc_event_elapsed_ms(ctx, 2, 3)
+        solve_ms += lib.bddc_event_elapsed_ms(ctx, 3, 4)
+    lib.bddc_event_record(ctx, 1)
+    elapsed = lib.bddc_event_elapsed_ms(ctx, 0, 1)
+    launches = lib.bddc_launch_count() - l0
+    barrier()
+    clocks = sampler.stop()
+    phases = {}
+    for name in ("apply.bt_solve", "apply.gamma1", "apply.coarse", "apply.gamma2", "setup.assemble",
+                 "setup.btchol", "setup.E", "setup.SG", "setup.SK", "setup.Phi", "setup.coarse",
+                 "pcg.spmv_dot"):
+        cnt = C.c_longlong()
+        ms = lib.bddc_profile_read(ctx, name.encode(), C.byref(cnt))
+        if cnt.value:
+            phases[name] = (ms, cnt.value)
+    lib.bddc_profile(ctx, 0)
+    if world > 1:
+        t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        elapsed = float(t.item())
+    x, alphas, betas, hist, k, conv = res
+    kappa = None
+    try:
+        from paper_2001_07289_b200.krylov import _lanczos_extremes
+
+        lo, hi = _lanczos_extremes(list(alphas), list(betas))
+        kappa = hi / lo
+    except Exception:
+        pass
+
+    # ---- e2e through the C ABI with host buffers ----
+    err = C.create_string_buffer(512)
+    rep = _capi.PcgReport()
+    al = np.zeros(maxit + 1)
+    be = np.zeros(maxit + 1)
+    rs = np.zeros(maxit + 2)
+    pd = C.POINTER(C.c_double)
+
+    def step_e2e():
+        rc = lib.bddc_refactor(ctx, C.cast(alpha_pin.data_ptr(), pd), err, len(err))
+        assert rc == 0, err.value
+        rc = lib.bddc_pcg_host(ctx, C.cast(b_pin.data_ptr(), pd), C.cast(x_pin.data_ptr(), pd), tol,
+                               maxit, _capi.ptr(al, C.c_double), _capi.ptr(be, C.c_double),
+                               _capi.ptr(rs, C.c_double), C.byref(rep), err, len(err))
+        assert rc == 0, err.value
+
+    for _ in range(max(1, min(args.warmup, 2))):
+        step_e2e()
+    barrier()
+    lib.bddc_event_record(ctx, 5)
+    for _ in range(args.steps):
+        step_e2e()
+    lib.bddc_event_record(ctx, 6)
+    e2e_ms = lib.bddc_event_elapsed_ms(ctx, 5, 6)
+    barrier()
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    xe2e = x_pin.numpy().copy()
+    e2e_consistent = float(np.linalg.norm(xe2e - x_dev.cpu().numpy()) / np.linalg.norm(xe2e))
+
+    # ---- preconditioner applies/s (device-resident r) ----
+    r = torch.from_numpy(np.random.default_rng(1).standard_normal(n)).cuda()
+    z = torch.empty_like(r)
+    stream = torch.cuda.current_stream().cuda_stream
+    for _ in range(3):
+        lib.bddc_apply(ctx, C.c_void_p(r.data_ptr()), C.c_void_p(z.data_ptr()), C.c_void_p(stream))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    napp = 50
+    e0.record()
+    for _ in range(napp):
+        lib.bddc_apply(ctx, C.c_void_p(r.data_ptr()), C.c_void_p(z.data_ptr()), C.c_void_p(stream))
+    e1.record()
+    torch.cuda.synchronize()
+    apply_ms = e0.elapsed_time(e1) / napp
+
+    # ---- rooflines per phase ----
+    hbm, hbm_src = _peaks()
+    work = phase_work(op, pb, k)
+    phase_out = {}
+    for name, (ms, cnt) in phases.items():
+        kind, amount = work.get(name, (None, None))
+        avg = ms / cnt
+        entry = {"ms_total": round(ms, 3), "launches": cnt, "avg_ms": round(avg, 4)}
+        if kind == "hbm":
+            ach = amount / (avg * 1e-3) / 1e9
+            entry.update(bound="hbm", achieved=round(ach, 1), unit="GB/s", frac=round(ach / hbm, 4))
+        elif kind == "fp64":
+            ach = amount / (avg * 1e-3) / 1e12
+            entry.update(bound="fp64", achieved=round(ach, 3), unit="TFLOP/s",
+                         frac=round(ach / FP64_PEAK_TFLOPS, 4))
+        phase_out[name] = entry
+    dominant = max(phase_out, key=lambda k2: phase_out[k2]["ms_total"]) if phase_out else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath) and dominant:
+        try:
+            traffic = json.load(open(tpath)).get(dominant)
+        except Exception:
+            traffic = None
+    roof = None
+    if dominant:
+        d = phase_out[dominant]
+        roof = {"kernel": dominant, "bound": "hbm" if d.get("bound") == "hbm" else "fp64",
+                "achieved": d.get("achieved"), "unit": d.get("unit"),
+                "peak": hbm if d.get("bound") == "hbm" else FP64_PEAK_TFLOPS,
+                "peak_source": hbm_src if d.get("bound") == "hbm" else
+                "measured cuBLAS FP64 GEMM (no FP64 entry in MEASURED_PEAKS.json)",
+                "frac": d.get("frac"), "traffic": traffic}
+
+    # ---- CPU baseline (oracle port, bounded sample, rank 0) ----
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.workload)
+
+    nsteps = args.steps
+    value = world * n * nsteps / (elapsed * 1e-3) / 1e6
+    e2e_val = world * n * nsteps / (e2e_ms * 1e-3) / 1e6
+    st = op.stats()
+    line = {
+        "metric": "BDDC-SO setup+PCG solve throughput (Mdof/s)",
+        "value": round(value, 3),
+        "unit": "Mdof/s",
+        "n_gpus": world,
+        "steps": nsteps,
+        "warmup": args.warmup,
+        "ms_per_step": round(elapsed / nsteps, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded f ~ U[-1,1] per dof, alpha = 1)",
+        "config": {
+            "workload": f"{args.workload}: 2D Poisson 2048^2 P1 (4,190,209 dofs), 64x64 subdomains of "
+                        "32^2 cells, L=4h subedges+vertices ('ve'), cardinality weights, rtol 1e-8, "
+                        "reference coarse scaling" if args.workload == "cfg2_L4h" else args.workload,
+            "dofs": n, "subdomains": int(st.nsub), "coarse_size": int(st.n_coarse),
+            "parallelism": "single GPU" if world == 1 else f"replicas x{world} (independent problems)",
+            "l2": "inputs > L2 (factors %.1f GB + fronts %.2f GB vs 126 MB L2)" % (
+                st.factor_bytes / 1e9, st.front_bytes / 1e9),
+        },
+        "e2e": {"value": round(e2e_val, 3), "unit": "Mdof/s",
+                "h2d_bytes_per_step": int(8 * (len(pb["cf"].alpha) + n)),
+                "d2h_bytes_per_step": int(8 * n + 8 * 4 * (k + 1)),
+                "ms_per_step": round(e2e_ms / nsteps, 3),
+                "x_matches_device_run": e2e_consistent < 1e-14},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "gpu_launches": int(launches),
+        "iterations": int(k),
+        "converged": bool(conv),
+        "kappa": kappa,
+        "setup_ms": round(setup_ms / nsteps, 3),
+        "solve_ms": round(solve_ms / nsteps, 3),
+        "applies_per_s": round(1000.0 / apply_ms, 1),
+        "apply_ms": round(apply_ms, 4),
+        "prep_s": round(pb["prep"] + op.times.prep_s, 2),
+        "first_setup_s": round(first_setup_s, 2),
+        "phases": phase_out,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    op.close()
+
+
+def cpu_baseline(workload):
+    """Oracle port on a bounded sample with the workload's local geometry (one run)."""
+    from oracle import bddc_oracle as orc
+
+    dim, cells, subs, split = SAMPLE[workload]
+    _, _, _, _, recipe, wmode, source = WORKLOADS[workload]
+    t0 = time.perf_counter()
+    o = orc.Oracle(dim, cells, subs, split, recipe, wmode, "p1", None, "reference")
+    t_build = time.perf_counter() - t0
+    mesh = o.mesh
+    b = orc.load(mesh, orc.uniform_f(mesh.n_free, 0)) if source == "uniform" else orc.load(mesh, 1.0)
+    t1 = time.perf_counter()
+    x, rep = orc.pcg(o.matvec, o.apply, b, 1e-8, 2000)
+    t_pcg = time.perf_counter() - t1
+    n = mesh.n_free
+    return {"value": round(n / (t_build + t_pcg) / 1e6, 5), "unit": "Mdof/s",
+            "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{dim}D {cells} P1, {subs} subdomains, split {split} (same local geometry), "
+                      f"{n} dofs: build {t_build:.2f} s + pcg {t_pcg:.2f} s ({rep['iterations']} its)"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from oracle import bddc_oracle as orc
+
+    dim, cells, subs, split = SAMPLE[args.workload]
+    _, _, _, _, recipe, wmode, source = WORKLOADS[args.workload]
+
+    def step():
+        o = orc.Oracle(dim, cells, subs, split, recipe, wmode, "p1", None, "reference")
+        mesh = o.mesh
+        b = orc.load(mesh, orc.uniform_f(mesh.n_free, 0)) if source == "uniform" else orc.load(mesh, 1.0)
+        x, rep = orc.pcg(o.matvec, o.apply, b, 1e-8, 2000)
+        return mesh.n_free, rep["iterations"]
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        n, its = step()
+    el = time.perf_counter() - t0
+    value = n * args.steps / el / 1e6
+    sample = (f"{dim}D {cells} P1, {subs} subdomains, split {split} ({n} dofs, same local geometry "
+              f"as {args.workload}); oracle port of the reference (SuperLU), setup+pcg per step")
+    line = {
+        "metric": "BDDC-SO setup+PCG solve throughput (Mdof/s)", "value": round(value, 5),
+        "unit": "Mdof/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1000 * el / args.steps, 2), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "sample": sample}, "impl": "reference",
+        "cpu_baseline": {"value": round(value, 5), "unit": "Mdof/s", "cores": os.cpu_count(),
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": round(value, 5), "unit": "Mdof/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "iterations": its,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--workload", default="cfg2_L4h", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+
+        torch.cuda.set_device(local_rank)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.distributed.init_process_group("nccl")
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch
+
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

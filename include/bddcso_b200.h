@@ -107,6 +107,15 @@ int bddc_pcg_host(bddc_ctx* ctx, const double* b_host, double* x_host, double to
 int bddc_get_stats(bddc_ctx* ctx, bddc_stats* out);
 int bddc_sync(bddc_ctx* ctx);
 int bddc_kernel_launches_per_apply(bddc_ctx* ctx);
+/* measurement: kernels launched by this library so far (process-wide); CUDA events on the
+   context stream (slots 0..7); optional per-phase event timers ("apply.bt_solve",
+   "apply.gamma1", "apply.coarse", "apply.gamma2", "setup.assemble", "setup.btchol",
+   "setup.E", "setup.SG", "setup.SK", "setup.Phi", "setup.coarse", "pcg.spmv_dot") */
+long long bddc_launch_count(void);
+int bddc_event_record(bddc_ctx* ctx, int slot);
+double bddc_event_elapsed_ms(bddc_ctx* ctx, int slot_a, int slot_b);
+int bddc_profile(bddc_ctx* ctx, int enable);
+double bddc_profile_read(bddc_ctx* ctx, const char* phase, long long* count);
 /* diagnostics: copy an internal buffer ("LI", "LS", "Phi", "Sloc", "cscale", "diag_s",
    "csr_val", "fronts") to host; returns the element count (or -1) */
 long long bddc_debug_copy(bddc_ctx* ctx, const char* name, double* host, long long capacity);

@@ -25,7 +25,8 @@ _vp = C.c_void_p
 EXPORTS = (
     "bddc_create", "bddc_destroy", "bddc_setup", "bddc_refactor", "bddc_apply", "bddc_harmonic",
     "bddc_spmv", "bddc_pcg", "bddc_pcg_host", "bddc_get_stats", "bddc_sync",
-    "bddc_kernel_launches_per_apply", "bddc_debug_copy", "bddc_dense_potrf", "bddc_dense_trsm", "bddc_dense_gemm",
+    "bddc_kernel_launches_per_apply", "bddc_debug_copy", "bddc_launch_count",
+    "bddc_event_record", "bddc_event_elapsed_ms", "bddc_profile", "bddc_profile_read", "bddc_dense_potrf", "bddc_dense_trsm", "bddc_dense_gemm",
 )
 
 
@@ -93,6 +94,14 @@ def load(required: bool = True):
     lib.bddc_kernel_launches_per_apply.argtypes = [_vp]
     lib.bddc_debug_copy.argtypes = [_vp, C.c_char_p, _pd, _ll]
     lib.bddc_debug_copy.restype = _ll
+    lib.bddc_launch_count.argtypes = []
+    lib.bddc_launch_count.restype = _ll
+    lib.bddc_event_record.argtypes = [_vp, _i]
+    lib.bddc_event_elapsed_ms.argtypes = [_vp, _i, _i]
+    lib.bddc_event_elapsed_ms.restype = _d
+    lib.bddc_profile.argtypes = [_vp, _i]
+    lib.bddc_profile_read.argtypes = [_vp, C.c_char_p, _pll]
+    lib.bddc_profile_read.restype = _d
     lib.bddc_dense_potrf.argtypes = [_vp, _i, _i, _ll, _i, _pi, _vp]
     lib.bddc_dense_trsm.argtypes = [_i, _vp, _i, _i, _ll, _vp, _i, _i, _ll, _i, _vp]
     lib.bddc_dense_gemm.argtypes = [_i, _i, _i, _i, _i, _d, _vp, _i, _ll, _vp, _i, _ll, _d, _vp,

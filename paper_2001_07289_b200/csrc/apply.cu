@@ -266,13 +266,14 @@ int grid_for(long long n, int threads) {
 void spmv(Ctx& c, const double* x, double* y, cudaStream_t s) {
   const Geometry& G = c.geo;
   const int th = 256, gr = grid_for(G.n, th);
-  if (G.dim == 2) spmv_kernel<2><<<gr, th, 0, s>>>(G, c.alpha, x, y);
-  else spmv_kernel<3><<<gr, th, 0, s>>>(G, c.alpha, x, y);
+  if (G.dim == 2) { spmv_kernel<2><<<gr, th, 0, s>>>(G, c.alpha, x, y); BDDC_COUNT(); }
+  else { spmv_kernel<3><<<gr, th, 0, s>>>(G, c.alpha, x, y); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
 }
 
 static void bt_solve(Ctx& c, const double* in, double* out, cudaStream_t s) {
   const Geometry& G = c.geo;
+  PhaseScope ps(c.prof, "apply.bt_solve", s);
   const int th = G.m_pad <= 32 ? 32 : 64;
   const size_t smem = sizeof(double) * (G.nI_pad + 2LL * G.m_pad * G.m_pad);
   static size_t attr = 0;
@@ -281,8 +282,8 @@ static void bt_solve(Ctx& c, const double* in, double* out, cudaStream_t s) {
     BDDC_CUDA(cudaFuncSetAttribute(bt_solve_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
-  if (G.dim == 2) bt_solve_kernel<2><<<G.nsub, th, smem, s>>>(G, c.lt, c.LI, in, out);
-  else bt_solve_kernel<3><<<G.nsub, th, smem, s>>>(G, c.lt, c.LI, in, out);
+  if (G.dim == 2) { bt_solve_kernel<2><<<G.nsub, th, smem, s>>>(G, c.lt, c.LI, in, out); BDDC_COUNT(); }
+  else { bt_solve_kernel<3><<<G.nsub, th, smem, s>>>(G, c.lt, c.LI, in, out); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
 }
 
@@ -290,8 +291,8 @@ static void bt_solve(Ctx& c, const double* in, double* out, cudaStream_t s) {
 void harmonic_interior(Ctx& c, double* out, cudaStream_t s) {
   const Geometry& G = c.geo;
   const int th = 256, gr = grid_for(G.n, th);
-  if (G.dim == 2) residual_kernel<2><<<gr, th, 0, s>>>(G, c.alpha, c.v1, out, c.v2);
-  else residual_kernel<3><<<gr, th, 0, s>>>(G, c.alpha, c.v1, out, c.v2);
+  if (G.dim == 2) { residual_kernel<2><<<gr, th, 0, s>>>(G, c.alpha, c.v1, out, c.v2); BDDC_COUNT(); }
+  else { residual_kernel<3><<<gr, th, 0, s>>>(G, c.alpha, c.v1, out, c.v2); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
   bt_solve(c, c.v2, out, s);
 }
@@ -304,34 +305,39 @@ void apply_bddc(Ctx& c, const double* r, double* z, cudaStream_t s) {
   bt_solve(c, r, c.v1, s);
   if (c.n_gamma > 0) {
     if (G.dim == 2)
-      gamma_residual_kernel<2><<<ceil_div(c.n_gamma, th), th, 0, s>>>(G, c.n_gamma, c.gamma_dof, c.alpha, r, c.v1, c.rpg);
+      { gamma_residual_kernel<2><<<ceil_div(c.n_gamma, th), th, 0, s>>>(G, c.n_gamma, c.gamma_dof, c.alpha, r, c.v1, c.rpg); BDDC_COUNT(); }
     else
-      gamma_residual_kernel<3><<<ceil_div(c.n_gamma, th), th, 0, s>>>(G, c.n_gamma, c.gamma_dof, c.alpha, r, c.v1, c.rpg);
+      { gamma_residual_kernel<3><<<ceil_div(c.n_gamma, th), th, 0, s>>>(G, c.n_gamma, c.gamma_dof, c.alpha, r, c.v1, c.rpg); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
     const size_t smem1 = sizeof(double) * 2 * G.nG_pad;
-    local_gamma1_kernel<<<G.nsub, 128, smem1, s>>>(G, c.st, c.LS, c.Phi, c.cscale, c.rpg, c.qloc,
-                                                   c.uloc, c.tloc);
+    c.prof.begin("apply.gamma1", s);
+    { local_gamma1_kernel<<<G.nsub, 128, smem1, s>>>(G, c.st, c.LS, c.Phi, c.cscale, c.rpg, c.qloc,
+                                                   c.uloc, c.tloc); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
+    c.prof.end("apply.gamma1", s);
     if (c.fp.n_coarse > 0) {
-      coarse_gather_kernel<<<ceil_div(c.fp.n_coarse, th), th, 0, s>>>(c.fp.n_coarse, c.fp.W,
-                                                                     c.fp.coarse_slots, c.qloc, c.crhs);
+      PhaseScope pc(c.prof, "apply.coarse", s);
+      { coarse_gather_kernel<<<ceil_div(c.fp.n_coarse, th), th, 0, s>>>(c.fp.n_coarse, c.fp.W,
+                                                                     c.fp.coarse_slots, c.qloc, c.crhs); BDDC_COUNT(); }
       BDDC_LAUNCH_CHECK();
       coarse_solve(c, c.crhs, c.csol, s);
     }
-    local_gamma2_kernel<<<G.nsub, 128, 0, s>>>(G, c.st, c.Phi, c.cscale, c.csol, c.uloc, c.tloc,
-                                               c.wloc);
+    c.prof.begin("apply.gamma2", s);
+    { local_gamma2_kernel<<<G.nsub, 128, 0, s>>>(G, c.st, c.Phi, c.cscale, c.csol, c.uloc, c.tloc,
+                                               c.wloc); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
+    c.prof.end("apply.gamma2", s);
   }
   BDDC_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * G.n, s));
   if (c.n_gamma > 0) {
-    gamma_gather_kernel<<<ceil_div(c.n_gamma, th), th, 0, s>>>(c.n_gamma, G.npe,
-                                                               c.gamma_dof, c.gamma_slots, c.wloc, z);
+    { gamma_gather_kernel<<<ceil_div(c.n_gamma, th), th, 0, s>>>(c.n_gamma, G.npe,
+                                                               c.gamma_dof, c.gamma_slots, c.wloc, z); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
   }
   // z_I = A_II^{-1} (r - A z_Gamma)_I
   const int gr = grid_for(G.n, th);
-  if (G.dim == 2) residual_kernel<2><<<gr, th, 0, s>>>(G, c.alpha, r, z, c.v2);
-  else residual_kernel<3><<<gr, th, 0, s>>>(G, c.alpha, r, z, c.v2);
+  if (G.dim == 2) { residual_kernel<2><<<gr, th, 0, s>>>(G, c.alpha, r, z, c.v2); BDDC_COUNT(); }
+  else { residual_kernel<3><<<gr, th, 0, s>>>(G, c.alpha, r, z, c.v2); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
   bt_solve(c, c.v2, z, s);
 }

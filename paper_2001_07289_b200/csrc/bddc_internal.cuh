@@ -7,6 +7,8 @@
 //     the reference's gamma_local order, bddc.py:429-433), padded to nG_pad; Dirichlet
 //     surface nodes keep their slot as a decoupled identity row.
 #pragma once
+#include <map>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -111,8 +113,63 @@ struct LevelSchedule {
   size_t max_fwd_smem = 0;
 };
 
+// Optional per-phase CUDA-event timers (bench.py reads them for the roofline of the
+// dominant kernel; disabled by default, zero cost when off).
+struct PhaseTimers {
+  bool on = false;
+  struct Timer {
+    std::vector<cudaEvent_t> ev;  // pairs
+    size_t used = 0;
+  };
+  std::map<std::string, Timer> t;
+  void begin(const char* name, cudaStream_t s) {
+    if (!on) return;
+    Timer& tm = t[name];
+    if (tm.used + 2 > tm.ev.size()) {
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      tm.ev.push_back(a);
+      tm.ev.push_back(b);
+    }
+    cudaEventRecord(tm.ev[tm.used], s);
+  }
+  void end(const char* name, cudaStream_t s) {
+    if (!on) return;
+    Timer& tm = t[name];
+    cudaEventRecord(tm.ev[tm.used + 1], s);
+    tm.used += 2;
+  }
+  void reset() {
+    for (auto& kv : t) kv.second.used = 0;
+  }
+  // total ms and count (synchronizes on the events)
+  double read(const std::string& name, long long* count) {
+    auto it = t.find(name);
+    if (it == t.end()) { *count = 0; return 0.0; }
+    double tot = 0.0;
+    for (size_t i = 0; i + 1 < it->second.used; i += 2) {
+      float ms = 0.f;
+      cudaEventSynchronize(it->second.ev[i + 1]);
+      cudaEventElapsedTime(&ms, it->second.ev[i], it->second.ev[i + 1]);
+      tot += ms;
+    }
+    *count = (long long)(it->second.used / 2);
+    return tot;
+  }
+};
+
+struct PhaseScope {
+  PhaseTimers& pt;
+  const char* name;
+  cudaStream_t s;
+  PhaseScope(PhaseTimers& p, const char* n, cudaStream_t st) : pt(p), name(n), s(st) { pt.begin(n, s); }
+  ~PhaseScope() { pt.end(name, s); }
+};
+
 struct Ctx {
   int device = 0;
+  PhaseTimers prof;
   cudaStream_t stream = nullptr;
   Geometry geo{};
   int element = 0;

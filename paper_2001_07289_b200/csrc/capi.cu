@@ -14,6 +14,7 @@ using namespace bddc;
 
 struct bddc_ctx {
   Ctx c;
+  cudaEvent_t ev[8] = {};
   double* ws = nullptr;
   size_t ws_doubles = 0;
   double* alpha_host_shadow = nullptr;
@@ -374,7 +375,7 @@ int bddc_harmonic(bddc_ctx* h, const double* g, double* out, void* stream) {
     BDDC_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * G.n, s));
     BDDC_CUDA(cudaMemsetAsync(c.v1, 0, sizeof(double) * G.n, s));
     if (c.n_gamma)
-      scatter_gamma_kernel<<<ceil_div(c.n_gamma, 256), 256, 0, s>>>(c.n_gamma, c.gamma_dof, g, out);
+      { scatter_gamma_kernel<<<ceil_div(c.n_gamma, 256), 256, 0, s>>>(c.n_gamma, c.gamma_dof, g, out); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
     harmonic_interior(c, out, s);
   }); });
@@ -465,6 +466,35 @@ int bddc_kernel_launches_per_apply(bddc_ctx* h) {
   int n = 2 + 1 + 1 + 1 + 1 + 1;
   if (c.fp.n_coarse) n += 1 + 2 * c.fp.nlevels;
   return n;
+}
+
+long long bddc_launch_count(void) { return launch_counter().load(); }
+
+int bddc_event_record(bddc_ctx* h, int slot) {
+  if (!h || slot < 0 || slot >= 8) return 1;
+  if (!h->ev[slot] && cudaEventCreate(&h->ev[slot]) != cudaSuccess) return 6;
+  return cudaEventRecord(h->ev[slot], h->c.stream) == cudaSuccess ? 0 : 6;
+}
+
+double bddc_event_elapsed_ms(bddc_ctx* h, int a, int b) {
+  if (!h || a < 0 || b < 0 || a >= 8 || b >= 8 || !h->ev[a] || !h->ev[b]) return -1.0;
+  float ms = 0.f;
+  if (cudaEventSynchronize(h->ev[b]) != cudaSuccess) return -1.0;
+  if (cudaEventElapsedTime(&ms, h->ev[a], h->ev[b]) != cudaSuccess) return -1.0;
+  return ms;
+}
+
+int bddc_profile(bddc_ctx* h, int enable) {
+  if (!h) return 1;
+  cudaStreamSynchronize(h->c.stream);
+  h->c.prof.on = enable != 0;
+  h->c.prof.reset();
+  return 0;
+}
+
+double bddc_profile_read(bddc_ctx* h, const char* phase, long long* count) {
+  if (!h || !phase || !count) return -1.0;
+  return h->c.prof.read(phase, count);
 }
 
 long long bddc_debug_copy(bddc_ctx* h, const char* name, double* host, long long cap) {

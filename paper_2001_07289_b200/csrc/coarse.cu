@@ -176,13 +176,14 @@ void coarse_assemble_and_factor(Ctx& c) {
   if (fp.n_coarse == 0) return;
   cudaStream_t s = c.stream;
   LevelSchedule& ls = c.sched;
+  PhaseScope ps(c.prof, "setup.coarse", s);
   const int th = 256;
-  csr_segsum_kernel<<<std::min<long long>((fp.nnz + th - 1) / th, 148 * 16), th, 0, s>>>(
-      fp.nnz, fp.seg_ptr, fp.contrib, c.Sloc, fp.csr_val);
+  { csr_segsum_kernel<<<std::min<long long>((fp.nnz + th - 1) / th, 148 * 16), th, 0, s>>>(
+      fp.nnz, fp.seg_ptr, fp.contrib, c.Sloc, fp.csr_val); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
   BDDC_CUDA(cudaMemsetAsync(fd.fronts, 0, sizeof(double) * fp.front_pool, s));
-  csr_to_front_kernel<<<std::min<long long>((fp.nnz + th - 1) / th, 148 * 16), th, 0, s>>>(
-      fp.nnz, fp.csr_front_pos, fp.csr_val, fd.fronts);
+  { csr_to_front_kernel<<<std::min<long long>((fp.nnz + th - 1) / th, 148 * 16), th, 0, s>>>(
+      fp.nnz, fp.csr_front_pos, fp.csr_val, fd.fronts); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
   for (int l = 0; l < fp.nlevels; ++l) {
     const int nn = ls.nodes_off[l + 1] - ls.nodes_off[l];
@@ -190,9 +191,9 @@ void coarse_assemble_and_factor(Ctx& c) {
     if (l > 0) {
       for (int k = 0; k < ls.max_children; ++k) {
         dim3 grid(64, nn);
-        extend_add_kernel<<<grid, 256, 0, s>>>(nodes, k, fd.child_ptr, fd.child_list,
+        { extend_add_kernel<<<grid, 256, 0, s>>>(nodes, k, fd.child_ptr, fd.child_list,
                                                fd.sep_size, fd.bnd_size, fd.ld,
-                                               fd.front_off, fd.rmap, fd.rmap_ptr, fd.fronts);
+                                               fd.front_off, fd.rmap, fd.rmap_ptr, fd.fronts); BDDC_COUNT(); }
         BDDC_LAUNCH_CHECK();
       }
     }
@@ -228,12 +229,12 @@ void coarse_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s) {
   }
   for (int l = 0; l < fp.nlevels; ++l) {
     const int nn = ls.nodes_off[l + 1] - ls.nodes_off[l];
-    front_fwd_kernel<<<nn, 256, smem, s>>>(ls.d_nodes + ls.nodes_off[l], fd, rhs, sol);
+    { front_fwd_kernel<<<nn, 256, smem, s>>>(ls.d_nodes + ls.nodes_off[l], fd, rhs, sol); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
   }
   for (int l = fp.nlevels - 1; l >= 0; --l) {
     const int nn = ls.nodes_off[l + 1] - ls.nodes_off[l];
-    front_bwd_kernel<<<nn, 256, smem, s>>>(ls.d_nodes + ls.nodes_off[l], fd, sol);
+    { front_bwd_kernel<<<nn, 256, smem, s>>>(ls.d_nodes + ls.nodes_off[l], fd, sol); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
   }
 }

@@ -1,6 +1,8 @@
 // Shared helpers for the BDDC-SO sm_100a kernels.
 #pragma once
 #include <cuda_runtime.h>
+
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
@@ -21,6 +23,13 @@ struct CudaError : std::runtime_error {
   } while (0)
 
 #define BDDC_LAUNCH_CHECK() BDDC_CUDA(cudaGetLastError())
+
+// Number of kernels this library has launched (reported by bench.py as gpu_launches).
+inline std::atomic<long long>& launch_counter() {
+  static std::atomic<long long> c{0};
+  return c;
+}
+#define BDDC_COUNT() (::bddc::launch_counter().fetch_add(1, std::memory_order_relaxed))
 
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 inline long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }

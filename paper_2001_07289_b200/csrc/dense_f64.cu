@@ -323,7 +323,7 @@ void launch_trsm(const TileArgs& a, cudaStream_t s) {
   int nvec = a.tasks ? a.max_nvec : a.nvec;
   if (nvec <= 0 || a.count <= 0) return;
   dim3 grid(ceil_div(nvec, 64), a.count);
-  trsm_tile_kernel<R, F><<<grid, 64, kTrsmSmem, s>>>(a);
+  { trsm_tile_kernel<R, F><<<grid, 64, kTrsmSmem, s>>>(a); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
 }
 
@@ -333,16 +333,16 @@ void gemm(const GemmArgs& a, bool tA, bool tB, cudaStream_t s) {
   int M = a.tasks ? a.max_M : a.M, N = a.tasks ? a.max_N : a.N;
   if (M <= 0 || N <= 0 || a.count <= 0) return;
   dim3 grid(ceil_div(M, BM) * ceil_div(N, BN), a.count);
-  if (!tA && !tB) gemm_f64_kernel<false, false><<<grid, 128, 0, s>>>(a);
-  else if (!tA && tB) gemm_f64_kernel<false, true><<<grid, 128, 0, s>>>(a);
-  else if (tA && !tB) gemm_f64_kernel<true, false><<<grid, 128, 0, s>>>(a);
-  else gemm_f64_kernel<true, true><<<grid, 128, 0, s>>>(a);
+  if (!tA && !tB) { gemm_f64_kernel<false, false><<<grid, 128, 0, s>>>(a); BDDC_COUNT(); }
+  else if (!tA && tB) { gemm_f64_kernel<false, true><<<grid, 128, 0, s>>>(a); BDDC_COUNT(); }
+  else if (tA && !tB) { gemm_f64_kernel<true, false><<<grid, 128, 0, s>>>(a); BDDC_COUNT(); }
+  else { gemm_f64_kernel<true, true><<<grid, 128, 0, s>>>(a); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
 }
 
 void potrf_tile(const TileArgs& a, cudaStream_t s) {
   if (a.count <= 0) return;
-  potrf_tile_kernel<<<a.count, 128, 0, s>>>(a);
+  { potrf_tile_kernel<<<a.count, 128, 0, s>>>(a); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
 }
 

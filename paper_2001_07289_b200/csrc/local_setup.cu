@@ -263,15 +263,20 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
     BDDC_CUDA(cudaMemsetAsync(LS, 0, sizeof(double) * cnt * lsS, s));
     BDDC_CUDA(cudaMemsetAsync(PH, 0, sizeof(double) * cnt * phS, s));
     // 1. assembly
+    c.prof.begin("setup.assemble", s);
     if (G.dim == 2)
-      assemble_local_kernel<2><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, LI, E, c.LS, c.diag_s);
+      { assemble_local_kernel<2><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, LI, E, c.LS, c.diag_s); BDDC_COUNT(); }
     else
-      assemble_local_kernel<3><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, LI, E, c.LS, c.diag_s);
+      { assemble_local_kernel<3><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, LI, E, c.LS, c.diag_s); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
+    c.prof.end("setup.assemble", s);
     // 2. interior block-tridiagonal Cholesky
-    btchol_kernel<<<cnt, 128, btchol_smem, s>>>(G, sub0, LI, c.info);
+    c.prof.begin("setup.btchol", s);
+    { btchol_kernel<<<cnt, 128, btchol_smem, s>>>(G, sub0, LI, c.info); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
+    c.prof.end("setup.btchol", s);
     // 3. E <- L_I^{-1} E, block forward substitution over planes
+    c.prof.begin("setup.E", s);
     for (int j = 0; j < G.nblk; ++j) {
       BMat Ej{E + (long long)j * G.m_pad, eS, G.nI_pad};
       if (j > 0) {
@@ -284,24 +289,30 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
       t.B = Ej.p; t.sB = eS; t.ldb = G.nI_pad; t.nvec = G.nG_pad; t.count = cnt;
       trsm_tile(t, TRSM_LLN, s);
     }
+    c.prof.end("setup.E", s);
     // S_Gamma = A_GG - E^T E  (in LS)
+    c.prof.begin("setup.SG", s);
     BMat Eb{E, eS, G.nI_pad};
     BMat LSb{LS, lsS, G.nG_pad};
     gemm_batched(true, false, G.nG_pad, G.nG_pad, G.nI_pad, -1.0, Eb, Eb, 1.0, LSb, cnt, s);
     BDDC_CUDA(cudaMemcpyAsync(SG, LS, sizeof(double) * cnt * lsS, cudaMemcpyDeviceToDevice, s));
+    c.prof.end("setup.SG", s);
     // 4. S_K = S_Gamma + s C^T C; Cholesky
-    add_ctc_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, c.diag_s, c.LS);
+    c.prof.begin("setup.SK", s);
+    { add_ctc_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, c.diag_s, c.LS); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
     potrf_batched(LSb, G.nG_pad, G.nG_pad, cnt, c.info_k + sub0, s);
+    c.prof.end("setup.SK", s);
     if (G.nc_pad > 0) {
+      PhaseScope pphi(c.prof, "setup.Phi", s);
       // 5. G = L_S^{-1} C^T ; S_C = G^T G ; Phi = L_S^{-T} G S_C^{-1}
-      build_ct_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, c.Phi);
+      { build_ct_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, c.Phi); BDDC_COUNT(); }
       BDDC_LAUNCH_CHECK();
       BMat PHb{PH, phS, G.nG_pad};
       BMat SCb{SC, scS, G.nc_pad};
       trsm_batched(TRSM_LLN, LSb, G.nG_pad, PHb, G.nc_pad, cnt, s);
       gemm_batched(true, false, G.nc_pad, G.nc_pad, G.nG_pad, 1.0, PHb, PHb, 0.0, SCb, cnt, s);
-      sc_pad_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, SC);
+      { sc_pad_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, SC); BDDC_COUNT(); }
       BDDC_LAUNCH_CHECK();
       potrf_batched(SCb, G.nc_pad, G.nc_pad, cnt, nullptr, s);
       trsm_batched(TRSM_RLT, SCb, G.nc_pad, PHb, G.nG_pad, cnt, s);
@@ -313,8 +324,8 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
       BMat Pb{P, scS, G.nc_pad};
       gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nG_pad, 1.0, SGb, PHb, 0.0, Xb, cnt, s);
       gemm_batched(true, false, G.nc_pad, G.nc_pad, G.nG_pad, 1.0, PHb, Xb, 0.0, Pb, cnt, s);
-      finish_local_kernel<<<cnt, 256, 0, s>>>(G, sub0, c.coarse_scaling, c.diag_s, c.cscale, P,
-                                              c.Sloc);
+      { finish_local_kernel<<<cnt, 256, 0, s>>>(G, sub0, c.coarse_scaling, c.diag_s, c.cscale, P,
+                                              c.Sloc); BDDC_COUNT(); }
       BDDC_LAUNCH_CHECK();
     }
   }

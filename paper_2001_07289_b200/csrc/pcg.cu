@@ -96,8 +96,8 @@ __global__ void copy_scalar_kernel(double* dst, const double* src) { *dst = *src
 }  // namespace
 
 double dot(Ctx& c, const double* a, const double* b, long long n, cudaStream_t s) {
-  dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(a, b, n, c.red);
-  reduce_final_kernel<<<1, 1024, 0, s>>>(c.red, kRedBlocks, c.scal + 7);
+  { dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(a, b, n, c.red); BDDC_COUNT(); }
+  { reduce_final_kernel<<<1, 1024, 0, s>>>(c.red, kRedBlocks, c.scal + 7); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
   BDDC_CUDA(cudaMemcpyAsync(c.h_scal + 7, c.scal + 7, sizeof(double), cudaMemcpyDeviceToHost, s));
   BDDC_CUDA(cudaStreamSynchronize(s));
@@ -105,8 +105,8 @@ double dot(Ctx& c, const double* a, const double* b, long long n, cudaStream_t s
 }
 
 static void dot_to(Ctx& c, const double* a, const double* b, long long n, double* out, cudaStream_t s) {
-  dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(a, b, n, c.red);
-  reduce_final_kernel<<<1, 1024, 0, s>>>(c.red, kRedBlocks, out);
+  { dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(a, b, n, c.red); BDDC_COUNT(); }
+  { reduce_final_kernel<<<1, 1024, 0, s>>>(c.red, kRedBlocks, out); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
 }
 
@@ -139,11 +139,13 @@ PcgResult pcg_solve(Ctx& c, const double* b, double* x, double tol, int max_iter
   BDDC_CUDA(cudaMemcpyAsync(c.p, c.z, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   int nbeta = 0;
   for (int it = 0; it < max_iters; ++it) {
-    if (G.dim == 2) spmv_dot_kernel<2><<<kRedBlocks, kRedThreads, 0, s>>>(G, c.alpha, c.p, c.Ap, c.red);
-    else spmv_dot_kernel<3><<<kRedBlocks, kRedThreads, 0, s>>>(G, c.alpha, c.p, c.Ap, c.red);
-    reduce_final_kernel<<<1, 1024, 0, s>>>(c.red, kRedBlocks, sc + 1);
-    update_xr_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(x, c.r, c.p, c.Ap, sc, n, c.red);
-    reduce_final_kernel<<<1, 1024, 0, s>>>(c.red, kRedBlocks, sc + 2);
+    c.prof.begin("pcg.spmv_dot", s);
+    if (G.dim == 2) { spmv_dot_kernel<2><<<kRedBlocks, kRedThreads, 0, s>>>(G, c.alpha, c.p, c.Ap, c.red); BDDC_COUNT(); }
+    else { spmv_dot_kernel<3><<<kRedBlocks, kRedThreads, 0, s>>>(G, c.alpha, c.p, c.Ap, c.red); BDDC_COUNT(); }
+    { reduce_final_kernel<<<1, 1024, 0, s>>>(c.red, kRedBlocks, sc + 1); BDDC_COUNT(); }
+    c.prof.end("pcg.spmv_dot", s);
+    { update_xr_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(x, c.r, c.p, c.Ap, sc, n, c.red); BDDC_COUNT(); }
+    { reduce_final_kernel<<<1, 1024, 0, s>>>(c.red, kRedBlocks, sc + 2); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
     BDDC_CUDA(cudaMemcpyAsync(hs, sc, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
     BDDC_CUDA(cudaStreamSynchronize(s));
@@ -184,8 +186,8 @@ PcgResult pcg_solve(Ctx& c, const double* b, double* x, double tol, int max_iter
     }
     apply_bddc(c, c.r, c.z, s);
     dot_to(c, c.r, c.z, n, sc + 3, s);
-    xpay_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(c.p, c.z, sc, n);
-    copy_scalar_kernel<<<1, 1, 0, s>>>(sc + 0, sc + 3);
+    { xpay_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(c.p, c.z, sc, n); BDDC_COUNT(); }
+    { copy_scalar_kernel<<<1, 1, 0, s>>>(sc + 0, sc + 3); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
   }
   return res;
