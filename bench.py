@@ -152,8 +152,9 @@ def phase_work(op, pb, its):
     n = int(st.n)
     T = lambda k: k * (k + 1) / 2  # noqa: E731
     w = {}
-    # interior solve: Ld_j lower + Lo_j dense, forward and backward, + vector in/out
-    li = nblk * T(m) + max(nblk - 1, 0) * m * m
+    # interior solve: packed Linv_j (T(m_pad)) + coupling stencil, forward and backward,
+    # + vector gather / scatter (as stored: li_stride doubles per subdomain)
+    li = nblk * T(lay.m_pad) + nblk * lay.m_pad * (1 if pb["mesh"].element == "p1" else 3 ** (lay.dim - 1))
     w["apply.bt_solve"] = ("hbm", 8.0 * (2 * nsub * li + 2 * nsub * nI))
     # local Gamma phase 1: L_S forward + backward (lower), Phi^T rho
     w["apply.gamma1"] = ("hbm", 8.0 * float(np.sum(2 * T(nG) + nG * nc)))

@@ -50,21 +50,69 @@ __global__ void gamma_residual_kernel(Geometry G, int n_gamma, const long long* 
   rpg[g] = r[f] - stencil_row<DIM>(G, alpha, u1, g0, g1, g2);
 }
 
-// Block-tridiagonal interior solve x_I = A_II^{-1} b_I per subdomain (forward + backward).
-template <int DIM>
-__global__ void bt_solve_kernel(Geometry G, LocalTables lt, const double* __restrict__ LI,
-                                const double* __restrict__ in, double* __restrict__ out) {
-  extern __shared__ double sm[];
-  const int M = G.m_pad;
-  const long long mm = (long long)M * M;
-  double* y = sm;             // nI_pad
-  double* Ld = sm + G.nI_pad; // M*M
-  double* Lo = Ld + mm;       // M*M
-  const int sub = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+// Block-tridiagonal interior solve x_I = A_II^{-1} b_I, one warp per subdomain.
+// Factor = packed inverses Linv_j of the diagonal Cholesky blocks + the sparse coupling
+// stencil B_j to the previous plane (Lo_j = B_j Linv_{j-1}^T):
+//   forward   t = b_j - B_j u_{j-1};  y_j = Linv_j t;  u_j = Linv_j^T y_j
+//   backward  t = B_{j+1}^T x_{j+1};  v = y_j - Linv_j t;  x_j = Linv_j^T v
+// Each lane owns rows r = lane + 32 i (i < R); the GEMVs broadcast the vector with
+// shuffles and read the packed column-major blocks straight from the cp.async staging
+// buffers (double-buffered: block j+-1 streams in while block j is used). Each Linv_j is
+// read from HBM once per pass.
+constexpr int kBtWarps = 4;
+
+template <int R>
+__device__ __forceinline__ void bt_bcast_gemv(const double* __restrict__ pk, int M, const double (&v)[R],
+                                              double (&out)[R], bool trans, int lane) {
+  // out_r = sum_k L[r][k] v_k  (trans: sum_k L[k][r] v_k), L packed lower column-major
+#pragma unroll
+  for (int i = 0; i < R; ++i) out[i] = 0.0;
+  for (int k = 0; k < M; ++k) {
+    double vk = 0.0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const double b = __shfl_sync(0xffffffffu, v[i], k & 31);
+      if ((k >> 5) == i) vk = b;
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int r = lane + 32 * i;
+      if (r >= M) continue;
+      if (!trans) {
+        if (k <= r) out[i] += pk[k * M - k * (k - 1) / 2 + (r - k)] * vk;
+      } else {
+        if (k >= r) out[i] += pk[r * M - r * (r - 1) / 2 + (k - r)] * vk;
+      }
+    }
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(32 * kBtWarps) bt_solve_kernel(Geometry G, LocalTables lt,
+                                                                 const double* __restrict__ LI,
+                                                                 const double* __restrict__ in,
+                                                                 double* __restrict__ out) {
+  extern __shared__ __align__(16) double sm[];
+  const int M = G.m_pad, Tm = G.Tm;
+  const int tm_pad = (Tm + 1) & ~1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = blockIdx.x * kBtWarps + warp;
+  const int per_warp = G.nI_pad + 2 * tm_pad + M + (M & 1);
+  double* y = sm + warp * per_warp;  // nI_pad
+  double* stg[2] = {y + G.nI_pad, y + G.nI_pad + tm_pad};
+  double* uv = y + G.nI_pad + 2 * tm_pad;  // M
+  if (sub >= G.nsub) return;
   int p[3];
   sub_coords(G, sub, p);
-  const double* li = LI + (long long)sub * G.nblk * 2 * mm;
-  for (int rr = tid; rr < G.nI_pad; rr += nt) {
+  const double* li = LI + (long long)sub * G.li_stride;
+  const double* bc = li + (long long)G.nblk * Tm;
+  const int px = G.blk[0] - 1;
+  auto prefetch = [&](int j, double* dst) {
+    const double* src = li + (long long)j * Tm;
+    for (int e = 2 * lane; e < Tm; e += 64) cp_async16(dst + e, src + e, min(2, Tm - e) * 8);
+    cp_async_commit();
+  };
+  for (int rr = lane; rr < G.nI_pad; rr += 32) {
     const int node = lt.irow_node[rr];
     double v = 0.0;
     if (node >= 0) {
@@ -74,59 +122,96 @@ __global__ void bt_solve_kernel(Geometry G, LocalTables lt, const double* __rest
     }
     y[rr] = v;
   }
-  // forward: y_j = Ld_j^{-1} (b_j - Lo_j y_{j-1})
+  double t[R], yv[R];
+  // ---- forward ----
+  if (G.nblk > 0) prefetch(0, stg[0]);
   for (int j = 0; j < G.nblk; ++j) {
-    for (int idx = tid; idx < mm; idx += nt) Ld[idx] = li[2LL * j * mm + idx];
-    if (j > 0)
-      for (int idx = tid; idx < mm; idx += nt) Lo[idx] = li[(2LL * j + 1) * mm + idx];
-    __syncthreads();
-    double* yj = y + j * M;
-    if (j > 0 && tid < M) {
-      const double* yp = y + (j - 1) * M;
-      double s0 = 0.0, s1 = 0.0;
-      int k = 0;
-      for (; k + 1 < M; k += 2) {
-        s0 += Lo[tid + k * M] * yp[k];
-        s1 += Lo[tid + (k + 1) * M] * yp[k + 1];
+    const double* pk = stg[j & 1];
+    if (j + 1 < G.nblk) {
+      prefetch(j + 1, stg[(j + 1) & 1]);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int r = lane + 32 * i;
+      double acc = 0.0;
+      if (r < M) {
+        acc = y[j * M + r];
+        if (j > 0) {
+          const double* bj = bc + ((long long)j * M + r) * G.nbo;
+          const int x = r % px, yy = r / px;
+          for (int k = 0; k < G.nbo; ++k) {
+            const double cf = bj[k];
+            if (cf != 0.0) acc -= cf * uv[(x + G.bo_dx[k]) + (yy + G.bo_dy[k]) * px];
+          }
+        }
       }
-      if (k < M) s0 += Lo[tid + k * M] * yp[k];
-      yj[tid] -= s0 + s1;
+      t[i] = acc;
     }
-    __syncthreads();
-    for (int k = 0; k < M; ++k) {
-      if (tid == k) yj[k] /= Ld[k + k * M];
-      __syncthreads();
-      if (tid > k && tid < M) yj[tid] -= Ld[tid + k * M] * yj[k];
-    }
-    __syncthreads();
+    __syncwarp();
+    bt_bcast_gemv<R>(pk, M, t, yv, false, lane);
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+      if (lane + 32 * i < M) y[j * M + lane + 32 * i] = yv[i];
+    bt_bcast_gemv<R>(pk, M, yv, t, true, lane);  // u_j = Linv_j^T y_j
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+      if (lane + 32 * i < M) uv[lane + 32 * i] = t[i];
+    __syncwarp();
   }
-  // backward: x_j = Ld_j^{-T} (y_j - Lo_{j+1}^T x_{j+1})
-  for (int j = G.nblk - 1; j >= 0; --j) {
-    for (int idx = tid; idx < mm; idx += nt) Ld[idx] = li[2LL * j * mm + idx];
-    if (j + 1 < G.nblk)
-      for (int idx = tid; idx < mm; idx += nt) Lo[idx] = li[(2LL * (j + 1) + 1) * mm + idx];
-    __syncthreads();
-    double* yj = y + j * M;
-    if (j + 1 < G.nblk && tid < M) {
+  // ---- backward ----
+  if (G.nblk > 0) prefetch(G.nblk - 1, stg[0]);
+  for (int j = G.nblk - 1, it = 0; j >= 0; --j, ++it) {
+    const double* pk = stg[it & 1];
+    if (j > 0) {
+      prefetch(j - 1, stg[(it + 1) & 1]);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+    double v[R];
+    if (j + 1 < G.nblk) {
       const double* xn = y + (j + 1) * M;
-      double s0 = 0.0, s1 = 0.0;
-      int k = 0;
-      for (; k + 1 < M; k += 2) {
-        s0 += Lo[k + tid * M] * xn[k];
-        s1 += Lo[k + 1 + tid * M] * xn[k + 1];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const int r = lane + 32 * i;
+        double acc = 0.0;
+        if (r < M) {
+          const int x = r % px, yy = r / px;
+          for (int k = 0; k < G.nbo; ++k) {
+            const int rs = (x - G.bo_dx[k]) + (yy - G.bo_dy[k]) * px;
+            if (rs < 0 || rs >= M) continue;
+            const double cf = bc[((long long)(j + 1) * M + rs) * G.nbo + k];
+            if (cf != 0.0) acc += cf * xn[rs];
+          }
+        }
+        t[i] = acc;
       }
-      if (k < M) s0 += Lo[k + tid * M] * xn[k];
-      yj[tid] -= s0 + s1;
+      bt_bcast_gemv<R>(pk, M, t, v, false, lane);
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const int r = lane + 32 * i;
+        v[i] = r < M ? y[j * M + r] - v[i] : 0.0;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const int r = lane + 32 * i;
+        v[i] = r < M ? y[j * M + r] : 0.0;
+      }
     }
-    __syncthreads();
-    for (int k = M - 1; k >= 0; --k) {
-      if (tid == k) yj[k] /= Ld[k + k * M];
-      __syncthreads();
-      if (tid < k) yj[tid] -= Ld[k + tid * M] * yj[k];
-    }
-    __syncthreads();
+    bt_bcast_gemv<R>(pk, M, v, t, true, lane);
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+      if (lane + 32 * i < M) y[j * M + lane + 32 * i] = t[i];
+    __syncwarp();
   }
-  for (int rr = tid; rr < G.nI_pad; rr += nt) {
+  for (int rr = lane; rr < G.nI_pad; rr += 32) {
     const int node = lt.irow_node[rr];
     if (node >= 0) {
       int a[3];
@@ -274,16 +359,18 @@ void spmv(Ctx& c, const double* x, double* y, cudaStream_t s) {
 static void bt_solve(Ctx& c, const double* in, double* out, cudaStream_t s) {
   const Geometry& G = c.geo;
   PhaseScope ps(c.prof, "apply.bt_solve", s);
-  const int th = G.m_pad <= 32 ? 32 : 64;
-  const size_t smem = sizeof(double) * (G.nI_pad + 2LL * G.m_pad * G.m_pad);
+  const int tm_pad = (G.Tm + 1) & ~1;
+  const size_t per_warp = G.nI_pad + 2 * tm_pad + G.m_pad + (G.m_pad & 1);
+  const size_t smem = sizeof(double) * per_warp * kBtWarps;
   static size_t attr = 0;
   if (smem > attr) {
+    BDDC_CUDA(cudaFuncSetAttribute(bt_solve_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     BDDC_CUDA(cudaFuncSetAttribute(bt_solve_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    BDDC_CUDA(cudaFuncSetAttribute(bt_solve_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
-  if (G.dim == 2) { bt_solve_kernel<2><<<G.nsub, th, smem, s>>>(G, c.lt, c.LI, in, out); BDDC_COUNT(); }
-  else { bt_solve_kernel<3><<<G.nsub, th, smem, s>>>(G, c.lt, c.LI, in, out); BDDC_COUNT(); }
+  const int grid = ceil_div(G.nsub, kBtWarps);
+  if (G.m_pad <= 32) { bt_solve_kernel<1><<<grid, 32 * kBtWarps, smem, s>>>(G, c.lt, c.LI, in, out); BDDC_COUNT(); }
+  else { bt_solve_kernel<2><<<grid, 32 * kBtWarps, smem, s>>>(G, c.lt, c.LI, in, out); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
 }
 

@@ -30,6 +30,13 @@ struct Geometry {
   int nc_pad;
   int npe;      // nodes per element = 2^dim
   double K[64]; // reference element matrix (alpha = 1), row-major npe x npe
+  // interior factor storage per subdomain: nblk packed lower-triangular inverses of the
+  // diagonal Cholesky blocks (Tm = m_pad(m_pad+1)/2 doubles each), then the coupling
+  // stencil to the previous plane, Bc[j][r][k] for the nbo structurally nonzero offsets
+  int Tm;
+  int nbo;
+  int bo_dx[9], bo_dy[9];
+  long long li_stride;
 };
 
 // Decoded local node information (host-built tables, device copies).
@@ -92,11 +99,30 @@ struct FrontPlan {
   int* coarse_slots = nullptr;         // [n_coarse x W] (sub*nc_pad + k), -1 pad
   int W = 0;
   std::vector<int> level_list;         // nodes sorted by level (see level_ptr)
+  std::vector<int> rmap_host;          // aligned with bnd_idx
   int* info = nullptr;                 // per node pivot failure (global coarse index)
 };
 
 // Plan-time schedule of the multifrontal factorization: per level, per 64-column panel
 // step, device task arrays for the tile Cholesky / tile TRSM / lower GEMM launches.
+struct CsTask {  // coarse-solve GEMV tile
+  int node, r0, c0, part;
+};
+struct CsRed {  // coarse-solve reduction over the partials of one row / column tile
+  int node, t0, p0, np;
+};
+struct InvTask {  // per front: copy L11 to scratch, then panel <- panel * L11^{-1}
+  int node;
+  long long scr;  // scratch offset
+  int lds;
+};
+
+struct LevelView {  // POD view of the gather maps for kernels
+  const int* gat_ptr;
+  const long long* gat_off;
+  const int* gat_src;
+};
+
 struct LevelSchedule {
   struct Step {
     TileTask* potrf = nullptr;
@@ -106,7 +132,19 @@ struct LevelSchedule {
     GemmTask* gemm = nullptr;
     int n_gemm = 0, max_gemm = 0;
   };
-  std::vector<std::vector<Step>> steps;  // [level][step]
+  std::vector<std::vector<Step>> steps;      // [level][step] factorization
+  std::vector<std::vector<Step>> inv_steps;  // [level][step] panel <- panel L11^{-1} (RLN)
+  std::vector<InvTask*> inv_prep;            // [level]
+  std::vector<int> n_inv_prep;
+  double* inv_scratch = nullptr;
+  // solve: per level fwd / bwd GEMV tiles and reductions
+  std::vector<CsTask*> fwd_t, bwd_t;
+  std::vector<CsRed*> fwd_r, bwd_r;
+  std::vector<int> n_fwd_t, n_bwd_t, n_fwd_r, n_bwd_r;
+  double* partial = nullptr;
+  int* gat_ptr = nullptr;    // per node front position -> sources in the update pool
+  long long* gat_off = nullptr;  // per node offset into gat_ptr
+  int* gat_src = nullptr;
   int* d_nodes = nullptr;                // level node lists concatenated
   std::vector<int> nodes_off;
   int max_children = 0;
@@ -183,7 +221,7 @@ struct Ctx {
   long long* gamma_dof = nullptr;  // [n_gamma]
   int* gamma_slots = nullptr;      // [n_gamma x W]
   // factors (device)
-  double* LI = nullptr;      // [nsub x nblk x 2 x m_pad^2] block-tridiagonal interior factor
+  double* LI = nullptr;      // [nsub x li_stride] interior factor: packed L_j^{-1} + coupling stencil
   double* LS = nullptr;      // [nsub x nG_pad^2] Cholesky of S_K = S_Gamma + rho C^T C
   double* Phi = nullptr;     // [nsub x nG_pad x nc_pad] energy-minimal coarse basis on Gamma
   double* cscale = nullptr;  // [nsub] c_i (1/s_i^2 reference, 1 spec)

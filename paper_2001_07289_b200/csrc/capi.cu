@@ -169,6 +169,7 @@ void build_plan(Ctx& c, const bddc_setup_desc* d) {
   fd.bnd_ptr = c.upload(fp.bnd_ptr.data(), N + 1);
   fd.bnd_idx = c.upload(d->bnd_idx, fp.bnd_ptr[N]);
   fd.rmap = c.upload(d->rmap, fp.bnd_ptr[N]);
+  fp.rmap_host.assign(d->rmap, d->rmap + fp.bnd_ptr[N]);
   fd.rmap_ptr = fd.bnd_ptr;
   fp.info = c.alloc<int>(N);
   // CSR -> front positions
@@ -225,6 +226,29 @@ void do_setup(bddc_ctx* h, const bddc_setup_desc* d) {
   if (G.nG_pad > 1024 || G.nG_pad % 8 || G.nc_pad > 1024 || G.nc_pad % 8)
     throw ApiError{1, "interface / constraint padding out of range"};
   for (int i = 0; i < G.npe * G.npe; ++i) G.K[i] = d->elem_K[i];
+  // structurally nonzero couplings from a plane to the previous one (last axis -1)
+  G.nbo = 0;
+  for (int dy = -1; dy <= 1; ++dy)
+    for (int dx = -1; dx <= 1; ++dx) {
+      if (G.dim == 2 && dy != 0) continue;
+      bool used = false;
+      for (int s0 = 0; s0 < G.npe && !used; ++s0)
+        for (int t0 = 0; t0 < G.npe && !used; ++t0) {
+          if (G.K[s0 * G.npe + t0] == 0.0) continue;
+          int d[3];
+          for (int ax = 0; ax < G.dim; ++ax) d[ax] = ((t0 >> ax) & 1) - ((s0 >> ax) & 1);
+          const int last = d[G.dim - 1];
+          const int ddx = d[0], ddy = G.dim == 3 ? d[1] : 0;
+          if (last == -1 && ddx == dx && ddy == dy) used = true;
+        }
+      if (used) {
+        G.bo_dx[G.nbo] = dx;
+        G.bo_dy[G.nbo] = dy;
+        G.nbo++;
+      }
+    }
+  G.Tm = G.m_pad * (G.m_pad + 1) / 2;
+  G.li_stride = round_up((long long)G.nblk * G.Tm + (long long)G.nblk * G.m_pad * G.nbo, 2);
   c.element = d->element;
   c.coarse_scaling = d->coarse_scaling;
   h->ncells = ncells;
@@ -254,8 +278,7 @@ void do_setup(bddc_ctx* h, const bddc_setup_desc* d) {
   cudaEventDestroy(e1);
 
   // persistent factors and workspaces
-  const long long mm = (long long)G.m_pad * G.m_pad;
-  c.LI = c.alloc<double>((size_t)G.nsub * G.nblk * 2 * mm);
+  c.LI = c.alloc<double>((size_t)G.nsub * G.li_stride);
   c.LS = c.alloc<double>((size_t)G.nsub * G.nG_pad * G.nG_pad);
   c.Phi = c.alloc<double>((size_t)G.nsub * G.nG_pad * G.nc_pad);
   c.Sloc = c.alloc<double>((size_t)G.nsub * G.nc_pad * G.nc_pad);
@@ -439,7 +462,7 @@ int bddc_get_stats(bddc_ctx* h, bddc_stats* o) {
   o->n_gamma = c.n_gamma;
   o->n_coarse = c.fp.n_coarse;
   o->nsub = G.nsub;
-  o->factor_bytes = 8LL * G.nsub * (2LL * G.nblk * G.m_pad * G.m_pad + (long long)G.nG_pad * G.nG_pad +
+  o->factor_bytes = 8LL * G.nsub * (G.li_stride + (long long)G.nG_pad * G.nG_pad +
                                     (long long)G.nG_pad * G.nc_pad);
   o->front_bytes = 8LL * c.fp.front_pool;
   o->workspace_bytes = 8LL * h->ws_doubles;
@@ -504,7 +527,7 @@ long long bddc_debug_copy(bddc_ctx* h, const char* name, double* host, long long
   const double* src = nullptr;
   long long n = 0;
   std::string nm(name);
-  if (nm == "LI") { src = c.LI; n = (long long)G.nsub * G.nblk * 2 * G.m_pad * G.m_pad; }
+  if (nm == "LI") { src = c.LI; n = (long long)G.nsub * G.li_stride; }
   else if (nm == "LS") { src = c.LS; n = (long long)G.nsub * G.nG_pad * G.nG_pad; }
   else if (nm == "Phi") { src = c.Phi; n = (long long)G.nsub * G.nG_pad * G.nc_pad; }
   else if (nm == "Sloc") { src = c.Sloc; n = (long long)G.nsub * G.nc_pad * G.nc_pad; }

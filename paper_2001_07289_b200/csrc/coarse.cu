@@ -7,7 +7,6 @@
 #include <climits>
 
 #include "bddc_internal.cuh"
-#include "trsv.cuh"
 
 namespace bddc {
 
@@ -55,49 +54,125 @@ __global__ void extend_add_kernel(const int* __restrict__ nodes, int k, const in
   }
 }
 
-// Forward solve of one level: v = [rhs(sep); 0] + sum_children ext(upd_c);
-// y = L11^{-1} v_sep; v_bnd -= L21 y; sol(sep) = y; upd_node = v_bnd.
-__global__ void front_fwd_kernel(const int* __restrict__ nodes, FrontDev fd,
-                                 const double* __restrict__ rhs, double* __restrict__ sol) {
-  extern __shared__ double sm[];
-  double* dblk = sm;
-  double* v = sm + kTrsvB * kTrsvP;
-  const int node = nodes[blockIdx.x];
-  const int s = fd.sep_size[node], b = fd.bnd_size[node], f = s + b;
-  const int s0 = fd.sep_start[node];
-  for (int i = threadIdx.x; i < f; i += blockDim.x) v[i] = i < s ? rhs[s0 + i] : 0.0;
-  __syncthreads();
-  const int c0 = fd.child_ptr[node], c1 = fd.child_ptr[node + 1];
-  for (int c = c0; c < c1; ++c) {
-    const int ch = fd.child_list[c];
-    const int bc = fd.bnd_size[ch];
-    const int* rm = fd.rmap + fd.rmap_ptr[ch];
-    const double* u = fd.upd + fd.upd_off[ch];
-    for (int i = threadIdx.x; i < bc; i += blockDim.x) v[rm[i]] += u[i];
-    __syncthreads();
+// ---- partitioned-inverse preparation: copy L11 to scratch, replace it by the identity ----
+__global__ void inv_prep_kernel(const InvTask* __restrict__ tasks, FrontDev fd, double* scratch) {
+  const InvTask t = tasks[blockIdx.x];
+  const int s = fd.sep_size[t.node], ld = fd.ld[t.node];
+  double* F = fd.fronts + fd.front_off[t.node];
+  double* S = scratch + t.scr;
+  for (long long idx = threadIdx.x; idx < (long long)s * s; idx += blockDim.x) {
+    const int i = (int)(idx % s), j = (int)(idx / s);
+    S[i + (long long)j * t.lds] = i >= j ? F[i + (long long)j * ld] : 0.0;
   }
-  const double* F = fd.fronts + fd.front_off[node];
-  cta_trsv_fwd(F, fd.ld[node], f, s, v, dblk);
-  for (int i = threadIdx.x; i < f; i += blockDim.x) {
-    if (i < s) sol[s0 + i] = v[i];
-    else fd.upd[fd.upd_off[node] + (i - s)] = v[i];
+  __syncthreads();
+  for (long long idx = threadIdx.x; idx < (long long)s * s; idx += blockDim.x) {
+    const int i = (int)(idx % s), j = (int)(idx / s);
+    F[i + (long long)j * ld] = i == j ? 1.0 : 0.0;
   }
 }
 
-// Backward solve of one level: x_sep = L11^{-T} (y - L21^T x_bnd).
-__global__ void front_bwd_kernel(const int* __restrict__ nodes, FrontDev fd, double* __restrict__ sol) {
-  extern __shared__ double sm[];
-  double* dblk = sm;
-  double* v = sm + kTrsvB * kTrsvP;
-  const int node = nodes[blockIdx.x];
-  const int s = fd.sep_size[node], b = fd.bnd_size[node], f = s + b;
+// Sum of the children update entries landing on front position `pos` of `node`.
+__device__ __forceinline__ double gather_children(const LevelView& lv, const double* __restrict__ upd,
+                                                  int node, int pos) {
+  const int* gp = lv.gat_ptr + lv.gat_off[node];
+  double acc = 0.0;
+  for (int q = gp[pos]; q < gp[pos + 1]; ++q) acc += upd[lv.gat_src[q]];
+  return acc;
+}
+
+// Forward tile: partial[r] = sum_{k in [c0, c0+256)} F'[r][k] v_S[k] for rows [r0, r0+64),
+// F' = [L11^{-1}; L21 L11^{-1}], v_S = rhs(sep) + children updates.
+__global__ void __launch_bounds__(256) cs_fwd_partial_kernel(const CsTask* __restrict__ tasks, FrontDev fd,
+                                                             LevelView lv, const double* __restrict__ rhs,
+                                                             double* __restrict__ partial) {
+  __shared__ double vs[256];
+  __shared__ double red[4][64];
+  const CsTask t = tasks[blockIdx.x];
+  const int node = t.node, s = fd.sep_size[node], f = s + fd.bnd_size[node];
+  const long long ld = fd.ld[node];
+  const int s0 = fd.sep_start[node];
+  const double* F = fd.fronts + fd.front_off[node];
+  for (int k = threadIdx.x; k < 256; k += blockDim.x) {
+    const int kk = t.c0 + k;
+    vs[k] = kk < s ? rhs[s0 + kk] + gather_children(lv, fd.upd, node, kk) : 0.0;
+  }
+  __syncthreads();
+  const int rr = threadIdx.x & 63, grp = threadIdx.x >> 6;
+  const int r = t.r0 + rr;
+  double a0 = 0.0, a1 = 0.0;
+  if (r < f) {
+    int kb = t.c0 + grp * 64;
+    int ke = min(kb + 64, s);
+    if (r < s) ke = min(ke, r + 1);  // L11^{-1} is lower triangular
+    int k = kb;
+    for (; k + 1 < ke; k += 2) {
+      a0 += F[r + k * ld] * vs[k - t.c0];
+      a1 += F[r + (k + 1) * ld] * vs[k + 1 - t.c0];
+    }
+    if (k < ke) a0 += F[r + k * ld] * vs[k - t.c0];
+  }
+  red[grp][rr] = a0 + a1;
+  __syncthreads();
+  if (threadIdx.x < 64)
+    partial[(long long)t.part * 64 + threadIdx.x] = red[0][threadIdx.x] + red[1][threadIdx.x] +
+                                                   red[2][threadIdx.x] + red[3][threadIdx.x];
+}
+
+// Forward reduction: y_S -> sol(sep); update of the boundary -> upd pool.
+__global__ void cs_fwd_reduce_kernel(const CsRed* __restrict__ reds, FrontDev fd, LevelView lv,
+                                     const double* __restrict__ partial, double* __restrict__ sol) {
+  const CsRed t = reds[blockIdx.x];
+  const int node = t.node, s = fd.sep_size[node], f = s + fd.bnd_size[node];
+  const int r = t.t0 + threadIdx.x;
+  if (threadIdx.x >= 64 || r >= f) return;
+  double acc = 0.0;
+  for (int p = 0; p < t.np; ++p) acc += partial[(long long)(t.p0 + p) * 64 + threadIdx.x];
+  if (r < s) sol[fd.sep_start[node] + r] = acc;
+  else fd.upd[fd.upd_off[node] + (r - s)] = gather_children(lv, fd.upd, node, r) - acc;
+}
+
+// Backward tile: partial[k] = sum_{r in [r0, r0+256)} F'[r][k] w[r] for columns [c0, c0+64),
+// w = [y_S; -x_B].
+__global__ void __launch_bounds__(256) cs_bwd_partial_kernel(const CsTask* __restrict__ tasks, FrontDev fd,
+                                                             const double* __restrict__ sol,
+                                                             double* __restrict__ partial) {
+  __shared__ double w[256];
+  const CsTask t = tasks[blockIdx.x];
+  const int node = t.node, s = fd.sep_size[node], f = s + fd.bnd_size[node];
+  const long long ld = fd.ld[node];
   const int s0 = fd.sep_start[node];
   const int* bidx = fd.bnd_idx + fd.bnd_ptr[node];
-  for (int i = threadIdx.x; i < f; i += blockDim.x) v[i] = i < s ? sol[s0 + i] : sol[bidx[i - s]];
-  __syncthreads();
   const double* F = fd.fronts + fd.front_off[node];
-  cta_trsv_bwd(F, fd.ld[node], f, s, v, dblk);
-  for (int i = threadIdx.x; i < s; i += blockDim.x) sol[s0 + i] = v[i];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    const int r = t.r0 + i;
+    w[i] = r < s ? sol[s0 + r] : (r < f ? -sol[bidx[r - s]] : 0.0);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int cc = 0; cc < 8; ++cc) {
+    const int kl = warp * 8 + cc, k = t.c0 + kl;
+    double acc = 0.0;
+    if (k < s) {
+      const double* col = F + k * ld;
+      for (int i = lane; i < 256; i += 32) {
+        const int r = t.r0 + i;
+        if (r < f && (r >= s || r >= k)) acc += col[r] * w[i];
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) partial[(long long)t.part * 64 + kl] = acc;
+  }
+}
+
+__global__ void cs_bwd_reduce_kernel(const CsRed* __restrict__ reds, FrontDev fd,
+                                     const double* __restrict__ partial, double* __restrict__ sol) {
+  const CsRed t = reds[blockIdx.x];
+  const int node = t.node, s = fd.sep_size[node];
+  const int k = t.t0 + threadIdx.x;
+  if (threadIdx.x >= 64 || k >= s) return;
+  double acc = 0.0;
+  for (int p = 0; p < t.np; ++p) acc += partial[(long long)(t.p0 + p) * 64 + threadIdx.x];
+  sol[fd.sep_start[node] + k] = acc;
 }
 
 }  // namespace
@@ -167,7 +242,160 @@ void build_level_schedule(Ctx& c) {
     st.gemm = dg + r.g0; st.n_gemm = r.ng; st.max_gemm = r.mg;
     ls.steps[r.l].push_back(st);
   }
-  ls.max_fwd_smem = sizeof(double) * ((size_t)kTrsvB * kTrsvP + fp.max_front);
+  // ---- partitioned inverse: per level, copy L11 to scratch, then RLN-TRSM the panel ----
+  ls.inv_steps.assign(L, {});
+  ls.inv_prep.assign(L, nullptr);
+  ls.n_inv_prep.assign(L, 0);
+  std::vector<InvTask> prep_all;
+  std::vector<TileTask> itile_all;
+  std::vector<GemmTask> igemm_all;
+  struct IRef { int l; size_t t0, g0; int nt, ng, mt, mgm, mgn; };
+  std::vector<IRef> irefs;
+  std::vector<size_t> prep_off(L + 1, 0);
+  long long scr_max = 0;
+  std::vector<long long> scr_of(fp.nnodes, 0);
+  std::vector<int> lds_of(fp.nnodes, 0);
+  for (int l = 0; l < L; ++l) {
+    prep_off[l] = prep_all.size();
+    long long scr = 0;
+    int max_np = 0;
+    for (int i = fp.level_ptr[l]; i < fp.level_ptr[l + 1]; ++i) {
+      const int nd = fp.level_list[i];
+      const int sz = fp.sep_size[nd];
+      if (sz <= 0) continue;
+      const int lds = (int)round_up(sz, 2);
+      scr_of[nd] = scr;
+      lds_of[nd] = lds;
+      prep_all.push_back(InvTask{nd, scr, lds});
+      scr += round_up((long long)lds * sz, 2);
+      max_np = std::max(max_np, ceil_div(sz, kTile));
+    }
+    scr_max = std::max(scr_max, scr);
+    for (int t = 0; t < max_np; ++t) {
+      IRef r{l, itile_all.size(), igemm_all.size(), 0, 0, 0, 0, 0};
+      for (int i = fp.level_ptr[l]; i < fp.level_ptr[l + 1]; ++i) {
+        const int nd = fp.level_list[i];
+        const int sz = fp.sep_size[nd];
+        const int np = ceil_div(sz, kTile);
+        if (t >= np) continue;
+        const int kb = np - 1 - t, k = kb * kTile, nb = std::min(kTile, sz - k);
+        const int f = sz + fp.bnd_size[nd], ld = fp.ld[nd], lds = lds_of[nd];
+        double* F = fp.d.fronts + fp.front_off[nd];
+        TileTask tt{};
+        tt.L = (double*)(intptr_t)(scr_of[nd] + k + (long long)k * lds);  // offset, patched later
+        tt.n = nb; tt.ldl = lds; tt.B = F + (long long)k * ld; tt.ldb = ld; tt.nvec = f;
+        tt.id = nd;
+        itile_all.push_back(tt);
+        r.mt = std::max(r.mt, f);
+        if (k > 0) {
+          GemmTask g{};
+          g.A = F + (long long)k * ld; g.lda = ld;
+          g.B = (const double*)(intptr_t)(scr_of[nd] + k);  // offset, patched later
+          g.ldb = lds;
+          g.C = F; g.ldc = ld;
+          g.M = f; g.N = k; g.K = nb;
+          igemm_all.push_back(g);
+          r.mgm = std::max(r.mgm, f);
+          r.mgn = std::max(r.mgn, k);
+        }
+      }
+      r.nt = (int)(itile_all.size() - r.t0);
+      r.ng = (int)(igemm_all.size() - r.g0);
+      irefs.push_back(r);
+    }
+  }
+  prep_off[L] = prep_all.size();
+  ls.inv_scratch = c.alloc<double>(std::max<long long>(scr_max, 2));
+  for (auto& t : itile_all) t.L = ls.inv_scratch + (intptr_t)t.L;
+  for (auto& g : igemm_all) g.B = ls.inv_scratch + (intptr_t)g.B;
+  InvTask* dprep = c.upload<InvTask>(prep_all.data(), prep_all.size());
+  for (int l = 0; l < L; ++l) {
+    ls.inv_prep[l] = dprep + prep_off[l];
+    ls.n_inv_prep[l] = (int)(prep_off[l + 1] - prep_off[l]);
+  }
+  TileTask* dit = c.upload<TileTask>(itile_all.data(), itile_all.size());
+  GemmTask* dig = c.upload<GemmTask>(igemm_all.data(), igemm_all.size());
+  for (const IRef& r : irefs) {
+    LevelSchedule::Step st;
+    st.trsm = dit + r.t0; st.n_trsm = r.nt; st.max_trsm = r.mt;
+    st.gemm = dig + r.g0; st.n_gemm = r.ng; st.max_gemm = std::max(r.mgm, r.mgn);
+    st.potrf = nullptr; st.n_potrf = r.mgn;  // n_potrf reused as max N of the gemm
+    st.max_gemm = r.mgm;
+    ls.inv_steps[r.l].push_back(st);
+  }
+  // ---- solve plan: GEMV tiles + reductions per level, gather maps ----
+  ls.fwd_t.assign(L, nullptr); ls.bwd_t.assign(L, nullptr);
+  ls.fwd_r.assign(L, nullptr); ls.bwd_r.assign(L, nullptr);
+  ls.n_fwd_t.assign(L, 0); ls.n_bwd_t.assign(L, 0); ls.n_fwd_r.assign(L, 0); ls.n_bwd_r.assign(L, 0);
+  std::vector<CsTask> ft, bt;
+  std::vector<CsRed> fr, br;
+  std::vector<size_t> ft_off(L + 1), bt_off(L + 1), fr_off(L + 1), br_off(L + 1);
+  int max_parts = 0;
+  for (int l = 0; l < L; ++l) {
+    ft_off[l] = ft.size(); bt_off[l] = bt.size(); fr_off[l] = fr.size(); br_off[l] = br.size();
+    int pf = 0, pb = 0;
+    for (int i = fp.level_ptr[l]; i < fp.level_ptr[l + 1]; ++i) {
+      const int nd = fp.level_list[i];
+      const int sz = fp.sep_size[nd], f = sz + fp.bnd_size[nd];
+      for (int r0 = 0; r0 < f; r0 += 64) {
+        const int p0 = pf;
+        int cnt = 0;
+        for (int c0 = 0; c0 < sz; c0 += 256) {
+          if (r0 < sz && c0 > r0 + 63) break;  // above the lower-triangular L11^{-1}
+          ft.push_back(CsTask{nd, r0, c0, pf++});
+          ++cnt;
+        }
+        fr.push_back(CsRed{nd, r0, p0, cnt});
+      }
+      for (int c0 = 0; c0 < sz; c0 += 64) {
+        const int p0 = pb;
+        int cnt = 0;
+        for (int r0 = (c0 / 256) * 256; r0 < f; r0 += 256) {
+          bt.push_back(CsTask{nd, r0, c0, pb++});
+          ++cnt;
+        }
+        br.push_back(CsRed{nd, c0, p0, cnt});
+      }
+    }
+    max_parts = std::max(max_parts, std::max(pf, pb));
+  }
+  ft_off[L] = ft.size(); bt_off[L] = bt.size(); fr_off[L] = fr.size(); br_off[L] = br.size();
+  CsTask* dft = c.upload<CsTask>(ft.data(), ft.size());
+  CsTask* dbt = c.upload<CsTask>(bt.data(), bt.size());
+  CsRed* dfr = c.upload<CsRed>(fr.data(), fr.size());
+  CsRed* dbr = c.upload<CsRed>(br.data(), br.size());
+  for (int l = 0; l < L; ++l) {
+    ls.fwd_t[l] = dft + ft_off[l]; ls.n_fwd_t[l] = (int)(ft_off[l + 1] - ft_off[l]);
+    ls.bwd_t[l] = dbt + bt_off[l]; ls.n_bwd_t[l] = (int)(bt_off[l + 1] - bt_off[l]);
+    ls.fwd_r[l] = dfr + fr_off[l]; ls.n_fwd_r[l] = (int)(fr_off[l + 1] - fr_off[l]);
+    ls.bwd_r[l] = dbr + br_off[l]; ls.n_bwd_r[l] = (int)(br_off[l + 1] - br_off[l]);
+  }
+  ls.partial = c.alloc<double>((size_t)std::max(max_parts, 1) * 64);
+  // gather maps: front position of every node <- child update entries (child order)
+  std::vector<long long> goff(fp.nnodes);
+  std::vector<int> gptr;
+  std::vector<int> gsrc;
+  std::vector<std::vector<int>> per_pos;
+  for (int nd = 0; nd < fp.nnodes; ++nd) {
+    const int f = fp.sep_size[nd] + fp.bnd_size[nd];
+    per_pos.assign(f, {});
+    for (int q = fp.child_ptr[nd]; q < fp.child_ptr[nd + 1]; ++q) {
+      const int ch = fp.child_list[q];
+      for (int i = 0; i < fp.bnd_size[ch]; ++i)
+        per_pos[fp.rmap_host[fp.bnd_ptr[ch] + i]].push_back((int)(fp.upd_off[ch] + i));
+    }
+    goff[nd] = (long long)gptr.size();
+    int acc = (int)gsrc.size();
+    for (int pos = 0; pos < f; ++pos) {
+      gptr.push_back(acc);
+      for (int v : per_pos[pos]) gsrc.push_back(v);
+      acc = (int)gsrc.size();
+    }
+    gptr.push_back(acc);
+  }
+  ls.gat_ptr = c.upload<int>(gptr.data(), gptr.size());
+  ls.gat_off = c.upload<long long>(goff.data(), goff.size());
+  ls.gat_src = c.upload<int>(gsrc.data(), std::max<size_t>(gsrc.size(), 1));
 }
 
 void coarse_assemble_and_factor(Ctx& c) {
@@ -213,6 +441,22 @@ void coarse_assemble_and_factor(Ctx& c) {
         gemm(ga, false, true, s);
       }
     }
+    // partitioned inverse of the factored panels of this level
+    if (ls.n_inv_prep[l]) {
+      { inv_prep_kernel<<<ls.n_inv_prep[l], 256, 0, s>>>(ls.inv_prep[l], fd, ls.inv_scratch); BDDC_COUNT(); }
+      BDDC_LAUNCH_CHECK();
+    }
+    for (const auto& st : ls.inv_steps[l]) {
+      TileArgs ta;
+      ta.tasks = st.trsm; ta.count = st.n_trsm; ta.max_nvec = st.max_trsm;
+      trsm_tile(ta, TRSM_RLN, s);
+      if (st.n_gemm) {
+        GemmArgs ga;
+        ga.tasks = st.gemm; ga.count = st.n_gemm; ga.max_M = st.max_gemm; ga.max_N = st.n_potrf;
+        ga.alpha = -1.0; ga.beta = 1.0; ga.lower = 0;
+        gemm(ga, false, false, s);
+      }
+    }
   }
 }
 
@@ -220,21 +464,17 @@ void coarse_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s) {
   FrontPlan& fp = c.fp;
   FrontDev& fd = fp.d;
   LevelSchedule& ls = c.sched;
-  const size_t smem = ls.max_fwd_smem;
-  static size_t attr = 0;
-  if (smem > attr) {
-    BDDC_CUDA(cudaFuncSetAttribute(front_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    BDDC_CUDA(cudaFuncSetAttribute(front_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  LevelView lv{ls.gat_ptr, ls.gat_off, ls.gat_src};
   for (int l = 0; l < fp.nlevels; ++l) {
-    const int nn = ls.nodes_off[l + 1] - ls.nodes_off[l];
-    { front_fwd_kernel<<<nn, 256, smem, s>>>(ls.d_nodes + ls.nodes_off[l], fd, rhs, sol); BDDC_COUNT(); }
+    if (!ls.n_fwd_r[l]) continue;
+    if (ls.n_fwd_t[l]) { cs_fwd_partial_kernel<<<ls.n_fwd_t[l], 256, 0, s>>>(ls.fwd_t[l], fd, lv, rhs, ls.partial); BDDC_COUNT(); }
+    { cs_fwd_reduce_kernel<<<ls.n_fwd_r[l], 64, 0, s>>>(ls.fwd_r[l], fd, lv, ls.partial, sol); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
   }
   for (int l = fp.nlevels - 1; l >= 0; --l) {
-    const int nn = ls.nodes_off[l + 1] - ls.nodes_off[l];
-    { front_bwd_kernel<<<nn, 256, smem, s>>>(ls.d_nodes + ls.nodes_off[l], fd, sol); BDDC_COUNT(); }
+    if (!ls.n_bwd_r[l]) continue;
+    { cs_bwd_partial_kernel<<<ls.n_bwd_t[l], 256, 0, s>>>(ls.bwd_t[l], fd, sol, ls.partial); BDDC_COUNT(); }
+    { cs_bwd_reduce_kernel<<<ls.n_bwd_r[l], 64, 0, s>>>(ls.bwd_r[l], fd, ls.partial, sol); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
   }
 }

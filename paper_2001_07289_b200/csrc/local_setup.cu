@@ -19,15 +19,16 @@ namespace {
 
 template <int DIM>
 __global__ void __launch_bounds__(256) assemble_local_kernel(Geometry G, const double* __restrict__ alpha,
-                                                             LocalTables lt, int sub0, double* LI,
-                                                             double* E, double* LS,
+                                                             LocalTables lt, int sub0, double* Wd,
+                                                             double* Wo, double* E, double* LS,
                                                              double* diag_s) {
   const int sub = sub0 + blockIdx.x;
   const long long b = blockIdx.x;
   int p[3];
   sub_coords(G, sub, p);
   const long long mm = (long long)G.m_pad * G.m_pad;
-  double* li = LI + (long long)sub * G.nblk * 2 * mm;
+  double* wd = Wd + b * G.nblk * mm;
+  double* wo = Wo + b * G.nblk * mm;
   double* e = E + b * (long long)G.nI_pad * G.nG_pad;
   double* ls = LS + (long long)sub * G.nG_pad * G.nG_pad;
   constexpr int NOFF = DIM == 3 ? 27 : 9;
@@ -59,8 +60,8 @@ __global__ void __launch_bounds__(256) assemble_local_kernel(Geometry G, const d
     }
     if (ca >= 0 && cb >= 0) {
       const int ja = ca / G.m_pad, jb = cb / G.m_pad, ra = ca % G.m_pad, rb = cb % G.m_pad;
-      if (ja == jb) li[(2LL * ja) * mm + ra + (long long)rb * G.m_pad] = v;
-      else if (ja == jb + 1) li[(2LL * ja + 1) * mm + ra + (long long)rb * G.m_pad] = v;
+      if (ja == jb) wd[ja * mm + ra + (long long)rb * G.m_pad] = v;
+      else if (ja == jb + 1) wo[ja * mm + ra + (long long)rb * G.m_pad] = v;
     } else if (ca >= 0 && cb < 0) {
       e[ca + (long long)(-cb - 1) * G.nI_pad] = v;
     } else if (ca < 0 && cb < 0) {
@@ -70,7 +71,7 @@ __global__ void __launch_bounds__(256) assemble_local_kernel(Geometry G, const d
   // identity on padding
   for (int idx = threadIdx.x; idx < G.nblk * (G.m_pad - G.m); idx += blockDim.x) {
     const int j = idx / (G.m_pad - G.m), r = G.m + idx % (G.m_pad - G.m);
-    li[(2LL * j) * mm + r + (long long)r * G.m_pad] = 1.0;
+    wd[j * mm + r + (long long)r * G.m_pad] = 1.0;
   }
   for (int s = G.nG + threadIdx.x; s < G.nG_pad; s += blockDim.x) ls[s + (long long)s * G.nG_pad] = 1.0;
   // s_i = mean |diag A_i| over local free nodes
@@ -90,47 +91,68 @@ __global__ void __launch_bounds__(256) assemble_local_kernel(Geometry G, const d
 }
 
 // Block-tridiagonal Cholesky of A_II, one CTA per subdomain (blocks of m_pad <= 64):
-//   Lo_j <- Lo_j Ld_{j-1}^{-T};  Ld_j <- chol(T_j - Lo_j Lo_j^T)
-__global__ void __launch_bounds__(128) btchol_kernel(Geometry G, int sub0, double* LI, int* info) {
+//   Lo_j = B_j Linv_{j-1}^T ;  Ld_j = chol(T_j - Lo_j Lo_j^T) ;  Linv_j = Ld_j^{-1}
+// In: T_j in Wd[j], B_j in Wo[j] (dense m_pad^2, setup workspace).
+// Out: Linv_j dense in Wd[j], Lo_j dense in Wo[j] (workspace, for E = L^{-1} A_IG),
+//      Linv_j packed + the coupling stencil Bc_j in LI (persistent, for the apply).
+__global__ void __launch_bounds__(128) btchol_kernel(Geometry G, int sub0, double* Wd, double* Wo,
+                                                     double* LI, int* info) {
   extern __shared__ double sm[];
   const int M = G.m_pad, P = M + 1;  // odd pitch
-  double* prev = sm;
-  double* cur = sm + M * P;
+  double* prev = sm;          // Linv_{j-1}
+  double* cur = sm + M * P;   // S_j -> Ld_j
   double* off = sm + 2 * M * P;
-  const int sub = sub0 + blockIdx.x;
+  double* inv = sm + 3 * M * P;
+  const int b = blockIdx.x, sub = sub0 + b;
   const long long mm = (long long)M * M;
-  double* li = LI + (long long)sub * G.nblk * 2 * mm;
+  double* wd = Wd + (long long)b * G.nblk * mm;
+  double* wo = Wo + (long long)b * G.nblk * mm;
+  double* li = LI + (long long)sub * G.li_stride;
+  double* bc = li + (long long)G.nblk * G.Tm;
   const int tid = threadIdx.x, nt = blockDim.x;
+  const int px = G.blk[0] - 1;  // in-plane row length
+  const int py = G.dim == 3 ? G.blk[1] - 1 : 1;
   __shared__ int failed;
   if (tid == 0) failed = -1;
   for (int j = 0; j < G.nblk; ++j) {
-    const double* dsrc = li + 2LL * j * mm;
-    for (int idx = tid; idx < M * M; idx += nt) cur[idx % M + (idx / M) * P] = dsrc[idx];
-    if (j > 0) {
-      const double* osrc = li + (2LL * j + 1) * mm;
-      for (int idx = tid; idx < M * M; idx += nt) off[idx % M + (idx / M) * P] = osrc[idx];
-    }
+    for (int idx = tid; idx < M * M; idx += nt) cur[idx % M + (idx / M) * P] = wd[j * mm + idx];
+    if (j > 0)
+      for (int idx = tid; idx < M * M; idx += nt) off[idx % M + (idx / M) * P] = wo[j * mm + idx];
     __syncthreads();
     if (j > 0) {
-      // off <- off * prev^{-T}: row r of off solves x prev^T = b (forward)
-      for (int r = tid; r < M; r += nt) {
-        for (int c = 0; c < M; ++c) {
-          double s = off[r + c * P];
-          for (int k = 0; k < c; ++k) s -= off[r + k * P] * prev[c + k * P];
-          off[r + c * P] = s / prev[c + c * P];
+      // coupling stencil of B_j (rows: plane j, cols: plane j-1) before it is overwritten
+      for (int idx = tid; idx < M * G.nbo; idx += nt) {
+        const int r = idx / G.nbo, k = idx % G.nbo;
+        double v = 0.0;
+        if (r < G.m) {
+          const int x = r % px + G.bo_dx[k], y = r / px + G.bo_dy[k];
+          if (x >= 0 && x < px && y >= 0 && y < py) v = off[r + (x + y * px) * P];
         }
+        bc[((long long)j * M + r) * G.nbo + k] = v;
       }
+      // off <- B_j Linv_{j-1}^T  (row r: sum_k B[r][k] Linv[c][k], k <= c)
+      for (int idx = tid; idx < M * M; idx += nt) {
+        const int r = idx % M, c = idx / M;
+        double acc = 0.0;
+        for (int k = 0; k <= c; ++k) acc += off[r + k * P] * prev[c + k * P];
+        inv[r + c * P] = acc;
+      }
+      __syncthreads();
+      for (int idx = tid; idx < M * M; idx += nt) off[idx % M + (idx / M) * P] = inv[idx % M + (idx / M) * P];
       __syncthreads();
       // cur -= off off^T (lower)
       for (int idx = tid; idx < M * M; idx += nt) {
         const int r = idx % M, c = idx / M;
         if (r < c) continue;
-        double s = 0.0;
-        for (int k = 0; k < M; ++k) s += off[r + k * P] * off[c + k * P];
-        cur[r + c * P] -= s;
+        double acc = 0.0;
+        for (int k = 0; k < M; ++k) acc += off[r + k * P] * off[c + k * P];
+        cur[r + c * P] -= acc;
       }
       __syncthreads();
+    } else {
+      for (int idx = tid; idx < M * G.nbo; idx += nt) bc[idx] = 0.0;
     }
+    // Cholesky of cur (lower), right-looking in shared memory
     for (int c = 0; c < M; ++c) {
       if (tid == 0) {
         double d = cur[c + c * P];
@@ -141,8 +163,8 @@ __global__ void __launch_bounds__(128) btchol_kernel(Geometry G, int sub0, doubl
         cur[c + c * P] = sqrt(d);
       }
       __syncthreads();
-      const double inv = 1.0 / cur[c + c * P];
-      for (int r = c + 1 + tid; r < M; r += nt) cur[r + c * P] *= inv;
+      const double iv = 1.0 / cur[c + c * P];
+      for (int r = c + 1 + tid; r < M; r += nt) cur[r + c * P] *= iv;
       __syncthreads();
       const int rr = M - c - 1;
       for (int idx = tid; idx < rr * rr; idx += nt) {
@@ -151,19 +173,31 @@ __global__ void __launch_bounds__(128) btchol_kernel(Geometry G, int sub0, doubl
       }
       __syncthreads();
     }
-    double* ddst = li + 2LL * j * mm;
+    // inv = cur^{-1}: thread per column c, forward substitution down the column
+    for (int c = tid; c < M; c += nt) {
+      for (int i = 0; i < c; ++i) inv[i + c * P] = 0.0;
+      for (int i = c; i < M; ++i) {
+        double acc = i == c ? 1.0 : 0.0;
+        for (int k = c; k < i; ++k) acc -= cur[i + k * P] * inv[k + c * P];
+        inv[i + c * P] = acc / cur[i + i * P];
+      }
+    }
+    __syncthreads();
+    // outputs
+    double* pk = li + (long long)j * G.Tm;
+    for (int c = 0; c < M; ++c) {
+      const long long cs = (long long)c * M - (long long)c * (c - 1) / 2;  // packed column start
+      for (int r = c + tid; r < M; r += nt) pk[cs + (r - c)] = inv[r + c * P];
+    }
     for (int idx = tid; idx < M * M; idx += nt) {
       const int r = idx % M, c = idx / M;
-      ddst[idx] = r >= c ? cur[r + c * P] : 0.0;
-    }
-    if (j > 0) {
-      double* odst = li + (2LL * j + 1) * mm;
-      for (int idx = tid; idx < M * M; idx += nt) odst[idx] = off[idx % M + (idx / M) * P];
+      wd[j * mm + idx] = inv[r + c * P];
+      if (j > 0) wo[j * mm + idx] = off[r + c * P];
     }
     __syncthreads();
     double* t = prev;
-    prev = cur;
-    cur = t;
+    prev = inv;
+    inv = t;
   }
   if (tid == 0 && failed >= 0) atomicMin(info + sub, failed);
 }
@@ -226,7 +260,7 @@ __global__ void finish_local_kernel(Geometry G, int sub0, int spec, const double
 }  // namespace
 
 size_t local_setup_workspace(const Geometry& g, int chunk) {
-  const size_t E = (size_t)g.nI_pad * g.nG_pad;
+  const size_t E = 2 * (size_t)g.nI_pad * g.nG_pad + 2 * (size_t)g.nblk * g.m_pad * g.m_pad;
   const size_t SG = (size_t)g.nG_pad * g.nG_pad;
   const size_t X = (size_t)g.nG_pad * g.nc_pad;
   const size_t SC = (size_t)g.nc_pad * g.nc_pad;
@@ -240,59 +274,62 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
   int chunk = (int)std::min<size_t>(G.nsub, ws_doubles / per);
   if (chunk <= 0) throw CudaError("local setup workspace too small");
   const long long mm = (long long)G.m_pad * G.m_pad;
-  const long long liS = (long long)G.nblk * 2 * mm;
+  const long long wS = (long long)G.nblk * mm;
   const long long lsS = (long long)G.nG_pad * G.nG_pad;
   const long long phS = (long long)G.nG_pad * G.nc_pad;
   const long long scS = (long long)G.nc_pad * G.nc_pad;
   const long long eS = (long long)G.nI_pad * G.nG_pad;
-  const int btchol_smem = 3 * G.m_pad * (G.m_pad + 1) * (int)sizeof(double);
+  const int btchol_smem = 4 * G.m_pad * (G.m_pad + 1) * (int)sizeof(double);
   BDDC_CUDA(cudaFuncSetAttribute(btchol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, btchol_smem));
 
   for (int sub0 = 0; sub0 < G.nsub; sub0 += chunk) {
     const int cnt = std::min(chunk, G.nsub - sub0);
-    double* E = ws;
-    double* SG = E + (size_t)chunk * eS;
+    double* E = ws;                             // A_IG, then E - Lo E (in place)
+    double* E2 = E + (size_t)chunk * eS;        // E = L_I^{-1} A_IG
+    double* Wd = E2 + (size_t)chunk * eS;       // T_j -> Linv_j (dense)
+    double* Wo = Wd + (size_t)chunk * wS;       // B_j -> Lo_j (dense)
+    double* SG = Wo + (size_t)chunk * wS;
     double* X = SG + (size_t)chunk * lsS;
     double* SC = X + (size_t)chunk * phS;
     double* P = SC + (size_t)chunk * scS;
-    double* LI = c.LI;  // indexed by global sub inside kernels
     double* LS = c.LS + sub0 * lsS;
     double* PH = c.Phi + sub0 * phS;
-    BDDC_CUDA(cudaMemsetAsync(c.LI + sub0 * liS, 0, sizeof(double) * cnt * liS, s));
+    BDDC_CUDA(cudaMemsetAsync(Wd, 0, sizeof(double) * 2 * (size_t)chunk * wS, s));
     BDDC_CUDA(cudaMemsetAsync(E, 0, sizeof(double) * cnt * eS, s));
     BDDC_CUDA(cudaMemsetAsync(LS, 0, sizeof(double) * cnt * lsS, s));
     BDDC_CUDA(cudaMemsetAsync(PH, 0, sizeof(double) * cnt * phS, s));
     // 1. assembly
     c.prof.begin("setup.assemble", s);
     if (G.dim == 2)
-      { assemble_local_kernel<2><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, LI, E, c.LS, c.diag_s); BDDC_COUNT(); }
+      { assemble_local_kernel<2><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, Wd, Wo, E, c.LS, c.diag_s); BDDC_COUNT(); }
     else
-      { assemble_local_kernel<3><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, LI, E, c.LS, c.diag_s); BDDC_COUNT(); }
+      { assemble_local_kernel<3><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, Wd, Wo, E, c.LS, c.diag_s); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
     c.prof.end("setup.assemble", s);
-    // 2. interior block-tridiagonal Cholesky
+    // 2. interior block-tridiagonal Cholesky (+ inverses of the diagonal blocks)
     c.prof.begin("setup.btchol", s);
-    { btchol_kernel<<<cnt, 128, btchol_smem, s>>>(G, sub0, LI, c.info); BDDC_COUNT(); }
-    BDDC_LAUNCH_CHECK();
+    if (G.nblk > 0) {
+      { btchol_kernel<<<cnt, 128, btchol_smem, s>>>(G, sub0, Wd, Wo, c.LI, c.info); BDDC_COUNT(); }
+      BDDC_LAUNCH_CHECK();
+    }
     c.prof.end("setup.btchol", s);
-    // 3. E <- L_I^{-1} E, block forward substitution over planes
+    // 3. E = L_I^{-1} A_IG:  E2_j = Linv_j (E_j - Lo_j E2_{j-1})
     c.prof.begin("setup.E", s);
     for (int j = 0; j < G.nblk; ++j) {
       BMat Ej{E + (long long)j * G.m_pad, eS, G.nI_pad};
+      BMat E2j{E2 + (long long)j * G.m_pad, eS, G.nI_pad};
       if (j > 0) {
-        BMat Lo{c.LI + sub0 * liS + (2LL * j + 1) * mm, liS, G.m_pad};
-        BMat Ejm{E + (long long)(j - 1) * G.m_pad, eS, G.nI_pad};
-        gemm_batched(false, false, G.m_pad, G.nG_pad, G.m_pad, -1.0, Lo, Ejm, 1.0, Ej, cnt, s);
+        BMat Lo{Wo + j * mm, wS, G.m_pad};
+        BMat E2p{E2 + (long long)(j - 1) * G.m_pad, eS, G.nI_pad};
+        gemm_batched(false, false, G.m_pad, G.nG_pad, G.m_pad, -1.0, Lo, E2p, 1.0, Ej, cnt, s);
       }
-      TileArgs t;
-      t.L = c.LI + sub0 * liS + 2LL * j * mm; t.sL = liS; t.ldl = G.m_pad; t.n = G.m_pad;
-      t.B = Ej.p; t.sB = eS; t.ldb = G.nI_pad; t.nvec = G.nG_pad; t.count = cnt;
-      trsm_tile(t, TRSM_LLN, s);
+      BMat Li{Wd + j * mm, wS, G.m_pad};
+      gemm_batched(false, false, G.m_pad, G.nG_pad, G.m_pad, 1.0, Li, Ej, 0.0, E2j, cnt, s);
     }
     c.prof.end("setup.E", s);
     // S_Gamma = A_GG - E^T E  (in LS)
     c.prof.begin("setup.SG", s);
-    BMat Eb{E, eS, G.nI_pad};
+    BMat Eb{E2, eS, G.nI_pad};
     BMat LSb{LS, lsS, G.nG_pad};
     gemm_batched(true, false, G.nG_pad, G.nG_pad, G.nI_pad, -1.0, Eb, Eb, 1.0, LSb, cnt, s);
     BDDC_CUDA(cudaMemcpyAsync(SG, LS, sizeof(double) * cnt * lsS, cudaMemcpyDeviceToDevice, s));
