@@ -125,18 +125,21 @@ struct LevelView {  // POD view of the gather maps for kernels
 
 struct LevelSchedule {
   struct Step {
-    TileTask* potrf = nullptr;
+    TileTask* potrf = nullptr;  // factorization only
     int n_potrf = 0;
-    TileTask* trsm = nullptr;
-    int n_trsm = 0, max_trsm = 0;
-    GemmTask* gemm = nullptr;
-    int n_gemm = 0, max_gemm = 0;
+    TileTask* trtri = nullptr;  // diagonal-tile inverses (into tile_scratch)
+    int n_trtri = 0;
+    GemmTask* tsolve = nullptr; // in-place tile solves with the inverses
+    int n_tsolve = 0, ts_M = 0, ts_N = 0;
+    GemmTask* gemm = nullptr;   // trailing / panel updates
+    int n_gemm = 0, g_M = 0, g_N = 0;
   };
   std::vector<std::vector<Step>> steps;      // [level][step] factorization
   std::vector<std::vector<Step>> inv_steps;  // [level][step] panel <- panel L11^{-1} (RLN)
   std::vector<InvTask*> inv_prep;            // [level]
   std::vector<int> n_inv_prep;
   double* inv_scratch = nullptr;
+  double* tile_scratch = nullptr;
   // solve: per level fwd / bwd GEMV tiles and reductions
   std::vector<CsTask*> fwd_t, bwd_t;
   std::vector<CsRed*> fwd_r, bwd_r;
@@ -229,6 +232,8 @@ struct Ctx {
   double* Sloc = nullptr;    // [nsub x nc_pad^2] local coarse blocks (kept for assembly)
   int* info = nullptr;       // [nsub] interior (A_II) pivot failure per subdomain
   int* info_k = nullptr;     // [nsub] S_K pivot failure (underconstrained) per subdomain
+  double* tinv = nullptr;    // diagonal-tile inverse scratch for batched TRSM / POTRF
+  size_t tinv_doubles = 0;
   FrontPlan fp;
   LevelSchedule sched;
   // apply workspaces (device)

@@ -313,6 +313,9 @@ void do_setup(bddc_ctx* h, const bddc_setup_desc* d) {
   size_t use = std::min(want, std::max(cap - cap % per, per));
   h->ws = c.alloc<double>(use);
   h->ws_doubles = use;
+  const int chunk = (int)std::min<size_t>(G.nsub, use / per);
+  c.tinv_doubles = std::max(trsm_scratch_doubles(G.nG_pad, chunk), trsm_scratch_doubles(G.nc_pad, chunk));
+  c.tinv = c.alloc<double>(c.tinv_doubles);
   numeric_setup(h);
 }
 
@@ -560,7 +563,10 @@ int bddc_dense_potrf(double* A, int n, int lda, long long stride, int count, int
     int* info = nullptr;
     BDDC_CUDA(cudaMallocAsync((void**)&info, sizeof(int) * count, s));
     BDDC_CUDA(cudaMemsetAsync(info, 0x7f, sizeof(int) * count, s));
-    potrf_batched(BMat{A, stride, lda}, n, n, count, info, s);
+    double* scr = nullptr;
+    BDDC_CUDA(cudaMallocAsync((void**)&scr, sizeof(double) * kTileInvStride * count, s));
+    potrf_batched(BMat{A, stride, lda}, n, n, count, info, scr, s);
+    BDDC_CUDA(cudaFreeAsync(scr, s));
     if (info_host) {
       BDDC_CUDA(cudaMemcpyAsync(info_host, info, sizeof(int) * count, cudaMemcpyDeviceToHost, s));
       BDDC_CUDA(cudaStreamSynchronize(s));
@@ -575,8 +581,12 @@ int bddc_dense_trsm(int kind, const double* L, int n, int ldl, long long sL, dou
                     int ldb, long long sB, int count, void* stream) {
   if (!L || !B || kind < 0 || kind > 3 || (ldl & 1) || (ldb & 1)) return 1;
   return guarded(nullptr, 0, [&] {
+    cudaStream_t s = (cudaStream_t)stream;
+    double* scr = nullptr;
+    BDDC_CUDA(cudaMallocAsync((void**)&scr, sizeof(double) * trsm_scratch_doubles(n, count), s));
     trsm_batched((TrsmKind)kind, BMat{(double*)L, sL, ldl}, n, BMat{B, sB, ldb}, nother, count,
-                 (cudaStream_t)stream);
+                 scr, s);
+    BDDC_CUDA(cudaFreeAsync(scr, s));
   });
 }
 

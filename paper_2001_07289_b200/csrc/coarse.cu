@@ -56,18 +56,17 @@ __global__ void extend_add_kernel(const int* __restrict__ nodes, int k, const in
 
 // ---- partitioned-inverse preparation: copy L11 to scratch, replace it by the identity ----
 __global__ void inv_prep_kernel(const InvTask* __restrict__ tasks, FrontDev fd, double* scratch) {
-  const InvTask t = tasks[blockIdx.x];
+  const InvTask t = tasks[blockIdx.y];
   const int s = fd.sep_size[t.node], ld = fd.ld[t.node];
   double* F = fd.fronts + fd.front_off[t.node];
   double* S = scratch + t.scr;
-  for (long long idx = threadIdx.x; idx < (long long)s * s; idx += blockDim.x) {
+  const long long total = (long long)s * s;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(idx % s), j = (int)(idx / s);
-    S[i + (long long)j * t.lds] = i >= j ? F[i + (long long)j * ld] : 0.0;
-  }
-  __syncthreads();
-  for (long long idx = threadIdx.x; idx < (long long)s * s; idx += blockDim.x) {
-    const int i = (int)(idx % s), j = (int)(idx / s);
-    F[i + (long long)j * ld] = i == j ? 1.0 : 0.0;
+    double* fp = F + i + (long long)j * ld;
+    S[i + (long long)j * t.lds] = i >= j ? *fp : 0.0;  // each element copied, then reset,
+    *fp = i == j ? 1.0 : 0.0;                          // by the same thread
   }
 }
 
@@ -193,16 +192,36 @@ void build_level_schedule(Ctx& c) {
   ls.d_nodes = c.upload<int>(flat.data(), flat.size());
   for (int n = 0; n < fp.nnodes; ++n)
     ls.max_children = std::max(ls.max_children, fp.child_ptr[n + 1] - fp.child_ptr[n]);
-  std::vector<TileTask> potrf_all, trsm_all;
-  std::vector<GemmTask> gemm_all;
-  struct Ref { int l, k; size_t p0, t0, g0; int np, nt, ng, mt, mg; };
+  // ---- factorization + partitioned inverse, per level and 64-column step ----
+  // factor step k:  potrf(diag) ; trtri(diag -> scratch slot) ; L21 <- L21 inv^T ; A22 -= L21 L21^T
+  // inverse step t (panel P = [I; L21] after inv_prep, L11 copy in inv_scratch), kb from last:
+  //                 trtri(L11[kb,kb]) ; P[:,kb] <- P[:,kb] inv ; P[:,0:k] -= P[:,kb] L11[kb,0:k]
+  std::vector<TileTask> potrf_all, trtri_all;
+  std::vector<GemmTask> ts_all, g_all;
+  struct Ref {
+    int l; bool inv;
+    size_t p0, r0, t0, g0;
+    int np, nr, nt, ng, tsM, tsN, gM, gN;
+  };
   std::vector<Ref> refs;
+  std::vector<InvTask> prep_all;
+  std::vector<size_t> prep_off(L + 1, 0);
+  long long scr_max = 0;
+  std::vector<long long> scr_of(fp.nnodes, 0);
+  std::vector<int> lds_of(fp.nnodes, 0);
+  size_t max_slots = 1;
+  const long long IS = kTileInvStride;
+  std::vector<std::pair<size_t, long long>> slot_fix_trtri;  // (task idx, slot) patched later
+  std::vector<std::pair<size_t, long long>> slot_fix_ts;     // GemmTask B = slot
+  std::vector<std::pair<size_t, long long>> scr_fix_trtri;   // TileTask L = inv_scratch offset
+  std::vector<std::pair<size_t, long long>> scr_fix_g;       // GemmTask B = inv_scratch offset
   for (int l = 0; l < L; ++l) {
     int max_s = 0;
     for (int i = fp.level_ptr[l]; i < fp.level_ptr[l + 1]; ++i)
       max_s = std::max(max_s, fp.sep_size[fp.level_list[i]]);
     for (int k = 0; k < max_s; k += kTile) {
-      Ref r{l, k, potrf_all.size(), trsm_all.size(), gemm_all.size(), 0, 0, 0, 0, 0};
+      Ref r{l, false, potrf_all.size(), trtri_all.size(), ts_all.size(), g_all.size(), 0, 0, 0, 0, 0, 0, 0, 0};
+      size_t slot = 0;
       for (int i = fp.level_ptr[l]; i < fp.level_ptr[l + 1]; ++i) {
         const int nd = fp.level_list[i];
         const int s = fp.sep_size[nd], f = s + fp.bnd_size[nd], ld = fp.ld[nd];
@@ -213,49 +232,32 @@ void build_level_schedule(Ctx& c) {
         t.L = F + k + (long long)k * ld; t.n = nb; t.ldl = ld; t.id = nd; t.offset = fp.sep_start[nd] + k;
         potrf_all.push_back(t);
         if (rest > 0) {
-          TileTask tt = t;
-          tt.B = F + (k + nb) + (long long)k * ld; tt.ldb = ld; tt.nvec = rest;
-          trsm_all.push_back(tt);
-          r.mt = std::max(r.mt, rest);
+          slot_fix_trtri.push_back({trtri_all.size(), (long long)slot});
+          trtri_all.push_back(t);
+          GemmTask ts{};
+          ts.A = F + (k + nb) + (long long)k * ld; ts.lda = ld;
+          ts.ldb = kTile;
+          ts.C = F + (k + nb) + (long long)k * ld; ts.ldc = ld;
+          ts.M = rest; ts.N = nb; ts.K = nb;
+          slot_fix_ts.push_back({ts_all.size(), (long long)slot});
+          ts_all.push_back(ts);
+          r.tsM = std::max(r.tsM, rest); r.tsN = std::max(r.tsN, nb);
+          ++slot;
           GemmTask g{};
           g.A = F + (k + nb) + (long long)k * ld; g.lda = ld;
           g.B = g.A; g.ldb = ld;
           g.C = F + (k + nb) + (long long)(k + nb) * ld; g.ldc = ld;
           g.M = rest; g.N = rest; g.K = nb;
-          gemm_all.push_back(g);
-          r.mg = std::max(r.mg, rest);
+          g_all.push_back(g);
+          r.gM = std::max(r.gM, rest); r.gN = std::max(r.gN, rest);
         }
       }
-      r.np = (int)(potrf_all.size() - r.p0);
-      r.nt = (int)(trsm_all.size() - r.t0);
-      r.ng = (int)(gemm_all.size() - r.g0);
+      max_slots = std::max(max_slots, slot);
+      r.np = (int)(potrf_all.size() - r.p0); r.nr = (int)(trtri_all.size() - r.r0);
+      r.nt = (int)(ts_all.size() - r.t0); r.ng = (int)(g_all.size() - r.g0);
       refs.push_back(r);
     }
-  }
-  TileTask* dp = c.upload<TileTask>(potrf_all.data(), potrf_all.size());
-  TileTask* dt = c.upload<TileTask>(trsm_all.data(), trsm_all.size());
-  GemmTask* dg = c.upload<GemmTask>(gemm_all.data(), gemm_all.size());
-  for (const Ref& r : refs) {
-    LevelSchedule::Step st;
-    st.potrf = dp + r.p0; st.n_potrf = r.np;
-    st.trsm = dt + r.t0; st.n_trsm = r.nt; st.max_trsm = r.mt;
-    st.gemm = dg + r.g0; st.n_gemm = r.ng; st.max_gemm = r.mg;
-    ls.steps[r.l].push_back(st);
-  }
-  // ---- partitioned inverse: per level, copy L11 to scratch, then RLN-TRSM the panel ----
-  ls.inv_steps.assign(L, {});
-  ls.inv_prep.assign(L, nullptr);
-  ls.n_inv_prep.assign(L, 0);
-  std::vector<InvTask> prep_all;
-  std::vector<TileTask> itile_all;
-  std::vector<GemmTask> igemm_all;
-  struct IRef { int l; size_t t0, g0; int nt, ng, mt, mgm, mgn; };
-  std::vector<IRef> irefs;
-  std::vector<size_t> prep_off(L + 1, 0);
-  long long scr_max = 0;
-  std::vector<long long> scr_of(fp.nnodes, 0);
-  std::vector<int> lds_of(fp.nnodes, 0);
-  for (int l = 0; l < L; ++l) {
+    // partitioned inverse of this level
     prep_off[l] = prep_all.size();
     long long scr = 0;
     int max_np = 0;
@@ -272,7 +274,8 @@ void build_level_schedule(Ctx& c) {
     }
     scr_max = std::max(scr_max, scr);
     for (int t = 0; t < max_np; ++t) {
-      IRef r{l, itile_all.size(), igemm_all.size(), 0, 0, 0, 0, 0};
+      Ref r{l, true, potrf_all.size(), trtri_all.size(), ts_all.size(), g_all.size(), 0, 0, 0, 0, 0, 0, 0, 0};
+      size_t slot = 0;
       for (int i = fp.level_ptr[l]; i < fp.level_ptr[l + 1]; ++i) {
         const int nd = fp.level_list[i];
         const int sz = fp.sep_size[nd];
@@ -282,46 +285,62 @@ void build_level_schedule(Ctx& c) {
         const int f = sz + fp.bnd_size[nd], ld = fp.ld[nd], lds = lds_of[nd];
         double* F = fp.d.fronts + fp.front_off[nd];
         TileTask tt{};
-        tt.L = (double*)(intptr_t)(scr_of[nd] + k + (long long)k * lds);  // offset, patched later
-        tt.n = nb; tt.ldl = lds; tt.B = F + (long long)k * ld; tt.ldb = ld; tt.nvec = f;
-        tt.id = nd;
-        itile_all.push_back(tt);
-        r.mt = std::max(r.mt, f);
+        tt.n = nb; tt.ldl = lds; tt.id = nd;
+        scr_fix_trtri.push_back({trtri_all.size(), scr_of[nd] + k + (long long)k * lds});
+        slot_fix_trtri.push_back({trtri_all.size(), (long long)slot});
+        trtri_all.push_back(tt);
+        GemmTask ts{};
+        ts.A = F + (long long)k * ld; ts.lda = ld;
+        ts.ldb = kTile;
+        ts.C = F + (long long)k * ld; ts.ldc = ld;
+        ts.M = f; ts.N = nb; ts.K = nb;
+        slot_fix_ts.push_back({ts_all.size(), (long long)slot});
+        ts_all.push_back(ts);
+        r.tsM = std::max(r.tsM, f); r.tsN = std::max(r.tsN, nb);
+        ++slot;
         if (k > 0) {
           GemmTask g{};
           g.A = F + (long long)k * ld; g.lda = ld;
-          g.B = (const double*)(intptr_t)(scr_of[nd] + k);  // offset, patched later
           g.ldb = lds;
           g.C = F; g.ldc = ld;
           g.M = f; g.N = k; g.K = nb;
-          igemm_all.push_back(g);
-          r.mgm = std::max(r.mgm, f);
-          r.mgn = std::max(r.mgn, k);
+          scr_fix_g.push_back({g_all.size(), scr_of[nd] + k});
+          g_all.push_back(g);
+          r.gM = std::max(r.gM, f); r.gN = std::max(r.gN, k);
         }
       }
-      r.nt = (int)(itile_all.size() - r.t0);
-      r.ng = (int)(igemm_all.size() - r.g0);
-      irefs.push_back(r);
+      max_slots = std::max(max_slots, slot);
+      r.np = 0; r.nr = (int)(trtri_all.size() - r.r0);
+      r.nt = (int)(ts_all.size() - r.t0); r.ng = (int)(g_all.size() - r.g0);
+      refs.push_back(r);
     }
   }
   prep_off[L] = prep_all.size();
   ls.inv_scratch = c.alloc<double>(std::max<long long>(scr_max, 2));
-  for (auto& t : itile_all) t.L = ls.inv_scratch + (intptr_t)t.L;
-  for (auto& g : igemm_all) g.B = ls.inv_scratch + (intptr_t)g.B;
+  ls.tile_scratch = c.alloc<double>(max_slots * IS);
+  for (auto& pr : slot_fix_trtri) trtri_all[pr.first].inv = ls.tile_scratch + pr.second * IS;
+  for (auto& pr : slot_fix_ts) ts_all[pr.first].B = ls.tile_scratch + pr.second * IS;
+  for (auto& pr : scr_fix_trtri) trtri_all[pr.first].L = ls.inv_scratch + pr.second;
+  for (auto& pr : scr_fix_g) g_all[pr.first].B = ls.inv_scratch + pr.second;
+  TileTask* dp = c.upload<TileTask>(potrf_all.data(), potrf_all.size());
+  TileTask* dr = c.upload<TileTask>(trtri_all.data(), trtri_all.size());
+  GemmTask* dt = c.upload<GemmTask>(ts_all.data(), ts_all.size());
+  GemmTask* dg = c.upload<GemmTask>(g_all.data(), g_all.size());
+  ls.inv_steps.assign(L, {});
+  ls.inv_prep.assign(L, nullptr);
+  ls.n_inv_prep.assign(L, 0);
+  for (const Ref& r : refs) {
+    LevelSchedule::Step st;
+    st.potrf = dp + r.p0; st.n_potrf = r.np;
+    st.trtri = dr + r.r0; st.n_trtri = r.nr;
+    st.tsolve = dt + r.t0; st.n_tsolve = r.nt; st.ts_M = r.tsM; st.ts_N = r.tsN;
+    st.gemm = dg + r.g0; st.n_gemm = r.ng; st.g_M = r.gM; st.g_N = r.gN;
+    (r.inv ? ls.inv_steps : ls.steps)[r.l].push_back(st);
+  }
   InvTask* dprep = c.upload<InvTask>(prep_all.data(), prep_all.size());
   for (int l = 0; l < L; ++l) {
     ls.inv_prep[l] = dprep + prep_off[l];
     ls.n_inv_prep[l] = (int)(prep_off[l + 1] - prep_off[l]);
-  }
-  TileTask* dit = c.upload<TileTask>(itile_all.data(), itile_all.size());
-  GemmTask* dig = c.upload<GemmTask>(igemm_all.data(), igemm_all.size());
-  for (const IRef& r : irefs) {
-    LevelSchedule::Step st;
-    st.trsm = dit + r.t0; st.n_trsm = r.nt; st.max_trsm = r.mt;
-    st.gemm = dig + r.g0; st.n_gemm = r.ng; st.max_gemm = std::max(r.mgm, r.mgn);
-    st.potrf = nullptr; st.n_potrf = r.mgn;  // n_potrf reused as max N of the gemm
-    st.max_gemm = r.mgm;
-    ls.inv_steps[r.l].push_back(st);
   }
   // ---- solve plan: GEMV tiles + reductions per level, gather maps ----
   ls.fwd_t.assign(L, nullptr); ls.bwd_t.assign(L, nullptr);
@@ -425,38 +444,38 @@ void coarse_assemble_and_factor(Ctx& c) {
         BDDC_LAUNCH_CHECK();
       }
     }
-    for (const auto& st : ls.steps[l]) {
-      TileArgs pa;
-      pa.tasks = st.potrf; pa.count = st.n_potrf; pa.info = fp.info;
-      potrf_tile(pa, s);
-      if (st.n_trsm) {
+    auto run_step = [&](const LevelSchedule::Step& st, bool lower_gemm, bool trans_ts) {
+      if (st.n_potrf) {
+        TileArgs pa;
+        pa.tasks = st.potrf; pa.count = st.n_potrf; pa.info = fp.info;
+        potrf_tile(pa, s);
+      }
+      if (st.n_trtri) {
         TileArgs ta;
-        ta.tasks = st.trsm; ta.count = st.n_trsm; ta.max_nvec = st.max_trsm;
-        trsm_tile(ta, TRSM_RLT, s);
+        ta.tasks = st.trtri; ta.count = st.n_trtri;
+        trtri_tile(ta, s);
+      }
+      if (st.n_tsolve) {
+        GemmArgs ga;
+        ga.tasks = st.tsolve; ga.count = st.n_tsolve; ga.max_M = st.ts_M; ga.max_N = st.ts_N;
+        ga.alpha = 1.0; ga.beta = 0.0;
+        gemm(ga, false, trans_ts, s);
       }
       if (st.n_gemm) {
         GemmArgs ga;
-        ga.tasks = st.gemm; ga.count = st.n_gemm; ga.max_M = st.max_gemm; ga.max_N = st.max_gemm;
-        ga.alpha = -1.0; ga.beta = 1.0; ga.lower = 1;
-        gemm(ga, false, true, s);
+        ga.tasks = st.gemm; ga.count = st.n_gemm; ga.max_M = st.g_M; ga.max_N = st.g_N;
+        ga.alpha = -1.0; ga.beta = 1.0; ga.lower = lower_gemm ? 1 : 0;
+        gemm(ga, false, lower_gemm, s);
       }
-    }
+    };
+    for (const auto& st : ls.steps[l]) run_step(st, true, true);
     // partitioned inverse of the factored panels of this level
     if (ls.n_inv_prep[l]) {
-      { inv_prep_kernel<<<ls.n_inv_prep[l], 256, 0, s>>>(ls.inv_prep[l], fd, ls.inv_scratch); BDDC_COUNT(); }
+      dim3 grid(32, ls.n_inv_prep[l]);
+      { inv_prep_kernel<<<grid, 256, 0, s>>>(ls.inv_prep[l], fd, ls.inv_scratch); BDDC_COUNT(); }
       BDDC_LAUNCH_CHECK();
     }
-    for (const auto& st : ls.inv_steps[l]) {
-      TileArgs ta;
-      ta.tasks = st.trsm; ta.count = st.n_trsm; ta.max_nvec = st.max_trsm;
-      trsm_tile(ta, TRSM_RLN, s);
-      if (st.n_gemm) {
-        GemmArgs ga;
-        ga.tasks = st.gemm; ga.count = st.n_gemm; ga.max_M = st.max_gemm; ga.max_N = st.n_potrf;
-        ga.alpha = -1.0; ga.beta = 1.0; ga.lower = 0;
-        gemm(ga, false, false, s);
-      }
-    }
+    for (const auto& st : ls.inv_steps[l]) run_step(st, false, false);
   }
 }
 

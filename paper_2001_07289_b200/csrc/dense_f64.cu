@@ -187,15 +187,44 @@ struct TileView {
   double* L;
   double* B;
   int n, ldl, ldb, nvec, id, offset;
+  double* inv;
 };
 
 __device__ __forceinline__ TileView tile_task(const TileArgs& a, int b) {
   if (a.tasks) {
     const TileTask& t = a.tasks[b];
-    return TileView{t.L, t.B, t.n, t.ldl, t.ldb, t.nvec, t.id, t.offset};
+    return TileView{t.L, t.B, t.n, t.ldl, t.ldb, t.nvec, t.id, t.offset, t.inv};
   }
   return TileView{a.L + b * a.sL, a.B ? a.B + b * a.sB : nullptr, a.n, a.ldl, a.ldb, a.nvec, b,
-                  a.offset};
+                  a.offset, a.inv ? a.inv + b * a.sInv : nullptr};
+}
+
+// X = L^{-1} for a lower n x n tile (n <= 64): thread c owns column c and runs the forward
+// substitution down it (no inter-thread dependency); all threads walk (i, k) in lockstep so
+// L[i][k] is a shared-memory broadcast. Output: 64 x 64 (ld 64), zero upper triangle.
+__global__ void __launch_bounds__(64) trtri_tile_kernel(TileArgs args) {
+  extern __shared__ double trtri_sm[];
+  double* Ls = trtri_sm;
+  double* Xs = trtri_sm + kTile * (kTile + 1);
+  const int P = kTile + 1;
+  const TileView t = tile_task(args, blockIdx.x);
+  const int n = t.n, c = threadIdx.x;
+  if (n <= 0 || !t.inv) return;
+  for (int idx = c; idx < n * n; idx += 64) {
+    const int i = idx % n, j = idx / n;
+    Ls[i + j * P] = i >= j ? t.L[i + (long long)j * t.ldl] : 0.0;
+  }
+  __syncthreads();
+  for (int i = 0; i < n; ++i) {
+    double acc = (i == c) ? 1.0 : 0.0;
+    for (int k = 0; k < i; ++k) acc -= Ls[i + k * P] * Xs[k + c * P];
+    Xs[i + c * P] = (c <= i && c < n) ? acc / Ls[i + i * P] : 0.0;
+  }
+  __syncthreads();
+  for (int idx = c; idx < kTile * kTile; idx += 64) {
+    const int i = idx % kTile, j = idx / kTile;
+    t.inv[idx] = (i < n && j < n) ? Xs[i + j * P] : 0.0;
+  }
 }
 
 __global__ void __launch_bounds__(128) potrf_tile_kernel(TileArgs args) {
@@ -346,6 +375,18 @@ void potrf_tile(const TileArgs& a, cudaStream_t s) {
   BDDC_LAUNCH_CHECK();
 }
 
+void trtri_tile(const TileArgs& a, cudaStream_t s) {
+  if (a.count <= 0) return;
+  constexpr int smem = 2 * kTile * (kTile + 1) * (int)sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    BDDC_CUDA(cudaFuncSetAttribute(trtri_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  { trtri_tile_kernel<<<a.count, 64, smem, s>>>(a); BDDC_COUNT(); }
+  BDDC_LAUNCH_CHECK();
+}
+
 void trsm_tile(const TileArgs& a, TrsmKind kind, cudaStream_t s) {
   switch (kind) {
     case TRSM_LLN: launch_trsm<false, true>(a, s); break;
@@ -370,7 +411,20 @@ void gemm_batched(bool tA, bool tB, int M, int N, int K, double alpha, BMat A, B
   gemm(g, tA, tB, s);
 }
 
-void potrf_batched(BMat A, int n, int npiv, int count, int* info, cudaStream_t s) {
+// In-place tile solve with an explicit 64 x 64 inverse tile Vinv (ld 64), as a DMMA GEMM:
+//   LLN: X = Vinv B   LLT: X = Vinv^T B   (B: nb x nother; one 64-row tile -> in place)
+//   RLT: X = B Vinv^T RLN: X = B Vinv      (B: nother x nb; one 64-col tile -> in place)
+static void tile_solve_gemm(TrsmKind kind, BMat Vinv, int nb, BMat B, int nother, int count,
+                            cudaStream_t s) {
+  switch (kind) {
+    case TRSM_LLN: gemm_batched(false, false, nb, nother, nb, 1.0, Vinv, B, 0.0, B, count, s); break;
+    case TRSM_LLT: gemm_batched(true, false, nb, nother, nb, 1.0, Vinv, B, 0.0, B, count, s); break;
+    case TRSM_RLT: gemm_batched(false, true, nother, nb, nb, 1.0, B, Vinv, 0.0, B, count, s); break;
+    case TRSM_RLN: gemm_batched(false, false, nother, nb, nb, 1.0, B, Vinv, 0.0, B, count, s); break;
+  }
+}
+
+void potrf_batched(BMat A, int n, int npiv, int count, int* info, double* scratch, cudaStream_t s) {
   for (int k = 0; k < npiv; k += kTile) {
     const int nb = std::min(kTile, npiv - k);
     TileArgs t;
@@ -379,45 +433,53 @@ void potrf_batched(BMat A, int n, int npiv, int count, int* info, cudaStream_t s
     potrf_tile(t, s);
     const int rest = n - k - nb;
     if (rest <= 0) continue;
-    TileArgs r = t;
-    r.B = A.p + (k + nb) + (long long)k * A.ld; r.sB = A.stride; r.ldb = A.ld; r.nvec = rest;
-    trsm_tile(r, TRSM_RLT, s);
-    // trailing update A22 -= L21 L21^T (lower tiles only)
+    t.inv = scratch; t.sInv = kTileInvStride;
+    trtri_tile(t, s);
     BMat L21 = A.at(k + nb, k);
+    tile_solve_gemm(TRSM_RLT, BMat{scratch, kTileInvStride, kTile}, nb, L21, rest, count, s);
+    // trailing update A22 -= L21 L21^T (lower tiles only)
     BMat A22 = A.at(k + nb, k + nb);
     gemm_batched(false, true, rest, rest, nb, -1.0, L21, L21, 1.0, A22, count, s, true);
   }
 }
 
-void trsm_batched(TrsmKind kind, BMat L, int n, BMat B, int nother, int count, cudaStream_t s) {
+size_t trsm_scratch_doubles(int n, int count) {
+  return (size_t)count * ceil_div(n, kTile) * kTileInvStride;
+}
+
+void trsm_batched(TrsmKind kind, BMat L, int n, BMat B, int nother, int count, double* scratch,
+                  cudaStream_t s) {
   const int nblk = ceil_div(n, kTile);
-  auto tile = [&](int kb, BMat Bv) {
-    const int k = kb * kTile, nb = std::min(kTile, n - k);
+  const long long sInv = (long long)nblk * kTileInvStride;  // per batch entry
+  for (int kb = 0; kb < nblk; ++kb) {
+    const int k = kb * kTile;
     TileArgs t;
-    t.L = L.p + k + (long long)k * L.ld; t.sL = L.stride; t.ldl = L.ld; t.n = nb;
-    t.B = Bv.p; t.sB = Bv.stride; t.ldb = Bv.ld; t.nvec = nother; t.count = count;
-    trsm_tile(t, kind, s);
-  };
+    t.L = L.p + k + (long long)k * L.ld; t.sL = L.stride; t.ldl = L.ld;
+    t.n = std::min(kTile, n - k); t.count = count;
+    t.inv = scratch + kb * kTileInvStride; t.sInv = sInv;
+    trtri_tile(t, s);
+  }
+  auto inv = [&](int kb) { return BMat{scratch + kb * kTileInvStride, sInv, kTile}; };
   if (kind == TRSM_LLN) {  // forward over row blocks
     for (int kb = 0; kb < nblk; ++kb) {
       const int k = kb * kTile, nb = std::min(kTile, n - k), rest = n - k - nb;
-      tile(kb, B.at(k, 0));
+      tile_solve_gemm(kind, inv(kb), nb, B.at(k, 0), nother, count, s);
       if (rest > 0)
         gemm_batched(false, false, rest, nother, nb, -1.0, L.at(k + nb, k), B.at(k, 0), 1.0,
                      B.at(k + nb, 0), count, s);
     }
   } else if (kind == TRSM_LLT) {  // backward over row blocks
     for (int kb = nblk - 1; kb >= 0; --kb) {
-      const int k = kb * kTile;
-      tile(kb, B.at(k, 0));
+      const int k = kb * kTile, nb = std::min(kTile, n - k);
+      tile_solve_gemm(kind, inv(kb), nb, B.at(k, 0), nother, count, s);
       if (k > 0)  // B[0:k] -= L[k:k+nb, 0:k]^T X_k
-        gemm_batched(true, false, k, nother, std::min(kTile, n - k), -1.0, L.at(k, 0),
-                     B.at(k, 0), 1.0, B.at(0, 0), count, s);
+        gemm_batched(true, false, k, nother, nb, -1.0, L.at(k, 0), B.at(k, 0), 1.0, B.at(0, 0),
+                     count, s);
     }
   } else if (kind == TRSM_RLT) {  // forward over column blocks: X L^T = B
     for (int kb = 0; kb < nblk; ++kb) {
       const int k = kb * kTile, nb = std::min(kTile, n - k), rest = n - k - nb;
-      tile(kb, B.at(0, k));
+      tile_solve_gemm(kind, inv(kb), nb, B.at(0, k), nother, count, s);
       if (rest > 0)  // B[:, k+nb:] -= X_k L[k+nb:, k]^T
         gemm_batched(false, true, nother, rest, nb, -1.0, B.at(0, k), L.at(k + nb, k), 1.0,
                      B.at(0, k + nb), count, s);
@@ -425,10 +487,10 @@ void trsm_batched(TrsmKind kind, BMat L, int n, BMat B, int nother, int count, c
   } else {  // RLN: backward over column blocks: X L = B
     for (int kb = nblk - 1; kb >= 0; --kb) {
       const int k = kb * kTile, nb = std::min(kTile, n - k);
-      tile(kb, B.at(0, k));
+      tile_solve_gemm(kind, inv(kb), nb, B.at(0, k), nother, count, s);
       if (k > 0)  // B[:, 0:k] -= X_k L[k:k+nb, 0:k]
-        gemm_batched(false, false, nother, k, nb, -1.0, B.at(0, k), L.at(k, 0), 1.0,
-                     B.at(0, 0), count, s);
+        gemm_batched(false, false, nother, k, nb, -1.0, B.at(0, k), L.at(k, 0), 1.0, B.at(0, 0),
+                     count, s);
     }
   }
 }

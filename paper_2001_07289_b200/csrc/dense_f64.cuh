@@ -8,6 +8,8 @@
 
 namespace bddc {
 
+constexpr long long kTileInvStride = 64 * 64;
+
 struct GemmTask {
   const double* A;
   const double* B;
@@ -30,10 +32,11 @@ struct GemmArgs {
 };
 
 struct TileTask {
-  double* L;  // n x n lower tile
-  double* B;  // right-hand sides (see kernels)
+  double* L;    // n x n lower tile
+  double* B;    // right-hand sides (see kernels)
   int n, ldl, ldb, nvec;  // nvec: rows (right side) or columns (left side) of B
   int id, offset;         // batch entry id and global index of the tile's first row
+  double* inv;  // 64 x 64 scratch receiving L^{-1} (trtri_tile)
 };
 
 struct TileArgs {
@@ -46,6 +49,8 @@ struct TileArgs {
   int max_nvec = 0;
   int offset = 0;      // global index of first row (pivot reporting)
   int* info = nullptr; // per batch entry: first failing pivot (INT_MAX if none)
+  double* inv = nullptr;  // strided: inverse scratch, 64 x 64 per entry (sInv apart)
+  long long sInv = kTileInvStride;
 };
 
 enum TrsmKind {
@@ -58,6 +63,8 @@ enum TrsmKind {
 
 void gemm(const GemmArgs& a, bool transA, bool transB, cudaStream_t s);
 void potrf_tile(const TileArgs& a, cudaStream_t s);
+// inverse of n x n lower tiles (n <= 64) into 64 x 64 scratch (lower, zero upper)
+void trtri_tile(const TileArgs& a, cudaStream_t s);
 void trsm_tile(const TileArgs& a, TrsmKind kind, cudaStream_t s);
 
 // Strided uniform batch view of n x n (or rows x cols) matrices.
@@ -70,10 +77,15 @@ struct BMat {
 
 // Blocked in-place lower Cholesky of `count` n x n matrices; factors the leading npiv
 // columns only (npiv < n: partial factorization, trailing block becomes the Schur complement).
-void potrf_batched(BMat A, int n, int npiv, int count, int* info, cudaStream_t s);
+// scratch: count * 64 * 64 doubles (diagonal-tile inverses).
+void potrf_batched(BMat A, int n, int npiv, int count, int* info, double* scratch, cudaStream_t s);
 // Blocked triangular solves with a batch of n x n lower factors L:
 //   left kinds: B is n x ncol; right kinds: B is nrow x n.
-void trsm_batched(TrsmKind kind, BMat L, int n, BMat B, int nother, int count, cudaStream_t s);
+// scratch: count * ceil(n/64) * 64 * 64 doubles. Diagonal tiles are inverted once (trtri)
+// and every tile solve is an in-place DMMA GEMM with the inverse.
+void trsm_batched(TrsmKind kind, BMat L, int n, BMat B, int nother, int count, double* scratch,
+                  cudaStream_t s);
+size_t trsm_scratch_doubles(int n, int count);
 // C = alpha op(A) op(B) + beta C over a strided batch.
 void gemm_batched(bool tA, bool tB, int M, int N, int K, double alpha, BMat A, BMat B,
                   double beta, BMat C, int count, cudaStream_t s, bool lower = false);

@@ -338,7 +338,7 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
     c.prof.begin("setup.SK", s);
     { add_ctc_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, c.diag_s, c.LS); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
-    potrf_batched(LSb, G.nG_pad, G.nG_pad, cnt, c.info_k + sub0, s);
+    potrf_batched(LSb, G.nG_pad, G.nG_pad, cnt, c.info_k + sub0, c.tinv, s);
     c.prof.end("setup.SK", s);
     if (G.nc_pad > 0) {
       PhaseScope pphi(c.prof, "setup.Phi", s);
@@ -347,14 +347,14 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
       BDDC_LAUNCH_CHECK();
       BMat PHb{PH, phS, G.nG_pad};
       BMat SCb{SC, scS, G.nc_pad};
-      trsm_batched(TRSM_LLN, LSb, G.nG_pad, PHb, G.nc_pad, cnt, s);
+      trsm_batched(TRSM_LLN, LSb, G.nG_pad, PHb, G.nc_pad, cnt, c.tinv, s);
       gemm_batched(true, false, G.nc_pad, G.nc_pad, G.nG_pad, 1.0, PHb, PHb, 0.0, SCb, cnt, s);
       { sc_pad_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, SC); BDDC_COUNT(); }
       BDDC_LAUNCH_CHECK();
-      potrf_batched(SCb, G.nc_pad, G.nc_pad, cnt, nullptr, s);
-      trsm_batched(TRSM_RLT, SCb, G.nc_pad, PHb, G.nG_pad, cnt, s);
-      trsm_batched(TRSM_RLN, SCb, G.nc_pad, PHb, G.nG_pad, cnt, s);
-      trsm_batched(TRSM_LLT, LSb, G.nG_pad, PHb, G.nc_pad, cnt, s);
+      potrf_batched(SCb, G.nc_pad, G.nc_pad, cnt, nullptr, c.tinv, s);
+      trsm_batched(TRSM_RLT, SCb, G.nc_pad, PHb, G.nG_pad, cnt, c.tinv, s);
+      trsm_batched(TRSM_RLN, SCb, G.nc_pad, PHb, G.nG_pad, cnt, c.tinv, s);
+      trsm_batched(TRSM_LLT, LSb, G.nG_pad, PHb, G.nc_pad, cnt, c.tinv, s);
       // 6. P = Phi^T (S_Gamma Phi)
       BMat SGb{SG, lsS, G.nG_pad};
       BMat Xb{X, phS, G.nG_pad};
