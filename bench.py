@@ -173,6 +173,8 @@ def phase_work(op, pb, its):
     w["setup.Phi"] = ("fp64", float(np.sum(2 * nG * nG * nc + 2 * nG * nc * nc + nc**3 / 3
                                            + 2 * nG * nG * nc + 2 * nG * nc * nc)))
     w["setup.btchol"] = ("fp64", nsub * nblk * (m**3 / 3 + 2 * m**3))
+    # fused interior elimination (2D): btchol + E + S_G (SYRK, lower half)
+    w["setup.schur"] = ("fp64", w["setup.btchol"][1] + w["setup.E"][1] + w["setup.SG"][1])
     return w
 
 
@@ -234,8 +236,8 @@ def run_ours(args, rank, world, local_rank):
     clocks = sampler.stop()
     phases = {}
     for name in ("apply.bt_solve", "apply.gamma1", "apply.coarse", "apply.gamma2", "setup.assemble",
-                 "setup.btchol", "setup.E", "setup.SG", "setup.SK", "setup.Phi", "setup.coarse",
-                 "pcg.spmv_dot"):
+                 "setup.schur", "setup.btchol", "setup.E", "setup.SG", "setup.SK", "setup.Phi",
+                 "setup.coarse", "pcg.spmv_dot"):
         cnt = C.c_longlong()
         ms = lib.bddc_profile_read(ctx, name.encode(), C.byref(cnt))
         if cnt.value:

@@ -15,6 +15,9 @@
 
 namespace bddc {
 
+bool schur2d(const Ctx& c, int sub0, int cnt, const double* Wd, const double* Wo, const double* E,
+             cudaStream_t s);
+
 namespace {
 
 template <int DIM>
@@ -306,6 +309,12 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
       { assemble_local_kernel<3><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, Wd, Wo, E, c.LS, c.diag_s); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
     c.prof.end("setup.assemble", s);
+    // 2-3. fused on-chip interior elimination (2D) or the generic batched path
+    c.prof.begin("setup.schur", s);
+    const bool fused = G.nblk > 0 && schur2d(c, sub0, cnt, Wd, Wo, E, s);
+    c.prof.end("setup.schur", s);
+    BMat LSb{LS, lsS, G.nG_pad};
+    if (!fused) {
     // 2. interior block-tridiagonal Cholesky (+ inverses of the diagonal blocks)
     c.prof.begin("setup.btchol", s);
     if (G.nblk > 0) {
@@ -330,10 +339,10 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
     // S_Gamma = A_GG - E^T E  (in LS)
     c.prof.begin("setup.SG", s);
     BMat Eb{E2, eS, G.nI_pad};
-    BMat LSb{LS, lsS, G.nG_pad};
     gemm_batched(true, false, G.nG_pad, G.nG_pad, G.nI_pad, -1.0, Eb, Eb, 1.0, LSb, cnt, s);
-    BDDC_CUDA(cudaMemcpyAsync(SG, LS, sizeof(double) * cnt * lsS, cudaMemcpyDeviceToDevice, s));
     c.prof.end("setup.SG", s);
+    }
+    BDDC_CUDA(cudaMemcpyAsync(SG, LS, sizeof(double) * cnt * lsS, cudaMemcpyDeviceToDevice, s));
     // 4. S_K = S_Gamma + s C^T C; Cholesky
     c.prof.begin("setup.SK", s);
     { add_ctc_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, c.diag_s, c.LS); BDDC_COUNT(); }
