@@ -50,21 +50,20 @@ __global__ void gamma_residual_kernel(Geometry G, int n_gamma, const long long* 
   rpg[g] = r[f] - stencil_row<DIM>(G, alpha, u1, g0, g1, g2);
 }
 
-// Block-tridiagonal interior solve x_I = A_II^{-1} b_I, one warp per subdomain.
-// Factor = packed inverses Linv_j of the diagonal Cholesky blocks + the sparse coupling
-// stencil B_j to the previous plane (Lo_j = B_j Linv_{j-1}^T):
-//   forward   t = b_j - B_j u_{j-1};  y_j = Linv_j t;  u_j = Linv_j^T y_j
-//   backward  t = B_{j+1}^T x_{j+1};  v = y_j - Linv_j t;  x_j = Linv_j^T v
-// Each lane owns rows r = lane + 32 i (i < R); the GEMVs broadcast the vector with
-// shuffles and read the packed column-major blocks straight from the cp.async staging
-// buffers (double-buffered: block j+-1 streams in while block j is used). Each Linv_j is
-// read from HBM once per pass.
+// Block-tridiagonal interior solve x_I = A_II^{-1} b_I, one warp per subdomain, with the
+// factor stored as packed symmetric Schur-complement inverses W_j = S_j^{-1} plus the
+// sparse coupling stencil B_j to the previous plane (block LDL^T):
+//   forward   h_j = W_j (b_j - B_j h_{j-1})
+//   backward  x_j = h_j - W_j (B_{j+1}^T x_{j+1})
+// Each lane owns rows r = lane + 32 i (i < R); the symmetric GEMV broadcasts the vector
+// with shuffles and reads the packed column-major lower triangle straight from the
+// cp.async staging buffers (double-buffered: block j+-1 streams in while block j is used).
+// Each W_j is read from HBM once per pass.
 constexpr int kBtWarps = 4;
 
 template <int R>
-__device__ __forceinline__ void bt_bcast_gemv(const double* __restrict__ pk, int M, const double (&v)[R],
-                                              double (&out)[R], bool trans, int lane) {
-  // out_r = sum_k L[r][k] v_k  (trans: sum_k L[k][r] v_k), L packed lower column-major
+__device__ __forceinline__ void bt_sym_gemv(const double* __restrict__ pk, int M, const double (&v)[R],
+                                            double (&out)[R], int lane) {
 #pragma unroll
   for (int i = 0; i < R; ++i) out[i] = 0.0;
   for (int k = 0; k < M; ++k) {
@@ -74,15 +73,13 @@ __device__ __forceinline__ void bt_bcast_gemv(const double* __restrict__ pk, int
       const double b = __shfl_sync(0xffffffffu, v[i], k & 31);
       if ((k >> 5) == i) vk = b;
     }
+    const int csk = k * M - k * (k - 1) / 2;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const int r = lane + 32 * i;
       if (r >= M) continue;
-      if (!trans) {
-        if (k <= r) out[i] += pk[k * M - k * (k - 1) / 2 + (r - k)] * vk;
-      } else {
-        if (k >= r) out[i] += pk[r * M - r * (r - 1) / 2 + (k - r)] * vk;
-      }
+      const double w = k <= r ? pk[csk + (r - k)] : pk[r * M - r * (r - 1) / 2 + (k - r)];
+      out[i] += w * vk;
     }
   }
 }
@@ -100,7 +97,7 @@ __global__ void __launch_bounds__(32 * kBtWarps) bt_solve_kernel(Geometry G, Loc
   const int per_warp = G.nI_pad + 2 * tm_pad + M + (M & 1);
   double* y = sm + warp * per_warp;  // nI_pad
   double* stg[2] = {y + G.nI_pad, y + G.nI_pad + tm_pad};
-  double* uv = y + G.nI_pad + 2 * tm_pad;  // M
+
   if (sub >= G.nsub) return;
   int p[3];
   sub_coords(G, sub, p);
@@ -122,8 +119,8 @@ __global__ void __launch_bounds__(32 * kBtWarps) bt_solve_kernel(Geometry G, Loc
     }
     y[rr] = v;
   }
-  double t[R], yv[R];
-  // ---- forward ----
+  double t[R], hv[R];
+  // ---- forward: h_j = W_j (b_j - B_j h_{j-1}) ----
   if (G.nblk > 0) prefetch(0, stg[0]);
   for (int j = 0; j < G.nblk; ++j) {
     const double* pk = stg[j & 1];
@@ -142,29 +139,26 @@ __global__ void __launch_bounds__(32 * kBtWarps) bt_solve_kernel(Geometry G, Loc
         acc = y[j * M + r];
         if (j > 0) {
           const double* bj = bc + ((long long)j * M + r) * G.nbo;
+          const double* hp = y + (j - 1) * M;
           const int x = r % px, yy = r / px;
           for (int k = 0; k < G.nbo; ++k) {
             const double cf = bj[k];
-            if (cf != 0.0) acc -= cf * uv[(x + G.bo_dx[k]) + (yy + G.bo_dy[k]) * px];
+            if (cf != 0.0) acc -= cf * hp[(x + G.bo_dx[k]) + (yy + G.bo_dy[k]) * px];
           }
         }
       }
       t[i] = acc;
     }
     __syncwarp();
-    bt_bcast_gemv<R>(pk, M, t, yv, false, lane);
+    bt_sym_gemv<R>(pk, M, t, hv, lane);
 #pragma unroll
     for (int i = 0; i < R; ++i)
-      if (lane + 32 * i < M) y[j * M + lane + 32 * i] = yv[i];
-    bt_bcast_gemv<R>(pk, M, yv, t, true, lane);  // u_j = Linv_j^T y_j
-#pragma unroll
-    for (int i = 0; i < R; ++i)
-      if (lane + 32 * i < M) uv[lane + 32 * i] = t[i];
+      if (lane + 32 * i < M) y[j * M + lane + 32 * i] = hv[i];
     __syncwarp();
   }
-  // ---- backward ----
-  if (G.nblk > 0) prefetch(G.nblk - 1, stg[0]);
-  for (int j = G.nblk - 1, it = 0; j >= 0; --j, ++it) {
+  // ---- backward: x_j = h_j - W_j (B_{j+1}^T x_{j+1}) ----
+  if (G.nblk > 1) prefetch(G.nblk - 2, stg[0]);
+  for (int j = G.nblk - 2, it = 0; j >= 0; --j, ++it) {
     const double* pk = stg[it & 1];
     if (j > 0) {
       prefetch(j - 1, stg[(it + 1) & 1]);
@@ -173,42 +167,29 @@ __global__ void __launch_bounds__(32 * kBtWarps) bt_solve_kernel(Geometry G, Loc
       cp_async_wait<0>();
     }
     __syncwarp();
-    double v[R];
-    if (j + 1 < G.nblk) {
-      const double* xn = y + (j + 1) * M;
+    const double* xn = y + (j + 1) * M;
 #pragma unroll
-      for (int i = 0; i < R; ++i) {
-        const int r = lane + 32 * i;
-        double acc = 0.0;
-        if (r < M) {
-          const int x = r % px, yy = r / px;
-          for (int k = 0; k < G.nbo; ++k) {
-            const int rs = (x - G.bo_dx[k]) + (yy - G.bo_dy[k]) * px;
-            if (rs < 0 || rs >= M) continue;
-            const double cf = bc[((long long)(j + 1) * M + rs) * G.nbo + k];
-            if (cf != 0.0) acc += cf * xn[rs];
-          }
+    for (int i = 0; i < R; ++i) {
+      const int r = lane + 32 * i;
+      double acc = 0.0;
+      if (r < M) {
+        const int x = r % px, yy = r / px;
+        for (int k = 0; k < G.nbo; ++k) {
+          const int rs = (x - G.bo_dx[k]) + (yy - G.bo_dy[k]) * px;
+          if (rs < 0 || rs >= M) continue;
+          const double cf = bc[((long long)(j + 1) * M + rs) * G.nbo + k];
+          if (cf != 0.0) acc += cf * xn[rs];
         }
-        t[i] = acc;
       }
-      bt_bcast_gemv<R>(pk, M, t, v, false, lane);
-#pragma unroll
-      for (int i = 0; i < R; ++i) {
-        const int r = lane + 32 * i;
-        v[i] = r < M ? y[j * M + r] - v[i] : 0.0;
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < R; ++i) {
-        const int r = lane + 32 * i;
-        v[i] = r < M ? y[j * M + r] : 0.0;
-      }
+      t[i] = acc;
     }
-    bt_bcast_gemv<R>(pk, M, v, t, true, lane);
+    bt_sym_gemv<R>(pk, M, t, hv, lane);
     __syncwarp();
 #pragma unroll
-    for (int i = 0; i < R; ++i)
-      if (lane + 32 * i < M) y[j * M + lane + 32 * i] = t[i];
+    for (int i = 0; i < R; ++i) {
+      const int r = lane + 32 * i;
+      if (r < M) y[j * M + r] -= hv[i];
+    }
     __syncwarp();
   }
   for (int rr = lane; rr < G.nI_pad; rr += 32) {

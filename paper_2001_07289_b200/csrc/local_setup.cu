@@ -186,11 +186,15 @@ __global__ void __launch_bounds__(128) btchol_kernel(Geometry G, int sub0, doubl
       }
     }
     __syncthreads();
-    // outputs
+    // outputs: packed W_j = S_j^{-1} = Linv^T Linv (apply), dense Linv / Lo (workspace)
     double* pk = li + (long long)j * G.Tm;
     for (int c = 0; c < M; ++c) {
       const long long cs = (long long)c * M - (long long)c * (c - 1) / 2;  // packed column start
-      for (int r = c + tid; r < M; r += nt) pk[cs + (r - c)] = inv[r + c * P];
+      for (int r = c + tid; r < M; r += nt) {
+        double a = 0.0;
+        for (int k = r; k < M; ++k) a += inv[k + r * P] * inv[k + c * P];
+        pk[cs + (r - c)] = a;
+      }
     }
     for (int idx = tid; idx < M * M; idx += nt) {
       const int r = idx % M, c = idx / M;
