@@ -34,6 +34,7 @@ struct Geometry {
   // diagonal Cholesky blocks (Tm = m_pad(m_pad+1)/2 doubles each), then the coupling
   // stencil to the previous plane, Bc[j][r][k] for the nbo structurally nonzero offsets
   int Tm;
+  int nact[64];  // 2D: active interface columns (prefix) of R_j / H_j at plane j
   int nbo;
   int bo_dx[9], bo_dy[9];
   long long li_stride;

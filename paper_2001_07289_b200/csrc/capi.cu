@@ -221,7 +221,7 @@ void do_setup(bddc_ctx* h, const bddc_setup_desc* d) {
   G.nblk = d->nblk;
   G.nI_pad = d->nI_pad;
   G.nc_pad = d->nc_pad;
-  if (G.m_pad > 64 || G.m_pad % 8 || G.nI_pad != G.m_pad * G.nblk)
+  if (G.m_pad > 64 || G.m_pad % 8 || G.nI_pad != G.m_pad * G.nblk || G.nblk > 64)
     throw ApiError{1, "interior planes must fit one 64-row tile (m_pad <= 64, multiple of 8)"};
   if (G.nG_pad > 1024 || G.nG_pad % 8 || G.nc_pad > 1024 || G.nc_pad % 8)
     throw ApiError{1, "interface / constraint padding out of range"};
@@ -248,6 +248,29 @@ void do_setup(bddc_ctx* h, const bddc_setup_desc* d) {
       }
     }
   G.Tm = G.m_pad * (G.m_pad + 1) / 2;
+  // active interface prefix per plane: the largest slot coupled to planes <= j (A_IG)
+  {
+    std::vector<int> code(d->node_code, d->node_code + G.nloc_nodes);
+    std::vector<int> act(std::max(G.nblk, 1), 0);
+    const int n0 = G.blk[0] + 1, n1 = G.blk[1] + 1;
+    for (int node = 0; node < G.nloc_nodes; ++node) {
+      if (code[node] < 0) continue;  // interior nodes only
+      const int plane = code[node] / G.m_pad;
+      const int a0 = node % n0, a1 = (node / n0) % n1, a2 = G.dim == 3 ? node / (n0 * n1) : 0;
+      for (int o = 0; o < (G.dim == 3 ? 27 : 9); ++o) {
+        const int b0 = a0 + o % 3 - 1, b1 = a1 + (o / 3) % 3 - 1, b2 = a2 + (G.dim == 3 ? o / 9 - 1 : 0);
+        if (b0 < 0 || b1 < 0 || b2 < 0 || b0 >= n0 || b1 >= n1) continue;
+        if (G.dim == 3 && b2 > G.blk[2]) continue;
+        const int nb = b0 + n0 * (b1 + n1 * b2);
+        if (code[nb] < 0) act[plane] = std::max(act[plane], -code[nb]);  // slot + 1
+      }
+    }
+    for (int j = 1; j < G.nblk; ++j) act[j] = std::max(act[j], act[j - 1]);
+    for (int j = 0; j < 64; ++j) {
+      const int a = j < G.nblk ? act[j] : G.nG_pad;
+      G.nact[j] = std::min<int>(G.nG_pad, (int)round_up(std::max(a, 8), 8));
+    }
+  }
   G.li_stride = round_up((long long)G.nblk * G.Tm + (long long)G.nblk * G.m_pad * G.nbo, 2);
   c.element = d->element;
   c.coarse_scaling = d->coarse_scaling;

@@ -1,24 +1,29 @@
-// Fused interior elimination for 2D subdomains (block rows of M <= 32, interface <= NGP):
-// one CTA per subdomain runs the whole plane recursion on chip as a block LDL^T with
-// explicit Schur-complement inverses (B_j = coupling stencil of plane j to plane j-1):
-//   S_j = T_j - B_j W_{j-1} B_j^T ;  W_j = S_j^{-1}  (Gauss-Jordan sweep, one barrier/pivot)
-//   R_j = A_IG,j - B_j H_{j-1}    ;  H_j = W_j R_j  (DMMA)
-//   S_G = A_GG - sum_j R_j^T H_j                    (lower 8x8 tiles in registers, DMMA)
-// The B_j products are stencil operations (1 coefficient per row for P1, 3 for Q1). It
-// replaces btchol_kernel + 2 nblk batched GEMM launches + the S_G GEMM of the generic
-// path and writes packed W_j + the coupling stencil (LI) and S_G (LS, full).
+// Fused interior elimination for 2D subdomains (plane rows M <= 32, interface <= NGP), as a
+// block LDL^T with explicit Schur-complement inverses (B_j = coupling stencil plane j -> j-1):
+//   S_j = T_j - B_j W_{j-1} B_j^T ;  W_j = S_j^{-1}
+//   R_j = A_IG,j - B_j H_{j-1}    ;  H_j = W_j R_j
+//   S_G = A_GG - sum_j R_j^T H_j
+// Two kernels:
+//  * wfactor2d: the W recursion, one warp per subdomain (Gauss-Jordan sweep with lane =
+//    column, __syncwarp only), writes packed W_j + the stencil (the apply's interior factor);
+//  * schur2d: one CTA per subdomain, R_j / H_j / S_G on the FP64 tensor pipe
+//    (mma.sync m8n8k4 -> DMMA.8x8x4), restricted to the active interface prefix of plane j
+//    (in the lexicographic slot order, R_j and H_j vanish beyond slot nact[j]).
+// Replaces btchol_kernel + 2 nblk batched GEMMs + the S_G GEMM of the generic path.
 #include "stencil.cuh"
 
 namespace bddc {
 
 namespace {
 
+constexpr int kWarpsW = 4;         // subdomains per CTA in wfactor2d
 constexpr int kSchurThreads = 256;
 
 // C(8x8 tile) += A(8 x K) B(K x 8); A(r,k) = A[r*ars + k*acs], B(k,c) = B[k*brs + c*bcs]
 __device__ __forceinline__ void mma_acc(double& c0, double& c1, const double* A, int ars, int acs,
                                         const double* B, int brs, int bcs, int K, int lane) {
   const int g = lane >> 2, t = lane & 3;
+#pragma unroll 4
   for (int k = 0; k < K; k += 4) {
     const double a = A[g * ars + (k + t) * acs];
     const double b = B[(k + t) * brs + g * bcs];
@@ -26,158 +31,205 @@ __device__ __forceinline__ void mma_acc(double& c0, double& c1, const double* A,
   }
 }
 
-template <int M, int NGP>
-__global__ void __launch_bounds__(kSchurThreads) schur2d_kernel(Geometry G, int sub0,
-                                                                const double* __restrict__ Wd,
-                                                                const double* __restrict__ Wo,
-                                                                const double* __restrict__ Eg,
-                                                                double* __restrict__ LI,
-                                                                double* __restrict__ LS,
-                                                                int* __restrict__ info) {
-  constexpr int P = M + 1;       // pitch of M x M blocks (col-major X[r + c*P])
-  constexpr int EP = NGP + 4;    // pitch of M x NGP blocks, row-major E[k*EP + col]
-  constexpr int NT = NGP / 8;    // interface tiles per dimension
-  constexpr int NLT = NT * (NT + 1) / 2;
-  constexpr int NW = kSchurThreads / 32;
-  constexpr int SYRK_PER_WARP = (NLT + NW - 1) / NW;
-  constexpr int ET = (M / 8) * NT;  // 8x8 tiles of an M x NGP block
-  extern __shared__ __align__(16) double sm[];
-  double* Ha = sm;                 // H_{j-1} / H_j   (M x EP)
-  double* Rb = Ha + M * EP;        // A_IG,j -> R_j   (M x EP)
-  double* Ww = Rb + M * EP;        // T_j -> S_j -> W_j = S_j^{-1}
-  double* Wp = Ww + M * P;         // W_{j-1}
-  double* Xs = Wp + M * P;         // B_j W_{j-1} (general stencils)
-  double* bcs = Xs + M * P;        // B_j stencil [M][nbo]
-  double* rb = bcs + M * 9;        // Gauss-Jordan row / column buffers, 2 parities
-  double* cb = rb + 2 * M;
-  __shared__ int failed;
-  const int b = blockIdx.x, sub = sub0 + b;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t4 = lane & 3;
-  const long long mm = (long long)G.m_pad * G.m_pad;
+// ---- W recursion: lane k owns column k of the M x M block (M <= 32) ----
+template <int M, bool DIAGB>
+__global__ void __launch_bounds__(32 * kWarpsW) wfactor2d_kernel(Geometry G, int sub0, int cnt,
+                                                                 const double* __restrict__ Wd,
+                                                                 const double* __restrict__ Wo,
+                                                                 double* __restrict__ LI,
+                                                                 int* __restrict__ info) {
+  constexpr int P = M + 1;
+  extern __shared__ __align__(16) double smw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * kWarpsW + warp;
+  if (b >= cnt) return;
+  const int sub = sub0 + b;
+  // per warp: W_j (in place), column buffer, [X scratch for general stencils]
+  double* W = smw + warp * ((DIAGB ? 1 : 2) * M * P + M);
+  double* tmp = W + M * P;
+  double* X = tmp + M;
+  const long long mm = (long long)M * M;
   const double* wd = Wd + (long long)b * G.nblk * mm;
   const double* wo = Wo + (long long)b * G.nblk * mm;
-  const double* eg = Eg + (long long)b * G.nI_pad * G.nG_pad;
   double* li = LI + (long long)sub * G.li_stride;
   double* bcg = li + (long long)G.nblk * G.Tm;
   const int px = G.blk[0] - 1;
   const int nbo = G.nbo;
-  if (tid == 0) failed = -1;
+  const int k = lane;  // owned column
+  int failed = -1;
+  for (int j = 0; j < G.nblk; ++j) {
+    // coupling stencil of plane j (row r = lane): bc[k] for the nbo offsets
+    double cf[3] = {0.0, 0.0, 0.0};
+    if (j > 0 && lane < G.m) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        if (q >= nbo) break;
+        const int x = lane + G.bo_dx[q];
+        if (x >= 0 && x < px) cf[q] = wo[j * mm + lane + (long long)x * M];
+      }
+    }
+    if (lane < M) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        if (q < nbo) bcg[((long long)j * M + lane) * nbo + q] = cf[q];
+    }
+    if (j > 0 && DIAGB) {
+      // B_j diagonal (P1): S_j[i][k] = T_j[i][k] - b_i W_{j-1}[i][k] b_k, in place
+      for (int i = 0; i < M; ++i) {
+        const double bi = __shfl_sync(0xffffffffu, cf[0], i);
+        if (k < M) W[i + k * P] = wd[j * mm + i + (long long)k * M] - bi * W[i + k * P] * cf[0];
+      }
+    } else if (j > 0) {
+      // X = B_j W_{j-1}: X[i][k] = sum_q cf_i[q] W[i + dx_q][k]  (cf of row i via shuffles)
+      for (int i = 0; i < M; ++i) {
+        double a = 0.0;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          if (q >= nbo) break;
+          const double ci = __shfl_sync(0xffffffffu, cf[q], i);
+          const int ii = i + G.bo_dx[q];
+          if (ci != 0.0 && ii >= 0 && ii < M && k < M) a += ci * W[ii + k * P];
+        }
+        if (k < M) X[i + k * P] = a;
+      }
+      __syncwarp();
+      // S_j = T_j - X B_j^T: S[i][k] = T[i][k] - sum_q X[i][k + dx_q] cf_k[q]
+      for (int i = 0; i < M; ++i) {
+        double a = 0.0;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          if (q >= nbo) break;
+          const int kk = k + G.bo_dx[q];
+          if (cf[q] != 0.0 && kk >= 0 && kk < M) a += X[i + kk * P] * cf[q];
+        }
+        if (k < M) W[i + k * P] = wd[j * mm + i + (long long)k * M] - a;
+      }
+    } else if (k < M) {
+      for (int i = 0; i < M; ++i) W[i + k * P] = wd[i + (long long)k * M];
+    }
+    __syncwarp();
+    // Gauss-Jordan sweep W <- S^{-1}: lane k updates column k; column c goes through tmp
+    for (int c = 0; c < M; ++c) {
+      double piv = W[c + c * P];
+      if (!(piv > 0.0)) {
+        if (failed < 0) failed = j * M + c;
+        piv = 1.0;
+      }
+      const double ip = 1.0 / piv;
+      const double rk = k < M ? W[c + k * P] : 0.0;  // row c, own column
+      for (int i = 0; i < M; ++i) {
+        const double ci = W[i + c * P];
+        double v;
+        if (i == c) v = (k == c) ? ip : rk * ip;
+        else if (k == c) v = -ci * ip;
+        else v = k < M ? fma(-ci * ip, rk, W[i + k * P]) : 0.0;
+        if (k == c) tmp[i] = v;
+        else if (k < M) W[i + k * P] = v;
+      }
+      __syncwarp();
+      if (k < M) W[k + c * P] = tmp[k];
+      __syncwarp();
+    }
+    // packed W_j (column-major lower)
+    if (k < M) {
+      const int cs = k * M - k * (k - 1) / 2;
+      for (int i = k; i < M; ++i) li[(long long)j * G.Tm + cs + (i - k)] = W[i + k * P];
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && failed >= 0) atomicMin(info + sub, failed);
+}
+
+// ---- R_j / H_j / S_G with DMMA, W_j streamed back from the packed factor ----
+template <int M, int NGP>
+__global__ void __launch_bounds__(kSchurThreads) schur2d_kernel(Geometry G, int sub0,
+                                                                const double* __restrict__ Eg,
+                                                                const double* __restrict__ LI,
+                                                                double* __restrict__ LS) {
+  constexpr int P = M + 1;
+  constexpr int EP = NGP + 4;
+  constexpr int NT = NGP / 8;
+  constexpr int NLT = NT * (NT + 1) / 2;
+  constexpr int NW = kSchurThreads / 32;
+  constexpr int SYRK_PER_WARP = (NLT + NW - 1) / NW;
+  constexpr int O_H = 0;               // H_{j-1} / H_j   (M x EP)
+  constexpr int O_R = O_H + M * EP;    // A_IG,j -> R_j   (M x EP)
+  constexpr int O_W = O_R + M * EP;    // W_j (square)
+  constexpr int O_BC = O_W + M * P;    // stencil [M][3]
+  extern __shared__ __align__(16) double sm[];
+  const int b = blockIdx.x, sub = sub0 + b;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const double* eg = Eg + (long long)b * G.nI_pad * G.nG_pad;
+  const double* li = LI + (long long)sub * G.li_stride;
+  const double* bcg = li + (long long)G.nblk * G.Tm;
+  const int nbo = G.nbo;
+  int bdx[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) bdx[q] = q < nbo ? G.bo_dx[q] : 0;
 
   double acc[SYRK_PER_WARP][2];
 #pragma unroll
   for (int q = 0; q < SYRK_PER_WARP; ++q) acc[q][0] = acc[q][1] = 0.0;
-
+  int nprev = 0;
   for (int j = 0; j < G.nblk; ++j) {
-    // ---- load T_j, the B_j stencil, A_IG rows of plane j ----
-    for (int idx = tid; idx < M * M; idx += kSchurThreads) Ww[idx % M + (idx / M) * P] = wd[j * mm + idx];
-    for (int idx = tid; idx < M * nbo; idx += kSchurThreads) {
-      const int r = idx / nbo, k = idx % nbo;
-      double v = 0.0;
-      if (j > 0 && r < G.m) {
-        const int x = r % px + G.bo_dx[k];
-        if (x >= 0 && x < px) v = wo[j * mm + r + (long long)x * M];
-      }
-      bcs[r * 9 + k] = v;
-      bcg[((long long)j * M + r) * nbo + k] = v;
-    }
-    for (int idx = tid; idx < M * NGP; idx += kSchurThreads) {
-      const int r = idx % M, cc = idx / M;
-      Rb[r * EP + cc] = eg[(j * M + r) + (long long)cc * G.nI_pad];
-    }
-    __syncthreads();
-    if (j > 0) {
-      // ---- S_j = T_j - B_j W_{j-1} B_j^T ;  R_j = A_IG,j - B_j H_{j-1} (stencil ops) ----
-      for (int idx = tid; idx < M * M; idx += kSchurThreads) {  // X = B W
-        const int r = idx % M, c = idx / M;
-        double a = 0.0;
-        for (int k = 0; k < nbo; ++k) {
-          const double cf = bcs[r * 9 + k];
-          if (cf != 0.0) a += cf * Wp[(r % px + G.bo_dx[k]) + c * P];
-        }
-        Xs[r + c * P] = a;
-      }
-      for (int idx = tid; idx < M * NGP; idx += kSchurThreads) {
-        const int r = idx / NGP, cc = idx % NGP;
-        double a = 0.0;
-        for (int k = 0; k < nbo; ++k) {
-          const double cf = bcs[r * 9 + k];
-          if (cf != 0.0) a += cf * Ha[(r % px + G.bo_dx[k]) * EP + cc];
-        }
-        Rb[r * EP + cc] -= a;
-      }
-      __syncthreads();
-      for (int idx = tid; idx < M * M; idx += kSchurThreads) {  // S -= X B^T
-        const int r = idx % M, c = idx / M;
-        double a = 0.0;
-        for (int k = 0; k < nbo; ++k) {
-          const double cf = bcs[c * 9 + k];
-          if (cf != 0.0) a += Xs[r + (c % px + G.bo_dx[k]) * P] * cf;
-        }
-        Ww[r + c * P] -= a;
-      }
-      __syncthreads();
-    }
-    // ---- W_j = S_j^{-1}: in-place Gauss-Jordan sweep, one barrier per pivot ----
-    for (int idx = tid; idx < M; idx += kSchurThreads) {
-      rb[idx] = Ww[0 + idx * P];
-      cb[idx] = Ww[idx + 0 * P];
-    }
-    __syncthreads();
+    const int na = G.nact[j];           // active columns (multiple of 8)
+    const int nat = na / 8;
+    // W_j (unpack), stencil, A_IG rows (active columns)
     for (int c = 0; c < M; ++c) {
-      const int pa = c & 1;
-      const double* rc = rb + pa * M;
-      const double* cc = cb + pa * M;
-      double* rn = rb + (pa ^ 1) * M;
-      double* cn = cb + (pa ^ 1) * M;
-      double piv = rc[c];
-      if (!(piv > 0.0)) {
-        if (tid == 0 && failed < 0) failed = j * M + c;
-        piv = 1.0;
+      const int cs = c * M - c * (c - 1) / 2;
+      for (int r = c + tid; r < M; r += kSchurThreads) {
+        const double v = li[(long long)j * G.Tm + cs + r - c];
+        sm[O_W + r + c * P] = v;
+        sm[O_W + c + r * P] = v;
       }
-      const double ip = 1.0 / piv;
-      for (int idx = tid; idx < M * M; idx += kSchurThreads) {
-        const int i = idx % M, k = idx / M;
-        double v;
-        if (i == c && k == c) v = ip;
-        else if (i == c) v = rc[k] * ip;
-        else if (k == c) v = -cc[i] * ip;
-        else v = Ww[i + k * P] - cc[i] * rc[k] * ip;
-        Ww[i + k * P] = v;
-        if (i == c + 1) rn[k] = v;
-        if (k == c + 1) cn[i] = v;
+    }
+    for (int idx = tid; idx < M * nbo; idx += kSchurThreads)
+      sm[O_BC + (idx / nbo) * 3 + idx % nbo] = bcg[(long long)j * M * nbo + idx];
+    for (int idx = tid; idx < M * na; idx += kSchurThreads) {
+      const int r = idx % M, cc = idx / M;
+      sm[O_R + r * EP + cc] = eg[(j * M + r) + (long long)cc * G.nI_pad];
+    }
+    __syncthreads();
+    if (j > 0) {  // R_j -= B_j H_{j-1} on the previously active columns
+      for (int idx = tid; idx < M * nprev; idx += kSchurThreads) {
+        const int r = idx / nprev, cc = idx % nprev;
+        double a = 0.0;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          if (q >= nbo) break;
+          const double cf = sm[O_BC + r * 3 + q];
+          if (cf != 0.0) a += cf * sm[O_H + (r + bdx[q]) * EP + cc];
+        }
+        sm[O_R + r * EP + cc] -= a;
       }
       __syncthreads();
     }
-    // packed W_j (lower, column-major) for the apply
-    for (int idx = tid; idx < M * M; idx += kSchurThreads) {
-      const int r = idx % M, c = idx / M;
-      if (r >= c) li[(long long)j * G.Tm + c * M - c * (c - 1) / 2 + (r - c)] = Ww[r + c * P];
-    }
-    // ---- H_j = W_j R_j (into Ha) ----
-    for (int tt = warp; tt < ET; tt += NW) {
+    // H_j = W_j R_j (active column tiles)
+    for (int tt = warp; tt < (M / 8) * nat; tt += NW) {
       const int ti = tt % (M / 8), tj = tt / (M / 8);
       double c0 = 0.0, c1 = 0.0;
-      mma_acc(c0, c1, Ww + ti * 8, 1, P, Rb + tj * 8, EP, 1, M, lane);
-      Ha[(ti * 8 + g) * EP + tj * 8 + 2 * t4] = c0;
-      Ha[(ti * 8 + g) * EP + tj * 8 + 2 * t4 + 1] = c1;
+      mma_acc(c0, c1, sm + O_W + ti * 8, 1, P, sm + O_R + tj * 8, EP, 1, M, lane);
+      sm[O_H + (ti * 8 + g) * EP + tj * 8 + 2 * t4] = c0;
+      sm[O_H + (ti * 8 + g) * EP + tj * 8 + 2 * t4 + 1] = c1;
     }
     __syncthreads();
-    // ---- S_acc += R_j^T H_j (lower interface tiles; = R^T W R, symmetric) ----
+    // S_acc += R_j^T H_j on active lower tiles (I, J < nat)
+    const int nlt_act = nat * (nat + 1) / 2;
 #pragma unroll
     for (int q = 0; q < SYRK_PER_WARP; ++q) {
       const int tt = warp + q * NW;
-      if (tt < NLT) {
+      if (tt < nlt_act) {
         int I = 0;
         while ((I + 1) * (I + 2) / 2 <= tt) ++I;
         const int J = tt - I * (I + 1) / 2;
-        mma_acc(acc[q][0], acc[q][1], Rb + I * 8, 1, EP, Ha + J * 8, EP, 1, M, lane);
+        mma_acc(acc[q][0], acc[q][1], sm + O_R + I * 8, 1, EP, sm + O_H + J * 8, EP, 1, M, lane);
       }
     }
-    { double* tmp = Wp; Wp = Ww; Ww = tmp; }
+    nprev = na;
     __syncthreads();
   }
-  // ---- S_G = A_GG - S_acc, mirrored to a full symmetric matrix ----
+  // S_G = A_GG - S_acc (full symmetric)
   double* ls = LS + (long long)sub * G.nG_pad * G.nG_pad;
   const int ld = G.nG_pad;
 #pragma unroll
@@ -197,25 +249,27 @@ __global__ void __launch_bounds__(kSchurThreads) schur2d_kernel(Geometry G, int 
       }
     }
   }
-  if (tid == 0 && failed >= 0) atomicMin(info + sub, failed);
-}
-
-template <int M, int NGP>
-size_t schur2d_smem() {
-  return sizeof(double) * (2 * M * (NGP + 4) + 3 * M * (M + 1) + 9 * M + 4 * M);
 }
 
 template <int M, int NGP>
 void launch_schur2d(const Ctx& c, int sub0, int cnt, const double* Wd, const double* Wo,
                     const double* E, cudaStream_t s) {
-  const size_t smem = schur2d_smem<M, NGP>();
+  const bool diagb = c.geo.nbo == 1 && c.geo.bo_dx[0] == 0;
+  const size_t smem_w = sizeof(double) * kWarpsW * ((diagb ? 1 : 2) * M * (M + 1) + M);
+  const size_t smem_s = sizeof(double) * (2 * M * (NGP + 4) + M * (M + 1) + 3 * M);
   static bool attr = false;
   if (!attr) {
-    BDDC_CUDA(cudaFuncSetAttribute(schur2d_kernel<M, NGP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
+    BDDC_CUDA(cudaFuncSetAttribute(wfactor2d_kernel<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(sizeof(double) * kWarpsW * (2 * M * (M + 1) + M))));
+    BDDC_CUDA(cudaFuncSetAttribute(wfactor2d_kernel<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(sizeof(double) * kWarpsW * (2 * M * (M + 1) + M))));
+    BDDC_CUDA(cudaFuncSetAttribute(schur2d_kernel<M, NGP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
     attr = true;
   }
-  { schur2d_kernel<M, NGP><<<cnt, kSchurThreads, smem, s>>>(c.geo, sub0, Wd, Wo, E, c.LI, c.LS, c.info); BDDC_COUNT(); }
+  if (diagb) { wfactor2d_kernel<M, true><<<ceil_div(cnt, kWarpsW), 32 * kWarpsW, smem_w, s>>>(c.geo, sub0, cnt, Wd, Wo, c.LI, c.info); BDDC_COUNT(); }
+  else { wfactor2d_kernel<M, false><<<ceil_div(cnt, kWarpsW), 32 * kWarpsW, smem_w, s>>>(c.geo, sub0, cnt, Wd, Wo, c.LI, c.info); BDDC_COUNT(); }
+  BDDC_LAUNCH_CHECK();
+  { schur2d_kernel<M, NGP><<<cnt, kSchurThreads, smem_s, s>>>(c.geo, sub0, E, c.LI, c.LS); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
 }
 
@@ -225,7 +279,7 @@ void launch_schur2d(const Ctx& c, int sub0, int cnt, const double* Wd, const dou
 bool schur2d(const Ctx& c, int sub0, int cnt, const double* Wd, const double* Wo, const double* E,
              cudaStream_t s) {
   const Geometry& G = c.geo;
-  if (G.dim != 2) return false;
+  if (G.dim != 2 || G.nbo > 3) return false;
   if (G.m_pad == 32 && G.nG_pad == 128) launch_schur2d<32, 128>(c, sub0, cnt, Wd, Wo, E, s);
   else if (G.m_pad == 16 && G.nG_pad == 64) launch_schur2d<16, 64>(c, sub0, cnt, Wd, Wo, E, s);
   else if (G.m_pad == 8 && G.nG_pad == 32) launch_schur2d<8, 32>(c, sub0, cnt, Wd, Wo, E, s);
