@@ -156,9 +156,9 @@ def phase_work(op, pb, its):
     # + vector gather / scatter (as stored: li_stride doubles per subdomain)
     li = nblk * T(lay.m_pad) + nblk * lay.m_pad * (1 if pb["mesh"].element == "p1" else 3 ** (lay.dim - 1))
     w["apply.bt_solve"] = ("hbm", 8.0 * (2 * nsub * li + 2 * nsub * nI))
-    # local Gamma phase 1: L_S forward + backward (lower), Phi^T rho
-    w["apply.gamma1"] = ("hbm", 8.0 * float(np.sum(2 * T(nG) + nG * nc)))
-    w["apply.gamma2"] = ("hbm", 8.0 * float(np.sum(nG * nc)))
+    # local Gamma phase 1: T rho (explicit interface operator, nG_pad^2) + Phi^T rho
+    w["apply.gamma1"] = ("hbm", 8.0 * nsub * (lay.nG_pad ** 2 + lay.nG_pad * op.plan.nc_pad))
+    w["apply.gamma2"] = ("hbm", 8.0 * nsub * lay.nG_pad * op.plan.nc_pad)
     cp = op.plan.coarse
     if cp is not None:
         w["apply.coarse"] = ("hbm", 8.0 * 2 * cp.factor_entries())
@@ -170,6 +170,8 @@ def phase_work(op, pb, its):
     w["setup.E"] = ("fp64", nsub * (max(nblk - 1, 0) * 2 * m * m * nG + nblk * m * m * nG))
     w["setup.SG"] = ("fp64", nsub * nG * (nG + 1) * nI)
     w["setup.SK"] = ("fp64", nsub * nG**3 / 3)
+    ng, ncp = lay.nG_pad, op.plan.nc_pad
+    w["setup.T"] = ("fp64", nsub * (ng**3 / 3 + 2 * ng**3 + 2 * ng * ncp * ncp + 2 * ng * ng * ncp))
     w["setup.Phi"] = ("fp64", float(np.sum(2 * nG * nG * nc + 2 * nG * nc * nc + nc**3 / 3
                                            + 2 * nG * nG * nc + 2 * nG * nc * nc)))
     w["setup.btchol"] = ("fp64", nsub * nblk * (m**3 / 3 + 2 * m**3))
@@ -237,7 +239,7 @@ def run_ours(args, rank, world, local_rank):
     phases = {}
     for name in ("apply.bt_solve", "apply.gamma1", "apply.coarse", "apply.gamma2", "setup.assemble",
                  "setup.schur", "setup.btchol", "setup.E", "setup.SG", "setup.SK", "setup.Phi",
-                 "setup.coarse", "pcg.spmv_dot"):
+                 "setup.T", "setup.coarse", "pcg.spmv_dot"):
         cnt = C.c_longlong()
         ms = lib.bddc_profile_read(ctx, name.encode(), C.byref(cnt))
         if cnt.value:

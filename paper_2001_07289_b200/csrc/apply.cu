@@ -213,26 +213,23 @@ __device__ double block_sum(double v, double* red) {
   return s;
 }
 
-// Per subdomain: rho = D rp_Gamma; q = c Phi^T rho; u = S_K^{-1} rho; t = C u.
+// Per subdomain: rho = D rp_Gamma;  q = c Phi^T rho (coarse rhs);  v = T rho, with the
+// explicit interface operator T = (I - Phi C) S_K^{-1} (the constrained Neumann solve on
+// Gamma, bddc.py:357; symmetric, built in setup).
 __global__ void __launch_bounds__(128) local_gamma1_kernel(Geometry G, SubTables st,
-                                                           const double* __restrict__ LS,
+                                                           const double* __restrict__ T,
                                                            const double* __restrict__ Phi,
                                                            const double* __restrict__ cscale,
                                                            const double* __restrict__ rpg,
-                                                           double* qloc, double* uloc,
-                                                           double* tloc) {
+                                                           double* qloc, double* vloc) {
   extern __shared__ double sm[];
   const int n = G.nG_pad, nc = G.nc_pad;
-  double* u = sm;          // n
-  double* rho = sm + n;    // n
-  __shared__ double red[32];
+  double* rho = sm;  // n
   const int sub = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   const long long so = (long long)sub * n;
   for (int s = tid; s < n; s += nt) {
     const int g = st.slot_gamma[so + s];
-    const double v = g >= 0 ? st.slot_w[so + s] * rpg[g] : 0.0;
-    rho[s] = v;
-    u[s] = v;
+    rho[s] = g >= 0 ? st.slot_w[so + s] * rpg[g] : 0.0;
   }
   __syncthreads();
   const double c = cscale[sub];
@@ -244,39 +241,25 @@ __global__ void __launch_bounds__(128) local_gamma1_kernel(Geometry G, SubTables
     acc = warp_sum(acc);
     if (lane == 0) qloc[(long long)sub * nc + k] = c * acc;
   }
-  // forward: L u = rho (column oriented)
-  const double* L = LS + (long long)sub * n * n;
-  for (int k = 0; k < n; ++k) {
-    if (tid == 0) u[k] /= L[k + (long long)k * n];
-    __syncthreads();
-    const double uk = u[k];
-    for (int i = k + 1 + tid; i < n; i += nt) u[i] -= L[i + (long long)k * n] * uk;
-    __syncthreads();
-  }
-  // backward: L^T u = y (dot form over column k)
-  for (int k = n - 1; k >= 0; --k) {
-    double part = 0.0;
-    for (int i = k + 1 + tid; i < n; i += nt) part += L[i + (long long)k * n] * u[i];
-    const double tot = block_sum(part, red);
-    if (tid == 0) u[k] = (u[k] - tot) / L[k + (long long)k * n];
-    __syncthreads();
-  }
-  for (int s = tid; s < n; s += nt) uloc[so + s] = u[s];
-  for (int k = tid; k < nc; k += nt) {
-    double acc = 0.0;
-    for (int s = 0; s < n; ++s)
-      if (st.slot_con[so + s] == k) acc += st.slot_coef[so + s] * u[s];
-    tloc[(long long)sub * nc + k] = acc;
+  const double* Ts = T + (long long)sub * n * n;
+  for (int i = tid; i < n; i += nt) {
+    double a0 = 0.0, a1 = 0.0;
+    int k = 0;
+    for (; k + 1 < n; k += 2) {
+      a0 += Ts[i + (long long)k * n] * rho[k];
+      a1 += Ts[i + (long long)(k + 1) * n] * rho[k + 1];
+    }
+    if (k < n) a0 += Ts[i + (long long)k * n] * rho[k];
+    vloc[so + i] = a0 + a1;
   }
 }
 
-// Per subdomain: e = c * csol[coarse] - t;  w = D (u + Phi e)
+// Per subdomain: w = D (v + c Phi csol[coarse])
 __global__ void __launch_bounds__(128) local_gamma2_kernel(Geometry G, SubTables st,
                                                            const double* __restrict__ Phi,
                                                            const double* __restrict__ cscale,
                                                            const double* __restrict__ csol,
-                                                           const double* __restrict__ uloc,
-                                                           const double* __restrict__ tloc,
+                                                           const double* __restrict__ vloc,
                                                            double* wloc) {
   __shared__ double e[1024];
   const int n = G.nG_pad, nc = G.nc_pad;
@@ -284,13 +267,13 @@ __global__ void __launch_bounds__(128) local_gamma2_kernel(Geometry G, SubTables
   const double c = cscale[sub];
   for (int k = tid; k < nc; k += nt) {
     const int j = st.con_coarse[(long long)sub * nc + k];
-    e[k] = j >= 0 ? c * csol[j] - tloc[(long long)sub * nc + k] : 0.0;
+    e[k] = j >= 0 ? c * csol[j] : 0.0;
   }
   __syncthreads();
   const double* ph = Phi + (long long)sub * n * nc;
   const long long so = (long long)sub * n;
   for (int s = tid; s < n; s += nt) {
-    double acc = uloc[so + s];
+    double acc = vloc[so + s];
     for (int k = 0; k < nc; ++k) acc += ph[s + (long long)k * n] * e[k];
     wloc[so + s] = st.slot_w[so + s] * acc;
   }
@@ -377,10 +360,10 @@ void apply_bddc(Ctx& c, const double* r, double* z, cudaStream_t s) {
     else
       { gamma_residual_kernel<3><<<ceil_div(c.n_gamma, th), th, 0, s>>>(G, c.n_gamma, c.gamma_dof, c.alpha, r, c.v1, c.rpg); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
-    const size_t smem1 = sizeof(double) * 2 * G.nG_pad;
+    const size_t smem1 = sizeof(double) * G.nG_pad;
     c.prof.begin("apply.gamma1", s);
     { local_gamma1_kernel<<<G.nsub, 128, smem1, s>>>(G, c.st, c.LS, c.Phi, c.cscale, c.rpg, c.qloc,
-                                                   c.uloc, c.tloc); BDDC_COUNT(); }
+                                                   c.uloc); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
     c.prof.end("apply.gamma1", s);
     if (c.fp.n_coarse > 0) {
@@ -391,7 +374,7 @@ void apply_bddc(Ctx& c, const double* r, double* z, cudaStream_t s) {
       coarse_solve(c, c.crhs, c.csol, s);
     }
     c.prof.begin("apply.gamma2", s);
-    { local_gamma2_kernel<<<G.nsub, 128, 0, s>>>(G, c.st, c.Phi, c.cscale, c.csol, c.uloc, c.tloc,
+    { local_gamma2_kernel<<<G.nsub, 128, 0, s>>>(G, c.st, c.Phi, c.cscale, c.csol, c.uloc,
                                                c.wloc); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
     c.prof.end("apply.gamma2", s);

@@ -239,6 +239,13 @@ __global__ void build_ct_kernel(Geometry G, int sub0, SubTables st, double* Gm) 
   }
 }
 
+// B = I (n x n, per batch entry)
+__global__ void identity_kernel(double* B, int n, long long stride) {
+  double* b = B + (long long)blockIdx.x * stride;
+  for (long long idx = threadIdx.x; idx < (long long)n * n; idx += blockDim.x)
+    b[idx] = (idx % n == idx / n) ? 1.0 : 0.0;
+}
+
 // identity on padded constraints of S_C
 __global__ void sc_pad_kernel(Geometry G, int sub0, SubTables st, double* SC) {
   const int b = blockIdx.x, sub = sub0 + b;
@@ -271,7 +278,7 @@ size_t local_setup_workspace(const Geometry& g, int chunk) {
   const size_t SG = (size_t)g.nG_pad * g.nG_pad;
   const size_t X = (size_t)g.nG_pad * g.nc_pad;
   const size_t SC = (size_t)g.nc_pad * g.nc_pad;
-  return (size_t)chunk * (E + SG + X + 2 * SC);
+  return (size_t)chunk * (E + SG + X + 3 * SC);
 }
 
 void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
@@ -299,6 +306,7 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
     double* X = SG + (size_t)chunk * lsS;
     double* SC = X + (size_t)chunk * phS;
     double* P = SC + (size_t)chunk * scS;
+    double* SCc = P + (size_t)chunk * scS;  // S_C before its factorization
     double* LS = c.LS + sub0 * lsS;
     double* PH = c.Phi + sub0 * phS;
     BDDC_CUDA(cudaMemsetAsync(Wd, 0, sizeof(double) * 2 * (size_t)chunk * wS, s));
@@ -364,6 +372,7 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
       gemm_batched(true, false, G.nc_pad, G.nc_pad, G.nG_pad, 1.0, PHb, PHb, 0.0, SCb, cnt, s);
       { sc_pad_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, SC); BDDC_COUNT(); }
       BDDC_LAUNCH_CHECK();
+      BDDC_CUDA(cudaMemcpyAsync(SCc, SC, sizeof(double) * cnt * scS, cudaMemcpyDeviceToDevice, s));
       potrf_batched(SCb, G.nc_pad, G.nc_pad, cnt, nullptr, c.tinv, s);
       trsm_batched(TRSM_RLT, SCb, G.nc_pad, PHb, G.nG_pad, cnt, c.tinv, s);
       trsm_batched(TRSM_RLN, SCb, G.nc_pad, PHb, G.nG_pad, cnt, c.tinv, s);
@@ -377,6 +386,16 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
       { finish_local_kernel<<<cnt, 256, 0, s>>>(G, sub0, c.coarse_scaling, c.diag_s, c.cscale, P,
                                               c.Sloc); BDDC_COUNT(); }
       BDDC_LAUNCH_CHECK();
+      // 7. explicit interface operator T = (I - Phi C) S_K^{-1} = S_K^{-1} - Phi S_C Phi^T
+      //    (symmetric; replaces L_S so the apply's local Neumann solve is one GEMV)
+      PhaseScope pt(c.prof, "setup.T", s);
+      { identity_kernel<<<cnt, 256, 0, s>>>(SG, G.nG_pad, lsS); BDDC_COUNT(); }
+      BDDC_LAUNCH_CHECK();
+      trsm_batched(TRSM_LLN, LSb, G.nG_pad, SGb, G.nG_pad, cnt, c.tinv, s);  // SG <- L_S^{-1}
+      gemm_batched(true, false, G.nG_pad, G.nG_pad, G.nG_pad, 1.0, SGb, SGb, 0.0, LSb, cnt, s);
+      BMat SCcb{SCc, scS, G.nc_pad};
+      gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nc_pad, 1.0, PHb, SCcb, 0.0, Xb, cnt, s);
+      gemm_batched(false, true, G.nG_pad, G.nG_pad, G.nc_pad, -1.0, Xb, PHb, 1.0, LSb, cnt, s);
     }
   }
 }
