@@ -237,9 +237,11 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     clocks = sampler.stop()
     phases = {}
-    for name in ("apply.bt_solve", "apply.gamma1", "apply.coarse", "apply.gamma2", "setup.assemble",
-                 "setup.schur", "setup.btchol", "setup.E", "setup.SG", "setup.SK", "setup.Phi",
-                 "setup.T", "setup.coarse", "pcg.spmv_dot"):
+    names = ("apply.bt_solve", "apply.gamma1", "apply.coarse", "apply.gamma2", "setup.assemble",
+             "setup.schur", "setup.btchol", "setup.E", "setup.SG", "setup.SK", "setup.Phi",
+             "setup.T", "setup.coarse", "pcg.spmv_dot", "coarse.inverse") + tuple(
+                 f"coarse.L{l:02d}" for l in range(20))
+    for name in names:
         cnt = C.c_longlong()
         ms = lib.bddc_profile_read(ctx, name.encode(), C.byref(cnt))
         if cnt.value:

@@ -12,6 +12,10 @@
 
 using namespace bddc;
 
+namespace bddc {
+void coop_release(const Ctx& c);
+}
+
 struct bddc_ctx {
   Ctx c;
   cudaEvent_t ev[8] = {};
@@ -382,6 +386,7 @@ int bddc_create(int device, bddc_ctx** out) {
 
 void bddc_destroy(bddc_ctx* h) {
   if (!h) return;
+  bddc::coop_release(h->c);
   cudaSetDevice(h->c.device);
   cudaStreamSynchronize(h->c.stream);
   h->c.free_all();

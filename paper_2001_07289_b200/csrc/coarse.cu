@@ -10,6 +10,10 @@
 
 namespace bddc {
 
+void coop_build(Ctx& c);
+void coop_factor(Ctx& c, cudaStream_t s);
+void coop_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s);
+
 namespace {
 
 __global__ void csr_segsum_kernel(long long nnz, const long long* __restrict__ seg,
@@ -415,6 +419,7 @@ void build_level_schedule(Ctx& c) {
   ls.gat_ptr = c.upload<int>(gptr.data(), gptr.size());
   ls.gat_off = c.upload<long long>(goff.data(), goff.size());
   ls.gat_src = c.upload<int>(gsrc.data(), std::max<size_t>(gsrc.size(), 1));
+  coop_build(c);
 }
 
 void coarse_assemble_and_factor(Ctx& c) {
@@ -432,70 +437,12 @@ void coarse_assemble_and_factor(Ctx& c) {
   { csr_to_front_kernel<<<std::min<long long>((fp.nnz + th - 1) / th, 148 * 16), th, 0, s>>>(
       fp.nnz, fp.csr_front_pos, fp.csr_val, fd.fronts); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
-  for (int l = 0; l < fp.nlevels; ++l) {
-    const int nn = ls.nodes_off[l + 1] - ls.nodes_off[l];
-    const int* nodes = ls.d_nodes + ls.nodes_off[l];
-    if (l > 0) {
-      for (int k = 0; k < ls.max_children; ++k) {
-        dim3 grid(64, nn);
-        { extend_add_kernel<<<grid, 256, 0, s>>>(nodes, k, fd.child_ptr, fd.child_list,
-                                               fd.sep_size, fd.bnd_size, fd.ld,
-                                               fd.front_off, fd.rmap, fd.rmap_ptr, fd.fronts); BDDC_COUNT(); }
-        BDDC_LAUNCH_CHECK();
-      }
-    }
-    auto run_step = [&](const LevelSchedule::Step& st, bool lower_gemm, bool trans_ts) {
-      if (st.n_potrf) {
-        TileArgs pa;
-        pa.tasks = st.potrf; pa.count = st.n_potrf; pa.info = fp.info;
-        potrf_tile(pa, s);
-      }
-      if (st.n_trtri) {
-        TileArgs ta;
-        ta.tasks = st.trtri; ta.count = st.n_trtri;
-        trtri_tile(ta, s);
-      }
-      if (st.n_tsolve) {
-        GemmArgs ga;
-        ga.tasks = st.tsolve; ga.count = st.n_tsolve; ga.max_M = st.ts_M; ga.max_N = st.ts_N;
-        ga.alpha = 1.0; ga.beta = 0.0;
-        gemm(ga, false, trans_ts, s);
-      }
-      if (st.n_gemm) {
-        GemmArgs ga;
-        ga.tasks = st.gemm; ga.count = st.n_gemm; ga.max_M = st.g_M; ga.max_N = st.g_N;
-        ga.alpha = -1.0; ga.beta = 1.0; ga.lower = lower_gemm ? 1 : 0;
-        gemm(ga, false, lower_gemm, s);
-      }
-    };
-    for (const auto& st : ls.steps[l]) run_step(st, true, true);
-    // partitioned inverse of the factored panels of this level
-    if (ls.n_inv_prep[l]) {
-      dim3 grid(32, ls.n_inv_prep[l]);
-      { inv_prep_kernel<<<grid, 256, 0, s>>>(ls.inv_prep[l], fd, ls.inv_scratch); BDDC_COUNT(); }
-      BDDC_LAUNCH_CHECK();
-    }
-    for (const auto& st : ls.inv_steps[l]) run_step(st, false, false);
-  }
+  // multifrontal factorization + partitioned inverse: one cooperative launch
+  coop_factor(c, s);
 }
 
 void coarse_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s) {
-  FrontPlan& fp = c.fp;
-  FrontDev& fd = fp.d;
-  LevelSchedule& ls = c.sched;
-  LevelView lv{ls.gat_ptr, ls.gat_off, ls.gat_src};
-  for (int l = 0; l < fp.nlevels; ++l) {
-    if (!ls.n_fwd_r[l]) continue;
-    if (ls.n_fwd_t[l]) { cs_fwd_partial_kernel<<<ls.n_fwd_t[l], 256, 0, s>>>(ls.fwd_t[l], fd, lv, rhs, ls.partial); BDDC_COUNT(); }
-    { cs_fwd_reduce_kernel<<<ls.n_fwd_r[l], 64, 0, s>>>(ls.fwd_r[l], fd, lv, ls.partial, sol); BDDC_COUNT(); }
-    BDDC_LAUNCH_CHECK();
-  }
-  for (int l = fp.nlevels - 1; l >= 0; --l) {
-    if (!ls.n_bwd_r[l]) continue;
-    { cs_bwd_partial_kernel<<<ls.n_bwd_t[l], 256, 0, s>>>(ls.bwd_t[l], fd, sol, ls.partial); BDDC_COUNT(); }
-    { cs_bwd_reduce_kernel<<<ls.n_bwd_r[l], 64, 0, s>>>(ls.bwd_r[l], fd, ls.partial, sol); BDDC_COUNT(); }
-    BDDC_LAUNCH_CHECK();
-  }
+  coop_solve(c, rhs, sol, s);
 }
 
 }  // namespace bddc

@@ -1,0 +1,492 @@
+// Cooperative (persistent, grid-synchronised) coarse engine.
+//
+// The top of the nested-dissection tree has few, large fronts: run level by level as
+// separate launches, each 64-column panel step is a chain of small, latency-bound kernels.
+// Here the whole multifrontal factorization and the whole coarse solve each run as ONE
+// cooperative launch (all CTAs co-resident, grid.sync() between phases), executing a
+// host-built program of phases; each phase is a list of independent tile tasks spread over
+// all CTAs. Per level l:
+//   EA(k)            extend-add child k's update block into the front
+//   per panel p:     PT   potrf + trtri of the diagonal tile (inverse -> scratch)
+//                    TS   L21 tile <- A21 tile inv^T                   | X1  Y = L[k,0:k] X[0:k,0:k]
+//                    SY   A22 tile -= L21 L21^T (lower)                | X2  X[k,0:k] = -inv Y ; X[k,k] = inv
+//   W                W21 = L21 X   (X = L11^{-1}, accumulated left-looking by X1/X2)
+//   CB               panel <- [X; W21]   (partitioned inverse, see coarse.cu)
+// The solve program: per level forward GEMV tiles, reduction; then backward likewise.
+#include <cooperative_groups.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+
+#include "bddc_internal.cuh"
+#include "tile_ops.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace bddc {
+
+enum CoopType : int {
+  CT_EA = 0, CT_PT = 1, CT_TS = 2, CT_X1 = 3, CT_SY = 4, CT_X2 = 5, CT_W = 6, CT_CB = 7,
+};
+
+struct CoopTask {
+  int type, node, a, b, arg;
+};
+
+struct CoopPhase {
+  int t0, nt;
+};
+
+struct CoopScratch {  // per-node offsets (doubles) into the scratch pool
+  long long* inv;
+  long long* X;
+  long long* Y;
+  long long* W;
+  int* ldx;   // leading dimension of X (even)
+  int* ldw;   // leading dimension of W (even)
+};
+
+struct CoopProgram {
+  const CoopTask* tasks;
+  const CoopPhase* phases;
+  int nphases;
+  CoopScratch sc;
+  double* pool;
+};
+
+namespace {
+
+using namespace tile;
+
+__device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgram& pg, int* info,
+                         double* smem) {
+  const int node = t.node;
+  const int s = fd.sep_size[node], f = s + fd.bnd_size[node], ld = fd.ld[node];
+  double* F = fd.fronts + fd.front_off[node];
+  double* X = pg.pool + pg.sc.X[node];
+  const int ldx = pg.sc.ldx[node];
+  switch (t.type) {
+    case CT_EA: {  // child #arg of node, columns [8a, 8a+8) of its lower update block
+      const int c0 = fd.child_ptr[node];
+      const int ch = fd.child_list[c0 + t.arg];
+      const int b = fd.bnd_size[ch], sc = fd.sep_size[ch], lc = fd.ld[ch];
+      const double* U = fd.fronts + fd.front_off[ch] + sc + (long long)sc * lc;
+      const int* rm = fd.rmap + fd.rmap_ptr[ch];
+      for (int j = t.a * 8; j < min(b, t.a * 8 + 8); ++j) {
+        double* Fc = F + (long long)rm[j] * ld;
+        const double* Uc = U + (long long)j * lc;
+        for (int i = j + threadIdx.x; i < b; i += blockDim.x) Fc[rm[i]] += Uc[i];
+      }
+      break;
+    }
+    case CT_PT: {  // factor + invert diagonal tile of panel arg
+      const int k = t.arg * kTile, nb = min(kTile, s - k);
+      double* inv = pg.pool + pg.sc.inv[node] + (t.arg & 1) * kTileInvStride;
+      const int bad = potrf_trtri_tile(F + k + (long long)k * ld, ld, nb, inv, smem);
+      if (threadIdx.x == 0 && bad >= 0) atomicMin(info + node, fd.sep_start[node] + k + bad);
+      break;
+    }
+    case CT_TS: {  // rows (k+nb) + 64a.. of the panel: L21 <- A21 inv^T (in place)
+      const int k = t.arg * kTile, nb = min(kTile, s - k), rest = f - k - nb;
+      double* A21 = F + (k + nb) + (long long)k * ld;
+      const double* inv = pg.pool + pg.sc.inv[node] + (t.arg & 1) * kTileInvStride;
+      gemm_tile<false, true>(A21, ld, inv, kTile, A21, ld, rest, nb, nb, t.a * kTile, 0, 1.0, 0.0,
+                             false, smem);
+      break;
+    }
+    case CT_X1: {  // Y[:, c] = L[k.., c*64 .. k) X[c*64 .. k, c]   (c = a)
+      const int k = t.arg * kTile, nb = min(kTile, s - k), c = t.a * kTile;
+      double* Y = pg.pool + pg.sc.Y[node];
+      gemm_tile<false, false>(F + k + (long long)c * ld, ld, X + c + (long long)c * ldx, ldx,
+                              Y + (long long)c * kTile, kTile, nb, min(kTile, k - c), k - c, 0, 0,
+                              1.0, 0.0, false, smem);
+      break;
+    }
+    case CT_SY: {  // trailing tile (a, b) of A22 -= L21 L21^T; tile (0,0) + lookahead:
+      const int k = t.arg * kTile, nb = min(kTile, s - k), rest = f - k - nb;
+      double* L21 = F + (k + nb) + (long long)k * ld;
+      double* A22 = F + (k + nb) + (long long)(k + nb) * ld;
+      gemm_tile<false, true>(L21, ld, L21, ld, A22, ld, rest, rest, nb, t.a * kTile, t.b * kTile,
+                             -1.0, 1.0, true, smem);
+      if (t.a == 0 && t.b == 0 && k + nb < s) {  // factor the next panel's diagonal tile now
+        __syncthreads();
+        const int k1 = k + nb, nb1 = min(kTile, s - k1);
+        double* inv1 = pg.pool + pg.sc.inv[node] + ((t.arg + 1) & 1) * kTileInvStride;
+        const int bad = potrf_trtri_tile(F + k1 + (long long)k1 * ld, ld, nb1, inv1, smem);
+        if (threadIdx.x == 0 && bad >= 0) atomicMin(info + node, fd.sep_start[node] + k1 + bad);
+      }
+      break;
+    }
+    case CT_X2: {  // X[k.., c] = -inv Y[:, c] (c < panel) or X[k.., k..] = inv
+      const int k = t.arg * kTile, nb = min(kTile, s - k), c = t.a * kTile;
+      const double* inv = pg.pool + pg.sc.inv[node] + (t.arg & 1) * kTileInvStride;
+      if (c < k) {
+        const double* Y = pg.pool + pg.sc.Y[node];
+        gemm_tile<false, false>(inv, kTile, Y + (long long)c * kTile, kTile, X + k + (long long)c * ldx,
+                                ldx, nb, kTile, nb, 0, 0, -1.0, 0.0, false, smem);
+      } else {
+        for (int idx = threadIdx.x; idx < nb * nb; idx += blockDim.x) {
+          const int i = idx % nb, j = idx / nb;
+          X[(k + i) + (long long)(k + j) * ldx] = inv[i + j * kTile];
+        }
+      }
+      break;
+    }
+    case CT_W: {  // W21 tile (a, c) = L21[a, c*64..s) X[c*64..s, c]
+      const int b = f - s, c = t.b * kTile;
+      double* W = pg.pool + pg.sc.W[node];
+      const int ldw = pg.sc.ldw[node];
+      gemm_tile<false, false>(F + s + (long long)c * ld, ld, X + c + (long long)c * ldx, ldx,
+                              W + (long long)c * ldw, ldw, b, min(kTile, s - c), s - c, t.a * kTile, 0,
+                              1.0, 0.0, false, smem);
+      break;
+    }
+    case CT_CB: {  // panel <- [X; W21], chunk a of 4096 entries of the f x s panel
+      const long long total = (long long)f * s;
+      const long long e0 = (long long)t.a * 4096, e1 = min(total, e0 + 4096);
+      const double* W = pg.pool + pg.sc.W[node];
+      const int ldw = pg.sc.ldw[node];
+      for (long long idx = e0 + threadIdx.x; idx < e1; idx += blockDim.x) {
+        const int i = (int)(idx % f), j = (int)(idx / f);
+        double v;
+        if (i < s) v = i >= j ? X[i + (long long)j * ldx] : 0.0;
+        else v = W[(i - s) + (long long)j * ldw];
+        F[i + (long long)j * ld] = v;
+      }
+      break;
+    }
+  }
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(128) coop_factor_kernel(FrontDev fd, CoopProgram pg, int* info,
+                                                          unsigned long long* ptime) {
+  extern __shared__ __align__(16) double smem[];
+  cg::grid_group grid = cg::this_grid();
+  for (int ph = 0; ph < pg.nphases; ++ph) {
+    const CoopPhase P = pg.phases[ph];
+    for (int t = blockIdx.x; t < P.nt; t += gridDim.x) {
+      const CoopTask task = pg.tasks[P.t0 + t];
+      run_task(task, fd, pg, info, smem);
+      __syncthreads();
+    }
+    grid.sync();
+    if (ptime && blockIdx.x == 0 && threadIdx.x == 0) ptime[ph] = gtimer();
+  }
+}
+
+// ---- cooperative coarse solve ----
+struct SolveProgram {
+  const CsTask* ft;
+  const CsTask* bt;
+  const CsRed* fr;
+  const CsRed* br;
+  const int* ft_off;  // [L+1]
+  const int* bt_off;
+  const int* fr_off;
+  const int* br_off;
+  int nlevels;
+};
+
+__device__ __forceinline__ double gather_children_c(const LevelView& lv, const double* __restrict__ upd,
+                                                    int node, int pos) {
+  const int* gp = lv.gat_ptr + lv.gat_off[node];
+  double acc = 0.0;
+  for (int q = gp[pos]; q < gp[pos + 1]; ++q) acc += upd[lv.gat_src[q]];
+  return acc;
+}
+
+__global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView lv, SolveProgram sp,
+                                                         const double* __restrict__ rhs,
+                                                         double* __restrict__ sol,
+                                                         double* __restrict__ partial) {
+  __shared__ double vs[256];
+  __shared__ double red[4][64];
+  cg::grid_group grid = cg::this_grid();
+  const int tid = threadIdx.x;
+  // forward: levels bottom-up
+  for (int l = 0; l < sp.nlevels; ++l) {
+    for (int ti = sp.ft_off[l] + blockIdx.x; ti < sp.ft_off[l + 1]; ti += gridDim.x) {
+      const CsTask t = sp.ft[ti];
+      const int node = t.node, s = fd.sep_size[node], f = s + fd.bnd_size[node];
+      const long long ld = fd.ld[node];
+      const int s0 = fd.sep_start[node];
+      const double* F = fd.fronts + fd.front_off[node];
+      __syncthreads();
+      {
+        const int kk = t.c0 + tid;
+        vs[tid] = kk < s ? rhs[s0 + kk] + gather_children_c(lv, fd.upd, node, kk) : 0.0;
+      }
+      __syncthreads();
+      const int rr = tid & 63, grp = tid >> 6;
+      const int r = t.r0 + rr;
+      double a0 = 0.0, a1 = 0.0;
+      if (r < f) {
+        const int kb = t.c0 + grp * 64;
+        int ke = min(kb + 64, s);
+        if (r < s) ke = min(ke, r + 1);
+        int k = kb;
+        for (; k + 1 < ke; k += 2) {
+          a0 += F[r + k * ld] * vs[k - t.c0];
+          a1 += F[r + (k + 1) * ld] * vs[k + 1 - t.c0];
+        }
+        if (k < ke) a0 += F[r + k * ld] * vs[k - t.c0];
+      }
+      red[grp][rr] = a0 + a1;
+      __syncthreads();
+      if (tid < 64)
+        partial[(long long)t.part * 64 + tid] = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
+    }
+    grid.sync();
+    for (int ti = sp.fr_off[l] + blockIdx.x * 4 + (tid >> 6); ti < sp.fr_off[l + 1]; ti += gridDim.x * 4) {
+      const CsRed t = sp.fr[ti];
+      const int node = t.node, s = fd.sep_size[node], f = s + fd.bnd_size[node];
+      const int lt = tid & 63, r = t.t0 + lt;
+      if (r < f) {
+        double acc = 0.0;
+        for (int p = 0; p < t.np; ++p) acc += partial[(long long)(t.p0 + p) * 64 + lt];
+        if (r < s) sol[fd.sep_start[node] + r] = acc;
+        else fd.upd[fd.upd_off[node] + (r - s)] = gather_children_c(lv, fd.upd, node, r) - acc;
+      }
+    }
+    grid.sync();
+  }
+  // backward: levels top-down
+  for (int l = sp.nlevels - 1; l >= 0; --l) {
+    for (int ti = sp.bt_off[l] + blockIdx.x; ti < sp.bt_off[l + 1]; ti += gridDim.x) {
+      const CsTask t = sp.bt[ti];
+      const int node = t.node, s = fd.sep_size[node], f = s + fd.bnd_size[node];
+      const long long ld = fd.ld[node];
+      const int s0 = fd.sep_start[node];
+      const int* bidx = fd.bnd_idx + fd.bnd_ptr[node];
+      const double* F = fd.fronts + fd.front_off[node];
+      __syncthreads();
+      {
+        const int r = t.r0 + tid;
+        vs[tid] = r < s ? sol[s0 + r] : (r < f ? -sol[bidx[r - s]] : 0.0);
+      }
+      __syncthreads();
+      const int lane = tid & 31, warp = tid >> 5;
+      for (int cc = 0; cc < 8; ++cc) {
+        const int kl = warp * 8 + cc, k = t.c0 + kl;
+        double acc = 0.0;
+        if (k < s) {
+          const double* col = F + k * ld;
+          for (int i = lane; i < 256; i += 32) {
+            const int r = t.r0 + i;
+            if (r < f && (r >= s || r >= k)) acc += col[r] * vs[i];
+          }
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) partial[(long long)t.part * 64 + kl] = acc;
+      }
+    }
+    grid.sync();
+    for (int ti = sp.br_off[l] + blockIdx.x * 4 + (tid >> 6); ti < sp.br_off[l + 1]; ti += gridDim.x * 4) {
+      const CsRed t = sp.br[ti];
+      const int node = t.node, s = fd.sep_size[node];
+      const int lt = tid & 63, k = t.t0 + lt;
+      if (k < s) {
+        double acc = 0.0;
+        for (int p = 0; p < t.np; ++p) acc += partial[(long long)(t.p0 + p) * 64 + lt];
+        sol[fd.sep_start[node] + k] = acc;
+      }
+    }
+    grid.sync();
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------
+// host: program construction and launches
+// ---------------------------------------------------------------------------------------
+
+struct CoopState {
+  std::vector<int> phase_type;  // first task type of each phase (diagnostics)
+  unsigned long long* ptime = nullptr;
+  CoopProgram pg{};
+  SolveProgram sp{};
+  int grid_f = 0, grid_s = 0;
+  size_t smem_f = 0;
+};
+
+static std::map<const Ctx*, CoopState> g_coop;
+
+void coop_build(Ctx& c) {
+  FrontPlan& fp = c.fp;
+  LevelSchedule& ls = c.sched;
+  CoopState& st = g_coop[&c];
+  st = CoopState{};
+  const int N = fp.nnodes, L = fp.nlevels;
+  std::vector<CoopTask> tasks;
+  std::vector<CoopPhase> phases;
+  std::vector<long long> inv(N, 0), X(N, 0), Y(N, 0), W(N, 0);
+  std::vector<int> ldx(N, 2), ldw(N, 2);
+  long long pool = 2;
+  auto phase_begin = [&]() { phases.push_back(CoopPhase{(int)tasks.size(), 0}); };
+  auto phase_end = [&]() {
+    phases.back().nt = (int)tasks.size() - phases.back().t0;
+    if (phases.back().nt == 0) phases.pop_back();
+  };
+  for (int l = 0; l < L; ++l) {
+    std::vector<int> nodes(fp.level_list.begin() + fp.level_ptr[l], fp.level_list.begin() + fp.level_ptr[l + 1]);
+    // scratch for this level (reused by the next level after its CB phase)
+    long long off = 0;
+    int max_np = 0, max_ch = 0;
+    for (int nd : nodes) {
+      const int s = fp.sep_size[nd], b = fp.bnd_size[nd];
+      ldx[nd] = (int)round_up(std::max(s, 2), 2);
+      ldw[nd] = (int)round_up(std::max(b, 2), 2);
+      inv[nd] = off; off += 2 * kTileInvStride;
+      X[nd] = off; off += round_up((long long)ldx[nd] * std::max(s, 1), 2);
+      Y[nd] = off; off += round_up((long long)kTile * std::max(s, 1), 2);
+      W[nd] = off; off += round_up((long long)ldw[nd] * std::max(s, 1), 2);
+      max_np = std::max(max_np, ceil_div(s, kTile));
+      max_ch = std::max(max_ch, fp.child_ptr[nd + 1] - fp.child_ptr[nd]);
+    }
+    pool = std::max(pool, off);
+    for (int k = 0; k < max_ch; ++k) {
+      phase_begin();
+      for (int nd : nodes) {
+        if (fp.child_ptr[nd + 1] - fp.child_ptr[nd] <= k) continue;
+        const int ch = fp.child_list[fp.child_ptr[nd] + k];
+        for (int q = 0; q < ceil_div(fp.bnd_size[ch], 8); ++q) tasks.push_back(CoopTask{CT_EA, nd, q, 0, k});
+      }
+      phase_end();
+    }
+    for (int p = 0; p < max_np; ++p) {
+      if (p == 0) {  // later diagonal tiles are factored by the lookahead in SY(p-1)
+        phase_begin();
+        for (int nd : nodes)
+          if (fp.sep_size[nd] > 0) tasks.push_back(CoopTask{CT_PT, nd, 0, 0, 0});
+        phase_end();
+      }
+      phase_begin();
+      for (int nd : nodes) {
+        const int s = fp.sep_size[nd], f = s + fp.bnd_size[nd];
+        if (s <= p * kTile) continue;
+        const int k = p * kTile, nb = std::min(kTile, s - k), rest = f - k - nb;
+        for (int a = 0; a < ceil_div(rest, kTile); ++a) tasks.push_back(CoopTask{CT_TS, nd, a, 0, p});
+        for (int cc = 0; cc < p; ++cc) tasks.push_back(CoopTask{CT_X1, nd, cc, 0, p});
+      }
+      phase_end();
+      phase_begin();
+      for (int nd : nodes) {
+        const int s = fp.sep_size[nd], f = s + fp.bnd_size[nd];
+        if (s <= p * kTile) continue;
+        const int k = p * kTile, nb = std::min(kTile, s - k), rest = f - k - nb;
+        const int nt = ceil_div(rest, kTile);
+        for (int a = 0; a < nt; ++a)
+          for (int b = 0; b <= a; ++b) tasks.push_back(CoopTask{CT_SY, nd, a, b, p});
+        (void)0;
+        for (int cc = 0; cc <= p; ++cc) tasks.push_back(CoopTask{CT_X2, nd, cc, 0, p});
+      }
+      phase_end();
+    }
+    phase_begin();
+    for (int nd : nodes) {
+      const int s = fp.sep_size[nd], b = fp.bnd_size[nd];
+      if (s == 0 || b == 0) continue;
+      for (int a = 0; a < ceil_div(b, kTile); ++a)
+        for (int cc = 0; cc < ceil_div(s, kTile); ++cc) tasks.push_back(CoopTask{CT_W, nd, a, cc, 0});
+    }
+    phase_end();
+    phase_begin();
+    for (int nd : nodes) {
+      const int s = fp.sep_size[nd], f = s + fp.bnd_size[nd];
+      const long long tot = (long long)f * s;
+      for (long long q = 0; q < (tot + 4095) / 4096; ++q) tasks.push_back(CoopTask{CT_CB, nd, (int)q, 0, 0});
+    }
+    phase_end();
+  }
+  for (const auto& ph : phases) st.phase_type.push_back(tasks[ph.t0].type);
+  if (getenv("BDDC_COOP_TIMING")) st.ptime = c.alloc<unsigned long long>(phases.size() + 1);
+  st.pg.tasks = c.upload(tasks.data(), tasks.size());
+  st.pg.phases = c.upload(phases.data(), phases.size());
+  st.pg.nphases = (int)phases.size();
+  st.pg.sc.inv = c.upload(inv.data(), N);
+  st.pg.sc.X = c.upload(X.data(), N);
+  st.pg.sc.Y = c.upload(Y.data(), N);
+  st.pg.sc.W = c.upload(W.data(), N);
+  st.pg.sc.ldx = c.upload(ldx.data(), N);
+  st.pg.sc.ldw = c.upload(ldw.data(), N);
+  st.pg.pool = c.alloc<double>(pool);
+  st.smem_f = sizeof(double) * std::max<int>(kGemmSmemDoubles, kFactSmemDoubles);
+  BDDC_CUDA(cudaFuncSetAttribute(coop_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st.smem_f));
+  int nsm = 0, per_f = 0, per_s = 0;
+  BDDC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device));
+  BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_f, coop_factor_kernel, 128, st.smem_f));
+  BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_s, coop_solve_kernel, 256, 0));
+  // few CTAs: the phases are small at the top of the tree and grid.sync cost grows with
+  // the number of arriving CTAs
+  st.grid_f = nsm * std::max(std::min(per_f, 2), 1);
+  st.grid_s = nsm * std::max(std::min(per_s, 4), 1);
+  // solve program: the per-level task arrays already built for the tiled solve
+  std::vector<int> ft_off(L + 1), bt_off(L + 1), fr_off(L + 1), br_off(L + 1);
+  for (int l = 0; l <= L; ++l) {
+    ft_off[l] = l < L ? (int)(ls.fwd_t[l] - ls.fwd_t[0]) : (int)(ls.fwd_t[L - 1] - ls.fwd_t[0]) + ls.n_fwd_t[L - 1];
+    bt_off[l] = l < L ? (int)(ls.bwd_t[l] - ls.bwd_t[0]) : (int)(ls.bwd_t[L - 1] - ls.bwd_t[0]) + ls.n_bwd_t[L - 1];
+    fr_off[l] = l < L ? (int)(ls.fwd_r[l] - ls.fwd_r[0]) : (int)(ls.fwd_r[L - 1] - ls.fwd_r[0]) + ls.n_fwd_r[L - 1];
+    br_off[l] = l < L ? (int)(ls.bwd_r[l] - ls.bwd_r[0]) : (int)(ls.bwd_r[L - 1] - ls.bwd_r[0]) + ls.n_bwd_r[L - 1];
+  }
+  st.sp.ft = ls.fwd_t[0];
+  st.sp.bt = ls.bwd_t[0];
+  st.sp.fr = ls.fwd_r[0];
+  st.sp.br = ls.bwd_r[0];
+  st.sp.ft_off = c.upload(ft_off.data(), L + 1);
+  st.sp.bt_off = c.upload(bt_off.data(), L + 1);
+  st.sp.fr_off = c.upload(fr_off.data(), L + 1);
+  st.sp.br_off = c.upload(br_off.data(), L + 1);
+  st.sp.nlevels = L;
+}
+
+void coop_release(const Ctx& c) { g_coop.erase(&c); }
+
+void coop_factor(Ctx& c, cudaStream_t s) {
+  CoopState& st = g_coop.at(&c);
+  FrontDev fd = c.fp.d;
+  int* info = c.fp.info;
+  void* args[] = {&fd, &st.pg, &info, &st.ptime};
+  unsigned long long t0 = 0;
+  if (st.ptime) {
+    BDDC_CUDA(cudaStreamSynchronize(s));
+    t0 = 0;
+  }
+  BDDC_CUDA(cudaLaunchCooperativeKernel((void*)coop_factor_kernel, st.grid_f, 128, args, st.smem_f, s));
+  BDDC_COUNT();
+  if (st.ptime) {
+    std::vector<unsigned long long> t(st.phase_type.size());
+    BDDC_CUDA(cudaStreamSynchronize(s));
+    BDDC_CUDA(cudaMemcpy(t.data(), st.ptime, sizeof(unsigned long long) * t.size(), cudaMemcpyDeviceToHost));
+    double by_type[8] = {0};
+    int cnt[8] = {0};
+    for (size_t i = 1; i < t.size(); ++i) {
+      by_type[st.phase_type[i]] += (t[i] - t[i - 1]) * 1e-3;
+      cnt[st.phase_type[i]]++;
+    }
+    const char* nm[8] = {"EA", "PT", "TS|X1", "X1", "SY|X2", "X2", "W", "CB"};
+    fprintf(stderr, "coop factor phases (us, from phase 1): total %.1f\n", (t.back() - t[0]) * 1e-3);
+    for (int k = 0; k < 8; ++k)
+      if (cnt[k]) fprintf(stderr, "  %-6s n=%4d  %9.1f us  avg %7.1f\n", nm[k], cnt[k], by_type[k], by_type[k] / cnt[k]);
+    (void)t0;
+  }
+}
+
+void coop_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s) {
+  CoopState& st = g_coop.at(&c);
+  FrontDev fd = c.fp.d;
+  LevelView lv{c.sched.gat_ptr, c.sched.gat_off, c.sched.gat_src};
+  double* partial = c.sched.partial;
+  void* args[] = {&fd, &lv, &st.sp, (void*)&rhs, (void*)&sol, &partial};
+  BDDC_CUDA(cudaLaunchCooperativeKernel((void*)coop_solve_kernel, st.grid_s, 256, args, 0, s));
+  BDDC_COUNT();
+}
+
+}  // namespace bddc

@@ -6,16 +6,13 @@
 #include <climits>
 
 #include "dense_f64.cuh"
+#include "tile_ops.cuh"
 
 namespace bddc {
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16;
-constexpr int LDW = BM + 4;  // pitch of [k][m] / [k][n] tiles (m or n contiguous)
-constexpr int LDK = BK + 4;  // pitch of [m][k] / [n][k] tiles (k contiguous)
-constexpr int TILE_A = BK * LDW > BM * LDK ? BK * LDW : BM * LDK;
-constexpr int TILE_B = TILE_A;
+using namespace tile;
 
 struct TaskView {
   const double* A;
@@ -33,70 +30,9 @@ __device__ __forceinline__ TaskView gemm_task(const GemmArgs& a, int b) {
                   a.lda,          a.ldb,          a.ldc};
 }
 
-// Copy a pair of consecutive doubles (valid = 0, 1 or 2 of them) into shared memory.
-__device__ __forceinline__ void copy_pair(double* dst, const double* src, int valid, bool al16) {
-  if (al16) {
-    cp_async16(dst, src, valid * 8);
-  } else {
-    cp_async8(dst, src, valid > 0 ? 8 : 0);
-    cp_async8(dst + 1, valid > 1 ? src + 1 : src, valid > 1 ? 8 : 0);
-  }
-}
-
-// Load a BM x BK slice of op(A) (rows m0.., k0..) into shared memory.
-//   !TA: A(m,k) = A[m + k*lda]  -> sm[k*LDW + m]
-//    TA: A(m,k) = A[k + m*lda]  -> sm[m*LDK + k]
-template <bool TA>
-__device__ __forceinline__ void load_a(double* sm, const double* A, int lda, int M, int K, int m0,
-                                       int k0, int tid, bool al) {
-#pragma unroll
-  for (int it = 0; it < 4; ++it) {
-    int c = tid + it * 128;
-    if (!TA) {
-      int k = c >> 5, m = (c & 31) * 2;
-      int gm = m0 + m, gk = k0 + k;
-      int valid = (gk < K) ? max(0, min(2, M - gm)) : 0;
-      const double* src = valid ? A + gm + (long long)gk * lda : A;
-      copy_pair(sm + k * LDW + m, src, valid, al);
-    } else {
-      int m = c >> 3, k = (c & 7) * 2;
-      int gm = m0 + m, gk = k0 + k;
-      int valid = (gm < M) ? max(0, min(2, K - gk)) : 0;
-      const double* src = valid ? A + gk + (long long)gm * lda : A;
-      copy_pair(sm + m * LDK + k, src, valid, al);
-    }
-  }
-}
-
-// Load a BK x BN slice of op(B) (k0.., cols n0..).
-//   !TB: B(k,n) = B[k + n*ldb]  -> sm[n*LDK + k]
-//    TB: B(k,n) = B[n + k*ldb]  -> sm[k*LDW + n]
-template <bool TB>
-__device__ __forceinline__ void load_b(double* sm, const double* B, int ldb, int N, int K, int n0,
-                                       int k0, int tid, bool al) {
-#pragma unroll
-  for (int it = 0; it < 4; ++it) {
-    int c = tid + it * 128;
-    if (!TB) {
-      int n = c >> 3, k = (c & 7) * 2;
-      int gn = n0 + n, gk = k0 + k;
-      int valid = (gn < N) ? max(0, min(2, K - gk)) : 0;
-      const double* src = valid ? B + gk + (long long)gn * ldb : B;
-      copy_pair(sm + n * LDK + k, src, valid, al);
-    } else {
-      int k = c >> 5, n = (c & 31) * 2;
-      int gn = n0 + n, gk = k0 + k;
-      int valid = (gk < K) ? max(0, min(2, N - gn)) : 0;
-      const double* src = valid ? B + gn + (long long)gk * ldb : B;
-      copy_pair(sm + k * LDW + n, src, valid, al);
-    }
-  }
-}
-
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(128) gemm_f64_kernel(GemmArgs args) {
-  __shared__ __align__(16) double As[2][TILE_A];
-  __shared__ __align__(16) double Bs[2][TILE_B];
+  __shared__ __align__(16) double smem[kGemmSmemDoubles];
   const TaskView t = gemm_task(args, blockIdx.y);
   const int tiles_m = (t.M + BM - 1) / BM;
   const int tiles_n = (t.N + BN - 1) / BN;
@@ -104,78 +40,8 @@ __global__ void __launch_bounds__(128) gemm_f64_kernel(GemmArgs args) {
   const int tm = blockIdx.x % tiles_m, tn = blockIdx.x / tiles_m;
   const int m0 = tm * BM, n0 = tn * BN;
   if (args.lower && n0 > m0 + BM - 1) return;  // tile strictly above the diagonal
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp & 1, wn = warp >> 1;
-  const int g = lane >> 2, q = lane & 3;
-
-  double acc[4][4][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-  const int nk = (t.K + BK - 1) / BK;
-  // 16-byte copies need 16-byte aligned pairs: base pointers aligned and even pitches
-  const bool al_a = ((((unsigned long long)t.A) & 15) == 0) && ((t.lda & 1) == 0);
-  const bool al_b = ((((unsigned long long)t.B) & 15) == 0) && ((t.ldb & 1) == 0);
-  if (nk > 0) {
-    load_a<TA>(As[0], t.A, t.lda, t.M, t.K, m0, 0, tid, al_a);
-    load_b<TB>(Bs[0], t.B, t.ldb, t.N, t.K, n0, 0, tid, al_b);
-    cp_async_commit();
-  }
-  for (int kt = 0; kt < nk; ++kt) {
-    const int st = kt & 1;
-    if (kt + 1 < nk) {
-      load_a<TA>(As[st ^ 1], t.A, t.lda, t.M, t.K, m0, (kt + 1) * BK, tid, al_a);
-      load_b<TB>(Bs[st ^ 1], t.B, t.ldb, t.N, t.K, n0, (kt + 1) * BK, tid, al_b);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const double* as = As[st];
-    const double* bs = Bs[st];
-#pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double af[4], bf[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        int m = wm * 32 + i * 8 + g;
-        af[i] = TA ? as[m * LDK + kk + q] : as[(kk + q) * LDW + m];
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        int n = wn * 32 + j * 8 + g;
-        bf[j] = TB ? bs[(kk + q) * LDW + n] : bs[n * LDK + kk + q];
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-    }
-    __syncthreads();
-  }
-
-  const double alpha = args.alpha, beta = args.beta;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int row = m0 + wm * 32 + i * 8 + g;
-    if (row >= t.M) continue;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int col = n0 + wn * 32 + j * 8 + 2 * q + e;
-        if (col >= t.N || (args.lower && col > row)) continue;
-        double* cp = t.C + row + (long long)col * t.ldc;
-        double v = alpha * acc[i][j][e];
-        if (beta != 0.0) v += beta * *cp;
-        *cp = v;
-      }
-    }
-  }
+  gemm_tile<TA, TB>(t.A, t.lda, t.B, t.ldb, t.C, t.ldc, t.M, t.N, t.K, m0, n0, args.alpha,
+                    args.beta, args.lower != 0, smem);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -199,74 +65,21 @@ __device__ __forceinline__ TileView tile_task(const TileArgs& a, int b) {
                   a.offset, a.inv ? a.inv + b * a.sInv : nullptr};
 }
 
-// X = L^{-1} for a lower n x n tile (n <= 64): thread c owns column c and runs the forward
-// substitution down it (no inter-thread dependency); all threads walk (i, k) in lockstep so
-// L[i][k] is a shared-memory broadcast. Output: 64 x 64 (ld 64), zero upper triangle.
-__global__ void __launch_bounds__(64) trtri_tile_kernel(TileArgs args) {
-  extern __shared__ double trtri_sm[];
-  double* Ls = trtri_sm;
-  double* Xs = trtri_sm + kTile * (kTile + 1);
-  const int P = kTile + 1;
+// X = L^{-1} for a lower n x n tile (n <= 64), blocked 8x8 with DMMA (tile_ops.cuh).
+__global__ void __launch_bounds__(128) trtri_tile_kernel(TileArgs args) {
+  extern __shared__ __align__(16) double fsm[];
   const TileView t = tile_task(args, blockIdx.x);
-  const int n = t.n, c = threadIdx.x;
-  if (n <= 0 || !t.inv) return;
-  for (int idx = c; idx < n * n; idx += 64) {
-    const int i = idx % n, j = idx / n;
-    Ls[i + j * P] = i >= j ? t.L[i + (long long)j * t.ldl] : 0.0;
-  }
-  __syncthreads();
-  for (int i = 0; i < n; ++i) {
-    double acc = (i == c) ? 1.0 : 0.0;
-    for (int k = 0; k < i; ++k) acc -= Ls[i + k * P] * Xs[k + c * P];
-    Xs[i + c * P] = (c <= i && c < n) ? acc / Ls[i + i * P] : 0.0;
-  }
-  __syncthreads();
-  for (int idx = c; idx < kTile * kTile; idx += 64) {
-    const int i = idx % kTile, j = idx / kTile;
-    t.inv[idx] = (i < n && j < n) ? Xs[i + j * P] : 0.0;
-  }
+  if (t.n <= 0 || !t.inv) return;
+  potrf_trtri_tile<false>(t.L, t.ldl, t.n, t.inv, fsm);
 }
 
+// Cholesky of 64x64 diagonal tiles (blocked 8x8, DMMA) + their inverses (if args.inv).
 __global__ void __launch_bounds__(128) potrf_tile_kernel(TileArgs args) {
-  __shared__ double S[kTile * TP];
+  extern __shared__ __align__(16) double fsm[];
   const TileView t = tile_task(args, blockIdx.x);
-  const int n = t.n, tid = threadIdx.x;
-  if (n <= 0) return;
-  for (int idx = tid; idx < n * n; idx += blockDim.x) {
-    int i = idx % n, j = idx / n;
-    if (i >= j) S[i + j * TP] = t.L[i + (long long)j * t.ldl];
-  }
-  __syncthreads();
-  __shared__ int failed;
-  if (tid == 0) failed = INT_MAX;
-  for (int j = 0; j < n; ++j) {
-    if (tid == 0) {
-      double d = S[j + j * TP];
-      if (!(d > 0.0)) {
-        if (failed == INT_MAX) failed = t.offset + j;
-        d = 1.0;
-      }
-      S[j + j * TP] = sqrt(d);
-    }
-    __syncthreads();
-    const double inv = 1.0 / S[j + j * TP];
-    for (int i = j + 1 + tid; i < n; i += blockDim.x) S[i + j * TP] *= inv;
-    __syncthreads();
-    const int r = n - j - 1;
-    for (int idx = tid; idx < r * r; idx += blockDim.x) {
-      int ii = idx % r, kk = idx / r;
-      if (ii >= kk) {
-        int i = j + 1 + ii, k = j + 1 + kk;
-        S[i + k * TP] -= S[i + j * TP] * S[k + j * TP];
-      }
-    }
-    __syncthreads();
-  }
-  for (int idx = tid; idx < n * n; idx += blockDim.x) {
-    int i = idx % n, j = idx / n;
-    if (i >= j) t.L[i + (long long)j * t.ldl] = S[i + j * TP];
-  }
-  if (tid == 0 && failed != INT_MAX && args.info) atomicMin(&args.info[t.id], failed);
+  if (t.n <= 0) return;
+  const int bad = potrf_trtri_tile(t.L, t.ldl, t.n, t.inv, fsm);
+  if (threadIdx.x == 0 && bad >= 0 && args.info) atomicMin(&args.info[t.id], t.offset + bad);
 }
 
 // Each thread owns one right-hand-side vector (a row of B for right-side solves, a column
@@ -371,19 +184,25 @@ void gemm(const GemmArgs& a, bool tA, bool tB, cudaStream_t s) {
 
 void potrf_tile(const TileArgs& a, cudaStream_t s) {
   if (a.count <= 0) return;
-  { potrf_tile_kernel<<<a.count, 128, 0, s>>>(a); BDDC_COUNT(); }
+  constexpr int smem = kFactSmemDoubles * (int)sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    BDDC_CUDA(cudaFuncSetAttribute(potrf_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  { potrf_tile_kernel<<<a.count, 128, smem, s>>>(a); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
 }
 
 void trtri_tile(const TileArgs& a, cudaStream_t s) {
   if (a.count <= 0) return;
-  constexpr int smem = 2 * kTile * (kTile + 1) * (int)sizeof(double);
+  constexpr int smem = kFactSmemDoubles * (int)sizeof(double);
   static bool attr = false;
   if (!attr) {
     BDDC_CUDA(cudaFuncSetAttribute(trtri_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  { trtri_tile_kernel<<<a.count, 64, smem, s>>>(a); BDDC_COUNT(); }
+  { trtri_tile_kernel<<<a.count, 128, smem, s>>>(a); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
 }
 
@@ -430,11 +249,10 @@ void potrf_batched(BMat A, int n, int npiv, int count, int* info, double* scratc
     TileArgs t;
     t.L = A.p + k + (long long)k * A.ld; t.sL = A.stride; t.ldl = A.ld;
     t.n = nb; t.count = count; t.offset = k; t.info = info;
+    t.inv = scratch; t.sInv = kTileInvStride;
     potrf_tile(t, s);
     const int rest = n - k - nb;
     if (rest <= 0) continue;
-    t.inv = scratch; t.sInv = kTileInvStride;
-    trtri_tile(t, s);
     BMat L21 = A.at(k + nb, k);
     tile_solve_gemm(TRSM_RLT, BMat{scratch, kTileInvStride, kTile}, nb, L21, rest, count, s);
     // trailing update A22 -= L21 L21^T (lower tiles only)
