@@ -26,6 +26,8 @@ namespace cg = cooperative_groups;
 
 namespace bddc {
 
+constexpr int kX1Chunk = 256;  // split-K of the left-looking inverse accumulation
+
 enum CoopType : int {
   CT_EA = 0, CT_PT = 1, CT_TS = 2, CT_X1 = 3, CT_SY = 4, CT_X2 = 5, CT_W = 6, CT_CB = 7,
 };
@@ -67,16 +69,32 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
   double* X = pg.pool + pg.sc.X[node];
   const int ldx = pg.sc.ldx[node];
   switch (t.type) {
-    case CT_EA: {  // child #arg of node, columns [8a, 8a+8) of its lower update block
+    case CT_EA: {  // child #arg of node, columns [a, a + b) of its lower update block
       const int c0 = fd.child_ptr[node];
       const int ch = fd.child_list[c0 + t.arg];
-      const int b = fd.bnd_size[ch], sc = fd.sep_size[ch], lc = fd.ld[ch];
+      const int bc = fd.bnd_size[ch], sc = fd.sep_size[ch], lc = fd.ld[ch];
       const double* U = fd.fronts + fd.front_off[ch] + sc + (long long)sc * lc;
       const int* rm = fd.rmap + fd.rmap_ptr[ch];
-      for (int j = t.a * 8; j < min(b, t.a * 8 + 8); ++j) {
-        double* Fc = F + (long long)rm[j] * ld;
-        const double* Uc = U + (long long)j * lc;
-        for (int i = j + threadIdx.x; i < b; i += blockDim.x) Fc[rm[i]] += Uc[i];
+      // columns [a, a + cb) in batches of 16; thread owns rows i = a + tid + 128 m, loads
+      // rm[i] once and issues 16 independent read-modify-writes per batch
+      const int je = min(bc, t.a + t.b);
+      for (int j0 = t.a; j0 < je; j0 += 16) {
+        long long cof[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) cof[c] = j0 + c < je ? (long long)rm[j0 + c] * ld : 0;
+        for (int i = j0 + threadIdx.x; i < bc; i += blockDim.x) {
+          const long long r = rm[i];
+          double u[16], fv[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            const bool ok = j0 + c < je && i >= j0 + c;
+            u[c] = ok ? U[i + (long long)(j0 + c) * lc] : 0.0;
+            fv[c] = ok ? F[r + cof[c]] : 0.0;
+          }
+#pragma unroll
+          for (int c = 0; c < 16; ++c)
+            if (j0 + c < je && i >= j0 + c) F[r + cof[c]] = fv[c] + u[c];
+        }
       }
       break;
     }
@@ -95,11 +113,12 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
                              false, smem);
       break;
     }
-    case CT_X1: {  // Y[:, c] = L[k.., c*64 .. k) X[c*64 .. k, c]   (c = a)
+    case CT_X1: {  // Y_q[:, c] = L[k.., c*64 + kq ..) X[.., c]  over K chunk q (c = a, q = b)
       const int k = t.arg * kTile, nb = min(kTile, s - k), c = t.a * kTile;
-      double* Y = pg.pool + pg.sc.Y[node];
-      gemm_tile<false, false>(F + k + (long long)c * ld, ld, X + c + (long long)c * ldx, ldx,
-                              Y + (long long)c * kTile, kTile, nb, min(kTile, k - c), k - c, 0, 0,
+      const int kq0 = c + t.b * kX1Chunk, kq1 = min(k, kq0 + kX1Chunk);
+      double* Y = pg.pool + pg.sc.Y[node] + (long long)t.b * kTile * s;
+      gemm_tile<false, false>(F + k + (long long)kq0 * ld, ld, X + kq0 + (long long)c * ldx, ldx,
+                              Y + (long long)c * kTile, kTile, nb, min(kTile, k - c), kq1 - kq0, 0, 0,
                               1.0, 0.0, false, smem);
       break;
     }
@@ -121,10 +140,14 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
     case CT_X2: {  // X[k.., c] = -inv Y[:, c] (c < panel) or X[k.., k..] = inv
       const int k = t.arg * kTile, nb = min(kTile, s - k), c = t.a * kTile;
       const double* inv = pg.pool + pg.sc.inv[node] + (t.arg & 1) * kTileInvStride;
-      if (c < k) {
-        const double* Y = pg.pool + pg.sc.Y[node];
-        gemm_tile<false, false>(inv, kTile, Y + (long long)c * kTile, kTile, X + k + (long long)c * ldx,
-                                ldx, nb, kTile, nb, 0, 0, -1.0, 0.0, false, smem);
+      if (c < k) {  // X[k, c] = -inv sum_q Y_q[:, c]
+        const int nq = (k - c + kX1Chunk - 1) / kX1Chunk;
+        for (int qq = 0; qq < nq; ++qq) {
+          const double* Y = pg.pool + pg.sc.Y[node] + (long long)qq * kTile * s;
+          gemm_tile<false, false>(inv, kTile, Y + (long long)c * kTile, kTile, X + k + (long long)c * ldx,
+                                  ldx, nb, kTile, nb, 0, 0, -1.0, qq ? 1.0 : 0.0, false, smem);
+          __syncthreads();
+        }
       } else {
         for (int idx = threadIdx.x; idx < nb * nb; idx += blockDim.x) {
           const int i = idx % nb, j = idx / nb;
@@ -310,6 +333,7 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
 
 struct CoopState {
   std::vector<int> phase_type;  // first task type of each phase (diagnostics)
+  std::vector<int> phase_nt;
   unsigned long long* ptime = nullptr;
   CoopProgram pg{};
   SolveProgram sp{};
@@ -324,6 +348,17 @@ void coop_build(Ctx& c) {
   LevelSchedule& ls = c.sched;
   CoopState& st = g_coop[&c];
   st = CoopState{};
+  st.smem_f = sizeof(double) * std::max<int>(kGemmSmemDoubles, kFactSmemDoubles);
+  BDDC_CUDA(cudaFuncSetAttribute(coop_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st.smem_f));
+  int nsm = 0, per_f = 0, per_s = 0;
+  BDDC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device));
+  BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_f, coop_factor_kernel, 128, st.smem_f));
+  BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_s, coop_solve_kernel, 256, 0));
+  // few CTAs: the phases are small at the top of the tree and grid.sync cost grows with
+  // the number of arriving CTAs
+  st.grid_f = nsm * std::max(std::min(per_f, 2), 1);
+  st.grid_s = nsm * std::max(std::min(per_s, 4), 1);
+  const int grid_f = st.grid_f;
   const int N = fp.nnodes, L = fp.nlevels;
   std::vector<CoopTask> tasks;
   std::vector<CoopPhase> phases;
@@ -346,18 +381,24 @@ void coop_build(Ctx& c) {
       ldw[nd] = (int)round_up(std::max(b, 2), 2);
       inv[nd] = off; off += 2 * kTileInvStride;
       X[nd] = off; off += round_up((long long)ldx[nd] * std::max(s, 1), 2);
-      Y[nd] = off; off += round_up((long long)kTile * std::max(s, 1), 2);
+      Y[nd] = off; off += round_up((long long)kTile * std::max(s, 1), 2) * ceil_div(std::max(s, 1), kX1Chunk);
       W[nd] = off; off += round_up((long long)ldw[nd] * std::max(s, 1), 2);
       max_np = std::max(max_np, ceil_div(s, kTile));
       max_ch = std::max(max_ch, fp.child_ptr[nd + 1] - fp.child_ptr[nd]);
     }
     pool = std::max(pool, off);
+    // extend-add: one phase per child slot; column chunks sized for >= 2 tasks per CTA
     for (int k = 0; k < max_ch; ++k) {
+      long long cols = 0;
+      for (int nd : nodes)
+        if (fp.child_ptr[nd + 1] - fp.child_ptr[nd] > k) cols += fp.bnd_size[fp.child_list[fp.child_ptr[nd] + k]];
+      int chunk = 64;
+      while (chunk > 2 && cols / chunk < 2LL * grid_f) chunk >>= 1;
       phase_begin();
       for (int nd : nodes) {
         if (fp.child_ptr[nd + 1] - fp.child_ptr[nd] <= k) continue;
         const int ch = fp.child_list[fp.child_ptr[nd] + k];
-        for (int q = 0; q < ceil_div(fp.bnd_size[ch], 8); ++q) tasks.push_back(CoopTask{CT_EA, nd, q, 0, k});
+        for (int q = 0; q < fp.bnd_size[ch]; q += chunk) tasks.push_back(CoopTask{CT_EA, nd, q, chunk, k});
       }
       phase_end();
     }
@@ -374,7 +415,8 @@ void coop_build(Ctx& c) {
         if (s <= p * kTile) continue;
         const int k = p * kTile, nb = std::min(kTile, s - k), rest = f - k - nb;
         for (int a = 0; a < ceil_div(rest, kTile); ++a) tasks.push_back(CoopTask{CT_TS, nd, a, 0, p});
-        for (int cc = 0; cc < p; ++cc) tasks.push_back(CoopTask{CT_X1, nd, cc, 0, p});
+        for (int cc = 0; cc < p; ++cc)
+          for (int qq = 0; qq < ceil_div(k - cc * kTile, kX1Chunk); ++qq) tasks.push_back(CoopTask{CT_X1, nd, cc, qq, p});
       }
       phase_end();
       phase_begin();
@@ -406,7 +448,10 @@ void coop_build(Ctx& c) {
     }
     phase_end();
   }
-  for (const auto& ph : phases) st.phase_type.push_back(tasks[ph.t0].type);
+  for (const auto& ph : phases) {
+    st.phase_type.push_back(tasks[ph.t0].type);
+    st.phase_nt.push_back(ph.nt);
+  }
   if (getenv("BDDC_COOP_TIMING")) st.ptime = c.alloc<unsigned long long>(phases.size() + 1);
   st.pg.tasks = c.upload(tasks.data(), tasks.size());
   st.pg.phases = c.upload(phases.data(), phases.size());
@@ -418,16 +463,6 @@ void coop_build(Ctx& c) {
   st.pg.sc.ldx = c.upload(ldx.data(), N);
   st.pg.sc.ldw = c.upload(ldw.data(), N);
   st.pg.pool = c.alloc<double>(pool);
-  st.smem_f = sizeof(double) * std::max<int>(kGemmSmemDoubles, kFactSmemDoubles);
-  BDDC_CUDA(cudaFuncSetAttribute(coop_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st.smem_f));
-  int nsm = 0, per_f = 0, per_s = 0;
-  BDDC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device));
-  BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_f, coop_factor_kernel, 128, st.smem_f));
-  BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_s, coop_solve_kernel, 256, 0));
-  // few CTAs: the phases are small at the top of the tree and grid.sync cost grows with
-  // the number of arriving CTAs
-  st.grid_f = nsm * std::max(std::min(per_f, 2), 1);
-  st.grid_s = nsm * std::max(std::min(per_s, 4), 1);
   // solve program: the per-level task arrays already built for the tiled solve
   std::vector<int> ft_off(L + 1), bt_off(L + 1), fr_off(L + 1), br_off(L + 1);
   for (int l = 0; l <= L; ++l) {
@@ -475,6 +510,10 @@ void coop_factor(Ctx& c, cudaStream_t s) {
     fprintf(stderr, "coop factor phases (us, from phase 1): total %.1f\n", (t.back() - t[0]) * 1e-3);
     for (int k = 0; k < 8; ++k)
       if (cnt[k]) fprintf(stderr, "  %-6s n=%4d  %9.1f us  avg %7.1f\n", nm[k], cnt[k], by_type[k], by_type[k] / cnt[k]);
+    if (atoi(getenv("BDDC_COOP_TIMING")) >= 2)
+      for (size_t i = 1; i < t.size(); ++i)
+        fprintf(stderr, "    phase %3zu %-6s tasks %6d  %8.1f us\n", i, nm[st.phase_type[i]], st.phase_nt[i],
+                (t[i] - t[i - 1]) * 1e-3);
     (void)t0;
   }
 }

@@ -135,6 +135,22 @@ __device__ __forceinline__ void gemm_tile(const double* A, int lda, const double
     }
     __syncthreads();
   }
+  // epilogue: all C reads issued before any store (no serial read-modify-write chain)
+  double cv[4][4][2];
+  if (beta != 0.0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int row = m0 + wm * 32 + i * 8 + g;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = n0 + wn * 32 + j * 8 + 2 * q + e;
+          const bool ok = row < M && col < N && !(lower && col > row);
+          cv[i][j][e] = ok ? __ldcg(C + row + (long long)col * ldc) : 0.0;
+        }
+    }
+  }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int row = m0 + wm * 32 + i * 8 + g;
@@ -145,10 +161,9 @@ __device__ __forceinline__ void gemm_tile(const double* A, int lda, const double
       for (int e = 0; e < 2; ++e) {
         const int col = n0 + wn * 32 + j * 8 + 2 * q + e;
         if (col >= N || (lower && col > row)) continue;
-        double* cp = C + row + (long long)col * ldc;
         double v = alpha * acc[i][j][e];
-        if (beta != 0.0) v += beta * *cp;
-        *cp = v;
+        if (beta != 0.0) v += beta * cv[i][j][e];
+        C[row + (long long)col * ldc] = v;
       }
     }
   }
@@ -159,7 +174,7 @@ __device__ __forceinline__ void gemm_tile(const double* A, int lda, const double
 // per-warp 8x8 scratch. The 8x8 diagonal blocks are factored / inverted in registers by one
 // warp with shuffles; panel solves, trailing updates and the inverse recursion are DMMA.8x8x4.
 constexpr int SP = kTile + 4;  // pitch = 4 mod 16 doubles: conflict-free 8x8x4 fragments
-constexpr int kFactSmemDoubles = 2 * kTile * SP + 4 * 64 + 64;
+constexpr int kFactSmemDoubles = 2 * kTile * SP + 128 + 8 * 64;  // S, X, 2 Dv, 8 warp tmps
 
 // C(8x8) (+)= A(8x8) B(8x8) from shared memory; A(r,k)=A[r*ars+k*acs], B(k,c)=B[k*brs+c*bcs]
 __device__ __forceinline__ void mma8(double& c0, double& c1, const double* A, int ars, int acs,
@@ -172,97 +187,133 @@ __device__ __forceinline__ void mma8(double& c0, double& c1, const double* A, in
 // FACTOR: factor the n x n lower tile L (ld, n <= 64) in place, then write L^{-1} to inv
 // (64 x 64, ld 64, zero upper / padding). !FACTOR: L is already a factor; only invert.
 // Returns the first failing local pivot or -1.
+// Warp-level Cholesky + inverse of the 8x8 diagonal block at k0 (lanes 0..7 = rows), in
+// registers: one rsqrt per pivot gives both the scaling and 1/L[c][c] for the inverse.
+// Writes the factor into S (FACTOR), the inverse into X's diagonal block and Dv (pitch 8).
+template <bool FACTOR>
+__device__ __forceinline__ void diag8(double* S, double* X, double* Dv, int k0, int lane,
+                                      int* failed) {
+  double row[8], rinv[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) row[c] = lane < 8 ? S[(k0 + lane) + (k0 + c) * SP] : 0.0;
+  if (FACTOR) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      double d = __shfl_sync(0xffffffffu, row[c], c);
+      if (!(d > 0.0)) {
+        if (lane == 0 && *failed < 0) *failed = k0 + c;
+        d = 1.0;
+      }
+      const double ri = rsqrt(d);
+      rinv[c] = ri;
+      const double l = lane > c ? row[c] * ri : (lane == c ? d * ri : 0.0);
+      row[c] = l;
+#pragma unroll
+      for (int k = c + 1; k < 8; ++k) {
+        const double lk = __shfl_sync(0xffffffffu, l, k);
+        if (lane >= k) row[k] -= l * lk;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) rinv[c] = 1.0 / __shfl_sync(0xffffffffu, row[c], c);
+  }
+  // lane c = column c of the inverse: x[r] = (delta_rc - sum_{m<r} L[r][m] x[m]) / L[r][r]
+  double x[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    double acc = (r == lane) ? 1.0 : 0.0;
+#pragma unroll
+    for (int m = 0; m < r; ++m) acc -= __shfl_sync(0xffffffffu, row[m], r) * x[m];
+    x[r] = acc * rinv[r];
+  }
+  if (lane < 8) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (FACTOR) S[(k0 + lane) + (k0 + c) * SP] = c <= lane ? row[c] : 0.0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      Dv[r + lane * 8] = r >= lane ? x[r] : 0.0;
+      X[(k0 + r) + (k0 + lane) * SP] = r >= lane ? x[r] : 0.0;
+    }
+  }
+}
+
+// Cholesky + inverse of an n x n (n <= 64) SPD tile held in shared memory, blocked by 8x8
+// DMMA blocks with one-block lookahead: while warps 1.. run the trailing update of step kb,
+// warp 0 updates and factors diagonal block kb+1.
 template <bool FACTOR = true>
 __device__ __forceinline__ int potrf_trtri_tile(double* L, int ld, int n, double* inv, double* smem) {
   double* S = smem;                  // factor
   double* X = smem + kTile * SP;     // inverse
-  double* Dv = X + kTile * SP;       // 8x8 inverse of the current diagonal block (pitch 8)
+  double* Dv = X + kTile * SP;       // 2 x (8x8) inverses of diagonal blocks (pitch 8)
   __shared__ int failed;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = nt >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   const int nb8 = (n + 7) >> 3, np = nb8 * 8;
   if (tid == 0) failed = -1;
-  for (int idx = tid; idx < np * np; idx += nt) {
-    const int i = idx % np, j = idx / np;
-    double v = 0.0;
-    if (i < n && j < n) v = i >= j ? L[i + (long long)j * ld] : 0.0;
-    else if (i == j) v = 1.0;  // identity padding
-    S[i + j * SP] = v;
-    X[i + j * SP] = 0.0;
+  for (int j = warp; j < np; j += nw) {
+    for (int i = lane; i < np; i += 32) {
+      double v = 0.0;
+      if (i < n && j < n) v = i >= j ? L[i + (long long)j * ld] : 0.0;
+      else if (i == j) v = 1.0;  // identity padding
+      S[i + j * SP] = v;
+      X[i + j * SP] = 0.0;
+    }
   }
+  __syncthreads();
+  if (warp == 0) diag8<FACTOR>(S, X, Dv, 0, lane, &failed);
   __syncthreads();
   for (int kb = 0; kb < nb8; ++kb) {
     const int k0 = kb * 8;
-    // (1) warp 0: Cholesky + inverse of the 8x8 diagonal block in registers (lane r < 8 = row r)
-    if (warp == 0) {
-      double row[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) row[c] = lane < 8 ? S[(k0 + lane) + (k0 + c) * SP] : 0.0;
-      if (FACTOR) {
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          double d = __shfl_sync(0xffffffffu, row[c], c);
-          if (!(d > 0.0)) {
-            if (lane == 0 && failed < 0) failed = k0 + c;
-            d = 1.0;
-          }
-          const double sd = sqrt(d);
-          const double l = lane > c ? row[c] / sd : (lane == c ? sd : 0.0);
-          row[c] = l;
-#pragma unroll
-          for (int k = c + 1; k < 8; ++k) {
-            const double lk = __shfl_sync(0xffffffffu, l, k);
-            if (lane >= k) row[k] -= l * lk;
-          }
-        }
+    if (!FACTOR) {
+      if (kb + 1 < nb8) {
+        if (warp == 0) diag8<FACTOR>(S, X, Dv, k0 + 8, lane, &failed);
+        __syncthreads();
       }
-      // inverse, lane c = column c: x[r] = (delta_rc - sum_{m<r} L[r][m] x[m]) / L[r][r]
-      double x[8];
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        double a = (r == lane) ? 1.0 : 0.0;
-#pragma unroll
-        for (int m = 0; m < r; ++m) a -= __shfl_sync(0xffffffffu, row[m], r) * x[m];
-        x[r] = a / __shfl_sync(0xffffffffu, row[r], r);
-      }
-      if (lane < 8) {
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          if (FACTOR) S[(k0 + lane) + (k0 + c) * SP] = c <= lane ? row[c] : 0.0;
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          Dv[r + lane * 8] = r >= lane ? x[r] : 0.0;
-          X[(k0 + r) + (k0 + lane) * SP] = r >= lane ? x[r] : 0.0;
-        }
-      }
+      continue;
     }
-    __syncthreads();
-    if (!FACTOR) continue;
+    const double* Dcur = Dv + (kb & 1) * 64;
     // (2) panel below: L[ib][kb] = S[ib][kb] Dinv^T
-    for (int ib = kb + 1 + warp; ib < nb8; ib += nt >> 5) {
+    for (int ib = kb + 1 + warp; ib < nb8; ib += nw) {
       double c0 = 0.0, c1 = 0.0;
-      mma8(c0, c1, S + ib * 8 + k0 * SP, 1, SP, Dv, 8, 1, lane);  // B(k,c) = Dinv[c][k]
+      mma8(c0, c1, S + ib * 8 + k0 * SP, 1, SP, Dcur, 8, 1, lane);  // B(k,c) = Dinv[c][k]
       __syncwarp();
       S[(ib * 8 + g) + (k0 + 2 * t4) * SP] = c0;
       S[(ib * 8 + g) + (k0 + 2 * t4 + 1) * SP] = c1;
     }
     __syncthreads();
-    // (3) trailing update S[ib][jb] -= L[ib][kb] L[jb][kb]^T  (kb < jb <= ib)
+    // (3) trailing update S[ib][jb] -= L[ib][kb] L[jb][kb]^T  (kb < jb <= ib); task 0 is the
+    // next diagonal block, done by warp 0 followed by its factorization (lookahead).
     const int nr = nb8 - kb - 1;
-    for (int q = warp; q < nr * (nr + 1) / 2; q += nt >> 5) {
-      int ib = 0;
-      while ((ib + 1) * (ib + 2) / 2 <= q) ++ib;
-      const int jb = q - ib * (ib + 1) / 2;
-      const int I = kb + 1 + ib, J = kb + 1 + jb;
+    const int ntask = nr * (nr + 1) / 2;
+    if (warp == 0 && nr > 0) {
+      const int I = kb + 1;
       double c0 = 0.0, c1 = 0.0;
-      mma8(c0, c1, S + I * 8 + k0 * SP, 1, SP, S + J * 8 + k0 * SP, SP, 1, lane);
-      S[(I * 8 + g) + (J * 8 + 2 * t4) * SP] -= c0;
-      S[(I * 8 + g) + (J * 8 + 2 * t4 + 1) * SP] -= c1;
+      mma8(c0, c1, S + I * 8 + k0 * SP, 1, SP, S + I * 8 + k0 * SP, SP, 1, lane);
+      S[(I * 8 + g) + (I * 8 + 2 * t4) * SP] -= c0;
+      S[(I * 8 + g) + (I * 8 + 2 * t4 + 1) * SP] -= c1;
+      __syncwarp();
+      diag8<FACTOR>(S, X, Dv + ((kb + 1) & 1) * 64, I * 8, lane, &failed);
+    }
+    const int w0 = nw > 1 ? 1 : 0, ws = nw > 1 ? nw - 1 : 1;
+    if (warp >= w0) {
+      for (int q = 1 + (warp - w0); q < ntask; q += ws) {
+        int ib = 0;
+        while ((ib + 1) * (ib + 2) / 2 <= q) ++ib;
+        const int jb = q - ib * (ib + 1) / 2;
+        const int I = kb + 1 + ib, J = kb + 1 + jb;
+        double c0 = 0.0, c1 = 0.0;
+        mma8(c0, c1, S + I * 8 + k0 * SP, 1, SP, S + J * 8 + k0 * SP, SP, 1, lane);
+        S[(I * 8 + g) + (J * 8 + 2 * t4) * SP] -= c0;
+        S[(I * 8 + g) + (J * 8 + 2 * t4 + 1) * SP] -= c1;
+      }
     }
     __syncthreads();
   }
   // inverse recursion by block rows: X[i][k] = -X[i][i] sum_{m=k}^{i-1} L[i][m] X[m][k]
-  double* tmp = Dv + 64 + warp * 64;  // per-warp 8x8 scratch
+  double* tmp = Dv + 128 + warp * 64;  // per-warp 8x8 scratch
   for (int ib = 1; ib < nb8; ++ib) {
     for (int kb = warp; kb < ib; kb += nt >> 5) {
       double c0 = 0.0, c1 = 0.0;
