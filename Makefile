@@ -4,12 +4,18 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 FLAGS := -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -Xptxas -warn-spills
 SRC := $(wildcard paper_2001_07289_b200/csrc/*.cu)
 HDR := $(wildcard paper_2001_07289_b200/csrc/*.cuh) include/bddcso_b200.h
+OBJDIR := paper_2001_07289_b200/build
+OBJ := $(patsubst paper_2001_07289_b200/csrc/%.cu,$(OBJDIR)/%.o,$(SRC))
 LIB := paper_2001_07289_b200/libbddcso_b200.so
 
 all: $(LIB)
 
-$(LIB): $(SRC) $(HDR)
-	$(NVCC) $(ARCH) $(FLAGS) -shared -o $@ $(SRC)
+$(OBJDIR)/%.o: paper_2001_07289_b200/csrc/%.cu $(HDR)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(ARCH) $(FLAGS) -c -o $@ $<
+
+$(LIB): $(OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ)
 
 clean:
-	rm -f $(LIB)
+	rm -rf $(LIB) $(OBJDIR)

@@ -55,32 +55,54 @@ __global__ void gamma_residual_kernel(Geometry G, int n_gamma, const long long* 
 // sparse coupling stencil B_j to the previous plane (block LDL^T):
 //   forward   h_j = W_j (b_j - B_j h_{j-1})
 //   backward  x_j = h_j - W_j (B_{j+1}^T x_{j+1})
-// Each lane owns rows r = lane + 32 i (i < R); the symmetric GEMV broadcasts the vector
-// with shuffles and reads the packed column-major lower triangle straight from the
-// cp.async staging buffers (double-buffered: block j+-1 streams in while block j is used).
-// Each W_j is read from HBM once per pass.
+// Each lane owns rows r = lane + 32 i (i < R). A plane's packed W and its coupling rows are
+// staged by cp.async (double-buffered: plane j -+ 1 streams in while plane j is used); the
+// GEMV reads the packed column-major lower triangle in shared memory with running offsets
+// and the vector by broadcast. Each W_j is read from HBM once per pass.
 constexpr int kBtWarps = 4;
+constexpr int kBtStages = 2;  // planes in flight per warp: current + 1 ahead
 
+struct BtSmem {  // per-warp layout (doubles)
+  int nI, tm_pad, bc_pad, M2;
+  __device__ __host__ int stage() const { return tm_pad + bc_pad; }
+  __device__ __host__ int per_warp() const { return nI + kBtStages * stage() + M2; }
+};
+
+__device__ __host__ inline BtSmem bt_smem(const Geometry& G) {
+  BtSmem b;
+  b.nI = G.nI_pad;
+  b.tm_pad = (G.Tm + 1) & ~1;
+  b.bc_pad = (G.m_pad * G.nbo + 1) & ~1;
+  b.M2 = (G.m_pad + 1) & ~1;
+  return b;
+}
+
+// out[r] = sum_k W[r][k] v[k]; W packed lower, column k at ck = k M - k(k-1)/2 (rows k..M-1):
+//   k <= r: W[r][k] = pk[ck + r - k]   (offset a1, advances by M - 1 - k per column)
+//   k >  r: W[r][k] = pk[cr + k - r]   (offset a2 + k, a2 = cr - r)
 template <int R>
-__device__ __forceinline__ void bt_sym_gemv(const double* __restrict__ pk, int M, const double (&v)[R],
-                                            double (&out)[R], int lane) {
+__device__ __forceinline__ void bt_gemv(const double* __restrict__ pk, const double* __restrict__ v, int M,
+                                        double (&out)[R], int lane) {
+  int a1[R], a2[R];
 #pragma unroll
-  for (int i = 0; i < R; ++i) out[i] = 0.0;
+  for (int i = 0; i < R; ++i) {
+    const int r = min(lane + 32 * i, M - 1);  // lanes past M repeat row M-1 (result unused)
+    out[i] = 0.0;
+    a1[i] = r;
+    a2[i] = r * M - r * (r - 1) / 2 - r;
+  }
+  int d = M - 1;
+#pragma unroll 4
   for (int k = 0; k < M; ++k) {
-    double vk = 0.0;
+    const double vk = v[k];
 #pragma unroll
     for (int i = 0; i < R; ++i) {
-      const double b = __shfl_sync(0xffffffffu, v[i], k & 31);
-      if ((k >> 5) == i) vk = b;
+      const int r = min(lane + 32 * i, M - 1);
+      const double w = pk[k <= r ? a1[i] : a2[i] + k];
+      out[i] = fma(w, vk, out[i]);
+      a1[i] += d;
     }
-    const int csk = k * M - k * (k - 1) / 2;
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int r = lane + 32 * i;
-      if (r >= M) continue;
-      const double w = k <= r ? pk[csk + (r - k)] : pk[r * M - r * (r - 1) / 2 + (k - r)];
-      out[i] += w * vk;
-    }
+    --d;
   }
 }
 
@@ -90,25 +112,49 @@ __global__ void __launch_bounds__(32 * kBtWarps) bt_solve_kernel(Geometry G, Loc
                                                                  const double* __restrict__ in,
                                                                  double* __restrict__ out) {
   extern __shared__ __align__(16) double sm[];
-  const int M = G.m_pad, Tm = G.Tm;
-  const int tm_pad = (Tm + 1) & ~1;
+  const BtSmem L = bt_smem(G);
+  const int M = G.m_pad, Tm = G.Tm, nbo = G.nbo, nblk = G.nblk;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sub = blockIdx.x * kBtWarps + warp;
-  const int per_warp = G.nI_pad + 2 * tm_pad + M + (M & 1);
-  double* y = sm + warp * per_warp;  // nI_pad
-  double* stg[2] = {y + G.nI_pad, y + G.nI_pad + tm_pad};
+  double* y = sm + warp * L.per_warp();        // nI_pad
+  double* stg = y + L.nI;                      // kBtStages x [W packed | coupling rows]
+  double* tv = stg + kBtStages * L.stage();    // M: the GEMV input vector
 
   if (sub >= G.nsub) return;
   int p[3];
   sub_coords(G, sub, p);
   const double* li = LI + (long long)sub * G.li_stride;
-  const double* bc = li + (long long)G.nblk * Tm;
-  const int px = G.blk[0] - 1;
-  auto prefetch = [&](int j, double* dst) {
-    const double* src = li + (long long)j * Tm;
+  const double* bc = li + (long long)nblk * Tm;
+  const int mb = M * nbo;
+  // stage st <- W_jw and the coupling rows of plane jb (jb < 0: none)
+  auto prefetch = [&](int jw, int jb, int st) {
+    double* dst = stg + st * L.stage();
+    const double* src = li + (long long)jw * Tm;
     for (int e = 2 * lane; e < Tm; e += 64) cp_async16(dst + e, src + e, min(2, Tm - e) * 8);
+    if (jb >= 0) {
+      const double* sb = bc + (long long)jb * mb;
+      for (int e = 2 * lane; e < mb; e += 64) cp_async16(dst + L.tm_pad + e, sb + e, min(2, mb - e) * 8);
+    }
     cp_async_commit();
   };
+  // lane rows: in-plane coordinates and the coupling neighbours (clamped; the coefficient
+  // of a structurally absent neighbour is zero)
+  const int px = G.blk[0] - 1;
+  int fwd_q[R][9], bwd_q[R][9];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int r = lane + 32 * i, x = r % px, yy = r / px;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      if (k < nbo) {
+        const int qf = (x + G.bo_dx[k]) + (yy + G.bo_dy[k]) * px;
+        const int qb = (x - G.bo_dx[k]) + (yy - G.bo_dy[k]) * px;
+        fwd_q[i][k] = min(max(qf, 0), M - 1);
+        bwd_q[i][k] = (qb >= 0 && qb < M && r < M) ? qb : -1;
+      }
+    }
+  }
+  if (nblk > 0) prefetch(0, 0, 0);
   for (int rr = lane; rr < G.nI_pad; rr += 32) {
     const int node = lt.irow_node[rr];
     double v = 0.0;
@@ -119,72 +165,65 @@ __global__ void __launch_bounds__(32 * kBtWarps) bt_solve_kernel(Geometry G, Loc
     }
     y[rr] = v;
   }
-  double t[R], hv[R];
+  double hv[R];
   // ---- forward: h_j = W_j (b_j - B_j h_{j-1}) ----
-  if (G.nblk > 0) prefetch(0, stg[0]);
-  for (int j = 0; j < G.nblk; ++j) {
-    const double* pk = stg[j & 1];
-    if (j + 1 < G.nblk) {
-      prefetch(j + 1, stg[(j + 1) & 1]);
+  for (int j = 0; j < nblk; ++j) {
+    const int st = j & 1;
+    if (j + 1 < nblk) {
+      prefetch(j + 1, j + 1, st ^ 1);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncwarp();
+    const double* pk = stg + st * L.stage();
+    const double* bj = pk + L.tm_pad;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const int r = lane + 32 * i;
-      double acc = 0.0;
       if (r < M) {
-        acc = y[j * M + r];
+        double acc = y[j * M + r];
         if (j > 0) {
-          const double* bj = bc + ((long long)j * M + r) * G.nbo;
           const double* hp = y + (j - 1) * M;
-          const int x = r % px, yy = r / px;
-          for (int k = 0; k < G.nbo; ++k) {
-            const double cf = bj[k];
-            if (cf != 0.0) acc -= cf * hp[(x + G.bo_dx[k]) + (yy + G.bo_dy[k]) * px];
-          }
+#pragma unroll
+          for (int k = 0; k < 9; ++k)
+            if (k < nbo) acc -= bj[r * nbo + k] * hp[fwd_q[i][k]];
         }
+        tv[r] = acc;
       }
-      t[i] = acc;
     }
     __syncwarp();
-    bt_sym_gemv<R>(pk, M, t, hv, lane);
+    bt_gemv<R>(pk, tv, M, hv, lane);
 #pragma unroll
     for (int i = 0; i < R; ++i)
       if (lane + 32 * i < M) y[j * M + lane + 32 * i] = hv[i];
     __syncwarp();
   }
   // ---- backward: x_j = h_j - W_j (B_{j+1}^T x_{j+1}) ----
-  if (G.nblk > 1) prefetch(G.nblk - 2, stg[0]);
-  for (int j = G.nblk - 2, it = 0; j >= 0; --j, ++it) {
-    const double* pk = stg[it & 1];
+  if (nblk > 1) prefetch(nblk - 2, nblk - 1, 0);
+  for (int j = nblk - 2, it = 0; j >= 0; --j, ++it) {
+    const int st = it & 1;
     if (j > 0) {
-      prefetch(j - 1, stg[(it + 1) & 1]);
+      prefetch(j - 1, j, st ^ 1);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncwarp();
+    const double* pk = stg + st * L.stage();
+    const double* bn = pk + L.tm_pad;  // coupling rows of plane j + 1
     const double* xn = y + (j + 1) * M;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const int r = lane + 32 * i;
       double acc = 0.0;
-      if (r < M) {
-        const int x = r % px, yy = r / px;
-        for (int k = 0; k < G.nbo; ++k) {
-          const int rs = (x - G.bo_dx[k]) + (yy - G.bo_dy[k]) * px;
-          if (rs < 0 || rs >= M) continue;
-          const double cf = bc[((long long)(j + 1) * M + rs) * G.nbo + k];
-          if (cf != 0.0) acc += cf * xn[rs];
-        }
-      }
-      t[i] = acc;
+#pragma unroll
+      for (int k = 0; k < 9; ++k)
+        if (k < nbo && bwd_q[i][k] >= 0) acc += bn[bwd_q[i][k] * nbo + k] * xn[bwd_q[i][k]];
+      if (r < M) tv[r] = acc;
     }
-    bt_sym_gemv<R>(pk, M, t, hv, lane);
     __syncwarp();
+    bt_gemv<R>(pk, tv, M, hv, lane);
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const int r = lane + 32 * i;
@@ -323,9 +362,7 @@ void spmv(Ctx& c, const double* x, double* y, cudaStream_t s) {
 static void bt_solve(Ctx& c, const double* in, double* out, cudaStream_t s) {
   const Geometry& G = c.geo;
   PhaseScope ps(c.prof, "apply.bt_solve", s);
-  const int tm_pad = (G.Tm + 1) & ~1;
-  const size_t per_warp = G.nI_pad + 2 * tm_pad + G.m_pad + (G.m_pad & 1);
-  const size_t smem = sizeof(double) * per_warp * kBtWarps;
+  const size_t smem = sizeof(double) * bt_smem(G).per_warp() * kBtWarps;
   static size_t attr = 0;
   if (smem > attr) {
     BDDC_CUDA(cudaFuncSetAttribute(bt_solve_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
