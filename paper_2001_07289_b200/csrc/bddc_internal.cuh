@@ -108,6 +108,7 @@ struct FrontPlan {
 // step, device task arrays for the tile Cholesky / tile TRSM / lower GEMM launches.
 struct CsTask {  // coarse-solve GEMV tile
   int node, r0, c0, part;
+  int red;  // global index of the reduction (CsRed) this tile's partial belongs to
 };
 struct CsRed {  // coarse-solve reduction over the partials of one row / column tile
   int node, t0, p0, np;
@@ -146,6 +147,8 @@ struct LevelSchedule {
   std::vector<CsRed*> fwd_r, bwd_r;
   std::vector<int> n_fwd_t, n_bwd_t, n_fwd_r, n_bwd_r;
   double* partial = nullptr;
+  double* ybuf = nullptr;     // forward-solve values of the separator rows (n)
+  int* red_cnt = nullptr;     // arrival counters of the fused reductions (self-resetting)
   int* gat_ptr = nullptr;    // per node front position -> sources in the update pool
   long long* gat_off = nullptr;  // per node offset into gat_ptr
   int* gat_src = nullptr;

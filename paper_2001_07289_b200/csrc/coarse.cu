@@ -365,7 +365,7 @@ void build_level_schedule(Ctx& c) {
         int cnt = 0;
         for (int c0 = 0; c0 < sz; c0 += 256) {
           if (r0 < sz && c0 > r0 + 63) break;  // above the lower-triangular L11^{-1}
-          ft.push_back(CsTask{nd, r0, c0, pf++});
+          ft.push_back(CsTask{nd, r0, c0, pf++, (int)fr.size()});
           ++cnt;
         }
         fr.push_back(CsRed{nd, r0, p0, cnt});
@@ -374,7 +374,7 @@ void build_level_schedule(Ctx& c) {
         const int p0 = pb;
         int cnt = 0;
         for (int r0 = (c0 / 256) * 256; r0 < f; r0 += 256) {
-          bt.push_back(CsTask{nd, r0, c0, pb++});
+          bt.push_back(CsTask{nd, r0, c0, pb++, (int)br.size()});
           ++cnt;
         }
         br.push_back(CsRed{nd, c0, p0, cnt});
@@ -394,6 +394,9 @@ void build_level_schedule(Ctx& c) {
     ls.bwd_r[l] = dbr + br_off[l]; ls.n_bwd_r[l] = (int)(br_off[l + 1] - br_off[l]);
   }
   ls.partial = c.alloc<double>((size_t)std::max(max_parts, 1) * 64);
+  ls.ybuf = c.alloc<double>((size_t)std::max(fp.n_coarse, 1));
+  ls.red_cnt = c.alloc<int>(fr.size() + br.size() + 1);
+  BDDC_CUDA(cudaMemset(ls.red_cnt, 0, sizeof(int) * (fr.size() + br.size() + 1)));
   // gather maps: front position of every node <- child update entries (child order)
   std::vector<long long> goff(fp.nnodes);
   std::vector<int> gptr;

@@ -215,6 +215,7 @@ struct SolveProgram {
   const int* fr_off;
   const int* br_off;
   int nlevels;
+  int nfr;  // number of forward reductions (offset of the backward counters)
 };
 
 __device__ __forceinline__ double gather_children_c(const LevelView& lv, const double* __restrict__ upd,
@@ -225,14 +226,30 @@ __device__ __forceinline__ double gather_children_c(const LevelView& lv, const d
   return acc;
 }
 
+// Forward (bottom-up): y_sep = X (rhs + child updates), upd = gathered - W21 (..);
+// backward (top-down): x_sep = X^T y_sep - W21^T x_bnd. Each level is ONE phase: the GEMV
+// tiles write 64-entry partials and the last tile to arrive at a row (column) chunk sums the
+// chunk's partials in fixed order (deterministic) and finishes it.
 __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView lv, SolveProgram sp,
                                                          const double* __restrict__ rhs,
                                                          double* __restrict__ sol,
-                                                         double* __restrict__ partial) {
+                                                         double* __restrict__ partial,
+                                                         double* __restrict__ ybuf, int* __restrict__ cnt,
+                                                         unsigned long long* __restrict__ ptime) {
   __shared__ double vs[256];
   __shared__ double red[4][64];
+  __shared__ int last;
   cg::grid_group grid = cg::this_grid();
-  const int tid = threadIdx.x;
+  int sync_id = 1;
+  if (ptime && blockIdx.x == 0 && threadIdx.x == 0) ptime[0] = gtimer();
+  auto gsync = [&]() {
+    grid.sync();
+    if (ptime && blockIdx.x == 0 && threadIdx.x == 0) ptime[sync_id] = gtimer();
+    ++sync_id;
+  };
+  int* cnt_f = cnt;
+  int* cnt_b = cnt + sp.nfr;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // forward: levels bottom-up
   for (int l = 0; l < sp.nlevels; ++l) {
     for (int ti = sp.ft_off[l] + blockIdx.x; ti < sp.ft_off[l + 1]; ti += gridDim.x) {
@@ -249,36 +266,43 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
       __syncthreads();
       const int rr = tid & 63, grp = tid >> 6;
       const int r = t.r0 + rr;
-      double a0 = 0.0, a1 = 0.0;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
       if (r < f) {
         const int kb = t.c0 + grp * 64;
         int ke = min(kb + 64, s);
         if (r < s) ke = min(ke, r + 1);
-        int k = kb;
-        for (; k + 1 < ke; k += 2) {
-          a0 += F[r + k * ld] * vs[k - t.c0];
-          a1 += F[r + (k + 1) * ld] * vs[k + 1 - t.c0];
+        const double* Fr = F + r;
+        for (int k0 = kb; k0 < ke; k0 += 16) {
+          double fv[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) fv[u] = k0 + u < ke ? __ldcs(Fr + (long long)(k0 + u) * ld) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 16; ++u) acc[u & 3] += k0 + u < ke ? fv[u] * vs[k0 + u - t.c0] : 0.0;
         }
-        if (k < ke) a0 += F[r + k * ld] * vs[k - t.c0];
       }
-      red[grp][rr] = a0 + a1;
+      red[grp][rr] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
       __syncthreads();
-      if (tid < 64)
+      if (tid < 64) {
         partial[(long long)t.part * 64 + tid] = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
-    }
-    grid.sync();
-    for (int ti = sp.fr_off[l] + blockIdx.x * 4 + (tid >> 6); ti < sp.fr_off[l + 1]; ti += gridDim.x * 4) {
-      const CsRed t = sp.fr[ti];
-      const int node = t.node, s = fd.sep_size[node], f = s + fd.bnd_size[node];
-      const int lt = tid & 63, r = t.t0 + lt;
-      if (r < f) {
-        double acc = 0.0;
-        for (int p = 0; p < t.np; ++p) acc += partial[(long long)(t.p0 + p) * 64 + lt];
-        if (r < s) sol[fd.sep_start[node] + r] = acc;
-        else fd.upd[fd.upd_off[node] + (r - s)] = gather_children_c(lv, fd.upd, node, r) - acc;
+        __threadfence();
+      }
+      __syncthreads();
+      const CsRed R = sp.fr[t.red];
+      if (tid == 0) last = atomicAdd(cnt_f + t.red, 1) == R.np - 1;
+      __syncthreads();
+      if (last) {
+        __threadfence();
+        const int rw = R.t0 + tid;
+        if (tid < 64 && rw < f) {
+          double a = 0.0;
+          for (int p = 0; p < R.np; ++p) a += __ldcg(partial + (long long)(R.p0 + p) * 64 + tid);
+          if (rw < s) ybuf[s0 + rw] = a;
+          else fd.upd[fd.upd_off[node] + (rw - s)] = gather_children_c(lv, fd.upd, node, rw) - a;
+        }
+        if (tid == 0) cnt_f[t.red] = 0;
       }
     }
-    grid.sync();
+    gsync();
   }
   // backward: levels top-down
   for (int l = sp.nlevels - 1; l >= 0; --l) {
@@ -292,36 +316,54 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
       __syncthreads();
       {
         const int r = t.r0 + tid;
-        vs[tid] = r < s ? sol[s0 + r] : (r < f ? -sol[bidx[r - s]] : 0.0);
+        vs[tid] = r < s ? ybuf[s0 + r] : (r < f ? -sol[bidx[r - s]] : 0.0);
       }
       __syncthreads();
-      const int lane = tid & 31, warp = tid >> 5;
-      for (int cc = 0; cc < 8; ++cc) {
-        const int kl = warp * 8 + cc, k = t.c0 + kl;
-        double acc = 0.0;
-        if (k < s) {
-          const double* col = F + k * ld;
-          for (int i = lane; i < 256; i += 32) {
-            const int r = t.r0 + i;
-            if (r < f && (r >= s || r >= k)) acc += col[r] * vs[i];
+      // warp: 8 columns; lane: rows i = lane + 32 m; 16 loads in flight per batch
+      double acc[8];
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) acc[cc] = 0.0;
+      const int kw = t.c0 + warp * 8;
+#pragma unroll
+      for (int m = 0; m < 8; m += 2) {
+        double fv[2][8];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = lane + 32 * (m + h), r = t.r0 + i;
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) {
+            const int k = kw + cc;
+            const bool ok = k < s && r < f && (r >= s || r >= k);
+            fv[h][cc] = ok ? __ldcs(F + r + (long long)k * ld) : 0.0;
           }
         }
-        acc = warp_sum(acc);
-        if (lane == 0) partial[(long long)t.part * 64 + kl] = acc;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) acc[cc] += fv[h][cc] * vs[lane + 32 * (m + h)];
+      }
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        const double v = warp_sum(acc[cc]);
+        if (lane == 0) partial[(long long)t.part * 64 + warp * 8 + cc] = v;
+      }
+      if (lane == 0) __threadfence();
+      __syncthreads();
+      const CsRed R = sp.br[t.red];
+      if (tid == 0) last = atomicAdd(cnt_b + t.red, 1) == R.np - 1;
+      __syncthreads();
+      if (last) {
+        __threadfence();
+        const int k = R.t0 + tid;
+        if (tid < 64 && k < s) {
+          double a = 0.0;
+          for (int p = 0; p < R.np; ++p) a += __ldcg(partial + (long long)(R.p0 + p) * 64 + tid);
+          sol[s0 + k] = a;
+        }
+        if (tid == 0) cnt_b[t.red] = 0;
       }
     }
-    grid.sync();
-    for (int ti = sp.br_off[l] + blockIdx.x * 4 + (tid >> 6); ti < sp.br_off[l + 1]; ti += gridDim.x * 4) {
-      const CsRed t = sp.br[ti];
-      const int node = t.node, s = fd.sep_size[node];
-      const int lt = tid & 63, k = t.t0 + lt;
-      if (k < s) {
-        double acc = 0.0;
-        for (int p = 0; p < t.np; ++p) acc += partial[(long long)(t.p0 + p) * 64 + lt];
-        sol[fd.sep_start[node] + k] = acc;
-      }
-    }
-    grid.sync();
+    gsync();
   }
 }
 
@@ -337,6 +379,7 @@ struct CoopState {
   unsigned long long* ptime = nullptr;
   CoopProgram pg{};
   SolveProgram sp{};
+  unsigned long long* stime = nullptr;  // per grid.sync timestamps of the solve (diagnostics)
   int grid_f = 0, grid_s = 0;
   size_t smem_f = 0;
 };
@@ -452,7 +495,10 @@ void coop_build(Ctx& c) {
     st.phase_type.push_back(tasks[ph.t0].type);
     st.phase_nt.push_back(ph.nt);
   }
-  if (getenv("BDDC_COOP_TIMING")) st.ptime = c.alloc<unsigned long long>(phases.size() + 1);
+  if (getenv("BDDC_COOP_TIMING")) {
+    st.ptime = c.alloc<unsigned long long>(phases.size() + 1);
+    st.stime = c.alloc<unsigned long long>(2 * L + 1);
+  }
   st.pg.tasks = c.upload(tasks.data(), tasks.size());
   st.pg.phases = c.upload(phases.data(), phases.size());
   st.pg.nphases = (int)phases.size();
@@ -480,6 +526,7 @@ void coop_build(Ctx& c) {
   st.sp.fr_off = c.upload(fr_off.data(), L + 1);
   st.sp.br_off = c.upload(br_off.data(), L + 1);
   st.sp.nlevels = L;
+  st.sp.nfr = fr_off[L];
 }
 
 void coop_release(const Ctx& c) { g_coop.erase(&c); }
@@ -523,9 +570,20 @@ void coop_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s) {
   FrontDev fd = c.fp.d;
   LevelView lv{c.sched.gat_ptr, c.sched.gat_off, c.sched.gat_src};
   double* partial = c.sched.partial;
-  void* args[] = {&fd, &lv, &st.sp, (void*)&rhs, (void*)&sol, &partial};
+  double* ybuf = c.sched.ybuf;
+  int* cnt = c.sched.red_cnt;
+  void* args[] = {&fd, &lv, &st.sp, (void*)&rhs, (void*)&sol, &partial, &ybuf, &cnt, &st.stime};
   BDDC_CUDA(cudaLaunchCooperativeKernel((void*)coop_solve_kernel, st.grid_s, 256, args, 0, s));
   BDDC_COUNT();
+  if (st.stime) {
+    const int L = st.sp.nlevels;
+    std::vector<unsigned long long> t(2 * L + 1);
+    BDDC_CUDA(cudaStreamSynchronize(s));
+    BDDC_CUDA(cudaMemcpy(t.data(), st.stime, sizeof(unsigned long long) * t.size(), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "coop solve (us): total %.1f\n", (t.back() - t[0]) * 1e-3);
+    for (int l = 0; l < L; ++l) fprintf(stderr, "  fwd L%-2d %7.1f\n", l, (t[l + 1] - t[l]) * 1e-3);
+    for (int q = 0; q < L; ++q) fprintf(stderr, "  bwd L%-2d %7.1f\n", L - 1 - q, (t[L + q + 1] - t[L + q]) * 1e-3);
+  }
 }
 
 }  // namespace bddc
