@@ -592,7 +592,7 @@ int bddc_dense_potrf(double* A, int n, int lda, long long stride, int count, int
     BDDC_CUDA(cudaMallocAsync((void**)&info, sizeof(int) * count, s));
     BDDC_CUDA(cudaMemsetAsync(info, 0x7f, sizeof(int) * count, s));
     double* scr = nullptr;
-    BDDC_CUDA(cudaMallocAsync((void**)&scr, sizeof(double) * kTileInvStride * count, s));
+    BDDC_CUDA(cudaMallocAsync((void**)&scr, sizeof(double) * trsm_scratch_doubles(n, count), s));
     potrf_batched(BMat{A, stride, lda}, n, n, count, info, scr, s);
     BDDC_CUDA(cudaFreeAsync(scr, s));
     if (info_host) {

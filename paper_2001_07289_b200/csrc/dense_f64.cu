@@ -244,17 +244,20 @@ static void tile_solve_gemm(TrsmKind kind, BMat Vinv, int nb, BMat B, int nother
 }
 
 void potrf_batched(BMat A, int n, int npiv, int count, int* info, double* scratch, cudaStream_t s) {
+  // the inverse of diagonal tile kb stays in scratch slot kb (trsm_batched's layout)
+  const long long sInv = (long long)ceil_div(npiv, kTile) * kTileInvStride;
   for (int k = 0; k < npiv; k += kTile) {
     const int nb = std::min(kTile, npiv - k);
+    double* inv = scratch + (k / kTile) * kTileInvStride;
     TileArgs t;
     t.L = A.p + k + (long long)k * A.ld; t.sL = A.stride; t.ldl = A.ld;
     t.n = nb; t.count = count; t.offset = k; t.info = info;
-    t.inv = scratch; t.sInv = kTileInvStride;
+    t.inv = inv; t.sInv = sInv;
     potrf_tile(t, s);
     const int rest = n - k - nb;
     if (rest <= 0) continue;
     BMat L21 = A.at(k + nb, k);
-    tile_solve_gemm(TRSM_RLT, BMat{scratch, kTileInvStride, kTile}, nb, L21, rest, count, s);
+    tile_solve_gemm(TRSM_RLT, BMat{inv, sInv, kTile}, nb, L21, rest, count, s);
     // trailing update A22 -= L21 L21^T (lower tiles only)
     BMat A22 = A.at(k + nb, k + nb);
     gemm_batched(false, true, rest, rest, nb, -1.0, L21, L21, 1.0, A22, count, s, true);
@@ -266,10 +269,10 @@ size_t trsm_scratch_doubles(int n, int count) {
 }
 
 void trsm_batched(TrsmKind kind, BMat L, int n, BMat B, int nother, int count, double* scratch,
-                  cudaStream_t s) {
+                  cudaStream_t s, bool have_inv) {
   const int nblk = ceil_div(n, kTile);
   const long long sInv = (long long)nblk * kTileInvStride;  // per batch entry
-  for (int kb = 0; kb < nblk; ++kb) {
+  for (int kb = 0; kb < nblk && !have_inv; ++kb) {
     const int k = kb * kTile;
     TileArgs t;
     t.L = L.p + k + (long long)k * L.ld; t.sL = L.stride; t.ldl = L.ld;

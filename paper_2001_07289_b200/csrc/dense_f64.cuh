@@ -77,14 +77,16 @@ struct BMat {
 
 // Blocked in-place lower Cholesky of `count` n x n matrices; factors the leading npiv
 // columns only (npiv < n: partial factorization, trailing block becomes the Schur complement).
-// scratch: count * 64 * 64 doubles (diagonal-tile inverses).
+// scratch: count * ceil(npiv/64) * 64 * 64 doubles; on return slot kb holds the inverse of
+// diagonal tile kb (the layout trsm_batched(..., have_inv = true) consumes).
 void potrf_batched(BMat A, int n, int npiv, int count, int* info, double* scratch, cudaStream_t s);
 // Blocked triangular solves with a batch of n x n lower factors L:
 //   left kinds: B is n x ncol; right kinds: B is nrow x n.
 // scratch: count * ceil(n/64) * 64 * 64 doubles. Diagonal tiles are inverted once (trtri)
-// and every tile solve is an in-place DMMA GEMM with the inverse.
+// and every tile solve is an in-place DMMA GEMM with the inverse. have_inv: scratch already
+// holds the inverses (left by potrf_batched on the same factor).
 void trsm_batched(TrsmKind kind, BMat L, int n, BMat B, int nother, int count, double* scratch,
-                  cudaStream_t s);
+                  cudaStream_t s, bool have_inv = false);
 size_t trsm_scratch_doubles(int n, int count);
 // C = alpha op(A) op(B) + beta C over a strided batch.
 void gemm_batched(bool tA, bool tB, int M, int N, int K, double alpha, BMat A, BMat B,

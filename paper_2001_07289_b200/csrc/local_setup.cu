@@ -278,7 +278,7 @@ size_t local_setup_workspace(const Geometry& g, int chunk) {
   const size_t SG = (size_t)g.nG_pad * g.nG_pad;
   const size_t X = (size_t)g.nG_pad * g.nc_pad;
   const size_t SC = (size_t)g.nc_pad * g.nc_pad;
-  return (size_t)chunk * (E + SG + X + 3 * SC);
+  return (size_t)chunk * (E + 2 * SG + 2 * X + 4 * SC);
 }
 
 void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
@@ -307,6 +307,9 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
     double* SC = X + (size_t)chunk * phS;
     double* P = SC + (size_t)chunk * scS;
     double* SCc = P + (size_t)chunk * scS;  // S_C before its factorization
+    double* LIv = SCc + (size_t)chunk * scS;  // L_S^{-1}
+    double* Y = LIv + (size_t)chunk * lsS;    // G S_C^{-1}
+    double* SCi = Y + (size_t)chunk * phS;    // S_C^{-1}
     double* LS = c.LS + sub0 * lsS;
     double* PH = c.Phi + sub0 * phS;
     BDDC_CUDA(cudaMemsetAsync(Wd, 0, sizeof(double) * 2 * (size_t)chunk * wS, s));
@@ -361,41 +364,64 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
     BDDC_LAUNCH_CHECK();
     potrf_batched(LSb, G.nG_pad, G.nG_pad, cnt, c.info_k + sub0, c.tinv, s);
     c.prof.end("setup.SK", s);
+    BMat SGb{SG, lsS, G.nG_pad};
+    BMat LIb{LIv, lsS, G.nG_pad};
+    {
+      // 5a. L_S^{-1} (the diagonal-tile inverses are left in c.tinv by the factorization)
+      PhaseScope pli(c.prof, "setup.Linv", s);
+      { identity_kernel<<<cnt, 256, 0, s>>>(LIv, G.nG_pad, lsS); BDDC_COUNT(); }
+      BDDC_LAUNCH_CHECK();
+      trsm_batched(TRSM_LLN, LSb, G.nG_pad, LIb, G.nG_pad, cnt, c.tinv, s, true);
+    }
     if (G.nc_pad > 0) {
       PhaseScope pphi(c.prof, "setup.Phi", s);
-      // 5. G = L_S^{-1} C^T ; S_C = G^T G ; Phi = L_S^{-T} G S_C^{-1}
+      // 5b. G = L_S^{-1} C^T ; S_C = G^T G ; Phi = L_S^{-T} (G S_C^{-1})   (C Phi = I)
       { build_ct_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, c.Phi); BDDC_COUNT(); }
       BDDC_LAUNCH_CHECK();
       BMat PHb{PH, phS, G.nG_pad};
       BMat SCb{SC, scS, G.nc_pad};
-      trsm_batched(TRSM_LLN, LSb, G.nG_pad, PHb, G.nc_pad, cnt, c.tinv, s);
-      gemm_batched(true, false, G.nc_pad, G.nc_pad, G.nG_pad, 1.0, PHb, PHb, 0.0, SCb, cnt, s);
+      BMat Xb{X, phS, G.nG_pad};
+      BMat Yb{Y, phS, G.nG_pad};
+      BMat SCib{SCi, scS, G.nc_pad};
+      gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nG_pad, 1.0, LIb, PHb, 0.0, Xb, cnt, s);
+      gemm_batched(true, false, G.nc_pad, G.nc_pad, G.nG_pad, 1.0, Xb, Xb, 0.0, SCb, cnt, s);
       { sc_pad_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, SC); BDDC_COUNT(); }
       BDDC_LAUNCH_CHECK();
       BDDC_CUDA(cudaMemcpyAsync(SCc, SC, sizeof(double) * cnt * scS, cudaMemcpyDeviceToDevice, s));
       potrf_batched(SCb, G.nc_pad, G.nc_pad, cnt, nullptr, c.tinv, s);
-      trsm_batched(TRSM_RLT, SCb, G.nc_pad, PHb, G.nG_pad, cnt, c.tinv, s);
-      trsm_batched(TRSM_RLN, SCb, G.nc_pad, PHb, G.nG_pad, cnt, c.tinv, s);
-      trsm_batched(TRSM_LLT, LSb, G.nG_pad, PHb, G.nc_pad, cnt, c.tinv, s);
+      // S_C^{-1} = L_C^{-T} L_C^{-1}
+      const int ncb = ceil_div(G.nc_pad, kTile);
+      BMat LCi{c.tinv, (long long)ncb * kTileInvStride, kTile};
+      if (ncb > 1) {  // general: L_C^{-1} by blocked solves into the SCi buffer
+        { identity_kernel<<<cnt, 256, 0, s>>>(SCi, G.nc_pad, scS); BDDC_COUNT(); }
+        BDDC_LAUNCH_CHECK();
+        trsm_batched(TRSM_LLN, SCb, G.nc_pad, SCib, G.nc_pad, cnt, c.tinv, s, true);
+        BDDC_CUDA(cudaMemcpyAsync(P, SCi, sizeof(double) * cnt * scS, cudaMemcpyDeviceToDevice, s));
+        LCi = BMat{P, scS, G.nc_pad};
+      }
+      gemm_batched(true, false, G.nc_pad, G.nc_pad, G.nc_pad, 1.0, LCi, LCi, 0.0, SCib, cnt, s);
+      gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nc_pad, 1.0, Xb, SCib, 0.0, Yb, cnt, s);
+      gemm_batched(true, false, G.nG_pad, G.nc_pad, G.nG_pad, 1.0, LIb, Yb, 0.0, PHb, cnt, s);
       // 6. P = Phi^T (S_Gamma Phi)
-      BMat SGb{SG, lsS, G.nG_pad};
-      BMat Xb{X, phS, G.nG_pad};
       BMat Pb{P, scS, G.nc_pad};
       gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nG_pad, 1.0, SGb, PHb, 0.0, Xb, cnt, s);
       gemm_batched(true, false, G.nc_pad, G.nc_pad, G.nG_pad, 1.0, PHb, Xb, 0.0, Pb, cnt, s);
       { finish_local_kernel<<<cnt, 256, 0, s>>>(G, sub0, c.coarse_scaling, c.diag_s, c.cscale, P,
                                               c.Sloc); BDDC_COUNT(); }
       BDDC_LAUNCH_CHECK();
-      // 7. explicit interface operator T = (I - Phi C) S_K^{-1} = S_K^{-1} - Phi S_C Phi^T
+    }
+    {
+      // 7. explicit interface operator T = (I - Phi C) S_K^{-1} = L^{-T} L^{-1} - Phi S_C Phi^T
       //    (symmetric; replaces L_S so the apply's local Neumann solve is one GEMV)
       PhaseScope pt(c.prof, "setup.T", s);
-      { identity_kernel<<<cnt, 256, 0, s>>>(SG, G.nG_pad, lsS); BDDC_COUNT(); }
-      BDDC_LAUNCH_CHECK();
-      trsm_batched(TRSM_LLN, LSb, G.nG_pad, SGb, G.nG_pad, cnt, c.tinv, s);  // SG <- L_S^{-1}
-      gemm_batched(true, false, G.nG_pad, G.nG_pad, G.nG_pad, 1.0, SGb, SGb, 0.0, LSb, cnt, s);
-      BMat SCcb{SCc, scS, G.nc_pad};
-      gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nc_pad, 1.0, PHb, SCcb, 0.0, Xb, cnt, s);
-      gemm_batched(false, true, G.nG_pad, G.nG_pad, G.nc_pad, -1.0, Xb, PHb, 1.0, LSb, cnt, s);
+      gemm_batched(true, false, G.nG_pad, G.nG_pad, G.nG_pad, 1.0, LIb, LIb, 0.0, LSb, cnt, s);
+      if (G.nc_pad > 0) {
+        BMat PHb{PH, phS, G.nG_pad};
+        BMat Xb{X, phS, G.nG_pad};
+        BMat SCcb{SCc, scS, G.nc_pad};
+        gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nc_pad, 1.0, PHb, SCcb, 0.0, Xb, cnt, s);
+        gemm_batched(false, true, G.nG_pad, G.nG_pad, G.nc_pad, -1.0, Xb, PHb, 1.0, LSb, cnt, s);
+      }
     }
   }
 }
