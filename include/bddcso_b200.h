@@ -120,6 +120,24 @@ double bddc_profile_read(bddc_ctx* ctx, const char* phase, long long* count);
    "csr_val", "fronts") to host; returns the element count (or -1) */
 long long bddc_debug_copy(bddc_ctx* ctx, const char* name, double* host, long long capacity);
 
+/* multi-GPU: one rank per GPU, each owning a slab of the subdomain lattice
+   along the last axis (rows [r*R/world, (r+1)*R/world) of the R subdomain rows). Call one
+   of the comm_init functions before bddc_setup; every rank passes the same global
+   descriptor. Vectors stay global-length on every rank: inputs must be valid on the rank's
+   active rows (both cut lines included), outputs are valid on its owned rows (a cut line
+   belongs to the lower rank). The reference is single-process; this replaces its
+   per-subdomain loop (bddc.py:419-511) across GPUs.
+   host exchange callback ops (host buffers of n doubles):
+     1 sendrecv(a -> peer, b <- peer), 2 broadcast(a from root = peer),
+     3 sum-allreduce(a), 4 max-allreduce(a); return 0 on success */
+typedef int (*bddc_host_exchange_fn)(void* user, int op, double* a, double* b, long long n, int peer);
+int bddc_nccl_unique_id(void* out128);
+int bddc_comm_init_nccl(bddc_ctx* ctx, int rank, int world, const void* unique_id128);
+int bddc_comm_init_host(bddc_ctx* ctx, int rank, int world, bddc_host_exchange_fn fn, void* user);
+/* host-only: slab of `rank` for a dim/cells/subs box; out[10] = s_lo, s_hi, f_lo, f_hi, fo_lo,
+   fo_hi, halo_lo_send, halo_lo_recv, halo_hi_send, halo_hi_recv (free-dof offsets, -1 none) */
+int bddc_partition_info(int dim, const int* cells, const int* subs, int rank, int world, long long* out);
+
 /* dense FP64 batched kernels (column-major, even leading dimensions, device pointers) */
 int bddc_dense_potrf(double* A, int n, int lda, long long stride, int count, int* info_host,
                      void* stream);

@@ -26,7 +26,9 @@ EXPORTS = (
     "bddc_create", "bddc_destroy", "bddc_setup", "bddc_refactor", "bddc_apply", "bddc_harmonic",
     "bddc_spmv", "bddc_pcg", "bddc_pcg_host", "bddc_get_stats", "bddc_sync",
     "bddc_kernel_launches_per_apply", "bddc_debug_copy", "bddc_launch_count",
-    "bddc_event_record", "bddc_event_elapsed_ms", "bddc_profile", "bddc_profile_read", "bddc_dense_potrf", "bddc_dense_trsm", "bddc_dense_gemm",
+    "bddc_event_record", "bddc_event_elapsed_ms", "bddc_profile", "bddc_profile_read",
+    "bddc_nccl_unique_id", "bddc_comm_init_nccl", "bddc_comm_init_host", "bddc_partition_info",
+    "bddc_dense_potrf", "bddc_dense_trsm", "bddc_dense_gemm",
 )
 
 
@@ -102,6 +104,10 @@ def load(required: bool = True):
     lib.bddc_profile.argtypes = [_vp, _i]
     lib.bddc_profile_read.argtypes = [_vp, C.c_char_p, _pll]
     lib.bddc_profile_read.restype = _d
+    lib.bddc_nccl_unique_id.argtypes = [_vp]
+    lib.bddc_comm_init_nccl.argtypes = [_vp, _i, _i, _vp]
+    lib.bddc_comm_init_host.argtypes = [_vp, _i, _i, _vp, _vp]
+    lib.bddc_partition_info.argtypes = [_i, _pi, _pi, _i, _i, _pll]
     lib.bddc_dense_potrf.argtypes = [_vp, _i, _i, _ll, _i, _pi, _vp]
     lib.bddc_dense_trsm.argtypes = [_i, _vp, _i, _i, _ll, _vp, _i, _i, _ll, _i, _vp]
     lib.bddc_dense_gemm.argtypes = [_i, _i, _i, _i, _i, _d, _vp, _i, _ll, _vp, _i, _ll, _d, _vp,

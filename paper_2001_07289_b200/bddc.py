@@ -24,6 +24,7 @@ from .layout import DevicePlan, build_device_plan
 from .linalg import NotSpdError, UnderconstrainedError
 from .mesh import AssembledSystem, element_matrix_box
 from .partition import ObjectTable, PartitionPair
+from .shard import slab_ranges
 from .weights import (ConstraintTable, Recipe, RecipeError, WeightingOperator,
                       select_constraints)
 
@@ -71,7 +72,7 @@ class BddcOperator:
 
     def __init__(self, system: AssembledSystem, pair: PartitionPair, weights: WeightingOperator,
                  recipe: Recipe, constraints: ConstraintTable, plan: DevicePlan,
-                 coarse_scaling: str = "reference", device: int = 0):
+                 coarse_scaling: str = "reference", device: int = 0, comm=None):
         self.system = system
         self.pair = pair
         self.weights = weights
@@ -90,6 +91,14 @@ class BddcOperator:
         rc = self._lib.bddc_create(device, C.byref(self._ctx))
         if rc:
             raise RuntimeError(f"bddc_create failed ({rc})")
+        # multi-GPU (shard.py): this rank's slab; vectors stay global-length, inputs valid on
+        # the active rows, outputs on the owned rows
+        self.comm = comm
+        rank, world = (comm.rank, comm.world) if comm is not None else (0, 1)
+        mesh = system.mesh
+        self.slab = slab_ranges(mesh.dim, mesh.cells_per_dim, pair.box_layout[0], rank, world)
+        if comm is not None:
+            comm.attach(self._lib, self._ctx)
         self._desc_arrays = None
         self._desc = None
 
@@ -254,14 +263,35 @@ class BddcOperator:
             bh = np.ascontiguousarray(b, dtype=np.float64)
             if bh.shape != (self.n,):
                 raise ValueError(f"right-hand side has shape {bh.shape}, expected ({self.n},)")
-            x = np.empty(self.n)
+            x = np.zeros(self.n)
             rc = self._lib.bddc_pcg_host(self._ctx, _capi.ptr(bh, C.c_double),
                                          _capi.ptr(x, C.c_double), float(tol), int(max_iters),
                                          _capi.ptr(alphas, C.c_double), _capi.ptr(betas, C.c_double),
                                          _capi.ptr(resid, C.c_double), C.byref(rep), err, len(err))
+            if rc == 0:
+                x = self.allgather_owned(x)
         raise_for(rc, err.value.decode(errors="replace"))
         k = rep.iterations
         return x, alphas[:k].copy(), betas[: max(k - 1, 0)].copy(), resid[: k + 1].copy(), k, bool(rep.converged)
+
+    @property
+    def world(self) -> int:
+        return self.comm.world if self.comm is not None else 1
+
+    def allgather_owned(self, v: np.ndarray) -> np.ndarray:
+        """Sharded: the full vector from every rank's owned rows (host numpy, all ranks)."""
+        if self.world == 1:
+            return v
+        import torch.distributed as dist
+
+        parts = [None] * self.world
+        sl = self.slab
+        dist.all_gather_object(parts, (sl.fo_lo, np.ascontiguousarray(v[sl.fo_lo:sl.fo_hi])),
+                               group=self.comm.group)
+        out = np.zeros(self.n)
+        for lo, part in parts:
+            out[lo:lo + len(part)] = part
+        return out
 
     def debug_buffer(self, name: str) -> np.ndarray:
         """Copy an internal device buffer to host (diagnostics / kernel-level tests)."""
@@ -294,10 +324,12 @@ class BddcOperator:
 
 def build_bddc(system: AssembledSystem, pair: PartitionPair, objects: ObjectTable, recipe,
                weights: WeightingOperator, coarse_scaling: str = "reference",
-               device: int = 0) -> BddcOperator:
+               device: int = 0, comm=None) -> BddcOperator:
     """Assemble the preconditioner on the GPU (bddc.py:393-523).
 
     The recipe is validated (RecipeError) before any factorization, as in the reference.
+    ``comm`` (shard.NcclComm / shard.HostComm): this process is one rank of a sharded
+    operator; every rank passes the same global problem.
     """
     if isinstance(recipe, str):
         recipe = Recipe.parse(recipe)
@@ -307,7 +339,7 @@ def build_bddc(system: AssembledSystem, pair: PartitionPair, objects: ObjectTabl
     constraints = select_constraints(objects, recipe, pair)
     plan = build_device_plan(pair, constraints, weights)
     prep = time.perf_counter() - t0
-    op = BddcOperator(system, pair, weights, recipe, constraints, plan, coarse_scaling, device)
+    op = BddcOperator(system, pair, weights, recipe, constraints, plan, coarse_scaling, device, comm)
     op.times.prep_s = prep
     op._setup()
     return op

@@ -17,7 +17,7 @@ namespace {
 template <int DIM>
 __global__ void spmv_kernel(Geometry G, const double* __restrict__ alpha, const double* __restrict__ x,
                             double* __restrict__ y) {
-  for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < G.n;
+  for (long long f = G.f_lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; f < G.f_hi;
        f += (long long)gridDim.x * blockDim.x) {
     int g0, g1, g2;
     free_coords(G, f, g0, g1, g2);
@@ -29,7 +29,7 @@ __global__ void spmv_kernel(Geometry G, const double* __restrict__ alpha, const 
 template <int DIM>
 __global__ void residual_kernel(Geometry G, const double* __restrict__ alpha, const double* __restrict__ r,
                                 const double* __restrict__ x, double* __restrict__ y) {
-  for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < G.n;
+  for (long long f = G.f_lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; f < G.f_hi;
        f += (long long)gridDim.x * blockDim.x) {
     int g0, g1, g2;
     free_coords(G, f, g0, g1, g2);
@@ -39,11 +39,11 @@ __global__ void residual_kernel(Geometry G, const double* __restrict__ alpha, co
 
 // rpg[g] = r - (A u1) at interface dofs
 template <int DIM>
-__global__ void gamma_residual_kernel(Geometry G, int n_gamma, const long long* __restrict__ gdof,
+__global__ void gamma_residual_kernel(Geometry G, const long long* __restrict__ gdof,
                                       const double* __restrict__ alpha, const double* __restrict__ r,
                                       const double* __restrict__ u1, double* __restrict__ rpg) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= n_gamma) return;
+  const int g = G.g_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= G.g_hi) return;
   const long long f = gdof[g];
   int g0, g1, g2;
   free_coords(G, f, g0, g1, g2);
@@ -115,12 +115,12 @@ __global__ void __launch_bounds__(32 * kBtWarps) bt_solve_kernel(Geometry G, Loc
   const BtSmem L = bt_smem(G);
   const int M = G.m_pad, Tm = G.Tm, nbo = G.nbo, nblk = G.nblk;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int sub = blockIdx.x * kBtWarps + warp;
+  const int sub = G.s_lo + blockIdx.x * kBtWarps + warp;
   double* y = sm + warp * L.per_warp();        // nI_pad
   double* stg = y + L.nI;                      // kBtStages x [W packed | coupling rows]
   double* tv = stg + kBtStages * L.stage();    // M: the GEMV input vector
 
-  if (sub >= G.nsub) return;
+  if (sub >= G.s_hi) return;
   int p[3];
   sub_coords(G, sub, p);
   const double* li = LI + (long long)sub * G.li_stride;
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(128) local_gamma1_kernel(Geometry G, SubTables
   extern __shared__ double sm[];
   const int n = G.nG_pad, nc = G.nc_pad;
   double* rho = sm;  // n
-  const int sub = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const int sub = G.s_lo + blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   const long long so = (long long)sub * n;
   for (int s = tid; s < n; s += nt) {
     const int g = st.slot_gamma[so + s];
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(128) local_gamma2_kernel(Geometry G, SubTables
                                                            double* wloc) {
   __shared__ double e[1024];
   const int n = G.nG_pad, nc = G.nc_pad;
-  const int sub = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const int sub = G.s_lo + blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   const double c = cscale[sub];
   for (int k = tid; k < nc; k += nt) {
     const int j = st.con_coarse[(long long)sub * nc + k];
@@ -319,11 +319,11 @@ __global__ void __launch_bounds__(128) local_gamma2_kernel(Geometry G, SubTables
 }
 
 // z[gamma dof] = sum over owner slots (ascending subdomain = reference summation order)
-__global__ void gamma_gather_kernel(int n_gamma, int W, const long long* __restrict__ gdof,
+__global__ void gamma_gather_kernel(int g_lo, int g_hi, int W, const long long* __restrict__ gdof,
                                     const int* __restrict__ gslots, const double* __restrict__ wloc,
                                     double* __restrict__ z) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= n_gamma) return;
+  const int g = g_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= g_hi) return;
   double acc = 0.0;
   for (int w = 0; w < W; ++w) {
     const int s = gslots[(long long)g * W + w];
@@ -353,7 +353,7 @@ int grid_for(long long n, int threads) {
 
 void spmv(Ctx& c, const double* x, double* y, cudaStream_t s) {
   const Geometry& G = c.geo;
-  const int th = 256, gr = grid_for(G.n, th);
+  const int th = 256, gr = grid_for(G.f_hi - G.f_lo, th);
   if (G.dim == 2) { spmv_kernel<2><<<gr, th, 0, s>>>(G, c.alpha, x, y); BDDC_COUNT(); }
   else { spmv_kernel<3><<<gr, th, 0, s>>>(G, c.alpha, x, y); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
@@ -369,7 +369,7 @@ static void bt_solve(Ctx& c, const double* in, double* out, cudaStream_t s) {
     BDDC_CUDA(cudaFuncSetAttribute(bt_solve_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
-  const int grid = ceil_div(G.nsub, kBtWarps);
+  const int grid = ceil_div(G.s_hi - G.s_lo, kBtWarps);
   if (G.m_pad <= 32) { bt_solve_kernel<1><<<grid, 32 * kBtWarps, smem, s>>>(G, c.lt, c.LI, in, out); BDDC_COUNT(); }
   else { bt_solve_kernel<2><<<grid, 32 * kBtWarps, smem, s>>>(G, c.lt, c.LI, in, out); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
@@ -378,7 +378,7 @@ static void bt_solve(Ctx& c, const double* in, double* out, cudaStream_t s) {
 // out holds g on Gamma and 0 on interiors; c.v1 must be zero.
 void harmonic_interior(Ctx& c, double* out, cudaStream_t s) {
   const Geometry& G = c.geo;
-  const int th = 256, gr = grid_for(G.n, th);
+  const int th = 256, gr = grid_for(G.f_hi - G.f_lo, th);
   if (G.dim == 2) { residual_kernel<2><<<gr, th, 0, s>>>(G, c.alpha, c.v1, out, c.v2); BDDC_COUNT(); }
   else { residual_kernel<3><<<gr, th, 0, s>>>(G, c.alpha, c.v1, out, c.v2); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
@@ -388,42 +388,48 @@ void harmonic_interior(Ctx& c, double* out, cudaStream_t s) {
 void apply_bddc(Ctx& c, const double* r, double* z, cudaStream_t s) {
   const Geometry& G = c.geo;
   const int th = 256;
+  const int ng = G.g_hi - G.g_lo, nl = G.s_hi - G.s_lo;
   // u1 = A_II^{-1} r_I (zero on Gamma)
   BDDC_CUDA(cudaMemsetAsync(c.v1, 0, sizeof(double) * G.n, s));
   bt_solve(c, r, c.v1, s);
   if (c.n_gamma > 0) {
-    if (G.dim == 2)
-      { gamma_residual_kernel<2><<<ceil_div(c.n_gamma, th), th, 0, s>>>(G, c.n_gamma, c.gamma_dof, c.alpha, r, c.v1, c.rpg); BDDC_COUNT(); }
-    else
-      { gamma_residual_kernel<3><<<ceil_div(c.n_gamma, th), th, 0, s>>>(G, c.n_gamma, c.gamma_dof, c.alpha, r, c.v1, c.rpg); BDDC_COUNT(); }
-    BDDC_LAUNCH_CHECK();
+    exchange_dof_halo(c, c.v1, s);  // sharded: u1 on the rows next to the cut lines
+    if (ng > 0) {
+      if (G.dim == 2)
+        { gamma_residual_kernel<2><<<ceil_div(ng, th), th, 0, s>>>(G, c.gamma_dof, c.alpha, r, c.v1, c.rpg); BDDC_COUNT(); }
+      else
+        { gamma_residual_kernel<3><<<ceil_div(ng, th), th, 0, s>>>(G, c.gamma_dof, c.alpha, r, c.v1, c.rpg); BDDC_COUNT(); }
+      BDDC_LAUNCH_CHECK();
+    }
     const size_t smem1 = sizeof(double) * G.nG_pad;
     c.prof.begin("apply.gamma1", s);
-    { local_gamma1_kernel<<<G.nsub, 128, smem1, s>>>(G, c.st, c.LS, c.Phi, c.cscale, c.rpg, c.qloc,
-                                                   c.uloc); BDDC_COUNT(); }
+    { local_gamma1_kernel<<<nl, 128, smem1, s>>>(G, c.st, c.LS, c.Phi, c.cscale, c.rpg, c.qloc,
+                                               c.uloc); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
     c.prof.end("apply.gamma1", s);
     if (c.fp.n_coarse > 0) {
       PhaseScope pc(c.prof, "apply.coarse", s);
+      allgather_subs(c, c.qloc, G.nc_pad, s);  // sharded: every rank's local coarse rhs
       { coarse_gather_kernel<<<ceil_div(c.fp.n_coarse, th), th, 0, s>>>(c.fp.n_coarse, c.fp.W,
                                                                      c.fp.coarse_slots, c.qloc, c.crhs); BDDC_COUNT(); }
       BDDC_LAUNCH_CHECK();
       coarse_solve(c, c.crhs, c.csol, s);
     }
     c.prof.begin("apply.gamma2", s);
-    { local_gamma2_kernel<<<G.nsub, 128, 0, s>>>(G, c.st, c.Phi, c.cscale, c.csol, c.uloc,
-                                               c.wloc); BDDC_COUNT(); }
+    { local_gamma2_kernel<<<nl, 128, 0, s>>>(G, c.st, c.Phi, c.cscale, c.csol, c.uloc,
+                                           c.wloc); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
     c.prof.end("apply.gamma2", s);
+    exchange_boundary_rows(c, c.wloc, G.nG_pad, s);  // sharded: w of the neighbours' cut rows
   }
   BDDC_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * G.n, s));
-  if (c.n_gamma > 0) {
-    { gamma_gather_kernel<<<ceil_div(c.n_gamma, th), th, 0, s>>>(c.n_gamma, G.npe,
-                                                               c.gamma_dof, c.gamma_slots, c.wloc, z); BDDC_COUNT(); }
+  if (ng > 0) {
+    { gamma_gather_kernel<<<ceil_div(ng, th), th, 0, s>>>(G.g_lo, G.g_hi, G.npe,
+                                                        c.gamma_dof, c.gamma_slots, c.wloc, z); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
   }
   // z_I = A_II^{-1} (r - A z_Gamma)_I
-  const int gr = grid_for(G.n, th);
+  const int gr = grid_for(G.f_hi - G.f_lo, th);
   if (G.dim == 2) { residual_kernel<2><<<gr, th, 0, s>>>(G, c.alpha, r, z, c.v2); BDDC_COUNT(); }
   else { residual_kernel<3><<<gr, th, 0, s>>>(G, c.alpha, r, z, c.v2); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();

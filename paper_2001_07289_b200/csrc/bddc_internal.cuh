@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include "../../include/bddcso_b200.h"
 #include "common.cuh"
 #include "dense_f64.cuh"
 
@@ -38,6 +39,38 @@ struct Geometry {
   int nbo;
   int bo_dx[9], bo_dy[9];
   long long li_stride;
+  // this rank's slab of the subdomain lattice (last axis); world = 1: everything
+  int s_lo, s_hi;          // subdomains [s_lo, s_hi) (global ids)
+  long long f_lo, f_hi;    // active free dofs: node rows from the lower to the upper cut line
+  long long fo_lo, fo_hi;  // owned free dofs (a cut line belongs to the lower rank): dots
+  int g_lo, g_hi;          // active interface dofs (indices into the ascending Gamma list)
+};
+
+// Rank-to-rank exchanges of the sharded operator (multigpu.cu). All pointers are device
+// pointers on the operator's stream; implementations: NCCL (one rank per GPU) and a host
+// callback transport (tests: ranks sharing one GPU, exchanges staged through the host).
+struct Transport {
+  int rank = 0, world = 1;
+  virtual ~Transport() {}
+  // send [lo_send, +lo_n) to rank-1 and receive [lo_recv, +lo_n) from it; same with rank+1
+  virtual void neighbors(const double* lo_send, double* lo_recv, long long lo_n, const double* hi_send,
+                         double* hi_recv, long long hi_n, cudaStream_t s) = 0;
+  // in place: block r ([off[r], off[r] + cnt[r])) comes from rank r
+  virtual void allgatherv(double* buf, const long long* off, const long long* cnt, cudaStream_t s) = 0;
+  virtual void allreduce_sum(double* buf, int n, cudaStream_t s) = 0;
+  // host value, max over ranks (error agreement)
+  virtual int allreduce_max_host(int v) = 0;
+};
+
+// Slab bookkeeping derived from the geometry (host).
+struct Slab {
+  long long row_len = 0;  // free dofs per node row (2D) / plane (3D) of the last axis
+  // halo rows of dof vectors (u1, p): offsets in free-dof index, -1 if no neighbour
+  long long lo_send = -1, lo_recv = -1, hi_send = -1, hi_recv = -1;
+  // boundary subdomain rows for the interface gather (w values, nG_pad per subdomain)
+  int sub_row = 0;  // subdomains per lattice row (last axis)
+  int lo_rows_send = -1, lo_rows_recv = -1, hi_rows_send = -1, hi_rows_recv = -1;  // first sub
+  std::vector<long long> sub_off, sub_cnt;  // per rank: [s_lo, s_hi) in subdomains
 };
 
 // Decoded local node information (host-built tables, device copies).
@@ -252,6 +285,9 @@ struct Ctx {
   double* red = nullptr;     // reduction partials
   double* scal = nullptr;    // device scalars
   double* h_scal = nullptr;  // pinned host mirror
+  // multi-GPU: slab of this rank and the exchange transport (null: single rank)
+  Slab slab;
+  Transport* tp = nullptr;
   // timing of the last setup (ms) per phase
   float t_local_ms = 0, t_coarse_ms = 0, t_upload_ms = 0;
   std::vector<void*> allocations;
@@ -298,5 +334,14 @@ struct PcgResult {
 PcgResult pcg_solve(Ctx& c, const double* b, double* x, double tol, int max_iters, double* alphas,
                     double* betas, double* resid);
 double dot(Ctx& c, const double* a, const double* b, long long n, cudaStream_t s);
+// multigpu.cu
+void slab_partition(Geometry& G, Slab& sl, int rank, int world, const long long* gamma_dof, int n_gamma);
+void exchange_dof_halo(Ctx& c, double* v, cudaStream_t s);        // rows next to the cut lines
+void exchange_boundary_rows(Ctx& c, double* per_sub, int stride, cudaStream_t s);  // nG_pad / sub
+void allgather_subs(Ctx& c, double* per_sub, long long stride, cudaStream_t s);   // [nsub x stride]
+void allreduce_scalars(Ctx& c, double* d, int n, cudaStream_t s);
+Transport* make_nccl_transport(int rank, int world, const void* unique_id);
+Transport* make_host_transport(int rank, int world, bddc_host_exchange_fn fn, void* user);
+void nccl_unique_id(void* out);
 
 }  // namespace bddc

@@ -73,6 +73,8 @@ void numeric_setup(bddc_ctx* h) {
   if (c.fp.nnodes) BDDC_CUDA(cudaMemsetAsync(c.fp.info, 0x7f, sizeof(int) * c.fp.nnodes, s));
   BDDC_CUDA(cudaEventRecord(e0, s));
   local_setup(c, h->ws, h->ws_doubles);
+  // sharded: every rank assembles the replicated coarse matrix from all local blocks
+  allgather_subs(c, c.Sloc, (long long)c.geo.nc_pad * c.geo.nc_pad, s);
   BDDC_CUDA(cudaEventRecord(e1, s));
   coarse_assemble_and_factor(c);
   BDDC_CUDA(cudaEventRecord(e2, s));
@@ -86,15 +88,21 @@ void numeric_setup(bddc_ctx* h) {
   std::vector<int> info(nsub), info_k(nsub);
   BDDC_CUDA(cudaMemcpy(info.data(), c.info, sizeof(int) * nsub, cudaMemcpyDeviceToHost));
   BDDC_CUDA(cudaMemcpy(info_k.data(), c.info_k, sizeof(int) * nsub, cudaMemcpyDeviceToHost));
-  for (int i = 0; i < nsub; ++i)
-    if (info[i] != kNoFail)
-      throw ApiError{2, "subdomain " + std::to_string(i) +
-                            ": matrix not SPD: nonpositive pivot at index " + std::to_string(info[i])};
-  for (int i = 0; i < nsub; ++i)
-    if (info_k[i] != kNoFail)
-      throw ApiError{3, "subdomain " + std::to_string(i) +
-                            ": saddle system numerically singular (floating subdomain "
-                            "underconstrained or rank-deficient constraints)"};
+  int bad_sub = -1, code = 0;
+  for (int i = c.geo.s_lo; i < c.geo.s_hi && !code; ++i)
+    if (info[i] != kNoFail) { code = 2; bad_sub = i; }
+  for (int i = c.geo.s_lo; i < c.geo.s_hi && !code; ++i)
+    if (info_k[i] != kNoFail) { code = 3; bad_sub = i; }
+  // all ranks agree on failure (a rank that failed alone would leave the others waiting)
+  const int any = c.tp ? c.tp->allreduce_max_host(code) : code;
+  if (code == 2)
+    throw ApiError{2, "subdomain " + std::to_string(bad_sub) +
+                          ": matrix not SPD: nonpositive pivot at index " + std::to_string(info[bad_sub])};
+  if (code == 3)
+    throw ApiError{3, "subdomain " + std::to_string(bad_sub) +
+                          ": saddle system numerically singular (floating subdomain "
+                          "underconstrained or rank-deficient constraints)"};
+  if (any) throw ApiError{any, "setup failed on another rank"};
   if (c.fp.nnodes) {
     std::vector<int> fi(c.fp.nnodes);
     BDDC_CUDA(cudaMemcpy(fi.data(), c.fp.info, sizeof(int) * c.fp.nnodes, cudaMemcpyDeviceToHost));
@@ -276,6 +284,14 @@ void do_setup(bddc_ctx* h, const bddc_setup_desc* d) {
     }
   }
   G.li_stride = round_up((long long)G.nblk * G.Tm + (long long)G.nblk * G.m_pad * G.nbo, 2);
+  if (d->n_gamma && !d->gamma_dof) throw ApiError{1, "gamma_dof missing"};
+  for (int g = 1; g < d->n_gamma; ++g)
+    if (d->gamma_dof[g] <= d->gamma_dof[g - 1]) throw ApiError{1, "gamma_dof must be ascending"};
+  try {
+    slab_partition(G, c.slab, c.tp ? c.tp->rank : 0, c.tp ? c.tp->world : 1, d->gamma_dof, d->n_gamma);
+  } catch (const std::runtime_error& e) {
+    throw ApiError{1, e.what()};
+  }
   c.element = d->element;
   c.coarse_scaling = d->coarse_scaling;
   h->ncells = ncells;
@@ -304,10 +320,13 @@ void do_setup(bddc_ctx* h, const bddc_setup_desc* d) {
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
 
-  // persistent factors and workspaces
-  c.LI = c.alloc<double>((size_t)G.nsub * G.li_stride);
-  c.LS = c.alloc<double>((size_t)G.nsub * G.nG_pad * G.nG_pad);
-  c.Phi = c.alloc<double>((size_t)G.nsub * G.nG_pad * G.nc_pad);
+  // persistent factors (this rank's subdomains; the base pointers are shifted so kernels
+  // index them with global subdomain ids) and workspaces
+  const size_t nl = (size_t)(G.s_hi - G.s_lo);
+  const long long lsS = (long long)G.nG_pad * G.nG_pad, phS = (long long)G.nG_pad * G.nc_pad;
+  c.LI = c.alloc<double>(nl * G.li_stride) - (long long)G.s_lo * G.li_stride;
+  c.LS = c.alloc<double>(nl * lsS) - (long long)G.s_lo * lsS;
+  c.Phi = c.alloc<double>(nl * phS) - (long long)G.s_lo * phS;
   c.Sloc = c.alloc<double>((size_t)G.nsub * G.nc_pad * G.nc_pad);
   c.cscale = c.alloc<double>(G.nsub);
   c.diag_s = c.alloc<double>(G.nsub);
@@ -335,12 +354,12 @@ void do_setup(bddc_ctx* h, const bddc_setup_desc* d) {
   size_t free_b = 0, total_b = 0;
   BDDC_CUDA(cudaMemGetInfo(&free_b, &total_b));
   const size_t per = local_setup_workspace(G, 1);
-  size_t want = per * G.nsub;
+  size_t want = per * nl;
   size_t cap = (size_t)(0.6 * free_b) / sizeof(double);
   size_t use = std::min(want, std::max(cap - cap % per, per));
   h->ws = c.alloc<double>(use);
   h->ws_doubles = use;
-  const int chunk = (int)std::min<size_t>(G.nsub, use / per);
+  const int chunk = (int)std::min<size_t>(nl, use / per);
   c.tinv_doubles = std::max(trsm_scratch_doubles(G.nG_pad, chunk), trsm_scratch_doubles(G.nc_pad, chunk));
   c.tinv = c.alloc<double>(c.tinv_doubles);
   numeric_setup(h);
@@ -390,6 +409,8 @@ void bddc_destroy(bddc_ctx* h) {
   cudaSetDevice(h->c.device);
   cudaStreamSynchronize(h->c.stream);
   h->c.free_all();
+  delete h->c.tp;
+  h->c.tp = nullptr;
   if (h->c.h_scal) cudaFreeHost(h->c.h_scal);
   cudaStreamDestroy(h->c.stream);
   delete h;
@@ -428,8 +449,9 @@ int bddc_harmonic(bddc_ctx* h, const double* g, double* out, void* stream) {
     // out_Gamma = g; out_I = A_II^{-1} (0 - A g_ext)_I
     BDDC_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * G.n, s));
     BDDC_CUDA(cudaMemsetAsync(c.v1, 0, sizeof(double) * G.n, s));
-    if (c.n_gamma)
-      { scatter_gamma_kernel<<<ceil_div(c.n_gamma, 256), 256, 0, s>>>(c.n_gamma, c.gamma_dof, g, out); BDDC_COUNT(); }
+    const int ng = G.g_hi - G.g_lo;
+    if (ng > 0)
+      { scatter_gamma_kernel<<<ceil_div(ng, 256), 256, 0, s>>>(ng, c.gamma_dof + G.g_lo, g + G.g_lo, out); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
     harmonic_interior(c, out, s);
   }); });
@@ -468,17 +490,76 @@ int bddc_pcg_host(bddc_ctx* h, const double* b_host, double* x_host, double tol,
   int code = 0;
   code = guarded(err, errlen, [&] {
     Ctx& c = h->c;
-    const size_t bytes = sizeof(double) * c.geo.n;
-    BDDC_CUDA(cudaMemcpyAsync(c.bbuf, b_host, bytes, cudaMemcpyHostToDevice, c.stream));
+    const Geometry& G = c.geo;  // sharded: this rank's active rows in, owned rows out
+    BDDC_CUDA(cudaMemcpyAsync(c.bbuf + G.f_lo, b_host + G.f_lo, sizeof(double) * (G.f_hi - G.f_lo),
+                              cudaMemcpyHostToDevice, c.stream));
   });
   if (code) return code;
   code = bddc_pcg(h, h->c.bbuf, h->c.xbuf, tol, max_iters, alphas, betas, resid, rep, err, errlen);
   int code2 = guarded(err, code ? 0 : errlen, [&] {
-    BDDC_CUDA(cudaMemcpyAsync(x_host, h->c.xbuf, sizeof(double) * h->c.geo.n, cudaMemcpyDeviceToHost,
-                              h->c.stream));
+    const Geometry& G = h->c.geo;
+    BDDC_CUDA(cudaMemcpyAsync(x_host + G.fo_lo, h->c.xbuf + G.fo_lo, sizeof(double) * (G.fo_hi - G.fo_lo),
+                              cudaMemcpyDeviceToHost, h->c.stream));
     BDDC_CUDA(cudaStreamSynchronize(h->c.stream));
   });
   return code ? code : code2;
+}
+
+int bddc_nccl_unique_id(void* out) {
+  if (!out) return 1;
+  try {
+    nccl_unique_id(out);
+    return 0;
+  } catch (const std::exception&) {
+    return 6;
+  }
+}
+
+int bddc_comm_init_nccl(bddc_ctx* h, int rank, int world, const void* id) {
+  if (!h || !id || world < 1 || rank < 0 || rank >= world) return 1;
+  try {
+    BDDC_CUDA(cudaSetDevice(h->c.device));
+    delete h->c.tp;
+    h->c.tp = world > 1 ? make_nccl_transport(rank, world, id) : nullptr;
+    return 0;
+  } catch (const std::exception&) {
+    return 6;
+  }
+}
+
+int bddc_comm_init_host(bddc_ctx* h, int rank, int world, bddc_host_exchange_fn fn, void* user) {
+  if (!h || !fn || world < 1 || rank < 0 || rank >= world) return 1;
+  delete h->c.tp;
+  h->c.tp = world > 1 ? make_host_transport(rank, world, fn, user) : nullptr;
+  return 0;
+}
+
+int bddc_partition_info(int dim, const int* cells, const int* subs, int rank, int world, long long* out) {
+  if ((dim != 2 && dim != 3) || !cells || !subs || !out) return 1;
+  Geometry G{};
+  G.dim = dim;
+  G.n = 1;
+  G.nsub = 1;
+  for (int a = 0; a < 3; ++a) {
+    const bool used = a < dim;
+    G.cells[a] = used ? cells[a] : 1;
+    G.subs[a] = used ? subs[a] : 1;
+    if (used && (G.subs[a] < 1 || G.cells[a] % G.subs[a])) return 1;
+    G.blk[a] = G.cells[a] / G.subs[a];
+    G.nfree[a] = used ? G.cells[a] - 1 : 1;
+    if (used) G.n *= G.nfree[a];
+    G.nsub *= G.subs[a];
+  }
+  Slab sl;
+  try {
+    slab_partition(G, sl, rank, world, nullptr, 0);
+  } catch (const std::exception&) {
+    return 1;
+  }
+  const long long v[10] = {G.s_lo, G.s_hi, G.f_lo, G.f_hi, G.fo_lo, G.fo_hi,
+                           sl.lo_send, sl.lo_recv, sl.hi_send, sl.hi_recv};
+  for (int i = 0; i < 10; ++i) out[i] = v[i];
+  return 0;
 }
 
 int bddc_get_stats(bddc_ctx* h, bddc_stats* o) {
@@ -493,7 +574,7 @@ int bddc_get_stats(bddc_ctx* h, bddc_stats* o) {
   o->n_gamma = c.n_gamma;
   o->n_coarse = c.fp.n_coarse;
   o->nsub = G.nsub;
-  o->factor_bytes = 8LL * G.nsub * (G.li_stride + (long long)G.nG_pad * G.nG_pad +
+  o->factor_bytes = 8LL * (G.s_hi - G.s_lo) * (G.li_stride + (long long)G.nG_pad * G.nG_pad +
                                     (long long)G.nG_pad * G.nc_pad);
   o->front_bytes = 8LL * c.fp.front_pool;
   o->workspace_bytes = 8LL * h->ws_doubles;
@@ -558,9 +639,10 @@ long long bddc_debug_copy(bddc_ctx* h, const char* name, double* host, long long
   const double* src = nullptr;
   long long n = 0;
   std::string nm(name);
-  if (nm == "LI") { src = c.LI; n = (long long)G.nsub * G.li_stride; }
-  else if (nm == "LS") { src = c.LS; n = (long long)G.nsub * G.nG_pad * G.nG_pad; }
-  else if (nm == "Phi") { src = c.Phi; n = (long long)G.nsub * G.nG_pad * G.nc_pad; }
+  const long long nl = G.s_hi - G.s_lo;  // this rank's subdomains (all of them when unsharded)
+  if (nm == "LI") { src = c.LI + (long long)G.s_lo * G.li_stride; n = nl * G.li_stride; }
+  else if (nm == "LS") { src = c.LS + (long long)G.s_lo * G.nG_pad * G.nG_pad; n = nl * G.nG_pad * G.nG_pad; }
+  else if (nm == "Phi") { src = c.Phi + (long long)G.s_lo * G.nG_pad * G.nc_pad; n = nl * G.nG_pad * G.nc_pad; }
   else if (nm == "Sloc") { src = c.Sloc; n = (long long)G.nsub * G.nc_pad * G.nc_pad; }
   else if (nm == "cscale") { src = c.cscale; n = G.nsub; }
   else if (nm == "diag_s") { src = c.diag_s; n = G.nsub; }

@@ -285,7 +285,7 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
   const Geometry& G = c.geo;
   cudaStream_t s = c.stream;
   const size_t per = local_setup_workspace(G, 1);
-  int chunk = (int)std::min<size_t>(G.nsub, ws_doubles / per);
+  int chunk = (int)std::min<size_t>(G.s_hi - G.s_lo, ws_doubles / per);
   if (chunk <= 0) throw CudaError("local setup workspace too small");
   const long long mm = (long long)G.m_pad * G.m_pad;
   const long long wS = (long long)G.nblk * mm;
@@ -296,8 +296,8 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
   const int btchol_smem = 4 * G.m_pad * (G.m_pad + 1) * (int)sizeof(double);
   BDDC_CUDA(cudaFuncSetAttribute(btchol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, btchol_smem));
 
-  for (int sub0 = 0; sub0 < G.nsub; sub0 += chunk) {
-    const int cnt = std::min(chunk, G.nsub - sub0);
+  for (int sub0 = G.s_lo; sub0 < G.s_hi; sub0 += chunk) {  // this rank's subdomains
+    const int cnt = std::min(chunk, G.s_hi - sub0);
     double* E = ws;                             // A_IG, then E - Lo E (in place)
     double* E2 = E + (size_t)chunk * eS;        // E = L_I^{-1} A_IG
     double* Wd = E2 + (size_t)chunk * eS;       // T_j -> Linv_j (dense)

@@ -53,13 +53,13 @@ __global__ void __launch_bounds__(kRedThreads) spmv_dot_kernel(Geometry G, const
                                                                const double* __restrict__ p,
                                                                double* __restrict__ Ap, double* partial) {
   double acc = 0.0;
-  for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < G.n;
+  for (long long f = G.f_lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; f < G.f_hi;
        f += (long long)gridDim.x * blockDim.x) {
     int g0, g1, g2;
     free_coords(G, f, g0, g1, g2);
     const double v = stencil_row<DIM>(G, alpha, p, g0, g1, g2);
     Ap[f] = v;
-    acc += p[f] * v;
+    if (f >= G.fo_lo) acc += p[f] * v;  // dot over owned rows (fo_hi == f_hi)
   }
   block_partial(acc, partial);
 }
@@ -69,24 +69,25 @@ __global__ void __launch_bounds__(kRedThreads) update_xr_kernel(double* __restri
                                                                 const double* __restrict__ p,
                                                                 const double* __restrict__ Ap,
                                                                 const double* __restrict__ scal,
-                                                                long long n, double* partial) {
+                                                                long long lo, long long hi, long long own_lo,
+                                                                double* partial) {
   const double a = scal[0] / scal[1];
   double acc = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+  for (long long i = lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < hi;
        i += (long long)gridDim.x * blockDim.x) {
     x[i] += a * p[i];
     const double ri = r[i] - a * Ap[i];
     r[i] = ri;
-    acc += ri * ri;
+    if (i >= own_lo) acc += ri * ri;
   }
   block_partial(acc, partial);
 }
 
 // beta = rz_new / rz; p = z + beta p
 __global__ void xpay_kernel(double* __restrict__ p, const double* __restrict__ z,
-                            const double* __restrict__ scal, long long n) {
+                            const double* __restrict__ scal, long long lo, long long n) {
   const double b = scal[3] / scal[0];
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+  for (long long i = lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     p[i] = z[i] + b * p[i];
 }
@@ -95,17 +96,23 @@ __global__ void copy_scalar_kernel(double* dst, const double* src) { *dst = *src
 
 }  // namespace
 
+// dots run over the rank's owned rows (all rows when unsharded) and are summed over ranks
 double dot(Ctx& c, const double* a, const double* b, long long n, cudaStream_t s) {
-  { dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(a, b, n, c.red); BDDC_COUNT(); }
+  const Geometry& G = c.geo;
+  (void)n;
+  { dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(a + G.fo_lo, b + G.fo_lo, G.fo_hi - G.fo_lo, c.red); BDDC_COUNT(); }
   { reduce_final_kernel<<<1, 1024, 0, s>>>(c.red, kRedBlocks, c.scal + 7); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
+  allreduce_scalars(c, c.scal + 7, 1, s);
   BDDC_CUDA(cudaMemcpyAsync(c.h_scal + 7, c.scal + 7, sizeof(double), cudaMemcpyDeviceToHost, s));
   BDDC_CUDA(cudaStreamSynchronize(s));
   return c.h_scal[7];
 }
 
 static void dot_to(Ctx& c, const double* a, const double* b, long long n, double* out, cudaStream_t s) {
-  { dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(a, b, n, c.red); BDDC_COUNT(); }
+  const Geometry& G = c.geo;
+  (void)n;
+  { dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(a + G.fo_lo, b + G.fo_lo, G.fo_hi - G.fo_lo, c.red); BDDC_COUNT(); }
   { reduce_final_kernel<<<1, 1024, 0, s>>>(c.red, kRedBlocks, out); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
 }
@@ -123,6 +130,7 @@ PcgResult pcg_solve(Ctx& c, const double* b, double* x, double tol, int max_iter
   dot_to(c, c.r, c.r, n, sc + 4, s);
   apply_bddc(c, c.r, c.z, s);
   dot_to(c, c.r, c.z, n, sc + 0, s);
+  allreduce_scalars(c, sc, 5, s);  // sharded: sum over ranks (sc[1..3] are rewritten before use)
   BDDC_CUDA(cudaMemcpyAsync(hs, sc, sizeof(double) * 8, cudaMemcpyDeviceToHost, s));
   BDDC_CUDA(cudaStreamSynchronize(s));
   const double norm0 = sqrt(hs[4]);
@@ -139,14 +147,17 @@ PcgResult pcg_solve(Ctx& c, const double* b, double* x, double tol, int max_iter
   BDDC_CUDA(cudaMemcpyAsync(c.p, c.z, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   int nbeta = 0;
   for (int it = 0; it < max_iters; ++it) {
+    exchange_dof_halo(c, c.p, s);  // sharded: p on the rows next to the cut lines
     c.prof.begin("pcg.spmv_dot", s);
     if (G.dim == 2) { spmv_dot_kernel<2><<<kRedBlocks, kRedThreads, 0, s>>>(G, c.alpha, c.p, c.Ap, c.red); BDDC_COUNT(); }
     else { spmv_dot_kernel<3><<<kRedBlocks, kRedThreads, 0, s>>>(G, c.alpha, c.p, c.Ap, c.red); BDDC_COUNT(); }
     { reduce_final_kernel<<<1, 1024, 0, s>>>(c.red, kRedBlocks, sc + 1); BDDC_COUNT(); }
     c.prof.end("pcg.spmv_dot", s);
-    { update_xr_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(x, c.r, c.p, c.Ap, sc, n, c.red); BDDC_COUNT(); }
+    allreduce_scalars(c, sc + 1, 1, s);
+    { update_xr_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(x, c.r, c.p, c.Ap, sc, G.f_lo, G.f_hi, G.fo_lo, c.red); BDDC_COUNT(); }
     { reduce_final_kernel<<<1, 1024, 0, s>>>(c.red, kRedBlocks, sc + 2); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
+    allreduce_scalars(c, sc + 2, 1, s);
     BDDC_CUDA(cudaMemcpyAsync(hs, sc, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
     BDDC_CUDA(cudaStreamSynchronize(s));
     if (it > 0) {  // rz_new of the previous iteration is now in hs[0]
@@ -177,6 +188,7 @@ PcgResult pcg_solve(Ctx& c, const double* b, double* x, double tol, int max_iter
       // the reference computes one more B-apply and beta that the Lanczos step ignores
       apply_bddc(c, c.r, c.z, s);
       dot_to(c, c.r, c.z, n, sc + 3, s);
+      allreduce_scalars(c, sc + 3, 1, s);
       BDDC_CUDA(cudaMemcpyAsync(hs + 3, sc + 3, sizeof(double), cudaMemcpyDeviceToHost, s));
       BDDC_CUDA(cudaStreamSynchronize(s));
       if (!(hs[3] > 0.0)) {
@@ -186,7 +198,8 @@ PcgResult pcg_solve(Ctx& c, const double* b, double* x, double tol, int max_iter
     }
     apply_bddc(c, c.r, c.z, s);
     dot_to(c, c.r, c.z, n, sc + 3, s);
-    { xpay_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(c.p, c.z, sc, n); BDDC_COUNT(); }
+    allreduce_scalars(c, sc + 3, 1, s);
+    { xpay_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(c.p, c.z, sc, G.f_lo, G.f_hi); BDDC_COUNT(); }
     { copy_scalar_kernel<<<1, 1, 0, s>>>(sc + 0, sc + 3); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
   }
