@@ -31,23 +31,125 @@ __device__ __forceinline__ void mma_acc(double& c0, double& c1, const double* A,
   }
 }
 
-// ---- W recursion: lane k owns column k of the M x M block (M <= 32) ----
+// ---- W recursion (one warp per subdomain) ----
+// W pitch = 4 mod 16 doubles: conflict-free 8x8x4 DMMA fragments; pivot-inverse pitch 20
+template <int M>
+constexpr int wpitch() { return M <= 16 ? 20 : 36; }
+constexpr int kDP = 20;
+template <int M, bool DIAGB>
+constexpr int wf_warp_doubles() { return (DIAGB ? 1 : 2) * M * wpitch<M>() + 8 * kDP; }
+
+// C(8x8) -= / += A B from shared memory (A(r,k) = A[r*ars + k*acs], B(k,c) = B[k*brs + c*bcs])
+__device__ __forceinline__ void mma8x8(double& c0, double& c1, const double* A, int ars, int acs,
+                                       const double* B, int brs, int bcs, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  dmma884(c0, c1, A[g * ars + t * acs], B[t * brs + g * bcs]);
+  dmma884(c0, c1, A[g * ars + (t + 4) * acs], B[(t + 4) * brs + g * bcs]);
+}
+
+// In-place inverse of the SPD M x M block W (column-major, pitch P) by blocked Gauss-Jordan
+// over 8x8 blocks: the pivot block is inverted in registers (lanes 0..7 own its columns), the
+// row / column / trailing block updates are DMMA.8x8x4 tiles. Returns the first bad pivot.
+template <int M>
+__device__ __forceinline__ int gj_inverse_blocked(double* W, double* Dm, int lane) {
+  constexpr int P = wpitch<M>(), NB = M / 8;
+  const int g = lane >> 2, t = lane & 3;
+  int bad = -1;
+#pragma unroll 1
+  for (int kb = 0; kb < NB; ++kb) {
+    const int K = kb * 8;
+    // (1) Dinv = inverse of the pivot block (scalar Gauss-Jordan on 8 lanes, registers)
+    {
+      double col[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) col[i] = lane < 8 ? W[(K + i) + (K + lane) * P] : 0.0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        double piv = __shfl_sync(0xffffffffu, col[c], c);
+        if (!(piv > 0.0)) {
+          if (bad < 0) bad = K + c;
+          piv = 1.0;
+        }
+        const double ip = 1.0 / piv;
+        const double rk = col[c] * ip;  // row c of this lane's column, scaled
+        double nc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const double ci = __shfl_sync(0xffffffffu, col[i], c);
+          if (i == c) nc[i] = lane == c ? ip : rk;
+          else if (lane == c) nc[i] = -ci * ip;
+          else nc[i] = fma(-ci, rk, col[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) col[i] = nc[i];
+      }
+      if (lane < 8) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) Dm[i + lane * kDP] = col[i];
+      }
+    }
+    __syncwarp();
+    // (2) pivot row blocks: W[K][J] = Dinv W[K][J]
+#pragma unroll
+    for (int jb = 0; jb < NB; ++jb) {
+      if (jb == kb) continue;
+      const int J = jb * 8;
+      double c0 = 0.0, c1 = 0.0;
+      mma8x8(c0, c1, Dm, 1, kDP, W + K + J * P, 1, P, lane);
+      __syncwarp();
+      W[(K + g) + (J + 2 * t) * P] = c0;
+      W[(K + g) + (J + 2 * t + 1) * P] = c1;
+    }
+    __syncwarp();
+    // (3) trailing blocks: W[I][J] -= W[I][K] W[K][J]   (I, J != K; old column, new row)
+#pragma unroll
+    for (int ib = 0; ib < NB; ++ib) {
+      if (ib == kb) continue;
+      const int I = ib * 8;
+#pragma unroll
+      for (int jb = 0; jb < NB; ++jb) {
+        if (jb == kb) continue;
+        const int J = jb * 8;
+        double d0 = 0.0, d1 = 0.0;
+        mma8x8(d0, d1, W + I + K * P, 1, P, W + K + J * P, 1, P, lane);
+        W[(I + g) + (J + 2 * t) * P] -= d0;
+        W[(I + g) + (J + 2 * t + 1) * P] -= d1;
+      }
+    }
+    __syncwarp();
+    // (4) pivot column blocks: W[I][K] = -W[I][K] Dinv ; (5) W[K][K] = Dinv
+#pragma unroll
+    for (int ib = 0; ib < NB; ++ib) {
+      if (ib == kb) continue;
+      const int I = ib * 8;
+      double d0 = 0.0, d1 = 0.0;
+      mma8x8(d0, d1, W + I + K * P, 1, P, Dm, 1, kDP, lane);
+      __syncwarp();
+      W[(I + g) + (K + 2 * t) * P] = -d0;
+      W[(I + g) + (K + 2 * t + 1) * P] = -d1;
+    }
+    for (int e = lane; e < 64; e += 32) W[(K + (e & 7)) + (K + (e >> 3)) * P] = Dm[(e & 7) + (e >> 3) * kDP];
+    __syncwarp();
+  }
+  return bad;
+}
+
 template <int M, bool DIAGB>
 __global__ void __launch_bounds__(32 * kWarpsW) wfactor2d_kernel(Geometry G, int sub0, int cnt,
                                                                  const double* __restrict__ Wd,
                                                                  const double* __restrict__ Wo,
                                                                  double* __restrict__ LI,
                                                                  int* __restrict__ info) {
-  constexpr int P = M + 1;
+  constexpr int P = wpitch<M>();
   extern __shared__ __align__(16) double smw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x * kWarpsW + warp;
   if (b >= cnt) return;
   const int sub = sub0 + b;
-  // per warp: W_j (in place), column buffer, [X scratch for general stencils]
-  double* W = smw + warp * ((DIAGB ? 1 : 2) * M * P + M);
-  double* tmp = W + M * P;
-  double* X = tmp + M;
+  // per warp: W_j (in place), pivot-block inverse, [X scratch for general stencils]
+  double* W = smw + warp * wf_warp_doubles<M, DIAGB>();
+  double* Dm = W + M * P;
+  double* X = Dm + 8 * kDP;
   const long long mm = (long long)M * M;
   const double* wd = Wd + (long long)b * G.nblk * mm;
   const double* wo = Wo + (long long)b * G.nblk * mm;
@@ -55,7 +157,7 @@ __global__ void __launch_bounds__(32 * kWarpsW) wfactor2d_kernel(Geometry G, int
   double* bcg = li + (long long)G.nblk * G.Tm;
   const int px = G.blk[0] - 1;
   const int nbo = G.nbo;
-  const int k = lane;  // owned column
+  const int k = lane;  // owned column (general stencil path) / owned row (elsewhere)
   int failed = -1;
   for (int j = 0; j < G.nblk; ++j) {
     // coupling stencil of plane j (row r = lane): bc[k] for the nbo offsets
@@ -74,10 +176,14 @@ __global__ void __launch_bounds__(32 * kWarpsW) wfactor2d_kernel(Geometry G, int
         if (q < nbo) bcg[((long long)j * M + lane) * nbo + q] = cf[q];
     }
     if (j > 0 && DIAGB) {
-      // B_j diagonal (P1): S_j[i][k] = T_j[i][k] - b_i W_{j-1}[i][k] b_k, in place
-      for (int i = 0; i < M; ++i) {
-        const double bi = __shfl_sync(0xffffffffu, cf[0], i);
-        if (k < M) W[i + k * P] = wd[j * mm + i + (long long)k * M] - bi * W[i + k * P] * cf[0];
+      // B_j diagonal (P1): S_j[i][k] = T_j[i][k] - b_i W_{j-1}[i][k] b_k (lane = row i)
+      if (lane < M) {
+        const double bi = cf[0];
+#pragma unroll 8
+        for (int kk = 0; kk < M; ++kk) {
+          const double bk = __shfl_sync(0xffffffffu >> (32 - M), cf[0], kk);
+          W[lane + kk * P] = wd[j * mm + lane + (long long)kk * M] - bi * W[lane + kk * P] * bk;
+        }
       }
     } else if (j > 0) {
       // X = B_j W_{j-1}: X[i][k] = sum_q cf_i[q] W[i + dx_q][k]  (cf of row i via shuffles)
@@ -104,36 +210,21 @@ __global__ void __launch_bounds__(32 * kWarpsW) wfactor2d_kernel(Geometry G, int
         }
         if (k < M) W[i + k * P] = wd[j * mm + i + (long long)k * M] - a;
       }
-    } else if (k < M) {
-      for (int i = 0; i < M; ++i) W[i + k * P] = wd[i + (long long)k * M];
+    } else if (lane < M) {
+      for (int kk = 0; kk < M; ++kk) W[lane + kk * P] = wd[lane + (long long)kk * M];
     }
     __syncwarp();
-    // Gauss-Jordan sweep W <- S^{-1}: lane k updates column k; column c goes through tmp
-    for (int c = 0; c < M; ++c) {
-      double piv = W[c + c * P];
-      if (!(piv > 0.0)) {
-        if (failed < 0) failed = j * M + c;
-        piv = 1.0;
+    const int bad = gj_inverse_blocked<M>(W, Dm, lane);
+    if (bad >= 0 && failed < 0) failed = j * M + bad;
+    // packed W_j (column-major lower), lane = row i: coalesced per column
+    if (lane < M) {
+      double* lj = li + (long long)j * G.Tm;
+      int cs = 0;
+#pragma unroll 4
+      for (int kk = 0; kk < M; ++kk) {
+        if (kk <= lane) lj[cs + (lane - kk)] = W[lane + kk * P];
+        cs += M - kk;
       }
-      const double ip = 1.0 / piv;
-      const double rk = k < M ? W[c + k * P] : 0.0;  // row c, own column
-      for (int i = 0; i < M; ++i) {
-        const double ci = W[i + c * P];
-        double v;
-        if (i == c) v = (k == c) ? ip : rk * ip;
-        else if (k == c) v = -ci * ip;
-        else v = k < M ? fma(-ci * ip, rk, W[i + k * P]) : 0.0;
-        if (k == c) tmp[i] = v;
-        else if (k < M) W[i + k * P] = v;
-      }
-      __syncwarp();
-      if (k < M) W[k + c * P] = tmp[k];
-      __syncwarp();
-    }
-    // packed W_j (column-major lower)
-    if (k < M) {
-      const int cs = k * M - k * (k - 1) / 2;
-      for (int i = k; i < M; ++i) li[(long long)j * G.Tm + cs + (i - k)] = W[i + k * P];
     }
     __syncwarp();
   }
@@ -255,14 +346,14 @@ template <int M, int NGP>
 void launch_schur2d(const Ctx& c, int sub0, int cnt, const double* Wd, const double* Wo,
                     const double* E, cudaStream_t s) {
   const bool diagb = c.geo.nbo == 1 && c.geo.bo_dx[0] == 0;
-  const size_t smem_w = sizeof(double) * kWarpsW * ((diagb ? 1 : 2) * M * (M + 1) + M);
+  const size_t smem_w = sizeof(double) * kWarpsW * (diagb ? wf_warp_doubles<M, true>() : wf_warp_doubles<M, false>());
   const size_t smem_s = sizeof(double) * (2 * M * (NGP + 4) + M * (M + 1) + 3 * M);
   static bool attr = false;
   if (!attr) {
     BDDC_CUDA(cudaFuncSetAttribute(wfactor2d_kernel<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(sizeof(double) * kWarpsW * (2 * M * (M + 1) + M))));
+                                   (int)(sizeof(double) * kWarpsW * wf_warp_doubles<M, true>())));
     BDDC_CUDA(cudaFuncSetAttribute(wfactor2d_kernel<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(sizeof(double) * kWarpsW * (2 * M * (M + 1) + M))));
+                                   (int)(sizeof(double) * kWarpsW * wf_warp_doubles<M, false>())));
     BDDC_CUDA(cudaFuncSetAttribute(schur2d_kernel<M, NGP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
     attr = true;
   }
