@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(32 * kWarpsW) wfactor2d_kernel(Geometry G, int
 
 // ---- R_j / H_j / S_G with DMMA, W_j streamed back from the packed factor ----
 template <int M, int NGP>
-__global__ void __launch_bounds__(kSchurThreads) schur2d_kernel(Geometry G, int sub0,
+__global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, int sub0,
                                                                 const double* __restrict__ Eg,
                                                                 const double* __restrict__ LI,
                                                                 double* __restrict__ LS) {
@@ -266,20 +266,45 @@ __global__ void __launch_bounds__(kSchurThreads) schur2d_kernel(Geometry G, int 
   for (int j = 0; j < G.nblk; ++j) {
     const int na = G.nact[j];           // active columns (multiple of 8)
     const int nat = na / 8;
-    // W_j (unpack), stencil, A_IG rows (active columns)
-    for (int c = 0; c < M; ++c) {
-      const int cs = c * M - c * (c - 1) / 2;
-      for (int r = c + tid; r < M; r += kSchurThreads) {
-        const double v = li[(long long)j * G.Tm + cs + r - c];
-        sm[O_W + r + c * P] = v;
-        sm[O_W + c + r * P] = v;
+    // W_j (unpack), stencil, A_IG rows (active columns): every global load of the plane is
+    // issued before the first shared-memory store (one latency per plane, not one per column)
+    {
+      constexpr int TM = M * (M + 1) / 2;
+      constexpr int NWL = (TM + kSchurThreads - 1) / kSchurThreads;
+      constexpr int NEL = (M * NGP + kSchurThreads - 1) / kSchurThreads;
+      double wv[NWL], ev[NEL];
+#pragma unroll
+      for (int u = 0; u < NWL; ++u) {
+        const int e = tid + u * kSchurThreads;
+        wv[u] = e < TM ? li[(long long)j * G.Tm + e] : 0.0;
       }
-    }
-    for (int idx = tid; idx < M * nbo; idx += kSchurThreads)
-      sm[O_BC + (idx / nbo) * 3 + idx % nbo] = bcg[(long long)j * M * nbo + idx];
-    for (int idx = tid; idx < M * na; idx += kSchurThreads) {
-      const int r = idx % M, cc = idx / M;
-      sm[O_R + r * EP + cc] = eg[(j * M + r) + (long long)cc * G.nI_pad];
+#pragma unroll
+      for (int u = 0; u < NEL; ++u) {
+        const int idx = tid + u * kSchurThreads;
+        const int r = idx % M, cc = idx / M;
+        ev[u] = idx < M * na ? eg[(j * M + r) + (long long)cc * G.nI_pad] : 0.0;
+      }
+      const double bv = tid < M * nbo ? bcg[(long long)j * M * nbo + tid] : 0.0;
+#pragma unroll
+      for (int u = 0; u < NWL; ++u) {
+        const int e = tid + u * kSchurThreads;
+        if (e < TM) {
+          // column c of packed entry e: cs(c) = c M - c(c-1)/2 <= e < cs(c+1)
+          const double q = 2.0 * M + 1.0;
+          int c = (int)((q - sqrt(q * q - 8.0 * e)) * 0.5);
+          if ((c + 1) * M - (c + 1) * c / 2 <= e) ++c;
+          if (c * M - c * (c - 1) / 2 > e) --c;
+          const int r = c + (e - (c * M - c * (c - 1) / 2));
+          sm[O_W + r + c * P] = wv[u];
+          sm[O_W + c + r * P] = wv[u];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < NEL; ++u) {
+        const int idx = tid + u * kSchurThreads;
+        if (idx < M * na) sm[O_R + (idx % M) * EP + idx / M] = ev[u];
+      }
+      if (tid < M * nbo) sm[O_BC + (tid / nbo) * 3 + tid % nbo] = bv;
     }
     __syncthreads();
     if (j > 0) {  // R_j -= B_j H_{j-1} on the previously active columns
