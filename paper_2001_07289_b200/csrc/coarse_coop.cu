@@ -26,7 +26,8 @@ namespace cg = cooperative_groups;
 
 namespace bddc {
 
-constexpr int kX1Chunk = 256;  // split-K of the left-looking inverse accumulation
+constexpr int kX1Chunk = 256;
+constexpr int kCoopStages = 3;  // cp.async depth of the engine's GEMM tiles (fits the factor smem)  // split-K of the left-looking inverse accumulation
 
 enum CoopType : int {
   CT_EA = 0, CT_PT = 1, CT_TS = 2, CT_X1 = 3, CT_SY = 4, CT_X2 = 5, CT_W = 6, CT_CB = 7,
@@ -109,7 +110,7 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
       const int k = t.arg * kTile, nb = min(kTile, s - k), rest = f - k - nb;
       double* A21 = F + (k + nb) + (long long)k * ld;
       const double* inv = pg.pool + pg.sc.inv[node] + (t.arg & 1) * kTileInvStride;
-      gemm_tile<false, true>(A21, ld, inv, kTile, A21, ld, rest, nb, nb, t.a * kTile, 0, 1.0, 0.0,
+      gemm_tile<false, true, kCoopStages>(A21, ld, inv, kTile, A21, ld, rest, nb, nb, t.a * kTile, 0, 1.0, 0.0,
                              false, smem);
       break;
     }
@@ -117,7 +118,7 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
       const int k = t.arg * kTile, nb = min(kTile, s - k), c = t.a * kTile;
       const int kq0 = c + t.b * kX1Chunk, kq1 = min(k, kq0 + kX1Chunk);
       double* Y = pg.pool + pg.sc.Y[node] + (long long)t.b * kTile * s;
-      gemm_tile<false, false>(F + k + (long long)kq0 * ld, ld, X + kq0 + (long long)c * ldx, ldx,
+      gemm_tile<false, false, kCoopStages>(F + k + (long long)kq0 * ld, ld, X + kq0 + (long long)c * ldx, ldx,
                               Y + (long long)c * kTile, kTile, nb, min(kTile, k - c), kq1 - kq0, 0, 0,
                               1.0, 0.0, false, smem);
       break;
@@ -126,7 +127,7 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
       const int k = t.arg * kTile, nb = min(kTile, s - k), rest = f - k - nb;
       double* L21 = F + (k + nb) + (long long)k * ld;
       double* A22 = F + (k + nb) + (long long)(k + nb) * ld;
-      gemm_tile<false, true>(L21, ld, L21, ld, A22, ld, rest, rest, nb, t.a * kTile, t.b * kTile,
+      gemm_tile<false, true, kCoopStages>(L21, ld, L21, ld, A22, ld, rest, rest, nb, t.a * kTile, t.b * kTile,
                              -1.0, 1.0, true, smem);
       if (t.a == 0 && t.b == 0 && k + nb < s) {  // factor the next panel's diagonal tile now
         __syncthreads();
@@ -144,7 +145,7 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
         const int nq = (k - c + kX1Chunk - 1) / kX1Chunk;
         for (int qq = 0; qq < nq; ++qq) {
           const double* Y = pg.pool + pg.sc.Y[node] + (long long)qq * kTile * s;
-          gemm_tile<false, false>(inv, kTile, Y + (long long)c * kTile, kTile, X + k + (long long)c * ldx,
+          gemm_tile<false, false, kCoopStages>(inv, kTile, Y + (long long)c * kTile, kTile, X + k + (long long)c * ldx,
                                   ldx, nb, kTile, nb, 0, 0, -1.0, qq ? 1.0 : 0.0, false, smem);
           __syncthreads();
         }
@@ -160,7 +161,7 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
       const int b = f - s, c = t.b * kTile;
       double* W = pg.pool + pg.sc.W[node];
       const int ldw = pg.sc.ldw[node];
-      gemm_tile<false, false>(F + s + (long long)c * ld, ld, X + c + (long long)c * ldx, ldx,
+      gemm_tile<false, false, kCoopStages>(F + s + (long long)c * ld, ld, X + c + (long long)c * ldx, ldx,
                               W + (long long)c * ldw, ldw, b, min(kTile, s - c), s - c, t.a * kTile, 0,
                               1.0, 0.0, false, smem);
       break;
@@ -391,7 +392,7 @@ void coop_build(Ctx& c) {
   LevelSchedule& ls = c.sched;
   CoopState& st = g_coop[&c];
   st = CoopState{};
-  st.smem_f = sizeof(double) * std::max<int>(kGemmSmemDoubles, kFactSmemDoubles);
+  st.smem_f = sizeof(double) * std::max<int>(gemm_smem_doubles<kCoopStages>(), kFactSmemDoubles);
   BDDC_CUDA(cudaFuncSetAttribute(coop_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st.smem_f));
   int nsm = 0, per_f = 0, per_s = 0;
   BDDC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device));

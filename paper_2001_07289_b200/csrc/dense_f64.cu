@@ -30,9 +30,11 @@ __device__ __forceinline__ TaskView gemm_task(const GemmArgs& a, int b) {
                   a.lda,          a.ldb,          a.ldc};
 }
 
+constexpr int kGemmStages = 3;
+
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(128) gemm_f64_kernel(GemmArgs args) {
-  __shared__ __align__(16) double smem[kGemmSmemDoubles];
+  extern __shared__ __align__(16) double smem[];
   const TaskView t = gemm_task(args, blockIdx.y);
   const int tiles_m = (t.M + BM - 1) / BM;
   const int tiles_n = (t.N + BN - 1) / BN;
@@ -40,7 +42,7 @@ __global__ void __launch_bounds__(128) gemm_f64_kernel(GemmArgs args) {
   const int tm = blockIdx.x % tiles_m, tn = blockIdx.x / tiles_m;
   const int m0 = tm * BM, n0 = tn * BN;
   if (args.lower && n0 > m0 + BM - 1) return;  // tile strictly above the diagonal
-  gemm_tile<TA, TB>(t.A, t.lda, t.B, t.ldb, t.C, t.ldc, t.M, t.N, t.K, m0, n0, args.alpha,
+  gemm_tile<TA, TB, kGemmStages>(t.A, t.lda, t.B, t.ldb, t.C, t.ldc, t.M, t.N, t.K, m0, n0, args.alpha,
                     args.beta, args.lower != 0, smem);
 }
 
@@ -175,10 +177,19 @@ void gemm(const GemmArgs& a, bool tA, bool tB, cudaStream_t s) {
   int M = a.tasks ? a.max_M : a.M, N = a.tasks ? a.max_N : a.N;
   if (M <= 0 || N <= 0 || a.count <= 0) return;
   dim3 grid(ceil_div(M, BM) * ceil_div(N, BN), a.count);
-  if (!tA && !tB) { gemm_f64_kernel<false, false><<<grid, 128, 0, s>>>(a); BDDC_COUNT(); }
-  else if (!tA && tB) { gemm_f64_kernel<false, true><<<grid, 128, 0, s>>>(a); BDDC_COUNT(); }
-  else if (tA && !tB) { gemm_f64_kernel<true, false><<<grid, 128, 0, s>>>(a); BDDC_COUNT(); }
-  else { gemm_f64_kernel<true, true><<<grid, 128, 0, s>>>(a); BDDC_COUNT(); }
+  constexpr int smem = gemm_smem_doubles<kGemmStages>() * (int)sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    BDDC_CUDA(cudaFuncSetAttribute(gemm_f64_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    BDDC_CUDA(cudaFuncSetAttribute(gemm_f64_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    BDDC_CUDA(cudaFuncSetAttribute(gemm_f64_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    BDDC_CUDA(cudaFuncSetAttribute(gemm_f64_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  if (!tA && !tB) { gemm_f64_kernel<false, false><<<grid, 128, smem, s>>>(a); BDDC_COUNT(); }
+  else if (!tA && tB) { gemm_f64_kernel<false, true><<<grid, 128, smem, s>>>(a); BDDC_COUNT(); }
+  else if (tA && !tB) { gemm_f64_kernel<true, false><<<grid, 128, smem, s>>>(a); BDDC_COUNT(); }
+  else { gemm_f64_kernel<true, true><<<grid, 128, smem, s>>>(a); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
 }
 

@@ -5,6 +5,14 @@
 
 #include "dense_f64.cuh"
 
+#ifdef BDDC_TILE_PROF
+__device__ long long g_tile_marks[16];
+#define TILE_MARK(i) \
+  do { if (blockIdx.x == 0 && threadIdx.x == 0) g_tile_marks[i] = clock64(); } while (0)
+#else
+#define TILE_MARK(i) do { } while (0)
+#endif
+
 namespace bddc {
 namespace tile {
 
@@ -76,16 +84,18 @@ __device__ __forceinline__ void load_b(double* sm, const double* B, int ldb, int
 
 
 constexpr int kGemmSmemDoubles = 4 * TILE_A;  // As[2] + Bs[2]
+template <int NS>
+constexpr int gemm_smem_doubles() { return 2 * NS * TILE_A; }
 
 // One 64x64 output tile (rows m0.., cols n0..) of C = alpha op(A) op(B) + beta C over the
-// full K range; 128 threads (4 warps, 2x2), DMMA.8x8x4 accumulators, cp.async staging.
+// full K range; 128 threads (4 warps, 2x2), DMMA.8x8x4 accumulators, NS-stage cp.async
+// pipeline (NS - 1 k-slices in flight ahead of the one being multiplied).
 // lower: only entries with row >= col are written.
-template <bool TA, bool TB>
+template <bool TA, bool TB, int NS = 2>
 __device__ __forceinline__ void gemm_tile(const double* A, int lda, const double* B, int ldb,
                                           double* C, int ldc, int M, int N, int K, int m0, int n0,
                                           double alpha, double beta, bool lower, double* smem) {
-  double* As[2] = {smem, smem + TILE_A};
-  double* Bs[2] = {smem + 2 * TILE_A, smem + 3 * TILE_A};
+  static_assert(NS >= 2, "at least double buffering");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 1, wn = warp >> 1;
   const int g = lane >> 2, q = lane & 3;
@@ -97,24 +107,29 @@ __device__ __forceinline__ void gemm_tile(const double* A, int lda, const double
   const int nk = (K + BK - 1) / BK;
   const bool al_a = ((((unsigned long long)A) & 15) == 0) && ((lda & 1) == 0);
   const bool al_b = ((((unsigned long long)B) & 15) == 0) && ((ldb & 1) == 0);
-  if (nk > 0) {
-    load_a<TA>(As[0], A, lda, M, K, m0, 0, tid, al_a);
-    load_b<TB>(Bs[0], B, ldb, N, K, n0, 0, tid, al_b);
-    cp_async_commit();
+  auto As = [&](int st) { return smem + st * TILE_A; };
+  auto Bs = [&](int st) { return smem + (NS + st) * TILE_A; };
+  // prologue: slices 0 .. NS-2
+#pragma unroll
+  for (int p = 0; p < NS - 1; ++p) {
+    if (p < nk) {
+      load_a<TA>(As(p), A, lda, M, K, m0, p * BK, tid, al_a);
+      load_b<TB>(Bs(p), B, ldb, N, K, n0, p * BK, tid, al_b);
+    }
+    cp_async_commit();  // empty groups keep the group count uniform
   }
   for (int kt = 0; kt < nk; ++kt) {
-    const int st = kt & 1;
-    if (kt + 1 < nk) {
-      load_a<TA>(As[st ^ 1], A, lda, M, K, m0, (kt + 1) * BK, tid, al_a);
-      load_b<TB>(Bs[st ^ 1], B, ldb, N, K, n0, (kt + 1) * BK, tid, al_b);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
+    const int st = kt % NS;
+    const int pf = kt + NS - 1;  // slice to prefetch into the stage freed last iteration
+    if (pf < nk) {
+      load_a<TA>(As(pf % NS), A, lda, M, K, m0, pf * BK, tid, al_a);
+      load_b<TB>(Bs(pf % NS), B, ldb, N, K, n0, pf * BK, tid, al_b);
     }
+    cp_async_commit();
+    cp_async_wait<NS - 1>();  // slice kt has landed
     __syncthreads();
-    const double* as = As[st];
-    const double* bs = Bs[st];
+    const double* as = As(st);
+    const double* bs = Bs(st);
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double af[4], bf[4];
@@ -135,6 +150,7 @@ __device__ __forceinline__ void gemm_tile(const double* A, int lda, const double
     }
     __syncthreads();
   }
+  cp_async_wait<0>();
   // epilogue: all C reads issued before any store (no serial read-modify-write chain)
   double cv[4][4][2];
   if (beta != 0.0) {
@@ -204,7 +220,10 @@ __device__ __forceinline__ void diag8(double* S, double* X, double* Dv, int k0, 
         if (lane == 0 && *failed < 0) *failed = k0 + c;
         d = 1.0;
       }
-      const double ri = rsqrt(d);
+      // 1/sqrt(d): float seed + 2 Newton steps in double (d > 0 here; no special cases)
+      double ri = (double)rsqrtf((float)d);
+      ri = ri * fma(-0.5 * d * ri, ri, 1.5);
+      ri = ri * fma(-0.5 * d * ri, ri, 1.5);
       rinv[c] = ri;
       const double l = lane > c ? row[c] * ri : (lane == c ? d * ri : 0.0);
       row[c] = l;
@@ -253,18 +272,27 @@ __device__ __forceinline__ int potrf_trtri_tile(double* L, int ld, int n, double
   const int g = lane >> 2, t4 = lane & 3;
   const int nb8 = (n + 7) >> 3, np = nb8 * 8;
   if (tid == 0) failed = -1;
-  for (int j = warp; j < np; j += nw) {
-    for (int i = lane; i < np; i += 32) {
-      double v = 0.0;
-      if (i < n && j < n) v = i >= j ? L[i + (long long)j * ld] : 0.0;
-      else if (i == j) v = 1.0;  // identity padding
-      S[i + j * SP] = v;
-      X[i + j * SP] = 0.0;
+  TILE_MARK(0);
+  // 64x64 region, 16 independent loads in flight per thread per batch (identity padding)
+#pragma unroll 1
+  for (int u0 = 0; u0 < kTile * kTile; u0 += 16 * 128) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int idx = u0 + u * nt + tid, i = idx & 63, j = idx >> 6;
+      v[u] = (i < n && j < n && i >= j) ? L[i + (long long)j * ld] : (i == j && i >= n ? 1.0 : 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int idx = u0 + u * nt + tid, i = idx & 63, j = idx >> 6;
+      if (i < np && j < np) S[i + j * SP] = v[u];
     }
   }
   __syncthreads();
+  TILE_MARK(1);
   if (warp == 0) diag8<FACTOR>(S, X, Dv, 0, lane, &failed);
   __syncthreads();
+  TILE_MARK(2);
   for (int kb = 0; kb < nb8; ++kb) {
     const int k0 = kb * 8;
     if (!FACTOR) {
@@ -312,6 +340,7 @@ __device__ __forceinline__ int potrf_trtri_tile(double* L, int ld, int n, double
     }
     __syncthreads();
   }
+  TILE_MARK(3);
   // inverse recursion by block rows: X[i][k] = -X[i][i] sum_{m=k}^{i-1} L[i][m] X[m][k]
   double* tmp = Dv + 128 + warp * 64;  // per-warp 8x8 scratch
   for (int ib = 1; ib < nb8; ++ib) {
@@ -330,19 +359,21 @@ __device__ __forceinline__ int potrf_trtri_tile(double* L, int ld, int n, double
     }
     __syncthreads();
   }
+  TILE_MARK(4);
   if (FACTOR) {
-    for (int idx = tid; idx < n * n; idx += nt) {
-      const int i = idx % n, j = idx / n;
-      if (i >= j) L[i + (long long)j * ld] = S[i + j * SP];
+    for (int idx = tid; idx < kTile * kTile; idx += nt) {
+      const int i = idx & 63, j = idx >> 6;
+      if (i < n && j < n && i >= j) L[i + (long long)j * ld] = S[i + j * SP];
     }
   }
   if (inv) {
     for (int idx = tid; idx < kTile * kTile; idx += nt) {
-      const int i = idx % kTile, j = idx / kTile;
-      inv[idx] = (i < n && j < n) ? X[i + j * SP] : 0.0;
+      const int i = idx & 63, j = idx >> 6;
+      inv[idx] = (i < n && j < n && i >= j) ? X[i + j * SP] : 0.0;
     }
   }
   __syncthreads();
+  TILE_MARK(5);
   return failed;
 }
 

@@ -1,4 +1,5 @@
 // Pure kernel timing of tile::potrf_trtri_tile (64x64) and tile::gemm_tile.
+#define BDDC_TILE_PROF 1
 #include <cstdio>
 #include <vector>
 #include "../paper_2001_07289_b200/csrc/tile_ops.cuh"
@@ -33,6 +34,12 @@ int main() {
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     printf("chol+inv tile: %d reps: %.1f us per tile (%s)\n", reps, 1000 * ms / reps, cudaGetErrorString(cudaGetLastError()));
+  }
+  {
+    long long m[16];
+    cudaMemcpyFromSymbol(m, g_tile_marks, sizeof(m));
+    const char* nm[6] = {"start", "loaded", "diag0", "factor loop", "inverse", "stored"};
+    for (int i = 1; i < 6; ++i) printf("  %-12s +%lld cycles\n", nm[i], m[i] - m[i - 1]);
   }
   cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, tile::kGemmSmemDoubles * 8);
   for (int reps : {1, 10}) {
