@@ -137,58 +137,38 @@ struct FrontPlan {
   int* info = nullptr;                 // per node pivot failure (global coarse index)
 };
 
-// Plan-time schedule of the multifrontal factorization: per level, per 64-column panel
-// step, device task arrays for the tile Cholesky / tile TRSM / lower GEMM launches.
-struct CsTask {  // coarse-solve GEMV tile
-  int node, r0, c0, part;
-  int red;  // global index of the reduction (CsRed) this tile's partial belongs to
+// Coarse-solve plan: per level, GEMV tasks over the partitioned-inverse fronts. Every task
+// carries its front's metadata (no dependent loads before its first front read).
+struct CsTask {
+  long long front_off;  // front base in the pool
+  long long gat_base;   // node's offset into gat_ptr (child-update gathers per position)
+  long long upd_off;    // node's update-vector offset
+  int node, r0, c0;
+  int s, f, ld, s0;     // separator size, front size, leading dimension, first coarse index
+  int part;             // partial slot (np > 1)
+  int red;              // global reduction index (arrival counter), -1 = none
+  int np;               // tasks contributing to this task's reduction (1: write directly)
+  int mode;             // forward: 0 = 64 rows x 256 columns, 1 = 256 rows x all s <= 64 columns
 };
-struct CsRed {  // coarse-solve reduction over the partials of one row / column tile
-  int node, t0, p0, np;
-};
-struct InvTask {  // per front: copy L11 to scratch, then panel <- panel * L11^{-1}
-  int node;
-  long long scr;  // scratch offset
-  int lds;
+struct CsRed {  // reduction over the partials of one row / column chunk
+  int t0, p0, np;
 };
 
 struct LevelView {  // POD view of the gather maps for kernels
   const int* gat_ptr;
-  const long long* gat_off;
   const int* gat_src;
 };
 
 struct LevelSchedule {
-  struct Step {
-    TileTask* potrf = nullptr;  // factorization only
-    int n_potrf = 0;
-    TileTask* trtri = nullptr;  // diagonal-tile inverses (into tile_scratch)
-    int n_trtri = 0;
-    GemmTask* tsolve = nullptr; // in-place tile solves with the inverses
-    int n_tsolve = 0, ts_M = 0, ts_N = 0;
-    GemmTask* gemm = nullptr;   // trailing / panel updates
-    int n_gemm = 0, g_M = 0, g_N = 0;
-  };
-  std::vector<std::vector<Step>> steps;      // [level][step] factorization
-  std::vector<std::vector<Step>> inv_steps;  // [level][step] panel <- panel L11^{-1} (RLN)
-  std::vector<InvTask*> inv_prep;            // [level]
-  std::vector<int> n_inv_prep;
-  double* inv_scratch = nullptr;
-  double* tile_scratch = nullptr;
-  // solve: per level fwd / bwd GEMV tiles and reductions
+  // solve: per level fwd / bwd GEMV tasks and reductions
   std::vector<CsTask*> fwd_t, bwd_t;
   std::vector<CsRed*> fwd_r, bwd_r;
   std::vector<int> n_fwd_t, n_bwd_t, n_fwd_r, n_bwd_r;
   double* partial = nullptr;
   double* ybuf = nullptr;     // forward-solve values of the separator rows (n)
   int* red_cnt = nullptr;     // arrival counters of the fused reductions (self-resetting)
-  int* gat_ptr = nullptr;    // per node front position -> sources in the update pool
-  long long* gat_off = nullptr;  // per node offset into gat_ptr
+  int* gat_ptr = nullptr;     // per node front position -> sources in the update pool
   int* gat_src = nullptr;
-  int* d_nodes = nullptr;                // level node lists concatenated
-  std::vector<int> nodes_off;
-  int max_children = 0;
-  size_t max_fwd_smem = 0;
 };
 
 // Optional per-phase CUDA-event timers (bench.py reads them for the roofline of the

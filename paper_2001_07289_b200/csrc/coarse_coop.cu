@@ -219,18 +219,18 @@ struct SolveProgram {
   int nfr;  // number of forward reductions (offset of the backward counters)
 };
 
-__device__ __forceinline__ double gather_children_c(const LevelView& lv, const double* __restrict__ upd,
-                                                    int node, int pos) {
-  const int* gp = lv.gat_ptr + lv.gat_off[node];
+__device__ __forceinline__ double gather_at(const LevelView& lv, const double* __restrict__ upd, long long gbase,
+                                           int pos) {
+  const int* gp = lv.gat_ptr + gbase;
   double acc = 0.0;
   for (int q = gp[pos]; q < gp[pos + 1]; ++q) acc += upd[lv.gat_src[q]];
   return acc;
 }
 
 // Forward (bottom-up): y_sep = X (rhs + child updates), upd = gathered - W21 (..);
-// backward (top-down): x_sep = X^T y_sep - W21^T x_bnd. Each level is ONE phase: the GEMV
-// tiles write 64-entry partials and the last tile to arrive at a row (column) chunk sums the
-// chunk's partials in fixed order (deterministic) and finishes it.
+// backward (top-down): x_sep = X^T y_sep - W21^T x_bnd. Each level is ONE phase (coarse.cu
+// describes the task shapes); a chunk with several tasks is finished by the last task to
+// arrive, which sums the partials in fixed order (deterministic).
 __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView lv, SolveProgram sp,
                                                          const double* __restrict__ rhs,
                                                          double* __restrict__ sol,
@@ -255,14 +255,34 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
   for (int l = 0; l < sp.nlevels; ++l) {
     for (int ti = sp.ft_off[l] + blockIdx.x; ti < sp.ft_off[l + 1]; ti += gridDim.x) {
       const CsTask t = sp.ft[ti];
-      const int node = t.node, s = fd.sep_size[node], f = s + fd.bnd_size[node];
-      const long long ld = fd.ld[node];
-      const int s0 = fd.sep_start[node];
-      const double* F = fd.fronts + fd.front_off[node];
+      const double* F = fd.fronts + t.front_off;
+      const long long ld = t.ld;
+      const int s = t.s, f = t.f;
       __syncthreads();
+      if (t.mode == 1) {  // s <= 64: one thread per row, all separator columns
+        if (tid < s) vs[tid] = rhs[t.s0 + tid] + gather_at(lv, fd.upd, t.gat_base, tid);
+        __syncthreads();
+        const int r = t.r0 + tid;
+        if (r < f) {
+          const int ke = r < s ? r + 1 : s;
+          const double* Fr = F + r;
+          double acc[4] = {0.0, 0.0, 0.0, 0.0};
+          for (int k0 = 0; k0 < ke; k0 += 16) {
+            double fv[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) fv[u] = k0 + u < ke ? __ldcs(Fr + (long long)(k0 + u) * ld) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) acc[u & 3] += k0 + u < ke ? fv[u] * vs[k0 + u] : 0.0;
+          }
+          const double a = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+          if (r < s) ybuf[t.s0 + r] = a;
+          else fd.upd[t.upd_off + (r - s)] = gather_at(lv, fd.upd, t.gat_base, r) - a;
+        }
+        continue;
+      }
       {
         const int kk = t.c0 + tid;
-        vs[tid] = kk < s ? rhs[s0 + kk] + gather_children_c(lv, fd.upd, node, kk) : 0.0;
+        vs[tid] = kk < s ? rhs[t.s0 + kk] + gather_at(lv, fd.upd, t.gat_base, kk) : 0.0;
       }
       __syncthreads();
       const int rr = tid & 63, grp = tid >> 6;
@@ -283,22 +303,31 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
       }
       red[grp][rr] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
       __syncthreads();
+      if (t.np == 1) {
+        const int rw = t.r0 + tid;
+        if (tid < 64 && rw < f) {
+          const double a = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
+          if (rw < s) ybuf[t.s0 + rw] = a;
+          else fd.upd[t.upd_off + (rw - s)] = gather_at(lv, fd.upd, t.gat_base, rw) - a;
+        }
+        continue;
+      }
       if (tid < 64) {
         partial[(long long)t.part * 64 + tid] = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
         __threadfence();
       }
       __syncthreads();
-      const CsRed R = sp.fr[t.red];
-      if (tid == 0) last = atomicAdd(cnt_f + t.red, 1) == R.np - 1;
+      if (tid == 0) last = atomicAdd(cnt_f + t.red, 1) == t.np - 1;
       __syncthreads();
       if (last) {
         __threadfence();
+        const CsRed R = sp.fr[t.red];
         const int rw = R.t0 + tid;
         if (tid < 64 && rw < f) {
           double a = 0.0;
           for (int p = 0; p < R.np; ++p) a += __ldcg(partial + (long long)(R.p0 + p) * 64 + tid);
-          if (rw < s) ybuf[s0 + rw] = a;
-          else fd.upd[fd.upd_off[node] + (rw - s)] = gather_children_c(lv, fd.upd, node, rw) - a;
+          if (rw < s) ybuf[t.s0 + rw] = a;
+          else fd.upd[t.upd_off + (rw - s)] = gather_at(lv, fd.upd, t.gat_base, rw) - a;
         }
         if (tid == 0) cnt_f[t.red] = 0;
       }
@@ -309,15 +338,14 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
   for (int l = sp.nlevels - 1; l >= 0; --l) {
     for (int ti = sp.bt_off[l] + blockIdx.x; ti < sp.bt_off[l + 1]; ti += gridDim.x) {
       const CsTask t = sp.bt[ti];
-      const int node = t.node, s = fd.sep_size[node], f = s + fd.bnd_size[node];
-      const long long ld = fd.ld[node];
-      const int s0 = fd.sep_start[node];
-      const int* bidx = fd.bnd_idx + fd.bnd_ptr[node];
-      const double* F = fd.fronts + fd.front_off[node];
+      const int s = t.s, f = t.f;
+      const long long ld = t.ld;
+      const int* bidx = fd.bnd_idx + fd.bnd_ptr[t.node];
+      const double* F = fd.fronts + t.front_off;
       __syncthreads();
       {
         const int r = t.r0 + tid;
-        vs[tid] = r < s ? ybuf[s0 + r] : (r < f ? -sol[bidx[r - s]] : 0.0);
+        vs[tid] = r < s ? ybuf[t.s0 + r] : (r < f ? -sol[bidx[r - s]] : 0.0);
       }
       __syncthreads();
       // warp: 8 columns; lane: rows i = lane + 32 m; 16 loads in flight per batch
@@ -343,6 +371,15 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
 #pragma unroll
           for (int cc = 0; cc < 8; ++cc) acc[cc] += fv[h][cc] * vs[lane + 32 * (m + h)];
       }
+      if (t.np == 1) {
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+          const double v = warp_sum(acc[cc]);
+          const int k = kw + cc;
+          if (lane == 0 && k < s) sol[t.s0 + k] = v;
+        }
+        continue;
+      }
 #pragma unroll
       for (int cc = 0; cc < 8; ++cc) {
         const double v = warp_sum(acc[cc]);
@@ -350,16 +387,16 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
       }
       if (lane == 0) __threadfence();
       __syncthreads();
-      const CsRed R = sp.br[t.red];
-      if (tid == 0) last = atomicAdd(cnt_b + t.red, 1) == R.np - 1;
+      if (tid == 0) last = atomicAdd(cnt_b + t.red, 1) == t.np - 1;
       __syncthreads();
       if (last) {
         __threadfence();
+        const CsRed R = sp.br[t.red];
         const int k = R.t0 + tid;
         if (tid < 64 && k < s) {
           double a = 0.0;
           for (int p = 0; p < R.np; ++p) a += __ldcg(partial + (long long)(R.p0 + p) * 64 + tid);
-          sol[s0 + k] = a;
+          sol[t.s0 + k] = a;
         }
         if (tid == 0) cnt_b[t.red] = 0;
       }
@@ -569,7 +606,7 @@ void coop_factor(Ctx& c, cudaStream_t s) {
 void coop_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s) {
   CoopState& st = g_coop.at(&c);
   FrontDev fd = c.fp.d;
-  LevelView lv{c.sched.gat_ptr, c.sched.gat_off, c.sched.gat_src};
+  LevelView lv{c.sched.gat_ptr, c.sched.gat_src};
   double* partial = c.sched.partial;
   double* ybuf = c.sched.ybuf;
   int* cnt = c.sched.red_cnt;
