@@ -260,17 +260,21 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
       const int s = t.s, f = t.f;
       __syncthreads();
       if (t.mode == 1) {  // s <= 64: one thread per row, all separator columns
+        const int r = t.r0 + tid;
+        const int ke = r < f ? (r < s ? r + 1 : s) : 0;
+        const double* Fr = F + r;
+        double fv[16];  // first batch in flight while the right-hand side is gathered
+#pragma unroll
+        for (int u = 0; u < 16; ++u) fv[u] = u < ke ? __ldcs(Fr + (long long)u * ld) : 0.0;
         if (tid < s) vs[tid] = rhs[t.s0 + tid] + gather_at(lv, fd.upd, t.gat_base, tid);
         __syncthreads();
-        const int r = t.r0 + tid;
         if (r < f) {
-          const int ke = r < s ? r + 1 : s;
-          const double* Fr = F + r;
           double acc[4] = {0.0, 0.0, 0.0, 0.0};
           for (int k0 = 0; k0 < ke; k0 += 16) {
-            double fv[16];
+            if (k0 > 0) {
 #pragma unroll
-            for (int u = 0; u < 16; ++u) fv[u] = k0 + u < ke ? __ldcs(Fr + (long long)(k0 + u) * ld) : 0.0;
+              for (int u = 0; u < 16; ++u) fv[u] = k0 + u < ke ? __ldcs(Fr + (long long)(k0 + u) * ld) : 0.0;
+            }
 #pragma unroll
             for (int u = 0; u < 16; ++u) acc[u & 3] += k0 + u < ke ? fv[u] * vs[k0 + u] : 0.0;
           }
@@ -280,26 +284,28 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
         }
         continue;
       }
+      const int rr = tid & 63, grp = tid >> 6;
+      const int r = t.r0 + rr;
+      const int kb = t.c0 + grp * 64;
+      int ke = r < f ? min(kb + 64, s) : kb;
+      if (r < s) ke = min(ke, r + 1);
+      const double* Fr = F + r;
+      double fv[16];  // first batch in flight while the right-hand side is gathered
+#pragma unroll
+      for (int u = 0; u < 16; ++u) fv[u] = kb + u < ke ? __ldcs(Fr + (long long)(kb + u) * ld) : 0.0;
       {
         const int kk = t.c0 + tid;
         vs[tid] = kk < s ? rhs[t.s0 + kk] + gather_at(lv, fd.upd, t.gat_base, kk) : 0.0;
       }
       __syncthreads();
-      const int rr = tid & 63, grp = tid >> 6;
-      const int r = t.r0 + rr;
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      if (r < f) {
-        const int kb = t.c0 + grp * 64;
-        int ke = min(kb + 64, s);
-        if (r < s) ke = min(ke, r + 1);
-        const double* Fr = F + r;
-        for (int k0 = kb; k0 < ke; k0 += 16) {
-          double fv[16];
+      for (int k0 = kb; k0 < ke; k0 += 16) {
+        if (k0 > kb) {
 #pragma unroll
           for (int u = 0; u < 16; ++u) fv[u] = k0 + u < ke ? __ldcs(Fr + (long long)(k0 + u) * ld) : 0.0;
-#pragma unroll
-          for (int u = 0; u < 16; ++u) acc[u & 3] += k0 + u < ke ? fv[u] * vs[k0 + u - t.c0] : 0.0;
         }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) acc[u & 3] += k0 + u < ke ? fv[u] * vs[k0 + u - t.c0] : 0.0;
       }
       red[grp][rr] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
       __syncthreads();
@@ -342,20 +348,11 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
       const long long ld = t.ld;
       const int* bidx = fd.bnd_idx + fd.bnd_ptr[t.node];
       const double* F = fd.fronts + t.front_off;
-      __syncthreads();
-      {
-        const int r = t.r0 + tid;
-        vs[tid] = r < s ? ybuf[t.s0 + r] : (r < f ? -sol[bidx[r - s]] : 0.0);
-      }
-      __syncthreads();
-      // warp: 8 columns; lane: rows i = lane + 32 m; 16 loads in flight per batch
-      double acc[8];
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc) acc[cc] = 0.0;
+      // warp: 8 columns; lane: rows i = lane + 32 m; 16 loads in flight per batch (the first
+      // batch is issued before the right-hand side is read)
       const int kw = t.c0 + warp * 8;
-#pragma unroll
-      for (int m = 0; m < 8; m += 2) {
-        double fv[2][8];
+      double fv[2][8];
+      auto load_rows = [&](int m) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int i = lane + 32 * (m + h), r = t.r0 + i;
@@ -366,6 +363,20 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
             fv[h][cc] = ok ? __ldcs(F + r + (long long)k * ld) : 0.0;
           }
         }
+      };
+      load_rows(0);
+      __syncthreads();
+      {
+        const int r = t.r0 + tid;
+        vs[tid] = r < s ? ybuf[t.s0 + r] : (r < f ? -sol[bidx[r - s]] : 0.0);
+      }
+      __syncthreads();
+      double acc[8];
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) acc[cc] = 0.0;
+#pragma unroll
+      for (int m = 0; m < 8; m += 2) {
+        if (m > 0) load_rows(m);
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
