@@ -241,6 +241,209 @@ __global__ void __launch_bounds__(32 * kBtWarps) bt_solve_kernel(Geometry G, Loc
   }
 }
 
+// ---- specialised interior solve: compile-time plane rows M and stencil width NBO ----
+// Each plane (packed W_j + its coupling rows) arrives by TMA bulk copy (cp.async.bulk,
+// issued by one lane, completing on a per-stage mbarrier); the GEMV is fully unrolled with
+// the packed-column offsets as immediates; the interior dofs of a subdomain are an affine
+// map of its base dof (irow_rel), so gather / scatter need no index arithmetic.
+template <int M>
+__host__ __device__ constexpr int bt_cs(int k) { return k * M - k * (k - 1) / 2; }
+
+template <int M, int NBO>
+struct BtT {
+  static constexpr int R = (M + 31) / 32;
+  static constexpr int TM = M * (M + 1) / 2;
+  static constexpr int MB = M * NBO;
+  static constexpr int STAGE = TM + MB;  // both even (M % 8 == 0): 16-byte aligned stages
+  static __host__ __device__ int per_warp(int nI) { return 2 + 2 * STAGE + nI + M; }
+};
+
+template <int M, int R>
+__device__ __forceinline__ void bt_gemv_t(const double* __restrict__ pk, const double* __restrict__ v,
+                                          double (&out)[R], int lane) {
+  const double* b1[R];
+  const double* b2[R];
+  int r[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    r[i] = min(lane + 32 * i, M - 1);  // lanes past M repeat row M-1 (result unused)
+    b1[i] = pk + r[i];                          // k <= r: pk[cs(k) - k + r]
+    b2[i] = pk + (r[i] * M - r[i] * (r[i] - 1) / 2) - r[i];  // k > r: pk[cs(r) - r + k]
+    out[i] = 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < M; ++k) {
+    const double vk = v[k];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const double w = k <= r[i] ? b1[i][bt_cs<M>(k) - k] : b2[i][k];
+      out[i] = fma(w, vk, out[i]);
+    }
+  }
+}
+
+template <int M, int NBO>
+__global__ void __launch_bounds__(32 * kBtWarps) bt_solve_t_kernel(Geometry G, LocalTables lt,
+                                                                   const double* __restrict__ LI,
+                                                                   const double* __restrict__ in,
+                                                                   double* __restrict__ out) {
+  using T = BtT<M, NBO>;
+  constexpr int R = T::R;
+  extern __shared__ __align__(16) double sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nI = G.nI_pad, nblk = G.nblk;
+  double* wb = sm + warp * T::per_warp(nI);
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(wb);
+  double* stg = wb + 2;
+  double* y = stg + 2 * T::STAGE;
+  double* tv = y + nI;
+  const int sub = G.s_lo + blockIdx.x * kBtWarps + warp;
+  if (sub >= G.s_hi) return;
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  const double* li = LI + (long long)sub * G.li_stride;
+  const double* bc = li + (long long)nblk * T::TM;
+  unsigned ph0 = 0, ph1 = 0;
+  auto issue = [&](int jw, int jb, int st) {  // plane jw's W (+ coupling rows of plane jb)
+    if (lane == 0) {
+      double* dst = stg + st * T::STAGE;
+      mbar_expect_tx(&bar[st], (unsigned)(T::TM * 8 + (jb >= 0 ? T::MB * 8 : 0)));
+      bulk_g2s(dst, li + (long long)jw * T::TM, T::TM * 8, &bar[st]);
+      if (jb >= 0) bulk_g2s(dst + T::TM, bc + (long long)jb * T::MB, T::MB * 8, &bar[st]);
+    }
+  };
+  auto wait = [&](int st) {
+    if (st == 0) { mbar_wait(&bar[0], ph0); ph0 ^= 1u; }
+    else { mbar_wait(&bar[1], ph1); ph1 ^= 1u; }
+  };
+  if (nblk > 0) issue(0, -1, 0);
+  // gather: free dof of interior row rr = base + rel[rr]
+  int p[3];
+  sub_coords(G, sub, p);
+  long long base = (long long)(p[0] * G.blk[0] - 1) + (long long)G.nfree[0] * (p[1] * G.blk[1] - 1);
+  if (G.dim == 3) base += (long long)G.nfree[0] * G.nfree[1] * (p[2] * G.blk[2] - 1);
+  for (int rr = lane; rr < nI; rr += 128) {
+    int rel[4];
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) rel[u] = rr + 32 * u < nI ? lt.irow_rel[rr + 32 * u] : -1;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = rel[u] >= 0 ? in[base + rel[u]] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (rr + 32 * u < nI) y[rr + 32 * u] = v[u];
+  }
+  // lane rows: coupling neighbours (clamped; absent neighbours have zero coefficients)
+  const int px = G.blk[0] - 1;
+  int fwd_q[R][NBO], bwd_q[R][NBO];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int r = lane + 32 * i, x = r % px, yy = r / px;
+#pragma unroll
+    for (int k = 0; k < NBO; ++k) {
+      const int qf = (x + G.bo_dx[k]) + (yy + G.bo_dy[k]) * px;
+      const int qb = (x - G.bo_dx[k]) + (yy - G.bo_dy[k]) * px;
+      fwd_q[i][k] = min(max(qf, 0), M - 1);
+      bwd_q[i][k] = (qb >= 0 && qb < M && r < M) ? qb : -1;
+    }
+  }
+  __syncwarp();
+  double hv[R];
+  // ---- forward: h_j = W_j (b_j - B_j h_{j-1}) ----
+  for (int j = 0; j < nblk; ++j) {
+    const int st = j & 1;
+    if (j + 1 < nblk) issue(j + 1, j + 1, st ^ 1);
+    wait(st);
+    const double* pk = stg + st * T::STAGE;
+    const double* bj = pk + T::TM;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int r = lane + 32 * i;
+      if (r < M) {
+        double acc = y[j * M + r];
+        if (j > 0) {
+          const double* hp = y + (j - 1) * M;
+#pragma unroll
+          for (int k = 0; k < NBO; ++k) acc -= bj[r * NBO + k] * hp[fwd_q[i][k]];
+        }
+        tv[r] = acc;
+      }
+    }
+    __syncwarp();
+    bt_gemv_t<M, R>(pk, tv, hv, lane);
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+      if (lane + 32 * i < M) y[j * M + lane + 32 * i] = hv[i];
+    __syncwarp();
+  }
+  // ---- backward: x_j = h_j - W_j (B_{j+1}^T x_{j+1}) ----
+  if (nblk > 1) issue(nblk - 2, nblk - 1, 0);
+  for (int j = nblk - 2, it = 0; j >= 0; --j, ++it) {
+    const int st = it & 1;
+    if (j > 0) issue(j - 1, j, st ^ 1);
+    wait(st);
+    const double* pk = stg + st * T::STAGE;
+    const double* bn = pk + T::TM;  // coupling rows of plane j + 1
+    const double* xn = y + (j + 1) * M;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int r = lane + 32 * i;
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < NBO; ++k)
+        if (bwd_q[i][k] >= 0) acc += bn[bwd_q[i][k] * NBO + k] * xn[bwd_q[i][k]];
+      if (r < M) tv[r] = acc;
+    }
+    __syncwarp();
+    bt_gemv_t<M, R>(pk, tv, hv, lane);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int r = lane + 32 * i;
+      if (r < M) y[j * M + r] -= hv[i];
+    }
+    __syncwarp();
+  }
+  for (int rr = lane; rr < nI; rr += 32) {
+    const int rel = lt.irow_rel[rr];
+    if (rel >= 0) out[base + rel] = y[rr];
+  }
+}
+
+template <int M, int NBO>
+bool launch_bt_t(const Geometry& G, const LocalTables& lt, const double* LI, const double* in, double* out,
+                 cudaStream_t s) {
+  if (G.m_pad != M || G.nbo != NBO || G.Tm != BtT<M, NBO>::TM) return false;
+  const size_t smem = sizeof(double) * BtT<M, NBO>::per_warp(G.nI_pad) * kBtWarps;
+  if (smem > 227 * 1024) return false;
+  static size_t attr = 0;
+  if (smem > attr) {
+    BDDC_CUDA(cudaFuncSetAttribute(bt_solve_t_kernel<M, NBO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  const int grid = ceil_div(G.s_hi - G.s_lo, kBtWarps);
+  bt_solve_t_kernel<M, NBO><<<grid, 32 * kBtWarps, smem, s>>>(G, lt, LI, in, out);
+  BDDC_COUNT();
+  BDDC_LAUNCH_CHECK();
+  return true;
+}
+
+template <int NBO>
+bool launch_bt_nbo(const Geometry& G, const LocalTables& lt, const double* LI, const double* in, double* out,
+                   cudaStream_t s) {
+  switch (G.m_pad) {
+    case 8: return launch_bt_t<8, NBO>(G, lt, LI, in, out, s);
+    case 16: return launch_bt_t<16, NBO>(G, lt, LI, in, out, s);
+    case 32: return launch_bt_t<32, NBO>(G, lt, LI, in, out, s);
+    case 56: return launch_bt_t<56, NBO>(G, lt, LI, in, out, s);
+    case 64: return launch_bt_t<64, NBO>(G, lt, LI, in, out, s);
+    default: return false;
+  }
+}
+
 __device__ double block_sum(double v, double* red) {
   v = warp_sum(v);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -362,6 +565,12 @@ void spmv(Ctx& c, const double* x, double* y, cudaStream_t s) {
 static void bt_solve(Ctx& c, const double* in, double* out, cudaStream_t s) {
   const Geometry& G = c.geo;
   PhaseScope ps(c.prof, "apply.bt_solve", s);
+  if (G.s_hi <= G.s_lo) return;
+  bool done = false;
+  if (G.nbo == 1) done = launch_bt_nbo<1>(G, c.lt, c.LI, in, out, s);
+  else if (G.nbo == 3) done = launch_bt_nbo<3>(G, c.lt, c.LI, in, out, s);
+  else if (G.nbo == 9) done = launch_bt_nbo<9>(G, c.lt, c.LI, in, out, s);
+  if (done) return;
   const size_t smem = sizeof(double) * bt_smem(G).per_warp() * kBtWarps;
   static size_t attr = 0;
   if (smem > attr) {

@@ -78,6 +78,7 @@ struct LocalTables {
   int* node_code = nullptr;  // [nloc_nodes]: >=0 interior row (j*m_pad+r); <0: -(slot+1)
   int* slot_node = nullptr;  // [nG]
   int* irow_node = nullptr;  // [nI_pad] local node of interior row, -1 for pad rows
+  int* irow_rel = nullptr;   // [nI_pad] free-dof offset of the row from the subdomain base, -1 pad
 };
 
 // Per-subdomain index data (device), shapes [nsub x nG_pad] / [nsub x nc_pad].

@@ -304,6 +304,19 @@ void do_setup(bddc_ctx* h, const bddc_setup_desc* d) {
   c.lt.node_code = c.upload(d->node_code, G.nloc_nodes);
   c.lt.slot_node = c.upload(d->slot_node, G.nG);
   c.lt.irow_node = c.upload(d->irow_node, G.nI_pad);
+  {
+    // interior rows: free dof = base(subdomain) + rel (the numbering is affine inside a box)
+    std::vector<int> rel(G.nI_pad, -1);
+    const long long nf0 = G.nfree[0], nf1 = G.nfree[1];
+    for (int rr = 0; rr < G.nI_pad; ++rr) {
+      const int node = d->irow_node[rr];
+      if (node < 0) continue;
+      const int a0 = node % (G.blk[0] + 1), a1 = (node / (G.blk[0] + 1)) % (G.blk[1] + 1);
+      const int a2 = G.dim == 3 ? node / ((G.blk[0] + 1) * (G.blk[1] + 1)) : 0;
+      rel[rr] = (int)(a0 + nf0 * (a1 + nf1 * a2));
+    }
+    c.lt.irow_rel = c.upload(rel.data(), G.nI_pad);
+  }
   const size_t ns = (size_t)G.nsub * G.nG_pad, nc = (size_t)G.nsub * G.nc_pad;
   c.st.slot_gamma = c.upload(d->slot_gamma, ns);
   c.st.slot_w = c.upload(d->slot_w, ns);
