@@ -15,12 +15,15 @@
 
 namespace bddc {
 
+bool schur2d_supported(const Geometry& G);
 bool schur2d(const Ctx& c, int sub0, int cnt, const double* Wd, const double* Wo, const double* E,
              cudaStream_t s);
 
 namespace {
 
-template <int DIM>
+// DENSE: also write the interior blocks T_j / B_j and A_IG densely (generic path); the fused
+// 2D path generates them from the stencil on chip and only needs A_GG and s_i here.
+template <int DIM, bool DENSE>
 __global__ void __launch_bounds__(256) assemble_local_kernel(Geometry G, const double* __restrict__ alpha,
                                                              LocalTables lt, int sub0, double* Wd,
                                                              double* Wo, double* E, double* LS,
@@ -61,6 +64,10 @@ __global__ void __launch_bounds__(256) assemble_local_kernel(Geometry G, const d
       dsum += fabs(v);
       nfree_loc += 1;
     }
+    if (!DENSE) {
+      if (ca < 0 && cb < 0) ls[(-ca - 1) + (long long)(-cb - 1) * G.nG_pad] = v;
+      continue;
+    }
     if (ca >= 0 && cb >= 0) {
       const int ja = ca / G.m_pad, jb = cb / G.m_pad, ra = ca % G.m_pad, rb = cb % G.m_pad;
       if (ja == jb) wd[ja * mm + ra + (long long)rb * G.m_pad] = v;
@@ -72,7 +79,7 @@ __global__ void __launch_bounds__(256) assemble_local_kernel(Geometry G, const d
     }
   }
   // identity on padding
-  for (int idx = threadIdx.x; idx < G.nblk * (G.m_pad - G.m); idx += blockDim.x) {
+  for (int idx = threadIdx.x; DENSE && idx < G.nblk * (G.m_pad - G.m); idx += blockDim.x) {
     const int j = idx / (G.m_pad - G.m), r = G.m + idx % (G.m_pad - G.m);
     wd[j * mm + r + (long long)r * G.m_pad] = 1.0;
   }
@@ -312,21 +319,26 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
     double* SCi = Y + (size_t)chunk * phS;    // S_C^{-1}
     double* LS = c.LS + sub0 * lsS;
     double* PH = c.Phi + sub0 * phS;
-    BDDC_CUDA(cudaMemsetAsync(Wd, 0, sizeof(double) * 2 * (size_t)chunk * wS, s));
-    BDDC_CUDA(cudaMemsetAsync(E, 0, sizeof(double) * cnt * eS, s));
+    const bool fused2d = G.nblk > 0 && schur2d_supported(G);
+    if (!fused2d) {  // the fused 2D kernels generate T_j, B_j and A_IG from the stencil
+      BDDC_CUDA(cudaMemsetAsync(Wd, 0, sizeof(double) * 2 * (size_t)chunk * wS, s));
+      BDDC_CUDA(cudaMemsetAsync(E, 0, sizeof(double) * cnt * eS, s));
+    }
     BDDC_CUDA(cudaMemsetAsync(LS, 0, sizeof(double) * cnt * lsS, s));
     BDDC_CUDA(cudaMemsetAsync(PH, 0, sizeof(double) * cnt * phS, s));
     // 1. assembly
     c.prof.begin("setup.assemble", s);
-    if (G.dim == 2)
-      { assemble_local_kernel<2><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, Wd, Wo, E, c.LS, c.diag_s); BDDC_COUNT(); }
+    if (G.dim == 2 && fused2d)
+      { assemble_local_kernel<2, false><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, Wd, Wo, E, c.LS, c.diag_s); BDDC_COUNT(); }
+    else if (G.dim == 2)
+      { assemble_local_kernel<2, true><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, Wd, Wo, E, c.LS, c.diag_s); BDDC_COUNT(); }
     else
-      { assemble_local_kernel<3><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, Wd, Wo, E, c.LS, c.diag_s); BDDC_COUNT(); }
+      { assemble_local_kernel<3, true><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, Wd, Wo, E, c.LS, c.diag_s); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
     c.prof.end("setup.assemble", s);
     // 2-3. fused on-chip interior elimination (2D) or the generic batched path
     c.prof.begin("setup.schur", s);
-    const bool fused = G.nblk > 0 && schur2d(c, sub0, cnt, Wd, Wo, E, s);
+    const bool fused = fused2d && schur2d(c, sub0, cnt, Wd, Wo, E, s);
     c.prof.end("setup.schur", s);
     BMat LSb{LS, lsS, G.nG_pad};
     if (!fused) {

@@ -136,8 +136,8 @@ __device__ __forceinline__ int gj_inverse_blocked(double* W, double* Dm, int lan
 
 template <int M, bool DIAGB>
 __global__ void __launch_bounds__(32 * kWarpsW) wfactor2d_kernel(Geometry G, int sub0, int cnt,
-                                                                 const double* __restrict__ Wd,
-                                                                 const double* __restrict__ Wo,
+                                                                 const double* __restrict__ alpha,
+                                                                 LocalTables lt,
                                                                  double* __restrict__ LI,
                                                                  int* __restrict__ info) {
   constexpr int P = wpitch<M>();
@@ -150,9 +150,8 @@ __global__ void __launch_bounds__(32 * kWarpsW) wfactor2d_kernel(Geometry G, int
   double* W = smw + warp * wf_warp_doubles<M, DIAGB>();
   double* Dm = W + M * P;
   double* X = Dm + 8 * kDP;
-  const long long mm = (long long)M * M;
-  const double* wd = Wd + (long long)b * G.nblk * mm;
-  const double* wo = Wo + (long long)b * G.nblk * mm;
+  int p[3];
+  sub_coords(G, sub, p);
   double* li = LI + (long long)sub * G.li_stride;
   double* bcg = li + (long long)G.nblk * G.Tm;
   const int px = G.blk[0] - 1;
@@ -160,16 +159,29 @@ __global__ void __launch_bounds__(32 * kWarpsW) wfactor2d_kernel(Geometry G, int
   const int k = lane;  // owned column (general stencil path) / owned row (elsewhere)
   int failed = -1;
   for (int j = 0; j < G.nblk; ++j) {
-    // coupling stencil of plane j (row r = lane): bc[k] for the nbo offsets
+    // this lane's row of plane j from the element stencil: T_j (in-plane, x-1 / x / x+1)
+    // and the coupling B_j to plane j-1 (bc[k] for the nbo offsets)
+    double t_m1 = 0.0, t_0 = 1.0, t_p1 = 0.0;  // identity on padding rows
     double cf[3] = {0.0, 0.0, 0.0};
-    if (j > 0 && lane < G.m) {
+    if (lane < G.m) {
+      int a[3];
+      local_coords(G, lt.irow_node[j * M + lane], a);
+      const int d0[3] = {0, 0, 0}, dm[3] = {-1, 0, 0}, dp[3] = {1, 0, 0};
+      t_0 = local_coef<2>(G, alpha, p, a, d0);
+      if (lane > 0) t_m1 = local_coef<2>(G, alpha, p, a, dm);
+      if (lane + 1 < G.m) t_p1 = local_coef<2>(G, alpha, p, a, dp);
+      if (j > 0) {
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        if (q >= nbo) break;
-        const int x = lane + G.bo_dx[q];
-        if (x >= 0 && x < px) cf[q] = wo[j * mm + lane + (long long)x * M];
+        for (int q = 0; q < 3; ++q) {
+          if (q >= nbo) break;
+          const int x = lane + G.bo_dx[q];
+          const int dq[3] = {G.bo_dx[q], -1, 0};
+          if (x >= 0 && x < px) cf[q] = local_coef<2>(G, alpha, p, a, dq);
+        }
       }
     }
+    // T_j[i][k] seen from row i = lane (tk) or, by symmetry, from column k = lane (ti)
+    auto tk = [&](int kk) { return kk == lane ? t_0 : (kk == lane - 1 ? t_m1 : (kk == lane + 1 ? t_p1 : 0.0)); };
     if (lane < M) {
 #pragma unroll
       for (int q = 0; q < 3; ++q)
@@ -182,7 +194,7 @@ __global__ void __launch_bounds__(32 * kWarpsW) wfactor2d_kernel(Geometry G, int
 #pragma unroll 8
         for (int kk = 0; kk < M; ++kk) {
           const double bk = __shfl_sync(0xffffffffu >> (32 - M), cf[0], kk);
-          W[lane + kk * P] = wd[j * mm + lane + (long long)kk * M] - bi * W[lane + kk * P] * bk;
+          W[lane + kk * P] = tk(kk) - bi * W[lane + kk * P] * bk;
         }
       }
     } else if (j > 0) {
@@ -208,10 +220,10 @@ __global__ void __launch_bounds__(32 * kWarpsW) wfactor2d_kernel(Geometry G, int
           const int kk = k + G.bo_dx[q];
           if (cf[q] != 0.0 && kk >= 0 && kk < M) a += X[i + kk * P] * cf[q];
         }
-        if (k < M) W[i + k * P] = wd[j * mm + i + (long long)k * M] - a;
+        if (k < M) W[i + k * P] = tk(i) - a;  // T symmetric: T[i][k] = T[k][i], k = lane
       }
     } else if (lane < M) {
-      for (int kk = 0; kk < M; ++kk) W[lane + kk * P] = wd[lane + (long long)kk * M];
+      for (int kk = 0; kk < M; ++kk) W[lane + kk * P] = tk(kk);
     }
     __syncwarp();
     const int bad = gj_inverse_blocked<M>(W, Dm, lane);
@@ -234,7 +246,8 @@ __global__ void __launch_bounds__(32 * kWarpsW) wfactor2d_kernel(Geometry G, int
 // ---- R_j / H_j / S_G with DMMA, W_j streamed back from the packed factor ----
 template <int M, int NGP>
 __global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, int sub0,
-                                                                const double* __restrict__ Eg,
+                                                                const double* __restrict__ alpha,
+                                                                LocalTables lt,
                                                                 const double* __restrict__ LI,
                                                                 double* __restrict__ LS) {
   constexpr int P = M + 1;
@@ -251,7 +264,8 @@ __global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, i
   const int b = blockIdx.x, sub = sub0 + b;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
-  const double* eg = Eg + (long long)b * G.nI_pad * G.nG_pad;
+  int p[3];
+  sub_coords(G, sub, p);
   const double* li = LI + (long long)sub * G.li_stride;
   const double* bcg = li + (long long)G.nblk * G.Tm;
   const int nbo = G.nbo;
@@ -266,25 +280,19 @@ __global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, i
   for (int j = 0; j < G.nblk; ++j) {
     const int na = G.nact[j];           // active columns (multiple of 8)
     const int nat = na / 8;
-    // W_j (unpack), stencil, A_IG rows (active columns): every global load of the plane is
-    // issued before the first shared-memory store (one latency per plane, not one per column)
+    // W_j (unpack) and the coupling stencil: every global load of the plane is issued before
+    // the first shared-memory store; A_IG rows (active columns) come from the element stencil
     {
       constexpr int TM = M * (M + 1) / 2;
       constexpr int NWL = (TM + kSchurThreads - 1) / kSchurThreads;
-      constexpr int NEL = (M * NGP + kSchurThreads - 1) / kSchurThreads;
-      double wv[NWL], ev[NEL];
+      double wv[NWL];
 #pragma unroll
       for (int u = 0; u < NWL; ++u) {
         const int e = tid + u * kSchurThreads;
         wv[u] = e < TM ? li[(long long)j * G.Tm + e] : 0.0;
       }
-#pragma unroll
-      for (int u = 0; u < NEL; ++u) {
-        const int idx = tid + u * kSchurThreads;
-        const int r = idx % M, cc = idx / M;
-        ev[u] = idx < M * na ? eg[(j * M + r) + (long long)cc * G.nI_pad] : 0.0;
-      }
       const double bv = tid < M * nbo ? bcg[(long long)j * M * nbo + tid] : 0.0;
+      for (int idx = tid; idx < M * na; idx += kSchurThreads) sm[O_R + (idx / na) * EP + idx % na] = 0.0;
 #pragma unroll
       for (int u = 0; u < NWL; ++u) {
         const int e = tid + u * kSchurThreads;
@@ -299,12 +307,22 @@ __global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, i
           sm[O_W + c + r * P] = wv[u];
         }
       }
-#pragma unroll
-      for (int u = 0; u < NEL; ++u) {
-        const int idx = tid + u * kSchurThreads;
-        if (idx < M * na) sm[O_R + (idx % M) * EP + idx / M] = ev[u];
-      }
       if (tid < M * nbo) sm[O_BC + (tid / nbo) * 3 + tid % nbo] = bv;
+      __syncthreads();
+      // A_IG: row r of plane j couples to the (non-Dirichlet) surface slots among its 8
+      // stencil neighbours
+      for (int idx = tid; idx < G.m * 8; idx += kSchurThreads) {
+        const int r = idx >> 3, o = idx & 7, oo = o < 4 ? o : o + 1;  // skip the centre
+        int a[3];
+        local_coords(G, lt.irow_node[j * M + r], a);
+        const int d[3] = {oo % 3 - 1, oo / 3 - 1, 0};
+        const int bn[3] = {a[0] + d[0], a[1] + d[1], 0};
+        const int code = lt.node_code[bn[0] + (G.blk[0] + 1) * bn[1]];
+        if (code >= 0) continue;
+        const int slot = -code - 1;
+        if (slot >= na || local_to_free(G, p, bn) < 0) continue;
+        sm[O_R + r * EP + slot] = local_coef<2>(G, alpha, p, a, d);
+      }
     }
     __syncthreads();
     if (j > 0) {  // R_j -= B_j H_{j-1} on the previously active columns
@@ -382,14 +400,20 @@ void launch_schur2d(const Ctx& c, int sub0, int cnt, const double* Wd, const dou
     BDDC_CUDA(cudaFuncSetAttribute(schur2d_kernel<M, NGP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
     attr = true;
   }
-  if (diagb) { wfactor2d_kernel<M, true><<<ceil_div(cnt, kWarpsW), 32 * kWarpsW, smem_w, s>>>(c.geo, sub0, cnt, Wd, Wo, c.LI, c.info); BDDC_COUNT(); }
-  else { wfactor2d_kernel<M, false><<<ceil_div(cnt, kWarpsW), 32 * kWarpsW, smem_w, s>>>(c.geo, sub0, cnt, Wd, Wo, c.LI, c.info); BDDC_COUNT(); }
+  if (diagb) { wfactor2d_kernel<M, true><<<ceil_div(cnt, kWarpsW), 32 * kWarpsW, smem_w, s>>>(c.geo, sub0, cnt, c.alpha, c.lt, c.LI, c.info); BDDC_COUNT(); }
+  else { wfactor2d_kernel<M, false><<<ceil_div(cnt, kWarpsW), 32 * kWarpsW, smem_w, s>>>(c.geo, sub0, cnt, c.alpha, c.lt, c.LI, c.info); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
-  { schur2d_kernel<M, NGP><<<cnt, kSchurThreads, smem_s, s>>>(c.geo, sub0, E, c.LI, c.LS); BDDC_COUNT(); }
+  { schur2d_kernel<M, NGP><<<cnt, kSchurThreads, smem_s, s>>>(c.geo, sub0, c.alpha, c.lt, c.LI, c.LS); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
 }
 
 }  // namespace
+
+bool schur2d_supported(const Geometry& G) {
+  if (G.dim != 2 || G.nbo > 3) return false;
+  return (G.m_pad == 32 && G.nG_pad == 128) || (G.m_pad == 16 && G.nG_pad == 64) ||
+         (G.m_pad == 8 && G.nG_pad == 32);
+}
 
 // Returns false if the geometry is not covered by a compiled instance.
 bool schur2d(const Ctx& c, int sub0, int cnt, const double* Wd, const double* Wo, const double* E,
