@@ -31,6 +31,19 @@ __device__ __forceinline__ void mma_acc(double& c0, double& c1, const double* A,
   }
 }
 
+// C(8x8 tile) += A(8 x K) B(K x 8) with compile-time K and strides (immediate offsets)
+template <int K, int ARS, int ACS, int BRS, int BCS>
+__device__ __forceinline__ void mma_acc_t(double& c0, double& c1, const double* A, const double* B, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  const double* a = A + g * ARS + t * ACS;
+  const double* b = B + t * BRS + g * BCS;
+#pragma unroll
+  for (int k = 0; k < K; k += 4) dmma884(c0, c1, a[k * ACS], b[k * BRS]);
+}
+
+// lower-triangular 8x8 tile coordinates (I, J) of tile index tt = I(I+1)/2 + J (NGP <= 128)
+__constant__ int2 c_lower_tiles[16 * 17 / 2];
+
 // ---- W recursion (one warp per subdomain) ----
 // W pitch = 4 mod 16 doubles: conflict-free 8x8x4 DMMA fragments; pivot-inverse pitch 20
 template <int M>
@@ -292,7 +305,8 @@ __global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, i
         wv[u] = e < TM ? li[(long long)j * G.Tm + e] : 0.0;
       }
       const double bv = tid < M * nbo ? bcg[(long long)j * M * nbo + tid] : 0.0;
-      for (int idx = tid; idx < M * na; idx += kSchurThreads) sm[O_R + (idx / na) * EP + idx % na] = 0.0;
+      for (int r = warp; r < M; r += NW)
+        for (int cc = lane; cc < na; cc += 32) sm[O_R + r * EP + cc] = 0.0;
 #pragma unroll
       for (int u = 0; u < NWL; ++u) {
         const int e = tid + u * kSchurThreads;
@@ -325,17 +339,18 @@ __global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, i
       }
     }
     __syncthreads();
-    if (j > 0) {  // R_j -= B_j H_{j-1} on the previously active columns
-      for (int idx = tid; idx < M * nprev; idx += kSchurThreads) {
-        const int r = idx / nprev, cc = idx % nprev;
-        double a = 0.0;
+    if (j > 0) {  // R_j -= B_j H_{j-1} on the previously active columns (warp = row)
+      for (int r = warp; r < M; r += NW) {
+        double cf[3];
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          if (q >= nbo) break;
-          const double cf = sm[O_BC + r * 3 + q];
-          if (cf != 0.0) a += cf * sm[O_H + (r + bdx[q]) * EP + cc];
+        for (int q = 0; q < 3; ++q) cf[q] = q < nbo ? sm[O_BC + r * 3 + q] : 0.0;
+        for (int cc = lane; cc < nprev; cc += 32) {
+          double a = 0.0;
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            if (q < nbo && cf[q] != 0.0) a += cf[q] * sm[O_H + (r + bdx[q]) * EP + cc];
+          sm[O_R + r * EP + cc] -= a;
         }
-        sm[O_R + r * EP + cc] -= a;
       }
       __syncthreads();
     }
@@ -343,7 +358,7 @@ __global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, i
     for (int tt = warp; tt < (M / 8) * nat; tt += NW) {
       const int ti = tt % (M / 8), tj = tt / (M / 8);
       double c0 = 0.0, c1 = 0.0;
-      mma_acc(c0, c1, sm + O_W + ti * 8, 1, P, sm + O_R + tj * 8, EP, 1, M, lane);
+      mma_acc_t<M, 1, P, EP, 1>(c0, c1, sm + O_W + ti * 8, sm + O_R + tj * 8, lane);
       sm[O_H + (ti * 8 + g) * EP + tj * 8 + 2 * t4] = c0;
       sm[O_H + (ti * 8 + g) * EP + tj * 8 + 2 * t4 + 1] = c1;
     }
@@ -354,10 +369,8 @@ __global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, i
     for (int q = 0; q < SYRK_PER_WARP; ++q) {
       const int tt = warp + q * NW;
       if (tt < nlt_act) {
-        int I = 0;
-        while ((I + 1) * (I + 2) / 2 <= tt) ++I;
-        const int J = tt - I * (I + 1) / 2;
-        mma_acc(acc[q][0], acc[q][1], sm + O_R + I * 8, 1, EP, sm + O_H + J * 8, EP, 1, M, lane);
+        const int2 ij = c_lower_tiles[tt];
+        mma_acc_t<M, 1, EP, EP, 1>(acc[q][0], acc[q][1], sm + O_R + ij.x * 8, sm + O_H + ij.y * 8, lane);
       }
     }
     nprev = na;
@@ -370,9 +383,7 @@ __global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, i
   for (int q = 0; q < SYRK_PER_WARP; ++q) {
     const int tt = warp + q * NW;
     if (tt >= NLT) continue;
-    int I = 0;
-    while ((I + 1) * (I + 2) / 2 <= tt) ++I;
-    const int J = tt - I * (I + 1) / 2;
+    const int I = c_lower_tiles[tt].x, J = c_lower_tiles[tt].y;
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int r = I * 8 + g, c = J * 8 + 2 * t4 + e;
@@ -393,6 +404,10 @@ void launch_schur2d(const Ctx& c, int sub0, int cnt, const double* Wd, const dou
   const size_t smem_s = sizeof(double) * (2 * M * (NGP + 4) + M * (M + 1) + 3 * M);
   static bool attr = false;
   if (!attr) {
+    int2 tiles[16 * 17 / 2];
+    for (int I = 0, t = 0; I < 16; ++I)
+      for (int J = 0; J <= I; ++J) tiles[t++] = make_int2(I, J);
+    BDDC_CUDA(cudaMemcpyToSymbol(c_lower_tiles, tiles, sizeof(tiles)));
     BDDC_CUDA(cudaFuncSetAttribute(wfactor2d_kernel<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)(sizeof(double) * kWarpsW * wf_warp_doubles<M, true>())));
     BDDC_CUDA(cudaFuncSetAttribute(wfactor2d_kernel<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
