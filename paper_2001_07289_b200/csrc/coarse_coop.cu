@@ -26,7 +26,7 @@ namespace cg = cooperative_groups;
 
 namespace bddc {
 
-constexpr int kX1Chunk = 256;
+constexpr int kX1Chunk = 64;
 constexpr int kCoopStages = 3;  // cp.async depth of the engine's GEMM tiles (fits the factor smem)  // split-K of the left-looking inverse accumulation
 
 enum CoopType : int {
@@ -141,14 +141,27 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
     case CT_X2: {  // X[k.., c] = -inv Y[:, c] (c < panel) or X[k.., k..] = inv
       const int k = t.arg * kTile, nb = min(kTile, s - k), c = t.a * kTile;
       const double* inv = pg.pool + pg.sc.inv[node] + (t.arg & 1) * kTileInvStride;
-      if (c < k) {  // X[k, c] = -inv sum_q Y_q[:, c]
+      if (c < k) {  // X[k, c] = -inv sum_q Y_q[:, c]: sum the partials into Y_0, one GEMM
         const int nq = (k - c + kX1Chunk - 1) / kX1Chunk;
-        for (int qq = 0; qq < nq; ++qq) {
-          const double* Y = pg.pool + pg.sc.Y[node] + (long long)qq * kTile * s;
-          gemm_tile<false, false, kCoopStages>(inv, kTile, Y + (long long)c * kTile, kTile, X + k + (long long)c * ldx,
-                                  ldx, nb, kTile, nb, 0, 0, -1.0, qq ? 1.0 : 0.0, false, smem);
+        double* Y0 = pg.pool + pg.sc.Y[node] + (long long)c * kTile;
+        if (nq > 1) {
+          const long long qs = (long long)kTile * s;  // stride between partials
+          constexpr int PER = kTile * kTile / 128;     // elements per thread (128 threads)
+          double acc[PER];  // one partial = PER independent loads in flight per thread
+#pragma unroll
+          for (int u = 0; u < PER; ++u) acc[u] = __ldcg(Y0 + threadIdx.x + 128 * u);
+          for (int qq = 1; qq < nq; ++qq) {
+            const double* Yq = Y0 + qq * qs;
+#pragma unroll
+            for (int u = 0; u < PER; ++u) acc[u] += __ldcg(Yq + threadIdx.x + 128 * u);
+          }
+#pragma unroll
+          for (int u = 0; u < PER; ++u) Y0[threadIdx.x + 128 * u] = acc[u];
+          __threadfence();
           __syncthreads();
         }
+        gemm_tile<false, false, kCoopStages>(inv, kTile, Y0, kTile, X + k + (long long)c * ldx, ldx, nb, kTile,
+                                             nb, 0, 0, -1.0, 0.0, false, smem);
       } else {
         for (int idx = threadIdx.x; idx < nb * nb; idx += blockDim.x) {
           const int i = idx % nb, j = idx / nb;
