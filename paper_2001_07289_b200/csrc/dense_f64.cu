@@ -42,8 +42,16 @@ __global__ void __launch_bounds__(128) gemm_f64_kernel(GemmArgs args) {
   const int tm = blockIdx.x % tiles_m, tn = blockIdx.x / tiles_m;
   const int m0 = tm * BM, n0 = tn * BN;
   if (args.lower && n0 > m0 + BM - 1) return;  // tile strictly above the diagonal
+  int k_lo = 0, k_hi = t.K;  // nonzero K range of the tile for triangular operands
+  switch (args.tri) {
+    case 1: k_hi = min(t.K, m0 + BM); break;  // op(A)(m, k) = 0 for k > m
+    case 2: k_lo = m0; break;                  // op(A)(m, k) = 0 for k < m
+    case 3: k_lo = n0; break;                  // op(B)(k, n) = 0 for k < n
+    case 4: k_hi = min(t.K, n0 + BN); break;   // op(B)(k, n) = 0 for k > n
+    default: break;
+  }
   gemm_tile<TA, TB, kGemmStages>(t.A, t.lda, t.B, t.ldb, t.C, t.ldc, t.M, t.N, t.K, m0, n0, args.alpha,
-                    args.beta, args.lower != 0, smem);
+                                 args.beta, args.lower != 0, smem, k_lo, k_hi, args.mirror != 0);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -227,7 +235,7 @@ void trsm_tile(const TileArgs& a, TrsmKind kind, cudaStream_t s) {
 }
 
 void gemm_batched(bool tA, bool tB, int M, int N, int K, double alpha, BMat A, BMat B,
-                  double beta, BMat C, int count, cudaStream_t s, bool lower) {
+                  double beta, BMat C, int count, cudaStream_t s, bool lower, int tri, bool mirror) {
   if (M <= 0 || N <= 0) return;
   GemmArgs g;
   g.A = A.p; g.sA = A.stride; g.lda = A.ld;
@@ -235,6 +243,7 @@ void gemm_batched(bool tA, bool tB, int M, int N, int K, double alpha, BMat A, B
   g.C = C.p; g.sC = C.stride; g.ldc = C.ld;
   g.M = M; g.N = N; g.K = K; g.count = count;
   g.alpha = alpha; g.beta = beta; g.lower = lower ? 1 : 0;
+  g.tri = tri; g.mirror = mirror ? 1 : 0;
   if (K <= 0) {
     if (beta == 1.0) return;
   }
@@ -273,6 +282,42 @@ void potrf_batched(BMat A, int n, int npiv, int count, int* info, double* scratc
     BMat A22 = A.at(k + nb, k + nb);
     gemm_batched(false, true, rest, rest, nb, -1.0, L21, L21, 1.0, A22, count, s, true);
   }
+}
+
+namespace {
+// Linv diagonal blocks <- the kept tile inverses (64 x 64, ld 64); zero the upper block
+__global__ void place_diag_inv_kernel(const double* __restrict__ scr, long long sInv, int n, double* Linv,
+                                      long long sL, int ldl) {
+  const int b = blockIdx.x;
+  const double* inv = scr + b * sInv;
+  double* L = Linv + b * sL;
+  const int nb = (n + kTile - 1) / kTile;
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    const int i = idx % n, j = idx / n;
+    const int bi = i / kTile, bj = j / kTile;
+    if (bi == bj) L[i + (long long)j * ldl] = inv[bi * kTileInvStride + (i - bi * kTile) + (j - bj * kTile) * kTile];
+    else if (bi < bj) L[i + (long long)j * ldl] = 0.0;
+  }
+  (void)nb;
+}
+}  // namespace
+
+bool trtri_from_tiles(BMat L, int n, BMat Linv, int count, const double* scratch, cudaStream_t s) {
+  if (n > 2 * kTile || n <= 0) return false;
+  const long long sInv = (long long)ceil_div(n, kTile) * kTileInvStride;
+  place_diag_inv_kernel<<<count, 256, 0, s>>>(scratch, sInv, n, Linv.p, Linv.stride, Linv.ld);
+  BDDC_COUNT();
+  BDDC_LAUNCH_CHECK();
+  if (n > kTile) {  // Linv10 = -D1 (L10 D0), through the upper-right block as scratch
+    const int n1 = n - kTile;
+    BMat D0{(double*)scratch, sInv, kTile}, D1{(double*)scratch + kTileInvStride, sInv, kTile};
+    gemm_batched(false, false, n1, kTile, kTile, 1.0, L.at(kTile, 0), D0, 0.0, Linv.at(kTile, 0), count, s,
+                 false, 3);  // D0 lower: B(k, n) = 0 for k < n
+    // Linv10 <- -D1 Linv10 is in place over rows: one 64-row tile (n1 <= 64) -> safe
+    gemm_batched(false, false, n1, kTile, n1, -1.0, D1, Linv.at(kTile, 0), 0.0, Linv.at(kTile, 0), count, s,
+                 false, 1);  // D1 lower: k <= m
+  }
+  return true;
 }
 
 size_t trsm_scratch_doubles(int n, int count) {

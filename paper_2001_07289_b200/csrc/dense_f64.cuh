@@ -29,6 +29,8 @@ struct GemmArgs {
   int max_M = 0, max_N = 0;         // grid sizing when tasks != nullptr
   double alpha = 1.0, beta = 1.0;
   int lower = 0;
+  int tri = 0;     // structural zeros: 1 op(A) lower, 2 op(A) upper, 3 op(B) lower, 4 op(B) upper
+  int mirror = 0;  // with lower: also write the upper triangle (symmetric result)
 };
 
 struct TileTask {
@@ -90,7 +92,11 @@ void trsm_batched(TrsmKind kind, BMat L, int n, BMat B, int nother, int count, d
 size_t trsm_scratch_doubles(int n, int count);
 // C = alpha op(A) op(B) + beta C over a strided batch.
 void gemm_batched(bool tA, bool tB, int M, int N, int K, double alpha, BMat A, BMat B,
-                  double beta, BMat C, int count, cudaStream_t s, bool lower = false);
+                  double beta, BMat C, int count, cudaStream_t s, bool lower = false, int tri = 0,
+                  bool mirror = false);
+// L^{-1} of a batch of n x n lower factors (n <= 128) from the diagonal-tile inverses left in
+// scratch by potrf_batched (2x2 block formula); Linv is written in full (zero upper).
+bool trtri_from_tiles(BMat L, int n, BMat Linv, int count, const double* scratch, cudaStream_t s);
 
 constexpr int kTile = 64;
 

@@ -381,9 +381,11 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
     {
       // 5a. L_S^{-1} (the diagonal-tile inverses are left in c.tinv by the factorization)
       PhaseScope pli(c.prof, "setup.Linv", s);
-      { identity_kernel<<<cnt, 256, 0, s>>>(LIv, G.nG_pad, lsS); BDDC_COUNT(); }
-      BDDC_LAUNCH_CHECK();
-      trsm_batched(TRSM_LLN, LSb, G.nG_pad, LIb, G.nG_pad, cnt, c.tinv, s, true);
+      if (!trtri_from_tiles(LSb, G.nG_pad, LIb, cnt, c.tinv, s)) {
+        { identity_kernel<<<cnt, 256, 0, s>>>(LIv, G.nG_pad, lsS); BDDC_COUNT(); }
+        BDDC_LAUNCH_CHECK();
+        trsm_batched(TRSM_LLN, LSb, G.nG_pad, LIb, G.nG_pad, cnt, c.tinv, s, true);
+      }
     }
     if (G.nc_pad > 0) {
       PhaseScope pphi(c.prof, "setup.Phi", s);
@@ -395,7 +397,7 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
       BMat Xb{X, phS, G.nG_pad};
       BMat Yb{Y, phS, G.nG_pad};
       BMat SCib{SCi, scS, G.nc_pad};
-      gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nG_pad, 1.0, LIb, PHb, 0.0, Xb, cnt, s);
+      gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nG_pad, 1.0, LIb, PHb, 0.0, Xb, cnt, s, false, 1);
       gemm_batched(true, false, G.nc_pad, G.nc_pad, G.nG_pad, 1.0, Xb, Xb, 0.0, SCb, cnt, s);
       { sc_pad_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, SC); BDDC_COUNT(); }
       BDDC_LAUNCH_CHECK();
@@ -413,7 +415,7 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
       }
       gemm_batched(true, false, G.nc_pad, G.nc_pad, G.nc_pad, 1.0, LCi, LCi, 0.0, SCib, cnt, s);
       gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nc_pad, 1.0, Xb, SCib, 0.0, Yb, cnt, s);
-      gemm_batched(true, false, G.nG_pad, G.nc_pad, G.nG_pad, 1.0, LIb, Yb, 0.0, PHb, cnt, s);
+      gemm_batched(true, false, G.nG_pad, G.nc_pad, G.nG_pad, 1.0, LIb, Yb, 0.0, PHb, cnt, s, false, 2);
       // 6. P = Phi^T (S_Gamma Phi)
       BMat Pb{P, scS, G.nc_pad};
       gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nG_pad, 1.0, SGb, PHb, 0.0, Xb, cnt, s);
@@ -426,13 +428,14 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
       // 7. explicit interface operator T = (I - Phi C) S_K^{-1} = L^{-T} L^{-1} - Phi S_C Phi^T
       //    (symmetric; replaces L_S so the apply's local Neumann solve is one GEMV)
       PhaseScope pt(c.prof, "setup.T", s);
-      gemm_batched(true, false, G.nG_pad, G.nG_pad, G.nG_pad, 1.0, LIb, LIb, 0.0, LSb, cnt, s);
+      // lower tiles only, mirrored (symmetric); L^{-T} upper: tile row m0 needs k >= m0
+      gemm_batched(true, false, G.nG_pad, G.nG_pad, G.nG_pad, 1.0, LIb, LIb, 0.0, LSb, cnt, s, true, 2, true);
       if (G.nc_pad > 0) {
         BMat PHb{PH, phS, G.nG_pad};
         BMat Xb{X, phS, G.nG_pad};
         BMat SCcb{SCc, scS, G.nc_pad};
         gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nc_pad, 1.0, PHb, SCcb, 0.0, Xb, cnt, s);
-        gemm_batched(false, true, G.nG_pad, G.nG_pad, G.nc_pad, -1.0, Xb, PHb, 1.0, LSb, cnt, s);
+        gemm_batched(false, true, G.nG_pad, G.nG_pad, G.nc_pad, -1.0, Xb, PHb, 1.0, LSb, cnt, s, true, 0, true);
       }
     }
   }

@@ -91,10 +91,13 @@ constexpr int gemm_smem_doubles() { return 2 * NS * TILE_A; }
 // full K range; 128 threads (4 warps, 2x2), DMMA.8x8x4 accumulators, NS-stage cp.async
 // pipeline (NS - 1 k-slices in flight ahead of the one being multiplied).
 // lower: only entries with row >= col are written.
+// k_lo / k_hi (multiples of BK or K): the nonzero K range of this tile (triangular operands);
+// mirror (with lower): also write C(c, r) = C(r, c) (symmetric result).
 template <bool TA, bool TB, int NS = 2>
 __device__ __forceinline__ void gemm_tile(const double* A, int lda, const double* B, int ldb,
                                           double* C, int ldc, int M, int N, int K, int m0, int n0,
-                                          double alpha, double beta, bool lower, double* smem) {
+                                          double alpha, double beta, bool lower, double* smem,
+                                          int k_lo = 0, int k_hi = -1, bool mirror = false) {
   static_assert(NS >= 2, "at least double buffering");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 1, wn = warp >> 1;
@@ -104,7 +107,8 @@ __device__ __forceinline__ void gemm_tile(const double* A, int lda, const double
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  const int nk = (K + BK - 1) / BK;
+  const int kb0 = k_lo / BK;
+  const int nk = ((k_hi < 0 ? K : min(K, k_hi)) + BK - 1) / BK - kb0;
   const bool al_a = ((((unsigned long long)A) & 15) == 0) && ((lda & 1) == 0);
   const bool al_b = ((((unsigned long long)B) & 15) == 0) && ((ldb & 1) == 0);
   auto As = [&](int st) { return smem + st * TILE_A; };
@@ -113,8 +117,8 @@ __device__ __forceinline__ void gemm_tile(const double* A, int lda, const double
 #pragma unroll
   for (int p = 0; p < NS - 1; ++p) {
     if (p < nk) {
-      load_a<TA>(As(p), A, lda, M, K, m0, p * BK, tid, al_a);
-      load_b<TB>(Bs(p), B, ldb, N, K, n0, p * BK, tid, al_b);
+      load_a<TA>(As(p), A, lda, M, K, m0, (kb0 + p) * BK, tid, al_a);
+      load_b<TB>(Bs(p), B, ldb, N, K, n0, (kb0 + p) * BK, tid, al_b);
     }
     cp_async_commit();  // empty groups keep the group count uniform
   }
@@ -122,8 +126,8 @@ __device__ __forceinline__ void gemm_tile(const double* A, int lda, const double
     const int st = kt % NS;
     const int pf = kt + NS - 1;  // slice to prefetch into the stage freed last iteration
     if (pf < nk) {
-      load_a<TA>(As(pf % NS), A, lda, M, K, m0, pf * BK, tid, al_a);
-      load_b<TB>(Bs(pf % NS), B, ldb, N, K, n0, pf * BK, tid, al_b);
+      load_a<TA>(As(pf % NS), A, lda, M, K, m0, (kb0 + pf) * BK, tid, al_a);
+      load_b<TB>(Bs(pf % NS), B, ldb, N, K, n0, (kb0 + pf) * BK, tid, al_b);
     }
     cp_async_commit();
     cp_async_wait<NS - 1>();  // slice kt has landed
@@ -180,6 +184,7 @@ __device__ __forceinline__ void gemm_tile(const double* A, int lda, const double
         double v = alpha * acc[i][j][e];
         if (beta != 0.0) v += beta * cv[i][j][e];
         C[row + (long long)col * ldc] = v;
+        if (mirror && row != col) C[col + (long long)row * ldc] = v;
       }
     }
   }
