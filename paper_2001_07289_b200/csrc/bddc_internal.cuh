@@ -233,6 +233,7 @@ struct Ctx {
   Geometry geo{};
   int element = 0;
   int coarse_scaling = 0;  // 0 reference (Psi = Phi / s^2), 1 spec (Psi = Phi)
+  bool coarse_sweep = false;  // coarse fronts by block symmetric sweep (else Cholesky + inverse)
   bool setup_done = false;
   // inputs (device)
   double* alpha = nullptr;  // [ncells]

@@ -294,6 +294,10 @@ void do_setup(bddc_ctx* h, const bddc_setup_desc* d) {
   }
   c.element = d->element;
   c.coarse_scaling = d->coarse_scaling;
+  {
+    const char* e = getenv("BDDC_COARSE_SWEEP");
+    c.coarse_sweep = e && atoi(e) != 0;
+  }
   h->ncells = ncells;
 
   cudaEvent_t e0, e1;

@@ -112,7 +112,8 @@ void build_level_schedule(Ctx& c) {
           const size_t first = ft.size();
           const int p0 = pf;
           for (int c0 = 0; c0 < sz; c0 += 256) {
-            if (r0 < sz && c0 > r0 + 63) break;  // above the lower-triangular L11^{-1}
+            // separator-only chunks: a copy (sweep) / the lower-triangular L11^{-1} (Cholesky)
+            if (c.coarse_sweep ? (r0 + 64 <= sz && c0 > 0) : (r0 < sz && c0 > r0 + 63)) break;
             CsTask t = base(nd);
             t.r0 = r0;
             t.c0 = c0;
@@ -131,7 +132,7 @@ void build_level_schedule(Ctx& c) {
       for (int c0 = 0; c0 < sz; c0 += 64) {
         const size_t first = bt.size();
         const int p0 = pb;
-        for (int r0 = (c0 / 256) * 256; r0 < f; r0 += 256) {
+        for (int r0 = c.coarse_sweep ? 0 : (c0 / 256) * 256; r0 < f; r0 += 256) {  // sweep: full A11^{-1}
           CsTask t = base(nd);
           t.r0 = r0;
           t.c0 = c0;

@@ -31,7 +31,22 @@ constexpr int kCoopStages = 3;  // cp.async depth of the engine's GEMM tiles (fi
 
 enum CoopType : int {
   CT_EA = 0, CT_PT = 1, CT_TS = 2, CT_X1 = 3, CT_SY = 4, CT_X2 = 5, CT_W = 6, CT_CB = 7,
+  // block symmetric sweep (Gauss-Jordan with inverse pivots) formulation
+  CT_SP = 8,   // D_P = inverse of the pivot tile (P, P)
+  CT_SB = 9,   // B_I = M_{I,P} D_P  (block I != P)
+  CT_SCP = 10, // column P <- B (block I), pivot tile <- -D_P
+  CT_SC = 11,  // M_IJ -= B_I M_{J,P}^T  (lower tiles, I, J != P) [+ lookahead D_{P+1}]
+  CT_SM = 12,  // separator block -> full +A11^{-1} (negate, mirror)
 };
+
+// Sweep block map of panel P (pivot columns [64P, 64P + nb)): the other rows / columns in
+// 64-blocks, before the panel aligned, after it starting at 64P + nb.
+__host__ __device__ __forceinline__ int sweep_rb(int P, int nb, int i) {
+  return i < P ? 64 * i : 64 * P + nb + 64 * (i - P);
+}
+__host__ __device__ __forceinline__ int sweep_nblocks(int P, int nb, int f) {
+  return P + (f - 64 * P - nb + 63) / 64;
+}
 
 struct CoopTask {
   int type, node, a, b, arg;
@@ -193,6 +208,92 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
       }
       break;
     }
+    case CT_SP: {  // D_P = (M_PP)^{-1}
+      const int k = t.arg * kTile, nb = min(kTile, s - k);
+      double* D = pg.pool + pg.sc.inv[node] + (t.arg & 1) * kTileInvStride;
+      const int bad = gj_tile_inverse(F + k + (long long)k * ld, ld, nb, D, smem);
+      if (threadIdx.x == 0 && bad >= 0) atomicMin(info + node, fd.sep_start[node] + k + bad);
+      break;
+    }
+    case CT_SB: {  // B_I = C_I D_P, C_I = M_{I,P}
+      const int P = t.arg, k = P * kTile, nb = min(kTile, s - k), I = t.a;
+      const int r0 = sweep_rb(P, nb, I), m = min(kTile, f - r0);
+      const int ldb = pg.sc.ldw[node];
+      const double* D = pg.pool + pg.sc.inv[node] + (P & 1) * kTileInvStride;
+      double* Bc = pg.pool + pg.sc.X[node] + (long long)(P & 1) * ldb * kTile;
+      if (I > P - 1 && r0 > k) {  // below the panel: tile (I, P) stored
+        gemm_tile<false, false, kCoopStages>(F + r0 + (long long)k * ld, ld, D, kTile, Bc + r0, ldb, m, nb, nb,
+                                             0, 0, 1.0, 0.0, false, smem);
+      } else if (I == P - 1) {  // M_{P-1,P} = (M_{P,P-1})^T = (B^{(P-1)} rows of panel P)^T
+        const double* Bp = pg.pool + pg.sc.X[node] + (long long)((P - 1) & 1) * ldb * kTile;
+        gemm_tile<true, false, kCoopStages>(Bp + k, ldb, D, kTile, Bc + r0, ldb, m, nb, nb, 0, 0, 1.0, 0.0,
+                                            false, smem);
+      } else {  // above: M_{I,P} = (tile (P, I))^T
+        gemm_tile<true, false, kCoopStages>(F + k + (long long)r0 * ld, ld, D, kTile, Bc + r0, ldb, m, nb, nb,
+                                            0, 0, 1.0, 0.0, false, smem);
+      }
+      break;
+    }
+    case CT_SCP: {  // panel P's column <- B (map block a), or (b = 1) pivot tile <- -D_P
+      const int P = t.arg, k = P * kTile, nb = min(kTile, s - k), I = t.a;
+      const int ldb = pg.sc.ldw[node];
+      if (t.b == 1) {
+        const double* D = pg.pool + pg.sc.inv[node] + (P & 1) * kTileInvStride;
+        for (int e = threadIdx.x; e < kTile * kTile; e += blockDim.x) {
+          const int r = e & 63, c = e >> 6;
+          if (r < nb && c < nb && r >= c) F[(k + r) + (long long)(k + c) * ld] = -D[e];
+        }
+        break;
+      }
+      const double* Bc = pg.pool + pg.sc.X[node] + (long long)(P & 1) * ldb * kTile;
+      const int r0 = sweep_rb(P, nb, I), m = min(kTile, f - r0);
+      if (r0 > k) {  // below: tile (I, P) <- B_I
+        for (int e = threadIdx.x; e < kTile * kTile; e += blockDim.x) {
+          const int r = e & 63, c = e >> 6;
+          if (r < m && c < nb) F[(r0 + r) + (long long)(k + c) * ld] = Bc[(r0 + r) + (long long)c * ldb];
+        }
+      } else {  // above: tile (P, I) <- B_I^T
+        for (int e = threadIdx.x; e < kTile * kTile; e += blockDim.x) {
+          const int c = e & 63, r = e >> 6;  // row r of the pivot panel, column c of block I
+          if (r < nb && c < m) F[(k + r) + (long long)(r0 + c) * ld] = Bc[(r0 + c) + (long long)r * ldb];
+        }
+      }
+      break;
+    }
+    case CT_SC: {  // M_IJ -= B_I C_J^T on the lower tile (I >= J), I, J != P
+      const int P = t.arg, k = P * kTile, nb = min(kTile, s - k), I = t.a, J = t.b;
+      const int ldb = pg.sc.ldw[node];
+      const int ri = sweep_rb(P, nb, I), rj = sweep_rb(P, nb, J);
+      const int mi = min(kTile, f - ri), nj = min(kTile, f - rj);
+      const double* Bc = pg.pool + pg.sc.X[node] + (long long)(P & 1) * ldb * kTile;
+      double* Cij = F + ri + (long long)rj * ld;
+      if (rj > k)  // C_J = tile (J, P): B(kk, n) = M[rj + n][k + kk]
+        gemm_tile<false, true, kCoopStages>(Bc + ri, ldb, F + rj + (long long)k * ld, ld, Cij, ld, mi, nj, nb, 0, 0,
+                                            -1.0, 1.0, I == J, smem);
+      else  // C_J = M_{J,P} = (tile (P, J))^T: B(kk, n) = M[k + kk][rj + n]
+        gemm_tile<false, false, kCoopStages>(Bc + ri, ldb, F + k + (long long)rj * ld, ld, Cij, ld, mi, nj, nb, 0,
+                                             0, -1.0, 1.0, I == J, smem);
+      if (I == J && ri == k + nb && k + nb < s) {  // lookahead: next panel's pivot tile is final
+        __syncthreads();
+        const int k1 = k + nb, nb1 = min(kTile, s - k1);
+        double* D1 = pg.pool + pg.sc.inv[node] + ((P + 1) & 1) * kTileInvStride;
+        const int bad = gj_tile_inverse(F + k1 + (long long)k1 * ld, ld, nb1, D1, smem);
+        if (threadIdx.x == 0 && bad >= 0) atomicMin(info + node, fd.sep_start[node] + k1 + bad);
+      }
+      break;
+    }
+    case CT_SM: {  // separator tile (I, J), I >= J: v = -M (lower), write both triangles
+      const int r0 = t.a * kTile, c0 = t.b * kTile;
+      for (int e = threadIdx.x; e < kTile * kTile; e += blockDim.x) {
+        const int r = r0 + (e & 63), c = c0 + (e >> 6);
+        if (r < s && c < s && r >= c) {
+          const double v = -F[r + (long long)c * ld];
+          F[r + (long long)c * ld] = v;
+          if (r != c) F[c + (long long)r * ld] = v;
+        }
+      }
+      break;
+    }
   }
 }
 
@@ -230,6 +331,7 @@ struct SolveProgram {
   const int* br_off;
   int nlevels;
   int nfr;  // number of forward reductions (offset of the backward counters)
+  int sweep;  // fronts hold [A11^{-1} (full); W21] (else [L11^{-1} (lower); W21])
 };
 
 __device__ __forceinline__ double gather_at(const LevelView& lv, const double* __restrict__ upd, long long gbase,
@@ -274,7 +376,7 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
       __syncthreads();
       if (t.mode == 1) {  // s <= 64: one thread per row, all separator columns
         const int r = t.r0 + tid;
-        const int ke = r < f ? (r < s ? r + 1 : s) : 0;
+        const int ke = r < f ? (r < s ? (sp.sweep ? 0 : r + 1) : s) : 0;
         const double* Fr = F + r;
         double fv[16];  // first batch in flight while the right-hand side is gathered
 #pragma unroll
@@ -292,7 +394,7 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
             for (int u = 0; u < 16; ++u) acc[u & 3] += k0 + u < ke ? fv[u] * vs[k0 + u] : 0.0;
           }
           const double a = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-          if (r < s) ybuf[t.s0 + r] = a;
+          if (r < s) ybuf[t.s0 + r] = sp.sweep ? vs[r] : a;
           else fd.upd[t.upd_off + (r - s)] = gather_at(lv, fd.upd, t.gat_base, r) - a;
         }
         continue;
@@ -301,7 +403,7 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
       const int r = t.r0 + rr;
       const int kb = t.c0 + grp * 64;
       int ke = r < f ? min(kb + 64, s) : kb;
-      if (r < s) ke = min(ke, r + 1);
+      if (r < s) ke = sp.sweep ? kb : min(ke, r + 1);
       const double* Fr = F + r;
       double fv[16];  // first batch in flight while the right-hand side is gathered
 #pragma unroll
@@ -326,7 +428,7 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
         const int rw = t.r0 + tid;
         if (tid < 64 && rw < f) {
           const double a = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
-          if (rw < s) ybuf[t.s0 + rw] = a;
+          if (rw < s) ybuf[t.s0 + rw] = sp.sweep ? rhs[t.s0 + rw] + gather_at(lv, fd.upd, t.gat_base, rw) : a;
           else fd.upd[t.upd_off + (rw - s)] = gather_at(lv, fd.upd, t.gat_base, rw) - a;
         }
         continue;
@@ -345,7 +447,7 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
         if (tid < 64 && rw < f) {
           double a = 0.0;
           for (int p = 0; p < R.np; ++p) a += __ldcg(partial + (long long)(R.p0 + p) * 64 + tid);
-          if (rw < s) ybuf[t.s0 + rw] = a;
+          if (rw < s) ybuf[t.s0 + rw] = sp.sweep ? rhs[t.s0 + rw] + gather_at(lv, fd.upd, t.gat_base, rw) : a;
           else fd.upd[t.upd_off + (rw - s)] = gather_at(lv, fd.upd, t.gat_base, rw) - a;
         }
         if (tid == 0) cnt_f[t.red] = 0;
@@ -372,7 +474,7 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
 #pragma unroll
           for (int cc = 0; cc < 8; ++cc) {
             const int k = kw + cc;
-            const bool ok = k < s && r < f && (r >= s || r >= k);
+            const bool ok = k < s && r < f && (sp.sweep || r >= s || r >= k);
             fv[h][cc] = ok ? __ldcs(F + r + (long long)k * ld) : 0.0;
           }
         }
@@ -475,7 +577,92 @@ void coop_build(Ctx& c) {
     phases.back().nt = (int)tasks.size() - phases.back().t0;
     if (phases.back().nt == 0) phases.pop_back();
   };
-  for (int l = 0; l < L; ++l) {
+  // extend-add of child slot k into the fronts of level l (column chunks sized for >= 2 tasks
+  // per CTA). It reads only the children's update blocks (columns >= s) and writes only the
+  // parents, so it shares the children's level's W (k = 0) and CB (k = 1) phases, which touch
+  // only the children's panel columns; child order is kept (deterministic sums).
+  int max_children = 0;
+  for (int nd = 0; nd < N; ++nd) max_children = std::max(max_children, fp.child_ptr[nd + 1] - fp.child_ptr[nd]);
+  auto emit_ea = [&](int l, int k) {
+    long long cols = 0;
+    for (int i = fp.level_ptr[l]; i < fp.level_ptr[l + 1]; ++i) {
+      const int nd = fp.level_list[i];
+      if (fp.child_ptr[nd + 1] - fp.child_ptr[nd] > k) cols += fp.bnd_size[fp.child_list[fp.child_ptr[nd] + k]];
+    }
+    int chunk = 64;
+    while (chunk > 2 && cols / chunk < 2LL * grid_f) chunk >>= 1;
+    for (int i = fp.level_ptr[l]; i < fp.level_ptr[l + 1]; ++i) {
+      const int nd = fp.level_list[i];
+      if (fp.child_ptr[nd + 1] - fp.child_ptr[nd] <= k) continue;
+      const int ch = fp.child_list[fp.child_ptr[nd] + k];
+      for (int q = 0; q < fp.bnd_size[ch]; q += chunk) tasks.push_back(CoopTask{CT_EA, nd, q, chunk, k});
+    }
+  };
+  for (int l = 0; l < L && c.coarse_sweep; ++l) {
+    // ---- block symmetric sweep program ----
+    std::vector<int> nodes(fp.level_list.begin() + fp.level_ptr[l], fp.level_list.begin() + fp.level_ptr[l + 1]);
+    long long off = 0;
+    int max_np = 0;
+    for (int nd : nodes) {
+      const int s = fp.sep_size[nd], f = s + fp.bnd_size[nd];
+      ldw[nd] = (int)round_up(std::max(f, 2), 2);  // B buffers: f x 64, two parities
+      inv[nd] = off; off += 2 * kTileInvStride;
+      X[nd] = off; off += 2LL * ldw[nd] * kTile;
+      max_np = std::max(max_np, ceil_div(s, kTile));
+    }
+    pool = std::max(pool, off);
+    phase_begin();
+    for (int nd : nodes)
+      if (fp.sep_size[nd] > 0) tasks.push_back(CoopTask{CT_SP, nd, 0, 0, 0});
+    phase_end();
+    auto emit_copy = [&](int P) {  // panel P's column <- B, pivot <- -D (nodes that have panel P)
+      for (int nd : nodes) {
+        const int s = fp.sep_size[nd], f = s + fp.bnd_size[nd];
+        if (s <= P * kTile) continue;
+        const int nb = std::min(kTile, s - P * kTile);
+        for (int I = 0; I < sweep_nblocks(P, nb, f); ++I) tasks.push_back(CoopTask{CT_SCP, nd, I, 0, P});
+        tasks.push_back(CoopTask{CT_SCP, nd, 0, 1, P});  // b = 1: the pivot tile
+      }
+    };
+    for (int P = 0; P < max_np; ++P) {
+      phase_begin();
+      for (int nd : nodes) {
+        const int s = fp.sep_size[nd], f = s + fp.bnd_size[nd];
+        if (s <= P * kTile) continue;
+        const int nb = std::min(kTile, s - P * kTile);
+        for (int I = 0; I < sweep_nblocks(P, nb, f); ++I) tasks.push_back(CoopTask{CT_SB, nd, I, 0, P});
+      }
+      if (P > 0) emit_copy(P - 1);
+      phase_end();
+      phase_begin();
+      for (int nd : nodes) {
+        const int s = fp.sep_size[nd], f = s + fp.bnd_size[nd];
+        if (s <= P * kTile) continue;
+        const int nb = std::min(kTile, s - P * kTile);
+        const int nbk = sweep_nblocks(P, nb, f);
+        for (int I = 0; I < nbk; ++I)
+          for (int J = 0; J <= I; ++J) tasks.push_back(CoopTask{CT_SC, nd, I, J, P});
+      }
+      phase_end();
+    }
+    phase_begin();
+    emit_copy(max_np - 1);
+    phase_end();
+    phase_begin();
+    for (int nd : nodes) {
+      const int s = fp.sep_size[nd];
+      for (int I = 0; I < ceil_div(s, kTile); ++I)
+        for (int J = 0; J <= I; ++J) tasks.push_back(CoopTask{CT_SM, nd, I, J, 0});
+    }
+    if (l + 1 < L) emit_ea(l + 1, 0);
+    phase_end();
+    for (int k = 1; l + 1 < L && k < max_children; ++k) {
+      phase_begin();
+      emit_ea(l + 1, k);
+      phase_end();
+    }
+  }
+  for (int l = 0; l < L && !c.coarse_sweep; ++l) {
     std::vector<int> nodes(fp.level_list.begin() + fp.level_ptr[l], fp.level_list.begin() + fp.level_ptr[l + 1]);
     // scratch for this level (reused by the next level after its CB phase)
     long long off = 0;
@@ -492,21 +679,6 @@ void coop_build(Ctx& c) {
       max_ch = std::max(max_ch, fp.child_ptr[nd + 1] - fp.child_ptr[nd]);
     }
     pool = std::max(pool, off);
-    // extend-add: one phase per child slot; column chunks sized for >= 2 tasks per CTA
-    for (int k = 0; k < max_ch; ++k) {
-      long long cols = 0;
-      for (int nd : nodes)
-        if (fp.child_ptr[nd + 1] - fp.child_ptr[nd] > k) cols += fp.bnd_size[fp.child_list[fp.child_ptr[nd] + k]];
-      int chunk = 64;
-      while (chunk > 2 && cols / chunk < 2LL * grid_f) chunk >>= 1;
-      phase_begin();
-      for (int nd : nodes) {
-        if (fp.child_ptr[nd + 1] - fp.child_ptr[nd] <= k) continue;
-        const int ch = fp.child_list[fp.child_ptr[nd] + k];
-        for (int q = 0; q < fp.bnd_size[ch]; q += chunk) tasks.push_back(CoopTask{CT_EA, nd, q, chunk, k});
-      }
-      phase_end();
-    }
     for (int p = 0; p < max_np; ++p) {
       if (p == 0) {  // later diagonal tiles are factored by the lookahead in SY(p-1)
         phase_begin();
@@ -544,6 +716,7 @@ void coop_build(Ctx& c) {
       for (int a = 0; a < ceil_div(b, kTile); ++a)
         for (int cc = 0; cc < ceil_div(s, kTile); ++cc) tasks.push_back(CoopTask{CT_W, nd, a, cc, 0});
     }
+    if (l + 1 < L) emit_ea(l + 1, 0);
     phase_end();
     phase_begin();
     for (int nd : nodes) {
@@ -551,7 +724,13 @@ void coop_build(Ctx& c) {
       const long long tot = (long long)f * s;
       for (long long q = 0; q < (tot + 4095) / 4096; ++q) tasks.push_back(CoopTask{CT_CB, nd, (int)q, 0, 0});
     }
+    if (l + 1 < L && max_children > 1) emit_ea(l + 1, 1);
     phase_end();
+    for (int k = 2; l + 1 < L && k < max_children; ++k) {
+      phase_begin();
+      emit_ea(l + 1, k);
+      phase_end();
+    }
   }
   for (const auto& ph : phases) {
     st.phase_type.push_back(tasks[ph.t0].type);
@@ -589,6 +768,7 @@ void coop_build(Ctx& c) {
   st.sp.br_off = c.upload(br_off.data(), L + 1);
   st.sp.nlevels = L;
   st.sp.nfr = fr_off[L];
+  st.sp.sweep = c.coarse_sweep ? 1 : 0;
 }
 
 void coop_release(const Ctx& c) { g_coop.erase(&c); }
@@ -609,15 +789,16 @@ void coop_factor(Ctx& c, cudaStream_t s) {
     std::vector<unsigned long long> t(st.phase_type.size());
     BDDC_CUDA(cudaStreamSynchronize(s));
     BDDC_CUDA(cudaMemcpy(t.data(), st.ptime, sizeof(unsigned long long) * t.size(), cudaMemcpyDeviceToHost));
-    double by_type[8] = {0};
-    int cnt[8] = {0};
+    double by_type[16] = {0};
+    int cnt[16] = {0};
     for (size_t i = 1; i < t.size(); ++i) {
       by_type[st.phase_type[i]] += (t[i] - t[i - 1]) * 1e-3;
       cnt[st.phase_type[i]]++;
     }
-    const char* nm[8] = {"EA", "PT", "TS|X1", "X1", "SY|X2", "X2", "W", "CB"};
+    const char* nm[16] = {"EA", "PT", "TS|X1", "X1", "SY|X2", "X2", "W", "CB", "SP", "SB|SCP", "SCP", "SC", "SM",
+                          "?", "?", "?"};
     fprintf(stderr, "coop factor phases (us, from phase 1): total %.1f\n", (t.back() - t[0]) * 1e-3);
-    for (int k = 0; k < 8; ++k)
+    for (int k = 0; k < 16; ++k)
       if (cnt[k]) fprintf(stderr, "  %-6s n=%4d  %9.1f us  avg %7.1f\n", nm[k], cnt[k], by_type[k], by_type[k] / cnt[k]);
     if (atoi(getenv("BDDC_COOP_TIMING")) >= 2)
       for (size_t i = 1; i < t.size(); ++i)

@@ -382,5 +382,120 @@ __device__ __forceinline__ int potrf_trtri_tile(double* L, int ld, int n, double
   return failed;
 }
 
+// ---- 64x64 SPD inverse by blocked Gauss-Jordan (128 threads) ----
+// D = M^{-1} for the n x n (n <= 64) SPD tile whose lower triangle is M (ld); D is 64 x 64
+// (ld 64), zero outside n x n. 8x8 pivot blocks are inverted in registers by warp 0; the row,
+// trailing and column block updates are DMMA.8x8x4 tiles over all warps. No square roots and
+// no separate inverse recursion: the critical path is 8 register 8x8 inverses.
+constexpr int kGjDP = 20;  // pitch of the 8x8 pivot inverse (4 mod 16)
+constexpr int kGjSmemDoubles = kTile * SP + 8 * kGjDP + 8;
+
+__device__ __forceinline__ int gj_tile_inverse(const double* M, int ld, int n, double* D, double* smem) {
+  double* W = smem;              // 64 x 64, pitch SP
+  double* Dm = smem + kTile * SP;
+  __shared__ int failed;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  if (tid == 0) failed = -1;
+  TILE_MARK(12);
+  // full symmetric tile from the lower triangle (identity padding), 16 loads in flight
+#pragma unroll 1
+  for (int u0 = 0; u0 < kTile * kTile; u0 += 16 * 128) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int idx = u0 + u * nt + tid, i = idx & 63, j = idx >> 6;
+      const int r = i >= j ? i : j, c = i >= j ? j : i;
+      v[u] = (r < n) ? M[r + (long long)c * ld] : (i == j ? 1.0 : 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int idx = u0 + u * nt + tid, i = idx & 63, j = idx >> 6;
+      W[i + j * SP] = v[u];
+    }
+  }
+  __syncthreads();
+  TILE_MARK(6);
+#pragma unroll 1
+  for (int kb = 0; kb < 8; ++kb) {
+    const int K = kb * 8;
+    if (kb == 1) TILE_MARK(7);
+    if (warp == 0) {  // (1) Dinv = inverse of the 8x8 pivot block (lanes 0..7 own columns)
+      double col[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) col[i] = lane < 8 ? W[(K + i) + (K + lane) * SP] : 0.0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        double piv = __shfl_sync(0xffffffffu, col[c], c);
+        if (!(piv > 0.0)) {
+          if (lane == 0 && failed < 0) failed = K + c;
+          piv = 1.0;
+        }
+        const double ip = 1.0 / piv;
+        const double rk = col[c] * ip;
+        double nc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const double ci = __shfl_sync(0xffffffffu, col[i], c);
+          if (i == c) nc[i] = lane == c ? ip : rk;
+          else if (lane == c) nc[i] = -ci * ip;
+          else nc[i] = fma(-ci, rk, col[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) col[i] = nc[i];
+      }
+      if (lane < 8) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) Dm[i + lane * kGjDP] = col[i];
+      }
+    }
+    __syncthreads();
+    if (kb == 1) TILE_MARK(8);
+    // (2) pivot row blocks: W[K][J] = Dinv W[K][J]   (J != K)
+    for (int jb = warp; jb < 8; jb += nw) {
+      if (jb == kb) continue;
+      const int J = jb * 8;
+      double c0 = 0.0, c1 = 0.0;
+      mma8(c0, c1, Dm, 1, kGjDP, W + K + J * SP, 1, SP, lane);
+      __syncwarp();
+      W[(K + g) + (J + 2 * t4) * SP] = c0;
+      W[(K + g) + (J + 2 * t4 + 1) * SP] = c1;
+    }
+    __syncthreads();
+    if (kb == 1) TILE_MARK(9);
+    // (3) trailing blocks: W[I][J] -= W[I][K] W[K][J]   (I, J != K)
+    for (int q = warp; q < 64; q += nw) {
+      const int ib = q >> 3, jb = q & 7;
+      if (ib == kb || jb == kb) continue;
+      const int I = ib * 8, J = jb * 8;
+      double d0 = 0.0, d1 = 0.0;
+      mma8(d0, d1, W + I + K * SP, 1, SP, W + K + J * SP, 1, SP, lane);
+      W[(I + g) + (J + 2 * t4) * SP] -= d0;
+      W[(I + g) + (J + 2 * t4 + 1) * SP] -= d1;
+    }
+    __syncthreads();
+    if (kb == 1) TILE_MARK(10);
+    // (4) pivot column blocks: W[I][K] = -W[I][K] Dinv ; W[K][K] = Dinv
+    for (int ib = warp; ib < 8; ib += nw) {
+      if (ib == kb) continue;
+      const int I = ib * 8;
+      double d0 = 0.0, d1 = 0.0;
+      mma8(d0, d1, W + I + K * SP, 1, SP, Dm, 1, kGjDP, lane);
+      __syncwarp();
+      W[(I + g) + (K + 2 * t4) * SP] = -d0;
+      W[(I + g) + (K + 2 * t4 + 1) * SP] = -d1;
+    }
+    if (tid < 64) W[(K + (tid & 7)) + (K + (tid >> 3)) * SP] = Dm[(tid & 7) + (tid >> 3) * kGjDP];
+    __syncthreads();
+  }
+  TILE_MARK(11);
+  for (int idx = tid; idx < kTile * kTile; idx += nt) {
+    const int i = idx & 63, j = idx >> 6;
+    D[idx] = (i < n && j < n) ? W[i + j * SP] : 0.0;
+  }
+  __syncthreads();
+  return failed;
+}
+
 }  // namespace tile
 }  // namespace bddc
