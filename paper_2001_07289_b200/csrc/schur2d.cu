@@ -83,7 +83,7 @@ __device__ __forceinline__ int gj_inverse_blocked(double* W, double* Dm, int lan
           if (bad < 0) bad = K + c;
           piv = 1.0;
         }
-        const double ip = 1.0 / piv;
+        const double ip = rcp_pos(piv);
         const double rk = col[c] * ip;  // row c of this lane's column, scaled
         double nc[8];
 #pragma unroll

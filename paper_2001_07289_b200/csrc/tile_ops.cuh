@@ -225,10 +225,7 @@ __device__ __forceinline__ void diag8(double* S, double* X, double* Dv, int k0, 
         if (lane == 0 && *failed < 0) *failed = k0 + c;
         d = 1.0;
       }
-      // 1/sqrt(d): float seed + 2 Newton steps in double (d > 0 here; no special cases)
-      double ri = (double)rsqrtf((float)d);
-      ri = ri * fma(-0.5 * d * ri, ri, 1.5);
-      ri = ri * fma(-0.5 * d * ri, ri, 1.5);
+      const double ri = rsqrt_pos(d);  // d > 0 here
       rinv[c] = ri;
       const double l = lane > c ? row[c] * ri : (lane == c ? d * ri : 0.0);
       row[c] = l;
@@ -431,7 +428,7 @@ __device__ __forceinline__ int gj_tile_inverse(const double* M, int ld, int n, d
           if (lane == 0 && failed < 0) failed = K + c;
           piv = 1.0;
         }
-        const double ip = 1.0 / piv;
+        const double ip = rcp_pos(piv);
         const double rk = col[c] * ip;
         double nc[8];
 #pragma unroll
