@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(32 * kWarpsW) wfactor2d_kernel(Geometry G, int
 }
 
 // ---- R_j / H_j / S_G with DMMA, W_j streamed back from the packed factor ----
-template <int M, int NGP>
+template <int M, int NGP, int NBO>
 __global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, int sub0,
                                                                 const double* __restrict__ alpha,
                                                                 LocalTables lt,
@@ -341,14 +341,17 @@ __global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, i
     __syncthreads();
     if (j > 0) {  // R_j -= B_j H_{j-1} on the previously active columns (warp = row)
       for (int r = warp; r < M; r += NW) {
-        double cf[3];
+        double cf[NBO];
+        int ro[NBO];
 #pragma unroll
-        for (int q = 0; q < 3; ++q) cf[q] = q < nbo ? sm[O_BC + r * 3 + q] : 0.0;
+        for (int q = 0; q < NBO; ++q) {
+          cf[q] = q < nbo ? sm[O_BC + r * 3 + q] : 0.0;
+          ro[q] = min(max(r + bdx[q], 0), M - 1) * EP;  // absent neighbours have cf = 0
+        }
         for (int cc = lane; cc < nprev; cc += 32) {
           double a = 0.0;
 #pragma unroll
-          for (int q = 0; q < 3; ++q)
-            if (q < nbo && cf[q] != 0.0) a += cf[q] * sm[O_H + (r + bdx[q]) * EP + cc];
+          for (int q = 0; q < NBO; ++q) a += cf[q] * sm[O_H + ro[q] + cc];
           sm[O_R + r * EP + cc] -= a;
         }
       }
@@ -396,7 +399,7 @@ __global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, i
   }
 }
 
-template <int M, int NGP>
+template <int M, int NGP, int NBO>
 void launch_schur2d(const Ctx& c, int sub0, int cnt, const double* Wd, const double* Wo,
                     const double* E, cudaStream_t s) {
   const bool diagb = c.geo.nbo == 1 && c.geo.bo_dx[0] == 0;
@@ -412,13 +415,13 @@ void launch_schur2d(const Ctx& c, int sub0, int cnt, const double* Wd, const dou
                                    (int)(sizeof(double) * kWarpsW * wf_warp_doubles<M, true>())));
     BDDC_CUDA(cudaFuncSetAttribute(wfactor2d_kernel<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)(sizeof(double) * kWarpsW * wf_warp_doubles<M, false>())));
-    BDDC_CUDA(cudaFuncSetAttribute(schur2d_kernel<M, NGP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
+    BDDC_CUDA(cudaFuncSetAttribute(schur2d_kernel<M, NGP, NBO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
     attr = true;
   }
   if (diagb) { wfactor2d_kernel<M, true><<<ceil_div(cnt, kWarpsW), 32 * kWarpsW, smem_w, s>>>(c.geo, sub0, cnt, c.alpha, c.lt, c.LI, c.info); BDDC_COUNT(); }
   else { wfactor2d_kernel<M, false><<<ceil_div(cnt, kWarpsW), 32 * kWarpsW, smem_w, s>>>(c.geo, sub0, cnt, c.alpha, c.lt, c.LI, c.info); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
-  { schur2d_kernel<M, NGP><<<cnt, kSchurThreads, smem_s, s>>>(c.geo, sub0, c.alpha, c.lt, c.LI, c.LS); BDDC_COUNT(); }
+  { schur2d_kernel<M, NGP, NBO><<<cnt, kSchurThreads, smem_s, s>>>(c.geo, sub0, c.alpha, c.lt, c.LI, c.LS); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
 }
 
@@ -435,10 +438,19 @@ bool schur2d(const Ctx& c, int sub0, int cnt, const double* Wd, const double* Wo
              cudaStream_t s) {
   const Geometry& G = c.geo;
   if (G.dim != 2 || G.nbo > 3) return false;
-  if (G.m_pad == 32 && G.nG_pad == 128) launch_schur2d<32, 128>(c, sub0, cnt, Wd, Wo, E, s);
-  else if (G.m_pad == 16 && G.nG_pad == 64) launch_schur2d<16, 64>(c, sub0, cnt, Wd, Wo, E, s);
-  else if (G.m_pad == 8 && G.nG_pad == 32) launch_schur2d<8, 32>(c, sub0, cnt, Wd, Wo, E, s);
-  else return false;
+  const bool one = G.nbo == 1;
+  if (G.m_pad == 32 && G.nG_pad == 128) {
+    if (one) launch_schur2d<32, 128, 1>(c, sub0, cnt, Wd, Wo, E, s);
+    else launch_schur2d<32, 128, 3>(c, sub0, cnt, Wd, Wo, E, s);
+  } else if (G.m_pad == 16 && G.nG_pad == 64) {
+    if (one) launch_schur2d<16, 64, 1>(c, sub0, cnt, Wd, Wo, E, s);
+    else launch_schur2d<16, 64, 3>(c, sub0, cnt, Wd, Wo, E, s);
+  } else if (G.m_pad == 8 && G.nG_pad == 32) {
+    if (one) launch_schur2d<8, 32, 1>(c, sub0, cnt, Wd, Wo, E, s);
+    else launch_schur2d<8, 32, 3>(c, sub0, cnt, Wd, Wo, E, s);
+  } else {
+    return false;
+  }
   return true;
 }
 
