@@ -142,6 +142,7 @@ struct FrontPlan {
 // carries its front's metadata (no dependent loads before its first front read).
 struct CsTask {
   long long front_off;  // front base in the pool
+  long long w_off;      // dataflow factorization: W21 (boundary rows) offset in the scratch pool
   long long gat_base;   // node's offset into gat_ptr (child-update gathers per position)
   long long upd_off;    // node's update-vector offset
   int node, r0, c0;
@@ -150,6 +151,7 @@ struct CsTask {
   int red;              // global reduction index (arrival counter), -1 = none
   int np;               // tasks contributing to this task's reduction (1: write directly)
   int mode;             // forward: 0 = 64 rows x 256 columns, 1 = 256 rows x all s <= 64 columns
+  int ldw;              // leading dimension of W21 (dataflow)
 };
 struct CsRed {  // reduction over the partials of one row / column chunk
   int t0, p0, np;
@@ -297,6 +299,11 @@ struct Ctx {
 // local_setup.cu
 void local_setup(Ctx& c, double* workspace, size_t ws_doubles);
 size_t local_setup_workspace(const Geometry& g, int chunk);
+// coarse_coop.cu: dataflow coarse factorization (default for the Cholesky formulation) and
+// its per-front scratch layout (inverse slots, Y partials, W21 = L21 X kept for the solve)
+bool coarse_df_enabled(const Ctx& c);
+long long coarse_df_layout(const FrontPlan& fp, std::vector<long long>& inv, std::vector<long long>& Y,
+                           std::vector<long long>& W, std::vector<int>& ldw);
 // coarse.cu
 void build_level_schedule(Ctx& c);
 void coarse_assemble_and_factor(Ctx& c);

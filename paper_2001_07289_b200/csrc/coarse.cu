@@ -80,6 +80,11 @@ void build_level_schedule(Ctx& c) {
   std::vector<CsRed> fr, br;
   std::vector<size_t> ft_off(L + 1), bt_off(L + 1), fr_off(L + 1), br_off(L + 1);
   int max_parts = 0;
+  // dataflow factorization: W21 (rows >= s of every front) stays in the scratch pool
+  std::vector<long long> l_inv, l_y, l_w;
+  std::vector<int> l_ldw;
+  const bool df = coarse_df_enabled(c);
+  if (df) coarse_df_layout(fp, l_inv, l_y, l_w, l_ldw);
   auto base = [&](int nd) {
     CsTask t{};
     t.front_off = fp.front_off[nd];
@@ -92,6 +97,8 @@ void build_level_schedule(Ctx& c) {
     t.s0 = fp.sep_start[nd];
     t.red = -1;
     t.np = 1;
+    t.w_off = df ? l_w[nd] : 0;
+    t.ldw = df ? l_ldw[nd] : 0;
     return t;
   };
   for (int l = 0; l < L; ++l) {

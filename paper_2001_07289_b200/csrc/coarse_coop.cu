@@ -15,6 +15,7 @@
 // The solve program: per level forward GEMV tiles, reduction; then backward likewise.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -71,6 +72,17 @@ struct CoopProgram {
   int nphases;
   CoopScratch sc;
   double* pool;
+  int df;  // dataflow mode: one inverse slot per panel, Y partials by panel parity
+};
+
+// Dataflow program: tasks in a topological order, each with up to kDeps dependencies
+// (counter >= target) and up to 3 counters it increments when done.
+constexpr int kDeps = 6;
+constexpr int kSigs = 6;
+struct DfTask {
+  CoopTask t;
+  int dep[kDeps], tgt[kDeps];
+  int sig[kSigs];
 };
 
 namespace {
@@ -82,8 +94,8 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
   const int node = t.node;
   const int s = fd.sep_size[node], f = s + fd.bnd_size[node], ld = fd.ld[node];
   double* F = fd.fronts + fd.front_off[node];
-  double* X = pg.pool + pg.sc.X[node];
-  const int ldx = pg.sc.ldx[node];
+  double* X = pg.df ? F : pg.pool + pg.sc.X[node];  // dataflow: L11^{-1} in place in the front
+  const int ldx = pg.df ? ld : pg.sc.ldx[node];
   switch (t.type) {
     case CT_EA: {  // child #arg of node, columns [a, a + b) of its lower update block
       const int c0 = fd.child_ptr[node];
@@ -104,8 +116,8 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
             const bool ok = j0 + c < je && i >= j0 + c;
-            u[c] = ok ? U[i + (long long)(j0 + c) * lc] : 0.0;
-            fv[c] = ok ? F[r + cof[c]] : 0.0;
+            u[c] = ok ? __ldcg(U + i + (long long)(j0 + c) * lc) : 0.0;
+            fv[c] = ok ? __ldcg(F + r + cof[c]) : 0.0;
           }
 #pragma unroll
           for (int c = 0; c < 16; ++c)
@@ -116,7 +128,7 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
     }
     case CT_PT: {  // factor + invert diagonal tile of panel arg
       const int k = t.arg * kTile, nb = min(kTile, s - k);
-      double* inv = pg.pool + pg.sc.inv[node] + (t.arg & 1) * kTileInvStride;
+      double* inv = pg.pool + pg.sc.inv[node] + (pg.df ? t.arg : (t.arg & 1)) * kTileInvStride;
       const int bad = potrf_trtri_tile(F + k + (long long)k * ld, ld, nb, inv, smem);
       if (threadIdx.x == 0 && bad >= 0) atomicMin(info + node, fd.sep_start[node] + k + bad);
       break;
@@ -124,7 +136,7 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
     case CT_TS: {  // rows (k+nb) + 64a.. of the panel: L21 <- A21 inv^T (in place)
       const int k = t.arg * kTile, nb = min(kTile, s - k), rest = f - k - nb;
       double* A21 = F + (k + nb) + (long long)k * ld;
-      const double* inv = pg.pool + pg.sc.inv[node] + (t.arg & 1) * kTileInvStride;
+      const double* inv = pg.pool + pg.sc.inv[node] + (pg.df ? t.arg : (t.arg & 1)) * kTileInvStride;
       gemm_tile<false, true, kCoopStages>(A21, ld, inv, kTile, A21, ld, rest, nb, nb, t.a * kTile, 0, 1.0, 0.0,
                              false, smem);
       break;
@@ -132,7 +144,9 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
     case CT_X1: {  // Y_q[:, c] = L[k.., c*64 + kq ..) X[.., c]  over K chunk q (c = a, q = b)
       const int k = t.arg * kTile, nb = min(kTile, s - k), c = t.a * kTile;
       const int kq0 = c + t.b * kX1Chunk, kq1 = min(k, kq0 + kX1Chunk);
-      double* Y = pg.pool + pg.sc.Y[node] + (long long)t.b * kTile * s;
+      // dataflow: panel-parity Y partial sets (X1 of panel p + 2 waits for X2 of panel p)
+      const long long ysz = (long long)kTile * s * ((s + kX1Chunk - 1) / kX1Chunk);
+      double* Y = pg.pool + pg.sc.Y[node] + (pg.df ? (t.arg & 1) * ysz : 0) + (long long)t.b * kTile * s;
       gemm_tile<false, false, kCoopStages>(F + k + (long long)kq0 * ld, ld, X + kq0 + (long long)c * ldx, ldx,
                               Y + (long long)c * kTile, kTile, nb, min(kTile, k - c), kq1 - kq0, 0, 0,
                               1.0, 0.0, false, smem);
@@ -147,7 +161,7 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
       if (t.a == 0 && t.b == 0 && k + nb < s) {  // factor the next panel's diagonal tile now
         __syncthreads();
         const int k1 = k + nb, nb1 = min(kTile, s - k1);
-        double* inv1 = pg.pool + pg.sc.inv[node] + ((t.arg + 1) & 1) * kTileInvStride;
+        double* inv1 = pg.pool + pg.sc.inv[node] + (pg.df ? t.arg + 1 : ((t.arg + 1) & 1)) * kTileInvStride;
         const int bad = potrf_trtri_tile(F + k1 + (long long)k1 * ld, ld, nb1, inv1, smem);
         if (threadIdx.x == 0 && bad >= 0) atomicMin(info + node, fd.sep_start[node] + k1 + bad);
       }
@@ -155,10 +169,11 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
     }
     case CT_X2: {  // X[k.., c] = -inv Y[:, c] (c < panel) or X[k.., k..] = inv
       const int k = t.arg * kTile, nb = min(kTile, s - k), c = t.a * kTile;
-      const double* inv = pg.pool + pg.sc.inv[node] + (t.arg & 1) * kTileInvStride;
+      const double* inv = pg.pool + pg.sc.inv[node] + (pg.df ? t.arg : (t.arg & 1)) * kTileInvStride;
       if (c < k) {  // X[k, c] = -inv sum_q Y_q[:, c]: sum the partials into Y_0, one GEMM
         const int nq = (k - c + kX1Chunk - 1) / kX1Chunk;
-        double* Y0 = pg.pool + pg.sc.Y[node] + (long long)c * kTile;
+        const long long ysz = (long long)kTile * s * ((s + kX1Chunk - 1) / kX1Chunk);
+        double* Y0 = pg.pool + pg.sc.Y[node] + (pg.df ? (t.arg & 1) * ysz : 0) + (long long)c * kTile;
         if (nq > 1) {
           const long long qs = (long long)kTile * s;  // stride between partials
           constexpr int PER = kTile * kTile / 128;     // elements per thread (128 threads)
@@ -180,7 +195,7 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
       } else {
         for (int idx = threadIdx.x; idx < nb * nb; idx += blockDim.x) {
           const int i = idx % nb, j = idx / nb;
-          X[(k + i) + (long long)(k + j) * ldx] = inv[i + j * kTile];
+          X[(k + i) + (long long)(k + j) * ldx] = __ldcg(inv + i + j * kTile);
         }
       }
       break;
@@ -202,8 +217,8 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
       for (long long idx = e0 + threadIdx.x; idx < e1; idx += blockDim.x) {
         const int i = (int)(idx % f), j = (int)(idx / f);
         double v;
-        if (i < s) v = i >= j ? X[i + (long long)j * ldx] : 0.0;
-        else v = W[(i - s) + (long long)j * ldw];
+        if (i < s) v = i >= j ? __ldcg(X + i + (long long)j * ldx) : 0.0;
+        else v = __ldcg(W + (i - s) + (long long)j * ldw);
         F[i + (long long)j * ld] = v;
       }
       break;
@@ -319,6 +334,60 @@ __global__ void __launch_bounds__(128) coop_factor_kernel(FrontDev fd, CoopProgr
   }
 }
 
+// Dataflow variant: CTAs pull tasks in the program's topological order from a global
+// counter; a task's first thread waits (bounded) until each dependency counter reaches its
+// target, the task runs, and its counters are incremented after a fence. A task only waits
+// on earlier tasks and all CTAs are co-resident (cooperative launch), so the queue always
+// progresses; a wait that exceeds the bound sets *err (the host raises) instead of hanging.
+__global__ void __launch_bounds__(128) coop_factor_df_kernel(FrontDev fd, CoopProgram pg,
+                                                             const DfTask* __restrict__ tasks, int ntasks,
+                                                             int* ctr, int* qhead, int* info, int* err,
+                                                             unsigned long long* prof) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int ti_s;
+  for (;;) {
+    if (threadIdx.x == 0) ti_s = atomicAdd(qhead, 1);
+    __syncthreads();
+    const int ti = ti_s;
+    if (ti >= ntasks) break;
+    const DfTask t = tasks[ti];
+    long long c0 = 0, c1 = 0;
+    if (prof && threadIdx.x == 0) c0 = clock64();
+    if (threadIdx.x == 0) {
+#pragma unroll 1
+      for (int d = 0; d < kDeps; ++d) {
+        const int cix = t.dep[d];
+        if (cix < 0) continue;
+        long long spins = 0;
+        while (*(volatile int*)(ctr + cix) < t.tgt[d]) {
+          __nanosleep(64);
+          if (++spins > (1LL << 25) || *(volatile int*)err) {  // bounded; after one timeout, none
+            atomicExch(err, 1);
+            break;
+          }
+        }
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    if (prof && threadIdx.x == 0) c1 = clock64();
+    run_task(t.t, fd, pg, info, smem);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+#pragma unroll
+      for (int q = 0; q < kSigs; ++q)
+        if (t.sig[q] >= 0) atomicAdd(ctr + t.sig[q], 1);
+      if (prof) {  // per task type: waiting cycles, running cycles, count
+        const long long c2 = clock64();
+        atomicAdd(prof + 3 * t.t.type + 0, (unsigned long long)(c1 - c0));
+        atomicAdd(prof + 3 * t.t.type + 1, (unsigned long long)(c2 - c1));
+        atomicAdd(prof + 3 * t.t.type + 2, 1ULL);
+      }
+    }
+  }
+}
+
 // ---- cooperative coarse solve ----
 struct SolveProgram {
   const CsTask* ft;
@@ -332,6 +401,7 @@ struct SolveProgram {
   int nlevels;
   int nfr;  // number of forward reductions (offset of the backward counters)
   int sweep;  // fronts hold [A11^{-1} (full); W21] (else [L11^{-1} (lower); W21])
+  const double* wpool;  // dataflow: W21 rows (r >= s) read from here (CsTask w_off / ldw)
 };
 
 __device__ __forceinline__ double gather_at(const LevelView& lv, const double* __restrict__ upd, long long gbase,
@@ -377,10 +447,12 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
       if (t.mode == 1) {  // s <= 64: one thread per row, all separator columns
         const int r = t.r0 + tid;
         const int ke = r < f ? (r < s ? (sp.sweep ? 0 : r + 1) : s) : 0;
-        const double* Fr = F + r;
+        const bool wr = sp.wpool && r >= s;  // dataflow: W21 rows from the scratch pool
+        const double* Fr = wr ? sp.wpool + t.w_off + (r - s) : F + r;
+        const long long lr = wr ? (long long)t.ldw : ld;
         double fv[16];  // first batch in flight while the right-hand side is gathered
 #pragma unroll
-        for (int u = 0; u < 16; ++u) fv[u] = u < ke ? __ldcs(Fr + (long long)u * ld) : 0.0;
+        for (int u = 0; u < 16; ++u) fv[u] = u < ke ? __ldcs(Fr + (long long)u * lr) : 0.0;
         if (tid < s) vs[tid] = rhs[t.s0 + tid] + gather_at(lv, fd.upd, t.gat_base, tid);
         __syncthreads();
         if (r < f) {
@@ -388,7 +460,7 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
           for (int k0 = 0; k0 < ke; k0 += 16) {
             if (k0 > 0) {
 #pragma unroll
-              for (int u = 0; u < 16; ++u) fv[u] = k0 + u < ke ? __ldcs(Fr + (long long)(k0 + u) * ld) : 0.0;
+              for (int u = 0; u < 16; ++u) fv[u] = k0 + u < ke ? __ldcs(Fr + (long long)(k0 + u) * lr) : 0.0;
             }
 #pragma unroll
             for (int u = 0; u < 16; ++u) acc[u & 3] += k0 + u < ke ? fv[u] * vs[k0 + u] : 0.0;
@@ -404,10 +476,12 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
       const int kb = t.c0 + grp * 64;
       int ke = r < f ? min(kb + 64, s) : kb;
       if (r < s) ke = sp.sweep ? kb : min(ke, r + 1);
-      const double* Fr = F + r;
+      const bool wr = sp.wpool && r >= s;
+      const double* Fr = wr ? sp.wpool + t.w_off + (r - s) : F + r;
+      const long long lr = wr ? (long long)t.ldw : ld;
       double fv[16];  // first batch in flight while the right-hand side is gathered
 #pragma unroll
-      for (int u = 0; u < 16; ++u) fv[u] = kb + u < ke ? __ldcs(Fr + (long long)(kb + u) * ld) : 0.0;
+      for (int u = 0; u < 16; ++u) fv[u] = kb + u < ke ? __ldcs(Fr + (long long)(kb + u) * lr) : 0.0;
       {
         const int kk = t.c0 + tid;
         vs[tid] = kk < s ? rhs[t.s0 + kk] + gather_at(lv, fd.upd, t.gat_base, kk) : 0.0;
@@ -417,7 +491,7 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
       for (int k0 = kb; k0 < ke; k0 += 16) {
         if (k0 > kb) {
 #pragma unroll
-          for (int u = 0; u < 16; ++u) fv[u] = k0 + u < ke ? __ldcs(Fr + (long long)(k0 + u) * ld) : 0.0;
+          for (int u = 0; u < 16; ++u) fv[u] = k0 + u < ke ? __ldcs(Fr + (long long)(k0 + u) * lr) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 16; ++u) acc[u & 3] += k0 + u < ke ? fv[u] * vs[k0 + u - t.c0] : 0.0;
@@ -471,11 +545,14 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int i = lane + 32 * (m + h), r = t.r0 + i;
+          const bool wr = sp.wpool && r >= s;
+          const double* Fr = wr ? sp.wpool + t.w_off + (r - s) : F + r;
+          const long long lr = wr ? (long long)t.ldw : ld;
 #pragma unroll
           for (int cc = 0; cc < 8; ++cc) {
             const int k = kw + cc;
             const bool ok = k < s && r < f && (sp.sweep || r >= s || r >= k);
-            fv[h][cc] = ok ? __ldcs(F + r + (long long)k * ld) : 0.0;
+            fv[h][cc] = ok ? __ldcs(Fr + (long long)k * lr) : 0.0;
           }
         }
       };
@@ -546,9 +623,37 @@ struct CoopState {
   unsigned long long* stime = nullptr;  // per grid.sync timestamps of the solve (diagnostics)
   int grid_f = 0, grid_s = 0;
   size_t smem_f = 0;
+  // dataflow factorization
+  bool df = false;
+  DfTask* dtasks = nullptr;
+  int ndtasks = 0;
+  int* ctr = nullptr;  // [nctr] dependency counters + queue head + error flag
+  int nctr = 0;
 };
 
 static std::map<const Ctx*, CoopState> g_coop;
+
+bool coarse_df_enabled(const Ctx& c) {
+  const char* e = getenv("BDDC_COARSE_DF");
+  return !c.coarse_sweep && !(e && atoi(e) == 0);
+}
+
+long long coarse_df_layout(const FrontPlan& fp, std::vector<long long>& inv, std::vector<long long>& Y,
+                           std::vector<long long>& W, std::vector<int>& ldw) {
+  const int N = fp.nnodes;
+  inv.assign(N, 0); Y.assign(N, 0); W.assign(N, 0); ldw.assign(N, 2);
+  long long off = 0;  // every front its own scratch (levels overlap in the dataflow program)
+  for (int l = 0; l < fp.nlevels; ++l)
+    for (int i = fp.level_ptr[l]; i < fp.level_ptr[l + 1]; ++i) {
+      const int nd = fp.level_list[i];
+      const int s = fp.sep_size[nd], b = fp.bnd_size[nd], np = ceil_div(s, kTile);
+      ldw[nd] = (int)round_up(std::max(b, 2), 2);
+      inv[nd] = off; off += (long long)std::max(np, 1) * kTileInvStride;
+      Y[nd] = off; off += 2 * round_up((long long)kTile * std::max(s, 1), 2) * ceil_div(std::max(s, 1), kX1Chunk);
+      W[nd] = off; off += round_up((long long)ldw[nd] * std::max(s, 1), 2);
+    }
+  return std::max(off, 2LL);
+}
 
 void coop_build(Ctx& c) {
   FrontPlan& fp = c.fp;
@@ -557,9 +662,15 @@ void coop_build(Ctx& c) {
   st = CoopState{};
   st.smem_f = sizeof(double) * std::max<int>(gemm_smem_doubles<kCoopStages>(), kFactSmemDoubles);
   BDDC_CUDA(cudaFuncSetAttribute(coop_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st.smem_f));
+  BDDC_CUDA(cudaFuncSetAttribute(coop_factor_df_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st.smem_f));
   int nsm = 0, per_f = 0, per_s = 0;
   BDDC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device));
   BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_f, coop_factor_kernel, 128, st.smem_f));
+  {
+    int per_df = 0;  // the dataflow kernel must be co-resident with the same grid
+    BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_df, coop_factor_df_kernel, 128, st.smem_f));
+    per_f = std::min(per_f, per_df);
+  }
   BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_s, coop_solve_kernel, 256, 0));
   // few CTAs: the phases are small at the top of the tree and grid.sync cost grows with
   // the number of arriving CTAs
@@ -598,6 +709,194 @@ void coop_build(Ctx& c) {
       for (int q = 0; q < fp.bnd_size[ch]; q += chunk) tasks.push_back(CoopTask{CT_EA, nd, q, chunk, k});
     }
   };
+  // ---- dataflow program (default for the Cholesky formulation) ----
+  st.df = coarse_df_enabled(c);
+  if (st.df) {
+    std::vector<DfTask> dt;
+    int nctr = 0;
+    auto newc = [&](int n) { const int b = nctr; nctr += n; return b; };
+    // per node counter bases and totals
+    std::vector<int> c_ea(N), c_syall(N), c_pt(N), c_tsr(N), c_upd(N), c_x1(N), c_x2(N), c_x2row(N),
+        c_x2col(N), c_x2all(N), c_tsall(N), c_w(N), c_syrd(N), nT(N), nP(N), tot_sy(N, 0), tot_ts(N, 0),
+        tot_w(N, 0), tot_x2(N, 0);
+    std::vector<std::vector<int>> nea(N);
+    for (int nd = 0; nd < N; ++nd) {
+      const int s = fp.sep_size[nd], f = s + fp.bnd_size[nd];
+      const int T = ceil_div(std::max(f, 1), kTile), np = ceil_div(s, kTile);
+      nT[nd] = T; nP[nd] = np;
+      c_ea[nd] = newc(std::max(1, fp.child_ptr[nd + 1] - fp.child_ptr[nd]));
+      c_syall[nd] = newc(1); c_tsall[nd] = newc(1); c_w[nd] = newc(1); c_x2all[nd] = newc(1);
+      c_pt[nd] = newc(std::max(np, 1));
+      c_tsr[nd] = newc(std::max(np * T, 1));
+      c_upd[nd] = newc(T * (T + 1) / 2);
+      c_x1[nd] = newc(std::max(np, 1));         // X1 tasks done per panel row
+      c_syrd[nd] = newc(std::max(np * T, 1));   // SY readers done per (panel, relative row tile)
+      c_x2[nd] = newc(std::max(np * np, 1));
+      c_x2row[nd] = newc(std::max(np, 1));
+      c_x2col[nd] = newc(std::max(np, 1));
+      nea[nd].assign(std::max(1, fp.child_ptr[nd + 1] - fp.child_ptr[nd]), 0);
+    }
+    auto upd = [&](int nd, int I, int J) { return c_upd[nd] + I * (I + 1) / 2 + J; };
+    auto mk = [&](int type, int nd, int a, int b, int arg) {
+      DfTask t;
+      t.t = CoopTask{type, nd, a, b, arg};
+      for (int d = 0; d < kDeps; ++d) { t.dep[d] = -1; t.tgt[d] = 0; }
+      for (int q = 0; q < kSigs; ++q) t.sig[q] = -1;
+      return t;
+    };
+    auto dep = [&](DfTask& t, int cix, int tgt) {
+      if (tgt <= 0) return;
+      for (int d = 0; d < kDeps; ++d)
+        if (t.dep[d] < 0) { t.dep[d] = cix; t.tgt[d] = tgt; return; }
+      throw std::runtime_error("coarse dataflow: too many dependencies");
+    };
+    auto sig = [&](DfTask& t, int cix) {
+      for (int q = 0; q < kSigs; ++q)
+        if (t.sig[q] < 0) { t.sig[q] = cix; return; }
+      throw std::runtime_error("coarse dataflow: too many signals");
+    };
+    const long long off = coarse_df_layout(fp, inv, Y, W, ldw);  // X lives in the fronts
+    for (int l = 0; l < L; ++l) {
+      std::vector<int> nodes(fp.level_list.begin() + fp.level_ptr[l], fp.level_list.begin() + fp.level_ptr[l + 1]);
+      // extend-add of the children (child order per parent)
+      for (int k = 0; k < max_children; ++k) {
+        long long cols = 0;
+        for (int nd : nodes)
+          if (fp.child_ptr[nd + 1] - fp.child_ptr[nd] > k) cols += fp.bnd_size[fp.child_list[fp.child_ptr[nd] + k]];
+        int chunk = 64;
+        while (chunk > 2 && cols / chunk < 2LL * grid_f) chunk >>= 1;
+        for (int nd : nodes) {
+          if (fp.child_ptr[nd + 1] - fp.child_ptr[nd] <= k) continue;
+          const int ch = fp.child_list[fp.child_ptr[nd] + k];
+          for (int q = 0; q < fp.bnd_size[ch]; q += chunk) {
+            DfTask t = mk(CT_EA, nd, q, chunk, k);
+            dep(t, c_syall[ch], tot_sy[ch]);
+            if (k > 0) dep(t, c_ea[nd] + k - 1, nea[nd][k - 1]);
+            sig(t, c_ea[nd] + k);
+            dt.push_back(t);
+            nea[nd][k]++;
+          }
+        }
+      }
+      for (int nd : nodes) {
+        const int s = fp.sep_size[nd], f = s + fp.bnd_size[nd], np = nP[nd], T = nT[nd];
+        const int nch = fp.child_ptr[nd + 1] - fp.child_ptr[nd];
+        if (s <= 0) continue;
+        {
+          DfTask t = mk(CT_PT, nd, 0, 0, 0);
+          if (nch > 0) dep(t, c_ea[nd] + nch - 1, nea[nd][nch - 1]);
+          sig(t, c_pt[nd] + 0);
+          dt.push_back(t);
+        }
+        auto tiles_of = [&](int r0, int r1) {  // absolute 64-tiles overlapping rows [r0, r1)
+          return std::make_pair(r0 / kTile, (std::min(r1, f) - 1) / kTile);
+        };
+        for (int p = 0; p < np; ++p) {
+          const int k = p * kTile, nb = std::min(kTile, s - k), rest = f - k - nb, nt = ceil_div(rest, kTile);
+          for (int a = 0; a < nt; ++a) {
+            DfTask t = mk(CT_TS, nd, a, 0, p);
+            dep(t, c_pt[nd] + p, 1);
+            if (p > 0) {
+              const auto ti = tiles_of(k + nb + a * kTile, k + nb + a * kTile + kTile);
+              for (int I = ti.first; I <= ti.second; ++I) dep(t, upd(nd, I, p), p);
+            }
+            sig(t, c_tsr[nd] + p * T + a);
+            sig(t, c_tsall[nd]);
+            dt.push_back(t);
+            tot_ts[nd]++;
+          }
+          for (int cc = 0; cc < p; ++cc)
+            for (int qq = 0; qq < p - cc; ++qq) {  // kX1Chunk = 64: chunk qq is column block m
+              const int m = cc + qq;
+              DfTask t = mk(CT_X1, nd, cc, qq, p);
+              dep(t, c_tsr[nd] + m * T + (p - m - 1), 1);
+              dep(t, c_x2[nd] + m * np + cc, 1);
+              if (p >= 2) dep(t, c_x2row[nd] + p - 2, p - 1);
+              sig(t, c_x1[nd] + p);
+              dt.push_back(t);
+            }
+          for (int a = 0; a < nt; ++a)
+            for (int bb = 0; bb <= a; ++bb) {
+              DfTask t = mk(CT_SY, nd, a, bb, p);
+              dep(t, c_tsr[nd] + p * T + a, 1);
+              if (bb != a) dep(t, c_tsr[nd] + p * T + bb, 1);
+              if (p > 0) {
+                const auto ri = tiles_of(k + nb + a * kTile, k + nb + a * kTile + kTile);
+                const auto ci = tiles_of(k + nb + bb * kTile, k + nb + bb * kTile + kTile);
+                for (int I = ri.first; I <= ri.second; ++I)
+                  for (int J = ci.first; J <= ci.second; ++J)
+                    if (I >= J) dep(t, upd(nd, I, J), p);
+              }
+              if (nb == kTile) sig(t, upd(nd, p + 1 + a, p + 1 + bb));
+              sig(t, c_syall[nd]);
+              // readers of the separator rows of L[:, p] (X2 overwrites them with X in place)
+              if (p + 1 + a < np) sig(t, c_syrd[nd] + p * T + a);
+              if (bb != a && p + 1 + bb < np) sig(t, c_syrd[nd] + p * T + bb);
+              if (a == 0 && bb == 0 && k + nb < s) sig(t, c_pt[nd] + p + 1);
+              dt.push_back(t);
+              tot_sy[nd]++;
+            }
+          for (int cc = 0; cc <= p; ++cc) {
+            DfTask t = mk(CT_X2, nd, cc, 0, p);
+            dep(t, c_pt[nd] + p, 1);
+            if (cc < p) {
+              // X[p, cc] replaces L[p, cc] in place: every X1 of row p and every SY tile of
+              // panel cc that reads L's row tile p must be done
+              dep(t, c_x1[nd] + p, p * (p + 1) / 2);
+              const int ntc = ceil_div(f - (cc + 1) * kTile, kTile);
+              dep(t, c_syrd[nd] + cc * T + (p - cc - 1), ntc);
+            }
+            sig(t, c_x2[nd] + p * np + cc);
+            sig(t, c_x2row[nd] + p);
+            sig(t, c_x2col[nd] + cc);
+            sig(t, c_x2all[nd]);
+            dt.push_back(t);
+            tot_x2[nd]++;
+          }
+        }
+        const int b = f - s;
+        if (b > 0) {
+          for (int a = 0; a < ceil_div(b, kTile); ++a)
+            for (int cc = 0; cc < np; ++cc) {
+              DfTask t = mk(CT_W, nd, a, cc, 0);
+              dep(t, c_tsall[nd], tot_ts[nd]);
+              dep(t, c_x2col[nd] + cc, np - cc);
+              sig(t, c_w[nd]);
+              dt.push_back(t);
+              tot_w[nd]++;
+            }
+        }
+        // no CB: X is written in place by X2 and W21 stays in the scratch pool for the solve
+      }
+    }
+    pool = std::max(pool, off);
+    // list-scheduling order: descending upward rank (estimated cost of the task plus the
+    // longest chain of work that depends on it). A producer always outranks its consumers,
+    // so the order stays topological; critical-path chains (pivot tiles) are dequeued first.
+    {
+      const double cost[8] = {4.0, 18.0, 6.0, 6.0, 7.0, 8.0, 8.0, 12.0};  // us: EA PT TS X1 SY X2 W CB
+      std::vector<double> maxc(nctr, 0.0), rank(dt.size(), 0.0);
+      for (long long i = (long long)dt.size() - 1; i >= 0; --i) {
+        const DfTask& t = dt[i];
+        double succ = 0.0;
+        for (int q = 0; q < kSigs; ++q)
+          if (t.sig[q] >= 0) succ = std::max(succ, maxc[t.sig[q]]);
+        rank[i] = cost[t.t.type] + succ;
+        for (int d = 0; d < kDeps; ++d)
+          if (t.dep[d] >= 0) maxc[t.dep[d]] = std::max(maxc[t.dep[d]], rank[i]);
+      }
+      std::vector<int> order(dt.size());
+      for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+      std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return rank[a] > rank[b]; });
+      std::vector<DfTask> sorted(dt.size());
+      for (size_t i = 0; i < order.size(); ++i) sorted[i] = dt[order[i]];
+      dt.swap(sorted);
+    }
+    st.ndtasks = (int)dt.size();
+    st.dtasks = c.upload(dt.data(), dt.size());
+    st.nctr = nctr;
+    st.ctr = c.alloc<int>(nctr + 2);  // + queue head + error flag
+  }
   for (int l = 0; l < L && c.coarse_sweep; ++l) {
     // ---- block symmetric sweep program ----
     std::vector<int> nodes(fp.level_list.begin() + fp.level_ptr[l], fp.level_list.begin() + fp.level_ptr[l + 1]);
@@ -662,7 +961,7 @@ void coop_build(Ctx& c) {
       phase_end();
     }
   }
-  for (int l = 0; l < L && !c.coarse_sweep; ++l) {
+  for (int l = 0; l < L && !c.coarse_sweep && !st.df; ++l) {
     std::vector<int> nodes(fp.level_list.begin() + fp.level_ptr[l], fp.level_list.begin() + fp.level_ptr[l + 1]);
     // scratch for this level (reused by the next level after its CB phase)
     long long off = 0;
@@ -737,9 +1036,10 @@ void coop_build(Ctx& c) {
     st.phase_nt.push_back(ph.nt);
   }
   if (getenv("BDDC_COOP_TIMING")) {
-    st.ptime = c.alloc<unsigned long long>(phases.size() + 1);
+    st.ptime = c.alloc<unsigned long long>(std::max<size_t>(phases.size() + 1, 48));
     st.stime = c.alloc<unsigned long long>(2 * L + 1);
   }
+  st.pg.df = st.df ? 1 : 0;
   st.pg.tasks = c.upload(tasks.data(), tasks.size());
   st.pg.phases = c.upload(phases.data(), phases.size());
   st.pg.nphases = (int)phases.size();
@@ -769,6 +1069,7 @@ void coop_build(Ctx& c) {
   st.sp.nlevels = L;
   st.sp.nfr = fr_off[L];
   st.sp.sweep = c.coarse_sweep ? 1 : 0;
+  st.sp.wpool = st.df ? st.pg.pool : nullptr;
 }
 
 void coop_release(const Ctx& c) { g_coop.erase(&c); }
@@ -777,6 +1078,49 @@ void coop_factor(Ctx& c, cudaStream_t s) {
   CoopState& st = g_coop.at(&c);
   FrontDev fd = c.fp.d;
   int* info = c.fp.info;
+  if (st.df) {
+    BDDC_CUDA(cudaMemsetAsync(st.ctr, 0, sizeof(int) * (st.nctr + 2), s));
+    int* qhead = st.ctr + st.nctr;
+    int* err = st.ctr + st.nctr + 1;
+    const DfTask* tasks = st.dtasks;
+    int ntasks = st.ndtasks;
+    unsigned long long* prof = nullptr;
+    if (st.ptime) {
+      prof = st.ptime;  // >= 48 entries (phases of the phased program are not used here)
+      BDDC_CUDA(cudaMemsetAsync(prof, 0, sizeof(unsigned long long) * 48, s));
+    }
+    void* dargs[] = {&fd, &st.pg, (void*)&tasks, &ntasks, &st.ctr, &qhead, &info, &err, &prof};
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (st.ptime) {
+      BDDC_CUDA(cudaEventCreate(&e0));
+      BDDC_CUDA(cudaEventCreate(&e1));
+      BDDC_CUDA(cudaEventRecord(e0, s));
+    }
+    BDDC_CUDA(cudaLaunchCooperativeKernel((void*)coop_factor_df_kernel, st.grid_f, 128, dargs, st.smem_f, s));
+    BDDC_COUNT();
+    int herr = 0;
+    BDDC_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
+    BDDC_CUDA(cudaStreamSynchronize(s));
+    if (herr) throw CudaError("coarse dataflow factorization: dependency wait timed out");
+    if (st.ptime) {
+      BDDC_CUDA(cudaEventRecord(e1, s));
+      BDDC_CUDA(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      BDDC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      fprintf(stderr, "coop factor (dataflow): %d tasks, %d counters, %.1f us\n", ntasks, st.nctr, ms * 1e3);
+      unsigned long long h[48];
+      BDDC_CUDA(cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost));
+      const char* nm[8] = {"EA", "PT", "TS", "X1", "SY", "X2", "W", "CB"};
+      for (int k = 0; k < 8; ++k)
+        if (h[3 * k + 2])
+          fprintf(stderr, "  %-3s n=%7llu  wait %8.1f us/CTA  run %8.1f us/CTA  (avg wait %.2f run %.2f us)\n", nm[k],
+                  h[3 * k + 2], h[3 * k] / 1.9e3 / st.grid_f, h[3 * k + 1] / 1.9e3 / st.grid_f,
+                  h[3 * k] / 1.9e3 / h[3 * k + 2], h[3 * k + 1] / 1.9e3 / h[3 * k + 2]);
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
+    return;
+  }
   void* args[] = {&fd, &st.pg, &info, &st.ptime};
   unsigned long long t0 = 0;
   if (st.ptime) {

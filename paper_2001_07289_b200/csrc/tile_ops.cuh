@@ -282,7 +282,7 @@ __device__ __forceinline__ int potrf_trtri_tile(double* L, int ld, int n, double
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
       const int idx = u0 + u * nt + tid, i = idx & 63, j = idx >> 6;
-      v[u] = (i < n && j < n && i >= j) ? L[i + (long long)j * ld] : (i == j && i >= n ? 1.0 : 0.0);
+      v[u] = (i < n && j < n && i >= j) ? __ldcg(L + i + (long long)j * ld) : (i == j && i >= n ? 1.0 : 0.0);
     }
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
