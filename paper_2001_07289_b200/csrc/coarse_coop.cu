@@ -16,6 +16,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <queue>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -342,25 +343,34 @@ __global__ void __launch_bounds__(128) coop_factor_kernel(FrontDev fd, CoopProgr
 __global__ void __launch_bounds__(128) coop_factor_df_kernel(FrontDev fd, CoopProgram pg,
                                                              const DfTask* __restrict__ tasks, int ntasks,
                                                              int* ctr, int* qhead, int* info, int* err,
-                                                             unsigned long long* prof) {
+                                                             unsigned long long* prof,
+                                                             unsigned long long* trace) {
   extern __shared__ __align__(16) double smem[];
-  __shared__ int ti_s;
-  for (;;) {
-    if (threadIdx.x == 0) ti_s = atomicAdd(qhead, 1);
-    __syncthreads();
-    const int ti = ti_s;
+  constexpr int kWords = (int)(sizeof(DfTask) / sizeof(int));
+  static_assert(kWords <= 32, "task descriptor must fit one warp");
+  __shared__ int ti_s[2];
+  __shared__ DfTask tsh[2];  // current / next task (the next one is claimed and loaded ahead)
+  const int tid = threadIdx.x;
+  if (tid == 0) ti_s[0] = atomicAdd(qhead, 1);
+  __syncthreads();
+  if (tid < kWords && ti_s[0] < ntasks) reinterpret_cast<int*>(&tsh[0])[tid] = reinterpret_cast<const int*>(tasks + ti_s[0])[tid];
+  __syncthreads();
+  for (int buf = 0;; buf ^= 1) {
+    const int ti = ti_s[buf];
     if (ti >= ntasks) break;
-    const DfTask t = tasks[ti];
+    const DfTask& t = tsh[buf];
+    // claim the next task now: the queue atomic's latency hides behind this task
+    if (tid == 0) ti_s[buf ^ 1] = atomicAdd(qhead, 1);
     long long c0 = 0, c1 = 0;
-    if (prof && threadIdx.x == 0) c0 = clock64();
-    if (threadIdx.x == 0) {
-#pragma unroll 1
-      for (int d = 0; d < kDeps; ++d) {
-        const int cix = t.dep[d];
-        if (cix < 0) continue;
+    if (prof && tid == 0) c0 = clock64();
+    if (trace && tid == 0) trace[4 * ti + 0] = gtimer();
+    if (tid < kDeps) {  // one thread per dependency
+      const int cix = t.dep[tid];
+      if (cix >= 0) {
+        const int tg = t.tgt[tid];
         long long spins = 0;
-        while (*(volatile int*)(ctr + cix) < t.tgt[d]) {
-          __nanosleep(64);
+        while (*(volatile int*)(ctr + cix) < tg) {
+          __nanosleep(32);
           if (++spins > (1LL << 25) || *(volatile int*)err) {  // bounded; after one timeout, none
             atomicExch(err, 1);
             break;
@@ -370,14 +380,22 @@ __global__ void __launch_bounds__(128) coop_factor_df_kernel(FrontDev fd, CoopPr
       __threadfence();
     }
     __syncthreads();
-    if (prof && threadIdx.x == 0) c1 = clock64();
+    if (prof && tid == 0) c1 = clock64();
+    if (trace && tid == 0) trace[4 * ti + 1] = gtimer();
+    const int tn = ti_s[buf ^ 1];
+    int nw = 0;  // next descriptor word, loaded before the task and parked in shared memory after it
+    if (tid < kWords && tn < ntasks) nw = __ldg(reinterpret_cast<const int*>(tasks + tn) + tid);
     run_task(t.t, fd, pg, info, smem);
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (tid < kSigs) {  // one thread per signal, each after its own release fence
       __threadfence();
-#pragma unroll
-      for (int q = 0; q < kSigs; ++q)
-        if (t.sig[q] >= 0) atomicAdd(ctr + t.sig[q], 1);
+      if (t.sig[tid] >= 0) atomicAdd(ctr + t.sig[tid], 1);
+    }
+    if (tid == 0) {
+      if (trace) {
+        trace[4 * ti + 2] = gtimer();
+        trace[4 * ti + 3] = blockIdx.x;
+      }
       if (prof) {  // per task type: waiting cycles, running cycles, count
         const long long c2 = clock64();
         atomicAdd(prof + 3 * t.t.type + 0, (unsigned long long)(c1 - c0));
@@ -385,6 +403,8 @@ __global__ void __launch_bounds__(128) coop_factor_df_kernel(FrontDev fd, CoopPr
         atomicAdd(prof + 3 * t.t.type + 2, 1ULL);
       }
     }
+    if (tid < kWords && tn < ntasks) reinterpret_cast<int*>(&tsh[buf ^ 1])[tid] = nw;
+    __syncthreads();
   }
 }
 
@@ -870,27 +890,90 @@ void coop_build(Ctx& c) {
       }
     }
     pool = std::max(pool, off);
-    // list-scheduling order: descending upward rank (estimated cost of the task plus the
-    // longest chain of work that depends on it). A producer always outranks its consumers,
-    // so the order stays topological; critical-path chains (pivot tiles) are dequeued first.
+    // Queue order = the start order of a simulated list schedule on grid_f CTAs: whenever a
+    // CTA is free it takes the ready task of highest upward rank (its estimated cost plus the
+    // longest chain of work depending on it). A task is only started after its producers
+    // finished, so the order is topological (deadlock-free under any real timing), and work
+    // with no successors (X, W21) fills the CTAs that would otherwise block on the serial
+    // panel chains of the top fronts.
     {
-      const double cost[8] = {4.0, 18.0, 6.0, 6.0, 7.0, 8.0, 8.0, 12.0};  // us: EA PT TS X1 SY X2 W CB
-      std::vector<double> maxc(nctr, 0.0), rank(dt.size(), 0.0);
-      for (long long i = (long long)dt.size() - 1; i >= 0; --i) {
+      const double ovh = 1.0;  // per-task scheduling cost (us)
+      auto cost_of = [&](const DfTask& t) {
+        const CoopTask& q = t.t;
+        const int s = fp.sep_size[q.node];
+        switch (q.type) {
+          case CT_EA: return 2.0 + 0.12 * q.b;
+          case CT_PT: return 11.0;
+          case CT_TS: return 5.5;
+          case CT_X1: return 6.5;
+          case CT_SY: {
+            const int k = q.arg * kTile;
+            return (q.a == 0 && q.b == 0 && k + kTile < s) ? 7.5 + 11.0 : 7.5;  // + lookahead PT
+          }
+          case CT_X2: return 6.0;
+          case CT_W: return 7.5;
+          default: return 8.0;
+        }
+      };
+      const size_t n = dt.size();
+      std::vector<double> cst(n), maxc(nctr, 0.0), rank(n, 0.0);
+      for (size_t i = 0; i < n; ++i) cst[i] = cost_of(dt[i]) + ovh;
+      for (long long i = (long long)n - 1; i >= 0; --i) {
         const DfTask& t = dt[i];
         double succ = 0.0;
         for (int q = 0; q < kSigs; ++q)
           if (t.sig[q] >= 0) succ = std::max(succ, maxc[t.sig[q]]);
-        rank[i] = cost[t.t.type] + succ;
+        rank[i] = cst[i] + succ;
         for (int d = 0; d < kDeps; ++d)
           if (t.dep[d] >= 0) maxc[t.dep[d]] = std::max(maxc[t.dep[d]], rank[i]);
       }
-      std::vector<int> order(dt.size());
-      for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
-      std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return rank[a] > rank[b]; });
-      std::vector<DfTask> sorted(dt.size());
-      for (size_t i = 0; i < order.size(); ++i) sorted[i] = dt[order[i]];
+      // waiters per counter, by target
+      std::vector<std::vector<std::pair<int, int>>> wait(nctr);
+      std::vector<int> ndep(n, 0), cval(nctr, 0), wptr(nctr, 0);
+      for (size_t i = 0; i < n; ++i)
+        for (int d = 0; d < kDeps; ++d)
+          if (dt[i].dep[d] >= 0) { wait[dt[i].dep[d]].push_back({dt[i].tgt[d], (int)i}); ndep[i]++; }
+      for (auto& w : wait) std::sort(w.begin(), w.end());
+      auto prio = [&](int a, int b) { return rank[a] < rank[b] || (rank[a] == rank[b] && a > b); };
+      std::priority_queue<int, std::vector<int>, decltype(prio)> ready(prio);
+      for (size_t i = 0; i < n; ++i)
+        if (!ndep[i]) ready.push((int)i);
+      using Ev = std::pair<double, int>;  // (finish time, task)
+      std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> running;
+      std::vector<int> order;
+      order.reserve(n);
+      int free = std::max(grid_f, 1);
+      double now = 0.0;
+      while (order.size() < n || !running.empty()) {
+        while (free > 0 && !ready.empty()) {
+          const int i = ready.top();
+          ready.pop();
+          order.push_back(i);
+          running.push({now + cst[i], i});
+          --free;
+        }
+        if (running.empty()) break;  // (cannot happen for a valid program)
+        const Ev e = running.top();
+        running.pop();
+        now = e.first;
+        ++free;
+        const DfTask& t = dt[e.second];
+        for (int q = 0; q < kSigs; ++q) {
+          const int cix = t.sig[q];
+          if (cix < 0) continue;
+          ++cval[cix];
+          auto& w = wait[cix];
+          while (wptr[cix] < (int)w.size() && w[wptr[cix]].first <= cval[cix])
+            if (--ndep[w[wptr[cix]++].second] == 0) ready.push(w[wptr[cix] - 1].second);
+        }
+      }
+      if (order.size() != n) throw std::runtime_error("coarse dataflow: program is not schedulable");
+      std::vector<DfTask> sorted(n);
+      for (size_t i = 0; i < n; ++i) sorted[i] = dt[order[i]];
       dt.swap(sorted);
+      if (getenv("BDDC_COOP_TIMING"))
+        fprintf(stderr, "coarse dataflow: simulated makespan %.1f us on %d CTAs (critical path %.1f us)\n", now,
+                grid_f, *std::max_element(rank.begin(), rank.end()));
     }
     st.ndtasks = (int)dt.size();
     st.dtasks = c.upload(dt.data(), dt.size());
@@ -1085,11 +1168,14 @@ void coop_factor(Ctx& c, cudaStream_t s) {
     const DfTask* tasks = st.dtasks;
     int ntasks = st.ndtasks;
     unsigned long long* prof = nullptr;
+    unsigned long long* trace = nullptr;
+    const char* tpath = getenv("BDDC_COOP_TRACE");  // per-task timestamps (diagnostics)
+    if (tpath) trace = c.alloc<unsigned long long>((size_t)ntasks * 4);
     if (st.ptime) {
       prof = st.ptime;  // >= 48 entries (phases of the phased program are not used here)
       BDDC_CUDA(cudaMemsetAsync(prof, 0, sizeof(unsigned long long) * 48, s));
     }
-    void* dargs[] = {&fd, &st.pg, (void*)&tasks, &ntasks, &st.ctr, &qhead, &info, &err, &prof};
+    void* dargs[] = {&fd, &st.pg, (void*)&tasks, &ntasks, &st.ctr, &qhead, &info, &err, &prof, &trace};
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (st.ptime) {
       BDDC_CUDA(cudaEventCreate(&e0));
@@ -1102,6 +1188,19 @@ void coop_factor(Ctx& c, cudaStream_t s) {
     BDDC_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
     BDDC_CUDA(cudaStreamSynchronize(s));
     if (herr) throw CudaError("coarse dataflow factorization: dependency wait timed out");
+    if (trace) {  // binary: ntasks, then per task DfTask + 4 x u64 (dequeue, ready, end, cta)
+      std::vector<DfTask> ht(ntasks);
+      std::vector<unsigned long long> tr((size_t)ntasks * 4);
+      BDDC_CUDA(cudaMemcpy(ht.data(), tasks, sizeof(DfTask) * ntasks, cudaMemcpyDeviceToHost));
+      BDDC_CUDA(cudaMemcpy(tr.data(), trace, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost));
+      if (FILE* fo = fopen(tpath, "wb")) {
+        const int hdr[4] = {ntasks, (int)sizeof(DfTask), kDeps, kSigs};
+        fwrite(hdr, sizeof(int), 4, fo);
+        fwrite(ht.data(), sizeof(DfTask), ntasks, fo);
+        fwrite(tr.data(), sizeof(unsigned long long), tr.size(), fo);
+        fclose(fo);
+      }
+    }
     if (st.ptime) {
       BDDC_CUDA(cudaEventRecord(e1, s));
       BDDC_CUDA(cudaEventSynchronize(e1));
