@@ -171,13 +171,12 @@ def phase_work(op, pb, its):
     w["setup.SG"] = ("fp64", nsub * nG * (nG + 1) * nI)
     w["setup.SK"] = ("fp64", nsub * nG**3 / 3)
     ng, ncp = lay.nG_pad, op.plan.nc_pad
-    # L^{-1} of the S_K factor (triangular inverse, n^3/3); Phi = L^{-T} (L^{-1} C^T) S_C^{-1}:
-    # G (triangular x dense), S_C = G^T G (SYRK), S_C^{-1} (~nc^3), G S_C^{-1}, L^{-T} Y,
-    # P = Phi^T S_G Phi; T = L^{-T} L^{-1} (SYRK-like, n^3/3) - (Phi S_C) Phi^T (symmetric)
+    # L^{-1} of the S_K factor (triangular inverse, n^3/3). Phi: G = L^{-1} C^T (triangular x
+    # dense), S_C = G^T G (SYRK), L_C and S_C^{-1} (~nc^3), Q = G L_C^{-T}, V = L^{-T} Q,
+    # Phi = V L_C^{-1}; P = S_C^{-1} - s I (no GEMM). T = L^{-T} L^{-1} (n^3/3) - V V^T (SYRK)
     w["setup.Linv"] = ("fp64", nsub * ng**3 / 3)
-    w["setup.T"] = ("fp64", nsub * (ng**3 / 3 + 2 * ng * ncp * ncp + ng * ng * ncp))
-    w["setup.Phi"] = ("fp64", float(np.sum(nG * nG * nc + nG * nc * nc + nc**3 + 2 * nG * nc * nc
-                                           + nG * nG * nc + 2 * nG * nG * nc + 2 * nG * nc * nc)))
+    w["setup.T"] = ("fp64", nsub * (ng**3 / 3 + ng * ng * ncp))
+    w["setup.Phi"] = ("fp64", float(np.sum(2 * nG * nG * nc + 3 * nG * nc * nc + nc**3)))
     w["setup.btchol"] = ("fp64", nsub * nblk * (m**3 / 3 + 2 * m**3))
     # fused interior elimination (2D): btchol + E + S_G (SYRK, lower half)
     w["setup.schur"] = ("fp64", w["setup.btchol"][1] + w["setup.E"][1] + w["setup.SG"][1])

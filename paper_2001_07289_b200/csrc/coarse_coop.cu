@@ -80,6 +80,7 @@ struct CoopProgram {
 // (counter >= target) and up to 3 counters it increments when done.
 constexpr int kDeps = 6;
 constexpr int kSigs = 6;
+constexpr int kDfCtasPerSm = 3;  // dataflow: no grid barrier, more CTAs hide tile latency
 struct DfTask {
   CoopTask t;
   int dep[kDeps], tgt[kDeps];
@@ -340,7 +341,7 @@ __global__ void __launch_bounds__(128) coop_factor_kernel(FrontDev fd, CoopProgr
 // target, the task runs, and its counters are incremented after a fence. A task only waits
 // on earlier tasks and all CTAs are co-resident (cooperative launch), so the queue always
 // progresses; a wait that exceeds the bound sets *err (the host raises) instead of hanging.
-__global__ void __launch_bounds__(128) coop_factor_df_kernel(FrontDev fd, CoopProgram pg,
+__global__ void __launch_bounds__(128, kDfCtasPerSm) coop_factor_df_kernel(FrontDev fd, CoopProgram pg,
                                                              const DfTask* __restrict__ tasks, int ntasks,
                                                              int* ctr, int* qhead, int* info, int* err,
                                                              unsigned long long* prof,
@@ -686,15 +687,17 @@ void coop_build(Ctx& c) {
   int nsm = 0, per_f = 0, per_s = 0;
   BDDC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device));
   BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_f, coop_factor_kernel, 128, st.smem_f));
-  {
-    int per_df = 0;  // the dataflow kernel must be co-resident with the same grid
-    BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_df, coop_factor_df_kernel, 128, st.smem_f));
-    per_f = std::min(per_f, per_df);
-  }
   BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_s, coop_solve_kernel, 256, 0));
   // few CTAs: the phases are small at the top of the tree and grid.sync cost grows with
   // the number of arriving CTAs
-  st.grid_f = nsm * std::max(std::min(per_f, 2), 1);
+  st.df = coarse_df_enabled(c);
+  if (st.df) {
+    int per_df = 0;
+    BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_df, coop_factor_df_kernel, 128, st.smem_f));
+    st.grid_f = nsm * std::max(std::min(per_df, kDfCtasPerSm), 1);
+  } else {
+    st.grid_f = nsm * std::max(std::min(per_f, 2), 1);
+  }
   st.grid_s = nsm * std::max(std::min(per_s, 4), 1);
   const int grid_f = st.grid_f;
   const int N = fp.nnodes, L = fp.nlevels;

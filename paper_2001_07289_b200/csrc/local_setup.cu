@@ -261,19 +261,25 @@ __global__ void sc_pad_kernel(Geometry G, int sub0, SubTables st, double* SC) {
     if (st.con_coarse[(long long)sub * G.nc_pad + k] < 0) sc[k + (long long)k * G.nc_pad] = 1.0;
 }
 
-// Sloc = c^2 * 0.5 (P + P^T);  cscale = c
-__global__ void finish_local_kernel(Geometry G, int sub0, int spec, const double* diag_s,
-                                    double* cscale, const double* P, double* Sloc) {
+// Local coarse matrix P = Phi^T S_Gamma Phi without forming S_Gamma Phi: with
+// S_K = S_Gamma + s C^T C, Phi = S_K^{-1} C^T S_C^{-1} and C Phi = I,
+//   S_Gamma Phi = C^T S_C^{-1} - s C^T   =>   Phi^T S_Gamma Phi = S_C^{-1} - s I
+// (zero on padded constraints, where Phi has zero columns). Then, as the reference scales
+// it, Sloc = c^2 * 0.5 (P + P^T) with c = 1 / s^2 (or 1 with the spectral option); cscale = c.
+__global__ void finish_local_kernel(Geometry G, int sub0, int spec, const double* diag_s, SubTables st,
+                                    double* cscale, const double* SCi, double* Sloc) {
   const int b = blockIdx.x, sub = sub0 + b;
   const double s = diag_s[sub];
   const double c = spec ? 1.0 : 1.0 / (s * s);
   if (threadIdx.x == 0) cscale[sub] = c;
   const int n = G.nc_pad;
-  const double* pp = P + (long long)b * n * n;
+  const int* cc = st.con_coarse + (long long)sub * n;
+  const double* pp = SCi + (long long)b * n * n;
   double* out = Sloc + (long long)sub * n * n;
   for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
     const int i = idx % n, j = idx / n;
-    const double v = 0.5 * (pp[i + j * n] + pp[j + i * n]);
+    double v = 0.0;
+    if (cc[i] >= 0 && cc[j] >= 0) v = 0.5 * (pp[i + j * n] + pp[j + i * n]) - (i == j ? s : 0.0);
     out[idx] = (c * c) * v;
   }
 }
@@ -285,7 +291,7 @@ size_t local_setup_workspace(const Geometry& g, int chunk) {
   const size_t SG = (size_t)g.nG_pad * g.nG_pad;
   const size_t X = (size_t)g.nG_pad * g.nc_pad;
   const size_t SC = (size_t)g.nc_pad * g.nc_pad;
-  return (size_t)chunk * (E + 2 * SG + 2 * X + 4 * SC);
+  return (size_t)chunk * (E + SG + 2 * X + 3 * SC);
 }
 
 void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
@@ -309,13 +315,11 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
     double* E2 = E + (size_t)chunk * eS;        // E = L_I^{-1} A_IG
     double* Wd = E2 + (size_t)chunk * eS;       // T_j -> Linv_j (dense)
     double* Wo = Wd + (size_t)chunk * wS;       // B_j -> Lo_j (dense)
-    double* SG = Wo + (size_t)chunk * wS;
-    double* X = SG + (size_t)chunk * lsS;
-    double* SC = X + (size_t)chunk * phS;
-    double* P = SC + (size_t)chunk * scS;
-    double* SCc = P + (size_t)chunk * scS;  // S_C before its factorization
-    double* LIv = SCc + (size_t)chunk * scS;  // L_S^{-1}
-    double* Y = LIv + (size_t)chunk * lsS;    // G S_C^{-1}
+    double* X = Wo + (size_t)chunk * wS;      // G = L^{-1} C^T, then V = L^{-T} Q
+    double* SC = X + (size_t)chunk * phS;     // S_C -> L_C
+    double* P = SC + (size_t)chunk * scS;     // L_C^{-1} (blocked path only)
+    double* LIv = P + (size_t)chunk * scS;    // L_S^{-1}
+    double* Y = LIv + (size_t)chunk * lsS;    // Q = G L_C^{-T}
     double* SCi = Y + (size_t)chunk * phS;    // S_C^{-1}
     double* LS = c.LS + sub0 * lsS;
     double* PH = c.Phi + sub0 * phS;
@@ -369,14 +373,12 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
     gemm_batched(true, false, G.nG_pad, G.nG_pad, G.nI_pad, -1.0, Eb, Eb, 1.0, LSb, cnt, s);
     c.prof.end("setup.SG", s);
     }
-    BDDC_CUDA(cudaMemcpyAsync(SG, LS, sizeof(double) * cnt * lsS, cudaMemcpyDeviceToDevice, s));
     // 4. S_K = S_Gamma + s C^T C; Cholesky
     c.prof.begin("setup.SK", s);
     { add_ctc_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, c.diag_s, c.LS); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
     potrf_batched(LSb, G.nG_pad, G.nG_pad, cnt, c.info_k + sub0, c.tinv, s);
     c.prof.end("setup.SK", s);
-    BMat SGb{SG, lsS, G.nG_pad};
     BMat LIb{LIv, lsS, G.nG_pad};
     {
       // 5a. L_S^{-1} (the diagonal-tile inverses are left in c.tinv by the factorization)
@@ -387,25 +389,24 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
         trsm_batched(TRSM_LLN, LSb, G.nG_pad, LIb, G.nG_pad, cnt, c.tinv, s, true);
       }
     }
+    BMat Xb{X, phS, G.nG_pad};
     if (G.nc_pad > 0) {
       PhaseScope pphi(c.prof, "setup.Phi", s);
-      // 5b. G = L_S^{-1} C^T ; S_C = G^T G ; Phi = L_S^{-T} (G S_C^{-1})   (C Phi = I)
+      // 5b. G = L^{-1} C^T, S_C = G^T G = L_C L_C^T, Q = G L_C^{-T} (orthonormal columns),
+      //     V = L^{-T} Q, Phi = V L_C^{-1} = S_K^{-1} C^T S_C^{-1}  (C Phi = I)
       { build_ct_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, c.Phi); BDDC_COUNT(); }
       BDDC_LAUNCH_CHECK();
       BMat PHb{PH, phS, G.nG_pad};
       BMat SCb{SC, scS, G.nc_pad};
-      BMat Xb{X, phS, G.nG_pad};
       BMat Yb{Y, phS, G.nG_pad};
       BMat SCib{SCi, scS, G.nc_pad};
       gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nG_pad, 1.0, LIb, PHb, 0.0, Xb, cnt, s, false, 1);
       gemm_batched(true, false, G.nc_pad, G.nc_pad, G.nG_pad, 1.0, Xb, Xb, 0.0, SCb, cnt, s);
       { sc_pad_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, SC); BDDC_COUNT(); }
       BDDC_LAUNCH_CHECK();
-      BDDC_CUDA(cudaMemcpyAsync(SCc, SC, sizeof(double) * cnt * scS, cudaMemcpyDeviceToDevice, s));
       potrf_batched(SCb, G.nc_pad, G.nc_pad, cnt, nullptr, c.tinv, s);
-      // S_C^{-1} = L_C^{-T} L_C^{-1}
       const int ncb = ceil_div(G.nc_pad, kTile);
-      BMat LCi{c.tinv, (long long)ncb * kTileInvStride, kTile};
+      BMat LCi{c.tinv, (long long)ncb * kTileInvStride, kTile};  // L_C^{-1} (one tile)
       if (ncb > 1) {  // general: L_C^{-1} by blocked solves into the SCi buffer
         { identity_kernel<<<cnt, 256, 0, s>>>(SCi, G.nc_pad, scS); BDDC_COUNT(); }
         BDDC_LAUNCH_CHECK();
@@ -413,30 +414,23 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
         BDDC_CUDA(cudaMemcpyAsync(P, SCi, sizeof(double) * cnt * scS, cudaMemcpyDeviceToDevice, s));
         LCi = BMat{P, scS, G.nc_pad};
       }
+      gemm_batched(false, true, G.nG_pad, G.nc_pad, G.nc_pad, 1.0, Xb, LCi, 0.0, Yb, cnt, s);        // Q
+      gemm_batched(true, false, G.nG_pad, G.nc_pad, G.nG_pad, 1.0, LIb, Yb, 0.0, Xb, cnt, s, false, 2);  // V
+      gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nc_pad, 1.0, Xb, LCi, 0.0, PHb, cnt, s);      // Phi
+      // 6. P = Phi^T S_Gamma Phi = S_C^{-1} - s I,  S_C^{-1} = L_C^{-T} L_C^{-1}
       gemm_batched(true, false, G.nc_pad, G.nc_pad, G.nc_pad, 1.0, LCi, LCi, 0.0, SCib, cnt, s);
-      gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nc_pad, 1.0, Xb, SCib, 0.0, Yb, cnt, s);
-      gemm_batched(true, false, G.nG_pad, G.nc_pad, G.nG_pad, 1.0, LIb, Yb, 0.0, PHb, cnt, s, false, 2);
-      // 6. P = Phi^T (S_Gamma Phi)
-      BMat Pb{P, scS, G.nc_pad};
-      gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nG_pad, 1.0, SGb, PHb, 0.0, Xb, cnt, s);
-      gemm_batched(true, false, G.nc_pad, G.nc_pad, G.nG_pad, 1.0, PHb, Xb, 0.0, Pb, cnt, s);
-      { finish_local_kernel<<<cnt, 256, 0, s>>>(G, sub0, c.coarse_scaling, c.diag_s, c.cscale, P,
+      { finish_local_kernel<<<cnt, 256, 0, s>>>(G, sub0, c.coarse_scaling, c.diag_s, c.st, c.cscale, SCi,
                                               c.Sloc); BDDC_COUNT(); }
       BDDC_LAUNCH_CHECK();
     }
     {
       // 7. explicit interface operator T = (I - Phi C) S_K^{-1} = L^{-T} L^{-1} - Phi S_C Phi^T
-      //    (symmetric; replaces L_S so the apply's local Neumann solve is one GEMV)
+      //    = L^{-T} L^{-1} - V V^T (symmetric; the apply's local Neumann solve is one GEMV)
       PhaseScope pt(c.prof, "setup.T", s);
       // lower tiles only, mirrored (symmetric); L^{-T} upper: tile row m0 needs k >= m0
       gemm_batched(true, false, G.nG_pad, G.nG_pad, G.nG_pad, 1.0, LIb, LIb, 0.0, LSb, cnt, s, true, 2, true);
-      if (G.nc_pad > 0) {
-        BMat PHb{PH, phS, G.nG_pad};
-        BMat Xb{X, phS, G.nG_pad};
-        BMat SCcb{SCc, scS, G.nc_pad};
-        gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nc_pad, 1.0, PHb, SCcb, 0.0, Xb, cnt, s);
-        gemm_batched(false, true, G.nG_pad, G.nG_pad, G.nc_pad, -1.0, Xb, PHb, 1.0, LSb, cnt, s, true, 0, true);
-      }
+      if (G.nc_pad > 0)
+        gemm_batched(false, true, G.nG_pad, G.nG_pad, G.nc_pad, -1.0, Xb, Xb, 1.0, LSb, cnt, s, true, 0, true);
     }
   }
 }
