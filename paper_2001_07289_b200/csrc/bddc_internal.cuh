@@ -153,6 +153,15 @@ struct CsTask {
   int mode;             // forward: 0 = 64 rows x 256 columns, 1 = 256 rows x all s <= 64 columns
   int ldw;              // leading dimension of W21 (dataflow)
 };
+// Dataflow coarse solve task: forward tasks (bottom-up) then backward tasks (top-down) in one
+// queue; dependencies are node counters of finalized chunks (coarse.cu builds them).
+struct SdTask {
+  CsTask t;
+  int dir;         // 0 forward, 1 backward
+  int dep, tgt;    // wait until ctr[dep] >= tgt (dep < 0: none)
+  int sig0, sig1;  // counters incremented when this task finalizes its chunk
+};
+
 struct CsRed {  // reduction over the partials of one row / column chunk
   int t0, p0, np;
 };
@@ -172,6 +181,11 @@ struct LevelSchedule {
   int* red_cnt = nullptr;     // arrival counters of the fused reductions (self-resetting)
   int* gat_ptr = nullptr;     // per node front position -> sources in the update pool
   int* gat_src = nullptr;
+  // dataflow solve (default): one task queue, node counters [3 N] + queue head + error flag
+  SdTask* df_tasks = nullptr;
+  int n_df = 0;
+  int* df_ctr = nullptr;
+  int n_ctr = 0;
 };
 
 // Optional per-phase CUDA-event timers (bench.py reads them for the roofline of the

@@ -101,9 +101,11 @@ void build_level_schedule(Ctx& c) {
     t.ldw = df ? l_ldw[nd] : 0;
     return t;
   };
+  // partial slots are unique over the whole solve (the dataflow solve overlaps levels)
+  std::vector<int> nfch(fp.nnodes, 0), nbch(fp.nnodes, 0);  // finalized chunks per node
+  int pf = 0, pb = 0;
   for (int l = 0; l < L; ++l) {
     ft_off[l] = ft.size(); bt_off[l] = bt.size(); fr_off[l] = fr.size(); br_off[l] = br.size();
-    int pf = 0, pb = 0;
     for (int i = fp.level_ptr[l]; i < fp.level_ptr[l + 1]; ++i) {
       const int nd = fp.level_list[i];
       const int sz = fp.sep_size[nd], f = sz + fp.bnd_size[nd];
@@ -113,6 +115,7 @@ void build_level_schedule(Ctx& c) {
           t.r0 = r0;
           t.mode = 1;
           ft.push_back(t);
+          nfch[nd]++;
         }
       } else {
         for (int r0 = 0; r0 < f; r0 += 64) {
@@ -129,6 +132,7 @@ void build_level_schedule(Ctx& c) {
             ft.push_back(t);
           }
           const int cnt = (int)(ft.size() - first);
+          if (cnt > 0) nfch[nd]++;
           for (size_t q = first; q < ft.size(); ++q) {
             ft[q].np = cnt;
             ft[q].red = cnt > 1 ? (int)fr.size() : -1;
@@ -147,6 +151,7 @@ void build_level_schedule(Ctx& c) {
           bt.push_back(t);
         }
         const int cnt = (int)(bt.size() - first);
+        if (cnt > 0) nbch[nd]++;
         for (size_t q = first; q < bt.size(); ++q) {
           bt[q].np = cnt;
           bt[q].red = cnt > 1 ? (int)br.size() : -1;
@@ -154,8 +159,10 @@ void build_level_schedule(Ctx& c) {
         if (cnt > 1) br.push_back(CsRed{c0, p0, cnt});
       }
     }
-    max_parts = std::max(max_parts, std::max(pf, pb));
   }
+  for (auto& t : bt) t.part += pf;  // backward partials after the forward ones
+  for (auto& r : br) r.p0 += pf;
+  max_parts = pf + pb;
   ft_off[L] = ft.size(); bt_off[L] = bt.size(); fr_off[L] = fr.size(); br_off[L] = br.size();
   CsTask* dft = c.upload<CsTask>(ft.data(), std::max<size_t>(ft.size(), 1));
   CsTask* dbt = c.upload<CsTask>(bt.data(), std::max<size_t>(bt.size(), 1));
@@ -171,6 +178,46 @@ void build_level_schedule(Ctx& c) {
   ls.ybuf = c.alloc<double>((size_t)std::max(fp.n_coarse, 1));
   ls.red_cnt = c.alloc<int>(fr.size() + br.size() + 1);
   BDDC_CUDA(cudaMemset(ls.red_cnt, 0, sizeof(int) * (fr.size() + br.size() + 1)));
+  {
+    // dataflow solve queue. Counters: [0, N) finalized forward chunks of each node's children,
+    // [N, 2N) own forward chunks, [2N, 3N) own backward chunks.
+    const int N = fp.nnodes;
+    std::vector<int> need(N, 0);
+    for (int nd = 0; nd < N; ++nd)
+      if (fp.parent[nd] >= 0) need[fp.parent[nd]] += nfch[nd];
+    std::vector<SdTask> q;
+    q.reserve(ft.size() + bt.size());
+    for (const CsTask& t : ft) {  // level order, bottom-up
+      SdTask d{};
+      d.t = t;
+      d.dir = 0;
+      d.dep = need[t.node] > 0 ? t.node : -1;
+      d.tgt = need[t.node];
+      d.sig0 = fp.parent[t.node] >= 0 ? fp.parent[t.node] : -1;
+      d.sig1 = N + t.node;
+      q.push_back(d);
+    }
+    for (int l = L - 1; l >= 0; --l)  // top-down
+      for (size_t i = bt_off[l]; i < bt_off[l + 1]; ++i) {
+        const CsTask& t = bt[i];
+        int anc = fp.parent[t.node];
+        while (anc >= 0 && nbch[anc] == 0) anc = fp.parent[anc];
+        SdTask d{};
+        d.t = t;
+        d.dir = 1;
+        d.dep = anc >= 0 ? 2 * N + anc : N + t.node;
+        d.tgt = anc >= 0 ? nbch[anc] : nfch[t.node];
+        if (d.tgt <= 0) d.dep = -1;
+        d.sig0 = 2 * N + t.node;
+        d.sig1 = -1;
+        q.push_back(d);
+      }
+    ls.n_df = (int)q.size();
+    ls.df_tasks = c.upload<SdTask>(q.data(), std::max<size_t>(q.size(), 1));
+    ls.n_ctr = 3 * N;
+    ls.df_ctr = c.alloc<int>(ls.n_ctr + 2);  // + queue head + error flag
+    BDDC_CUDA(cudaMemset(ls.df_ctr, 0, sizeof(int) * (ls.n_ctr + 2)));
+  }
   coop_build(c);
 }
 

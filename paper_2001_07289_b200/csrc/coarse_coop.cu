@@ -423,29 +423,250 @@ struct SolveProgram {
   int nfr;  // number of forward reductions (offset of the backward counters)
   int sweep;  // fronts hold [A11^{-1} (full); W21] (else [L11^{-1} (lower); W21])
   const double* wpool;  // dataflow: W21 rows (r >= s) read from here (CsTask w_off / ldw)
+  int n;                // coarse size
 };
 
 __device__ __forceinline__ double gather_at(const LevelView& lv, const double* __restrict__ upd, long long gbase,
                                            int pos) {
   const int* gp = lv.gat_ptr + gbase;
   double acc = 0.0;
-  for (int q = gp[pos]; q < gp[pos + 1]; ++q) acc += upd[lv.gat_src[q]];
+  for (int q = gp[pos]; q < gp[pos + 1]; ++q) acc += __ldcg(upd + lv.gat_src[q]);  // other CTAs' results
   return acc;
 }
 
-// Forward (bottom-up): y_sep = X (rhs + child updates), upd = gathered - W21 (..);
-// backward (top-down): x_sep = X^T y_sep - W21^T x_bnd. Each level is ONE phase (coarse.cu
-// describes the task shapes); a chunk with several tasks is finished by the last task to
-// arrive, which sums the partials in fixed order (deterministic).
+struct SolveShared {
+  double vs[256];
+  double red[4][64];
+  int last;
+};
+
+// Static part of one gather (child-update sources of one front position), loaded before the
+// dependency wait; value() then only reads the update entries (same summation order).
+struct GatherPre {
+  int q0, q1, i0, i1;
+  __device__ __forceinline__ void load(const LevelView& lv, long long gbase, int pos, bool on) {
+    q0 = q1 = 0;
+    i0 = i1 = -1;
+    if (!on) return;
+    const int* gp = lv.gat_ptr + gbase;
+    q0 = gp[pos];
+    q1 = gp[pos + 1];
+    if (q1 > q0) i0 = lv.gat_src[q0];
+    if (q1 > q0 + 1) i1 = lv.gat_src[q0 + 1];
+  }
+  __device__ __forceinline__ double value(const LevelView& lv, const double* __restrict__ upd) const {
+    double acc = 0.0;
+    if (i0 >= 0) acc += __ldcg(upd + i0);
+    if (i1 >= 0) acc += __ldcg(upd + i1);
+    for (int q = q0 + 2; q < q1; ++q) acc += __ldcg(upd + lv.gat_src[q]);
+    return acc;
+  }
+};
+
+// sum_p partial[(p0 + p) * 64 + i] in order p = 0 .. np-1, four loads in flight
+__device__ __forceinline__ double sum_partials(const double* __restrict__ partial, int p0, int np, int i) {
+  double a = 0.0;
+  int p = 0;
+  for (; p + 4 <= np; p += 4) {
+    const double v0 = __ldcg(partial + (long long)(p0 + p) * 64 + i);
+    const double v1 = __ldcg(partial + (long long)(p0 + p + 1) * 64 + i);
+    const double v2 = __ldcg(partial + (long long)(p0 + p + 2) * 64 + i);
+    const double v3 = __ldcg(partial + (long long)(p0 + p + 3) * 64 + i);
+    a += v0;
+    a += v1;
+    a += v2;
+    a += v3;
+  }
+  for (; p < np; ++p) a += __ldcg(partial + (long long)(p0 + p) * 64 + i);
+  return a;
+}
+
+// Forward task (bottom-up): y_sep = X (rhs + child updates), upd = gathered - W21 (..).
+// Everything that does not depend on other tasks (front entries, gather indices) is loaded
+// before wait() (the dataflow dependency wait; a no-op between grid barriers). Returns true
+// when this CTA wrote the chunk's final values (single task, or the last of the chunk's
+// tasks to arrive, which sums the partials in fixed order: deterministic).
+template <class Wait>
+__device__ bool solve_fwd_task(const CsTask& t, const FrontDev& fd, const LevelView& lv, const SolveProgram& sp,
+                               const double* __restrict__ rhs, double* __restrict__ partial,
+                               double* __restrict__ ybuf, int* __restrict__ cnt_f, SolveShared& sh, Wait wait) {
+  const int tid = threadIdx.x;
+  const double* F = fd.fronts + t.front_off;
+  const long long ld = t.ld;
+  const int s = t.s, f = t.f;
+  __syncthreads();
+  if (t.mode == 1) {  // s <= 64: one thread per row, all separator columns
+    const int r = t.r0 + tid;
+    const int ke = r < f ? (r < s ? (sp.sweep ? 0 : r + 1) : s) : 0;
+    const bool wr = sp.wpool && r >= s;  // dataflow factorization: W21 rows from the scratch pool
+    const double* Fr = wr ? sp.wpool + t.w_off + (r - s) : F + r;
+    const long long lr = wr ? (long long)t.ldw : ld;
+    double fv[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) fv[u] = u < ke ? __ldcs(Fr + (long long)u * lr) : 0.0;
+    GatherPre gv, gr;
+    gv.load(lv, t.gat_base, tid, tid < s);
+    gr.load(lv, t.gat_base, r, r >= s && r < f);
+    const double rv = tid < s ? rhs[t.s0 + tid] : 0.0;
+    wait();
+    if (tid < s) sh.vs[tid] = rv + gv.value(lv, fd.upd);
+    const double gu = gr.value(lv, fd.upd);
+    __syncthreads();
+    if (r < f) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int k0 = 0; k0 < ke; k0 += 16) {
+        if (k0 > 0) {
+#pragma unroll
+          for (int u = 0; u < 16; ++u) fv[u] = k0 + u < ke ? __ldcs(Fr + (long long)(k0 + u) * lr) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) acc[u & 3] += k0 + u < ke ? fv[u] * sh.vs[k0 + u] : 0.0;
+      }
+      const double a = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+      if (r < s) ybuf[t.s0 + r] = sp.sweep ? sh.vs[r] : a;
+      else fd.upd[t.upd_off + (r - s)] = gu - a;
+    }
+    return true;
+  }
+  const int rr = tid & 63, grp = tid >> 6;
+  const int r = t.r0 + rr;
+  const int kb = t.c0 + grp * 64;
+  int ke = r < f ? min(kb + 64, s) : kb;
+  if (r < s) ke = sp.sweep ? kb : min(ke, r + 1);
+  const bool wr = sp.wpool && r >= s;
+  const double* Fr = wr ? sp.wpool + t.w_off + (r - s) : F + r;
+  const long long lr = wr ? (long long)t.ldw : ld;
+  double fv[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) fv[u] = kb + u < ke ? __ldcs(Fr + (long long)(kb + u) * lr) : 0.0;
+  const int kk = t.c0 + tid;
+  const int rw = t.r0 + tid;  // row finalized by this thread (tid < 64)
+  GatherPre gv, gr;
+  gv.load(lv, t.gat_base, kk, kk < s);
+  gr.load(lv, t.gat_base, rw, tid < 64 && rw < f && (rw >= s || sp.sweep));
+  const double rv = kk < s ? rhs[t.s0 + kk] : 0.0;
+  const double rrw = (tid < 64 && rw < s && sp.sweep) ? rhs[t.s0 + rw] : 0.0;
+  wait();
+  sh.vs[tid] = kk < s ? rv + gv.value(lv, fd.upd) : 0.0;
+  __syncthreads();
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int k0 = kb; k0 < ke; k0 += 16) {
+    if (k0 > kb) {
+#pragma unroll
+      for (int u = 0; u < 16; ++u) fv[u] = k0 + u < ke ? __ldcs(Fr + (long long)(k0 + u) * lr) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) acc[u & 3] += k0 + u < ke ? fv[u] * sh.vs[k0 + u - t.c0] : 0.0;
+  }
+  sh.red[grp][rr] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  __syncthreads();
+  auto finish = [&](double a) {
+    if (rw < s) ybuf[t.s0 + rw] = sp.sweep ? rrw + gr.value(lv, fd.upd) : a;
+    else fd.upd[t.upd_off + (rw - s)] = gr.value(lv, fd.upd) - a;
+  };
+  if (t.np == 1) {
+    if (tid < 64 && rw < f) finish(sh.red[0][tid] + sh.red[1][tid] + sh.red[2][tid] + sh.red[3][tid]);
+    return true;
+  }
+  if (tid < 64) {
+    partial[(long long)t.part * 64 + tid] = sh.red[0][tid] + sh.red[1][tid] + sh.red[2][tid] + sh.red[3][tid];
+    __threadfence();
+  }
+  __syncthreads();
+  if (tid == 0) sh.last = atomicAdd(cnt_f + t.red, 1) == t.np - 1;
+  __syncthreads();
+  if (!sh.last) return false;
+  __threadfence();
+  const CsRed R = sp.fr[t.red];
+  if (tid < 64 && rw < f) finish(sum_partials(partial, R.p0, R.np, tid));
+  if (tid == 0) cnt_f[t.red] = 0;
+  return true;
+}
+
+// Backward task (top-down): x_sep = X^T y_sep - W21^T x_bnd, 256 rows x 64 columns.
+template <class Wait>
+__device__ bool solve_bwd_task(const CsTask& t, const FrontDev& fd, const SolveProgram& sp,
+                               double* __restrict__ sol, double* __restrict__ partial,
+                               const double* __restrict__ ybuf, int* __restrict__ cnt_b, SolveShared& sh,
+                               Wait wait) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int s = t.s, f = t.f;
+  const long long ld = t.ld;
+  const int* bidx = fd.bnd_idx + fd.bnd_ptr[t.node];
+  const double* F = fd.fronts + t.front_off;
+  __syncthreads();
+  // warp: 8 columns; lane: rows i = lane + 32 m; 16 loads in flight per batch
+  const int kw = t.c0 + warp * 8;
+  double fv[2][8];
+  auto load_rows = [&](int m) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = lane + 32 * (m + h), r = t.r0 + i;
+      const bool wr = sp.wpool && r >= s;
+      const double* Fr = wr ? sp.wpool + t.w_off + (r - s) : F + r;
+      const long long lr = wr ? (long long)t.ldw : ld;
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        const int k = kw + cc;
+        const bool ok = k < s && r < f && (sp.sweep || r >= s || r >= k);
+        fv[h][cc] = ok ? __ldcs(Fr + (long long)k * lr) : 0.0;
+      }
+    }
+  };
+  load_rows(0);
+  const int r = t.r0 + tid;
+  const int bi = (r >= s && r < f) ? bidx[r - s] : -1;
+  wait();
+  sh.vs[tid] = r < s ? __ldcg(ybuf + t.s0 + r) : (bi >= 0 ? -__ldcg(sol + bi) : 0.0);
+  __syncthreads();
+  double acc[8];
+#pragma unroll
+  for (int cc = 0; cc < 8; ++cc) acc[cc] = 0.0;
+  const int mend = min(8, (f - t.r0 + 31) / 32);  // row batches that hold front rows
+#pragma unroll
+  for (int m = 0; m < 8; m += 2) {
+    if (m >= mend) break;
+    if (m > 0) load_rows(m);
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) acc[cc] += fv[h][cc] * sh.vs[lane + 32 * (m + h)];
+  }
+  if (t.np == 1) {
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) {
+      const double v = warp_sum(acc[cc]);
+      const int k = kw + cc;
+      if (lane == 0 && k < s) sol[t.s0 + k] = v;
+    }
+    return true;
+  }
+#pragma unroll
+  for (int cc = 0; cc < 8; ++cc) {
+    const double v = warp_sum(acc[cc]);
+    if (lane == 0) partial[(long long)t.part * 64 + warp * 8 + cc] = v;
+  }
+  if (lane == 0) __threadfence();
+  __syncthreads();
+  if (tid == 0) sh.last = atomicAdd(cnt_b + t.red, 1) == t.np - 1;
+  __syncthreads();
+  if (!sh.last) return false;
+  __threadfence();
+  const CsRed R = sp.br[t.red];
+  const int k = R.t0 + tid;
+  if (tid < 64 && k < s) sol[t.s0 + k] = sum_partials(partial, R.p0, R.np, tid);
+  if (tid == 0) cnt_b[t.red] = 0;
+  return true;
+}
+
+// Level-synchronous solve: each level is one phase between grid barriers.
 __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView lv, SolveProgram sp,
                                                          const double* __restrict__ rhs,
                                                          double* __restrict__ sol,
                                                          double* __restrict__ partial,
                                                          double* __restrict__ ybuf, int* __restrict__ cnt,
                                                          unsigned long long* __restrict__ ptime) {
-  __shared__ double vs[256];
-  __shared__ double red[4][64];
-  __shared__ int last;
+  __shared__ SolveShared sh;
   cg::grid_group grid = cg::this_grid();
   int sync_id = 1;
   if (ptime && blockIdx.x == 0 && threadIdx.x == 0) ptime[0] = gtimer();
@@ -456,177 +677,87 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
   };
   int* cnt_f = cnt;
   int* cnt_b = cnt + sp.nfr;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // forward: levels bottom-up
   for (int l = 0; l < sp.nlevels; ++l) {
-    for (int ti = sp.ft_off[l] + blockIdx.x; ti < sp.ft_off[l + 1]; ti += gridDim.x) {
-      const CsTask t = sp.ft[ti];
-      const double* F = fd.fronts + t.front_off;
-      const long long ld = t.ld;
-      const int s = t.s, f = t.f;
-      __syncthreads();
-      if (t.mode == 1) {  // s <= 64: one thread per row, all separator columns
-        const int r = t.r0 + tid;
-        const int ke = r < f ? (r < s ? (sp.sweep ? 0 : r + 1) : s) : 0;
-        const bool wr = sp.wpool && r >= s;  // dataflow: W21 rows from the scratch pool
-        const double* Fr = wr ? sp.wpool + t.w_off + (r - s) : F + r;
-        const long long lr = wr ? (long long)t.ldw : ld;
-        double fv[16];  // first batch in flight while the right-hand side is gathered
-#pragma unroll
-        for (int u = 0; u < 16; ++u) fv[u] = u < ke ? __ldcs(Fr + (long long)u * lr) : 0.0;
-        if (tid < s) vs[tid] = rhs[t.s0 + tid] + gather_at(lv, fd.upd, t.gat_base, tid);
-        __syncthreads();
-        if (r < f) {
-          double acc[4] = {0.0, 0.0, 0.0, 0.0};
-          for (int k0 = 0; k0 < ke; k0 += 16) {
-            if (k0 > 0) {
-#pragma unroll
-              for (int u = 0; u < 16; ++u) fv[u] = k0 + u < ke ? __ldcs(Fr + (long long)(k0 + u) * lr) : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < 16; ++u) acc[u & 3] += k0 + u < ke ? fv[u] * vs[k0 + u] : 0.0;
-          }
-          const double a = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-          if (r < s) ybuf[t.s0 + r] = sp.sweep ? vs[r] : a;
-          else fd.upd[t.upd_off + (r - s)] = gather_at(lv, fd.upd, t.gat_base, r) - a;
-        }
-        continue;
-      }
-      const int rr = tid & 63, grp = tid >> 6;
-      const int r = t.r0 + rr;
-      const int kb = t.c0 + grp * 64;
-      int ke = r < f ? min(kb + 64, s) : kb;
-      if (r < s) ke = sp.sweep ? kb : min(ke, r + 1);
-      const bool wr = sp.wpool && r >= s;
-      const double* Fr = wr ? sp.wpool + t.w_off + (r - s) : F + r;
-      const long long lr = wr ? (long long)t.ldw : ld;
-      double fv[16];  // first batch in flight while the right-hand side is gathered
-#pragma unroll
-      for (int u = 0; u < 16; ++u) fv[u] = kb + u < ke ? __ldcs(Fr + (long long)(kb + u) * lr) : 0.0;
-      {
-        const int kk = t.c0 + tid;
-        vs[tid] = kk < s ? rhs[t.s0 + kk] + gather_at(lv, fd.upd, t.gat_base, kk) : 0.0;
-      }
-      __syncthreads();
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int k0 = kb; k0 < ke; k0 += 16) {
-        if (k0 > kb) {
-#pragma unroll
-          for (int u = 0; u < 16; ++u) fv[u] = k0 + u < ke ? __ldcs(Fr + (long long)(k0 + u) * lr) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 16; ++u) acc[u & 3] += k0 + u < ke ? fv[u] * vs[k0 + u - t.c0] : 0.0;
-      }
-      red[grp][rr] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-      __syncthreads();
-      if (t.np == 1) {
-        const int rw = t.r0 + tid;
-        if (tid < 64 && rw < f) {
-          const double a = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
-          if (rw < s) ybuf[t.s0 + rw] = sp.sweep ? rhs[t.s0 + rw] + gather_at(lv, fd.upd, t.gat_base, rw) : a;
-          else fd.upd[t.upd_off + (rw - s)] = gather_at(lv, fd.upd, t.gat_base, rw) - a;
-        }
-        continue;
-      }
-      if (tid < 64) {
-        partial[(long long)t.part * 64 + tid] = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
-        __threadfence();
-      }
-      __syncthreads();
-      if (tid == 0) last = atomicAdd(cnt_f + t.red, 1) == t.np - 1;
-      __syncthreads();
-      if (last) {
-        __threadfence();
-        const CsRed R = sp.fr[t.red];
-        const int rw = R.t0 + tid;
-        if (tid < 64 && rw < f) {
-          double a = 0.0;
-          for (int p = 0; p < R.np; ++p) a += __ldcg(partial + (long long)(R.p0 + p) * 64 + tid);
-          if (rw < s) ybuf[t.s0 + rw] = sp.sweep ? rhs[t.s0 + rw] + gather_at(lv, fd.upd, t.gat_base, rw) : a;
-          else fd.upd[t.upd_off + (rw - s)] = gather_at(lv, fd.upd, t.gat_base, rw) - a;
-        }
-        if (tid == 0) cnt_f[t.red] = 0;
-      }
-    }
+    for (int ti = sp.ft_off[l] + blockIdx.x; ti < sp.ft_off[l + 1]; ti += gridDim.x)
+      solve_fwd_task(sp.ft[ti], fd, lv, sp, rhs, partial, ybuf, cnt_f, sh, [] {});
     gsync();
   }
-  // backward: levels top-down
   for (int l = sp.nlevels - 1; l >= 0; --l) {
-    for (int ti = sp.bt_off[l] + blockIdx.x; ti < sp.bt_off[l + 1]; ti += gridDim.x) {
-      const CsTask t = sp.bt[ti];
-      const int s = t.s, f = t.f;
-      const long long ld = t.ld;
-      const int* bidx = fd.bnd_idx + fd.bnd_ptr[t.node];
-      const double* F = fd.fronts + t.front_off;
-      // warp: 8 columns; lane: rows i = lane + 32 m; 16 loads in flight per batch (the first
-      // batch is issued before the right-hand side is read)
-      const int kw = t.c0 + warp * 8;
-      double fv[2][8];
-      auto load_rows = [&](int m) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int i = lane + 32 * (m + h), r = t.r0 + i;
-          const bool wr = sp.wpool && r >= s;
-          const double* Fr = wr ? sp.wpool + t.w_off + (r - s) : F + r;
-          const long long lr = wr ? (long long)t.ldw : ld;
-#pragma unroll
-          for (int cc = 0; cc < 8; ++cc) {
-            const int k = kw + cc;
-            const bool ok = k < s && r < f && (sp.sweep || r >= s || r >= k);
-            fv[h][cc] = ok ? __ldcs(Fr + (long long)k * lr) : 0.0;
-          }
-        }
-      };
-      load_rows(0);
-      __syncthreads();
-      {
-        const int r = t.r0 + tid;
-        vs[tid] = r < s ? ybuf[t.s0 + r] : (r < f ? -sol[bidx[r - s]] : 0.0);
-      }
-      __syncthreads();
-      double acc[8];
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc) acc[cc] = 0.0;
-#pragma unroll
-      for (int m = 0; m < 8; m += 2) {
-        if (m > 0) load_rows(m);
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int cc = 0; cc < 8; ++cc) acc[cc] += fv[h][cc] * vs[lane + 32 * (m + h)];
-      }
-      if (t.np == 1) {
-#pragma unroll
-        for (int cc = 0; cc < 8; ++cc) {
-          const double v = warp_sum(acc[cc]);
-          const int k = kw + cc;
-          if (lane == 0 && k < s) sol[t.s0 + k] = v;
-        }
-        continue;
-      }
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc) {
-        const double v = warp_sum(acc[cc]);
-        if (lane == 0) partial[(long long)t.part * 64 + warp * 8 + cc] = v;
-      }
-      if (lane == 0) __threadfence();
-      __syncthreads();
-      if (tid == 0) last = atomicAdd(cnt_b + t.red, 1) == t.np - 1;
-      __syncthreads();
-      if (last) {
-        __threadfence();
-        const CsRed R = sp.br[t.red];
-        const int k = R.t0 + tid;
-        if (tid < 64 && k < s) {
-          double a = 0.0;
-          for (int p = 0; p < R.np; ++p) a += __ldcg(partial + (long long)(R.p0 + p) * 64 + tid);
-          sol[t.s0 + k] = a;
-        }
-        if (tid == 0) cnt_b[t.red] = 0;
-      }
-    }
+    for (int ti = sp.bt_off[l] + blockIdx.x; ti < sp.bt_off[l + 1]; ti += gridDim.x)
+      solve_bwd_task(sp.bt[ti], fd, sp, sol, partial, ybuf, cnt_b, sh, [] {});
     gsync();
   }
+}
+
+// Dataflow solve: one queue (forward tasks bottom-up, then backward tasks top-down). A
+// forward task waits until every row chunk of the node's children is final; a backward
+// task until the nearest ancestor with separator columns is final (or, without one, its own
+// forward sweep). Chunks finalized signal their node counters. No grid barriers.
+__global__ void __launch_bounds__(256, 3) coop_solve_df_kernel(FrontDev fd, LevelView lv, SolveProgram sp,
+                                                            const SdTask* __restrict__ tasks, int ntasks,
+                                                            int* ctr, int* qhead, int* err,
+                                                            const double* __restrict__ rhs,
+                                                            double* __restrict__ sol,
+                                                            double* __restrict__ partial,
+                                                            double* __restrict__ ybuf, int* __restrict__ cnt,
+                                                            unsigned long long* __restrict__ trace) {
+  __shared__ SolveShared sh;
+  constexpr int kWords = (int)(sizeof(SdTask) / sizeof(int));
+  static_assert(kWords <= 64, "solve task descriptor too large");
+  __shared__ int ti_s[2];
+  __shared__ SdTask tsh[2];
+  const int tid = threadIdx.x;
+  int* cnt_f = cnt;
+  int* cnt_b = cnt + sp.nfr;
+  if (tid == 0) ti_s[0] = atomicAdd(qhead, 1);
+  __syncthreads();
+  if (tid < kWords && ti_s[0] < ntasks)
+    reinterpret_cast<int*>(&tsh[0])[tid] = reinterpret_cast<const int*>(tasks + ti_s[0])[tid];
+  __syncthreads();
+  for (int buf = 0;; buf ^= 1) {
+    const int ti = ti_s[buf];
+    if (ti >= ntasks) break;
+    const SdTask& T = tsh[buf];
+    if (trace && tid == 32) trace[4 * ti] = gtimer();
+    int tn = ntasks, nw = 0;
+    // dependency wait, after the task has issued its static loads; the next task is claimed
+    // meanwhile and its descriptor loaded (parked in shared memory after this task)
+    auto wait = [&] {
+      if (tid == 0) ti_s[buf ^ 1] = atomicAdd(qhead, 1);
+      if (tid == 32 && T.dep >= 0) {
+        long long spins = 0;
+        while (*(volatile int*)(ctr + T.dep) < T.tgt) {
+          __nanosleep(20);
+          if (++spins > (1LL << 25) || *(volatile int*)err) {
+            atomicExch(err, 1);
+            break;
+          }
+        }
+        __threadfence();
+      }
+      if (trace && tid == 32) trace[4 * ti + 1] = gtimer();
+      __syncthreads();
+      tn = ti_s[buf ^ 1];
+      if (tid < kWords && tn < ntasks) nw = __ldg(reinterpret_cast<const int*>(tasks + tn) + tid);
+    };
+    const bool fin = T.dir == 0 ? solve_fwd_task(T.t, fd, lv, sp, rhs, partial, ybuf, cnt_f, sh, wait)
+                                : solve_bwd_task(T.t, fd, sp, sol, partial, ybuf, cnt_b, sh, wait);
+    __syncthreads();
+    if (trace && tid == 0) {
+      trace[4 * ti + 2] = gtimer();
+      trace[4 * ti + 3] = blockIdx.x;
+    }
+    if (fin && tid == 0) {
+      __threadfence();
+      if (T.sig0 >= 0) atomicAdd(ctr + T.sig0, 1);
+      if (T.sig1 >= 0) atomicAdd(ctr + T.sig1, 1);
+    }
+    if (tid < kWords && tn < ntasks) reinterpret_cast<int*>(&tsh[buf ^ 1])[tid] = nw;
+    __syncthreads();
+  }
+  if (*(volatile int*)err)  // a dependency wait timed out: poison the result (PCG reports it)
+    for (int i = blockIdx.x * blockDim.x + tid; i < sp.n; i += gridDim.x * blockDim.x)
+      sol[i] = __longlong_as_double(0x7ff8000000000000LL);
 }
 
 }  // namespace
@@ -650,6 +781,7 @@ struct CoopState {
   int ndtasks = 0;
   int* ctr = nullptr;  // [nctr] dependency counters + queue head + error flag
   int nctr = 0;
+  bool solve_df = true;  // dataflow coarse solve (BDDC_SOLVE_DF=0: level-synchronous)
 };
 
 static std::map<const Ctx*, CoopState> g_coop;
@@ -688,6 +820,13 @@ void coop_build(Ctx& c) {
   BDDC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device));
   BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_f, coop_factor_kernel, 128, st.smem_f));
   BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_s, coop_solve_kernel, 256, 0));
+  {
+    int per_sd = 0;
+    BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sd, coop_solve_df_kernel, 256, 0));
+    const char* e = getenv("BDDC_SOLVE_DF");
+    st.solve_df = !(e && atoi(e) == 0);
+    if (st.solve_df) per_s = per_sd;  // no grid barrier: as many CTAs as fit
+  }
   // few CTAs: the phases are small at the top of the tree and grid.sync cost grows with
   // the number of arriving CTAs
   st.df = coarse_df_enabled(c);
@@ -1156,6 +1295,7 @@ void coop_build(Ctx& c) {
   st.sp.nfr = fr_off[L];
   st.sp.sweep = c.coarse_sweep ? 1 : 0;
   st.sp.wpool = st.df ? st.pg.pool : nullptr;
+  st.sp.n = fp.n_coarse;
 }
 
 void coop_release(const Ctx& c) { g_coop.erase(&c); }
@@ -1187,10 +1327,12 @@ void coop_factor(Ctx& c, cudaStream_t s) {
     }
     BDDC_CUDA(cudaLaunchCooperativeKernel((void*)coop_factor_df_kernel, st.grid_f, 128, dargs, st.smem_f, s));
     BDDC_COUNT();
-    int herr = 0;
+    int herr = 0, serr = 0;  // (serr: a dataflow coarse solve since the last setup timed out)
     BDDC_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
+    BDDC_CUDA(cudaMemcpyAsync(&serr, c.sched.df_ctr + c.sched.n_ctr + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
     BDDC_CUDA(cudaStreamSynchronize(s));
     if (herr) throw CudaError("coarse dataflow factorization: dependency wait timed out");
+    if (serr) throw CudaError("coarse dataflow solve: dependency wait timed out");
     if (trace) {  // binary: ntasks, then per task DfTask + 4 x u64 (dequeue, ready, end, cta)
       std::vector<DfTask> ht(ntasks);
       std::vector<unsigned long long> tr((size_t)ntasks * 4);
@@ -1261,6 +1403,40 @@ void coop_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s) {
   double* partial = c.sched.partial;
   double* ybuf = c.sched.ybuf;
   int* cnt = c.sched.red_cnt;
+  if (st.solve_df) {
+    const LevelSchedule& ls = c.sched;
+    int* ctr = ls.df_ctr;
+    int* qhead = ctr + ls.n_ctr;
+    int* err = qhead + 1;
+    const SdTask* tasks = ls.df_tasks;
+    int ntasks = ls.n_df;
+    BDDC_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int) * (ls.n_ctr + 1), s));  // the error flag stays
+    unsigned long long* trace = nullptr;
+    const char* tpath = getenv("BDDC_SOLVE_TRACE");  // per-task timestamps (diagnostics)
+    if (tpath) {
+      static unsigned long long* tbuf = nullptr;
+      if (!tbuf) tbuf = c.alloc<unsigned long long>((size_t)ntasks * 4);
+      trace = tbuf;
+    }
+    void* dargs[] = {&fd, &lv, &st.sp, (void*)&tasks, &ntasks, &ctr, &qhead, &err, (void*)&rhs, (void*)&sol,
+                     &partial, &ybuf, &cnt, &trace};
+    BDDC_CUDA(cudaLaunchCooperativeKernel((void*)coop_solve_df_kernel, st.grid_s, 256, dargs, 0, s));
+    BDDC_COUNT();
+    if (trace) {  // binary: ntasks, sizeof(SdTask), then tasks, then 4 x u64 per task
+      std::vector<SdTask> ht(ntasks);
+      std::vector<unsigned long long> tr((size_t)ntasks * 4);
+      BDDC_CUDA(cudaMemcpy(ht.data(), tasks, sizeof(SdTask) * ntasks, cudaMemcpyDeviceToHost));
+      BDDC_CUDA(cudaMemcpy(tr.data(), trace, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost));
+      if (FILE* fo = fopen(tpath, "wb")) {
+        const int hdr[2] = {ntasks, (int)sizeof(SdTask)};
+        fwrite(hdr, sizeof(int), 2, fo);
+        fwrite(ht.data(), sizeof(SdTask), ntasks, fo);
+        fwrite(tr.data(), sizeof(unsigned long long), tr.size(), fo);
+        fclose(fo);
+      }
+    }
+    return;
+  }
   void* args[] = {&fd, &lv, &st.sp, (void*)&rhs, (void*)&sol, &partial, &ybuf, &cnt, &st.stime};
   BDDC_CUDA(cudaLaunchCooperativeKernel((void*)coop_solve_kernel, st.grid_s, 256, args, 0, s));
   BDDC_COUNT();
