@@ -156,12 +156,16 @@ def phase_work(op, pb, its):
     # + vector gather / scatter (as stored: li_stride doubles per subdomain)
     li = nblk * T(lay.m_pad) + nblk * lay.m_pad * (1 if pb["mesh"].element == "p1" else 3 ** (lay.dim - 1))
     w["apply.bt_solve"] = ("hbm", 8.0 * (2 * nsub * li + 2 * nsub * nI))
-    # local Gamma phase 1: T rho (explicit interface operator, nG_pad^2) + Phi^T rho
-    w["apply.gamma1"] = ("hbm", 8.0 * nsub * (lay.nG_pad ** 2 + lay.nG_pad * op.plan.nc_pad))
+    # local Gamma phase 1: q = c Phi^T rho; v = T rho (explicit interface operator, nG_pad^2)
+    # runs inside the dataflow coarse solve (its idle CTAs), so its bytes count there
+    tbytes = 8.0 * nsub * lay.nG_pad ** 2
+    w["apply.gamma1"] = ("hbm", 8.0 * nsub * lay.nG_pad * op.plan.nc_pad)
     w["apply.gamma2"] = ("hbm", 8.0 * nsub * lay.nG_pad * op.plan.nc_pad)
     cp = op.plan.coarse
     if cp is not None:
-        w["apply.coarse"] = ("hbm", 8.0 * 2 * cp.factor_entries())
+        w["apply.coarse"] = ("hbm", 8.0 * 2 * cp.factor_entries() + tbytes)
+    else:
+        w["apply.gamma1"] = ("hbm", w["apply.gamma1"][1] + tbytes)
         w["setup.coarse"] = ("fp64", cp.factor_flops())
     # pcg SpMV + dot: x, y, alpha (cells ~ n)
     w["pcg.spmv_dot"] = ("hbm", 8.0 * 3 * n)

@@ -458,6 +458,8 @@ __device__ double block_sum(double v, double* red) {
 // Per subdomain: rho = D rp_Gamma;  q = c Phi^T rho (coarse rhs);  v = T rho, with the
 // explicit interface operator T = (I - Phi C) S_K^{-1} (the constrained Neumann solve on
 // Gamma, bddc.py:357; symmetric, built in setup).
+// WITH_T = false: the coarse solve computes v = T rho (TvArgs); rho is stored in vloc.
+template <bool WITH_T>
 __global__ void __launch_bounds__(128) local_gamma1_kernel(Geometry G, SubTables st,
                                                            const double* __restrict__ T,
                                                            const double* __restrict__ Phi,
@@ -472,6 +474,7 @@ __global__ void __launch_bounds__(128) local_gamma1_kernel(Geometry G, SubTables
   for (int s = tid; s < n; s += nt) {
     const int g = st.slot_gamma[so + s];
     rho[s] = g >= 0 ? st.slot_w[so + s] * rpg[g] : 0.0;
+    if (!WITH_T) vloc[so + s] = rho[s];
   }
   __syncthreads();
   const double c = cscale[sub];
@@ -483,6 +486,7 @@ __global__ void __launch_bounds__(128) local_gamma1_kernel(Geometry G, SubTables
     acc = warp_sum(acc);
     if (lane == 0) qloc[(long long)sub * nc + k] = c * acc;
   }
+  if (!WITH_T) return;
   const double* Ts = T + (long long)sub * n * n;
   for (int i = tid; i < n; i += nt) {
     double a0 = 0.0, a1 = 0.0;
@@ -611,9 +615,11 @@ void apply_bddc(Ctx& c, const double* r, double* z, cudaStream_t s) {
       BDDC_LAUNCH_CHECK();
     }
     const size_t smem1 = sizeof(double) * G.nG_pad;
+    // v = T rho inside the coarse solve when its schedule holds those tasks (rho parked in wloc)
+    const bool tv_fused = c.fp.n_coarse > 0 && c.sched.n_tv > 0;
     c.prof.begin("apply.gamma1", s);
-    { local_gamma1_kernel<<<nl, 128, smem1, s>>>(G, c.st, c.LS, c.Phi, c.cscale, c.rpg, c.qloc,
-                                               c.uloc); BDDC_COUNT(); }
+    if (tv_fused) { local_gamma1_kernel<false><<<nl, 128, smem1, s>>>(G, c.st, c.LS, c.Phi, c.cscale, c.rpg, c.qloc, c.wloc); BDDC_COUNT(); }
+    else { local_gamma1_kernel<true><<<nl, 128, smem1, s>>>(G, c.st, c.LS, c.Phi, c.cscale, c.rpg, c.qloc, c.uloc); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
     c.prof.end("apply.gamma1", s);
     if (c.fp.n_coarse > 0) {
@@ -622,7 +628,8 @@ void apply_bddc(Ctx& c, const double* r, double* z, cudaStream_t s) {
       { coarse_gather_kernel<<<ceil_div(c.fp.n_coarse, th), th, 0, s>>>(c.fp.n_coarse, c.fp.W,
                                                                      c.fp.coarse_slots, c.qloc, c.crhs); BDDC_COUNT(); }
       BDDC_LAUNCH_CHECK();
-      coarse_solve(c, c.crhs, c.csol, s);
+      const TvArgs tv{c.LS, c.wloc, c.uloc, G.nG_pad};
+      coarse_solve(c, c.crhs, c.csol, s, tv_fused ? &tv : nullptr);
     }
     c.prof.begin("apply.gamma2", s);
     { local_gamma2_kernel<<<nl, 128, 0, s>>>(G, c.st, c.Phi, c.cscale, c.csol, c.uloc,

@@ -152,6 +152,7 @@ struct CsTask {
   int np;               // tasks contributing to this task's reduction (1: write directly)
   int mode;             // forward: 0 = 64 rows x 256 columns, 1 = 256 rows x all s <= 64 columns
   int ldw;              // leading dimension of W21 (dataflow)
+  int span;             // forward mode 0: columns per task; backward: rows per task (256 or 64)
 };
 // Dataflow coarse solve task: forward tasks (bottom-up) then backward tasks (top-down) in one
 // queue; dependencies are node counters of finalized chunks (coarse.cu builds them).
@@ -184,6 +185,7 @@ struct LevelSchedule {
   // dataflow solve (default): one task queue, node counters [3 N] + queue head + error flag
   SdTask* df_tasks = nullptr;
   int n_df = 0;
+  int n_tv = 0;               // of which v = T rho tasks of the apply's local Gamma phase (dir 2)
   int* df_ctr = nullptr;
   int n_ctr = 0;
 };
@@ -321,7 +323,16 @@ long long coarse_df_layout(const FrontPlan& fp, std::vector<long long>& inv, std
 // coarse.cu
 void build_level_schedule(Ctx& c);
 void coarse_assemble_and_factor(Ctx& c);
-void coarse_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s);
+// v_i = T_i rho_i for the local subdomains, run by the dataflow coarse solve in the time its
+// top-of-tree chain leaves CTAs idle (apply.cu passes it when the schedule holds those tasks)
+struct TvArgs {
+  const double* T;    // [nsub][n][n] explicit interface operators
+  const double* rho;  // [nsub][n]
+  double* v;          // [nsub][n]
+  int n;
+};
+bool coarse_solve_df_enabled();
+void coarse_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s, const TvArgs* tv = nullptr);
 // apply.cu
 void apply_bddc(Ctx& c, const double* r, double* z, cudaStream_t s);
 void spmv(Ctx& c, const double* x, double* y, cudaStream_t s);

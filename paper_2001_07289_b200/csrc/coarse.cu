@@ -11,7 +11,7 @@ namespace bddc {
 
 void coop_build(Ctx& c);
 void coop_factor(Ctx& c, cudaStream_t s);
-void coop_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s);
+void coop_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s, const TvArgs* tv);
 
 namespace {
 
@@ -99,6 +99,7 @@ void build_level_schedule(Ctx& c) {
     t.np = 1;
     t.w_off = df ? l_w[nd] : 0;
     t.ldw = df ? l_ldw[nd] : 0;
+    t.span = 256;
     return t;
   };
   // partial slots are unique over the whole solve (the dataflow solve overlaps levels)
@@ -118,10 +119,13 @@ void build_level_schedule(Ctx& c) {
           nfch[nd]++;
         }
       } else {
+        // large separators (the top of the tree, where the level chain is the critical path):
+        // narrow tasks whose front entries are all in flight before the dependency wait
+        const int cw = sz >= 128 ? 64 : 256;
         for (int r0 = 0; r0 < f; r0 += 64) {
           const size_t first = ft.size();
           const int p0 = pf;
-          for (int c0 = 0; c0 < sz; c0 += 256) {
+          for (int c0 = 0; c0 < sz; c0 += cw) {
             // separator-only chunks: a copy (sweep) / the lower-triangular L11^{-1} (Cholesky)
             if (c.coarse_sweep ? (r0 + 64 <= sz && c0 > 0) : (r0 < sz && c0 > r0 + 63)) break;
             CsTask t = base(nd);
@@ -129,6 +133,7 @@ void build_level_schedule(Ctx& c) {
             t.c0 = c0;
             t.part = pf++;
             t.mode = 0;
+            t.span = cw;
             ft.push_back(t);
           }
           const int cnt = (int)(ft.size() - first);
@@ -140,13 +145,15 @@ void build_level_schedule(Ctx& c) {
           if (cnt > 1) fr.push_back(CsRed{r0, p0, cnt});
         }
       }
+      const int rw = sz >= 128 ? 64 : 256;
       for (int c0 = 0; c0 < sz; c0 += 64) {
         const size_t first = bt.size();
         const int p0 = pb;
-        for (int r0 = c.coarse_sweep ? 0 : (c0 / 256) * 256; r0 < f; r0 += 256) {  // sweep: full A11^{-1}
+        for (int r0 = c.coarse_sweep ? 0 : (c0 / rw) * rw; r0 < f; r0 += rw) {  // sweep: full A11^{-1}
           CsTask t = base(nd);
           t.r0 = r0;
           t.c0 = c0;
+          t.span = rw;
           t.part = pb++;
           bt.push_back(t);
         }
@@ -186,18 +193,45 @@ void build_level_schedule(Ctx& c) {
     for (int nd = 0; nd < N; ++nd)
       if (fp.parent[nd] >= 0) need[fp.parent[nd]] += nfch[nd];
     std::vector<SdTask> q;
-    q.reserve(ft.size() + bt.size());
-    for (const CsTask& t : ft) {  // level order, bottom-up
-      SdTask d{};
-      d.t = t;
-      d.dir = 0;
-      d.dep = need[t.node] > 0 ? t.node : -1;
-      d.tgt = need[t.node];
-      d.sig0 = fp.parent[t.node] >= 0 ? fp.parent[t.node] : -1;
-      d.sig1 = N + t.node;
-      q.push_back(d);
+    q.reserve(ft.size() + bt.size() + (c.geo.s_hi - c.geo.s_lo));
+    // v = T rho tasks (no dependencies), in slices before each of the top K forward and top K
+    // backward levels: the CTAs take them while the chains at the top of the tree leave them
+    // idle, and each slice drains in about one level's latency
+    const bool tv = coarse_solve_df_enabled() && c.geo.nG_pad > 0 && c.geo.nG_pad <= 256;
+    const int K = std::min(8, L);
+    const int nsl = std::max(2 * K, 1);
+    const int nl = c.geo.s_hi - c.geo.s_lo;
+    int next_sub = c.geo.s_lo, slice = 0;
+    ls.n_tv = 0;
+    auto emit_tv = [&](bool last) {
+      if (!tv) return;
+      const int upto = last ? c.geo.s_hi : c.geo.s_lo + (int)((long long)nl * (slice + 1) / nsl);
+      ++slice;
+      for (; next_sub < upto; ++next_sub) {
+        SdTask d{};
+        d.t.node = next_sub;
+        d.dir = 2;
+        d.dep = d.sig0 = d.sig1 = -1;
+        q.push_back(d);
+        ls.n_tv++;
+      }
+    };
+    for (int l = 0; l < L; ++l) {  // forward: level order, bottom-up
+      if (l >= L - K) emit_tv(false);
+      for (size_t i = ft_off[l]; i < ft_off[l + 1]; ++i) {
+        const CsTask& t = ft[i];
+        SdTask d{};
+        d.t = t;
+        d.dir = 0;
+        d.dep = need[t.node] > 0 ? t.node : -1;
+        d.tgt = need[t.node];
+        d.sig0 = fp.parent[t.node] >= 0 ? fp.parent[t.node] : -1;
+        d.sig1 = N + t.node;
+        q.push_back(d);
+      }
     }
-    for (int l = L - 1; l >= 0; --l)  // top-down
+    for (int l = L - 1; l >= 0; --l) {  // backward: top-down
+      if (l >= L - K) emit_tv(l == L - K);
       for (size_t i = bt_off[l]; i < bt_off[l + 1]; ++i) {
         const CsTask& t = bt[i];
         int anc = fp.parent[t.node];
@@ -212,6 +246,8 @@ void build_level_schedule(Ctx& c) {
         d.sig1 = -1;
         q.push_back(d);
       }
+    }
+    emit_tv(true);  // (L == 0)
     ls.n_df = (int)q.size();
     ls.df_tasks = c.upload<SdTask>(q.data(), std::max<size_t>(q.size(), 1));
     ls.n_ctr = 3 * N;
@@ -239,8 +275,8 @@ void coarse_assemble_and_factor(Ctx& c) {
   coop_factor(c, s);
 }
 
-void coarse_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s) {
-  coop_solve(c, rhs, sol, s);
+void coarse_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s, const TvArgs* tv) {
+  coop_solve(c, rhs, sol, s, tv);
 }
 
 }  // namespace bddc

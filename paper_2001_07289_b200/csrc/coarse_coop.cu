@@ -481,6 +481,18 @@ __device__ __forceinline__ double sum_partials(const double* __restrict__ partia
   return a;
 }
 
+// sum over the np partials of all 64 outputs by the whole CTA: thread (o, quarter) sums its
+// quarter in order, the quarters are added in order (deterministic). Valid for tid < 64.
+__device__ __forceinline__ double sum_partials_cta(const double* __restrict__ partial, int p0, int np,
+                                                   SolveShared& sh) {
+  const int tid = threadIdx.x, o = tid & 63, qt = tid >> 6;
+  const int a = (np * qt) >> 2, b = (np * (qt + 1)) >> 2;
+  double* red = &sh.red[0][0];
+  red[qt * 64 + o] = sum_partials(partial, p0 + a, b - a, o);
+  __syncthreads();
+  return tid < 64 ? ((red[o] + red[64 + o]) + (red[128 + o] + red[192 + o])) : 0.0;
+}
+
 // Forward task (bottom-up): y_sep = X (rhs + child updates), upd = gathered - W21 (..).
 // Everything that does not depend on other tasks (front entries, gather indices) is loaded
 // before wait() (the dataflow dependency wait; a no-op between grid barriers). Returns true
@@ -530,8 +542,9 @@ __device__ bool solve_fwd_task(const CsTask& t, const FrontDev& fd, const LevelV
   }
   const int rr = tid & 63, grp = tid >> 6;
   const int r = t.r0 + rr;
-  const int kb = t.c0 + grp * 64;
-  int ke = r < f ? min(kb + 64, s) : kb;
+  const int cg = t.span >> 2;  // columns per thread group: 64, or 16 (one batch, before the wait)
+  const int kb = t.c0 + grp * cg;
+  int ke = r < f ? min(kb + cg, s) : kb;
   if (r < s) ke = sp.sweep ? kb : min(ke, r + 1);
   const bool wr = sp.wpool && r >= s;
   const double* Fr = wr ? sp.wpool + t.w_off + (r - s) : F + r;
@@ -542,12 +555,12 @@ __device__ bool solve_fwd_task(const CsTask& t, const FrontDev& fd, const LevelV
   const int kk = t.c0 + tid;
   const int rw = t.r0 + tid;  // row finalized by this thread (tid < 64)
   GatherPre gv, gr;
-  gv.load(lv, t.gat_base, kk, kk < s);
+  gv.load(lv, t.gat_base, kk, kk < s && tid < t.span);
   gr.load(lv, t.gat_base, rw, tid < 64 && rw < f && (rw >= s || sp.sweep));
   const double rv = kk < s ? rhs[t.s0 + kk] : 0.0;
   const double rrw = (tid < 64 && rw < s && sp.sweep) ? rhs[t.s0 + rw] : 0.0;
   wait();
-  sh.vs[tid] = kk < s ? rv + gv.value(lv, fd.upd) : 0.0;
+  sh.vs[tid] = (kk < s && tid < t.span) ? rv + gv.value(lv, fd.upd) : 0.0;
   __syncthreads();
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   for (int k0 = kb; k0 < ke; k0 += 16) {
@@ -578,7 +591,8 @@ __device__ bool solve_fwd_task(const CsTask& t, const FrontDev& fd, const LevelV
   if (!sh.last) return false;
   __threadfence();
   const CsRed R = sp.fr[t.red];
-  if (tid < 64 && rw < f) finish(sum_partials(partial, R.p0, R.np, tid));
+  const double a = sum_partials_cta(partial, R.p0, R.np, sh);
+  if (tid < 64 && rw < f) finish(a);
   if (tid == 0) cnt_f[t.red] = 0;
   return true;
 }
@@ -615,14 +629,15 @@ __device__ bool solve_bwd_task(const CsTask& t, const FrontDev& fd, const SolveP
   };
   load_rows(0);
   const int r = t.r0 + tid;
-  const int bi = (r >= s && r < f) ? bidx[r - s] : -1;
+  const bool mine = tid < t.span;
+  const int bi = (mine && r >= s && r < f) ? bidx[r - s] : -1;
   wait();
-  sh.vs[tid] = r < s ? __ldcg(ybuf + t.s0 + r) : (bi >= 0 ? -__ldcg(sol + bi) : 0.0);
+  sh.vs[tid] = (mine && r < s) ? __ldcg(ybuf + t.s0 + r) : (bi >= 0 ? -__ldcg(sol + bi) : 0.0);
   __syncthreads();
   double acc[8];
 #pragma unroll
   for (int cc = 0; cc < 8; ++cc) acc[cc] = 0.0;
-  const int mend = min(8, (f - t.r0 + 31) / 32);  // row batches that hold front rows
+  const int mend = min(t.span >> 5, (f - t.r0 + 31) / 32);  // row batches that hold front rows
 #pragma unroll
   for (int m = 0; m < 8; m += 2) {
     if (m >= mend) break;
@@ -654,7 +669,8 @@ __device__ bool solve_bwd_task(const CsTask& t, const FrontDev& fd, const SolveP
   __threadfence();
   const CsRed R = sp.br[t.red];
   const int k = R.t0 + tid;
-  if (tid < 64 && k < s) sol[t.s0 + k] = sum_partials(partial, R.p0, R.np, tid);
+  const double a = sum_partials_cta(partial, R.p0, R.np, sh);
+  if (tid < 64 && k < s) sol[t.s0 + k] = a;
   if (tid == 0) cnt_b[t.red] = 0;
   return true;
 }
@@ -693,6 +709,36 @@ __global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView 
 // forward task waits until every row chunk of the node's children is final; a backward
 // task until the nearest ancestor with separator columns is final (or, without one, its own
 // forward sweep). Chunks finalized signal their node counters. No grid barriers.
+// v = T rho for one subdomain (n <= 256): thread (row i, half h) sums k = h, h + 2, ...; the
+// halves are combined in fixed order.
+__device__ void solve_tv_task(int sub, const TvArgs& tv, SolveShared& sh) {
+  const int tid = threadIdx.x, n = tv.n;
+  const double* T = tv.T + (long long)sub * n * n;
+  __syncthreads();
+  if (tid < n) sh.vs[tid] = tv.rho[(long long)sub * n + tid];
+  __syncthreads();
+  double* part = &sh.red[0][0];  // [2][128]
+  for (int i0 = 0; i0 < n; i0 += 128) {
+    const int i = i0 + (tid & 127), h = tid >> 7;
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    if (i < n) {
+      int k = h;
+      for (; k + 14 < n; k += 16) {
+        double tv8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) tv8[u] = __ldcs(T + i + (long long)(k + 2 * u) * n);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u & 3] += tv8[u] * sh.vs[k + 2 * u];
+      }
+      for (; k < n; k += 2) a[0] += __ldcs(T + i + (long long)k * n) * sh.vs[k];
+    }
+    part[h * 128 + (tid & 127)] = (a[0] + a[1]) + (a[2] + a[3]);
+    __syncthreads();
+    if (tid < 128 && i0 + tid < n) tv.v[(long long)sub * n + i0 + tid] = part[tid] + part[128 + tid];
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(256, 3) coop_solve_df_kernel(FrontDev fd, LevelView lv, SolveProgram sp,
                                                             const SdTask* __restrict__ tasks, int ntasks,
                                                             int* ctr, int* qhead, int* err,
@@ -700,7 +746,7 @@ __global__ void __launch_bounds__(256, 3) coop_solve_df_kernel(FrontDev fd, Leve
                                                             double* __restrict__ sol,
                                                             double* __restrict__ partial,
                                                             double* __restrict__ ybuf, int* __restrict__ cnt,
-                                                            unsigned long long* __restrict__ trace) {
+                                                            TvArgs tv, unsigned long long* __restrict__ trace) {
   __shared__ SolveShared sh;
   constexpr int kWords = (int)(sizeof(SdTask) / sizeof(int));
   static_assert(kWords <= 64, "solve task descriptor too large");
@@ -720,10 +766,13 @@ __global__ void __launch_bounds__(256, 3) coop_solve_df_kernel(FrontDev fd, Leve
     const SdTask& T = tsh[buf];
     if (trace && tid == 32) trace[4 * ti] = gtimer();
     int tn = ntasks, nw = 0;
-    // dependency wait, after the task has issued its static loads; the next task is claimed
-    // meanwhile and its descriptor loaded (parked in shared memory after this task)
+    // the next task is claimed now (the result is first needed at the wait below) and its
+    // descriptor loaded after the wait (parked in shared memory after this task)
+    int claim = 0;
+    if (tid == 0) claim = atomicAdd(qhead, 1);
+    // dependency wait, after the task has issued its static loads
     auto wait = [&] {
-      if (tid == 0) ti_s[buf ^ 1] = atomicAdd(qhead, 1);
+      if (tid == 0) ti_s[buf ^ 1] = claim;
       if (tid == 32 && T.dep >= 0) {
         long long spins = 0;
         while (*(volatile int*)(ctr + T.dep) < T.tgt) {
@@ -740,8 +789,13 @@ __global__ void __launch_bounds__(256, 3) coop_solve_df_kernel(FrontDev fd, Leve
       tn = ti_s[buf ^ 1];
       if (tid < kWords && tn < ntasks) nw = __ldg(reinterpret_cast<const int*>(tasks + tn) + tid);
     };
-    const bool fin = T.dir == 0 ? solve_fwd_task(T.t, fd, lv, sp, rhs, partial, ybuf, cnt_f, sh, wait)
-                                : solve_bwd_task(T.t, fd, sp, sol, partial, ybuf, cnt_b, sh, wait);
+    bool fin = false;
+    if (T.dir == 0) fin = solve_fwd_task(T.t, fd, lv, sp, rhs, partial, ybuf, cnt_f, sh, wait);
+    else if (T.dir == 1) fin = solve_bwd_task(T.t, fd, sp, sol, partial, ybuf, cnt_b, sh, wait);
+    else {
+      wait();
+      if (tv.T) solve_tv_task(T.t.node, tv, sh);
+    }
     __syncthreads();
     if (trace && tid == 0) {
       trace[4 * ti + 2] = gtimer();
@@ -823,8 +877,7 @@ void coop_build(Ctx& c) {
   {
     int per_sd = 0;
     BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sd, coop_solve_df_kernel, 256, 0));
-    const char* e = getenv("BDDC_SOLVE_DF");
-    st.solve_df = !(e && atoi(e) == 0);
+    st.solve_df = coarse_solve_df_enabled();
     if (st.solve_df) per_s = per_sd;  // no grid barrier: as many CTAs as fit
   }
   // few CTAs: the phases are small at the top of the tree and grid.sync cost grows with
@@ -1396,7 +1449,12 @@ void coop_factor(Ctx& c, cudaStream_t s) {
   }
 }
 
-void coop_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s) {
+bool coarse_solve_df_enabled() {
+  const char* e = getenv("BDDC_SOLVE_DF");
+  return !(e && atoi(e) == 0);
+}
+
+void coop_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s, const TvArgs* tva) {
   CoopState& st = g_coop.at(&c);
   FrontDev fd = c.fp.d;
   LevelView lv{c.sched.gat_ptr, c.sched.gat_src};
@@ -1418,8 +1476,10 @@ void coop_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s) {
       if (!tbuf) tbuf = c.alloc<unsigned long long>((size_t)ntasks * 4);
       trace = tbuf;
     }
+    TvArgs tv{};
+    if (tva) tv = *tva;
     void* dargs[] = {&fd, &lv, &st.sp, (void*)&tasks, &ntasks, &ctr, &qhead, &err, (void*)&rhs, (void*)&sol,
-                     &partial, &ybuf, &cnt, &trace};
+                     &partial, &ybuf, &cnt, &tv, &trace};
     BDDC_CUDA(cudaLaunchCooperativeKernel((void*)coop_solve_df_kernel, st.grid_s, 256, dargs, 0, s));
     BDDC_COUNT();
     if (trace) {  // binary: ntasks, sizeof(SdTask), then tasks, then 4 x u64 per task

@@ -19,7 +19,8 @@ def main(path, verbose=False):
     tr = np.frombuffer(raw[8 + n * tsz:], dtype=np.uint64).reshape(n, 4).astype(np.int64)
     node, r0, c0, s, f = w[:, 8], w[:, 9], w[:, 10], w[:, 11], w[:, 12]
     np_, mode = w[:, 17], w[:, 18]
-    dirn, dep, tgt, sig0, sig1 = w[:, 20], w[:, 21], w[:, 22], w[:, 23], w[:, 24]
+    cw = ((tsz - 20) // 8 * 8) // 4  # CsTask words (8-byte aligned) precede the SdTask fields
+    dirn, dep, tgt, sig0, sig1 = (w[:, cw + k] for k in range(5))
     t0 = tr[:, 0].min()
     deq, rdy, end, cta = tr[:, 0] - t0, tr[:, 1] - t0, tr[:, 2] - t0, tr[:, 3]
     span = end.max()
