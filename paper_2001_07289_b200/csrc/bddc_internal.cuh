@@ -244,6 +244,16 @@ struct PhaseScope {
   ~PhaseScope() { pt.end(name, s); }
 };
 
+// T = L^{-T} L^{-1} - V V^T of the local setup, computed by the dataflow coarse factorization
+// in the time its critical path leaves CTAs idle (local_setup sets it when it defers T)
+struct LtArgs {
+  const double* LI;  // [cnt][n][n] L^{-1}, subdomain sub at (sub - sub0)
+  const double* V;   // [cnt][n][nc]
+  double* T;         // [nsub][n][n] (absolute subdomain index)
+  long long sL, sV;
+  int n, nc, sub0, on;
+};
+
 struct Ctx {
   int device = 0;
   PhaseTimers prof;
@@ -310,6 +320,8 @@ struct Ctx {
     for (void* p : allocations) cudaFree(p);
     allocations.clear();
   }
+  LtArgs lt_defer{};      // local T deferred into the coarse factorization (on = 1)
+  bool lt_fusable = false;  // the coarse factor program holds the T tasks
 };
 
 // local_setup.cu

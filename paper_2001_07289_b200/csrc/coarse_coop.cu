@@ -39,6 +39,7 @@ enum CoopType : int {
   CT_SCP = 10, // column P <- B (block I), pivot tile <- -D_P
   CT_SC = 11,  // M_IJ -= B_I M_{J,P}^T  (lower tiles, I, J != P) [+ lookahead D_{P+1}]
   CT_SM = 12,  // separator block -> full +A11^{-1} (negate, mirror)
+  CT_LT = 13,  // local interface operator tile T_IJ of subdomain (node) = LI^T LI - V V^T
 };
 
 // Sweep block map of panel P (pivot columns [64P, 64P + nb)): the other rows / columns in
@@ -74,6 +75,7 @@ struct CoopProgram {
   CoopScratch sc;
   double* pool;
   int df;  // dataflow mode: one inverse slot per panel, Y partials by panel parity
+  LtArgs lt;  // deferred local T (CT_LT tasks; no-ops when lt.on == 0)
 };
 
 // Dataflow program: tasks in a topological order, each with up to kDeps dependencies
@@ -93,6 +95,22 @@ using namespace tile;
 
 __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgram& pg, int* info,
                          double* smem) {
+  if (t.type == CT_LT) {  // (node = subdomain) T_IJ = sum_{k >= I} LI_kI^T LI_kJ - V_I V_J^T
+    const LtArgs& a = pg.lt;
+    if (!a.on) return;
+    const int sub = t.node, m0 = t.a * kTile, n0 = t.b * kTile;
+    const double* LI = a.LI + (long long)(sub - a.sub0) * a.sL;
+    double* T = a.T + (long long)sub * a.sL;
+    gemm_tile<true, false, kCoopStages>(LI, a.n, LI, a.n, T, a.n, a.n, a.n, a.n, m0, n0, 1.0, 0.0, true, smem,
+                                        m0, -1, a.nc == 0);
+    if (a.nc > 0) {
+      __syncthreads();
+      const double* V = a.V + (long long)(sub - a.sub0) * a.sV;
+      gemm_tile<false, true, kCoopStages>(V, a.n, V, a.n, T, a.n, a.n, a.n, a.nc, m0, n0, -1.0, 1.0, true, smem, 0,
+                                          -1, true);
+    }
+    return;
+  }
   const int node = t.node;
   const int s = fd.sep_size[node], f = s + fd.bnd_size[node], ld = fd.ld[node];
   double* F = fd.fronts + fd.front_off[node];
@@ -971,6 +989,15 @@ void coop_build(Ctx& c) {
       throw std::runtime_error("coarse dataflow: too many signals");
     };
     const long long off = coarse_df_layout(fp, inv, Y, W, ldw);  // X lives in the fronts
+    // the local setup's T tiles (no dependencies): the simulated schedule places them in the
+    // CTA time the critical path leaves idle
+    c.lt_fusable = c.geo.nG_pad > 0 && c.geo.nG_pad % kTile == 0 && !getenv("BDDC_NO_T_IN_COARSE");
+    if (c.lt_fusable) {
+      const int nt = c.geo.nG_pad / kTile;
+      for (int sub = c.geo.s_lo; sub < c.geo.s_hi; ++sub)
+        for (int I = 0; I < nt; ++I)
+          for (int J = 0; J <= I; ++J) dt.push_back(mk(CT_LT, sub, I, J, 0));
+    }
     for (int l = 0; l < L; ++l) {
       std::vector<int> nodes(fp.level_list.begin() + fp.level_ptr[l], fp.level_list.begin() + fp.level_ptr[l + 1]);
       // extend-add of the children (child order per parent)
@@ -1096,17 +1123,18 @@ void coop_build(Ctx& c) {
       auto cost_of = [&](const DfTask& t) {
         const CoopTask& q = t.t;
         const int s = fp.sep_size[q.node];
-        switch (q.type) {
-          case CT_EA: return 2.0 + 0.12 * q.b;
-          case CT_PT: return 11.0;
-          case CT_TS: return 5.5;
-          case CT_X1: return 6.5;
+        switch (q.type) {  // measured averages at 3 CTAs per SM (tools/df_trace.py)
+          case CT_EA: return 2.5 + 0.15 * q.b;
+          case CT_PT: return 15.0;
+          case CT_TS: return 6.5;
+          case CT_X1: return 8.5;
           case CT_SY: {
             const int k = q.arg * kTile;
-            return (q.a == 0 && q.b == 0 && k + kTile < s) ? 7.5 + 11.0 : 7.5;  // + lookahead PT
+            return (q.a == 0 && q.b == 0 && k + kTile < s) ? 10.7 + 15.0 : 10.7;  // + lookahead PT
           }
-          case CT_X2: return 6.0;
-          case CT_W: return 7.5;
+          case CT_X2: return 6.9;
+          case CT_W: return 9.1;
+          case CT_LT: return 18.2;
           default: return 8.0;
         }
       };
@@ -1166,6 +1194,7 @@ void coop_build(Ctx& c) {
       std::vector<DfTask> sorted(n);
       for (size_t i = 0; i < n; ++i) sorted[i] = dt[order[i]];
       dt.swap(sorted);
+
       if (getenv("BDDC_COOP_TIMING"))
         fprintf(stderr, "coarse dataflow: simulated makespan %.1f us on %d CTAs (critical path %.1f us)\n", now,
                 grid_f, *std::max_element(rank.begin(), rank.end()));
@@ -1371,6 +1400,7 @@ void coop_factor(Ctx& c, cudaStream_t s) {
       prof = st.ptime;  // >= 48 entries (phases of the phased program are not used here)
       BDDC_CUDA(cudaMemsetAsync(prof, 0, sizeof(unsigned long long) * 48, s));
     }
+    st.pg.lt = c.lt_defer;
     void* dargs[] = {&fd, &st.pg, (void*)&tasks, &ntasks, &st.ctr, &qhead, &info, &err, &prof, &trace};
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (st.ptime) {
@@ -1407,8 +1437,8 @@ void coop_factor(Ctx& c, cudaStream_t s) {
       fprintf(stderr, "coop factor (dataflow): %d tasks, %d counters, %.1f us\n", ntasks, st.nctr, ms * 1e3);
       unsigned long long h[48];
       BDDC_CUDA(cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost));
-      const char* nm[8] = {"EA", "PT", "TS", "X1", "SY", "X2", "W", "CB"};
-      for (int k = 0; k < 8; ++k)
+      const char* nm[14] = {"EA", "PT", "TS", "X1", "SY", "X2", "W", "CB", "SP", "SB", "SCP", "SC", "SM", "LT"};
+      for (int k = 0; k < 14; ++k)
         if (h[3 * k + 2])
           fprintf(stderr, "  %-3s n=%7llu  wait %8.1f us/CTA  run %8.1f us/CTA  (avg wait %.2f run %.2f us)\n", nm[k],
                   h[3 * k + 2], h[3 * k] / 1.9e3 / st.grid_f, h[3 * k + 1] / 1.9e3 / st.grid_f,

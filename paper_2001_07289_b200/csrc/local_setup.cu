@@ -423,9 +423,16 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
                                               c.Sloc); BDDC_COUNT(); }
       BDDC_LAUNCH_CHECK();
     }
+    // 7. explicit interface operator T = (I - Phi C) S_K^{-1} = L^{-T} L^{-1} - Phi S_C Phi^T
+    //    = L^{-T} L^{-1} - V V^T (symmetric; the apply's local Neumann solve is one GEMV).
+    //    With all subdomains in one chunk it is deferred into the dataflow coarse
+    //    factorization, whose schedule runs its tiles on the CTAs the critical path leaves idle.
+    c.lt_defer = LtArgs{};
+    if (c.lt_fusable && c.fp.n_coarse > 0 && sub0 == G.s_lo && cnt == G.s_hi - G.s_lo) {
+      c.lt_defer = LtArgs{LIv, X, c.LS, lsS, phS, G.nG_pad, G.nc_pad, sub0, 1};
+      continue;
+    }
     {
-      // 7. explicit interface operator T = (I - Phi C) S_K^{-1} = L^{-T} L^{-1} - Phi S_C Phi^T
-      //    = L^{-T} L^{-1} - V V^T (symmetric; the apply's local Neumann solve is one GEMV)
       PhaseScope pt(c.prof, "setup.T", s);
       // lower tiles only, mirrored (symmetric); L^{-T} upper: tile row m0 needs k >= m0
       gemm_batched(true, false, G.nG_pad, G.nG_pad, G.nG_pad, 1.0, LIb, LIb, 0.0, LSb, cnt, s, true, 2, true);

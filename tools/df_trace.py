@@ -13,7 +13,7 @@ from collections import defaultdict
 
 import numpy as np
 
-NAMES = ["EA", "PT", "TS", "X1", "SY", "X2", "W", "CB"]
+NAMES = ["EA", "PT", "TS", "X1", "SY", "X2", "W", "CB", "SP", "SB", "SCP", "SC", "SM", "LT"]
 
 
 def load(path):
