@@ -41,13 +41,18 @@ FP64_PEAK_TFLOPS = 35.43  # cuBLAS (torch.matmul) FP64 8192^3 measured on this p
 FP64_DMMA_ISSUE_TFLOPS = 37.07  # mma.sync m8n8k4 issue-bound loop, same probe
 
 WORKLOADS = {
-    # name: (dim, cells, subs, split, recipe, weighting, source)
-    "cfg2_L4h": (2, (2048, 2048), (64, 64), 8, "ve", "cardinality", "uniform"),
-    "cfg2_Lh": (2, (2048, 2048), (64, 64), 32, "ve", "cardinality", "uniform"),
-    "cfg2_L16h": (2, (2048, 2048), (64, 64), 2, "ve", "cardinality", "uniform"),
-    "cfg2_LH": (2, (2048, 2048), (64, 64), 1, "ve", "cardinality", "uniform"),
-    "cfg3": (3, (128, 128, 128), (16, 16, 16), 2, "vef", "cardinality", "one"),
-    "cfg1": (2, (64, 64), (4, 4), 4, "ve", "cardinality", "one"),
+    # name: (dim, cells, subs, split, recipe, weighting, source, coefficient, coarse scaling)
+    # coefficient "one": alpha = 1; "blocks4": log10 alpha ~ U[-6, 6] per 4^d-cell block (seed 0)
+    "cfg2_L4h": (2, (2048, 2048), (64, 64), 8, "ve", "cardinality", "uniform", "one", "reference"),
+    "cfg2_Lh": (2, (2048, 2048), (64, 64), 32, "ve", "cardinality", "uniform", "one", "reference"),
+    "cfg2_L16h": (2, (2048, 2048), (64, 64), 2, "ve", "cardinality", "uniform", "one", "reference"),
+    "cfg2_LH": (2, (2048, 2048), (64, 64), 1, "ve", "cardinality", "uniform", "one", "reference"),
+    "cfg3": (3, (128, 128, 128), (16, 16, 16), 2, "vef", "cardinality", "one", "one", "reference"),
+    # cfg4 runs in spec scaling: with the reference's coarse-basis scaling it does not converge
+    # in 2000 iterations
+    "cfg4": (3, (128, 128, 128), (16, 16, 16), 2, "vef", "coefficient", "one", "blocks4", "spec"),
+    "cfg5": (3, (256, 256, 256), (32, 32, 32), 2, "vef", "cardinality", "uniform", "one", "reference"),
+    "cfg1": (2, (64, 64), (4, 4), 4, "ve", "cardinality", "one", "one", "reference"),
 }
 SAMPLE = {  # bounded CPU sample with the same local geometry (subdomain size, split, recipe)
     "cfg2_L4h": (2, (128, 128), (4, 4), 8),
@@ -55,8 +60,28 @@ SAMPLE = {  # bounded CPU sample with the same local geometry (subdomain size, s
     "cfg2_L16h": (2, (128, 128), (4, 4), 2),
     "cfg2_LH": (2, (128, 128), (4, 4), 1),
     "cfg3": (3, (24, 24, 24), (3, 3, 3), 2),
+    "cfg4": (3, (24, 24, 24), (3, 3, 3), 2),
+    "cfg5": (3, (24, 24, 24), (3, 3, 3), 2),
     "cfg1": (2, (64, 64), (4, 4), 4),
 }
+DESCR = {
+    "cfg2": "2D Poisson 2048^2 P1 (4,190,209 dofs), 64x64 subdomains of 32^2 cells, {L} subedges + "
+            "vertices ('ve'), cardinality weights, f ~ U[-1,1] (seed 0), rtol 1e-8, reference coarse scaling",
+    "cfg3": "3D Poisson 128^3 P1 tets (2,048,383 dofs), 16^3 subdomains of 8^3 cells, 4h subfaces/subedges "
+            "+ vertices ('vef'), cardinality weights, f = 1, rtol 1e-8, reference coarse scaling",
+    "cfg4": "3D diffusion 128^3 P1 tets, 16^3 subdomains of 8^3, alpha on 4^3-cell blocks with log10 alpha "
+            "~ U[-6,6] (seed 0), 4h objects ('vef'), coefficient weights, f = 1, rtol 1e-8, spec coarse scaling",
+    "cfg5": "3D Poisson 256^3 P1 tets (16,581,375 dofs), 32^3 subdomains of 8^3 cells, 4h objects ('vef'), "
+            "cardinality weights, f ~ U[-1,1] (seed 0), rtol 1e-8, reference coarse scaling",
+    "cfg1": "2D Poisson 64^2 P1, 4x4 subdomains of 16^2, L=4h ('ve'), f = 1, rtol 1e-8",
+}
+
+
+def describe(name):
+    if name.startswith("cfg2_"):
+        return f"{name}: " + DESCR["cfg2"].format(L={"L4h": "L=4h", "Lh": "L=h", "L16h": "L=16h",
+                                                     "LH": "L=32h=H"}[name[5:]])
+    return f"{name}: " + DESCR[name]
 
 
 def _peaks():
@@ -125,10 +150,10 @@ class ClockSampler:
 def build_host_problem(name):
     import paper_2001_07289_b200 as P
 
-    dim, cells, subs, split, recipe, wmode, source = WORKLOADS[name]
+    dim, cells, subs, split, recipe, wmode, source, coef, scaling = WORKLOADS[name]
     t0 = time.perf_counter()
     mesh = P.build_mesh(dim, cells, "p1")
-    cf = P.make_constant(mesh, 1.0)
+    cf = P.make_constant(mesh, 1.0) if coef == "one" else P.make_blocks(mesh, 4, 0)
     pair = P.refine_uniform(mesh, P.partition_uniform(mesh, subs), split, validate=False)
     objs = P.classify_objects(pair)
     w = P.compute_weights(pair, wmode, cf, objs)
@@ -139,7 +164,7 @@ def build_host_problem(name):
         b = system.rhs
     prep = time.perf_counter() - t0
     return dict(P=P, mesh=mesh, cf=cf, pair=pair, objs=objs, w=w, system=system, b=b,
-                recipe=recipe, prep=prep)
+                recipe=recipe, prep=prep, scaling=scaling)
 
 
 def phase_work(op, pb, its):
@@ -163,10 +188,12 @@ def phase_work(op, pb, its):
     w["apply.gamma2"] = ("hbm", 8.0 * nsub * lay.nG_pad * op.plan.nc_pad)
     cp = op.plan.coarse
     if cp is not None:
-        w["apply.coarse"] = ("hbm", 8.0 * 2 * cp.factor_entries() + tbytes)
+        w["apply.coarse"] = ("hbm", 8.0 * 2 * cp.factor_entries())
+        w["setup.coarse"] = ("fp64", cp.factor_flops())
+    if st.tv_in_coarse_solve:
+        w["apply.coarse"] = ("hbm", w["apply.coarse"][1] + tbytes)
     else:
         w["apply.gamma1"] = ("hbm", w["apply.gamma1"][1] + tbytes)
-        w["setup.coarse"] = ("fp64", cp.factor_flops())
     # pcg SpMV + dot: x, y, alpha (cells ~ n)
     w["pcg.spmv_dot"] = ("hbm", 8.0 * 3 * n)
     # setup: E = L_I^{-1} A_IG (block forward, dense n_G RHS), S_G = A_GG - E^T E (SYRK),
@@ -212,7 +239,7 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         comm = P.HostComm(rank, world) if args.transport == "host" else P.NcclComm(rank, world)
     op = P.build_bddc(pb["system"], pb["pair"], pb["objs"], pb["recipe"], pb["w"],
-                      coarse_scaling="reference", device=local_rank, comm=comm)
+                      coarse_scaling=pb["scaling"], device=local_rank, comm=comm)
     sl = op.slab
     first_setup_s = time.perf_counter() - t0
     lib = _capi.load()
@@ -334,7 +361,7 @@ def run_ours(args, rank, world, local_rank):
     # ---- rooflines per phase ----
     hbm, hbm_src = _peaks()
     work = phase_work(op, pb, k)
-    if "setup.T" not in phases and "setup.coarse" in work and "setup.T" in work:
+    if op.stats().t_in_coarse_factor and "setup.coarse" in work and "setup.T" in work:
         # the local T tiles ran inside the dataflow coarse factorization
         work["setup.coarse"] = ("fp64", work["setup.coarse"][1] + work["setup.T"][1])
     phase_out = {}
@@ -395,11 +422,9 @@ def run_ours(args, rank, world, local_rank):
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (seeded f ~ U[-1,1] per dof, alpha = 1)",
+        "data": "synthetic (seeded f / alpha as in config.workload)",
         "config": {
-            "workload": f"{args.workload}: 2D Poisson 2048^2 P1 (4,190,209 dofs), 64x64 subdomains of "
-                        "32^2 cells, L=4h subedges+vertices ('ve'), cardinality weights, rtol 1e-8, "
-                        "reference coarse scaling" if args.workload == "cfg2_L4h" else args.workload,
+            "workload": describe(args.workload),
             "dofs": n, "subdomains": int(st.nsub), "coarse_size": int(st.n_coarse),
             "parallelism": "single GPU" if world == 1 else
                            f"sharded x{world}: slabs of subdomain rows along y, NCCL halo / allgather "
@@ -432,14 +457,20 @@ def run_ours(args, rank, world, local_rank):
     op.close()
 
 
+def _sample_alpha(cells, coef):
+    from oracle import bddc_oracle as orc
+
+    return None if coef == "one" else orc.block_alpha(cells, 4, 0)
+
+
 def cpu_baseline(workload):
     """Oracle port on a bounded sample with the workload's local geometry (one run)."""
     from oracle import bddc_oracle as orc
 
     dim, cells, subs, split = SAMPLE[workload]
-    _, _, _, _, recipe, wmode, source = WORKLOADS[workload]
+    _, _, _, _, recipe, wmode, source, coef, scaling = WORKLOADS[workload]
     t0 = time.perf_counter()
-    o = orc.Oracle(dim, cells, subs, split, recipe, wmode, "p1", None, "reference")
+    o = orc.Oracle(dim, cells, subs, split, recipe, wmode, "p1", _sample_alpha(cells, coef), scaling)
     t_build = time.perf_counter() - t0
     mesh = o.mesh
     b = orc.load(mesh, orc.uniform_f(mesh.n_free, 0)) if source == "uniform" else orc.load(mesh, 1.0)
@@ -459,10 +490,11 @@ def run_reference(args, rank, world):
     from oracle import bddc_oracle as orc
 
     dim, cells, subs, split = SAMPLE[args.workload]
-    _, _, _, _, recipe, wmode, source = WORKLOADS[args.workload]
+    _, _, _, _, recipe, wmode, source, coef, scaling = WORKLOADS[args.workload]
+    alpha = _sample_alpha(cells, coef)
 
     def step():
-        o = orc.Oracle(dim, cells, subs, split, recipe, wmode, "p1", None, "reference")
+        o = orc.Oracle(dim, cells, subs, split, recipe, wmode, "p1", alpha, scaling)
         mesh = o.mesh
         b = orc.load(mesh, orc.uniform_f(mesh.n_free, 0)) if source == "uniform" else orc.load(mesh, 1.0)
         x, rep = orc.pcg(o.matvec, o.apply, b, 1e-8, 2000)

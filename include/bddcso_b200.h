@@ -89,6 +89,8 @@ typedef struct {
   long long n, n_gamma, n_coarse, nsub;
   long long factor_bytes, front_bytes, workspace_bytes;
   int nG_pad, nI_pad, m_pad, nblk, nc_pad, nlevels, max_front;
+  int t_in_coarse_factor; /* the local T tiles run inside the coarse factorization */
+  int tv_in_coarse_solve; /* the apply's v = T rho runs inside the coarse solve */
 } bddc_stats;
 
 int bddc_create(int device, bddc_ctx** out);

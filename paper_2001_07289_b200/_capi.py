@@ -61,6 +61,7 @@ class Stats(C.Structure):
         ("factor_bytes", _ll), ("front_bytes", _ll), ("workspace_bytes", _ll),
         ("nG_pad", _i), ("nI_pad", _i), ("m_pad", _i), ("nblk", _i), ("nc_pad", _i),
         ("nlevels", _i), ("max_front", _i),
+        ("t_in_coarse_factor", _i), ("tv_in_coarse_solve", _i),
     ]
 
 

@@ -602,6 +602,8 @@ int bddc_get_stats(bddc_ctx* h, bddc_stats* o) {
   o->nc_pad = G.nc_pad;
   o->nlevels = c.fp.nlevels;
   o->max_front = c.fp.max_front;
+  o->t_in_coarse_factor = c.lt_defer.on;
+  o->tv_in_coarse_solve = c.fp.n_coarse > 0 && c.sched.n_tv > 0;
   return 0;
 }
 
