@@ -382,7 +382,7 @@ def run_ours(args, rank, world, local_rank):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath) and dominant:
         try:
-            traffic = json.load(open(tpath)).get(dominant)
+            traffic = json.load(open(tpath)).get(args.workload, {}).get(dominant)
         except Exception:
             traffic = None
     roof = None

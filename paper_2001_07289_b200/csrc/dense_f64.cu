@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(128) gemm_f64_kernel(GemmArgs args) {
     case 4: k_hi = min(t.K, n0 + BN); break;   // op(B)(k, n) = 0 for k > n
     default: break;
   }
+  if (args.klo_on) k_lo = max(k_lo, args.klo[tm]);
   gemm_tile<TA, TB, kGemmStages>(t.A, t.lda, t.B, t.ldb, t.C, t.ldc, t.M, t.N, t.K, m0, n0, args.alpha,
                                  args.beta, args.lower != 0, smem, k_lo, k_hi, args.mirror != 0);
 }
@@ -235,9 +236,15 @@ void trsm_tile(const TileArgs& a, TrsmKind kind, cudaStream_t s) {
 }
 
 void gemm_batched(bool tA, bool tB, int M, int N, int K, double alpha, BMat A, BMat B,
-                  double beta, BMat C, int count, cudaStream_t s, bool lower, int tri, bool mirror) {
+                  double beta, BMat C, int count, cudaStream_t s, bool lower, int tri, bool mirror,
+                  const int* klo) {
   if (M <= 0 || N <= 0) return;
   GemmArgs g;
+  if (klo) {
+    if (ceil_div(M, BM) > 16) throw CudaError("gemm_batched: klo table covers 16 row tiles");
+    g.klo_on = 1;
+    for (int i = 0; i < ceil_div(M, BM); ++i) g.klo[i] = klo[i];
+  }
   g.A = A.p; g.sA = A.stride; g.lda = A.ld;
   g.B = B.p; g.sB = B.stride; g.ldb = B.ld;
   g.C = C.p; g.sC = C.stride; g.ldc = C.ld;

@@ -31,6 +31,9 @@ struct GemmArgs {
   int lower = 0;
   int tri = 0;     // structural zeros: 1 op(A) lower, 2 op(A) upper, 3 op(B) lower, 4 op(B) upper
   int mirror = 0;  // with lower: also write the upper triangle (symmetric result)
+  // staircase operands: rows (op(A)) of 64-tile i have no nonzero K below klo[i] (klo_on)
+  int klo_on = 0;
+  int klo[16] = {};
 };
 
 struct TileTask {
@@ -91,9 +94,10 @@ void trsm_batched(TrsmKind kind, BMat L, int n, BMat B, int nother, int count, d
                   cudaStream_t s, bool have_inv = false);
 size_t trsm_scratch_doubles(int n, int count);
 // C = alpha op(A) op(B) + beta C over a strided batch.
+// klo (optional, ceil(M/64) <= 16 entries): first nonzero K of op(A)'s 64-row tile i.
 void gemm_batched(bool tA, bool tB, int M, int N, int K, double alpha, BMat A, BMat B,
                   double beta, BMat C, int count, cudaStream_t s, bool lower = false, int tri = 0,
-                  bool mirror = false);
+                  bool mirror = false, const int* klo = nullptr);
 // L^{-1} of a batch of n x n lower factors (n <= 128) from the diagonal-tile inverses left in
 // scratch by potrf_batched (2x2 block formula); Linv is written in full (zero upper).
 bool trtri_from_tiles(BMat L, int n, BMat Linv, int count, const double* scratch, cudaStream_t s);

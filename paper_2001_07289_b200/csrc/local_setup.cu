@@ -18,12 +18,16 @@ namespace bddc {
 bool schur2d_supported(const Geometry& G);
 bool schur2d(const Ctx& c, int sub0, int cnt, const double* Wd, const double* Wo, const double* E,
              cudaStream_t s);
+bool schur3d_supported(const Geometry& G);
+void schur3d(const Ctx& c, int sub0, int cnt, double* Rt, double* Ht, long long sE, int* klo,
+             cudaStream_t s);
 
 namespace {
 
 // DENSE: also write the interior blocks T_j / B_j and A_IG densely (generic path); the fused
 // 2D path generates them from the stencil on chip and only needs A_GG and s_i here.
-template <int DIM, bool DENSE>
+// ADD (fused 3D): A_GG is added to LS, which already holds -R~^T H~ (no memset of LS).
+template <int DIM, bool DENSE, bool ADD = false>
 __global__ void __launch_bounds__(256) assemble_local_kernel(Geometry G, const double* __restrict__ alpha,
                                                              LocalTables lt, int sub0, double* Wd,
                                                              double* Wo, double* E, double* LS,
@@ -55,7 +59,8 @@ __global__ void __launch_bounds__(256) assemble_local_kernel(Geometry G, const d
     if (dir_a || dir_b) {
       if (node == nb && ca < 0) {
         const int s = -ca - 1;
-        ls[s + (long long)s * G.nG_pad] = 1.0;
+        if (ADD) ls[s + (long long)s * G.nG_pad] += 1.0;
+        else ls[s + (long long)s * G.nG_pad] = 1.0;
       }
       continue;
     }
@@ -65,7 +70,10 @@ __global__ void __launch_bounds__(256) assemble_local_kernel(Geometry G, const d
       nfree_loc += 1;
     }
     if (!DENSE) {
-      if (ca < 0 && cb < 0) ls[(-ca - 1) + (long long)(-cb - 1) * G.nG_pad] = v;
+      if (ca < 0 && cb < 0) {
+        if (ADD) ls[(-ca - 1) + (long long)(-cb - 1) * G.nG_pad] += v;
+        else ls[(-ca - 1) + (long long)(-cb - 1) * G.nG_pad] = v;
+      }
       continue;
     }
     if (ca >= 0 && cb >= 0) {
@@ -83,7 +91,10 @@ __global__ void __launch_bounds__(256) assemble_local_kernel(Geometry G, const d
     const int j = idx / (G.m_pad - G.m), r = G.m + idx % (G.m_pad - G.m);
     wd[j * mm + r + (long long)r * G.m_pad] = 1.0;
   }
-  for (int s = G.nG + threadIdx.x; s < G.nG_pad; s += blockDim.x) ls[s + (long long)s * G.nG_pad] = 1.0;
+  for (int s = G.nG + threadIdx.x; s < G.nG_pad; s += blockDim.x) {
+    if (ADD) ls[s + (long long)s * G.nG_pad] += 1.0;
+    else ls[s + (long long)s * G.nG_pad] = 1.0;
+  }
   // s_i = mean |diag A_i| over local free nodes
   __shared__ double red[256];
   __shared__ int cnt[256];
@@ -324,15 +335,28 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
     double* LS = c.LS + sub0 * lsS;
     double* PH = c.Phi + sub0 * phS;
     const bool fused2d = G.nblk > 0 && schur2d_supported(G);
-    if (!fused2d) {  // the fused 2D kernels generate T_j, B_j and A_IG from the stencil
+    const bool fused3d = G.nblk > 0 && !fused2d && schur3d_supported(G) && !getenv("BDDC_NO_SCHUR3D");
+    if (!fused2d && !fused3d) {  // the fused kernels generate T_j, B_j and A_IG from the stencil
       BDDC_CUDA(cudaMemsetAsync(Wd, 0, sizeof(double) * 2 * (size_t)chunk * wS, s));
       BDDC_CUDA(cudaMemsetAsync(E, 0, sizeof(double) * cnt * eS, s));
     }
-    BDDC_CUDA(cudaMemsetAsync(LS, 0, sizeof(double) * cnt * lsS, s));
+    if (!fused3d) BDDC_CUDA(cudaMemsetAsync(LS, 0, sizeof(double) * cnt * lsS, s));
     BDDC_CUDA(cudaMemsetAsync(PH, 0, sizeof(double) * cnt * phS, s));
+    BMat LSb{LS, lsS, G.nG_pad};
+    if (fused3d) {
+      // 3D: W recursion + per-chunk R_j / H_j, then S_G = A_GG - R~^T H~ as one staircase
+      // GEMM (beta = 0, both triangles); A_GG is added by the assembly below
+      PhaseScope ps(c.prof, "setup.schur", s);
+      int klo[16];
+      schur3d(c, sub0, cnt, E, E2, eS, klo, s);
+      BMat Rb{E, eS, G.nI_pad}, Hb{E2, eS, G.nI_pad};
+      gemm_batched(true, false, G.nG_pad, G.nG_pad, G.nI_pad, -1.0, Rb, Hb, 0.0, LSb, cnt, s, true, 0, true, klo);
+    }
     // 1. assembly
     c.prof.begin("setup.assemble", s);
-    if (G.dim == 2 && fused2d)
+    if (fused3d)
+      { assemble_local_kernel<3, false, true><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, Wd, Wo, E, c.LS, c.diag_s); BDDC_COUNT(); }
+    else if (G.dim == 2 && fused2d)
       { assemble_local_kernel<2, false><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, Wd, Wo, E, c.LS, c.diag_s); BDDC_COUNT(); }
     else if (G.dim == 2)
       { assemble_local_kernel<2, true><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, Wd, Wo, E, c.LS, c.diag_s); BDDC_COUNT(); }
@@ -341,10 +365,12 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
     BDDC_LAUNCH_CHECK();
     c.prof.end("setup.assemble", s);
     // 2-3. fused on-chip interior elimination (2D) or the generic batched path
-    c.prof.begin("setup.schur", s);
-    const bool fused = fused2d && schur2d(c, sub0, cnt, Wd, Wo, E, s);
-    c.prof.end("setup.schur", s);
-    BMat LSb{LS, lsS, G.nG_pad};
+    bool fused = fused3d;
+    if (fused2d) {
+      c.prof.begin("setup.schur", s);
+      fused = schur2d(c, sub0, cnt, Wd, Wo, E, s);
+      c.prof.end("setup.schur", s);
+    }
     if (!fused) {
     // 2. interior block-tridiagonal Cholesky (+ inverses of the diagonal blocks)
     c.prof.begin("setup.btchol", s);

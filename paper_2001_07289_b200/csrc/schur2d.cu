@@ -47,7 +47,7 @@ __constant__ int2 c_lower_tiles[16 * 17 / 2];
 // ---- W recursion (one warp per subdomain) ----
 // W pitch = 4 mod 16 doubles: conflict-free 8x8x4 DMMA fragments; pivot-inverse pitch 20
 template <int M>
-constexpr int wpitch() { return M <= 16 ? 20 : 36; }
+constexpr int wpitch() { return M <= 16 ? 20 : (M <= 32 ? 36 : 68); }
 constexpr int kDP = 20;
 template <int M, bool DIAGB>
 constexpr int wf_warp_doubles() { return (DIAGB ? 1 : 2) * M * wpitch<M>() + 8 * kDP; }
@@ -425,6 +425,207 @@ void launch_schur2d(const Ctx& c, int sub0, int cnt, const double* Wd, const dou
   BDDC_LAUNCH_CHECK();
 }
 
+
+// ---- 3D (planes of m = (b-1)^2 rows, P1: diagonal coupling B_j to the plane below) ----
+// wfactor3d: the W recursion S_j = T_j - B_j W_{j-1} B_j, W_j = S_j^{-1}, one warp per
+// subdomain (lane owns rows lane, lane + 32); T_j comes from the in-plane element stencil.
+constexpr int kWarps3 = 3;
+template <int M>
+constexpr int wf3_warp_doubles() { return M * wpitch<M>() + 8 * kDP + M; }
+
+template <int M>
+__global__ void __launch_bounds__(32 * kWarps3) wfactor3d_kernel(Geometry G, int sub0, int cnt,
+                                                                 const double* __restrict__ alpha,
+                                                                 LocalTables lt,
+                                                                 double* __restrict__ LI,
+                                                                 int* __restrict__ info) {
+  constexpr int P = wpitch<M>();
+  constexpr int RPL = (M + 31) / 32;
+  extern __shared__ __align__(16) double smw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * kWarps3 + warp;
+  if (b >= cnt) return;
+  const int sub = sub0 + b;
+  double* W = smw + warp * wf3_warp_doubles<M>();
+  double* Dm = W + M * P;
+  double* bsh = Dm + 8 * kDP;
+  int p[3];
+  sub_coords(G, sub, p);
+  double* li = LI + (long long)sub * G.li_stride;
+  double* bcg = li + (long long)G.nblk * G.Tm;
+  const int px = G.blk[0] - 1, py = G.blk[1] - 1;
+  int failed = -1;
+  for (int j = 0; j < G.nblk; ++j) {
+    double tc[RPL][9], bi[RPL];
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+      const int r = lane + 32 * q;
+      bi[q] = 0.0;
+#pragma unroll
+      for (int o = 0; o < 9; ++o) tc[q][o] = 0.0;
+      if (r < G.m) {
+        int a[3];
+        local_coords(G, lt.irow_node[j * M + r], a);
+#pragma unroll
+        for (int o = 0; o < 9; ++o) {
+          const int dx = o % 3 - 1, dy = o / 3 - 1;
+          const int x = r % px + dx, y = r / px + dy;
+          if (x < 0 || x >= px || y < 0 || y >= py) continue;
+          const int d[3] = {dx, dy, 0};
+          tc[q][o] = local_coef<3>(G, alpha, p, a, d);
+        }
+        if (j > 0) {
+          const int d[3] = {0, 0, -1};
+          bi[q] = local_coef<3>(G, alpha, p, a, d);
+        }
+      } else if (r < M) {
+        tc[q][4] = 1.0;  // identity on padding rows
+      }
+      if (r < M) {
+        bcg[(long long)j * M + r] = bi[q];
+        bsh[r] = bi[q];
+      }
+    }
+    __syncwarp();
+    // S_j = T_j - diag(b) W_{j-1} diag(b)  (rows owned by this lane)
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+      const int i = lane + 32 * q;
+      if (i >= M) continue;
+      if (j > 0) {
+        const double bq = bi[q];
+#pragma unroll 8
+        for (int k = 0; k < M; ++k) W[i + k * P] = -bq * W[i + k * P] * bsh[k];
+      } else {
+#pragma unroll 8
+        for (int k = 0; k < M; ++k) W[i + k * P] = 0.0;
+      }
+#pragma unroll
+      for (int o = 0; o < 9; ++o)
+        if (tc[q][o] != 0.0) W[i + (i + (o % 3 - 1) + (o / 3 - 1) * px) * P] += tc[q][o];
+    }
+    __syncwarp();
+    const int bad = gj_inverse_blocked<M>(W, Dm, lane);
+    if (bad >= 0 && failed < 0) failed = j * M + bad;
+    // packed W_j (column-major lower), lane = row i: coalesced per column
+    double* lj = li + (long long)j * G.Tm;
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+      const int i = lane + 32 * q;
+      if (i >= M) continue;
+      int cs = 0;
+#pragma unroll 4
+      for (int kk = 0; kk <= i; ++kk) {
+        lj[cs + (i - kk)] = W[i + kk * P];
+        cs += M - kk;
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && failed >= 0) atomicMin(info + sub, failed);
+}
+
+// rh3d: R_j = A_IG,j - B_j H_{j-1}, H_j = W_j R_j for one 64-column chunk of the interface
+// (columns evolve independently), all planes; R~ / H~ (plane-stacked, nI_pad x nG_pad,
+// column-major) feed S_G = A_GG - R~^T H~ (one staircase GEMM). Planes whose active prefix
+// ends before the chunk are skipped; the rows a 16-aligned GEMM k-slice reads below the
+// chunk's first active plane are zeroed.
+constexpr int kRh3Threads = 256;
+template <int M>
+__global__ void __launch_bounds__(kRh3Threads, 2) rh3d_kernel(Geometry G, int sub0,
+                                                            const double* __restrict__ alpha,
+                                                            LocalTables lt,
+                                                            const double* __restrict__ LI,
+                                                            double* __restrict__ Rt,
+                                                            double* __restrict__ Ht, long long sE) {
+  constexpr int P = M + 1;
+  constexpr int CW = 64, EP = CW + 4;
+  constexpr int NW = kRh3Threads / 32;
+  extern __shared__ __align__(16) double sm[];
+  double* Wsm = sm;               // M x P
+  double* R = Wsm + M * P;        // M x EP (row-major)
+  double* H = R + M * EP;         // M x EP
+  double* bsh = H + M * EP;       // M
+  const int c0 = blockIdx.x * CW;
+  const int w = min(CW, G.nG_pad - c0);
+  const int b = blockIdx.y, sub = sub0 + b;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  int p[3];
+  sub_coords(G, sub, p);
+  const double* li = LI + (long long)sub * G.li_stride;
+  const double* bcg = li + (long long)G.nblk * G.Tm;
+  double* rt = Rt + b * sE;
+  double* ht = Ht + b * sE;
+  const int ld = G.nI_pad;
+  const int n0 = G.blk[0] + 1, n1 = G.blk[1] + 1;
+  for (int idx = tid; idx < M * EP; idx += kRh3Threads) H[idx] = 0.0;
+  int jmin = 0;
+  while (jmin < G.nblk && G.nact[jmin] <= c0) ++jmin;
+  {  // zero the k-slice rows below the first active plane (see above)
+    const int r1 = jmin * M, r0 = r1 & ~15;
+    for (int idx = tid; idx < (r1 - r0) * w; idx += kRh3Threads) {
+      const int r = r0 + idx % (r1 - r0), c = c0 + idx / (r1 - r0);
+      rt[r + (long long)c * ld] = 0.0;
+      ht[r + (long long)c * ld] = 0.0;
+    }
+  }
+  for (int j = jmin; j < G.nblk; ++j) {
+    {  // W_j unpacked (symmetric) and the coupling to plane j-1; R_j <- 0
+      constexpr int TM = M * (M + 1) / 2;
+      for (int e = tid; e < TM; e += kRh3Threads) {
+        const double q = 2.0 * M + 1.0;
+        int c = (int)((q - sqrt(q * q - 8.0 * e)) * 0.5);
+        if ((c + 1) * M - (c + 1) * c / 2 <= e) ++c;
+        if (c * M - c * (c - 1) / 2 > e) --c;
+        const int r = c + (e - (c * M - c * (c - 1) / 2));
+        const double v = li[(long long)j * G.Tm + e];
+        Wsm[r + c * P] = v;
+        Wsm[c + r * P] = v;
+      }
+      if (tid < M) bsh[tid] = bcg[(long long)j * M + tid];
+      for (int idx = tid; idx < M * EP; idx += kRh3Threads) R[idx] = 0.0;
+    }
+    __syncthreads();
+    // A_IG,j on the chunk: row r couples to the non-Dirichlet surface slots among its 26
+    // neighbours (structurally zero couplings give 0)
+    for (int idx = tid; idx < G.m * 26; idx += kRh3Threads) {
+      const int r = idx / 26, o0 = idx % 26, o = o0 < 13 ? o0 : o0 + 1;  // skip the centre
+      int a[3];
+      local_coords(G, lt.irow_node[j * M + r], a);
+      const int d[3] = {o % 3 - 1, (o / 3) % 3 - 1, o / 9 - 1};
+      const int bn[3] = {a[0] + d[0], a[1] + d[1], a[2] + d[2]};
+      const int code = lt.node_code[bn[0] + n0 * (bn[1] + n1 * bn[2])];
+      if (code >= 0) continue;
+      const int slot = -code - 1 - c0;
+      if (slot < 0 || slot >= w || local_to_free(G, p, bn) < 0) continue;
+      R[r * EP + slot] = local_coef<3>(G, alpha, p, a, d);
+    }
+    __syncthreads();
+    if (j > jmin)  // R_j -= B_j H_{j-1} (B_j diagonal)
+      for (int idx = tid; idx < M * w; idx += kRh3Threads) {
+        const int r = idx / w, c = idx % w;
+        R[r * EP + c] -= bsh[r] * H[r * EP + c];
+      }
+    __syncthreads();
+    // H_j = W_j R_j
+    for (int tt = warp; tt < (M / 8) * (w / 8); tt += NW) {
+      const int ti = tt % (M / 8), tj = tt / (M / 8);
+      double d0 = 0.0, d1 = 0.0;
+      mma_acc_t<M, 1, P, EP, 1>(d0, d1, Wsm + ti * 8, R + tj * 8, lane);
+      H[(ti * 8 + g) * EP + tj * 8 + 2 * t4] = d0;
+      H[(ti * 8 + g) * EP + tj * 8 + 2 * t4 + 1] = d1;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < M * w; idx += kRh3Threads) {
+      const int r = idx % M, c = idx / M;
+      const long long o = (long long)(j * M + r) + (long long)(c0 + c) * ld;
+      rt[o] = R[r * EP + c];
+      ht[o] = H[r * EP + c];
+    }
+    __syncthreads();
+  }
+}
 }  // namespace
 
 bool schur2d_supported(const Geometry& G) {
@@ -452,6 +653,38 @@ bool schur2d(const Ctx& c, int sub0, int cnt, const double* Wd, const double* Wo
     return false;
   }
   return true;
+}
+
+
+bool schur3d_supported(const Geometry& G) {
+  return G.dim == 3 && G.nbo == 1 && G.bo_dx[0] == 0 && G.bo_dy[0] == 0 && G.m_pad == 56 &&
+         G.nG_pad <= 1024;
+}
+
+// 3D interior elimination: packed W_j into LI (the apply's interior factor), R~ / H~ into
+// Rt / Ht (cnt x sE doubles each), and the staircase K table of S_G = A_GG - R~^T H~.
+void schur3d(const Ctx& c, int sub0, int cnt, double* Rt, double* Ht, long long sE, int* klo,
+             cudaStream_t s) {
+  const Geometry& G = c.geo;
+  constexpr int M = 56;
+  const size_t smem_w = sizeof(double) * kWarps3 * wf3_warp_doubles<M>();
+  const size_t smem_r = sizeof(double) * (M * (M + 1) + 2 * M * 68 + M);
+  static bool attr = false;
+  if (!attr) {
+    BDDC_CUDA(cudaFuncSetAttribute(wfactor3d_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_w));
+    BDDC_CUDA(cudaFuncSetAttribute(rh3d_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r));
+    attr = true;
+  }
+  { wfactor3d_kernel<M><<<ceil_div(cnt, kWarps3), 32 * kWarps3, smem_w, s>>>(G, sub0, cnt, c.alpha, c.lt, c.LI, c.info); BDDC_COUNT(); }
+  BDDC_LAUNCH_CHECK();
+  dim3 grid(ceil_div(G.nG_pad, 64), cnt);
+  { rh3d_kernel<M><<<grid, kRh3Threads, smem_r, s>>>(G, sub0, c.alpha, c.lt, c.LI, Rt, Ht, sE); BDDC_COUNT(); }
+  BDDC_LAUNCH_CHECK();
+  for (int i = 0; i < ceil_div(G.nG_pad, 64); ++i) {
+    int j = 0;
+    while (j < G.nblk && G.nact[j] <= 64 * i) ++j;
+    klo[i] = j * M;
+  }
 }
 
 }  // namespace bddc
