@@ -500,6 +500,96 @@ __global__ void __launch_bounds__(128) local_gamma1_kernel(Geometry G, SubTables
   }
 }
 
+// local_gamma1 with T stored as its lower triangle (t_lower_only): rho = D rp, q = c Phi^T rho,
+// v = T rho reading every stored entry once. Warp per 32-column block J (snake order over
+// the warps): each 32x32 block (I >= J) gives the direct part T_IJ rho_J (rows of I) and,
+// accumulated in registers down the block column, the transposed part T_IJ^T rho_I (rows of
+// J, one shared-memory transpose-sum per column). Partials are summed in a fixed order.
+constexpr int kG1LThreads = 256;
+size_t gamma1_lower_smem(int n) {
+  const int nb = (n + 31) / 32;
+  return sizeof(double) * ((size_t)nb * 32 * (nb + 2) + (kG1LThreads / 32) * 32 * 33);
+}
+
+__global__ void __launch_bounds__(kG1LThreads, 1) local_gamma1_lower_kernel(
+    Geometry G, SubTables st, const double* __restrict__ T, const double* __restrict__ Phi,
+    const double* __restrict__ cscale, const double* __restrict__ rpg, double* qloc, double* vloc) {
+  extern __shared__ double sm[];
+  const int n = G.nG_pad, nc = G.nc_pad, nb = (n + 31) / 32, nr = nb * 32;
+  constexpr int NW = kG1LThreads / 32;
+  double* rho = sm;                       // nr
+  double* pd = rho + nr;                  // [nb][nr] direct partials
+  double* pt = pd + (size_t)nb * nr;      // nr transposed partials
+  double* tb = pt + nr;                   // per warp 32 x 33
+  const int sub = G.s_lo + blockIdx.x, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const long long so = (long long)sub * n;
+  for (int s = tid; s < nr; s += kG1LThreads) {
+    const int g = s < n ? st.slot_gamma[so + s] : -1;
+    rho[s] = g >= 0 ? st.slot_w[so + s] * rpg[g] : 0.0;
+  }
+  __syncthreads();
+  const double c = cscale[sub];
+  const double* ph = Phi + (long long)sub * n * nc;
+  for (int k = warp; k < nc; k += NW) {
+    double acc = 0.0;
+    for (int s = lane; s < n; s += 32) acc += ph[s + (long long)k * n] * rho[s];
+    acc = warp_sum(acc);
+    if (lane == 0) qloc[(long long)sub * nc + k] = c * acc;
+  }
+  const double* Ts = T + (long long)sub * n * n;
+  double* mtb = tb + warp * 32 * 33;
+  for (int round = 0; round * NW < nb; ++round) {
+    const int J = round * NW + ((round & 1) ? NW - 1 - warp : warp);
+    if (J >= nb) continue;
+    double p[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) p[k] = 0.0;
+    for (int I = J; I < nb; ++I) {
+      const int r = 32 * I + lane;
+      double t[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const int col = 32 * J + k;
+        t[k] = (r < n && col < n) ? Ts[r + (long long)col * n] : 0.0;
+      }
+      double d0 = 0.0, d1 = 0.0;
+      const double rr = rho[r];
+      if (I == J) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const double tk = k <= lane ? t[k] : 0.0;
+          if (k & 1) d1 += tk * rho[32 * J + k];
+          else d0 += tk * rho[32 * J + k];
+          p[k] += (k < lane ? t[k] : 0.0) * rr;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          if (k & 1) d1 += t[k] * rho[32 * J + k];
+          else d0 += t[k] * rho[32 * J + k];
+          p[k] += t[k] * rr;
+        }
+      }
+      pd[(size_t)J * nr + r] = d0 + d1;
+    }
+#pragma unroll
+    for (int k = 0; k < 32; ++k) mtb[lane * 33 + k] = p[k];
+    __syncwarp();
+    double sum = 0.0;
+#pragma unroll 8
+    for (int i = 0; i < 32; ++i) sum += mtb[i * 33 + lane];
+    pt[32 * J + lane] = sum;
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int r = tid; r < n; r += kG1LThreads) {
+    double y = pt[r];
+    for (int J = 0; J <= r / 32; ++J) y += pd[(size_t)J * nr + r];
+    vloc[so + r] = y;
+  }
+}
+
 // Per subdomain: w = D (v + c Phi csol[coarse])
 __global__ void __launch_bounds__(128) local_gamma2_kernel(Geometry G, SubTables st,
                                                            const double* __restrict__ Phi,
@@ -619,6 +709,16 @@ void apply_bddc(Ctx& c, const double* r, double* z, cudaStream_t s) {
     const bool tv_fused = c.fp.n_coarse > 0 && c.sched.n_tv > 0;
     c.prof.begin("apply.gamma1", s);
     if (tv_fused) { local_gamma1_kernel<false><<<nl, 128, smem1, s>>>(G, c.st, c.LS, c.Phi, c.cscale, c.rpg, c.qloc, c.wloc); BDDC_COUNT(); }
+    else if (t_lower_only(G)) {
+      static bool attr = false;
+      const size_t sm = gamma1_lower_smem(G.nG_pad);
+      if (!attr) {
+        BDDC_CUDA(cudaFuncSetAttribute(local_gamma1_lower_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gamma1_lower_smem(512)));
+        attr = true;
+      }
+      local_gamma1_lower_kernel<<<nl, kG1LThreads, sm, s>>>(G, c.st, c.LS, c.Phi, c.cscale, c.rpg, c.qloc, c.uloc);
+      BDDC_COUNT();
+    }
     else { local_gamma1_kernel<true><<<nl, 128, smem1, s>>>(G, c.st, c.LS, c.Phi, c.cscale, c.rpg, c.qloc, c.uloc); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
     c.prof.end("apply.gamma1", s);

@@ -254,6 +254,11 @@ struct LtArgs {
   int n, nc, sub0, on;
 };
 
+// The explicit interface operator T is stored as its lower triangle only (the apply's GEMV
+// reads each stored entry once for both triangles) when nG_pad is in (256, 512]; smaller
+// interfaces run v = T rho inside the coarse solve and keep T full.
+inline bool t_lower_only(const Geometry& G) { return G.nG_pad > 256 && G.nG_pad <= 512; }
+
 struct Ctx {
   int device = 0;
   PhaseTimers prof;

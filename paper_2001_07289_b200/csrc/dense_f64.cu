@@ -310,19 +310,22 @@ __global__ void place_diag_inv_kernel(const double* __restrict__ scr, long long 
 }  // namespace
 
 bool trtri_from_tiles(BMat L, int n, BMat Linv, int count, const double* scratch, cudaStream_t s) {
-  if (n > 2 * kTile || n <= 0) return false;
-  const long long sInv = (long long)ceil_div(n, kTile) * kTileInvStride;
+  if (n > 16 * kTile || n <= 0) return false;
+  const int nb = ceil_div(n, kTile);
+  const long long sInv = (long long)nb * kTileInvStride;
   place_diag_inv_kernel<<<count, 256, 0, s>>>(scratch, sInv, n, Linv.p, Linv.stride, Linv.ld);
   BDDC_COUNT();
   BDDC_LAUNCH_CHECK();
-  if (n > kTile) {  // Linv10 = -D1 (L10 D0), through the upper-right block as scratch
-    const int n1 = n - kTile;
-    BMat D0{(double*)scratch, sInv, kTile}, D1{(double*)scratch + kTileInvStride, sInv, kTile};
-    gemm_batched(false, false, n1, kTile, kTile, 1.0, L.at(kTile, 0), D0, 0.0, Linv.at(kTile, 0), count, s,
-                 false, 3);  // D0 lower: B(k, n) = 0 for k < n
-    // Linv10 <- -D1 Linv10 is in place over rows: one 64-row tile (n1 <= 64) -> safe
-    gemm_batched(false, false, n1, kTile, n1, -1.0, D1, Linv.at(kTile, 0), 0.0, Linv.at(kTile, 0), count, s,
-                 false, 1);  // D1 lower: k <= m
+  // block row i: X[i, 0:i] = -D_i (L[i, 0:i] X[0:i, 0:i]); X[0:i, 0:i] (block lower
+  // triangular, done by the earlier rows) is the structurally lower B operand
+  for (int i = 1; i < nb; ++i) {
+    const int r0 = i * kTile, ni = std::min(kTile, n - r0);
+    BMat Di{(double*)scratch + i * kTileInvStride, sInv, kTile};
+    gemm_batched(false, false, ni, r0, r0, 1.0, L.at(r0, 0), Linv, 0.0, Linv.at(r0, 0), count, s,
+                 false, 3);  // B(k, n) = 0 for k < n
+    // in place over rows: one 64-row tile, each CTA reads only its own column block
+    gemm_batched(false, false, ni, r0, ni, -1.0, Di, Linv.at(r0, 0), 0.0, Linv.at(r0, 0), count, s,
+                 false, 1);  // D_i lower: k <= m
   }
   return true;
 }

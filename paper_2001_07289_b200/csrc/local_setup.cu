@@ -264,6 +264,60 @@ __global__ void identity_kernel(double* B, int n, long long stride) {
     b[idx] = (idx % n == idx / n) ? 1.0 : 0.0;
 }
 
+// G = L_S^{-1} C^T without a GEMM: C^T is one nonzero per constrained slot, so column k of
+// G is the coefficient-weighted sum of the columns of L_S^{-1} at the slots of constraint k
+// (ascending slot order: deterministic). Warp per constraint; lane owns rows lane + 32 r.
+template <int RPL>
+__global__ void __launch_bounds__(256) g_gather_kernel(Geometry G, int sub0, SubTables st,
+                                                       const double* __restrict__ LIv, long long sL,
+                                                       double* __restrict__ X, long long sX) {
+  __shared__ int con[1024];
+  __shared__ double cf[1024];
+  const int b = blockIdx.x, sub = sub0 + b, n = G.nG_pad, nc = G.nc_pad;
+  for (int s = threadIdx.x; s < n; s += blockDim.x) {
+    con[s] = st.slot_con[(long long)sub * n + s];
+    cf[s] = st.slot_coef[(long long)sub * n + s];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double* li = LIv + b * sL;
+  double* x = X + b * sX;
+  for (int k = warp; k < nc; k += nw) {
+    double acc[RPL];
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) acc[r] = 0.0;
+    for (int s0 = 0; s0 < n; s0 += 32) {
+      unsigned mask = __ballot_sync(0xffffffffu, s0 + lane < n && con[s0 + lane] == k);
+      while (mask) {
+        const int s = s0 + __ffs(mask) - 1;
+        mask &= mask - 1;
+        const double c = cf[s];
+        const double* col = li + (long long)s * n;
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+          const int i = lane + 32 * r;
+          if (i < n) acc[r] += c * col[i];
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = lane + 32 * r;
+      if (i < n) x[i + (long long)k * n] = acc[r];
+    }
+  }
+}
+
+bool g_gather(const Geometry& G, int sub0, int cnt, const SubTables& st, const double* LIv, long long sL,
+              double* X, long long sX, cudaStream_t s) {
+  const int rpl = ceil_div(G.nG_pad, 32);
+#define BDDC_GG(R) \
+  if (rpl <= R) { g_gather_kernel<R><<<cnt, 256, 0, s>>>(G, sub0, st, LIv, sL, X, sX); BDDC_COUNT(); BDDC_LAUNCH_CHECK(); return true; }
+  BDDC_GG(1) BDDC_GG(2) BDDC_GG(4) BDDC_GG(8) BDDC_GG(13) BDDC_GG(16)
+#undef BDDC_GG
+  return false;
+}
+
 // identity on padded constraints of S_C
 __global__ void sc_pad_kernel(Geometry G, int sub0, SubTables st, double* SC) {
   const int b = blockIdx.x, sub = sub0 + b;
@@ -341,7 +395,6 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
       BDDC_CUDA(cudaMemsetAsync(E, 0, sizeof(double) * cnt * eS, s));
     }
     if (!fused3d) BDDC_CUDA(cudaMemsetAsync(LS, 0, sizeof(double) * cnt * lsS, s));
-    BDDC_CUDA(cudaMemsetAsync(PH, 0, sizeof(double) * cnt * phS, s));
     BMat LSb{LS, lsS, G.nG_pad};
     if (fused3d) {
       // 3D: W recursion + per-chunk R_j / H_j, then S_G = A_GG - R~^T H~ as one staircase
@@ -420,13 +473,16 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
       PhaseScope pphi(c.prof, "setup.Phi", s);
       // 5b. G = L^{-1} C^T, S_C = G^T G = L_C L_C^T, Q = G L_C^{-T} (orthonormal columns),
       //     V = L^{-T} Q, Phi = V L_C^{-1} = S_K^{-1} C^T S_C^{-1}  (C Phi = I)
-      { build_ct_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, c.Phi); BDDC_COUNT(); }
-      BDDC_LAUNCH_CHECK();
       BMat PHb{PH, phS, G.nG_pad};
       BMat SCb{SC, scS, G.nc_pad};
       BMat Yb{Y, phS, G.nG_pad};
       BMat SCib{SCi, scS, G.nc_pad};
-      gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nG_pad, 1.0, LIb, PHb, 0.0, Xb, cnt, s, false, 1);
+      if (!g_gather(G, sub0, cnt, c.st, LIv, lsS, X, phS, s)) {
+        BDDC_CUDA(cudaMemsetAsync(PH, 0, sizeof(double) * cnt * phS, s));
+        { build_ct_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, c.Phi); BDDC_COUNT(); }
+        BDDC_LAUNCH_CHECK();
+        gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nG_pad, 1.0, LIb, PHb, 0.0, Xb, cnt, s, false, 1);
+      }
       gemm_batched(true, false, G.nc_pad, G.nc_pad, G.nG_pad, 1.0, Xb, Xb, 0.0, SCb, cnt, s);
       { sc_pad_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, SC); BDDC_COUNT(); }
       BDDC_LAUNCH_CHECK();
@@ -461,9 +517,10 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
     {
       PhaseScope pt(c.prof, "setup.T", s);
       // lower tiles only, mirrored (symmetric); L^{-T} upper: tile row m0 needs k >= m0
-      gemm_batched(true, false, G.nG_pad, G.nG_pad, G.nG_pad, 1.0, LIb, LIb, 0.0, LSb, cnt, s, true, 2, true);
+      const bool mir = !t_lower_only(G);
+      gemm_batched(true, false, G.nG_pad, G.nG_pad, G.nG_pad, 1.0, LIb, LIb, 0.0, LSb, cnt, s, true, 2, mir);
       if (G.nc_pad > 0)
-        gemm_batched(false, true, G.nG_pad, G.nG_pad, G.nc_pad, -1.0, Xb, Xb, 1.0, LSb, cnt, s, true, 0, true);
+        gemm_batched(false, true, G.nG_pad, G.nG_pad, G.nc_pad, -1.0, Xb, Xb, 1.0, LSb, cnt, s, true, 0, mir);
     }
   }
 }
