@@ -184,6 +184,8 @@ def phase_work(op, pb, its):
     # local Gamma phase 1: q = c Phi^T rho; v = T rho (explicit interface operator, nG_pad^2)
     # runs inside the dataflow coarse solve (its idle CTAs), so its bytes count there
     tbytes = 8.0 * nsub * lay.nG_pad ** 2
+    if 256 < lay.nG_pad <= 512:  # T stored and read as its lower triangle (t_lower_only)
+        tbytes = 8.0 * nsub * lay.nG_pad * (lay.nG_pad + 1) / 2
     w["apply.gamma1"] = ("hbm", 8.0 * nsub * lay.nG_pad * op.plan.nc_pad)
     w["apply.gamma2"] = ("hbm", 8.0 * nsub * lay.nG_pad * op.plan.nc_pad)
     cp = op.plan.coarse

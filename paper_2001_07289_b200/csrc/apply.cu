@@ -508,19 +508,21 @@ __global__ void __launch_bounds__(128) local_gamma1_kernel(Geometry G, SubTables
 constexpr int kG1LThreads = 256;
 size_t gamma1_lower_smem(int n) {
   const int nb = (n + 31) / 32;
-  return sizeof(double) * ((size_t)nb * 32 * (nb + 2) + (kG1LThreads / 32) * 32 * 33);
+  return sizeof(double) * ((size_t)nb * 32 * 2 + (size_t)nb * 32 * nb - 16 * nb * (nb - 1) +
+                           (kG1LThreads / 32) * 32 * 33);
 }
 
-__global__ void __launch_bounds__(kG1LThreads, 1) local_gamma1_lower_kernel(
+__global__ void __launch_bounds__(kG1LThreads, 2) local_gamma1_lower_kernel(
     Geometry G, SubTables st, const double* __restrict__ T, const double* __restrict__ Phi,
     const double* __restrict__ cscale, const double* __restrict__ rpg, double* qloc, double* vloc) {
   extern __shared__ double sm[];
   const int n = G.nG_pad, nc = G.nc_pad, nb = (n + 31) / 32, nr = nb * 32;
   constexpr int NW = kG1LThreads / 32;
   double* rho = sm;                       // nr
-  double* pd = rho + nr;                  // [nb][nr] direct partials
-  double* pt = pd + (size_t)nb * nr;      // nr transposed partials
-  double* tb = pt + nr;                   // per warp 32 x 33
+  double* pt = rho + nr;                  // nr transposed partials
+  double* tb = pt + nr;                   // per warp 32 x 33: lane's transposed accumulators
+  double* pd = tb + NW * 32 * 33;         // direct partials of block column J: rows >= 32 J
+  auto pdo = [&](int J) { return (size_t)J * nr - 16 * J * (J - 1) - 32 * J; };
   const int sub = G.s_lo + blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const long long so = (long long)sub * n;
@@ -531,20 +533,26 @@ __global__ void __launch_bounds__(kG1LThreads, 1) local_gamma1_lower_kernel(
   __syncthreads();
   const double c = cscale[sub];
   const double* ph = Phi + (long long)sub * n * nc;
-  for (int k = warp; k < nc; k += NW) {
+  for (int k = warp; k < nc; k += NW) {  // all of a column's loads in flight at once
+    double a[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int s = lane + 32 * i;
+      a[i] = s < n ? ph[s + (long long)k * n] : 0.0;
+    }
     double acc = 0.0;
-    for (int s = lane; s < n; s += 32) acc += ph[s + (long long)k * n] * rho[s];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc += a[i] * rho[min(lane + 32 * i, nr - 1)];
     acc = warp_sum(acc);
     if (lane == 0) qloc[(long long)sub * nc + k] = c * acc;
   }
   const double* Ts = T + (long long)sub * n * n;
-  double* mtb = tb + warp * 32 * 33;
+  double* mtb = tb + warp * 32 * 33 + lane * 33;
   for (int round = 0; round * NW < nb; ++round) {
     const int J = round * NW + ((round & 1) ? NW - 1 - warp : warp);
     if (J >= nb) continue;
-    double p[32];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) p[k] = 0.0;
+    for (int k = 0; k < 32; ++k) mtb[k] = 0.0;
     for (int I = J; I < nb; ++I) {
       const int r = 32 * I + lane;
       double t[32];
@@ -553,39 +561,30 @@ __global__ void __launch_bounds__(kG1LThreads, 1) local_gamma1_lower_kernel(
         const int col = 32 * J + k;
         t[k] = (r < n && col < n) ? Ts[r + (long long)col * n] : 0.0;
       }
-      double d0 = 0.0, d1 = 0.0;
       const double rr = rho[r];
-      if (I == J) {
+      double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const double tk = k <= lane ? t[k] : 0.0;
-          if (k & 1) d1 += tk * rho[32 * J + k];
-          else d0 += tk * rho[32 * J + k];
-          p[k] += (k < lane ? t[k] : 0.0) * rr;
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          if (k & 1) d1 += t[k] * rho[32 * J + k];
-          else d0 += t[k] * rho[32 * J + k];
-          p[k] += t[k] * rr;
-        }
+      for (int k = 0; k < 32; ++k) {
+        const double td = (I > J || k <= lane) ? t[k] : 0.0;  // diagonal block: lower incl.
+        const double tt = (I > J || k < lane) ? t[k] : 0.0;   // strictly lower
+        if (k & 1) d1 += td * rho[32 * J + k];
+        else d0 += td * rho[32 * J + k];
+        mtb[k] += tt * rr;
       }
-      pd[(size_t)J * nr + r] = d0 + d1;
+      pd[pdo(J) + r] = d0 + d1;
     }
-#pragma unroll
-    for (int k = 0; k < 32; ++k) mtb[lane * 33 + k] = p[k];
     __syncwarp();
     double sum = 0.0;
+    const double* col = tb + warp * 32 * 33 + lane;
 #pragma unroll 8
-    for (int i = 0; i < 32; ++i) sum += mtb[i * 33 + lane];
+    for (int i = 0; i < 32; ++i) sum += col[i * 33];
     pt[32 * J + lane] = sum;
     __syncwarp();
   }
   __syncthreads();
   for (int r = tid; r < n; r += kG1LThreads) {
     double y = pt[r];
-    for (int J = 0; J <= r / 32; ++J) y += pd[(size_t)J * nr + r];
+    for (int J = 0; J <= r / 32; ++J) y += pd[pdo(J) + r];
     vloc[so + r] = y;
   }
 }
