@@ -103,6 +103,12 @@ int bddc_spmv(bddc_ctx* ctx, const double* x_dev, double* y_dev, void* stream);
 int bddc_pcg(bddc_ctx* ctx, const double* b_dev, double* x_dev, double tol, int max_iters,
              double* alphas, double* betas, double* resid, bddc_pcg_report* rep, char* err,
              size_t errlen);
+/* setup (alpha_host, NULL: keep the resident alpha) + PCG with host buffers: replaces
+   build_bddc's numeric phase + pcg (bddc.py:393-523, krylov.py:31-92) as experiments.py
+   run() calls them; alpha / b uploads overlap the setup, x is downloaded at the end */
+int bddc_solve_host(bddc_ctx* ctx, const double* alpha_host, const double* b_host, double* x_host,
+                    double tol, int max_iters, double* alphas, double* betas, double* resid,
+                    bddc_pcg_report* rep, char* err, size_t errlen);
 int bddc_pcg_host(bddc_ctx* ctx, const double* b_host, double* x_host, double tol, int max_iters,
                   double* alphas, double* betas, double* resid, bddc_pcg_report* rep, char* err,
                   size_t errlen);

@@ -24,7 +24,7 @@ _vp = C.c_void_p
 
 EXPORTS = (
     "bddc_create", "bddc_destroy", "bddc_setup", "bddc_refactor", "bddc_apply", "bddc_harmonic",
-    "bddc_spmv", "bddc_pcg", "bddc_pcg_host", "bddc_get_stats", "bddc_sync",
+    "bddc_spmv", "bddc_pcg", "bddc_pcg_host", "bddc_solve_host", "bddc_get_stats", "bddc_sync",
     "bddc_kernel_launches_per_apply", "bddc_debug_copy", "bddc_launch_count",
     "bddc_event_record", "bddc_event_elapsed_ms", "bddc_profile", "bddc_profile_read",
     "bddc_nccl_unique_id", "bddc_comm_init_nccl", "bddc_comm_init_host", "bddc_partition_info",
@@ -92,6 +92,8 @@ def load(required: bool = True):
                              C.c_char_p, C.c_size_t]
     lib.bddc_pcg_host.argtypes = [_vp, _pd, _pd, _d, _i, _pd, _pd, _pd, C.POINTER(PcgReport),
                                   C.c_char_p, C.c_size_t]
+    lib.bddc_solve_host.argtypes = [_vp, _pd, _pd, _pd, _d, _i, _pd, _pd, _pd, C.POINTER(PcgReport),
+                                    C.c_char_p, C.c_size_t]
     lib.bddc_get_stats.argtypes = [_vp, C.POINTER(Stats)]
     lib.bddc_sync.argtypes = [_vp]
     lib.bddc_kernel_launches_per_apply.argtypes = [_vp]

@@ -263,6 +263,14 @@ struct Ctx {
   int device = 0;
   PhaseTimers prof;
   cudaStream_t stream = nullptr;
+  // host-buffer solve (bddc_solve_host): alpha arrives in slabs of subdomain rows on the copy
+  // stream; the first setup kernels of slab k wait on alpha_ev[k] (alpha_nslab = 0: resident)
+  cudaStream_t copy_stream = nullptr;
+  static constexpr int kMaxSlabs = 8;
+  cudaEvent_t alpha_ev[kMaxSlabs] = {};
+  cudaEvent_t b_ev = nullptr;
+  int alpha_nslab = 0;
+  int alpha_slab_sub[kMaxSlabs + 1] = {};
   Geometry geo{};
   int element = 0;
   int coarse_scaling = 0;  // 0 reference (Psi = Phi / s^2), 1 spec (Psi = Phi)

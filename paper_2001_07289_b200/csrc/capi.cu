@@ -403,6 +403,10 @@ void on_stream(bddc_ctx* h, void* stream, F&& f) {
 
 }  // namespace
 
+namespace bddc {
+bool schur2d_supported(const Geometry& G);
+}
+
 extern "C" {
 
 int bddc_create(int device, bddc_ctx** out) {
@@ -429,6 +433,12 @@ void bddc_destroy(bddc_ctx* h) {
   delete h->c.tp;
   h->c.tp = nullptr;
   if (h->c.h_scal) cudaFreeHost(h->c.h_scal);
+  if (h->c.copy_stream) {
+    cudaStreamSynchronize(h->c.copy_stream);
+    for (int k = 0; k < Ctx::kMaxSlabs; ++k) cudaEventDestroy(h->c.alpha_ev[k]);
+    cudaEventDestroy(h->c.b_ev);
+    cudaStreamDestroy(h->c.copy_stream);
+  }
   cudaStreamDestroy(h->c.stream);
   delete h;
 }
@@ -498,6 +508,72 @@ int bddc_pcg(bddc_ctx* h, const double* b, double* x, double tol, int max_iters,
       throw ApiError{5, buf};
     }
   });
+}
+
+// Setup + solve with host buffers (the reference's build_bddc + pcg pair, experiments.py
+// run): alpha goes up in slabs of subdomain rows on a copy stream and the 2D elimination of
+// slab k starts when its cells land; b goes up behind alpha while the setup runs; x comes
+// back after the solve. Same results as bddc_refactor + bddc_pcg_host.
+int bddc_solve_host(bddc_ctx* h, const double* alpha_host, const double* b_host, double* x_host,
+                    double tol, int max_iters, double* alphas, double* betas, double* resid,
+                    bddc_pcg_report* rep, char* err, size_t errlen) {
+  if (!h || !h->c.setup_done) return 1;
+  int code = guarded(err, errlen, [&] {
+    Ctx& c = h->c;
+    const Geometry& G = c.geo;
+    BDDC_CUDA(cudaSetDevice(c.device));
+    if (!c.copy_stream) {
+      BDDC_CUDA(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+      for (int k = 0; k < Ctx::kMaxSlabs; ++k)
+        BDDC_CUDA(cudaEventCreateWithFlags(&c.alpha_ev[k], cudaEventDisableTiming));
+      BDDC_CUDA(cudaEventCreateWithFlags(&c.b_ev, cudaEventDisableTiming));
+    }
+    // the copy stream must not overwrite buffers the context stream may still read
+    BDDC_CUDA(cudaEventRecord(c.b_ev, c.stream));
+    BDDC_CUDA(cudaStreamWaitEvent(c.copy_stream, c.b_ev, 0));
+    const int last = G.dim - 1;
+    const int rows = G.subs[last];
+    long long row_cells = G.blk[last];
+    for (int a = 0; a < last; ++a) row_cells *= G.cells[a];
+    const int per_row = G.nsub / rows;
+    c.alpha_nslab = 0;
+    if (alpha_host) {
+      const bool slab = bddc::schur2d_supported(G) && G.nblk > 0;
+      const int ns = slab ? std::min(4, rows) : 1;
+      for (int k = 0; k < ns; ++k) {
+        const int r0 = (int)((long long)rows * k / ns), r1 = (int)((long long)rows * (k + 1) / ns);
+        const long long c0 = r0 * row_cells, c1 = r1 * row_cells;
+        BDDC_CUDA(cudaMemcpyAsync(c.alpha + c0, alpha_host + c0, sizeof(double) * (c1 - c0),
+                                  cudaMemcpyHostToDevice, c.copy_stream));
+        BDDC_CUDA(cudaEventRecord(c.alpha_ev[k], c.copy_stream));
+        c.alpha_slab_sub[k] = r0 * per_row;
+        c.alpha_slab_sub[k + 1] = r1 * per_row;
+      }
+      if (slab) c.alpha_nslab = ns;
+      else BDDC_CUDA(cudaStreamWaitEvent(c.stream, c.alpha_ev[0], 0));
+    }
+    BDDC_CUDA(cudaMemcpyAsync(c.bbuf + G.f_lo, b_host + G.f_lo, sizeof(double) * (G.f_hi - G.f_lo),
+                              cudaMemcpyHostToDevice, c.copy_stream));
+    BDDC_CUDA(cudaEventRecord(c.b_ev, c.copy_stream));
+    try {
+      numeric_setup(h);
+    } catch (...) {
+      c.alpha_nslab = 0;
+      BDDC_CUDA(cudaStreamWaitEvent(c.stream, c.b_ev, 0));
+      throw;
+    }
+    c.alpha_nslab = 0;
+    BDDC_CUDA(cudaStreamWaitEvent(c.stream, c.b_ev, 0));
+  });
+  if (code) return code;
+  code = bddc_pcg(h, h->c.bbuf, h->c.xbuf, tol, max_iters, alphas, betas, resid, rep, err, errlen);
+  int code2 = guarded(err, code ? 0 : errlen, [&] {
+    const Geometry& G = h->c.geo;
+    BDDC_CUDA(cudaMemcpyAsync(x_host + G.fo_lo, h->c.xbuf + G.fo_lo, sizeof(double) * (G.fo_hi - G.fo_lo),
+                              cudaMemcpyDeviceToHost, h->c.stream));
+    BDDC_CUDA(cudaStreamSynchronize(h->c.stream));
+  });
+  return code ? code : code2;
 }
 
 int bddc_pcg_host(bddc_ctx* h, const double* b_host, double* x_host, double tol, int max_iters,

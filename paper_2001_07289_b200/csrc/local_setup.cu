@@ -405,6 +405,19 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
       BMat Rb{E, eS, G.nI_pad}, Hb{E2, eS, G.nI_pad};
       gemm_batched(true, false, G.nG_pad, G.nG_pad, G.nI_pad, -1.0, Rb, Hb, 0.0, LSb, cnt, s, true, 0, true, klo);
     }
+    // host-buffer path: alpha arrives in slabs; the 2D on-chip elimination of slab k starts as
+    // soon as its cells have landed (assembly + W recursion + Schur kernels per slab)
+    if (fused2d && c.alpha_nslab > 0 && sub0 == G.s_lo && cnt == G.s_hi - G.s_lo) {
+      PhaseScope ps(c.prof, "setup.schur", s);
+      for (int k = 0; k < c.alpha_nslab; ++k) {
+        const int sa = std::max(sub0, c.alpha_slab_sub[k]), sb = std::min(sub0 + cnt, c.alpha_slab_sub[k + 1]);
+        BDDC_CUDA(cudaStreamWaitEvent(s, c.alpha_ev[k], 0));
+        if (sa >= sb) continue;
+        { assemble_local_kernel<2, false><<<sb - sa, 256, 0, s>>>(G, c.alpha, c.lt, sa, Wd, Wo, E, c.LS, c.diag_s); BDDC_COUNT(); }
+        BDDC_LAUNCH_CHECK();
+        if (!schur2d(c, sa, sb - sa, Wd, Wo, E, s)) throw CudaError("schur2d: unsupported geometry");
+      }
+    } else {
     // 1. assembly
     c.prof.begin("setup.assemble", s);
     if (fused3d)
@@ -452,6 +465,7 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
     gemm_batched(true, false, G.nG_pad, G.nG_pad, G.nI_pad, -1.0, Eb, Eb, 1.0, LSb, cnt, s);
     c.prof.end("setup.SG", s);
     }
+    }  // alpha slabs
     // 4. S_K = S_Gamma + s C^T C; Cholesky
     c.prof.begin("setup.SK", s);
     { add_ctc_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, c.diag_s, c.LS); BDDC_COUNT(); }
