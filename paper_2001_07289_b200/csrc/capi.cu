@@ -539,9 +539,14 @@ int bddc_solve_host(bddc_ctx* h, const double* alpha_host, const double* b_host,
     c.alpha_nslab = 0;
     if (alpha_host) {
       const bool slab = bddc::schur2d_supported(G) && G.nblk > 0;
-      const int ns = slab ? std::min(4, rows) : 1;
+      // two halves: the second lands while the first is eliminated (measured on cfg2: 4 or 8
+      // slabs, or a smaller first slab, cost more in kernel tails than they hide)
+      double first = 0.5;
+      if (const char* e = getenv("BDDC_ALPHA_FIRST")) first = atof(e);
+      const int ns = slab && rows >= 4 && first > 0.0 && first < 1.0 ? 2 : 1;
+      const int rsplit = std::max(1, (int)(rows * first));
       for (int k = 0; k < ns; ++k) {
-        const int r0 = (int)((long long)rows * k / ns), r1 = (int)((long long)rows * (k + 1) / ns);
+        const int r0 = k == 0 ? 0 : rsplit, r1 = (ns == 1 || k == 1) ? rows : rsplit;
         const long long c0 = r0 * row_cells, c1 = r1 * row_cells;
         BDDC_CUDA(cudaMemcpyAsync(c.alpha + c0, alpha_host + c0, sizeof(double) * (c1 - c0),
                                   cudaMemcpyHostToDevice, c.copy_stream));
