@@ -255,7 +255,12 @@ struct BtT {
   static constexpr int TM = M * (M + 1) / 2;
   static constexpr int MB = M * NBO;
   static constexpr int STAGE = TM + MB;  // both even (M % 8 == 0): 16-byte aligned stages
-  static __host__ __device__ int per_warp(int nI) { return 2 + 2 * STAGE + nI + M; }
+  // planes in flight per warp (NS) and warps per CTA (W): deeper prefetch for the small 2D
+  // planes, more warps (latency hiding) for the large 3D ones; both fill the shared memory
+  static constexpr int NS = M <= 32 ? 3 : 2;
+  static constexpr int W = M <= 32 ? 5 : 7;
+  static constexpr int NB = (NS + 1) & ~1;  // mbarrier slots (keeps the stages 16-byte aligned)
+  static __host__ __device__ int per_warp(int nI) { return NB + NS * STAGE + nI + M; }
 };
 
 template <int M, int R>
@@ -283,31 +288,31 @@ __device__ __forceinline__ void bt_gemv_t(const double* __restrict__ pk, const d
 }
 
 template <int M, int NBO>
-__global__ void __launch_bounds__(32 * kBtWarps) bt_solve_t_kernel(Geometry G, LocalTables lt,
+__global__ void __launch_bounds__(32 * BtT<M, NBO>::W) bt_solve_t_kernel(Geometry G, LocalTables lt,
                                                                    const double* __restrict__ LI,
                                                                    const double* __restrict__ in,
                                                                    double* __restrict__ out) {
   using T = BtT<M, NBO>;
-  constexpr int R = T::R;
+  constexpr int R = T::R, NS = T::NS;
   extern __shared__ __align__(16) double sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nI = G.nI_pad, nblk = G.nblk;
   double* wb = sm + warp * T::per_warp(nI);
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(wb);
-  double* stg = wb + 2;
-  double* y = stg + 2 * T::STAGE;
+  double* stg = wb + T::NB;
+  double* y = stg + NS * T::STAGE;
   double* tv = y + nI;
-  const int sub = G.s_lo + blockIdx.x * kBtWarps + warp;
+  const int sub = G.s_lo + blockIdx.x * T::W + warp;
   if (sub >= G.s_hi) return;
   if (lane == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+#pragma unroll
+    for (int q = 0; q < NS; ++q) mbar_init(&bar[q], 1);
     mbar_fence_init();
   }
   __syncwarp();
   const double* li = LI + (long long)sub * G.li_stride;
   const double* bc = li + (long long)nblk * T::TM;
-  unsigned ph0 = 0, ph1 = 0;
+  unsigned ph = 0;  // parity bit per stage
   auto issue = [&](int jw, int jb, int st) {  // plane jw's W (+ coupling rows of plane jb)
     if (lane == 0) {
       double* dst = stg + st * T::STAGE;
@@ -317,10 +322,12 @@ __global__ void __launch_bounds__(32 * kBtWarps) bt_solve_t_kernel(Geometry G, L
     }
   };
   auto wait = [&](int st) {
-    if (st == 0) { mbar_wait(&bar[0], ph0); ph0 ^= 1u; }
-    else { mbar_wait(&bar[1], ph1); ph1 ^= 1u; }
+    mbar_wait(&bar[st], (ph >> st) & 1u);
+    ph ^= 1u << st;
   };
-  if (nblk > 0) issue(0, -1, 0);
+#pragma unroll
+  for (int q = 0; q < NS - 1; ++q)
+    if (q < nblk) issue(q, q > 0 ? q : -1, q);
   // gather: free dof of interior row rr = base + rel[rr]
   int p[3];
   sub_coords(G, sub, p);
@@ -355,8 +362,8 @@ __global__ void __launch_bounds__(32 * kBtWarps) bt_solve_t_kernel(Geometry G, L
   double hv[R];
   // ---- forward: h_j = W_j (b_j - B_j h_{j-1}) ----
   for (int j = 0; j < nblk; ++j) {
-    const int st = j & 1;
-    if (j + 1 < nblk) issue(j + 1, j + 1, st ^ 1);
+    const int st = j % NS;
+    if (j + NS - 1 < nblk) issue(j + NS - 1, j + NS - 1, (j + NS - 1) % NS);
     wait(st);
     const double* pk = stg + st * T::STAGE;
     const double* bj = pk + T::TM;
@@ -381,10 +388,12 @@ __global__ void __launch_bounds__(32 * kBtWarps) bt_solve_t_kernel(Geometry G, L
     __syncwarp();
   }
   // ---- backward: x_j = h_j - W_j (B_{j+1}^T x_{j+1}) ----
-  if (nblk > 1) issue(nblk - 2, nblk - 1, 0);
+#pragma unroll
+  for (int q = 0; q < NS - 1; ++q)
+    if (nblk - 2 - q >= 0) issue(nblk - 2 - q, nblk - 1 - q, q);
   for (int j = nblk - 2, it = 0; j >= 0; --j, ++it) {
-    const int st = it & 1;
-    if (j > 0) issue(j - 1, j, st ^ 1);
+    const int st = it % NS;
+    if (j - (NS - 1) >= 0) issue(j - (NS - 1), j - (NS - 2), (it + NS - 1) % NS);
     wait(st);
     const double* pk = stg + st * T::STAGE;
     const double* bn = pk + T::TM;  // coupling rows of plane j + 1
@@ -417,15 +426,15 @@ template <int M, int NBO>
 bool launch_bt_t(const Geometry& G, const LocalTables& lt, const double* LI, const double* in, double* out,
                  cudaStream_t s) {
   if (G.m_pad != M || G.nbo != NBO || G.Tm != BtT<M, NBO>::TM) return false;
-  const size_t smem = sizeof(double) * BtT<M, NBO>::per_warp(G.nI_pad) * kBtWarps;
+  const size_t smem = sizeof(double) * BtT<M, NBO>::per_warp(G.nI_pad) * BtT<M, NBO>::W;
   if (smem > 227 * 1024) return false;
   static size_t attr = 0;
   if (smem > attr) {
     BDDC_CUDA(cudaFuncSetAttribute(bt_solve_t_kernel<M, NBO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
-  const int grid = ceil_div(G.s_hi - G.s_lo, kBtWarps);
-  bt_solve_t_kernel<M, NBO><<<grid, 32 * kBtWarps, smem, s>>>(G, lt, LI, in, out);
+  const int grid = ceil_div(G.s_hi - G.s_lo, BtT<M, NBO>::W);
+  bt_solve_t_kernel<M, NBO><<<grid, 32 * BtT<M, NBO>::W, smem, s>>>(G, lt, LI, in, out);
   BDDC_COUNT();
   BDDC_LAUNCH_CHECK();
   return true;

@@ -19,6 +19,20 @@ __device__ __forceinline__ long long cell_id(const Geometry& G, int c0, int c1, 
 
 __device__ __forceinline__ void free_coords(const Geometry& G, long long f, int& g0, int& g1,
                                             int& g2) {
+  if (G.n < (1LL << 31)) {  // 32-bit division (the 64-bit one is a long software sequence)
+    unsigned u = (unsigned)f;
+    const unsigned q = u / (unsigned)G.nfree[0];
+    g0 = (int)(u - q * (unsigned)G.nfree[0]) + 1;
+    if (G.dim == 3) {
+      const unsigned q2 = q / (unsigned)G.nfree[1];
+      g1 = (int)(q - q2 * (unsigned)G.nfree[1]) + 1;
+      g2 = (int)q2 + 1;
+    } else {
+      g1 = (int)q + 1;
+      g2 = 0;
+    }
+    return;
+  }
   g0 = (int)(f % G.nfree[0]) + 1;
   f /= G.nfree[0];
   if (G.dim == 3) {
