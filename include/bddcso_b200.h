@@ -11,6 +11,8 @@
  *   bddc_harmonic  <- harmonic_extension(bddc, g) / BddcOperator._harmonic bddc.py:382-390, 530
  *   bddc_spmv      <- SparseSym.matvec / `A @ v` in run()                   linalg.py:79, experiments.py:232
  *   bddc_pcg       <- pcg(lambda v: A @ v, op.apply, b, tol, max_iters)    krylov.py:31-92
+ *   bddc_solve_host<- build_bddc numeric phase + pcg from host arrays, as   experiments.py:207, 231
+ *                     run() calls them (uploads overlapped with the setup)
  *   bddc_dense_*   <- spd_factor / saddle_factor / their solves            linalg.py:117-212
  *
  * Streams: `stream` is a cudaStream_t (NULL = the legacy default stream); work is ordered
@@ -104,7 +106,7 @@ int bddc_pcg(bddc_ctx* ctx, const double* b_dev, double* x_dev, double tol, int 
              double* alphas, double* betas, double* resid, bddc_pcg_report* rep, char* err,
              size_t errlen);
 /* setup (alpha_host, NULL: keep the resident alpha) + PCG with host buffers: replaces
-   build_bddc's numeric phase + pcg (bddc.py:393-523, krylov.py:31-92) as experiments.py
+   build_bddc's numeric phase + pcg (bddc.py:393-523, krylov.py:31-92) as experiments.py:207,231
    run() calls them; alpha / b uploads overlap the setup, x is downloaded at the end */
 int bddc_solve_host(bddc_ctx* ctx, const double* alpha_host, const double* b_host, double* x_host,
                     double tol, int max_iters, double* alphas, double* betas, double* resid,
