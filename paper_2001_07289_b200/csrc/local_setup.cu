@@ -44,7 +44,45 @@ __global__ void __launch_bounds__(256) assemble_local_kernel(Geometry G, const d
   constexpr int NOFF = DIM == 3 ? 27 : 9;
   double dsum = 0.0;
   int nfree_loc = 0;
-  const int total = G.nloc_nodes * NOFF;
+  if (!DENSE) {
+    // A_GG only: the couplings of the surface slots among themselves, then the diagonal of
+    // every local node for s_i (interior couplings are generated on chip by the fused kernels)
+    const int tot1 = G.nG * NOFF;
+    for (int idx = threadIdx.x; idx < tot1 + G.nloc_nodes; idx += blockDim.x) {
+      if (idx < tot1) {
+        const int slot = idx / NOFF, o = idx % NOFF;
+        const int node = lt.slot_node[slot];
+        int a[3], d[3] = {o % 3 - 1, (o / 3) % 3 - 1, DIM == 3 ? o / 9 - 1 : 0};
+        local_coords(G, node, a);
+        const int bn[3] = {a[0] + d[0], a[1] + d[1], a[2] + d[2]};
+        if (bn[0] < 0 || bn[0] > G.blk[0] || bn[1] < 0 || bn[1] > G.blk[1]) continue;
+        if (DIM == 3 && (bn[2] < 0 || bn[2] > G.blk[2])) continue;
+        const int nb = bn[0] + (G.blk[0] + 1) * (bn[1] + (G.blk[1] + 1) * bn[2]);
+        const int cb = lt.node_code[nb];
+        if (cb >= 0) continue;  // interior neighbour: A_IG, generated on chip
+        const long long pos = slot + (long long)(-cb - 1) * G.nG_pad;
+        if (local_to_free(G, p, a) < 0 || local_to_free(G, p, bn) < 0) {
+          if (node == nb) {
+            if (ADD) ls[pos] += 1.0;
+            else ls[pos] = 1.0;
+          }
+          continue;
+        }
+        const double v = local_coef<DIM>(G, alpha, p, a, d);
+        if (ADD) ls[pos] += v;
+        else ls[pos] = v;
+      } else {
+        const int node = idx - tot1;
+        int a[3];
+        local_coords(G, node, a);
+        if (local_to_free(G, p, a) < 0) continue;
+        const int d0[3] = {0, 0, 0};
+        dsum += fabs(local_coef<DIM>(G, alpha, p, a, d0));
+        nfree_loc += 1;
+      }
+    }
+  }
+  const int total = DENSE ? G.nloc_nodes * NOFF : 0;
   for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
     const int node = idx / NOFF, o = idx % NOFF;
     int a[3], d[3] = {o % 3 - 1, (o / 3) % 3 - 1, DIM == 3 ? o / 9 - 1 : 0};
@@ -483,6 +521,50 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
       }
     }
     BMat Xb{X, phS, G.nG_pad};
+    // T deferred into the dataflow coarse factorization (all subdomains in one chunk)
+    const bool defer_t = c.lt_fusable && c.fp.n_coarse > 0 && sub0 == G.s_lo && cnt == G.s_hi - G.s_lo;
+    c.lt_defer = LtArgs{};
+    if (G.nc_pad > 0 && !defer_t) {
+      // 5b/7 through Z = S_K^{-1}: S_C = G^T G with G = L^{-1} C^T (a Gram matrix: stays SPD
+      // at 1e12 coefficient contrast, where C Z C^T does not), W = Z C^T (a gather, no GEMM),
+      // Phi = W S_C^{-1}, T = Z - Phi W^T (= S_K^{-1} - Phi S_C Phi^T). Z and then T in LS.
+      BMat PHb{PH, phS, G.nG_pad};
+      BMat SCb{SC, scS, G.nc_pad};
+      BMat SCib{SCi, scS, G.nc_pad};
+      {
+        PhaseScope pphi(c.prof, "setup.Phi", s);
+        BMat Yb{Y, phS, G.nG_pad};
+        const bool gathered = g_gather(G, sub0, cnt, c.st, LIv, lsS, Y, phS, s);  // G
+        if (!gathered) {
+          BDDC_CUDA(cudaMemsetAsync(PH, 0, sizeof(double) * cnt * phS, s));
+          { build_ct_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, c.Phi); BDDC_COUNT(); }  // C^T
+          BDDC_LAUNCH_CHECK();
+          gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nG_pad, 1.0, LIb, PHb, 0.0, Yb, cnt, s, false, 1);
+        }
+        gemm_batched(true, false, G.nc_pad, G.nc_pad, G.nG_pad, 1.0, Yb, Yb, 0.0, SCb, cnt, s);  // S_C
+        { sc_pad_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, SC); BDDC_COUNT(); }
+        BDDC_LAUNCH_CHECK();
+        gemm_batched(true, false, G.nG_pad, G.nG_pad, G.nG_pad, 1.0, LIb, LIb, 0.0, LSb, cnt, s, true, 2, true);  // Z
+        if (gathered) g_gather(G, sub0, cnt, c.st, LS, lsS, X, phS, s);  // W = Z C^T
+        else gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nG_pad, 1.0, LSb, PHb, 0.0, Xb, cnt, s);
+        potrf_batched(SCb, G.nc_pad, G.nc_pad, cnt, nullptr, c.tinv, s);
+        const int ncb = ceil_div(G.nc_pad, kTile);
+        BMat LCi{c.tinv, (long long)ncb * kTileInvStride, kTile};  // L_C^{-1} (one tile)
+        if (ncb > 1) {
+          LCi = BMat{P, scS, G.nc_pad};
+          if (!trtri_from_tiles(SCb, G.nc_pad, LCi, cnt, c.tinv, s)) throw CudaError("S_C too large");
+        }
+        gemm_batched(true, false, G.nc_pad, G.nc_pad, G.nc_pad, 1.0, LCi, LCi, 0.0, SCib, cnt, s);  // S_C^{-1}
+        gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nc_pad, 1.0, Xb, SCib, 0.0, PHb, cnt, s);   // Phi
+        { finish_local_kernel<<<cnt, 256, 0, s>>>(G, sub0, c.coarse_scaling, c.diag_s, c.st, c.cscale, SCi,
+                                                c.Sloc); BDDC_COUNT(); }
+        BDDC_LAUNCH_CHECK();
+      }
+      PhaseScope pt(c.prof, "setup.T", s);
+      gemm_batched(false, true, G.nG_pad, G.nG_pad, G.nc_pad, -1.0, PHb, Xb, 1.0, LSb, cnt, s, true, 0,
+                   !t_lower_only(G));
+      continue;
+    }
     if (G.nc_pad > 0) {
       PhaseScope pphi(c.prof, "setup.Phi", s);
       // 5b. G = L^{-1} C^T, S_C = G^T G = L_C L_C^T, Q = G L_C^{-T} (orthonormal columns),
@@ -523,8 +605,7 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
     //    = L^{-T} L^{-1} - V V^T (symmetric; the apply's local Neumann solve is one GEMV).
     //    With all subdomains in one chunk it is deferred into the dataflow coarse
     //    factorization, whose schedule runs its tiles on the CTAs the critical path leaves idle.
-    c.lt_defer = LtArgs{};
-    if (c.lt_fusable && c.fp.n_coarse > 0 && sub0 == G.s_lo && cnt == G.s_hi - G.s_lo) {
+    if (defer_t) {
       c.lt_defer = LtArgs{LIv, X, c.LS, lsS, phS, G.nG_pad, G.nc_pad, sub0, 1};
       continue;
     }
