@@ -273,6 +273,24 @@ static void tile_solve_gemm(TrsmKind kind, BMat Vinv, int nb, BMat B, int nother
 void potrf_batched(BMat A, int n, int npiv, int count, int* info, double* scratch, cudaStream_t s) {
   // the inverse of diagonal tile kb stays in scratch slot kb (trsm_batched's layout)
   const long long sInv = (long long)ceil_div(npiv, kTile) * kTileInvStride;
+  if (npiv == n) {
+    // left-looking: block column k is updated once with all earlier panels (one GEMM of
+    // inner dimension k instead of k / 64 rank-64 read-modify-writes of the trailing matrix)
+    for (int k = 0; k < n; k += kTile) {
+      const int nb = std::min(kTile, n - k);
+      double* inv = scratch + (k / kTile) * kTileInvStride;
+      if (k > 0)  // A[k:, k:k+nb] -= L[k:, 0:k] L[k:k+nb, 0:k]^T (lower part of the diagonal tile)
+        gemm_batched(false, true, n - k, nb, k, -1.0, A.at(k, 0), A.at(k, 0), 1.0, A.at(k, k), count, s, true);
+      TileArgs t;
+      t.L = A.p + k + (long long)k * A.ld; t.sL = A.stride; t.ldl = A.ld;
+      t.n = nb; t.count = count; t.offset = k; t.info = info;
+      t.inv = inv; t.sInv = sInv;
+      potrf_tile(t, s);
+      const int rest = n - k - nb;
+      if (rest > 0) tile_solve_gemm(TRSM_RLT, BMat{inv, sInv, kTile}, nb, A.at(k + nb, k), rest, count, s);
+    }
+    return;
+  }
   for (int k = 0; k < npiv; k += kTile) {
     const int nb = std::min(kTile, npiv - k);
     double* inv = scratch + (k / kTile) * kTileInvStride;

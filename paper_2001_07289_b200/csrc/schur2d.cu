@@ -290,28 +290,21 @@ __global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, i
 #pragma unroll
   for (int q = 0; q < SYRK_PER_WARP; ++q) acc[q][0] = acc[q][1] = 0.0;
   int nprev = 0;
-  // packed W_j and the coupling stencil are loaded one plane ahead into registers, so their
-  // HBM latency overlaps the previous plane's DMMA work
-  constexpr int TM = M * (M + 1) / 2;
-  constexpr int NWL = (TM + kSchurThreads - 1) / kSchurThreads;
-  double wv[NWL], bv;
-  auto load_plane = [&](int jj, double (&w)[NWL], double& b) {
-#pragma unroll
-    for (int u = 0; u < NWL; ++u) {
-      const int e = tid + u * kSchurThreads;
-      w[u] = (jj < G.nblk && e < TM) ? li[(long long)jj * G.Tm + e] : 0.0;
-    }
-    b = (jj < G.nblk && tid < M * nbo) ? bcg[(long long)jj * M * nbo + tid] : 0.0;
-  };
-  load_plane(0, wv, bv);
   for (int j = 0; j < G.nblk; ++j) {
     const int na = G.nact[j];           // active columns (multiple of 8)
     const int nat = na / 8;
-    double wn[NWL], bn;
-    load_plane(j + 1, wn, bn);
-    // W_j (unpack) and the coupling stencil; A_IG rows (active columns) come from the
-    // element stencil
+    // W_j (unpack) and the coupling stencil: every global load of the plane is issued before
+    // the first shared-memory store; A_IG rows (active columns) come from the element stencil
     {
+      constexpr int TM = M * (M + 1) / 2;
+      constexpr int NWL = (TM + kSchurThreads - 1) / kSchurThreads;
+      double wv[NWL];
+#pragma unroll
+      for (int u = 0; u < NWL; ++u) {
+        const int e = tid + u * kSchurThreads;
+        wv[u] = e < TM ? li[(long long)j * G.Tm + e] : 0.0;
+      }
+      const double bv = tid < M * nbo ? bcg[(long long)j * M * nbo + tid] : 0.0;
       for (int r = warp; r < M; r += NW)
         for (int cc = lane; cc < na; cc += 32) sm[O_R + r * EP + cc] = 0.0;
 #pragma unroll
@@ -384,9 +377,6 @@ __global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, i
       }
     }
     nprev = na;
-#pragma unroll
-    for (int u = 0; u < NWL; ++u) wv[u] = wn[u];
-    bv = bn;
     __syncthreads();
   }
   // S_G = A_GG - S_acc (full symmetric)
