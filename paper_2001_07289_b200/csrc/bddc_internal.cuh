@@ -37,6 +37,10 @@ struct Geometry {
   int Tm;
   int nact[64];  // 2D: active interface columns (prefix) of R_j / H_j at plane j
   int nbo;
+  // structurally nonzero neighbour offsets of the assembled stencil (excluding the node
+  // itself): code = (dx+1) + 3 (dy+1) + 9 (dz+1); P1: 4 (2D) / 6 (3D), Q1: 8 / 26
+  int nnb;
+  int nb_code[26];
   int bo_dx[9], bo_dy[9];
   long long li_stride;
   // this rank's slab of the subdomain lattice (last axis); world = 1: everything

@@ -238,6 +238,23 @@ void do_setup(bddc_ctx* h, const bddc_setup_desc* d) {
   if (G.nG_pad > 1024 || G.nG_pad % 8 || G.nc_pad > 1024 || G.nc_pad % 8)
     throw ApiError{1, "interface / constraint padding out of range"};
   for (int i = 0; i < G.npe * G.npe; ++i) G.K[i] = d->elem_K[i];
+  // structurally nonzero neighbour offsets: some corner pair (s, t) of an element with
+  // K[s][t] != 0 and t - s = the offset
+  G.nnb = 0;
+  for (int o = 0; o < 27; ++o) {
+    const int dd[3] = {o % 3 - 1, (o / 3) % 3 - 1, o / 9 - 1};
+    if (o == 13 || (G.dim == 2 && dd[2] != 0)) continue;
+    bool used = false;
+    for (int s0 = 0; s0 < G.npe && !used; ++s0)
+      for (int t0 = 0; t0 < G.npe && !used; ++t0) {
+        if (G.K[s0 * G.npe + t0] == 0.0) continue;
+        bool match = true;
+        for (int ax = 0; ax < G.dim; ++ax)
+          if (((t0 >> ax) & 1) - ((s0 >> ax) & 1) != dd[ax]) match = false;
+        used = match;
+      }
+    if (used) G.nb_code[G.nnb++] = o;
+  }
   // structurally nonzero couplings from a plane to the previous one (last axis -1)
   G.nbo = 0;
   for (int dy = -1; dy <= 1; ++dy)

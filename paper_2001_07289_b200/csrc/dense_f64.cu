@@ -310,20 +310,20 @@ void potrf_batched(BMat A, int n, int npiv, int count, int* info, double* scratc
 }
 
 namespace {
-// Linv diagonal blocks <- the kept tile inverses (64 x 64, ld 64); zero the upper block
+// Linv diagonal blocks <- the kept tile inverses (64 x 64, ld 64, zero upper part). The
+// blocks above the diagonal are left unwritten: every consumer skips them (triangular K
+// ranges, the column gather starts at the column's diagonal block).
 __global__ void place_diag_inv_kernel(const double* __restrict__ scr, long long sInv, int n, double* Linv,
                                       long long sL, int ldl) {
   const int b = blockIdx.x;
   const double* inv = scr + b * sInv;
   double* L = Linv + b * sL;
   const int nb = (n + kTile - 1) / kTile;
-  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
-    const int i = idx % n, j = idx / n;
-    const int bi = i / kTile, bj = j / kTile;
-    if (bi == bj) L[i + (long long)j * ldl] = inv[bi * kTileInvStride + (i - bi * kTile) + (j - bj * kTile) * kTile];
-    else if (bi < bj) L[i + (long long)j * ldl] = 0.0;
+  for (int idx = threadIdx.x; idx < nb * kTile * kTile; idx += blockDim.x) {
+    const int bi = idx / (kTile * kTile), e = idx % (kTile * kTile);
+    const int i = bi * kTile + e % kTile, j = bi * kTile + e / kTile;
+    if (i < n && j < n) L[i + (long long)j * ldl] = inv[bi * kTileInvStride + e];
   }
-  (void)nb;
 }
 }  // namespace
 

@@ -99,7 +99,8 @@ void gemm_batched(bool tA, bool tB, int M, int N, int K, double alpha, BMat A, B
                   double beta, BMat C, int count, cudaStream_t s, bool lower = false, int tri = 0,
                   bool mirror = false, const int* klo = nullptr);
 // L^{-1} of a batch of n x n lower factors (n <= 1024) from the diagonal-tile inverses left in
-// scratch by potrf_batched (blocked, one block row at a time); Linv is written in full (zero upper).
+// scratch by potrf_batched (blocked, one block row at a time). Written: the lower block
+// triangle (diagonal tiles with zero upper parts); the blocks above the diagonal are not.
 bool trtri_from_tiles(BMat L, int n, BMat Linv, int count, const double* scratch, cudaStream_t s);
 
 constexpr int kTile = 64;

@@ -305,7 +305,9 @@ __global__ void identity_kernel(double* B, int n, long long stride) {
 // G = L_S^{-1} C^T without a GEMM: C^T is one nonzero per constrained slot, so column k of
 // G is the coefficient-weighted sum of the columns of L_S^{-1} at the slots of constraint k
 // (ascending slot order: deterministic). Warp per constraint; lane owns rows lane + 32 r.
-template <int RPL>
+// LOWER: LIv is L^{-1} with only its diagonal 64-tiles' upper parts zeroed (the blocks above
+// them are never written): column s is read from row 64 floor(s / 64) on.
+template <int RPL, bool LOWER>
 __global__ void __launch_bounds__(256) g_gather_kernel(Geometry G, int sub0, SubTables st,
                                                        const double* __restrict__ LIv, long long sL,
                                                        double* __restrict__ X, long long sX) {
@@ -331,10 +333,11 @@ __global__ void __launch_bounds__(256) g_gather_kernel(Geometry G, int sub0, Sub
         mask &= mask - 1;
         const double c = cf[s];
         const double* col = li + (long long)s * n;
+        const int i0 = LOWER ? (s & ~63) : 0;
 #pragma unroll
         for (int r = 0; r < RPL; ++r) {
           const int i = lane + 32 * r;
-          if (i < n) acc[r] += c * col[i];
+          if (i < n && i >= i0) acc[r] += c * col[i];
         }
       }
     }
@@ -347,10 +350,13 @@ __global__ void __launch_bounds__(256) g_gather_kernel(Geometry G, int sub0, Sub
 }
 
 bool g_gather(const Geometry& G, int sub0, int cnt, const SubTables& st, const double* LIv, long long sL,
-              double* X, long long sX, cudaStream_t s) {
+              double* X, long long sX, cudaStream_t s, bool lower) {
   const int rpl = ceil_div(G.nG_pad, 32);
 #define BDDC_GG(R) \
-  if (rpl <= R) { g_gather_kernel<R><<<cnt, 256, 0, s>>>(G, sub0, st, LIv, sL, X, sX); BDDC_COUNT(); BDDC_LAUNCH_CHECK(); return true; }
+  if (rpl <= R) { \
+    if (lower) g_gather_kernel<R, true><<<cnt, 256, 0, s>>>(G, sub0, st, LIv, sL, X, sX); \
+    else g_gather_kernel<R, false><<<cnt, 256, 0, s>>>(G, sub0, st, LIv, sL, X, sX); \
+    BDDC_COUNT(); BDDC_LAUNCH_CHECK(); return true; }
   BDDC_GG(1) BDDC_GG(2) BDDC_GG(4) BDDC_GG(8) BDDC_GG(13) BDDC_GG(16)
 #undef BDDC_GG
   return false;
@@ -534,7 +540,7 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
       {
         PhaseScope pphi(c.prof, "setup.Phi", s);
         BMat Yb{Y, phS, G.nG_pad};
-        const bool gathered = g_gather(G, sub0, cnt, c.st, LIv, lsS, Y, phS, s);  // G
+        const bool gathered = g_gather(G, sub0, cnt, c.st, LIv, lsS, Y, phS, s, true);  // G
         if (!gathered) {
           BDDC_CUDA(cudaMemsetAsync(PH, 0, sizeof(double) * cnt * phS, s));
           { build_ct_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, c.Phi); BDDC_COUNT(); }  // C^T
@@ -545,13 +551,14 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
         { sc_pad_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, SC); BDDC_COUNT(); }
         BDDC_LAUNCH_CHECK();
         gemm_batched(true, false, G.nG_pad, G.nG_pad, G.nG_pad, 1.0, LIb, LIb, 0.0, LSb, cnt, s, true, 2, true);  // Z
-        if (gathered) g_gather(G, sub0, cnt, c.st, LS, lsS, X, phS, s);  // W = Z C^T
+        if (gathered) g_gather(G, sub0, cnt, c.st, LS, lsS, X, phS, s, false);  // W = Z C^T
         else gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nG_pad, 1.0, LSb, PHb, 0.0, Xb, cnt, s);
         potrf_batched(SCb, G.nc_pad, G.nc_pad, cnt, nullptr, c.tinv, s);
         const int ncb = ceil_div(G.nc_pad, kTile);
         BMat LCi{c.tinv, (long long)ncb * kTileInvStride, kTile};  // L_C^{-1} (one tile)
-        if (ncb > 1) {
+        if (ncb > 1) {  // L_C^{-1} in full: the S_C^{-1} product reads both triangles' blocks
           LCi = BMat{P, scS, G.nc_pad};
+          BDDC_CUDA(cudaMemsetAsync(P, 0, sizeof(double) * cnt * scS, s));
           if (!trtri_from_tiles(SCb, G.nc_pad, LCi, cnt, c.tinv, s)) throw CudaError("S_C too large");
         }
         gemm_batched(true, false, G.nc_pad, G.nc_pad, G.nc_pad, 1.0, LCi, LCi, 0.0, SCib, cnt, s);  // S_C^{-1}
@@ -573,7 +580,7 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
       BMat SCb{SC, scS, G.nc_pad};
       BMat Yb{Y, phS, G.nG_pad};
       BMat SCib{SCi, scS, G.nc_pad};
-      if (!g_gather(G, sub0, cnt, c.st, LIv, lsS, X, phS, s)) {
+      if (!g_gather(G, sub0, cnt, c.st, LIv, lsS, X, phS, s, true)) {
         BDDC_CUDA(cudaMemsetAsync(PH, 0, sizeof(double) * cnt * phS, s));
         { build_ct_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, c.Phi); BDDC_COUNT(); }
         BDDC_LAUNCH_CHECK();

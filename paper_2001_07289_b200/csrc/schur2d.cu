@@ -572,16 +572,15 @@ __global__ void __launch_bounds__(kRh3Threads, 2) rh3d_kernel(Geometry G, int su
   }
   for (int j = jmin; j < G.nblk; ++j) {
     {  // W_j unpacked (symmetric) and the coupling to plane j-1; R_j <- 0
-      constexpr int TM = M * (M + 1) / 2;
-      for (int e = tid; e < TM; e += kRh3Threads) {
-        const double q = 2.0 * M + 1.0;
-        int c = (int)((q - sqrt(q * q - 8.0 * e)) * 0.5);
-        if ((c + 1) * M - (c + 1) * c / 2 <= e) ++c;
-        if (c * M - c * (c - 1) / 2 > e) --c;
-        const int r = c + (e - (c * M - c * (c - 1) / 2));
-        const double v = li[(long long)j * G.Tm + e];
-        Wsm[r + c * P] = v;
-        Wsm[c + r * P] = v;
+      // 4 threads per column c walk its packed entries (column start c M - c (c - 1) / 2)
+      if (tid < 4 * M) {
+        const int c = tid >> 2, q = tid & 3;
+        const double* col = li + (long long)j * G.Tm + (c * M - c * (c - 1) / 2) - c;
+        for (int r = c + q; r < M; r += 4) {
+          const double v = col[r];
+          Wsm[r + c * P] = v;
+          Wsm[c + r * P] = v;
+        }
       }
       if (tid < M) bsh[tid] = bcg[(long long)j * M + tid];
       for (int idx = tid; idx < M * EP; idx += kRh3Threads) R[idx] = 0.0;
@@ -589,8 +588,8 @@ __global__ void __launch_bounds__(kRh3Threads, 2) rh3d_kernel(Geometry G, int su
     __syncthreads();
     // A_IG,j on the chunk: row r couples to the non-Dirichlet surface slots among its 26
     // neighbours (structurally zero couplings give 0)
-    for (int idx = tid; idx < G.m * 26; idx += kRh3Threads) {
-      const int r = idx / 26, o0 = idx % 26, o = o0 < 13 ? o0 : o0 + 1;  // skip the centre
+    for (int idx = tid; idx < G.m * G.nnb; idx += kRh3Threads) {
+      const int r = idx / G.nnb, o = G.nb_code[idx % G.nnb];
       int a[3];
       local_coords(G, lt.irow_node[j * M + r], a);
       const int d[3] = {o % 3 - 1, (o / 3) % 3 - 1, o / 9 - 1};

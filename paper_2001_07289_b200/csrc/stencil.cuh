@@ -44,11 +44,41 @@ __device__ __forceinline__ void free_coords(const Geometry& G, long long f, int&
   }
 }
 
+// Row g of A applied to x with 32-bit index arithmetic (cell and free-dof counts < 2^31):
+// the neighbour offsets are compile-time after unrolling, so each load is base + constant.
+template <int DIM>
+__device__ __forceinline__ double stencil_row32(const Geometry& G, const double* __restrict__ alpha,
+                                                const double* __restrict__ x, int g0, int g1, int g2) {
+  constexpr int NPE = 1 << DIM;
+  const int c0n = G.cells[0], c1n = G.cells[1], nf0 = G.nfree[0], nf1 = G.nfree[1];
+  const int fg = (g0 - 1) + nf0 * ((g1 - 1) + (DIM == 3 ? nf1 * (g2 - 1) : 0));
+  const int cg = g0 + c0n * (g1 + (DIM == 3 ? c1n * g2 : 0));
+  double acc = 0.0;
+#pragma unroll
+  for (int s = 0; s < NPE; ++s) {
+    const int sx = s & 1, sy = (s >> 1) & 1, sz = DIM == 3 ? (s >> 2) & 1 : 0;
+    const double a = __ldg(alpha + (cg - sx - c0n * (sy + (DIM == 3 ? c1n * sz : 0))));
+    double part = 0.0;
+#pragma unroll
+    for (int t = 0; t < NPE; ++t) {
+      const double k = G.K[s * NPE + t];
+      if (k == 0.0) continue;
+      const int dx = (t & 1) - sx, dy = ((t >> 1) & 1) - sy, dz = DIM == 3 ? ((t >> 2) & 1) - sz : 0;
+      if ((dx && (g0 + dx == 0 || g0 + dx == c0n)) || (dy && (g1 + dy == 0 || g1 + dy == c1n))) continue;
+      if (DIM == 3 && dz && (g2 + dz == 0 || g2 + dz == G.cells[2])) continue;
+      part += k * __ldg(x + (fg + dx + nf0 * (dy + (DIM == 3 ? nf1 * dz : 0))));
+    }
+    acc += a * part;
+  }
+  return acc;
+}
+
 // Row g of A applied to x (g is a free node).
 template <int DIM>
 __device__ __forceinline__ double stencil_row(const Geometry& G, const double* __restrict__ alpha,
                                               const double* __restrict__ x, int g0, int g1,
                                               int g2) {
+  if (G.n < (1LL << 30)) return stencil_row32<DIM>(G, alpha, x, g0, g1, g2);
   constexpr int NPE = 1 << DIM;
   double acc = 0.0;
 #pragma unroll
