@@ -195,7 +195,9 @@ __device__ __forceinline__ void gemm_tile(const double* A, int lda, const double
 // per-warp 8x8 scratch. The 8x8 diagonal blocks are factored / inverted in registers by one
 // warp with shuffles; panel solves, trailing updates and the inverse recursion are DMMA.8x8x4.
 constexpr int SP = kTile + 4;  // pitch = 4 mod 16 doubles: conflict-free 8x8x4 fragments
-constexpr int kFactSmemDoubles = 2 * kTile * SP + 128 + 8 * 64;  // S, X, 2 Dv, 8 warp tmps
+// S (factor in the lower triangle, off-diagonal blocks of the inverse X transposed in the
+// upper triangle), Xd (X's 8 diagonal 8x8 blocks), 2 Dv, 8 warp tmps: 43 KB, 5 tiles per SM
+constexpr int kFactSmemDoubles = kTile * SP + 8 * 64 + 128 + 8 * 64;
 
 // C(8x8) (+)= A(8x8) B(8x8) from shared memory; A(r,k)=A[r*ars+k*acs], B(k,c)=B[k*brs+c*bcs]
 __device__ __forceinline__ void mma8(double& c0, double& c1, const double* A, int ars, int acs,
@@ -210,9 +212,9 @@ __device__ __forceinline__ void mma8(double& c0, double& c1, const double* A, in
 // Returns the first failing local pivot or -1.
 // Warp-level Cholesky + inverse of the 8x8 diagonal block at k0 (lanes 0..7 = rows), in
 // registers: one rsqrt per pivot gives both the scaling and 1/L[c][c] for the inverse.
-// Writes the factor into S (FACTOR), the inverse into X's diagonal block and Dv (pitch 8).
+// Writes the factor into S (FACTOR), the inverse into Xd's block k0 / 8 and Dv (pitch 8).
 template <bool FACTOR>
-__device__ __forceinline__ void diag8(double* S, double* X, double* Dv, int k0, int lane,
+__device__ __forceinline__ void diag8(double* S, double* Xd, double* Dv, int k0, int lane,
                                       int* failed) {
   double row[8], rinv[8];
 #pragma unroll
@@ -255,7 +257,7 @@ __device__ __forceinline__ void diag8(double* S, double* X, double* Dv, int k0, 
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       Dv[r + lane * 8] = r >= lane ? x[r] : 0.0;
-      X[(k0 + r) + (k0 + lane) * SP] = r >= lane ? x[r] : 0.0;
+      Xd[k0 * 8 + r + lane * 8] = r >= lane ? x[r] : 0.0;
     }
   }
 }
@@ -265,9 +267,9 @@ __device__ __forceinline__ void diag8(double* S, double* X, double* Dv, int k0, 
 // warp 0 updates and factors diagonal block kb+1.
 template <bool FACTOR = true>
 __device__ __forceinline__ int potrf_trtri_tile(double* L, int ld, int n, double* inv, double* smem) {
-  double* S = smem;                  // factor
-  double* X = smem + kTile * SP;     // inverse
-  double* Dv = X + kTile * SP;       // 2 x (8x8) inverses of diagonal blocks (pitch 8)
+  double* S = smem;                  // factor (lower) | X^T off-diagonal blocks (upper)
+  double* Xd = smem + kTile * SP;    // X's diagonal 8x8 blocks (pitch 8)
+  double* Dv = Xd + 8 * 64;          // 2 x (8x8) inverses of diagonal blocks (pitch 8)
   __shared__ int failed;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int nw = nt >> 5;
@@ -292,14 +294,14 @@ __device__ __forceinline__ int potrf_trtri_tile(double* L, int ld, int n, double
   }
   __syncthreads();
   TILE_MARK(1);
-  if (warp == 0) diag8<FACTOR>(S, X, Dv, 0, lane, &failed);
+  if (warp == 0) diag8<FACTOR>(S, Xd, Dv, 0, lane, &failed);
   __syncthreads();
   TILE_MARK(2);
   for (int kb = 0; kb < nb8; ++kb) {
     const int k0 = kb * 8;
     if (!FACTOR) {
       if (kb + 1 < nb8) {
-        if (warp == 0) diag8<FACTOR>(S, X, Dv, k0 + 8, lane, &failed);
+        if (warp == 0) diag8<FACTOR>(S, Xd, Dv, k0 + 8, lane, &failed);
         __syncthreads();
       }
       continue;
@@ -325,7 +327,7 @@ __device__ __forceinline__ int potrf_trtri_tile(double* L, int ld, int n, double
       S[(I * 8 + g) + (I * 8 + 2 * t4) * SP] -= c0;
       S[(I * 8 + g) + (I * 8 + 2 * t4 + 1) * SP] -= c1;
       __syncwarp();
-      diag8<FACTOR>(S, X, Dv + ((kb + 1) & 1) * 64, I * 8, lane, &failed);
+      diag8<FACTOR>(S, Xd, Dv + ((kb + 1) & 1) * 64, I * 8, lane, &failed);
     }
     const int w0 = nw > 1 ? 1 : 0, ws = nw > 1 ? nw - 1 : 1;
     if (warp >= w0) {
@@ -343,20 +345,23 @@ __device__ __forceinline__ int potrf_trtri_tile(double* L, int ld, int n, double
     __syncthreads();
   }
   TILE_MARK(3);
-  // inverse recursion by block rows: X[i][k] = -X[i][i] sum_{m=k}^{i-1} L[i][m] X[m][k]
+  // inverse recursion by block rows: X[i][k] = -X[i][i] sum_{m=k}^{i-1} L[i][m] X[m][k];
+  // X block (m, k), m > k, lives transposed in S's (free) upper triangle: X[m8+r][k8+c] at
+  // S[(k8 + c) + (m8 + r) SP]
   double* tmp = Dv + 128 + warp * 64;  // per-warp 8x8 scratch
   for (int ib = 1; ib < nb8; ++ib) {
     for (int kb = warp; kb < ib; kb += nt >> 5) {
       double c0 = 0.0, c1 = 0.0;
-      for (int m = kb; m < ib; ++m)
-        mma8(c0, c1, S + ib * 8 + m * 8 * SP, 1, SP, X + m * 8 + kb * 8 * SP, 1, SP, lane);
+      mma8(c0, c1, S + ib * 8 + kb * 8 * SP, 1, SP, Xd + kb * 64, 1, 8, lane);
+      for (int m = kb + 1; m < ib; ++m)
+        mma8(c0, c1, S + ib * 8 + m * 8 * SP, 1, SP, S + kb * 8 + m * 8 * SP, SP, 1, lane);
       tmp[g + (2 * t4) * 8] = c0;
       tmp[g + (2 * t4 + 1) * 8] = c1;
       __syncwarp();
       double d0 = 0.0, d1 = 0.0;
-      mma8(d0, d1, X + ib * 8 + ib * 8 * SP, 1, SP, tmp, 1, 8, lane);
-      X[(ib * 8 + g) + (kb * 8 + 2 * t4) * SP] = -d0;
-      X[(ib * 8 + g) + (kb * 8 + 2 * t4 + 1) * SP] = -d1;
+      mma8(d0, d1, Xd + ib * 64, 1, 8, tmp, 1, 8, lane);
+      S[(kb * 8 + 2 * t4) + (ib * 8 + g) * SP] = -d0;
+      S[(kb * 8 + 2 * t4 + 1) + (ib * 8 + g) * SP] = -d1;
       __syncwarp();
     }
     __syncthreads();
@@ -371,7 +376,10 @@ __device__ __forceinline__ int potrf_trtri_tile(double* L, int ld, int n, double
   if (inv) {
     for (int idx = tid; idx < kTile * kTile; idx += nt) {
       const int i = idx & 63, j = idx >> 6;
-      inv[idx] = (i < n && j < n && i >= j) ? X[i + j * SP] : 0.0;
+      double v = 0.0;
+      if (i < n && j < n && i >= j)
+        v = (i >> 3) == (j >> 3) ? Xd[(i >> 3) * 64 + (i & 7) + 8 * (j & 7)] : S[j + i * SP];
+      inv[idx] = v;
     }
   }
   __syncthreads();
