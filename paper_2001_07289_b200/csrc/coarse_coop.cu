@@ -29,7 +29,7 @@ namespace cg = cooperative_groups;
 namespace bddc {
 
 constexpr int kX1Chunk = 64;
-constexpr int kCoopStages = 3;  // cp.async depth of the engine's GEMM tiles (fits the factor smem)  // split-K of the left-looking inverse accumulation
+constexpr int kCoopStages = 2;  // cp.async depth of the engine GEMM tiles: 41 KB smem leaves more L1 (measured: 3 stages and 4 CTAs/SM are slower)
 
 enum CoopType : int {
   CT_EA = 0, CT_PT = 1, CT_TS = 2, CT_X1 = 3, CT_SY = 4, CT_X2 = 5, CT_W = 6, CT_CB = 7,
