@@ -30,7 +30,7 @@ __device__ __forceinline__ TaskView gemm_task(const GemmArgs& a, int b) {
                   a.lda,          a.ldb,          a.ldc};
 }
 
-constexpr int kGemmStages = 3;
+constexpr int kGemmStages = 2;
 
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(128) gemm_f64_kernel(GemmArgs args) {
