@@ -211,9 +211,33 @@ def phase_work(op, pb, its):
     w["setup.T"] = ("fp64", nsub * (ng**3 / 3 + ng * ng * ncp))
     w["setup.Phi"] = ("fp64", float(np.sum(2 * nG * nG * nc + 3 * nG * nc * nc + nc**3)))
     w["setup.btchol"] = ("fp64", nsub * nblk * (m**3 / 3 + 2 * m**3))
-    # fused interior elimination (2D): btchol + E + S_G (SYRK, lower half)
-    w["setup.schur"] = ("fp64", w["setup.btchol"][1] + w["setup.E"][1] + w["setup.SG"][1])
+    # fused interior elimination (2D schur2d / 3D schur3d), the formulation's own work: W
+    # recursion (Gauss-Jordan inverse of each plane block, 2 m^3) + per plane j with na_j
+    # active interface columns: H_j = W_j R_j (2 m^2 na_j) and S_G -= R_j^T H_j (lower half,
+    # m na_j^2)
+    na = active_prefix(lay)
+    w["setup.schur"] = ("fp64", nsub * float(sum(2 * m**3 + 2 * m * m * a + m * a * a for a in na)))
     return w
+
+
+def active_prefix(lay):
+    """Exact active interface prefix per plane (the kernels round it up to 8): one past the
+    largest surface slot coupled to an interior node of planes <= j (capi.cu, G.nact)."""
+    npd = [b + 1 for b in lay.blk]
+    code = lay.node_code
+    act = np.zeros(max(lay.nblk, 1), dtype=np.int64)
+    coords = np.stack(np.unravel_index(np.arange(lay.nloc_nodes), npd[::-1])[::-1], axis=1)
+    interior = np.flatnonzero(code >= 0)
+    offs = np.array(np.meshgrid(*[[-1, 0, 1]] * lay.dim, indexing="ij")).reshape(lay.dim, -1).T
+    for o in offs:
+        nb = coords[interior] + o
+        ok = np.all((nb >= 0) & (nb < np.array(npd)), axis=1)
+        nbi = np.ravel_multi_index(nb[ok].T[::-1], npd[::-1])
+        c = code[nbi]
+        surf = c < 0
+        planes = code[interior[ok]][surf] // lay.m_pad
+        np.maximum.at(act, planes, -c[surf])
+    return np.maximum.accumulate(act).tolist()
 
 
 def _allmax(v, args):

@@ -251,11 +251,12 @@ struct PhaseScope {
 // T = L^{-T} L^{-1} - V V^T of the local setup, computed by the dataflow coarse factorization
 // in the time its critical path leaves CTAs idle (local_setup sets it when it defers T)
 struct LtArgs {
-  const double* LI;  // [cnt][n][n] L^{-1}, subdomain sub at (sub - sub0)
-  const double* V;   // [cnt][n][nc]
+  const double* LI;  // zmode 0: [cnt][n][n] L^{-1}; zmode 1: Phi [cnt][n][nc] (stride sV)
+  const double* V;   // zmode 0: [cnt][n][nc] V; zmode 1: W = Z C^T (sub at (sub - sub0))
   double* T;         // [nsub][n][n] (absolute subdomain index)
   long long sL, sV;
   int n, nc, sub0, on;
+  int zmode;         // 1: T already holds Z = S_K^{-1}; the tasks do T -= Phi W^T
 };
 
 // The explicit interface operator T is stored as its lower triangle only (the apply's GEMV

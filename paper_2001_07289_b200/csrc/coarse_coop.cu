@@ -99,8 +99,15 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
     const LtArgs& a = pg.lt;
     if (!a.on) return;
     const int sub = t.node, m0 = t.a * kTile, n0 = t.b * kTile;
-    const double* LI = a.LI + (long long)(sub - a.sub0) * a.sL;
     double* T = a.T + (long long)sub * a.sL;
+    if (a.zmode) {  // T = Z - Phi W^T (lower tile, mirrored)
+      const double* Ph = a.LI + (long long)(sub - a.sub0) * a.sV;
+      const double* W = a.V + (long long)(sub - a.sub0) * a.sV;
+      gemm_tile<false, true, kCoopStages>(Ph, a.n, W, a.n, T, a.n, a.n, a.n, a.nc, m0, n0, -1.0, 1.0, true, smem, 0,
+                                          -1, true);
+      return;
+    }
+    const double* LI = a.LI + (long long)(sub - a.sub0) * a.sL;
     gemm_tile<true, false, kCoopStages>(LI, a.n, LI, a.n, T, a.n, a.n, a.n, a.n, m0, n0, 1.0, 0.0, true, smem,
                                         m0, -1, a.nc == 0);
     if (a.nc > 0) {

@@ -530,7 +530,7 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
     // T deferred into the dataflow coarse factorization (all subdomains in one chunk)
     const bool defer_t = c.lt_fusable && c.fp.n_coarse > 0 && sub0 == G.s_lo && cnt == G.s_hi - G.s_lo;
     c.lt_defer = LtArgs{};
-    if (G.nc_pad > 0 && !defer_t) {
+    if (G.nc_pad > 0) {
       // 5b/7 through Z = S_K^{-1}: S_C = G^T G with G = L^{-1} C^T (a Gram matrix: stays SPD
       // at 1e12 coefficient contrast, where C Z C^T does not), W = Z C^T (a gather, no GEMM),
       // Phi = W S_C^{-1}, T = Z - Phi W^T (= S_K^{-1} - Phi S_C Phi^T). Z and then T in LS.
@@ -563,66 +563,31 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
         }
         gemm_batched(true, false, G.nc_pad, G.nc_pad, G.nc_pad, 1.0, LCi, LCi, 0.0, SCib, cnt, s);  // S_C^{-1}
         gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nc_pad, 1.0, Xb, SCib, 0.0, PHb, cnt, s);   // Phi
+        // 6. local coarse block P = Phi^T S_Gamma Phi = S_C^{-1} - s I
         { finish_local_kernel<<<cnt, 256, 0, s>>>(G, sub0, c.coarse_scaling, c.diag_s, c.st, c.cscale, SCi,
                                                 c.Sloc); BDDC_COUNT(); }
         BDDC_LAUNCH_CHECK();
+      }
+      // 7. T -= Phi W^T: deferred into the dataflow coarse factorization when all subdomains are
+      //    one chunk (its schedule runs the tiles on the CTAs the critical path leaves idle)
+      if (defer_t) {
+        c.lt_defer = LtArgs{PH, X, c.LS, lsS, phS, G.nG_pad, G.nc_pad, sub0, 1, 1};
+        continue;
       }
       PhaseScope pt(c.prof, "setup.T", s);
       gemm_batched(false, true, G.nG_pad, G.nG_pad, G.nc_pad, -1.0, PHb, Xb, 1.0, LSb, cnt, s, true, 0,
                    !t_lower_only(G));
       continue;
     }
-    if (G.nc_pad > 0) {
-      PhaseScope pphi(c.prof, "setup.Phi", s);
-      // 5b. G = L^{-1} C^T, S_C = G^T G = L_C L_C^T, Q = G L_C^{-T} (orthonormal columns),
-      //     V = L^{-T} Q, Phi = V L_C^{-1} = S_K^{-1} C^T S_C^{-1}  (C Phi = I)
-      BMat PHb{PH, phS, G.nG_pad};
-      BMat SCb{SC, scS, G.nc_pad};
-      BMat Yb{Y, phS, G.nG_pad};
-      BMat SCib{SCi, scS, G.nc_pad};
-      if (!g_gather(G, sub0, cnt, c.st, LIv, lsS, X, phS, s, true)) {
-        BDDC_CUDA(cudaMemsetAsync(PH, 0, sizeof(double) * cnt * phS, s));
-        { build_ct_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, c.Phi); BDDC_COUNT(); }
-        BDDC_LAUNCH_CHECK();
-        gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nG_pad, 1.0, LIb, PHb, 0.0, Xb, cnt, s, false, 1);
-      }
-      gemm_batched(true, false, G.nc_pad, G.nc_pad, G.nG_pad, 1.0, Xb, Xb, 0.0, SCb, cnt, s);
-      { sc_pad_kernel<<<cnt, 128, 0, s>>>(G, sub0, c.st, SC); BDDC_COUNT(); }
-      BDDC_LAUNCH_CHECK();
-      potrf_batched(SCb, G.nc_pad, G.nc_pad, cnt, nullptr, c.tinv, s);
-      const int ncb = ceil_div(G.nc_pad, kTile);
-      BMat LCi{c.tinv, (long long)ncb * kTileInvStride, kTile};  // L_C^{-1} (one tile)
-      if (ncb > 1) {  // general: L_C^{-1} by blocked solves into the SCi buffer
-        { identity_kernel<<<cnt, 256, 0, s>>>(SCi, G.nc_pad, scS); BDDC_COUNT(); }
-        BDDC_LAUNCH_CHECK();
-        trsm_batched(TRSM_LLN, SCb, G.nc_pad, SCib, G.nc_pad, cnt, c.tinv, s, true);
-        BDDC_CUDA(cudaMemcpyAsync(P, SCi, sizeof(double) * cnt * scS, cudaMemcpyDeviceToDevice, s));
-        LCi = BMat{P, scS, G.nc_pad};
-      }
-      gemm_batched(false, true, G.nG_pad, G.nc_pad, G.nc_pad, 1.0, Xb, LCi, 0.0, Yb, cnt, s);        // Q
-      gemm_batched(true, false, G.nG_pad, G.nc_pad, G.nG_pad, 1.0, LIb, Yb, 0.0, Xb, cnt, s, false, 2);  // V
-      gemm_batched(false, false, G.nG_pad, G.nc_pad, G.nc_pad, 1.0, Xb, LCi, 0.0, PHb, cnt, s);      // Phi
-      // 6. P = Phi^T S_Gamma Phi = S_C^{-1} - s I,  S_C^{-1} = L_C^{-T} L_C^{-1}
-      gemm_batched(true, false, G.nc_pad, G.nc_pad, G.nc_pad, 1.0, LCi, LCi, 0.0, SCib, cnt, s);
-      { finish_local_kernel<<<cnt, 256, 0, s>>>(G, sub0, c.coarse_scaling, c.diag_s, c.st, c.cscale, SCi,
-                                              c.Sloc); BDDC_COUNT(); }
-      BDDC_LAUNCH_CHECK();
-    }
-    // 7. explicit interface operator T = (I - Phi C) S_K^{-1} = L^{-T} L^{-1} - Phi S_C Phi^T
-    //    = L^{-T} L^{-1} - V V^T (symmetric; the apply's local Neumann solve is one GEMV).
-    //    With all subdomains in one chunk it is deferred into the dataflow coarse
-    //    factorization, whose schedule runs its tiles on the CTAs the critical path leaves idle.
+    // no constraints: T = S_K^{-1} = L^{-T} L^{-1}
     if (defer_t) {
-      c.lt_defer = LtArgs{LIv, X, c.LS, lsS, phS, G.nG_pad, G.nc_pad, sub0, 1};
+      c.lt_defer = LtArgs{LIv, X, c.LS, lsS, phS, G.nG_pad, 0, sub0, 1, 0};
       continue;
     }
     {
       PhaseScope pt(c.prof, "setup.T", s);
-      // lower tiles only, mirrored (symmetric); L^{-T} upper: tile row m0 needs k >= m0
-      const bool mir = !t_lower_only(G);
-      gemm_batched(true, false, G.nG_pad, G.nG_pad, G.nG_pad, 1.0, LIb, LIb, 0.0, LSb, cnt, s, true, 2, mir);
-      if (G.nc_pad > 0)
-        gemm_batched(false, true, G.nG_pad, G.nG_pad, G.nc_pad, -1.0, Xb, Xb, 1.0, LSb, cnt, s, true, 0, mir);
+      gemm_batched(true, false, G.nG_pad, G.nG_pad, G.nG_pad, 1.0, LIb, LIb, 0.0, LSb, cnt, s, true, 2,
+                   !t_lower_only(G));
     }
   }
 }
