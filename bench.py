@@ -10,8 +10,8 @@ f ~ U[-1,1] per dof (seed 0), PCG rtol 1e-8 from x0 = 0, FP64, reference coarse 
 One step = numeric BDDC-SO setup on device-resident inputs (local factorizations, coarse
 basis, coarse assembly + multifrontal factorization) + the PCG solve to rtol 1e-8.
 `value` = dofs solved per second over the timed steps (CUDA events on the library stream);
-`e2e` = the same through the C ABI with host buffers (alpha and b uploaded from pinned
-memory, x downloaded) every step. Host index tables / symbolic analysis are one-time prep
+`e2e` = the same through the C ABI with host buffers (bddc_solve_host: alpha and b uploaded
+from pinned memory, overlapped with the setup; x downloaded) every step. Host index tables / symbolic analysis are one-time prep
 (reported as prep_s). Inputs (factors ~3.5 GB) exceed the 126 MB L2 between steps.
 
 --impl reference times the CPU oracle port (oracle/bddc_oracle.py: SuperLU factorizations,
