@@ -168,13 +168,14 @@ def build_host_problem(name):
 
 
 def phase_work(op, pb, its):
-    """Algorithmic bytes / flops per launch of each timed phase."""
-    st = op.stats()
+    """Algorithmic bytes / flops per launch of each timed phase on this rank (DESIGN.md §5);
+    the coarse problem is replicated, so its work is the full problem's on every rank."""
     lay = op.plan.layout
-    nsub = int(st.nsub)
+    sl = op.slab  # this rank's subdomains / active rows (everything when unsharded)
+    nsub = int(sl.s_hi - sl.s_lo)
     m, nblk, nG, nI = lay.m, lay.nblk, lay.nG, lay.m * lay.nblk
-    nc = op.plan.n_con_local
-    n = int(st.n)
+    nc = op.plan.n_con_local[sl.s_lo:sl.s_hi]
+    n = int(sl.f_hi - sl.f_lo)
     T = lambda k: k * (k + 1) / 2  # noqa: E731
     w = {}
     # interior solve: packed Linv_j (T(m_pad)) + coupling stencil, forward and backward,
@@ -192,7 +193,7 @@ def phase_work(op, pb, its):
     if cp is not None:
         w["apply.coarse"] = ("hbm", 8.0 * 2 * cp.factor_entries())
         w["setup.coarse"] = ("fp64", cp.factor_flops())
-    if st.tv_in_coarse_solve:
+    if op.stats().tv_in_coarse_solve:
         w["apply.coarse"] = ("hbm", w["apply.coarse"][1] + tbytes)
     else:
         w["apply.gamma1"] = ("hbm", w["apply.gamma1"][1] + tbytes)
@@ -204,12 +205,12 @@ def phase_work(op, pb, its):
     w["setup.SG"] = ("fp64", nsub * nG * (nG + 1) * nI)
     w["setup.SK"] = ("fp64", nsub * nG**3 / 3)
     ng, ncp = lay.nG_pad, op.plan.nc_pad
-    # L^{-1} of the S_K factor (triangular inverse, n^3/3). Phi: G = L^{-1} C^T (triangular x
-    # dense), S_C = G^T G (SYRK), L_C and S_C^{-1} (~nc^3), Q = G L_C^{-T}, V = L^{-T} Q,
-    # Phi = V L_C^{-1}; P = S_C^{-1} - s I (no GEMM). T = L^{-T} L^{-1} (n^3/3) - V V^T (SYRK)
-    w["setup.Linv"] = ("fp64", nsub * ng**3 / 3)
-    w["setup.T"] = ("fp64", nsub * (ng**3 / 3 + ng * ng * ncp))
-    w["setup.Phi"] = ("fp64", float(np.sum(2 * nG * nG * nc + 3 * nG * nc * nc + nc**3)))
+    # L^{-1} of the S_K factor (triangular inverse, n^3/3). Phi phase: G = L^{-1} C^T and
+    # W = Z C^T are gathers; S_C = G^T G (n nc^2, symmetric), Z = L^{-T} L^{-1} (n^3/3),
+    # S_C^{-1} (~nc^3), Phi = W S_C^{-1} (2 n nc^2). T -= Phi W^T (lower: n^2 nc)
+    w["setup.Linv"] = ("fp64", nsub * nG**3 / 3)
+    w["setup.Phi"] = ("fp64", float(np.sum(nG**3 / 3 + 3 * nG * nc * nc + nc**3)))
+    w["setup.T"] = ("fp64", float(np.sum(nG * nG * nc)))
     w["setup.btchol"] = ("fp64", nsub * nblk * (m**3 / 3 + 2 * m**3))
     # fused interior elimination (2D schur2d / 3D schur3d), the formulation's own work: W
     # recursion (Gauss-Jordan inverse of each plane block, 2 m^3) + per plane j with na_j
