@@ -582,14 +582,17 @@ __global__ void __launch_bounds__(kRh3Threads, 2) rh3d_kernel(Geometry G, int su
           Wsm[c + r * P] = v;
         }
       }
-      if (tid < M) bsh[tid] = bcg[(long long)j * M + tid];
-      for (int idx = tid; idx < M * EP; idx += kRh3Threads) R[idx] = 0.0;
+      // R_j <- -B_j H_{j-1} (B_j diagonal; zero on the chunk's first active plane)
+      for (int r = warp; r < M; r += NW) {
+        const double br = j > jmin ? bcg[(long long)j * M + r] : 0.0;
+        for (int c = lane; c < w; c += 32) R[r * EP + c] = -br * H[r * EP + c];
+      }
     }
     __syncthreads();
-    // A_IG,j on the chunk: row r couples to the non-Dirichlet surface slots among its 26
-    // neighbours (structurally zero couplings give 0)
-    for (int idx = tid; idx < G.m * G.nnb; idx += kRh3Threads) {
-      const int r = idx / G.nnb, o = G.nb_code[idx % G.nnb];
+    // R_j += A_IG,j on the chunk: row r couples to the non-Dirichlet surface slots among its
+    // 6 face neighbours (P1: schur3d_supported)
+    for (int idx = tid; idx < G.m * 6; idx += kRh3Threads) {
+      const int r = idx / 6, o = G.nb_code[idx % 6];
       int a[3];
       local_coords(G, lt.irow_node[j * M + r], a);
       const int d[3] = {o % 3 - 1, (o / 3) % 3 - 1, o / 9 - 1};
@@ -598,14 +601,8 @@ __global__ void __launch_bounds__(kRh3Threads, 2) rh3d_kernel(Geometry G, int su
       if (code >= 0) continue;
       const int slot = -code - 1 - c0;
       if (slot < 0 || slot >= w || local_to_free(G, p, bn) < 0) continue;
-      R[r * EP + slot] = local_coef<3>(G, alpha, p, a, d);
+      R[r * EP + slot] += local_coef<3>(G, alpha, p, a, d);
     }
-    __syncthreads();
-    if (j > jmin)  // R_j -= B_j H_{j-1} (B_j diagonal)
-      for (int idx = tid; idx < M * w; idx += kRh3Threads) {
-        const int r = idx / w, c = idx % w;
-        R[r * EP + c] -= bsh[r] * H[r * EP + c];
-      }
     __syncthreads();
     // H_j = W_j R_j
     for (int tt = warp; tt < (M / 8) * (w / 8); tt += NW) {
@@ -656,8 +653,8 @@ bool schur2d(const Ctx& c, int sub0, int cnt, const double* Wd, const double* Wo
 
 
 bool schur3d_supported(const Geometry& G) {
-  return G.dim == 3 && G.nbo == 1 && G.bo_dx[0] == 0 && G.bo_dy[0] == 0 && G.m_pad == 56 &&
-         G.nG_pad <= 1024;
+  return G.dim == 3 && G.nbo == 1 && G.bo_dx[0] == 0 && G.bo_dy[0] == 0 && G.nnb == 6 &&
+         G.m_pad == 56 && G.nG_pad <= 1024;
 }
 
 // 3D interior elimination: packed W_j into LI (the apply's interior factor), R~ / H~ into
