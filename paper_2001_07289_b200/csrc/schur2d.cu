@@ -41,6 +41,15 @@ __device__ __forceinline__ void mma_acc_t(double& c0, double& c1, const double* 
   for (int k = 0; k < K; k += 4) dmma884(c0, c1, a[k * ACS], b[k * BRS]);
 }
 
+// Pitch (doubles) of a square operand read as DMMA fragments A(r, k) = X[r + k P]: a half-warp
+// (g, t in 0..3) touches g + t P, conflict-free iff P = 4 or 12 mod 16 (M + 1 gives 2-4 way
+// conflicts: the dominant stall of schur2d / rh3d in the ncu source counters)
+constexpr int frag_pitch(int M) {
+  int p = M + 1;
+  while (p % 16 != 4 && p % 16 != 12) ++p;
+  return p;
+}
+
 // lower-triangular 8x8 tile coordinates (I, J) of tile index tt = I(I+1)/2 + J (NGP <= 128)
 __constant__ int2 c_lower_tiles[16 * 17 / 2];
 
@@ -263,7 +272,7 @@ __global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, i
                                                                 LocalTables lt,
                                                                 const double* __restrict__ LI,
                                                                 double* __restrict__ LS) {
-  constexpr int P = M + 1;
+  constexpr int P = frag_pitch(M);
   constexpr int EP = NGP + 4;
   constexpr int NT = NGP / 8;
   constexpr int NLT = NT * (NT + 1) / 2;
@@ -404,7 +413,7 @@ void launch_schur2d(const Ctx& c, int sub0, int cnt, const double* Wd, const dou
                     const double* E, cudaStream_t s) {
   const bool diagb = c.geo.nbo == 1 && c.geo.bo_dx[0] == 0;
   const size_t smem_w = sizeof(double) * kWarpsW * (diagb ? wf_warp_doubles<M, true>() : wf_warp_doubles<M, false>());
-  const size_t smem_s = sizeof(double) * (2 * M * (NGP + 4) + M * (M + 1) + 3 * M);
+  const size_t smem_s = sizeof(double) * (2 * M * (NGP + 4) + M * frag_pitch(M) + 3 * M);
   static bool attr = false;
   if (!attr) {
     int2 tiles[16 * 17 / 2];
@@ -538,7 +547,7 @@ __global__ void __launch_bounds__(kRh3Threads, 2) rh3d_kernel(Geometry G, int su
                                                             const double* __restrict__ LI,
                                                             double* __restrict__ Rt,
                                                             double* __restrict__ Ht, long long sE) {
-  constexpr int P = M + 1;
+  constexpr int P = frag_pitch(M);
   constexpr int CW = 64, EP = CW + 4;
   constexpr int NW = kRh3Threads / 32;
   extern __shared__ __align__(16) double sm[];
@@ -664,7 +673,7 @@ void schur3d(const Ctx& c, int sub0, int cnt, double* Rt, double* Ht, long long 
   const Geometry& G = c.geo;
   constexpr int M = 56;
   const size_t smem_w = sizeof(double) * kWarps3 * wf3_warp_doubles<M>();
-  const size_t smem_r = sizeof(double) * (M * (M + 1) + 2 * M * 68 + M);
+  const size_t smem_r = sizeof(double) * (M * frag_pitch(M) + 2 * M * 68 + M);
   static bool attr = false;
   if (!attr) {
     BDDC_CUDA(cudaFuncSetAttribute(wfactor3d_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_w));
