@@ -110,6 +110,7 @@ struct FrontDev {
   int* rmap_ptr = nullptr;
   int* bnd_idx = nullptr;       // per node: boundary dofs (elimination order)
   int* bnd_ptr = nullptr;
+  unsigned char* ualias = nullptr;  // per node: update columns on shared pool pages (front_vmm.cu)
 };
 
 // Coarse multifrontal plan (device data + host schedule).
@@ -127,6 +128,9 @@ struct FrontPlan {
   std::vector<int> parent;
   long long front_pool = 0, upd_pool = 0;
   int max_front = 0;
+  bool alias = false;                  // update blocks aliased through the page pool (front_vmm.cu)
+  long long alias_resident_bytes = 0;  // physical bytes behind the fronts when aliased
+  std::vector<unsigned char> ualias;
   FrontDev d;  // device pointers (POD, passed to kernels)
   // CSR of the assembled coarse operator (elimination order, lower triangle) + maps
   long long nnz = 0;
@@ -264,8 +268,16 @@ struct LtArgs {
 // interfaces run v = T rho inside the coarse solve and keep T full.
 inline bool t_lower_only(const Geometry& G) { return G.nG_pad > 256 && G.nG_pad <= 512; }
 
+struct Ctx;
+struct FrontVmm;
+void front_vmm_release(Ctx& c);
+bool front_alias_layout(Ctx& c);
+void front_memset(Ctx& c, cudaStream_t s);
+bool coarse_df_enabled(const Ctx& c);
+
 struct Ctx {
   int device = 0;
+  FrontVmm* vmm = nullptr;  // aliased coarse fronts (front_vmm.cu), released by free_all
   PhaseTimers prof;
   cudaStream_t stream = nullptr;
   // host-buffer solve (bddc_solve_host): alpha arrives in slabs of subdomain rows on the copy
@@ -335,6 +347,7 @@ struct Ctx {
     return d;
   }
   void free_all() {
+    front_vmm_release(*this);
     for (void* p : allocations) cudaFree(p);
     allocations.clear();
   }

@@ -147,6 +147,8 @@ void build_plan(Ctx& c, const bddc_setup_desc* d) {
   }
   fp.front_pool = off;
   fp.upd_pool = uoff;
+  fp.alias = false;
+  fp.ualias.assign(N, 0);
   // children CSR (in node order) and level lists
   fp.child_ptr.assign(N + 1, 0);
   for (int i = 0; i < N; ++i)
@@ -168,7 +170,9 @@ void build_plan(Ctx& c, const bddc_setup_desc* d) {
   }
   // device copies
   FrontDev& fd = fp.d;
-  fd.fronts = c.alloc<double>(fp.front_pool);
+  // multifrontal update blocks share pages when the resident fronts would not fit (front_vmm.cu)
+  if (!front_alias_layout(c)) fd.fronts = c.alloc<double>(fp.front_pool);
+  fd.ualias = c.upload(fp.ualias.data(), N);
   fd.upd = c.alloc<double>(std::max<long long>(fp.upd_pool, 1));
   fd.sep_start = c.upload(fp.sep_start.data(), N);
   fd.sep_size = c.upload(fp.sep_size.data(), N);
@@ -189,6 +193,7 @@ void build_plan(Ctx& c, const bddc_setup_desc* d) {
   std::vector<long long> pos(d->nnz);
   for (long long e = 0; e < d->nnz; ++e) {
     const int nd = d->csr_node[e];
+    if (d->csr_col[e] >= fp.sep_size[nd]) throw ApiError{1, "coarse CSR entry outside its front's panel"};
     pos[e] = fp.front_off[nd] + d->csr_row[e] + (long long)d->csr_col[e] * fp.ld[nd];
   }
   fp.csr_front_pos = c.upload(pos.data(), pos.size());
@@ -691,7 +696,7 @@ int bddc_get_stats(bddc_ctx* h, bddc_stats* o) {
   o->nsub = G.nsub;
   o->factor_bytes = 8LL * (G.s_hi - G.s_lo) * (G.li_stride + (long long)G.nG_pad * G.nG_pad +
                                     (long long)G.nG_pad * G.nc_pad);
-  o->front_bytes = 8LL * c.fp.front_pool;
+  o->front_bytes = c.fp.alias ? c.fp.alias_resident_bytes : 8LL * c.fp.front_pool;
   o->workspace_bytes = 8LL * h->ws_doubles;
   o->nG_pad = G.nG_pad;
   o->nI_pad = G.nI_pad;

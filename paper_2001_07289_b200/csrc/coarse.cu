@@ -267,7 +267,7 @@ void coarse_assemble_and_factor(Ctx& c) {
   { csr_segsum_kernel<<<std::min<long long>((fp.nnz + th - 1) / th, 148 * 16), th, 0, s>>>(
       fp.nnz, fp.seg_ptr, fp.contrib, c.Sloc, fp.csr_val); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
-  BDDC_CUDA(cudaMemsetAsync(fd.fronts, 0, sizeof(double) * fp.front_pool, s));
+  front_memset(c, s);
   { csr_to_front_kernel<<<std::min<long long>((fp.nnz + th - 1) / th, 148 * 16), th, 0, s>>>(
       fp.nnz, fp.csr_front_pos, fp.csr_val, fd.fronts); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();

@@ -128,7 +128,8 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
       const int c0 = fd.child_ptr[node];
       const int ch = fd.child_list[c0 + t.arg];
       const int bc = fd.bnd_size[ch], sc = fd.sep_size[ch], lc = fd.ld[ch];
-      const double* U = fd.fronts + fd.front_off[ch] + sc + (long long)sc * lc;
+      double* U = fd.fronts + fd.front_off[ch] + sc + (long long)sc * lc;
+      const bool zu = fd.ualias[ch];  // pool pages: leave them zero for the next block
       const int* rm = fd.rmap + fd.rmap_ptr[ch];
       // columns [a, a + cb) in batches of 16; thread owns rows i = a + tid + 128 m, loads
       // rm[i] once and issues 16 independent read-modify-writes per batch
@@ -148,7 +149,10 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
           }
 #pragma unroll
           for (int c = 0; c < 16; ++c)
-            if (j0 + c < je && i >= j0 + c) F[r + cof[c]] = fv[c] + u[c];
+            if (j0 + c < je && i >= j0 + c) {
+              F[r + cof[c]] = fv[c] + u[c];
+              if (zu) U[i + (long long)(j0 + c) * lc] = 0.0;
+            }
         }
       }
       break;
@@ -1020,6 +1024,11 @@ void coop_build(Ctx& c) {
           for (int q = 0; q < fp.bnd_size[ch]; q += chunk) {
             DfTask t = mk(CT_EA, nd, q, chunk, k);
             dep(t, c_syall[ch], tot_sy[ch]);
+            // an aliased update block may share pages with grandchildren's: no write into it
+            // before every child subtree is done (front_vmm.cu)
+            if (fp.ualias[nd] && k == 0)
+              for (int o = fp.child_ptr[nd] + 1; o < fp.child_ptr[nd + 1]; ++o)
+                dep(t, c_syall[fp.child_list[o]], tot_sy[fp.child_list[o]]);
             if (k > 0) dep(t, c_ea[nd] + k - 1, nea[nd][k - 1]);
             sig(t, c_ea[nd] + k);
             dt.push_back(t);
