@@ -27,7 +27,8 @@ namespace {
 // DENSE: also write the interior blocks T_j / B_j and A_IG densely (generic path); the fused
 // 2D path generates them from the stencil on chip and only needs A_GG and s_i here.
 // ADD (fused 3D): A_GG is added to LS, which already holds -R~^T H~ (no memset of LS).
-template <int DIM, bool DENSE, bool ADD = false>
+// AGG = false (fused 2D): s_i only; the Schur kernel generates A_GG in its epilogue.
+template <int DIM, bool DENSE, bool ADD = false, bool AGG = true>
 __global__ void __launch_bounds__(256) assemble_local_kernel(Geometry G, const double* __restrict__ alpha,
                                                              LocalTables lt, int sub0, double* Wd,
                                                              double* Wo, double* E, double* LS,
@@ -47,7 +48,7 @@ __global__ void __launch_bounds__(256) assemble_local_kernel(Geometry G, const d
   if (!DENSE) {
     // A_GG only: the couplings of the surface slots among themselves, then the diagonal of
     // every local node for s_i (interior couplings are generated on chip by the fused kernels)
-    const int tot1 = G.nG * NOFF;
+    const int tot1 = AGG ? G.nG * NOFF : 0;
     for (int idx = threadIdx.x; idx < tot1 + G.nloc_nodes; idx += blockDim.x) {
       if (idx < tot1) {
         const int slot = idx / NOFF, o = idx % NOFF;
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(256) assemble_local_kernel(Geometry G, const d
     const int j = idx / (G.m_pad - G.m), r = G.m + idx % (G.m_pad - G.m);
     wd[j * mm + r + (long long)r * G.m_pad] = 1.0;
   }
-  for (int s = G.nG + threadIdx.x; s < G.nG_pad; s += blockDim.x) {
+  for (int s = G.nG + threadIdx.x; AGG && s < G.nG_pad; s += blockDim.x) {
     if (ADD) ls[s + (long long)s * G.nG_pad] += 1.0;
     else ls[s + (long long)s * G.nG_pad] = 1.0;
   }
@@ -438,7 +439,7 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
       BDDC_CUDA(cudaMemsetAsync(Wd, 0, sizeof(double) * 2 * (size_t)chunk * wS, s));
       BDDC_CUDA(cudaMemsetAsync(E, 0, sizeof(double) * cnt * eS, s));
     }
-    if (!fused3d) BDDC_CUDA(cudaMemsetAsync(LS, 0, sizeof(double) * cnt * lsS, s));
+    if (!fused3d && !fused2d) BDDC_CUDA(cudaMemsetAsync(LS, 0, sizeof(double) * cnt * lsS, s));  // fused: every entry written
     BMat LSb{LS, lsS, G.nG_pad};
     if (fused3d) {
       // 3D: W recursion + per-chunk R_j / H_j, then S_G = A_GG - R~^T H~ as one staircase
@@ -457,7 +458,7 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
         const int sa = std::max(sub0, c.alpha_slab_sub[k]), sb = std::min(sub0 + cnt, c.alpha_slab_sub[k + 1]);
         BDDC_CUDA(cudaStreamWaitEvent(s, c.alpha_ev[k], 0));
         if (sa >= sb) continue;
-        { assemble_local_kernel<2, false><<<sb - sa, 256, 0, s>>>(G, c.alpha, c.lt, sa, Wd, Wo, E, c.LS, c.diag_s); BDDC_COUNT(); }
+        { assemble_local_kernel<2, false, false, false><<<sb - sa, 256, 0, s>>>(G, c.alpha, c.lt, sa, Wd, Wo, E, c.LS, c.diag_s); BDDC_COUNT(); }
         BDDC_LAUNCH_CHECK();
         if (!schur2d(c, sa, sb - sa, Wd, Wo, E, s)) throw CudaError("schur2d: unsupported geometry");
       }
@@ -467,7 +468,7 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
     if (fused3d)
       { assemble_local_kernel<3, false, true><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, Wd, Wo, E, c.LS, c.diag_s); BDDC_COUNT(); }
     else if (G.dim == 2 && fused2d)
-      { assemble_local_kernel<2, false><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, Wd, Wo, E, c.LS, c.diag_s); BDDC_COUNT(); }
+      { assemble_local_kernel<2, false, false, false><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, Wd, Wo, E, c.LS, c.diag_s); BDDC_COUNT(); }
     else if (G.dim == 2)
       { assemble_local_kernel<2, true><<<cnt, 256, 0, s>>>(G, c.alpha, c.lt, sub0, Wd, Wo, E, c.LS, c.diag_s); BDDC_COUNT(); }
     else

@@ -282,7 +282,9 @@ __global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, i
   constexpr int O_R = O_H + M * EP;    // A_IG,j -> R_j   (M x EP)
   constexpr int O_W = O_R + M * EP;    // W_j (square)
   constexpr int O_BC = O_W + M * P;    // stencil [M][3]
+  constexpr int O_SL = O_BC + 3 * M;   // surface slot -> local node | Dirichlet bit (ints)
   extern __shared__ __align__(16) double sm[];
+  int* slot_sm = reinterpret_cast<int*>(sm + O_SL);
   const int b = blockIdx.x, sub = sub0 + b;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
@@ -298,6 +300,12 @@ __global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, i
   double acc[SYRK_PER_WARP][2];
 #pragma unroll
   for (int q = 0; q < SYRK_PER_WARP; ++q) acc[q][0] = acc[q][1] = 0.0;
+  for (int k = tid; k < G.nG; k += kSchurThreads) {
+    const int node = lt.slot_node[k];
+    int a[3];
+    local_coords(G, node, a);
+    slot_sm[k] = node | (local_to_free(G, p, a) < 0 ? (1 << 30) : 0);
+  }
   int nprev = 0;
   for (int j = 0; j < G.nblk; ++j) {
     const int na = G.nact[j];           // active columns (multiple of 8)
@@ -388,9 +396,22 @@ __global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, i
     nprev = na;
     __syncthreads();
   }
-  // S_G = A_GG - S_acc (full symmetric)
+  // S_G = A_GG - S_acc (full symmetric). A_GG from the element stencil (the local Neumann
+  // coupling of two surface slots, as assemble_local_kernel writes it: local_coef at the row
+  // slot's node toward the column slot's node; identity on Dirichlet and padding slots)
   double* ls = LS + (long long)sub * G.nG_pad * G.nG_pad;
   const int ld = G.nG_pad;
+  const int nx1 = G.blk[0] + 1;
+  auto agg = [&](int r, int c) -> double {
+    if (r >= G.nG || c >= G.nG) return r == c ? 1.0 : 0.0;
+    const int sr = slot_sm[r], sc = slot_sm[c];
+    const int nr = sr & ((1 << 30) - 1), nc = sc & ((1 << 30) - 1);
+    const int a[3] = {nr % nx1, nr / nx1, 0};
+    const int d[3] = {nc % nx1 - a[0], nc / nx1 - a[1], 0};
+    if (d[0] < -1 || d[0] > 1 || d[1] < -1 || d[1] > 1) return 0.0;
+    if ((sr | sc) >> 30) return r == c ? 1.0 : 0.0;
+    return local_coef<2>(G, alpha, p, a, d);
+  };
 #pragma unroll
   for (int q = 0; q < SYRK_PER_WARP; ++q) {
     const int tt = warp + q * NW;
@@ -400,7 +421,7 @@ __global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, i
     for (int e = 0; e < 2; ++e) {
       const int r = I * 8 + g, c = J * 8 + 2 * t4 + e;
       if (r >= c) {
-        const double v = ls[r + (long long)c * ld] - acc[q][e];
+        const double v = agg(r, c) - acc[q][e];
         ls[r + (long long)c * ld] = v;
         if (r != c) ls[c + (long long)r * ld] = v;
       }
@@ -413,7 +434,7 @@ void launch_schur2d(const Ctx& c, int sub0, int cnt, const double* Wd, const dou
                     const double* E, cudaStream_t s) {
   const bool diagb = c.geo.nbo == 1 && c.geo.bo_dx[0] == 0;
   const size_t smem_w = sizeof(double) * kWarpsW * (diagb ? wf_warp_doubles<M, true>() : wf_warp_doubles<M, false>());
-  const size_t smem_s = sizeof(double) * (2 * M * (NGP + 4) + M * frag_pitch(M) + 3 * M);
+  const size_t smem_s = sizeof(double) * (2 * M * (NGP + 4) + M * frag_pitch(M) + 3 * M + NGP / 2);
   static bool attr = false;
   if (!attr) {
     int2 tiles[16 * 17 / 2];
