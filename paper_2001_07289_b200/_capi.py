@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbddcso_b200.so")
+LIB_PATH = os.environ.get("BDDC_LIB") or os.path.join(_HERE, "libbddcso_b200.so")  # BDDC_LIB: A/B builds (tools)
 
 _i = C.c_int
 _ll = C.c_longlong

@@ -50,6 +50,16 @@ constexpr int frag_pitch(int M) {
   return p;
 }
 
+// Store a DMMA.8x8 accumulator (lane holds C[g][2t], C[g][2t+1]) into a row-major tile of
+// pitch = 4 mod 16 doubles: odd rows store their second element first, so each of the two
+// 64-bit store instructions hits 16 distinct bank pairs per half-warp (no 2-way conflict)
+__device__ __forceinline__ void store_frag_rowmajor(double* C, int ldc, double c0, double c1, int lane) {
+  const int g = lane >> 2, t = lane & 3, odd = g & 1;
+  double* p = C + g * ldc + 2 * t;
+  p[odd] = odd ? c1 : c0;
+  p[odd ^ 1] = odd ? c0 : c1;
+}
+
 // lower-triangular 8x8 tile coordinates (I, J) of tile index tt = I(I+1)/2 + J (NGP <= 128)
 __constant__ int2 c_lower_tiles[16 * 17 / 2];
 
@@ -379,8 +389,7 @@ __global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, i
       const int ti = tt % (M / 8), tj = tt / (M / 8);
       double c0 = 0.0, c1 = 0.0;
       mma_acc_t<M, 1, P, EP, 1>(c0, c1, sm + O_W + ti * 8, sm + O_R + tj * 8, lane);
-      sm[O_H + (ti * 8 + g) * EP + tj * 8 + 2 * t4] = c0;
-      sm[O_H + (ti * 8 + g) * EP + tj * 8 + 2 * t4 + 1] = c1;
+      store_frag_rowmajor(sm + O_H + (ti * 8) * EP + tj * 8, EP, c0, c1, lane);
     }
     __syncthreads();
     // S_acc += R_j^T H_j on active lower tiles (I, J < nat)
@@ -639,8 +648,7 @@ __global__ void __launch_bounds__(kRh3Threads, 2) rh3d_kernel(Geometry G, int su
       const int ti = tt % (M / 8), tj = tt / (M / 8);
       double d0 = 0.0, d1 = 0.0;
       mma_acc_t<M, 1, P, EP, 1>(d0, d1, Wsm + ti * 8, R + tj * 8, lane);
-      H[(ti * 8 + g) * EP + tj * 8 + 2 * t4] = d0;
-      H[(ti * 8 + g) * EP + tj * 8 + 2 * t4 + 1] = d1;
+      store_frag_rowmajor(H + (ti * 8) * EP + tj * 8, EP, d0, d1, lane);
     }
     __syncthreads();
     for (int idx = tid; idx < M * w; idx += kRh3Threads) {
