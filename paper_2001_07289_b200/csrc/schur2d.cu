@@ -41,6 +41,20 @@ __device__ __forceinline__ void mma_acc_t(double& c0, double& c1, const double* 
   for (int k = 0; k < K; k += 4) dmma884(c0, c1, a[k * ACS], b[k * BRS]);
 }
 
+// C(8x8 tile) += W(rows r0.., all K) B(K x 8) with W symmetric and only its lower triangle
+// (row >= col, column-major, pitch P) stored: entries above the diagonal are read at their
+// transposed position (a half-warp then touches t + 4g instead of g + 4t: still conflict-free)
+template <int K, int P, int BRS>
+__device__ __forceinline__ void mma_symlower(double& c0, double& c1, const double* W, int r0, const double* B, int lane) {
+  const int g = lane >> 2, t = lane & 3, row = r0 + g;
+  const double* b = B + t * BRS + g;
+#pragma unroll
+  for (int k = 0; k < K; k += 4) {
+    const int kk = k + t;
+    dmma884(c0, c1, W[row >= kk ? row + kk * P : kk + row * P], b[k * BRS]);
+  }
+}
+
 // Pitch (doubles) of a square operand read as DMMA fragments A(r, k) = X[r + k P]: a half-warp
 // (g, t in 0..3) touches g + t P, conflict-free iff P = 4 or 12 mod 16 (M + 1 gives 2-4 way
 // conflicts: the dominant stall of schur2d / rh3d in the ncu source counters)
@@ -344,8 +358,7 @@ __global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, i
           if ((c + 1) * M - (c + 1) * c / 2 <= e) ++c;
           if (c * M - c * (c - 1) / 2 > e) --c;
           const int r = c + (e - (c * M - c * (c - 1) / 2));
-          sm[O_W + r + c * P] = wv[u];
-          sm[O_W + c + r * P] = wv[u];
+          sm[O_W + r + c * P] = wv[u];  // lower triangle only (mma_symlower)
         }
       }
       if (tid < M * nbo) sm[O_BC + (tid / nbo) * 3 + tid % nbo] = bv;
@@ -388,7 +401,7 @@ __global__ void __launch_bounds__(kSchurThreads, 2) schur2d_kernel(Geometry G, i
     for (int tt = warp; tt < (M / 8) * nat; tt += NW) {
       const int ti = tt % (M / 8), tj = tt / (M / 8);
       double c0 = 0.0, c1 = 0.0;
-      mma_acc_t<M, 1, P, EP, 1>(c0, c1, sm + O_W + ti * 8, sm + O_R + tj * 8, lane);
+      mma_symlower<M, P, EP>(c0, c1, sm + O_W, ti * 8, sm + O_R + tj * 8, lane);
       store_frag_rowmajor(sm + O_H + (ti * 8) * EP + tj * 8, EP, c0, c1, lane);
     }
     __syncthreads();
@@ -616,9 +629,7 @@ __global__ void __launch_bounds__(kRh3Threads, 2) rh3d_kernel(Geometry G, int su
         const int c = tid >> 2, q = tid & 3;
         const double* col = li + (long long)j * G.Tm + (c * M - c * (c - 1) / 2) - c;
         for (int r = c + q; r < M; r += 4) {
-          const double v = col[r];
-          Wsm[r + c * P] = v;
-          Wsm[c + r * P] = v;
+          Wsm[r + c * P] = col[r];  // lower triangle only (mma_symlower)
         }
       }
       // R_j <- -B_j H_{j-1} (B_j diagonal; zero on the chunk's first active plane)
@@ -647,7 +658,7 @@ __global__ void __launch_bounds__(kRh3Threads, 2) rh3d_kernel(Geometry G, int su
     for (int tt = warp; tt < (M / 8) * (w / 8); tt += NW) {
       const int ti = tt % (M / 8), tj = tt / (M / 8);
       double d0 = 0.0, d1 = 0.0;
-      mma_acc_t<M, 1, P, EP, 1>(d0, d1, Wsm + ti * 8, R + tj * 8, lane);
+      mma_symlower<M, P, EP>(d0, d1, Wsm, ti * 8, R + tj * 8, lane);
       store_frag_rowmajor(H + (ti * 8) * EP + tj * 8, EP, d0, d1, lane);
     }
     __syncthreads();
