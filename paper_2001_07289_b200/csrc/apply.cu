@@ -700,8 +700,7 @@ void apply_bddc(Ctx& c, const double* r, double* z, cudaStream_t s) {
   const Geometry& G = c.geo;
   const int th = 256;
   const int ng = G.g_hi - G.g_lo, nl = G.s_hi - G.s_lo;
-  // u1 = A_II^{-1} r_I (zero on Gamma)
-  BDDC_CUDA(cudaMemsetAsync(c.v1, 0, sizeof(double) * G.n, s));
+  // u1 = A_II^{-1} r_I (zero on Gamma: set once at setup, never written there)
   bt_solve(c, r, c.v1, s);
   if (c.n_gamma > 0) {
     exchange_dof_halo(c, c.v1, s);  // sharded: u1 on the rows next to the cut lines

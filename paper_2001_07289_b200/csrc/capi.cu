@@ -372,6 +372,9 @@ void do_setup(bddc_ctx* h, const bddc_setup_desc* d) {
   c.info = c.alloc<int>(G.nsub);
   c.info_k = c.alloc<int>(G.nsub);
   c.v1 = c.alloc<double>(G.n);
+  // u1 scratch: zero once; the interior solve only ever writes interior entries, so its
+  // Gamma entries stay zero (no memset per apply)
+  BDDC_CUDA(cudaMemsetAsync(c.v1, 0, sizeof(double) * G.n, c.stream));
   c.v2 = c.alloc<double>(G.n);
   c.rpg = c.alloc<double>(std::max(c.n_gamma, 1));
   c.qloc = c.alloc<double>(nc);
