@@ -520,8 +520,9 @@ def run_ours(args, rank, world, local_rank):
             "workload": describe(args.workload),
             "dofs": n, "subdomains": int(st.nsub), "coarse_size": int(st.n_coarse),
             "parallelism": "single GPU" if world == 1 else
-                           f"sharded x{world}: slabs of subdomain rows along y, NCCL halo / allgather "
-                           "exchanges, replicated coarse problem",
+                           f"sharded x{world}: slabs of subdomain rows along the last axis, "
+                           + ("host-staged (gloo, ranks sharing one GPU: test transport)" if args.transport == "host"
+                              else "NCCL") + " halo / allgather exchanges, replicated coarse problem",
             "l2": "inputs > L2 (factors %.1f GB + fronts %.2f GB vs 126 MB L2)" % (
                 st.factor_bytes / 1e9, st.front_bytes / 1e9),
         },
