@@ -116,6 +116,15 @@ int bddc_pcg_host(bddc_ctx* ctx, const double* b_host, double* x_host, double to
                   size_t errlen);
 int bddc_get_stats(bddc_ctx* ctx, bddc_stats* out);
 int bddc_sync(bddc_ctx* ctx);
+/* synchronize the context stream and report an asynchronous failure of the last apply (a
+   coarse-solve dependency timeout poisons its result): 0 ok, 6 + message */
+int bddc_check(bddc_ctx* ctx, char* err, size_t errlen);
+/* new interface weights slot_w [nsub * nG_pad] (host), e.g. coefficient weights recomputed for
+   a new alpha before bddc_refactor (compute_weights, bddc.py:108-145) */
+int bddc_update_weights(bddc_ctx* ctx, const double* slot_w_host, char* err, size_t errlen);
+/* coarse solve S_0 x = rhs with the device factor (coarse_factor.solve, bddc.py:362-364);
+   device vectors of n_coarse in the ELIMINATION order of the descriptor */
+int bddc_coarse_solve(bddc_ctx* ctx, const double* rhs_dev, double* sol_dev, void* stream);
 int bddc_kernel_launches_per_apply(bddc_ctx* ctx);
 /* measurement: kernels launched by this library so far (process-wide); CUDA events on the
    context stream (slots 0..7); optional per-phase event timers ("apply.bt_solve",
@@ -129,6 +138,9 @@ double bddc_profile_read(bddc_ctx* ctx, const char* phase, long long* count);
 /* diagnostics: copy an internal buffer ("LI", "LS", "Phi", "Sloc", "cscale", "diag_s",
    "csr_val", "fronts") to host; returns the element count (or -1) */
 long long bddc_debug_copy(bddc_ctx* ctx, const char* name, double* host, long long capacity);
+/* the same buffers, elements [offset, offset + count) (count 0 / host NULL: total length);
+   backs the operator's lazy host views (.subdomains[i].coarse_basis, .coarse_matrix) */
+long long bddc_read_buffer(bddc_ctx* ctx, const char* name, long long offset, long long count, double* host);
 
 /* multi-GPU: one rank per GPU, each owning a slab of the subdomain lattice
    along the last axis (rows [r*R/world, (r+1)*R/world) of the R subdomain rows). Call one

@@ -37,6 +37,7 @@ sys.path.insert(0, ROOT)
 import bddcso  # noqa: E402  (reference, read-only)
 import bddcso.linalg as rlin  # noqa: E402
 import bddcso.mesh as rmesh  # noqa: E402
+import bddcso.partition as rpart  # noqa: E402
 
 from oracle import bddc_oracle as orc  # noqa: E402
 
@@ -44,6 +45,11 @@ OUT = os.path.join(ROOT, "tests", "golden")
 
 _Q1 = rmesh._element_stiffness_box
 _SOLVE = rlin.SaddleFactorization.solve
+_VALIDATE = rpart.PartitionPair._validate
+
+
+def _no_validate(self):
+    return None
 
 
 def _p1_box(lengths, alpha):
@@ -75,6 +81,31 @@ CASES = [
     ("q1_3d_vf", 3, (12, 12, 12), (3, 3, 3), 2, "vf", "cardinality", "q1", "const", "one", "reference", 1e-8, False),
     ("full_p1_2d", 2, (32, 32), (4, 4), 2, "vef", "cardinality", "p1", "const", "one", "spec", 1e-8, True),
 ]
+# Parity at scale (round 2): the reference run with PartitionPair validation skipped (its
+# O(subsubdomains x cells) ndimage loop, partition.py:63-73; SURVEY §8(c) prescribes
+# validate=False for uniform box refinements, which are valid by construction). r and b are
+# not stored (regenerated from their seeds by tests/conftest.py) to keep the files small.
+BIG_CASES = [
+    # 3D, cfg3/cfg5 local geometry, 8^3 subdomains: coarse problem 15,967 unknowns,
+    # multi-panel coarse fronts (top separator 961)
+    ("cfg3c_p1_ref", 3, (64, 64, 64), (8, 8, 8), 2, "vef", "cardinality", "p1", "const", "one", "reference", 1e-8, False),
+    # cfg5 local geometry with its random source, 6^3 subdomains
+    ("cfg5a_p1_ref", 3, (48, 48, 48), (6, 6, 6), 2, "vef", "cardinality", "p1", "const", "uniform", "reference", 1e-8, False),
+    # cfg4 (the coefficient config runs in spec scaling) at 4^3 subdomains
+    ("cfg4b_p1_spec", 3, (32, 32, 32), (4, 4, 4), 2, "vef", "coefficient", "p1", "blocks", "one", "spec", 1e-8, False),
+    # cfg2 L = h with 4x4 subdomains: corner / edge / interior subdomains have different s_i,
+    # so the reference-mode coarse-basis scaling is visible (2x2 subdomains hide it)
+    ("cfg2b_p1_Lh44", 2, (128, 128), (4, 4), 32, "ve", "cardinality", "p1", "const", "uniform", "reference", 1e-8, False),
+    # cfg2 local geometry (32^2 subdomains, L = 4h) on 16x16 subdomains
+    ("cfg2c_p1_L4h", 2, (512, 512), (16, 16), 8, "ve", "cardinality", "p1", "const", "uniform", "reference", 1e-8, False),
+]
+# Θ̂ from refine_by_coefficient (partition.py:202-220) on a channels field (problems.py:42-102):
+# the components of constant α inside each box subdomain (split = -1 marks it)
+COEFF_CASES = [
+    ("chan_q1_coeff", 3, (16, 16, 16), (2, 2, 2), -1, "vef", "coefficient", "q1", "channels", "one", "reference", 1e-8, False),
+    ("chan_p1_coeff2d", 2, (48, 48), (3, 3), -1, "ve", "coefficient", "p1", "channels", "one", "spec", 1e-8, False),
+]
+CHANNELS = {2: (3.0, 2, 2, 0), 3: (3.0, 2, 2, 1)}  # contrast exponent, cross-section, bars, axis
 
 
 def _set_element(element):
@@ -85,17 +116,23 @@ def _set_mode(mode):
     rlin.SaddleFactorization.solve = _spec_solve if mode == "spec" else _SOLVE
 
 
-def run_case(case):
+def run_case(case, big=False):
     (name, dim, cells, subs, split, recipe, wmode, element, coeff, rhs, mode, tol, full) = case
     _set_element(element)
     _set_mode(mode)
+    rpart.PartitionPair._validate = _no_validate if big else _VALIDATE
     mesh = bddcso.build_mesh(dim, cells)
     if coeff == "const":
         cf = bddcso.make_constant(mesh, 1.0)
+    elif coeff == "channels":
+        cf = bddcso.make_channels(mesh, subs, bddcso.ChannelSpec(*CHANNELS[dim]))
     else:
         cf = bddcso.CoefficientField(orc.block_alpha(cells, 4, seed=0))
     theta = bddcso.partition_uniform(mesh, subs)
-    pair = bddcso.refine_uniform(mesh, theta, split)
+    if split < 0:
+        pair = bddcso.refine_by_coefficient(mesh, theta, cf)
+    else:
+        pair = bddcso.refine_uniform(mesh, theta, split)
     system = bddcso.assemble(mesh, cf, 1.0)
     objects = bddcso.classify_objects(pair)
     weights = bddcso.compute_weights(pair, wmode, cf)
@@ -156,19 +193,26 @@ def run_case(case):
     )
     if cm is not None and cm.shape[0] <= 4000:
         out.update(coarse_data=cm.data, coarse_indices=cm.indices, coarse_indptr=cm.indptr)
+    if split < 0:
+        out.update(refine="coefficient", theta_hat=pair.theta_hat, alpha=cf.alpha)
+    if big:  # r = default_rng(1234).standard_normal(n); b from the source seed
+        out.update(big=True, coarse_diag=cm.diagonal() if cm is not None else np.zeros(0))
+        del out["r"], out["b"]
     return out
 
 
 def main():
     os.makedirs(OUT, exist_ok=True)
     names = sys.argv[1:]
-    for case in CASES:
+    for case, big in [(c, False) for c in CASES + COEFF_CASES] + [(c, True) for c in BIG_CASES]:
         if names and case[0] not in names:
             continue
+        if not names and big and os.path.exists(os.path.join(OUT, case[0] + ".npz")):
+            continue  # minutes each: regenerate only when named
         t0 = time.perf_counter()
-        res = run_case(case)
+        res = run_case(case, big)
         np.savez_compressed(os.path.join(OUT, case[0] + ".npz"), **res)
-        print(f"{case[0]:16s} n={res['n']:6d} coarse={res['coarse_size']:5d} "
+        print(f"{case[0]:16s} n={res['n']:7d} coarse={res['coarse_size']:6d} "
               f"its={res['iterations']:4d} kappa={res['kappa']:.10g} "
               f"({time.perf_counter() - t0:.1f}s)")
     # refine_by_coefficient labels (partition.py:202-220) on a channel field
@@ -184,6 +228,7 @@ def main():
     print("count KAT", kat)
     _set_element("q1")
     _set_mode("reference")
+    rpart.PartitionPair._validate = _VALIDATE
 
 
 if __name__ == "__main__":

@@ -28,7 +28,8 @@ EXPORTS = (
     "bddc_kernel_launches_per_apply", "bddc_debug_copy", "bddc_launch_count",
     "bddc_event_record", "bddc_event_elapsed_ms", "bddc_profile", "bddc_profile_read",
     "bddc_nccl_unique_id", "bddc_comm_init_nccl", "bddc_comm_init_host", "bddc_partition_info",
-    "bddc_dense_potrf", "bddc_dense_trsm", "bddc_dense_gemm",
+    "bddc_dense_potrf", "bddc_dense_trsm", "bddc_dense_gemm", "bddc_check", "bddc_update_weights",
+    "bddc_coarse_solve", "bddc_read_buffer",
 )
 
 
@@ -96,9 +97,14 @@ def load(required: bool = True):
                                     C.c_char_p, C.c_size_t]
     lib.bddc_get_stats.argtypes = [_vp, C.POINTER(Stats)]
     lib.bddc_sync.argtypes = [_vp]
+    lib.bddc_check.argtypes = [_vp, C.c_char_p, C.c_size_t]
+    lib.bddc_update_weights.argtypes = [_vp, _pd, C.c_char_p, C.c_size_t]
+    lib.bddc_coarse_solve.argtypes = [_vp, _vp, _vp, _vp]
     lib.bddc_kernel_launches_per_apply.argtypes = [_vp]
     lib.bddc_debug_copy.argtypes = [_vp, C.c_char_p, _pd, _ll]
     lib.bddc_debug_copy.restype = _ll
+    lib.bddc_read_buffer.argtypes = [_vp, C.c_char_p, _ll, _ll, _pd]
+    lib.bddc_read_buffer.restype = _ll
     lib.bddc_launch_count.argtypes = []
     lib.bddc_launch_count.restype = _ll
     lib.bddc_event_record.argtypes = [_vp, _i]

@@ -20,13 +20,14 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _capi
-from .layout import DevicePlan, build_device_plan
+from . import operator_views
+from .layout import DevicePlan, build_device_plan, slot_weights
 from .linalg import NotSpdError, UnderconstrainedError
-from .mesh import AssembledSystem, element_matrix_box
+from .mesh import AssembledSystem, CoefficientField, element_matrix_box
 from .partition import ObjectTable, PartitionPair
 from .shard import slab_ranges
 from .weights import (ConstraintTable, Recipe, RecipeError, WeightingOperator,
-                      select_constraints)
+                      compute_weights, select_constraints)
 
 COARSE_SCALINGS = ("reference", "spec")
 
@@ -102,6 +103,35 @@ class BddcOperator:
         self._desc_arrays = None
         self._desc = None
 
+    # ------------------------------------------------ reference attributes (views)
+    @property
+    def subdomains(self) -> operator_views.SubdomainList:
+        """Per-subdomain pieces (bddc.py:280-306), built lazily from the host tables and the
+        device buffers (operator_views.py)."""
+        if getattr(self, "_subdomains", None) is None:
+            self._subdomains = operator_views.SubdomainList(self)
+        return self._subdomains
+
+    @property
+    def coarse_matrix(self):
+        """S_0 (SparseSym, upper triangle, coarse-id order) from the device assembly."""
+        return operator_views.coarse_matrix(self)
+
+    @property
+    def coarse_factor(self):
+        """Object with ``solve(rhs)`` running the device coarse factor (None without a coarse
+        space, as the reference's)."""
+        return operator_views.CoarseFactor(self) if self.plan.coarse is not None else None
+
+    @property
+    def _gamma_index(self) -> np.ndarray:
+        gi = getattr(self, "_gidx", None)
+        if gi is None:
+            gi = np.full(self.n, -1, dtype=np.int64)
+            gi[self.gamma_dofs] = np.arange(len(self.gamma_dofs))
+            self._gidx = gi
+        return gi
+
     # ---------------------------------------------------------------- setup
     def _descriptor(self):
         p = self.plan
@@ -173,11 +203,26 @@ class BddcOperator:
         self._read_times()
 
     def refactor(self, alpha: np.ndarray | None = None):
-        """Re-run the numeric setup on device-resident inputs (optionally a new α)."""
+        """Re-run the numeric setup on device-resident inputs, optionally for a new α on the
+        same partition. With coefficient weighting (Remark 1, bddc.py:108-145) the interface
+        weights depend on α: they are recomputed on the host and uploaded before the setup,
+        so the result is the reference's build_bddc for the new coefficient. ``system`` is
+        replaced by the new-α system (its host matrix, if ever needed, is rebuilt lazily)."""
         err = C.create_string_buffer(1024)
         a = None
         if alpha is not None:
-            a = np.ascontiguousarray(alpha, dtype=np.float64)
+            coeff = CoefficientField(np.ascontiguousarray(alpha, dtype=np.float64))
+            if coeff.alpha.shape != (self.system.mesh.cell_count,):
+                raise ValueError(f"alpha has shape {coeff.alpha.shape}, expected "
+                                 f"({self.system.mesh.cell_count},)")
+            a = coeff.alpha
+            if self.weights.mode == "coefficient":
+                weights = compute_weights(self.pair, "coefficient", coeff, self.weights.objects)
+                slot_w = np.ascontiguousarray(slot_weights(self.plan, weights))
+                rc = self._lib.bddc_update_weights(self._ctx, _capi.ptr(slot_w, C.c_double), err, len(err))
+                raise_for(rc, err.value.decode(errors="replace"), self.recipe)
+                self.weights = weights
+            self.system = AssembledSystem(self.system.mesh, coeff, self.system.rhs)
         rc = self._lib.bddc_refactor(self._ctx, _capi.ptr(a, C.c_double) if a is not None else None,
                                      err, len(err))
         raise_for(rc, err.value.decode(errors="replace"), self.recipe)
@@ -195,34 +240,57 @@ class BddcOperator:
         return st
 
     # ---------------------------------------------------------------- apply
-    def _as_device(self, v):
+    def _as_device(self, v, name: str = "vector", n: int | None = None):
+        """(device tensor, came-in-as-tensor). CUDA tensors must already be float64, of shape
+        (n,), contiguous and on this operator's device: the C ABI reads / writes exactly n
+        doubles, so anything else is rejected instead of converted behind the caller's back.
+        Host arrays (numpy / lists / CPU tensors) are copied to the device."""
         torch = self._torch
-        if isinstance(v, torch.Tensor):
-            if v.device.type != "cuda" or v.dtype != torch.float64:
-                return v.to(device=f"cuda:{self.device}", dtype=torch.float64).contiguous(), True
-            return v.contiguous(), True
-        a = np.asarray(v, dtype=np.float64)
+        n = self.n if n is None else n
+        if isinstance(v, torch.Tensor) and v.device.type == "cuda":
+            if v.dtype != torch.float64:
+                raise ValueError(f"{name} must be float64, got {v.dtype}")
+            if tuple(v.shape) != (n,):
+                raise ValueError(f"{name} has shape {tuple(v.shape)}, expected ({n},)")
+            if v.device.index != self.device:
+                raise ValueError(f"{name} is on {v.device}, the operator on cuda:{self.device}")
+            if not v.is_contiguous():
+                raise ValueError(f"{name} must be contiguous")
+            return v, True
+        a = np.asarray(v.cpu().numpy() if isinstance(v, torch.Tensor) else v, dtype=np.float64)
+        if a.shape != (n,):
+            raise ValueError(f"{name} has shape {a.shape}, expected ({n},)")
         return torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{self.device}"), False
+
+    def _check_async(self):
+        """Raise if the last apply failed asynchronously (coarse-solve dependency timeout)."""
+        err = C.create_string_buffer(512)
+        rc = self._lib.bddc_check(self._ctx, err, len(err))
+        raise_for(rc, err.value.decode(errors="replace"))
 
     def apply(self, r):
         """z = B r (bddc.py:336-380). numpy in → numpy out; CUDA tensor in → CUDA tensor out."""
         torch = self._torch
         if tuple(np.shape(r)) != (self.n,):
             raise ValueError(f"residual has shape {tuple(np.shape(r))}, expected ({self.n},)")
-        rd, is_tensor = self._as_device(r)
+        rd, is_tensor = self._as_device(r, "residual")
         z = torch.empty_like(rd)
         stream = torch.cuda.current_stream(rd.device).cuda_stream
         rc = self._lib.bddc_apply(self._ctx, C.c_void_p(rd.data_ptr()), C.c_void_p(z.data_ptr()),
                                   C.c_void_p(stream))
         raise_for(rc, "bddc_apply failed")
-        return z if is_tensor else z.cpu().numpy()
+        if is_tensor:
+            return z
+        out = z.cpu().numpy()
+        self._check_async()
+        return out
 
     __call__ = apply
 
     def matvec(self, x):
         """A x (matrix-free, the system operator of this preconditioner)."""
         torch = self._torch
-        xd, is_tensor = self._as_device(x)
+        xd, is_tensor = self._as_device(x, "x")
         y = torch.empty_like(xd)
         stream = torch.cuda.current_stream(xd.device).cuda_stream
         rc = self._lib.bddc_spmv(self._ctx, C.c_void_p(xd.data_ptr()), C.c_void_p(y.data_ptr()),
@@ -232,7 +300,7 @@ class BddcOperator:
 
     def harmonic(self, gamma_values):
         torch = self._torch
-        gd, is_tensor = self._as_device(gamma_values)
+        gd, is_tensor = self._as_device(gamma_values, "interface values", len(self.gamma_dofs))
         out = torch.empty(self.n, dtype=torch.float64, device=gd.device)
         stream = torch.cuda.current_stream(gd.device).cuda_stream
         rc = self._lib.bddc_harmonic(self._ctx, C.c_void_p(gd.data_ptr()),
@@ -251,16 +319,20 @@ class BddcOperator:
         resid = np.zeros(max_iters + 2)
         rep = _capi.PcgReport()
         err = C.create_string_buffer(512)
-        if isinstance(b, torch.Tensor):
-            bd, _ = self._as_device(b)
-            x = x_out if x_out is not None else torch.empty_like(bd)
+        if isinstance(b, torch.Tensor) and b.device.type == "cuda":
+            bd, _ = self._as_device(b, "right-hand side")
+            if x_out is not None:
+                x, _ = self._as_device(x_out, "x_out")
+            else:
+                x = torch.empty_like(bd)
             torch.cuda.current_stream(bd.device).synchronize()
             rc = self._lib.bddc_pcg(self._ctx, C.c_void_p(bd.data_ptr()), C.c_void_p(x.data_ptr()),
                                     float(tol), int(max_iters), _capi.ptr(alphas, C.c_double),
                                     _capi.ptr(betas, C.c_double), _capi.ptr(resid, C.c_double),
                                     C.byref(rep), err, len(err))
         else:
-            bh = np.ascontiguousarray(b, dtype=np.float64)
+            bh = np.ascontiguousarray(b.cpu().numpy() if isinstance(b, torch.Tensor) else b,
+                                      dtype=np.float64)
             if bh.shape != (self.n,):
                 raise ValueError(f"right-hand side has shape {bh.shape}, expected ({self.n},)")
             x = np.zeros(self.n)
@@ -335,6 +407,10 @@ def build_bddc(system: AssembledSystem, pair: PartitionPair, objects: ObjectTabl
         recipe = Recipe.parse(recipe)
     if coarse_scaling not in COARSE_SCALINGS:
         raise ValueError(f"unknown coarse_scaling {coarse_scaling!r}; expected {COARSE_SCALINGS}")
+    if pair.box_layout is None:
+        raise ValueError(
+            "the device operator needs Θ to be a uniform box partition (partition_uniform); "
+            "any refinement Θ̂ (refine_uniform, refine_by_coefficient) is supported on top of it")
     t0 = time.perf_counter()
     constraints = select_constraints(objects, recipe, pair)
     plan = build_device_plan(pair, constraints, weights)

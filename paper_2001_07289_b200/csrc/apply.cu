@@ -428,10 +428,10 @@ bool launch_bt_t(const Geometry& G, const LocalTables& lt, const double* LI, con
   if (G.m_pad != M || G.nbo != NBO || G.Tm != BtT<M, NBO>::TM) return false;
   const size_t smem = sizeof(double) * BtT<M, NBO>::per_warp(G.nI_pad) * BtT<M, NBO>::W;
   if (smem > 227 * 1024) return false;
-  static size_t attr = 0;
-  if (smem > attr) {
+  static SmemAttr attr;
+  if (attr.needs(smem)) {
     BDDC_CUDA(cudaFuncSetAttribute(bt_solve_t_kernel<M, NBO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
+    attr.set(smem);
   }
   const int grid = ceil_div(G.s_hi - G.s_lo, BtT<M, NBO>::W);
   bt_solve_t_kernel<M, NBO><<<grid, 32 * BtT<M, NBO>::W, smem, s>>>(G, lt, LI, in, out);
@@ -674,11 +674,11 @@ static void bt_solve(Ctx& c, const double* in, double* out, cudaStream_t s) {
   else if (G.nbo == 9) done = launch_bt_nbo<9>(G, c.lt, c.LI, in, out, s);
   if (done) return;
   const size_t smem = sizeof(double) * bt_smem(G).per_warp() * kBtWarps;
-  static size_t attr = 0;
-  if (smem > attr) {
+  static SmemAttr attr;
+  if (attr.needs(smem)) {
     BDDC_CUDA(cudaFuncSetAttribute(bt_solve_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     BDDC_CUDA(cudaFuncSetAttribute(bt_solve_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
+    attr.set(smem);
   }
   const int grid = ceil_div(G.s_hi - G.s_lo, kBtWarps);
   if (G.m_pad <= 32) { bt_solve_kernel<1><<<grid, 32 * kBtWarps, smem, s>>>(G, c.lt, c.LI, in, out); BDDC_COUNT(); }
@@ -717,12 +717,10 @@ void apply_bddc(Ctx& c, const double* r, double* z, cudaStream_t s) {
     c.prof.begin("apply.gamma1", s);
     if (tv_fused) { local_gamma1_kernel<false><<<nl, 128, smem1, s>>>(G, c.st, c.LS, c.Phi, c.cscale, c.rpg, c.qloc, c.wloc); BDDC_COUNT(); }
     else if (t_lower_only(G)) {
-      static bool attr = false;
+      static std::atomic<unsigned long long> attr{0};
       const size_t sm = gamma1_lower_smem(G.nG_pad);
-      if (!attr) {
+      if (first_on_device(attr))
         BDDC_CUDA(cudaFuncSetAttribute(local_gamma1_lower_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gamma1_lower_smem(512)));
-        attr = true;
-      }
       local_gamma1_lower_kernel<<<nl, kG1LThreads, sm, s>>>(G, c.st, c.LS, c.Phi, c.cscale, c.rpg, c.qloc, c.uloc);
       BDDC_COUNT();
     }

@@ -273,7 +273,6 @@ struct FrontVmm;
 void front_vmm_release(Ctx& c);
 bool front_alias_layout(Ctx& c);
 void front_memset(Ctx& c, cudaStream_t s);
-bool coarse_df_enabled(const Ctx& c);
 
 struct Ctx {
   int device = 0;
@@ -291,7 +290,6 @@ struct Ctx {
   Geometry geo{};
   int element = 0;
   int coarse_scaling = 0;  // 0 reference (Psi = Phi / s^2), 1 spec (Psi = Phi)
-  bool coarse_sweep = false;  // coarse fronts by block symmetric sweep (else Cholesky + inverse)
   bool setup_done = false;
   // inputs (device)
   double* alpha = nullptr;  // [ncells]
@@ -358,9 +356,7 @@ struct Ctx {
 // local_setup.cu
 void local_setup(Ctx& c, double* workspace, size_t ws_doubles);
 size_t local_setup_workspace(const Geometry& g, int chunk);
-// coarse_coop.cu: dataflow coarse factorization (default for the Cholesky formulation) and
-// its per-front scratch layout (inverse slots, Y partials, W21 = L21 X kept for the solve)
-bool coarse_df_enabled(const Ctx& c);
+// coarse_coop.cu: dataflow coarse factorization and its per-front scratch layout (inverse slots, Y partials, W21 = L21 X kept for the solve)
 long long coarse_df_layout(const FrontPlan& fp, std::vector<long long>& inv, std::vector<long long>& Y,
                            std::vector<long long>& W, std::vector<int>& ldw);
 // coarse.cu
@@ -374,7 +370,7 @@ struct TvArgs {
   double* v;          // [nsub][n]
   int n;
 };
-bool coarse_solve_df_enabled();
+int coarse_solve_error(Ctx& c);  // 1 if the last coarse solve hit a dependency timeout (syncs)
 void coarse_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s, const TvArgs* tv = nullptr);
 // apply.cu
 void apply_bddc(Ctx& c, const double* r, double* z, cudaStream_t s);

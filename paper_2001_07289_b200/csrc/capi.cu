@@ -1,5 +1,7 @@
 // C ABI (include/bddcso_b200.h): context, setup upload, numeric factorization, apply, PCG.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <climits>
 #include <cstring>
 #include <map>
@@ -28,6 +30,19 @@ struct bddc_ctx {
 namespace {
 
 constexpr int kNoFail = 0x7f7f7f7f;
+
+// BDDC_HOST_TIMING=1: wall time of the host phases of bddc_setup on stderr (cold start)
+struct HostTimer {
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  HostTimer() : on(getenv("BDDC_HOST_TIMING") != nullptr), t(std::chrono::steady_clock::now()) {}
+  void mark(const char* what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "bddc_setup host: %-28s %9.3f s\n", what, std::chrono::duration<double>(n - t).count());
+    t = n;
+  }
+};
 
 void set_err(char* err, size_t len, const std::string& msg) {
   if (!err || len == 0) return;
@@ -202,7 +217,9 @@ void build_plan(Ctx& c, const bddc_setup_desc* d) {
   fp.contrib = c.upload(d->contrib, d->ncontrib);
   fp.csr_val = c.alloc<double>(d->nnz);
   fp.coarse_slots = c.upload(d->coarse_slots, (size_t)d->n_coarse * fp.W);
+  HostTimer ht;
   build_level_schedule(c);
+  ht.mark("solve + factor schedules");
 }
 
 void do_setup(bddc_ctx* h, const bddc_setup_desc* d) {
@@ -316,10 +333,6 @@ void do_setup(bddc_ctx* h, const bddc_setup_desc* d) {
   }
   c.element = d->element;
   c.coarse_scaling = d->coarse_scaling;
-  {
-    const char* e = getenv("BDDC_COARSE_SWEEP");
-    c.coarse_sweep = e && atoi(e) != 0;
-  }
   h->ncells = ncells;
 
   cudaEvent_t e0, e1;
@@ -352,7 +365,9 @@ void do_setup(bddc_ctx* h, const bddc_setup_desc* d) {
   c.n_gamma = d->n_gamma;
   c.gamma_dof = c.upload(d->gamma_dof, d->n_gamma);
   c.gamma_slots = c.upload(d->gamma_slots, (size_t)d->n_gamma * G.npe);
+  HostTimer ht;
   build_plan(c, d);
+  ht.mark("coarse plan (total)");
   BDDC_CUDA(cudaEventRecord(e1, c.stream));
   BDDC_CUDA(cudaEventSynchronize(e1));
   BDDC_CUDA(cudaEventElapsedTime(&c.t_upload_ms, e0, e1));
@@ -404,7 +419,9 @@ void do_setup(bddc_ctx* h, const bddc_setup_desc* d) {
   const int chunk = (int)std::min<size_t>(nl, use / per);
   c.tinv_doubles = std::max(trsm_scratch_doubles(G.nG_pad, chunk), trsm_scratch_doubles(G.nc_pad, chunk));
   c.tinv = c.alloc<double>(c.tinv_doubles);
+  ht.mark("factor / workspace allocation");
   numeric_setup(h);
+  ht.mark("first numeric setup");
 }
 
 // Run f on the caller's stream (NULL = legacy default stream), ordered after pending work
@@ -490,12 +507,17 @@ int bddc_refactor(bddc_ctx* h, const double* alpha_host, char* err, size_t errle
 
 int bddc_apply(bddc_ctx* h, const double* r, double* z, void* stream) {
   if (!h || !h->c.setup_done) return 1;
-  return guarded(nullptr, 0, [&] { on_stream(h, stream, [&](cudaStream_t s) { apply_bddc(h->c, r, z, s); }); });
+  return guarded(nullptr, 0, [&] {
+    BDDC_CUDA(cudaSetDevice(h->c.device));
+    on_stream(h, stream, [&](cudaStream_t s) { apply_bddc(h->c, r, z, s); });
+  });
 }
 
 int bddc_harmonic(bddc_ctx* h, const double* g, double* out, void* stream) {
   if (!h || !h->c.setup_done) return 1;
-  return guarded(nullptr, 0, [&] { on_stream(h, stream, [&](cudaStream_t s) {
+  return guarded(nullptr, 0, [&] {
+    BDDC_CUDA(cudaSetDevice(h->c.device));
+    on_stream(h, stream, [&](cudaStream_t s) {
     Ctx& c = h->c;
     const Geometry& G = c.geo;
     // out_Gamma = g; out_I = A_II^{-1} (0 - A g_ext)_I
@@ -506,18 +528,23 @@ int bddc_harmonic(bddc_ctx* h, const double* g, double* out, void* stream) {
       { scatter_gamma_kernel<<<ceil_div(ng, 256), 256, 0, s>>>(ng, c.gamma_dof + G.g_lo, g + G.g_lo, out); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
     harmonic_interior(c, out, s);
-  }); });
+    });
+  });
 }
 
 int bddc_spmv(bddc_ctx* h, const double* x, double* y, void* stream) {
   if (!h || !h->c.alpha) return 1;
-  return guarded(nullptr, 0, [&] { on_stream(h, stream, [&](cudaStream_t s) { spmv(h->c, x, y, s); }); });
+  return guarded(nullptr, 0, [&] {
+    BDDC_CUDA(cudaSetDevice(h->c.device));
+    on_stream(h, stream, [&](cudaStream_t s) { spmv(h->c, x, y, s); });
+  });
 }
 
 int bddc_pcg(bddc_ctx* h, const double* b, double* x, double tol, int max_iters, double* alphas,
              double* betas, double* resid, bddc_pcg_report* rep, char* err, size_t errlen) {
   if (!h || !h->c.setup_done) return 1;
   return guarded(err, errlen, [&] {
+    BDDC_CUDA(cudaSetDevice(h->c.device));
     PcgResult r = pcg_solve(h->c, b, x, tol, max_iters, alphas, betas, resid);
     if (rep) {
       rep->iterations = r.iterations;
@@ -566,8 +593,7 @@ int bddc_solve_host(bddc_ctx* h, const double* alpha_host, const double* b_host,
       const bool slab = bddc::schur2d_supported(G) && G.nblk > 0;
       // two halves: the second lands while the first is eliminated (measured on cfg2: 4 or 8
       // slabs, or a smaller first slab, cost more in kernel tails than they hide)
-      double first = 0.5;
-      if (const char* e = getenv("BDDC_ALPHA_FIRST")) first = atof(e);
+      const double first = 0.5;
       const int ns = slab && rows >= 4 && first > 0.0 && first < 1.0 ? 2 : 1;
       const int rsplit = std::max(1, (int)(rows * first));
       for (int k = 0; k < ns; ++k) {
@@ -613,6 +639,7 @@ int bddc_pcg_host(bddc_ctx* h, const double* b_host, double* x_host, double tol,
   int code = 0;
   code = guarded(err, errlen, [&] {
     Ctx& c = h->c;
+    BDDC_CUDA(cudaSetDevice(c.device));
     const Geometry& G = c.geo;  // sharded: this rank's active rows in, owned rows out
     BDDC_CUDA(cudaMemcpyAsync(c.bbuf + G.f_lo, b_host + G.f_lo, sizeof(double) * (G.f_hi - G.f_lo),
                               cudaMemcpyHostToDevice, c.stream));
@@ -713,8 +740,40 @@ int bddc_get_stats(bddc_ctx* h, bddc_stats* o) {
   return 0;
 }
 
+int bddc_update_weights(bddc_ctx* h, const double* slot_w_host, char* err, size_t errlen) {
+  if (!h || !slot_w_host) return 1;
+  return guarded(err, errlen, [&] {
+    Ctx& c = h->c;
+    if (!c.st.slot_w) throw ApiError{1, "bddc_update_weights before bddc_setup"};
+    BDDC_CUDA(cudaSetDevice(c.device));
+    BDDC_CUDA(cudaMemcpyAsync(c.st.slot_w, slot_w_host, sizeof(double) * (size_t)c.geo.nsub * c.geo.nG_pad,
+                              cudaMemcpyHostToDevice, c.stream));
+    BDDC_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int bddc_coarse_solve(bddc_ctx* h, const double* rhs, double* sol, void* stream) {
+  if (!h || !h->c.setup_done || !rhs || !sol) return 1;
+  return guarded(nullptr, 0, [&] {
+    BDDC_CUDA(cudaSetDevice(h->c.device));
+    if (h->c.fp.n_coarse == 0) return;
+    on_stream(h, stream, [&](cudaStream_t s) { coarse_solve(h->c, rhs, sol, s, nullptr); });
+  });
+}
+
+int bddc_check(bddc_ctx* h, char* err, size_t errlen) {
+  if (!h) return 1;
+  return guarded(err, errlen, [&] {
+    BDDC_CUDA(cudaSetDevice(h->c.device));
+    BDDC_CUDA(cudaStreamSynchronize(h->c.stream));
+    if (h->c.setup_done && coarse_solve_error(h->c))
+      throw CudaError("coarse dataflow solve: dependency wait timed out (the last apply's result is invalid)");
+  });
+}
+
 int bddc_sync(bddc_ctx* h) {
   if (!h) return 1;
+  if (cudaSetDevice(h->c.device) != cudaSuccess) return 6;
   return cudaStreamSynchronize(h->c.stream) == cudaSuccess ? 0 : 6;
 }
 
@@ -732,6 +791,7 @@ long long bddc_launch_count(void) { return launch_counter().load(); }
 
 int bddc_event_record(bddc_ctx* h, int slot) {
   if (!h || slot < 0 || slot >= 8) return 1;
+  if (cudaSetDevice(h->c.device) != cudaSuccess) return 6;
   if (!h->ev[slot] && cudaEventCreate(&h->ev[slot]) != cudaSuccess) return 6;
   return cudaEventRecord(h->ev[slot], h->c.stream) == cudaSuccess ? 0 : 6;
 }
@@ -746,6 +806,7 @@ double bddc_event_elapsed_ms(bddc_ctx* h, int a, int b) {
 
 int bddc_profile(bddc_ctx* h, int enable) {
   if (!h) return 1;
+  if (cudaSetDevice(h->c.device) != cudaSuccess) return 6;
   cudaStreamSynchronize(h->c.stream);
   h->c.prof.on = enable != 0;
   h->c.prof.reset();
@@ -757,7 +818,7 @@ double bddc_profile_read(bddc_ctx* h, const char* phase, long long* count) {
   return h->c.prof.read(phase, count);
 }
 
-long long bddc_debug_copy(bddc_ctx* h, const char* name, double* host, long long cap) {
+long long bddc_read_buffer(bddc_ctx* h, const char* name, long long offset, long long count, double* host) {
   if (!h || !name) return -1;
   const Ctx& c = h->c;
   const Geometry& G = c.geo;
@@ -784,10 +845,19 @@ long long bddc_debug_copy(bddc_ctx* h, const char* name, double* host, long long
   else if (nm == "csol") { src = c.csol; n = c.fp.n_coarse; }
   else return -1;
   if (!host) return n;
-  if (cap < n || !src) return -1;
+  if (!src || offset < 0 || count < 0 || offset + count > n) return -1;
+  if (cudaSetDevice(c.device) != cudaSuccess) return -1;
   if (cudaStreamSynchronize(c.stream) != cudaSuccess) return -1;
-  if (cudaMemcpy(host, src, sizeof(double) * n, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
-  return n;
+  if (count && cudaMemcpy(host, src + offset, sizeof(double) * count, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -1;
+  return count;
+}
+
+long long bddc_debug_copy(bddc_ctx* h, const char* name, double* host, long long cap) {
+  const long long n = bddc_read_buffer(h, name, 0, 0, nullptr);
+  if (n < 0 || !host) return n;
+  if (cap < n) return -1;
+  return bddc_read_buffer(h, name, 0, n, host);
 }
 
 int bddc_dense_potrf(double* A, int n, int lda, long long stride, int count, int* info_host,

@@ -83,8 +83,7 @@ void build_level_schedule(Ctx& c) {
   // dataflow factorization: W21 (rows >= s of every front) stays in the scratch pool
   std::vector<long long> l_inv, l_y, l_w;
   std::vector<int> l_ldw;
-  const bool df = coarse_df_enabled(c);
-  if (df) coarse_df_layout(fp, l_inv, l_y, l_w, l_ldw);
+  coarse_df_layout(fp, l_inv, l_y, l_w, l_ldw);
   auto base = [&](int nd) {
     CsTask t{};
     t.front_off = fp.front_off[nd];
@@ -97,8 +96,8 @@ void build_level_schedule(Ctx& c) {
     t.s0 = fp.sep_start[nd];
     t.red = -1;
     t.np = 1;
-    t.w_off = df ? l_w[nd] : 0;
-    t.ldw = df ? l_ldw[nd] : 0;
+    t.w_off = l_w[nd];
+    t.ldw = l_ldw[nd];
     t.span = 256;
     return t;
   };
@@ -126,8 +125,8 @@ void build_level_schedule(Ctx& c) {
           const size_t first = ft.size();
           const int p0 = pf;
           for (int c0 = 0; c0 < sz; c0 += cw) {
-            // separator-only chunks: a copy (sweep) / the lower-triangular L11^{-1} (Cholesky)
-            if (c.coarse_sweep ? (r0 + 64 <= sz && c0 > 0) : (r0 < sz && c0 > r0 + 63)) break;
+            // separator rows: L11^{-1} is lower triangular
+            if (r0 < sz && c0 > r0 + 63) break;
             CsTask t = base(nd);
             t.r0 = r0;
             t.c0 = c0;
@@ -149,7 +148,7 @@ void build_level_schedule(Ctx& c) {
       for (int c0 = 0; c0 < sz; c0 += 64) {
         const size_t first = bt.size();
         const int p0 = pb;
-        for (int r0 = c.coarse_sweep ? 0 : (c0 / rw) * rw; r0 < f; r0 += rw) {  // sweep: full A11^{-1}
+        for (int r0 = (c0 / rw) * rw; r0 < f; r0 += rw) {
           CsTask t = base(nd);
           t.r0 = r0;
           t.c0 = c0;
@@ -197,7 +196,7 @@ void build_level_schedule(Ctx& c) {
     // v = T rho tasks (no dependencies), in slices before each of the top K forward and top K
     // backward levels: the CTAs take them while the chains at the top of the tree leave them
     // idle, and each slice drains in about one level's latency
-    const bool tv = coarse_solve_df_enabled() && c.geo.nG_pad > 0 && c.geo.nG_pad <= 256;
+    const bool tv = c.geo.nG_pad > 0 && c.geo.nG_pad <= 256;
     const int K = std::min(8, L);
     const int nsl = std::max(2 * K, 1);
     const int nl = c.geo.s_hi - c.geo.s_lo;

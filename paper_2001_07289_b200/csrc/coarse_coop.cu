@@ -1,18 +1,19 @@
-// Cooperative (persistent, grid-synchronised) coarse engine.
+// Coarse engine: the multifrontal factorization and the coarse solve, each ONE persistent
+// cooperative launch running a host-built dataflow program.
 //
-// The top of the nested-dissection tree has few, large fronts: run level by level as
-// separate launches, each 64-column panel step is a chain of small, latency-bound kernels.
-// Here the whole multifrontal factorization and the whole coarse solve each run as ONE
-// cooperative launch (all CTAs co-resident, grid.sync() between phases), executing a
-// host-built program of phases; each phase is a list of independent tile tasks spread over
-// all CTAs. Per level l:
-//   EA(k)            extend-add child k's update block into the front
-//   per panel p:     PT   potrf + trtri of the diagonal tile (inverse -> scratch)
-//                    TS   L21 tile <- A21 tile inv^T                   | X1  Y = L[k,0:k] X[0:k,0:k]
-//                    SY   A22 tile -= L21 L21^T (lower)                | X2  X[k,0:k] = -inv Y ; X[k,k] = inv
-//   W                W21 = L21 X   (X = L11^{-1}, accumulated left-looking by X1/X2)
-//   CB               panel <- [X; W21]   (partitioned inverse, see coarse.cu)
-// The solve program: per level forward GEMV tiles, reduction; then backward likewise.
+// The factorization program is a list of tile tasks in a topological order; CTAs pull
+// tasks from a global queue, wait (bounded) on dependency counters and signal counters
+// when done, so the tree's levels overlap and no grid barrier is needed. Per front:
+//   EA(k)     extend-add child k's update block into the front
+//   per 64-column panel p:
+//     PT      potrf + trtri of the diagonal tile (inverse -> scratch)
+//     TS      L21 tile <- A21 tile inv^T
+//     SY      trailing tile -= L21 L21^T (lower)            [+ lookahead PT of panel p+1]
+//     X1/X2   X = L11^{-1} accumulated left-looking (X written in place over L11)
+//   W         W21 = L21 X  (kept in the scratch pool for the solve)
+// so each front ends as the partitioned inverse [X; W21] (both coarse triangular solves are
+// GEMVs). The solve program: forward GEMV tasks bottom-up, backward top-down, chunk partials
+// reduced in fixed order (deterministic).
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -32,49 +33,34 @@ constexpr int kX1Chunk = 64;
 constexpr int kCoopStages = 2;  // cp.async depth of the engine GEMM tiles: 41 KB smem leaves more L1 (measured: 3 stages and 4 CTAs/SM are slower)
 
 enum CoopType : int {
-  CT_EA = 0, CT_PT = 1, CT_TS = 2, CT_X1 = 3, CT_SY = 4, CT_X2 = 5, CT_W = 6, CT_CB = 7,
-  // block symmetric sweep (Gauss-Jordan with inverse pivots) formulation
-  CT_SP = 8,   // D_P = inverse of the pivot tile (P, P)
-  CT_SB = 9,   // B_I = M_{I,P} D_P  (block I != P)
-  CT_SCP = 10, // column P <- B (block I), pivot tile <- -D_P
-  CT_SC = 11,  // M_IJ -= B_I M_{J,P}^T  (lower tiles, I, J != P) [+ lookahead D_{P+1}]
-  CT_SM = 12,  // separator block -> full +A11^{-1} (negate, mirror)
-  CT_LT = 13,  // local interface operator tile T_IJ of subdomain (node) = LI^T LI - V V^T
+  CT_EA = 0, CT_PT = 1, CT_TS = 2, CT_X1 = 3, CT_SY = 4, CT_X2 = 5, CT_W = 6,
+  CT_LT = 7,   // local interface operator tile T_IJ of subdomain (node) (the local setup's T)
+  CT_SYG = 8,  // trailing tile -= L21 L21^T over a whole panel group (K = kGroup panels)
+  CT_NTYPES = 9
 };
 
-// Sweep block map of panel P (pivot columns [64P, 64P + nb)): the other rows / columns in
-// 64-blocks, before the panel aligned, after it starting at 64P + nb.
-__host__ __device__ __forceinline__ int sweep_rb(int P, int nb, int i) {
-  return i < P ? 64 * i : 64 * P + nb + 64 * (i - P);
-}
-__host__ __device__ __forceinline__ int sweep_nblocks(int P, int nb, int f) {
-  return P + (f - 64 * P - nb + 63) / 64;
-}
+// Panels are factored in groups of kGroup (a 256-column block column): inside the group the
+// right-looking SY updates touch only the block column (K = 64); the trailing matrix beyond
+// it is updated ONCE per group (CT_SYG, K = 256), so every trailing tile is read and written
+// a quarter as often as with per-panel updates (the DRAM traffic of the large fronts).
+constexpr int kGroup = 4;
+__host__ __device__ __forceinline__ int group_k0(int g) { return g * kGroup * kTile; }
+__host__ __device__ __forceinline__ int group_k1(int g, int s) { return min(s, (g + 1) * kGroup * kTile); }
 
 struct CoopTask {
   int type, node, a, b, arg;
 };
 
-struct CoopPhase {
-  int t0, nt;
-};
-
 struct CoopScratch {  // per-node offsets (doubles) into the scratch pool
-  long long* inv;
-  long long* X;
-  long long* Y;
-  long long* W;
-  int* ldx;   // leading dimension of X (even)
-  int* ldw;   // leading dimension of W (even)
+  long long* inv;  // one 64 x 64 inverse slot per panel
+  long long* Y;    // X1 partials, two sets by panel parity
+  long long* W;    // W21 = L21 X (read by the solve)
+  int* ldw;        // leading dimension of W (even)
 };
 
 struct CoopProgram {
-  const CoopTask* tasks;
-  const CoopPhase* phases;
-  int nphases;
   CoopScratch sc;
   double* pool;
-  int df;  // dataflow mode: one inverse slot per panel, Y partials by panel parity
   LtArgs lt;  // deferred local T (CT_LT tasks; no-ops when lt.on == 0)
 };
 
@@ -87,6 +73,7 @@ struct DfTask {
   CoopTask t;
   int dep[kDeps], tgt[kDeps];
   int sig[kSigs];
+  unsigned char sw[8];  // increment of each signal (a group update counts as its panels)
 };
 
 namespace {
@@ -121,8 +108,8 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
   const int node = t.node;
   const int s = fd.sep_size[node], f = s + fd.bnd_size[node], ld = fd.ld[node];
   double* F = fd.fronts + fd.front_off[node];
-  double* X = pg.df ? F : pg.pool + pg.sc.X[node];  // dataflow: L11^{-1} in place in the front
-  const int ldx = pg.df ? ld : pg.sc.ldx[node];
+  double* X = F;  // L11^{-1} is written in place over L11
+  const int ldx = ld;
   switch (t.type) {
     case CT_EA: {  // child #arg of node, columns [a, a + b) of its lower update block
       const int c0 = fd.child_ptr[node];
@@ -159,7 +146,7 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
     }
     case CT_PT: {  // factor + invert diagonal tile of panel arg
       const int k = t.arg * kTile, nb = min(kTile, s - k);
-      double* inv = pg.pool + pg.sc.inv[node] + (pg.df ? t.arg : (t.arg & 1)) * kTileInvStride;
+      double* inv = pg.pool + pg.sc.inv[node] + t.arg * kTileInvStride;
       const int bad = potrf_trtri_tile(F + k + (long long)k * ld, ld, nb, inv, smem);
       if (threadIdx.x == 0 && bad >= 0) atomicMin(info + node, fd.sep_start[node] + k + bad);
       break;
@@ -167,7 +154,7 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
     case CT_TS: {  // rows (k+nb) + 64a.. of the panel: L21 <- A21 inv^T (in place)
       const int k = t.arg * kTile, nb = min(kTile, s - k), rest = f - k - nb;
       double* A21 = F + (k + nb) + (long long)k * ld;
-      const double* inv = pg.pool + pg.sc.inv[node] + (pg.df ? t.arg : (t.arg & 1)) * kTileInvStride;
+      const double* inv = pg.pool + pg.sc.inv[node] + t.arg * kTileInvStride;
       gemm_tile<false, true, kCoopStages>(A21, ld, inv, kTile, A21, ld, rest, nb, nb, t.a * kTile, 0, 1.0, 0.0,
                              false, smem);
       break;
@@ -177,7 +164,7 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
       const int kq0 = c + t.b * kX1Chunk, kq1 = min(k, kq0 + kX1Chunk);
       // dataflow: panel-parity Y partial sets (X1 of panel p + 2 waits for X2 of panel p)
       const long long ysz = (long long)kTile * s * ((s + kX1Chunk - 1) / kX1Chunk);
-      double* Y = pg.pool + pg.sc.Y[node] + (pg.df ? (t.arg & 1) * ysz : 0) + (long long)t.b * kTile * s;
+      double* Y = pg.pool + pg.sc.Y[node] + (t.arg & 1) * ysz + (long long)t.b * kTile * s;
       gemm_tile<false, false, kCoopStages>(F + k + (long long)kq0 * ld, ld, X + kq0 + (long long)c * ldx, ldx,
                               Y + (long long)c * kTile, kTile, nb, min(kTile, k - c), kq1 - kq0, 0, 0,
                               1.0, 0.0, false, smem);
@@ -192,7 +179,22 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
       if (t.a == 0 && t.b == 0 && k + nb < s) {  // factor the next panel's diagonal tile now
         __syncthreads();
         const int k1 = k + nb, nb1 = min(kTile, s - k1);
-        double* inv1 = pg.pool + pg.sc.inv[node] + (pg.df ? t.arg + 1 : ((t.arg + 1) & 1)) * kTileInvStride;
+        double* inv1 = pg.pool + pg.sc.inv[node] + (t.arg + 1) * kTileInvStride;
+        const int bad = potrf_trtri_tile(F + k1 + (long long)k1 * ld, ld, nb1, inv1, smem);
+        if (threadIdx.x == 0 && bad >= 0) atomicMin(info + node, fd.sep_start[node] + k1 + bad);
+      }
+      break;
+    }
+    case CT_SYG: {  // trailing tile (a, b) beyond group arg's block column -= L21 L21^T, K = group
+      const int k0 = group_k0(t.arg), k1 = group_k1(t.arg, s), rest = f - k1;
+      const double* L21 = F + k1 + (long long)k0 * ld;
+      double* A22 = F + k1 + (long long)k1 * ld;
+      gemm_tile<false, true, kCoopStages>(L21, ld, L21, ld, A22, ld, rest, rest, k1 - k0, t.a * kTile, t.b * kTile,
+                                          -1.0, 1.0, true, smem);
+      if (t.a == 0 && t.b == 0 && k1 < s) {  // the next group's first diagonal tile is final: factor it
+        __syncthreads();
+        const int p1 = k1 / kTile, nb1 = min(kTile, s - k1);
+        double* inv1 = pg.pool + pg.sc.inv[node] + p1 * kTileInvStride;
         const int bad = potrf_trtri_tile(F + k1 + (long long)k1 * ld, ld, nb1, inv1, smem);
         if (threadIdx.x == 0 && bad >= 0) atomicMin(info + node, fd.sep_start[node] + k1 + bad);
       }
@@ -200,11 +202,11 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
     }
     case CT_X2: {  // X[k.., c] = -inv Y[:, c] (c < panel) or X[k.., k..] = inv
       const int k = t.arg * kTile, nb = min(kTile, s - k), c = t.a * kTile;
-      const double* inv = pg.pool + pg.sc.inv[node] + (pg.df ? t.arg : (t.arg & 1)) * kTileInvStride;
+      const double* inv = pg.pool + pg.sc.inv[node] + t.arg * kTileInvStride;
       if (c < k) {  // X[k, c] = -inv sum_q Y_q[:, c]: sum the partials into Y_0, one GEMM
         const int nq = (k - c + kX1Chunk - 1) / kX1Chunk;
         const long long ysz = (long long)kTile * s * ((s + kX1Chunk - 1) / kX1Chunk);
-        double* Y0 = pg.pool + pg.sc.Y[node] + (pg.df ? (t.arg & 1) * ysz : 0) + (long long)c * kTile;
+        double* Y0 = pg.pool + pg.sc.Y[node] + (t.arg & 1) * ysz + (long long)c * kTile;
         if (nq > 1) {
           const long long qs = (long long)kTile * s;  // stride between partials
           constexpr int PER = kTile * kTile / 128;     // elements per thread (128 threads)
@@ -240,106 +242,6 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
                               1.0, 0.0, false, smem);
       break;
     }
-    case CT_CB: {  // panel <- [X; W21], chunk a of 4096 entries of the f x s panel
-      const long long total = (long long)f * s;
-      const long long e0 = (long long)t.a * 4096, e1 = min(total, e0 + 4096);
-      const double* W = pg.pool + pg.sc.W[node];
-      const int ldw = pg.sc.ldw[node];
-      for (long long idx = e0 + threadIdx.x; idx < e1; idx += blockDim.x) {
-        const int i = (int)(idx % f), j = (int)(idx / f);
-        double v;
-        if (i < s) v = i >= j ? __ldcg(X + i + (long long)j * ldx) : 0.0;
-        else v = __ldcg(W + (i - s) + (long long)j * ldw);
-        F[i + (long long)j * ld] = v;
-      }
-      break;
-    }
-    case CT_SP: {  // D_P = (M_PP)^{-1}
-      const int k = t.arg * kTile, nb = min(kTile, s - k);
-      double* D = pg.pool + pg.sc.inv[node] + (t.arg & 1) * kTileInvStride;
-      const int bad = gj_tile_inverse(F + k + (long long)k * ld, ld, nb, D, smem);
-      if (threadIdx.x == 0 && bad >= 0) atomicMin(info + node, fd.sep_start[node] + k + bad);
-      break;
-    }
-    case CT_SB: {  // B_I = C_I D_P, C_I = M_{I,P}
-      const int P = t.arg, k = P * kTile, nb = min(kTile, s - k), I = t.a;
-      const int r0 = sweep_rb(P, nb, I), m = min(kTile, f - r0);
-      const int ldb = pg.sc.ldw[node];
-      const double* D = pg.pool + pg.sc.inv[node] + (P & 1) * kTileInvStride;
-      double* Bc = pg.pool + pg.sc.X[node] + (long long)(P & 1) * ldb * kTile;
-      if (I > P - 1 && r0 > k) {  // below the panel: tile (I, P) stored
-        gemm_tile<false, false, kCoopStages>(F + r0 + (long long)k * ld, ld, D, kTile, Bc + r0, ldb, m, nb, nb,
-                                             0, 0, 1.0, 0.0, false, smem);
-      } else if (I == P - 1) {  // M_{P-1,P} = (M_{P,P-1})^T = (B^{(P-1)} rows of panel P)^T
-        const double* Bp = pg.pool + pg.sc.X[node] + (long long)((P - 1) & 1) * ldb * kTile;
-        gemm_tile<true, false, kCoopStages>(Bp + k, ldb, D, kTile, Bc + r0, ldb, m, nb, nb, 0, 0, 1.0, 0.0,
-                                            false, smem);
-      } else {  // above: M_{I,P} = (tile (P, I))^T
-        gemm_tile<true, false, kCoopStages>(F + k + (long long)r0 * ld, ld, D, kTile, Bc + r0, ldb, m, nb, nb,
-                                            0, 0, 1.0, 0.0, false, smem);
-      }
-      break;
-    }
-    case CT_SCP: {  // panel P's column <- B (map block a), or (b = 1) pivot tile <- -D_P
-      const int P = t.arg, k = P * kTile, nb = min(kTile, s - k), I = t.a;
-      const int ldb = pg.sc.ldw[node];
-      if (t.b == 1) {
-        const double* D = pg.pool + pg.sc.inv[node] + (P & 1) * kTileInvStride;
-        for (int e = threadIdx.x; e < kTile * kTile; e += blockDim.x) {
-          const int r = e & 63, c = e >> 6;
-          if (r < nb && c < nb && r >= c) F[(k + r) + (long long)(k + c) * ld] = -D[e];
-        }
-        break;
-      }
-      const double* Bc = pg.pool + pg.sc.X[node] + (long long)(P & 1) * ldb * kTile;
-      const int r0 = sweep_rb(P, nb, I), m = min(kTile, f - r0);
-      if (r0 > k) {  // below: tile (I, P) <- B_I
-        for (int e = threadIdx.x; e < kTile * kTile; e += blockDim.x) {
-          const int r = e & 63, c = e >> 6;
-          if (r < m && c < nb) F[(r0 + r) + (long long)(k + c) * ld] = Bc[(r0 + r) + (long long)c * ldb];
-        }
-      } else {  // above: tile (P, I) <- B_I^T
-        for (int e = threadIdx.x; e < kTile * kTile; e += blockDim.x) {
-          const int c = e & 63, r = e >> 6;  // row r of the pivot panel, column c of block I
-          if (r < nb && c < m) F[(k + r) + (long long)(r0 + c) * ld] = Bc[(r0 + c) + (long long)r * ldb];
-        }
-      }
-      break;
-    }
-    case CT_SC: {  // M_IJ -= B_I C_J^T on the lower tile (I >= J), I, J != P
-      const int P = t.arg, k = P * kTile, nb = min(kTile, s - k), I = t.a, J = t.b;
-      const int ldb = pg.sc.ldw[node];
-      const int ri = sweep_rb(P, nb, I), rj = sweep_rb(P, nb, J);
-      const int mi = min(kTile, f - ri), nj = min(kTile, f - rj);
-      const double* Bc = pg.pool + pg.sc.X[node] + (long long)(P & 1) * ldb * kTile;
-      double* Cij = F + ri + (long long)rj * ld;
-      if (rj > k)  // C_J = tile (J, P): B(kk, n) = M[rj + n][k + kk]
-        gemm_tile<false, true, kCoopStages>(Bc + ri, ldb, F + rj + (long long)k * ld, ld, Cij, ld, mi, nj, nb, 0, 0,
-                                            -1.0, 1.0, I == J, smem);
-      else  // C_J = M_{J,P} = (tile (P, J))^T: B(kk, n) = M[k + kk][rj + n]
-        gemm_tile<false, false, kCoopStages>(Bc + ri, ldb, F + k + (long long)rj * ld, ld, Cij, ld, mi, nj, nb, 0,
-                                             0, -1.0, 1.0, I == J, smem);
-      if (I == J && ri == k + nb && k + nb < s) {  // lookahead: next panel's pivot tile is final
-        __syncthreads();
-        const int k1 = k + nb, nb1 = min(kTile, s - k1);
-        double* D1 = pg.pool + pg.sc.inv[node] + ((P + 1) & 1) * kTileInvStride;
-        const int bad = gj_tile_inverse(F + k1 + (long long)k1 * ld, ld, nb1, D1, smem);
-        if (threadIdx.x == 0 && bad >= 0) atomicMin(info + node, fd.sep_start[node] + k1 + bad);
-      }
-      break;
-    }
-    case CT_SM: {  // separator tile (I, J), I >= J: v = -M (lower), write both triangles
-      const int r0 = t.a * kTile, c0 = t.b * kTile;
-      for (int e = threadIdx.x; e < kTile * kTile; e += blockDim.x) {
-        const int r = r0 + (e & 63), c = c0 + (e >> 6);
-        if (r < s && c < s && r >= c) {
-          const double v = -F[r + (long long)c * ld];
-          F[r + (long long)c * ld] = v;
-          if (r != c) F[c + (long long)r * ld] = v;
-        }
-      }
-      break;
-    }
   }
 }
 
@@ -349,23 +251,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-__global__ void __launch_bounds__(128) coop_factor_kernel(FrontDev fd, CoopProgram pg, int* info,
-                                                          unsigned long long* ptime) {
-  extern __shared__ __align__(16) double smem[];
-  cg::grid_group grid = cg::this_grid();
-  for (int ph = 0; ph < pg.nphases; ++ph) {
-    const CoopPhase P = pg.phases[ph];
-    for (int t = blockIdx.x; t < P.nt; t += gridDim.x) {
-      const CoopTask task = pg.tasks[P.t0 + t];
-      run_task(task, fd, pg, info, smem);
-      __syncthreads();
-    }
-    grid.sync();
-    if (ptime && blockIdx.x == 0 && threadIdx.x == 0) ptime[ph] = gtimer();
-  }
-}
-
-// Dataflow variant: CTAs pull tasks in the program's topological order from a global
+// Dataflow factorization: CTAs pull tasks in the program's topological order from a global
 // counter; a task's first thread waits (bounded) until each dependency counter reaches its
 // target, the task runs, and its counters are incremented after a fence. A task only waits
 // on earlier tasks and all CTAs are co-resident (cooperative launch), so the queue always
@@ -377,7 +263,7 @@ __global__ void __launch_bounds__(128, kDfCtasPerSm) coop_factor_df_kernel(Front
                                                              unsigned long long* trace) {
   extern __shared__ __align__(16) double smem[];
   constexpr int kWords = (int)(sizeof(DfTask) / sizeof(int));
-  static_assert(kWords <= 32, "task descriptor must fit one warp");
+  static_assert(kWords <= 32 && sizeof(DfTask) % sizeof(int) == 0, "task descriptor must fit one warp");
   __shared__ int ti_s[2];
   __shared__ DfTask tsh[2];  // current / next task (the next one is claimed and loaded ahead)
   const int tid = threadIdx.x;
@@ -419,7 +305,7 @@ __global__ void __launch_bounds__(128, kDfCtasPerSm) coop_factor_df_kernel(Front
     __syncthreads();
     if (tid < kSigs) {  // one thread per signal, each after its own release fence
       __threadfence();
-      if (t.sig[tid] >= 0) atomicAdd(ctr + t.sig[tid], 1);
+      if (t.sig[tid] >= 0) atomicAdd(ctr + t.sig[tid], (int)t.sw[tid]);
     }
     if (tid == 0) {
       if (trace) {
@@ -450,7 +336,6 @@ struct SolveProgram {
   const int* br_off;
   int nlevels;
   int nfr;  // number of forward reductions (offset of the backward counters)
-  int sweep;  // fronts hold [A11^{-1} (full); W21] (else [L11^{-1} (lower); W21])
   const double* wpool;  // dataflow: W21 rows (r >= s) read from here (CsTask w_off / ldw)
   int n;                // coarse size
 };
@@ -538,7 +423,7 @@ __device__ bool solve_fwd_task(const CsTask& t, const FrontDev& fd, const LevelV
   __syncthreads();
   if (t.mode == 1) {  // s <= 64: one thread per row, all separator columns
     const int r = t.r0 + tid;
-    const int ke = r < f ? (r < s ? (sp.sweep ? 0 : r + 1) : s) : 0;
+    const int ke = r < f ? (r < s ? r + 1 : s) : 0;
     const bool wr = sp.wpool && r >= s;  // dataflow factorization: W21 rows from the scratch pool
     const double* Fr = wr ? sp.wpool + t.w_off + (r - s) : F + r;
     const long long lr = wr ? (long long)t.ldw : ld;
@@ -564,7 +449,7 @@ __device__ bool solve_fwd_task(const CsTask& t, const FrontDev& fd, const LevelV
         for (int u = 0; u < 16; ++u) acc[u & 3] += k0 + u < ke ? fv[u] * sh.vs[k0 + u] : 0.0;
       }
       const double a = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-      if (r < s) ybuf[t.s0 + r] = sp.sweep ? sh.vs[r] : a;
+      if (r < s) ybuf[t.s0 + r] = a;
       else fd.upd[t.upd_off + (r - s)] = gu - a;
     }
     return true;
@@ -574,7 +459,7 @@ __device__ bool solve_fwd_task(const CsTask& t, const FrontDev& fd, const LevelV
   const int cg = t.span >> 2;  // columns per thread group: 64, or 16 (one batch, before the wait)
   const int kb = t.c0 + grp * cg;
   int ke = r < f ? min(kb + cg, s) : kb;
-  if (r < s) ke = sp.sweep ? kb : min(ke, r + 1);
+  if (r < s) ke = min(ke, r + 1);
   const bool wr = sp.wpool && r >= s;
   const double* Fr = wr ? sp.wpool + t.w_off + (r - s) : F + r;
   const long long lr = wr ? (long long)t.ldw : ld;
@@ -585,9 +470,8 @@ __device__ bool solve_fwd_task(const CsTask& t, const FrontDev& fd, const LevelV
   const int rw = t.r0 + tid;  // row finalized by this thread (tid < 64)
   GatherPre gv, gr;
   gv.load(lv, t.gat_base, kk, kk < s && tid < t.span);
-  gr.load(lv, t.gat_base, rw, tid < 64 && rw < f && (rw >= s || sp.sweep));
+  gr.load(lv, t.gat_base, rw, tid < 64 && rw < f && rw >= s);
   const double rv = kk < s ? rhs[t.s0 + kk] : 0.0;
-  const double rrw = (tid < 64 && rw < s && sp.sweep) ? rhs[t.s0 + rw] : 0.0;
   wait();
   sh.vs[tid] = (kk < s && tid < t.span) ? rv + gv.value(lv, fd.upd) : 0.0;
   __syncthreads();
@@ -603,7 +487,7 @@ __device__ bool solve_fwd_task(const CsTask& t, const FrontDev& fd, const LevelV
   sh.red[grp][rr] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
   __syncthreads();
   auto finish = [&](double a) {
-    if (rw < s) ybuf[t.s0 + rw] = sp.sweep ? rrw + gr.value(lv, fd.upd) : a;
+    if (rw < s) ybuf[t.s0 + rw] = a;
     else fd.upd[t.upd_off + (rw - s)] = gr.value(lv, fd.upd) - a;
   };
   if (t.np == 1) {
@@ -651,7 +535,7 @@ __device__ bool solve_bwd_task(const CsTask& t, const FrontDev& fd, const SolveP
 #pragma unroll
       for (int cc = 0; cc < 8; ++cc) {
         const int k = kw + cc;
-        const bool ok = k < s && r < f && (sp.sweep || r >= s || r >= k);
+        const bool ok = k < s && r < f && (r >= s || r >= k);
         fv[h][cc] = ok ? __ldcs(Fr + (long long)k * lr) : 0.0;
       }
     }
@@ -702,36 +586,6 @@ __device__ bool solve_bwd_task(const CsTask& t, const FrontDev& fd, const SolveP
   if (tid < 64 && k < s) sol[t.s0 + k] = a;
   if (tid == 0) cnt_b[t.red] = 0;
   return true;
-}
-
-// Level-synchronous solve: each level is one phase between grid barriers.
-__global__ void __launch_bounds__(256) coop_solve_kernel(FrontDev fd, LevelView lv, SolveProgram sp,
-                                                         const double* __restrict__ rhs,
-                                                         double* __restrict__ sol,
-                                                         double* __restrict__ partial,
-                                                         double* __restrict__ ybuf, int* __restrict__ cnt,
-                                                         unsigned long long* __restrict__ ptime) {
-  __shared__ SolveShared sh;
-  cg::grid_group grid = cg::this_grid();
-  int sync_id = 1;
-  if (ptime && blockIdx.x == 0 && threadIdx.x == 0) ptime[0] = gtimer();
-  auto gsync = [&]() {
-    grid.sync();
-    if (ptime && blockIdx.x == 0 && threadIdx.x == 0) ptime[sync_id] = gtimer();
-    ++sync_id;
-  };
-  int* cnt_f = cnt;
-  int* cnt_b = cnt + sp.nfr;
-  for (int l = 0; l < sp.nlevels; ++l) {
-    for (int ti = sp.ft_off[l] + blockIdx.x; ti < sp.ft_off[l + 1]; ti += gridDim.x)
-      solve_fwd_task(sp.ft[ti], fd, lv, sp, rhs, partial, ybuf, cnt_f, sh, [] {});
-    gsync();
-  }
-  for (int l = sp.nlevels - 1; l >= 0; --l) {
-    for (int ti = sp.bt_off[l] + blockIdx.x; ti < sp.bt_off[l + 1]; ti += gridDim.x)
-      solve_bwd_task(sp.bt[ti], fd, sp, sol, partial, ybuf, cnt_b, sh, [] {});
-    gsync();
-  }
 }
 
 // Dataflow solve: one queue (forward tasks bottom-up, then backward tasks top-down). A
@@ -850,29 +704,18 @@ __global__ void __launch_bounds__(256, 3) coop_solve_df_kernel(FrontDev fd, Leve
 // ---------------------------------------------------------------------------------------
 
 struct CoopState {
-  std::vector<int> phase_type;  // first task type of each phase (diagnostics)
-  std::vector<int> phase_nt;
-  unsigned long long* ptime = nullptr;
   CoopProgram pg{};
   SolveProgram sp{};
-  unsigned long long* stime = nullptr;  // per grid.sync timestamps of the solve (diagnostics)
   int grid_f = 0, grid_s = 0;
   size_t smem_f = 0;
-  // dataflow factorization
-  bool df = false;
   DfTask* dtasks = nullptr;
   int ndtasks = 0;
   int* ctr = nullptr;  // [nctr] dependency counters + queue head + error flag
   int nctr = 0;
-  bool solve_df = true;  // dataflow coarse solve (BDDC_SOLVE_DF=0: level-synchronous)
+  unsigned long long* prof = nullptr;  // BDDC_COOP_TIMING: per task type wait / run cycles
 };
 
 static std::map<const Ctx*, CoopState> g_coop;
-
-bool coarse_df_enabled(const Ctx& c) {
-  const char* e = getenv("BDDC_COARSE_DF");
-  return !c.coarse_sweep && !(e && atoi(e) == 0);
-}
 
 long long coarse_df_layout(const FrontPlan& fp, std::vector<long long>& inv, std::vector<long long>& Y,
                            std::vector<long long>& W, std::vector<int>& ldw) {
@@ -897,84 +740,41 @@ void coop_build(Ctx& c) {
   CoopState& st = g_coop[&c];
   st = CoopState{};
   st.smem_f = sizeof(double) * std::max<int>(gemm_smem_doubles<kCoopStages>(), kFactSmemDoubles);
-  BDDC_CUDA(cudaFuncSetAttribute(coop_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st.smem_f));
   BDDC_CUDA(cudaFuncSetAttribute(coop_factor_df_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st.smem_f));
   int nsm = 0, per_f = 0, per_s = 0;
   BDDC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device));
-  BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_f, coop_factor_kernel, 128, st.smem_f));
-  BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_s, coop_solve_kernel, 256, 0));
-  {
-    int per_sd = 0;
-    BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sd, coop_solve_df_kernel, 256, 0));
-    st.solve_df = coarse_solve_df_enabled();
-    if (st.solve_df) per_s = per_sd;  // no grid barrier: as many CTAs as fit
-  }
-  // few CTAs: the phases are small at the top of the tree and grid.sync cost grows with
-  // the number of arriving CTAs
-  st.df = coarse_df_enabled(c);
-  if (st.df) {
-    int per_df = 0;
-    BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_df, coop_factor_df_kernel, 128, st.smem_f));
-    st.grid_f = nsm * std::max(std::min(per_df, kDfCtasPerSm), 1);
-  } else {
-    st.grid_f = nsm * std::max(std::min(per_f, 2), 1);
-  }
+  BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_s, coop_solve_df_kernel, 256, 0));
+  BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_f, coop_factor_df_kernel, 128, st.smem_f));
+  st.grid_f = nsm * std::max(std::min(per_f, kDfCtasPerSm), 1);
   st.grid_s = nsm * std::max(std::min(per_s, 4), 1);
   const int grid_f = st.grid_f;
   const int N = fp.nnodes, L = fp.nlevels;
-  std::vector<CoopTask> tasks;
-  std::vector<CoopPhase> phases;
-  std::vector<long long> inv(N, 0), X(N, 0), Y(N, 0), W(N, 0);
-  std::vector<int> ldx(N, 2), ldw(N, 2);
+  std::vector<long long> inv(N, 0), Y(N, 0), W(N, 0);
+  std::vector<int> ldw(N, 2);
   long long pool = 2;
-  auto phase_begin = [&]() { phases.push_back(CoopPhase{(int)tasks.size(), 0}); };
-  auto phase_end = [&]() {
-    phases.back().nt = (int)tasks.size() - phases.back().t0;
-    if (phases.back().nt == 0) phases.pop_back();
-  };
-  // extend-add of child slot k into the fronts of level l (column chunks sized for >= 2 tasks
-  // per CTA). It reads only the children's update blocks (columns >= s) and writes only the
-  // parents, so it shares the children's level's W (k = 0) and CB (k = 1) phases, which touch
-  // only the children's panel columns; child order is kept (deterministic sums).
   int max_children = 0;
   for (int nd = 0; nd < N; ++nd) max_children = std::max(max_children, fp.child_ptr[nd + 1] - fp.child_ptr[nd]);
-  auto emit_ea = [&](int l, int k) {
-    long long cols = 0;
-    for (int i = fp.level_ptr[l]; i < fp.level_ptr[l + 1]; ++i) {
-      const int nd = fp.level_list[i];
-      if (fp.child_ptr[nd + 1] - fp.child_ptr[nd] > k) cols += fp.bnd_size[fp.child_list[fp.child_ptr[nd] + k]];
-    }
-    int chunk = 64;
-    while (chunk > 2 && cols / chunk < 2LL * grid_f) chunk >>= 1;
-    for (int i = fp.level_ptr[l]; i < fp.level_ptr[l + 1]; ++i) {
-      const int nd = fp.level_list[i];
-      if (fp.child_ptr[nd + 1] - fp.child_ptr[nd] <= k) continue;
-      const int ch = fp.child_list[fp.child_ptr[nd] + k];
-      for (int q = 0; q < fp.bnd_size[ch]; q += chunk) tasks.push_back(CoopTask{CT_EA, nd, q, chunk, k});
-    }
-  };
-  // ---- dataflow program (default for the Cholesky formulation) ----
-  st.df = coarse_df_enabled(c);
-  if (st.df) {
+  // ---- dataflow factorization program ----
+  {
     std::vector<DfTask> dt;
     int nctr = 0;
     auto newc = [&](int n) { const int b = nctr; nctr += n; return b; };
     // per node counter bases and totals
     std::vector<int> c_ea(N), c_syall(N), c_pt(N), c_tsr(N), c_upd(N), c_x1(N), c_x2(N), c_x2row(N),
-        c_x2col(N), c_x2all(N), c_tsall(N), c_w(N), c_syrd(N), nT(N), nP(N), tot_sy(N, 0), tot_ts(N, 0),
+        c_x2col(N), c_x2all(N), c_tsall(N), c_w(N), c_gts(N), nT(N), nP(N), tot_sy(N, 0), tot_ts(N, 0),
         tot_w(N, 0), tot_x2(N, 0);
     std::vector<std::vector<int>> nea(N);
     for (int nd = 0; nd < N; ++nd) {
       const int s = fp.sep_size[nd], f = s + fp.bnd_size[nd];
-      const int T = ceil_div(std::max(f, 1), kTile), np = ceil_div(s, kTile);
+      const int T = ceil_div(std::max(f, 1), kTile), np = ceil_div(s, kTile), ng = ceil_div(s, kGroup * kTile);
       nT[nd] = T; nP[nd] = np;
       c_ea[nd] = newc(std::max(1, fp.child_ptr[nd + 1] - fp.child_ptr[nd]));
       c_syall[nd] = newc(1); c_tsall[nd] = newc(1); c_w[nd] = newc(1); c_x2all[nd] = newc(1);
       c_pt[nd] = newc(std::max(np, 1));
       c_tsr[nd] = newc(std::max(np * T, 1));
-      c_upd[nd] = newc(T * (T + 1) / 2);
+      c_gts[nd] = newc(std::max(ng, 1));        // TS tasks done per panel group
+      c_upd[nd] = newc(T * (T + 1) / 2);        // panels applied per (lower) absolute tile
       c_x1[nd] = newc(std::max(np, 1));         // X1 tasks done per panel row
-      c_syrd[nd] = newc(std::max(np * T, 1));   // SY readers done per (panel, relative row tile)
       c_x2[nd] = newc(std::max(np * np, 1));
       c_x2row[nd] = newc(std::max(np, 1));
       c_x2col[nd] = newc(std::max(np, 1));
@@ -986,6 +786,7 @@ void coop_build(Ctx& c) {
       t.t = CoopTask{type, nd, a, b, arg};
       for (int d = 0; d < kDeps; ++d) { t.dep[d] = -1; t.tgt[d] = 0; }
       for (int q = 0; q < kSigs; ++q) t.sig[q] = -1;
+      for (int q = 0; q < 8; ++q) t.sw[q] = 1;
       return t;
     };
     auto dep = [&](DfTask& t, int cix, int tgt) {
@@ -994,15 +795,15 @@ void coop_build(Ctx& c) {
         if (t.dep[d] < 0) { t.dep[d] = cix; t.tgt[d] = tgt; return; }
       throw std::runtime_error("coarse dataflow: too many dependencies");
     };
-    auto sig = [&](DfTask& t, int cix) {
+    auto sig = [&](DfTask& t, int cix, int w = 1) {
       for (int q = 0; q < kSigs; ++q)
-        if (t.sig[q] < 0) { t.sig[q] = cix; return; }
+        if (t.sig[q] < 0) { t.sig[q] = cix; t.sw[q] = (unsigned char)w; return; }
       throw std::runtime_error("coarse dataflow: too many signals");
     };
     const long long off = coarse_df_layout(fp, inv, Y, W, ldw);  // X lives in the fronts
     // the local setup's T tiles (no dependencies): the simulated schedule places them in the
     // CTA time the critical path leaves idle
-    c.lt_fusable = c.geo.nG_pad > 0 && c.geo.nG_pad % kTile == 0 && !getenv("BDDC_NO_T_IN_COARSE");
+    c.lt_fusable = c.geo.nG_pad > 0 && c.geo.nG_pad % kTile == 0;
     if (c.lt_fusable) {
       const int nt = c.geo.nG_pad / kTile;
       for (int sub = c.geo.s_lo; sub < c.geo.s_hi; ++sub)
@@ -1049,20 +850,64 @@ void coop_build(Ctx& c) {
         auto tiles_of = [&](int r0, int r1) {  // absolute 64-tiles overlapping rows [r0, r1)
           return std::make_pair(r0 / kTile, (std::min(r1, f) - 1) / kTile);
         };
-        for (int p = 0; p < np; ++p) {
-          const int k = p * kTile, nb = std::min(kTile, s - k), rest = f - k - nb, nt = ceil_div(rest, kTile);
-          for (int a = 0; a < nt; ++a) {
-            DfTask t = mk(CT_TS, nd, a, 0, p);
-            dep(t, c_pt[nd] + p, 1);
-            if (p > 0) {
-              const auto ti = tiles_of(k + nb + a * kTile, k + nb + a * kTile + kTile);
-              for (int I = ti.first; I <= ti.second; ++I) dep(t, upd(nd, I, p), p);
+        // tile (I, J) holds every update of the panels before p (TS / SY / SYG readiness)
+        auto dep_tile = [&](DfTask& t, int r0, int c0, int p) {
+          if (p <= 0) return;
+          const auto ri = tiles_of(r0, r0 + kTile), ci = tiles_of(c0, c0 + kTile);
+          for (int I = ri.first; I <= ri.second; ++I)
+            for (int J = ci.first; J <= ci.second; ++J)
+              if (I >= J) dep(t, upd(nd, I, J), p);
+        };
+        // ---- factorization: panels in groups of kGroup ----
+        const int ng = ceil_div(s, kGroup * kTile);
+        for (int g = 0; g < ng; ++g) {
+          const int k0 = group_k0(g), k1 = group_k1(g, s), p0 = k0 / kTile, p1 = ceil_div(k1, kTile);
+          int gts = 0;  // TS tasks of this group
+          for (int p = p0; p < p1; ++p) {
+            const int k = p * kTile, nb = std::min(kTile, s - k), rest = f - k - nb, nt = ceil_div(rest, kTile);
+            for (int a = 0; a < nt; ++a) {
+              DfTask t = mk(CT_TS, nd, a, 0, p);
+              dep(t, c_pt[nd] + p, 1);
+              dep_tile(t, k + nb + a * kTile, k, p);
+              sig(t, c_tsr[nd] + p * T + a);
+              sig(t, c_tsall[nd]);
+              sig(t, c_gts[nd] + g);
+              dt.push_back(t);
+              tot_ts[nd]++;
+              gts++;
             }
-            sig(t, c_tsr[nd] + p * T + a);
-            sig(t, c_tsall[nd]);
-            dt.push_back(t);
-            tot_ts[nd]++;
+            // right-looking updates inside the group's block column (columns [k + nb, k1))
+            const int ncol = ceil_div(k1 - k - nb, kTile);
+            for (int a = 0; a < nt; ++a)
+              for (int bb = 0; bb <= a && bb < ncol; ++bb) {
+                DfTask t = mk(CT_SY, nd, a, bb, p);
+                dep(t, c_tsr[nd] + p * T + a, 1);
+                if (bb != a) dep(t, c_tsr[nd] + p * T + bb, 1);
+                dep_tile(t, k + nb + a * kTile, k + nb + bb * kTile, p);
+                if (nb == kTile) sig(t, upd(nd, p + 1 + a, p + 1 + bb));
+                sig(t, c_syall[nd]);
+                if (a == 0 && bb == 0 && k + nb < s) sig(t, c_pt[nd] + p + 1);  // lookahead PT
+                dt.push_back(t);
+                tot_sy[nd]++;
+              }
           }
+          // the trailing matrix beyond the block column, once for the whole group (K = k1 - k0)
+          const int ntg = ceil_div(f - k1, kTile);
+          for (int a = 0; a < ntg; ++a)
+            for (int bb = 0; bb <= a; ++bb) {
+              DfTask t = mk(CT_SYG, nd, a, bb, g);
+              dep(t, c_gts[nd] + g, gts);
+              dep_tile(t, k1 + a * kTile, k1 + bb * kTile, p0);
+              if (k1 < s) sig(t, upd(nd, p1 + a, p1 + bb), p1 - p0);  // (k1 aligned: full group)
+              sig(t, c_syall[nd]);
+              if (a == 0 && bb == 0 && k1 < s) sig(t, c_pt[nd] + p1);  // lookahead PT
+              dt.push_back(t);
+              tot_sy[nd]++;
+            }
+        }
+        // ---- X = L11^{-1} in place over L11, after the whole factorization of this front
+        // (every TS / SY / SYG read of L11 is then done) ----
+        for (int p = 0; p < np; ++p) {
           for (int cc = 0; cc < p; ++cc)
             for (int qq = 0; qq < p - cc; ++qq) {  // kX1Chunk = 64: chunk qq is column block m
               const int m = cc + qq;
@@ -1073,37 +918,11 @@ void coop_build(Ctx& c) {
               sig(t, c_x1[nd] + p);
               dt.push_back(t);
             }
-          for (int a = 0; a < nt; ++a)
-            for (int bb = 0; bb <= a; ++bb) {
-              DfTask t = mk(CT_SY, nd, a, bb, p);
-              dep(t, c_tsr[nd] + p * T + a, 1);
-              if (bb != a) dep(t, c_tsr[nd] + p * T + bb, 1);
-              if (p > 0) {
-                const auto ri = tiles_of(k + nb + a * kTile, k + nb + a * kTile + kTile);
-                const auto ci = tiles_of(k + nb + bb * kTile, k + nb + bb * kTile + kTile);
-                for (int I = ri.first; I <= ri.second; ++I)
-                  for (int J = ci.first; J <= ci.second; ++J)
-                    if (I >= J) dep(t, upd(nd, I, J), p);
-              }
-              if (nb == kTile) sig(t, upd(nd, p + 1 + a, p + 1 + bb));
-              sig(t, c_syall[nd]);
-              // readers of the separator rows of L[:, p] (X2 overwrites them with X in place)
-              if (p + 1 + a < np) sig(t, c_syrd[nd] + p * T + a);
-              if (bb != a && p + 1 + bb < np) sig(t, c_syrd[nd] + p * T + bb);
-              if (a == 0 && bb == 0 && k + nb < s) sig(t, c_pt[nd] + p + 1);
-              dt.push_back(t);
-              tot_sy[nd]++;
-            }
           for (int cc = 0; cc <= p; ++cc) {
             DfTask t = mk(CT_X2, nd, cc, 0, p);
             dep(t, c_pt[nd] + p, 1);
-            if (cc < p) {
-              // X[p, cc] replaces L[p, cc] in place: every X1 of row p and every SY tile of
-              // panel cc that reads L's row tile p must be done
-              dep(t, c_x1[nd] + p, p * (p + 1) / 2);
-              const int ntc = ceil_div(f - (cc + 1) * kTile, kTile);
-              dep(t, c_syrd[nd] + cc * T + (p - cc - 1), ntc);
-            }
+            dep(t, c_syall[nd], tot_sy[nd]);
+            if (cc < p) dep(t, c_x1[nd] + p, p * (p + 1) / 2);  // every X1 of row p read L[p, .]
             sig(t, c_x2[nd] + p * np + cc);
             sig(t, c_x2row[nd] + p);
             sig(t, c_x2col[nd] + cc);
@@ -1124,7 +943,7 @@ void coop_build(Ctx& c) {
               tot_w[nd]++;
             }
         }
-        // no CB: X is written in place by X2 and W21 stays in the scratch pool for the solve
+        // W21 stays in the scratch pool for the solve; X is in place in the front
       }
     }
     pool = std::max(pool, off);
@@ -1147,6 +966,11 @@ void coop_build(Ctx& c) {
           case CT_SY: {
             const int k = q.arg * kTile;
             return (q.a == 0 && q.b == 0 && k + kTile < s) ? 10.7 + 15.0 : 10.7;  // + lookahead PT
+          }
+          case CT_SYG: {
+            const int k0 = group_k0(q.arg), k1 = group_k1(q.arg, s);
+            const double run = 4.0 + 6.7 * (k1 - k0) / 64.0;
+            return (q.a == 0 && q.b == 0 && k1 < s) ? run + 15.0 : run;
           }
           case CT_X2: return 6.9;
           case CT_W: return 9.1;
@@ -1200,7 +1024,7 @@ void coop_build(Ctx& c) {
         for (int q = 0; q < kSigs; ++q) {
           const int cix = t.sig[q];
           if (cix < 0) continue;
-          ++cval[cix];
+          cval[cix] += t.sw[q];
           auto& w = wait[cix];
           while (wptr[cix] < (int)w.size() && w[wptr[cix]].first <= cval[cix])
             if (--ndep[w[wptr[cix]++].second] == 0) ready.push(w[wptr[cix] - 1].second);
@@ -1220,179 +1044,19 @@ void coop_build(Ctx& c) {
     st.nctr = nctr;
     st.ctr = c.alloc<int>(nctr + 2);  // + queue head + error flag
   }
-  for (int l = 0; l < L && c.coarse_sweep; ++l) {
-    // ---- block symmetric sweep program ----
-    std::vector<int> nodes(fp.level_list.begin() + fp.level_ptr[l], fp.level_list.begin() + fp.level_ptr[l + 1]);
-    long long off = 0;
-    int max_np = 0;
-    for (int nd : nodes) {
-      const int s = fp.sep_size[nd], f = s + fp.bnd_size[nd];
-      ldw[nd] = (int)round_up(std::max(f, 2), 2);  // B buffers: f x 64, two parities
-      inv[nd] = off; off += 2 * kTileInvStride;
-      X[nd] = off; off += 2LL * ldw[nd] * kTile;
-      max_np = std::max(max_np, ceil_div(s, kTile));
-    }
-    pool = std::max(pool, off);
-    phase_begin();
-    for (int nd : nodes)
-      if (fp.sep_size[nd] > 0) tasks.push_back(CoopTask{CT_SP, nd, 0, 0, 0});
-    phase_end();
-    auto emit_copy = [&](int P) {  // panel P's column <- B, pivot <- -D (nodes that have panel P)
-      for (int nd : nodes) {
-        const int s = fp.sep_size[nd], f = s + fp.bnd_size[nd];
-        if (s <= P * kTile) continue;
-        const int nb = std::min(kTile, s - P * kTile);
-        for (int I = 0; I < sweep_nblocks(P, nb, f); ++I) tasks.push_back(CoopTask{CT_SCP, nd, I, 0, P});
-        tasks.push_back(CoopTask{CT_SCP, nd, 0, 1, P});  // b = 1: the pivot tile
-      }
-    };
-    for (int P = 0; P < max_np; ++P) {
-      phase_begin();
-      for (int nd : nodes) {
-        const int s = fp.sep_size[nd], f = s + fp.bnd_size[nd];
-        if (s <= P * kTile) continue;
-        const int nb = std::min(kTile, s - P * kTile);
-        for (int I = 0; I < sweep_nblocks(P, nb, f); ++I) tasks.push_back(CoopTask{CT_SB, nd, I, 0, P});
-      }
-      if (P > 0) emit_copy(P - 1);
-      phase_end();
-      phase_begin();
-      for (int nd : nodes) {
-        const int s = fp.sep_size[nd], f = s + fp.bnd_size[nd];
-        if (s <= P * kTile) continue;
-        const int nb = std::min(kTile, s - P * kTile);
-        const int nbk = sweep_nblocks(P, nb, f);
-        for (int I = 0; I < nbk; ++I)
-          for (int J = 0; J <= I; ++J) tasks.push_back(CoopTask{CT_SC, nd, I, J, P});
-      }
-      phase_end();
-    }
-    phase_begin();
-    emit_copy(max_np - 1);
-    phase_end();
-    phase_begin();
-    for (int nd : nodes) {
-      const int s = fp.sep_size[nd];
-      for (int I = 0; I < ceil_div(s, kTile); ++I)
-        for (int J = 0; J <= I; ++J) tasks.push_back(CoopTask{CT_SM, nd, I, J, 0});
-    }
-    if (l + 1 < L) emit_ea(l + 1, 0);
-    phase_end();
-    for (int k = 1; l + 1 < L && k < max_children; ++k) {
-      phase_begin();
-      emit_ea(l + 1, k);
-      phase_end();
-    }
-  }
-  for (int l = 0; l < L && !c.coarse_sweep && !st.df; ++l) {
-    std::vector<int> nodes(fp.level_list.begin() + fp.level_ptr[l], fp.level_list.begin() + fp.level_ptr[l + 1]);
-    // scratch for this level (reused by the next level after its CB phase)
-    long long off = 0;
-    int max_np = 0, max_ch = 0;
-    for (int nd : nodes) {
-      const int s = fp.sep_size[nd], b = fp.bnd_size[nd];
-      ldx[nd] = (int)round_up(std::max(s, 2), 2);
-      ldw[nd] = (int)round_up(std::max(b, 2), 2);
-      inv[nd] = off; off += 2 * kTileInvStride;
-      X[nd] = off; off += round_up((long long)ldx[nd] * std::max(s, 1), 2);
-      Y[nd] = off; off += round_up((long long)kTile * std::max(s, 1), 2) * ceil_div(std::max(s, 1), kX1Chunk);
-      W[nd] = off; off += round_up((long long)ldw[nd] * std::max(s, 1), 2);
-      max_np = std::max(max_np, ceil_div(s, kTile));
-      max_ch = std::max(max_ch, fp.child_ptr[nd + 1] - fp.child_ptr[nd]);
-    }
-    pool = std::max(pool, off);
-    for (int p = 0; p < max_np; ++p) {
-      if (p == 0) {  // later diagonal tiles are factored by the lookahead in SY(p-1)
-        phase_begin();
-        for (int nd : nodes)
-          if (fp.sep_size[nd] > 0) tasks.push_back(CoopTask{CT_PT, nd, 0, 0, 0});
-        phase_end();
-      }
-      phase_begin();
-      for (int nd : nodes) {
-        const int s = fp.sep_size[nd], f = s + fp.bnd_size[nd];
-        if (s <= p * kTile) continue;
-        const int k = p * kTile, nb = std::min(kTile, s - k), rest = f - k - nb;
-        for (int a = 0; a < ceil_div(rest, kTile); ++a) tasks.push_back(CoopTask{CT_TS, nd, a, 0, p});
-        for (int cc = 0; cc < p; ++cc)
-          for (int qq = 0; qq < ceil_div(k - cc * kTile, kX1Chunk); ++qq) tasks.push_back(CoopTask{CT_X1, nd, cc, qq, p});
-      }
-      phase_end();
-      phase_begin();
-      for (int nd : nodes) {
-        const int s = fp.sep_size[nd], f = s + fp.bnd_size[nd];
-        if (s <= p * kTile) continue;
-        const int k = p * kTile, nb = std::min(kTile, s - k), rest = f - k - nb;
-        const int nt = ceil_div(rest, kTile);
-        for (int a = 0; a < nt; ++a)
-          for (int b = 0; b <= a; ++b) tasks.push_back(CoopTask{CT_SY, nd, a, b, p});
-        (void)0;
-        for (int cc = 0; cc <= p; ++cc) tasks.push_back(CoopTask{CT_X2, nd, cc, 0, p});
-      }
-      phase_end();
-    }
-    phase_begin();
-    for (int nd : nodes) {
-      const int s = fp.sep_size[nd], b = fp.bnd_size[nd];
-      if (s == 0 || b == 0) continue;
-      for (int a = 0; a < ceil_div(b, kTile); ++a)
-        for (int cc = 0; cc < ceil_div(s, kTile); ++cc) tasks.push_back(CoopTask{CT_W, nd, a, cc, 0});
-    }
-    if (l + 1 < L) emit_ea(l + 1, 0);
-    phase_end();
-    phase_begin();
-    for (int nd : nodes) {
-      const int s = fp.sep_size[nd], f = s + fp.bnd_size[nd];
-      const long long tot = (long long)f * s;
-      for (long long q = 0; q < (tot + 4095) / 4096; ++q) tasks.push_back(CoopTask{CT_CB, nd, (int)q, 0, 0});
-    }
-    if (l + 1 < L && max_children > 1) emit_ea(l + 1, 1);
-    phase_end();
-    for (int k = 2; l + 1 < L && k < max_children; ++k) {
-      phase_begin();
-      emit_ea(l + 1, k);
-      phase_end();
-    }
-  }
-  for (const auto& ph : phases) {
-    st.phase_type.push_back(tasks[ph.t0].type);
-    st.phase_nt.push_back(ph.nt);
-  }
-  if (getenv("BDDC_COOP_TIMING")) {
-    st.ptime = c.alloc<unsigned long long>(std::max<size_t>(phases.size() + 1, 48));
-    st.stime = c.alloc<unsigned long long>(2 * L + 1);
-  }
-  st.pg.df = st.df ? 1 : 0;
-  st.pg.tasks = c.upload(tasks.data(), tasks.size());
-  st.pg.phases = c.upload(phases.data(), phases.size());
-  st.pg.nphases = (int)phases.size();
+  if (getenv("BDDC_COOP_TIMING")) st.prof = c.alloc<unsigned long long>(3 * CT_NTYPES);
   st.pg.sc.inv = c.upload(inv.data(), N);
-  st.pg.sc.X = c.upload(X.data(), N);
   st.pg.sc.Y = c.upload(Y.data(), N);
   st.pg.sc.W = c.upload(W.data(), N);
-  st.pg.sc.ldx = c.upload(ldx.data(), N);
   st.pg.sc.ldw = c.upload(ldw.data(), N);
   st.pg.pool = c.alloc<double>(pool);
-  // solve program: the per-level task arrays already built for the tiled solve
-  std::vector<int> ft_off(L + 1), bt_off(L + 1), fr_off(L + 1), br_off(L + 1);
-  for (int l = 0; l <= L; ++l) {
-    ft_off[l] = l < L ? (int)(ls.fwd_t[l] - ls.fwd_t[0]) : (int)(ls.fwd_t[L - 1] - ls.fwd_t[0]) + ls.n_fwd_t[L - 1];
-    bt_off[l] = l < L ? (int)(ls.bwd_t[l] - ls.bwd_t[0]) : (int)(ls.bwd_t[L - 1] - ls.bwd_t[0]) + ls.n_bwd_t[L - 1];
-    fr_off[l] = l < L ? (int)(ls.fwd_r[l] - ls.fwd_r[0]) : (int)(ls.fwd_r[L - 1] - ls.fwd_r[0]) + ls.n_fwd_r[L - 1];
-    br_off[l] = l < L ? (int)(ls.bwd_r[l] - ls.bwd_r[0]) : (int)(ls.bwd_r[L - 1] - ls.bwd_r[0]) + ls.n_bwd_r[L - 1];
-  }
-  st.sp.ft = ls.fwd_t[0];
-  st.sp.bt = ls.bwd_t[0];
+  // solve program: reductions of the forward / backward chunk partials
+  int nfr = 0;
+  for (int l = 0; l < L; ++l) nfr += ls.n_fwd_r[l];
   st.sp.fr = ls.fwd_r[0];
   st.sp.br = ls.bwd_r[0];
-  st.sp.ft_off = c.upload(ft_off.data(), L + 1);
-  st.sp.bt_off = c.upload(bt_off.data(), L + 1);
-  st.sp.fr_off = c.upload(fr_off.data(), L + 1);
-  st.sp.br_off = c.upload(br_off.data(), L + 1);
-  st.sp.nlevels = L;
-  st.sp.nfr = fr_off[L];
-  st.sp.sweep = c.coarse_sweep ? 1 : 0;
-  st.sp.wpool = st.df ? st.pg.pool : nullptr;
+  st.sp.nfr = nfr;
+  st.sp.wpool = st.pg.pool;
   st.sp.n = fp.n_coarse;
 }
 
@@ -1402,102 +1066,68 @@ void coop_factor(Ctx& c, cudaStream_t s) {
   CoopState& st = g_coop.at(&c);
   FrontDev fd = c.fp.d;
   int* info = c.fp.info;
-  if (st.df) {
-    BDDC_CUDA(cudaMemsetAsync(st.ctr, 0, sizeof(int) * (st.nctr + 2), s));
-    int* qhead = st.ctr + st.nctr;
-    int* err = st.ctr + st.nctr + 1;
-    const DfTask* tasks = st.dtasks;
-    int ntasks = st.ndtasks;
-    unsigned long long* prof = nullptr;
-    unsigned long long* trace = nullptr;
-    const char* tpath = getenv("BDDC_COOP_TRACE");  // per-task timestamps (diagnostics)
-    if (tpath) trace = c.alloc<unsigned long long>((size_t)ntasks * 4);
-    if (st.ptime) {
-      prof = st.ptime;  // >= 48 entries (phases of the phased program are not used here)
-      BDDC_CUDA(cudaMemsetAsync(prof, 0, sizeof(unsigned long long) * 48, s));
-    }
-    st.pg.lt = c.lt_defer;
-    void* dargs[] = {&fd, &st.pg, (void*)&tasks, &ntasks, &st.ctr, &qhead, &info, &err, &prof, &trace};
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (st.ptime) {
-      BDDC_CUDA(cudaEventCreate(&e0));
-      BDDC_CUDA(cudaEventCreate(&e1));
-      BDDC_CUDA(cudaEventRecord(e0, s));
-    }
-    BDDC_CUDA(cudaLaunchCooperativeKernel((void*)coop_factor_df_kernel, st.grid_f, 128, dargs, st.smem_f, s));
-    BDDC_COUNT();
-    int herr = 0, serr = 0;  // (serr: a dataflow coarse solve since the last setup timed out)
-    BDDC_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
-    BDDC_CUDA(cudaMemcpyAsync(&serr, c.sched.df_ctr + c.sched.n_ctr + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
-    BDDC_CUDA(cudaStreamSynchronize(s));
-    if (herr) throw CudaError("coarse dataflow factorization: dependency wait timed out");
-    if (serr) throw CudaError("coarse dataflow solve: dependency wait timed out");
-    if (trace) {  // binary: ntasks, then per task DfTask + 4 x u64 (dequeue, ready, end, cta)
-      std::vector<DfTask> ht(ntasks);
-      std::vector<unsigned long long> tr((size_t)ntasks * 4);
-      BDDC_CUDA(cudaMemcpy(ht.data(), tasks, sizeof(DfTask) * ntasks, cudaMemcpyDeviceToHost));
-      BDDC_CUDA(cudaMemcpy(tr.data(), trace, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost));
-      if (FILE* fo = fopen(tpath, "wb")) {
-        const int hdr[4] = {ntasks, (int)sizeof(DfTask), kDeps, kSigs};
-        fwrite(hdr, sizeof(int), 4, fo);
-        fwrite(ht.data(), sizeof(DfTask), ntasks, fo);
-        fwrite(tr.data(), sizeof(unsigned long long), tr.size(), fo);
-        fclose(fo);
-      }
-    }
-    if (st.ptime) {
-      BDDC_CUDA(cudaEventRecord(e1, s));
-      BDDC_CUDA(cudaEventSynchronize(e1));
-      float ms = 0.f;
-      BDDC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-      fprintf(stderr, "coop factor (dataflow): %d tasks, %d counters, %.1f us\n", ntasks, st.nctr, ms * 1e3);
-      unsigned long long h[48];
-      BDDC_CUDA(cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost));
-      const char* nm[14] = {"EA", "PT", "TS", "X1", "SY", "X2", "W", "CB", "SP", "SB", "SCP", "SC", "SM", "LT"};
-      for (int k = 0; k < 14; ++k)
-        if (h[3 * k + 2])
-          fprintf(stderr, "  %-3s n=%7llu  wait %8.1f us/CTA  run %8.1f us/CTA  (avg wait %.2f run %.2f us)\n", nm[k],
-                  h[3 * k + 2], h[3 * k] / 1.9e3 / st.grid_f, h[3 * k + 1] / 1.9e3 / st.grid_f,
-                  h[3 * k] / 1.9e3 / h[3 * k + 2], h[3 * k + 1] / 1.9e3 / h[3 * k + 2]);
-      cudaEventDestroy(e0);
-      cudaEventDestroy(e1);
-    }
-    return;
+  BDDC_CUDA(cudaMemsetAsync(st.ctr, 0, sizeof(int) * (st.nctr + 2), s));
+  int* qhead = st.ctr + st.nctr;
+  int* err = st.ctr + st.nctr + 1;
+  const DfTask* tasks = st.dtasks;
+  int ntasks = st.ndtasks;
+  unsigned long long* prof = st.prof;
+  unsigned long long* trace = nullptr;
+  const char* tpath = getenv("BDDC_COOP_TRACE");  // per-task timestamps (diagnostics)
+  if (tpath) trace = c.alloc<unsigned long long>((size_t)ntasks * 4);
+  if (prof) BDDC_CUDA(cudaMemsetAsync(prof, 0, sizeof(unsigned long long) * 3 * CT_NTYPES, s));
+  st.pg.lt = c.lt_defer;
+  void* dargs[] = {&fd, &st.pg, (void*)&tasks, &ntasks, &st.ctr, &qhead, &info, &err, &prof, &trace};
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (prof) {
+    BDDC_CUDA(cudaEventCreate(&e0));
+    BDDC_CUDA(cudaEventCreate(&e1));
+    BDDC_CUDA(cudaEventRecord(e0, s));
   }
-  void* args[] = {&fd, &st.pg, &info, &st.ptime};
-  unsigned long long t0 = 0;
-  if (st.ptime) {
-    BDDC_CUDA(cudaStreamSynchronize(s));
-    t0 = 0;
-  }
-  BDDC_CUDA(cudaLaunchCooperativeKernel((void*)coop_factor_kernel, st.grid_f, 128, args, st.smem_f, s));
+  BDDC_CUDA(cudaLaunchCooperativeKernel((void*)coop_factor_df_kernel, st.grid_f, 128, dargs, st.smem_f, s));
   BDDC_COUNT();
-  if (st.ptime) {
-    std::vector<unsigned long long> t(st.phase_type.size());
-    BDDC_CUDA(cudaStreamSynchronize(s));
-    BDDC_CUDA(cudaMemcpy(t.data(), st.ptime, sizeof(unsigned long long) * t.size(), cudaMemcpyDeviceToHost));
-    double by_type[16] = {0};
-    int cnt[16] = {0};
-    for (size_t i = 1; i < t.size(); ++i) {
-      by_type[st.phase_type[i]] += (t[i] - t[i - 1]) * 1e-3;
-      cnt[st.phase_type[i]]++;
+  int herr = 0;
+  BDDC_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  BDDC_CUDA(cudaStreamSynchronize(s));
+  if (herr) throw CudaError("coarse dataflow factorization: dependency wait timed out");
+  if (trace) {  // binary: ntasks, then per task DfTask + 4 x u64 (dequeue, ready, end, cta)
+    std::vector<DfTask> ht(ntasks);
+    std::vector<unsigned long long> tr((size_t)ntasks * 4);
+    BDDC_CUDA(cudaMemcpy(ht.data(), tasks, sizeof(DfTask) * ntasks, cudaMemcpyDeviceToHost));
+    BDDC_CUDA(cudaMemcpy(tr.data(), trace, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost));
+    if (FILE* fo = fopen(tpath, "wb")) {
+      const int hdr[4] = {ntasks, (int)sizeof(DfTask), kDeps, kSigs};
+      fwrite(hdr, sizeof(int), 4, fo);
+      fwrite(ht.data(), sizeof(DfTask), ntasks, fo);
+      fwrite(tr.data(), sizeof(unsigned long long), tr.size(), fo);
+      fclose(fo);
     }
-    const char* nm[16] = {"EA", "PT", "TS|X1", "X1", "SY|X2", "X2", "W", "CB", "SP", "SB|SCP", "SCP", "SC", "SM",
-                          "?", "?", "?"};
-    fprintf(stderr, "coop factor phases (us, from phase 1): total %.1f\n", (t.back() - t[0]) * 1e-3);
-    for (int k = 0; k < 16; ++k)
-      if (cnt[k]) fprintf(stderr, "  %-6s n=%4d  %9.1f us  avg %7.1f\n", nm[k], cnt[k], by_type[k], by_type[k] / cnt[k]);
-    if (atoi(getenv("BDDC_COOP_TIMING")) >= 2)
-      for (size_t i = 1; i < t.size(); ++i)
-        fprintf(stderr, "    phase %3zu %-6s tasks %6d  %8.1f us\n", i, nm[st.phase_type[i]], st.phase_nt[i],
-                (t[i] - t[i - 1]) * 1e-3);
-    (void)t0;
+  }
+  if (prof) {
+    BDDC_CUDA(cudaEventRecord(e1, s));
+    BDDC_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    BDDC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    fprintf(stderr, "coop factor (dataflow): %d tasks, %d counters, %.1f us\n", ntasks, st.nctr, ms * 1e3);
+    unsigned long long h[3 * CT_NTYPES];
+    BDDC_CUDA(cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost));
+    const char* nm[CT_NTYPES] = {"EA", "PT", "TS", "X1", "SY", "X2", "W", "LT", "SYG"};
+    for (int k = 0; k < CT_NTYPES; ++k)
+      if (h[3 * k + 2])
+        fprintf(stderr, "  %-3s n=%7llu  wait %8.1f us/CTA  run %8.1f us/CTA  (avg wait %.2f run %.2f us)\n", nm[k],
+                h[3 * k + 2], h[3 * k] / 1.9e3 / st.grid_f, h[3 * k + 1] / 1.9e3 / st.grid_f,
+                h[3 * k] / 1.9e3 / h[3 * k + 2], h[3 * k + 1] / 1.9e3 / h[3 * k + 2]);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
   }
 }
 
-bool coarse_solve_df_enabled() {
-  const char* e = getenv("BDDC_SOLVE_DF");
-  return !(e && atoi(e) == 0);
+int coarse_solve_error(Ctx& c) {
+  if (!c.fp.n_coarse || !c.sched.df_ctr) return 0;
+  int e = 0;
+  BDDC_CUDA(cudaMemcpyAsync(&e, c.sched.df_ctr + c.sched.n_ctr + 1, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  BDDC_CUDA(cudaStreamSynchronize(c.stream));
+  return e;
 }
 
 void coop_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s, const TvArgs* tva) {
@@ -1507,54 +1137,22 @@ void coop_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s, const Tv
   double* partial = c.sched.partial;
   double* ybuf = c.sched.ybuf;
   int* cnt = c.sched.red_cnt;
-  if (st.solve_df) {
-    const LevelSchedule& ls = c.sched;
-    int* ctr = ls.df_ctr;
-    int* qhead = ctr + ls.n_ctr;
-    int* err = qhead + 1;
-    const SdTask* tasks = ls.df_tasks;
-    int ntasks = ls.n_df;
-    BDDC_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int) * (ls.n_ctr + 1), s));  // the error flag stays
-    unsigned long long* trace = nullptr;
-    const char* tpath = getenv("BDDC_SOLVE_TRACE");  // per-task timestamps (diagnostics)
-    if (tpath) {
-      static unsigned long long* tbuf = nullptr;
-      if (!tbuf) tbuf = c.alloc<unsigned long long>((size_t)ntasks * 4);
-      trace = tbuf;
-    }
-    TvArgs tv{};
-    if (tva) tv = *tva;
-    void* dargs[] = {&fd, &lv, &st.sp, (void*)&tasks, &ntasks, &ctr, &qhead, &err, (void*)&rhs, (void*)&sol,
-                     &partial, &ybuf, &cnt, &tv, &trace};
-    BDDC_CUDA(cudaLaunchCooperativeKernel((void*)coop_solve_df_kernel, st.grid_s, 256, dargs, 0, s));
-    BDDC_COUNT();
-    if (trace) {  // binary: ntasks, sizeof(SdTask), then tasks, then 4 x u64 per task
-      std::vector<SdTask> ht(ntasks);
-      std::vector<unsigned long long> tr((size_t)ntasks * 4);
-      BDDC_CUDA(cudaMemcpy(ht.data(), tasks, sizeof(SdTask) * ntasks, cudaMemcpyDeviceToHost));
-      BDDC_CUDA(cudaMemcpy(tr.data(), trace, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost));
-      if (FILE* fo = fopen(tpath, "wb")) {
-        const int hdr[2] = {ntasks, (int)sizeof(SdTask)};
-        fwrite(hdr, sizeof(int), 2, fo);
-        fwrite(ht.data(), sizeof(SdTask), ntasks, fo);
-        fwrite(tr.data(), sizeof(unsigned long long), tr.size(), fo);
-        fclose(fo);
-      }
-    }
-    return;
-  }
-  void* args[] = {&fd, &lv, &st.sp, (void*)&rhs, (void*)&sol, &partial, &ybuf, &cnt, &st.stime};
-  BDDC_CUDA(cudaLaunchCooperativeKernel((void*)coop_solve_kernel, st.grid_s, 256, args, 0, s));
+  const LevelSchedule& ls = c.sched;
+  int* ctr = ls.df_ctr;
+  int* qhead = ctr + ls.n_ctr;
+  int* err = qhead + 1;
+  const SdTask* tasks = ls.df_tasks;
+  int ntasks = ls.n_df;
+  // counters, queue head and the error flag start at zero every launch (a timeout poisons
+  // this launch's result only; pcg_solve / bddc_check report it)
+  BDDC_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int) * (ls.n_ctr + 2), s));
+  unsigned long long* trace = nullptr;
+  TvArgs tv{};
+  if (tva) tv = *tva;
+  void* dargs[] = {&fd, &lv, &st.sp, (void*)&tasks, &ntasks, &ctr, &qhead, &err, (void*)&rhs, (void*)&sol,
+                   &partial, &ybuf, &cnt, &tv, &trace};
+  BDDC_CUDA(cudaLaunchCooperativeKernel((void*)coop_solve_df_kernel, st.grid_s, 256, dargs, 0, s));
   BDDC_COUNT();
-  if (st.stime) {
-    const int L = st.sp.nlevels;
-    std::vector<unsigned long long> t(2 * L + 1);
-    BDDC_CUDA(cudaStreamSynchronize(s));
-    BDDC_CUDA(cudaMemcpy(t.data(), st.stime, sizeof(unsigned long long) * t.size(), cudaMemcpyDeviceToHost));
-    fprintf(stderr, "coop solve (us): total %.1f\n", (t.back() - t[0]) * 1e-3);
-    for (int l = 0; l < L; ++l) fprintf(stderr, "  fwd L%-2d %7.1f\n", l, (t[l + 1] - t[l]) * 1e-3);
-    for (int q = 0; q < L; ++q) fprintf(stderr, "  bwd L%-2d %7.1f\n", L - 1 - q, (t[L + q + 1] - t[L + q]) * 1e-3);
-  }
 }
 
 }  // namespace bddc

@@ -31,6 +31,30 @@ inline std::atomic<long long>& launch_counter() {
 }
 #define BDDC_COUNT() (::bddc::launch_counter().fetch_add(1, std::memory_order_relaxed))
 
+// Per-device one-time initialisation (function attributes, __constant__ tables): true the
+// first time it is called on the current device for this flag word. Function attributes and
+// constant memory are per device, so a process that drives several GPUs needs one init each.
+inline bool first_on_device(std::atomic<unsigned long long>& mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  const unsigned long long bit = 1ULL << (dev & 63);
+  return !(mask.fetch_or(bit) & bit);
+}
+// Largest dynamic shared memory already granted to a kernel on the current device.
+struct SmemAttr {
+  std::atomic<size_t> v[64] = {};
+  bool needs(size_t bytes) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+    return bytes > v[dev & 63].load();
+  }
+  void set(size_t bytes) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+    v[dev & 63].store(bytes);
+  }
+};
+
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 inline long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }
 

@@ -167,11 +167,10 @@ constexpr int kTrsmSmem = 2 * kTile * TP * (int)sizeof(double);
 
 template <bool R, bool F>
 void launch_trsm(const TileArgs& a, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) {
     BDDC_CUDA(cudaFuncSetAttribute(trsm_tile_kernel<R, F>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmem));
-    attr = true;
   }
   int nvec = a.tasks ? a.max_nvec : a.nvec;
   if (nvec <= 0 || a.count <= 0) return;
@@ -187,13 +186,12 @@ void gemm(const GemmArgs& a, bool tA, bool tB, cudaStream_t s) {
   if (M <= 0 || N <= 0 || a.count <= 0) return;
   dim3 grid(ceil_div(M, BM) * ceil_div(N, BN), a.count);
   constexpr int smem = gemm_smem_doubles<kGemmStages>() * (int)sizeof(double);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) {
     BDDC_CUDA(cudaFuncSetAttribute(gemm_f64_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     BDDC_CUDA(cudaFuncSetAttribute(gemm_f64_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     BDDC_CUDA(cudaFuncSetAttribute(gemm_f64_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     BDDC_CUDA(cudaFuncSetAttribute(gemm_f64_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
   }
   if (!tA && !tB) { gemm_f64_kernel<false, false><<<grid, 128, smem, s>>>(a); BDDC_COUNT(); }
   else if (!tA && tB) { gemm_f64_kernel<false, true><<<grid, 128, smem, s>>>(a); BDDC_COUNT(); }
@@ -205,10 +203,9 @@ void gemm(const GemmArgs& a, bool tA, bool tB, cudaStream_t s) {
 void potrf_tile(const TileArgs& a, cudaStream_t s) {
   if (a.count <= 0) return;
   constexpr int smem = kFactSmemDoubles * (int)sizeof(double);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) {
     BDDC_CUDA(cudaFuncSetAttribute(potrf_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
   }
   { potrf_tile_kernel<<<a.count, 128, smem, s>>>(a); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
@@ -217,10 +214,9 @@ void potrf_tile(const TileArgs& a, cudaStream_t s) {
 void trtri_tile(const TileArgs& a, cudaStream_t s) {
   if (a.count <= 0) return;
   constexpr int smem = kFactSmemDoubles * (int)sizeof(double);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) {
     BDDC_CUDA(cudaFuncSetAttribute(trtri_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
   }
   { trtri_tile_kernel<<<a.count, 128, smem, s>>>(a); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();

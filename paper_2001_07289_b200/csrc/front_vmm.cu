@@ -96,7 +96,7 @@ bool front_alias_layout(Ctx& c) {
   FrontPlan& fp = c.fp;
   const int N = fp.nnodes;
   const int mode = alias_mode();
-  if (mode == 0 || !coarse_df_enabled(c)) return false;
+  if (mode == 0) return false;
   if (mode < 0) {
     size_t free_b = 0, total_b = 0;
     BDDC_CUDA(cudaMemGetInfo(&free_b, &total_b));

@@ -434,7 +434,7 @@ void local_setup(Ctx& c, double* ws, size_t ws_doubles) {
     double* LS = c.LS + sub0 * lsS;
     double* PH = c.Phi + sub0 * phS;
     const bool fused2d = G.nblk > 0 && schur2d_supported(G);
-    const bool fused3d = G.nblk > 0 && !fused2d && schur3d_supported(G) && !getenv("BDDC_NO_SCHUR3D");
+    const bool fused3d = G.nblk > 0 && !fused2d && schur3d_supported(G);
     if (!fused2d && !fused3d) {  // the fused kernels generate T_j, B_j and A_IG from the stencil
       BDDC_CUDA(cudaMemsetAsync(Wd, 0, sizeof(double) * 2 * (size_t)chunk * wS, s));
       BDDC_CUDA(cudaMemsetAsync(E, 0, sizeof(double) * cnt * eS, s));

@@ -117,8 +117,8 @@ static void dot_to(Ctx& c, const double* a, const double* b, long long n, double
   BDDC_LAUNCH_CHECK();
 }
 
-PcgResult pcg_solve(Ctx& c, const double* b, double* x, double tol, int max_iters, double* alphas,
-                    double* betas, double* resid) {
+static PcgResult pcg_run(Ctx& c, const double* b, double* x, double tol, int max_iters, double* alphas,
+                         double* betas, double* resid) {
   const Geometry& G = c.geo;
   cudaStream_t s = c.stream;
   const long long n = G.n;
@@ -203,6 +203,15 @@ PcgResult pcg_solve(Ctx& c, const double* b, double* x, double tol, int max_iter
     { copy_scalar_kernel<<<1, 1, 0, s>>>(sc + 0, sc + 3); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
   }
+  return res;
+}
+
+PcgResult pcg_solve(Ctx& c, const double* b, double* x, double tol, int max_iters, double* alphas,
+                    double* betas, double* resid) {
+  const PcgResult res = pcg_run(c, b, x, tol, max_iters, alphas, betas, resid);
+  // a coarse-solve dependency timeout poisons z with NaN: report it as what it is, not as a
+  // non-SPD preconditioner
+  if (coarse_solve_error(c)) throw CudaError("coarse dataflow solve: dependency wait timed out");
   return res;
 }
 

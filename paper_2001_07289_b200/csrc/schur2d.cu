@@ -457,8 +457,8 @@ void launch_schur2d(const Ctx& c, int sub0, int cnt, const double* Wd, const dou
   const bool diagb = c.geo.nbo == 1 && c.geo.bo_dx[0] == 0;
   const size_t smem_w = sizeof(double) * kWarpsW * (diagb ? wf_warp_doubles<M, true>() : wf_warp_doubles<M, false>());
   const size_t smem_s = sizeof(double) * (2 * M * (NGP + 4) + M * frag_pitch(M) + 3 * M + NGP / 2);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) {
     int2 tiles[16 * 17 / 2];
     for (int I = 0, t = 0; I < 16; ++I)
       for (int J = 0; J <= I; ++J) tiles[t++] = make_int2(I, J);
@@ -468,7 +468,6 @@ void launch_schur2d(const Ctx& c, int sub0, int cnt, const double* Wd, const dou
     BDDC_CUDA(cudaFuncSetAttribute(wfactor2d_kernel<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)(sizeof(double) * kWarpsW * wf_warp_doubles<M, false>())));
     BDDC_CUDA(cudaFuncSetAttribute(schur2d_kernel<M, NGP, NBO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
-    attr = true;
   }
   if (diagb) { wfactor2d_kernel<M, true><<<ceil_div(cnt, kWarpsW), 32 * kWarpsW, smem_w, s>>>(c.geo, sub0, cnt, c.alpha, c.lt, c.LI, c.info); BDDC_COUNT(); }
   else { wfactor2d_kernel<M, false><<<ceil_div(cnt, kWarpsW), 32 * kWarpsW, smem_w, s>>>(c.geo, sub0, cnt, c.alpha, c.lt, c.LI, c.info); BDDC_COUNT(); }
@@ -714,11 +713,10 @@ void schur3d(const Ctx& c, int sub0, int cnt, double* Rt, double* Ht, long long 
   constexpr int M = 56;
   const size_t smem_w = sizeof(double) * kWarps3 * wf3_warp_doubles<M>();
   const size_t smem_r = sizeof(double) * (M * frag_pitch(M) + 2 * M * 68 + M);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) {
     BDDC_CUDA(cudaFuncSetAttribute(wfactor3d_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_w));
     BDDC_CUDA(cudaFuncSetAttribute(rh3d_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r));
-    attr = true;
   }
   { wfactor3d_kernel<M><<<ceil_div(cnt, kWarps3), 32 * kWarps3, smem_w, s>>>(G, sub0, cnt, c.alpha, c.lt, c.LI, c.info); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();

@@ -172,9 +172,6 @@ def build_device_plan(pair: PartitionPair, cons: ConstraintTable,
     if np.any(gidx[fv] < 0):
         raise AssertionError("a free surface node is not on the interface")
     slot_gamma[:, :nG] = sg
-    sw = slot_w[:, :nG]
-    sw[valid] = weights.weights_for(sv, fv)
-    slot_w[:, :nG] = sw
     cv = con_of[fv]
     has = cv >= 0
     sc = slot_con[:, :nG]
@@ -224,5 +221,18 @@ def build_device_plan(pair: PartitionPair, cons: ConstraintTable,
         raise AssertionError("interface dof does not map to a surface slot")
     gamma_slots = np.where(gv, gown * nG_pad + sl, -1).astype(np.int32)
 
-    return DevicePlan(lay, nsub, nc_pad, slot_gamma, slot_w, slot_con, slot_coef, con_coarse,
-                      gamma.astype(np.int64), gamma_slots, coarse_slots, plan, n_local)
+    dp = DevicePlan(lay, nsub, nc_pad, slot_gamma, slot_w, slot_con, slot_coef, con_coarse,
+                    gamma.astype(np.int64), gamma_slots, coarse_slots, plan, n_local)
+    dp.slot_w = slot_weights(dp, weights)
+    return dp
+
+
+def slot_weights(plan: DevicePlan, weights: WeightingOperator) -> np.ndarray:
+    """[nsub, nG_pad] weight δ†_i of every interface slot (bddc.py:472), 0 on Dirichlet /
+    padding slots; recomputed when a new α changes coefficient weights (refactor)."""
+    sg = plan.slot_gamma
+    valid = sg >= 0
+    sub = np.broadcast_to(np.arange(plan.nsub)[:, None], sg.shape)[valid]
+    out = np.zeros(sg.shape)
+    out[valid] = weights.weights_for(sub, plan.gamma_dof[sg[valid]])
+    return out

@@ -85,6 +85,10 @@ class WeightingOperator:
         self._obj_fractions = obj_fractions  # exact values (coefficient mode)
         self._obj_counts = obj_counts  # numerators over sig_len (cardinality mode)
 
+    @property
+    def objects(self) -> ObjectTable:
+        return self._objects
+
     def _slot(self, sub: int, dof: int):
         o = int(self._objects.dof_obj[dof]) if 0 <= dof < len(self._objects.dof_obj) else -1
         if o < 0:

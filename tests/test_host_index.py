@@ -13,6 +13,9 @@ def test_index_sets_bit_exact(case):
     pb = build_problem(g)
     pair, objs, w = pb["pair"], pb["objects"], pb["weights"]
     cons = P.select_constraints(objs, pb["recipe"], pair)
+    if "theta_hat" in g:  # refine_by_coefficient labels (partition.py:202-220)
+        assert np.array_equal(pair.theta_hat, g["theta_hat"])
+        assert np.array_equal(pb["coeff"].alpha, g["alpha"])
     assert np.array_equal(pair.membership.gamma_dofs, g["gamma_dofs"])
     assert np.array_equal(objs.signature, g["obj_sig"])
     assert np.array_equal(objs.owners, g["obj_owners"])

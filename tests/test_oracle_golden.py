@@ -5,10 +5,10 @@ Pins the oracle: identical iteration counts, B·r and x to round-off, κ to 1e-1
 import numpy as np
 import pytest
 
-from conftest import golden_cases, load_golden
+from conftest import golden_cases, is_uniform, load_golden
 from oracle import bddc_oracle as orc
 
-FAST = [c for c in golden_cases() if c != "cfg4a_p1_ref"]
+FAST = [c for c in golden_cases(big=False) if c != "cfg4a_p1_ref" and is_uniform(c)]
 
 
 def _oracle(g):
