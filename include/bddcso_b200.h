@@ -160,6 +160,18 @@ int bddc_comm_init_host(bddc_ctx* ctx, int rank, int world, bddc_host_exchange_f
    fo_hi, halo_lo_send, halo_lo_recv, halo_hi_send, halo_hi_recv (free-dof offsets, -1 none) */
 int bddc_partition_info(int dim, const int* cells, const int* subs, int rank, int world, long long* out);
 
+/* host-only symbolic work (no GPU): the lower CSR pattern of the coarse matrix in elimination
+   order, its segmented contribution lists (ascending subdomain per entry, the reference's COO
+   duplicate order, bddc.py:494-505) and the CSR -> front positions; output arrays hold up to the
+   number of lower contributions (incl. the diagonal). Returns nnz, -1 if an entry falls outside
+   its front. Same result as the numpy statement symbolic.coarse_csr. */
+long long bddc_coarse_pattern(int nsub, const long long* sub_con_ptr, const long long* sub_con_ids,
+                              const long long* iperm, long long n, int nc_pad, int nnodes,
+                              const long long* sep_start, const long long* sep_size, const long long* bnd_ptr,
+                              const long long* bnd_idx, long long* csr_row, long long* csr_col,
+                              long long* csr_node, long long* frow, long long* fcol, long long* seg_ptr,
+                              int* contrib);
+
 /* dense FP64 batched kernels (column-major, even leading dimensions, device pointers) */
 int bddc_dense_potrf(double* A, int n, int lda, long long stride, int count, int* info_host,
                      void* stream);

@@ -29,7 +29,7 @@ EXPORTS = (
     "bddc_event_record", "bddc_event_elapsed_ms", "bddc_profile", "bddc_profile_read",
     "bddc_nccl_unique_id", "bddc_comm_init_nccl", "bddc_comm_init_host", "bddc_partition_info",
     "bddc_dense_potrf", "bddc_dense_trsm", "bddc_dense_gemm", "bddc_check", "bddc_update_weights",
-    "bddc_coarse_solve", "bddc_read_buffer",
+    "bddc_coarse_solve", "bddc_read_buffer", "bddc_coarse_pattern",
 )
 
 
@@ -105,6 +105,9 @@ def load(required: bool = True):
     lib.bddc_debug_copy.restype = _ll
     lib.bddc_read_buffer.argtypes = [_vp, C.c_char_p, _ll, _ll, _pd]
     lib.bddc_read_buffer.restype = _ll
+    lib.bddc_coarse_pattern.argtypes = [_i, _pll, _pll, _pll, _ll, _i, _i, _pll, _pll, _pll, _pll, _pll, _pll,
+                                        _pll, _pll, _pll, _pll, _pi]
+    lib.bddc_coarse_pattern.restype = _ll
     lib.bddc_launch_count.argtypes = []
     lib.bddc_launch_count.restype = _ll
     lib.bddc_event_record.argtypes = [_vp, _i]

@@ -7,6 +7,9 @@
 //     the reference's gamma_local order, bddc.py:429-433), padded to nG_pad; Dirichlet
 //     surface nodes keep their slot as a decoupled identity row.
 #pragma once
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <string>
 #include <vector>
@@ -16,6 +19,19 @@
 #include "dense_f64.cuh"
 
 namespace bddc {
+
+// BDDC_HOST_TIMING=1: wall time of the host phases of bddc_setup on stderr (cold start)
+struct HostTimer {
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  HostTimer() : on(getenv("BDDC_HOST_TIMING") != nullptr), t(std::chrono::steady_clock::now()) {}
+  void mark(const char* what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "bddc_setup host: %-28s %9.3f s\n", what, std::chrono::duration<double>(n - t).count());
+    t = n;
+  }
+};
 
 struct Geometry {
   int dim;

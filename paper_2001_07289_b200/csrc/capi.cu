@@ -31,18 +31,6 @@ namespace {
 
 constexpr int kNoFail = 0x7f7f7f7f;
 
-// BDDC_HOST_TIMING=1: wall time of the host phases of bddc_setup on stderr (cold start)
-struct HostTimer {
-  bool on;
-  std::chrono::steady_clock::time_point t;
-  HostTimer() : on(getenv("BDDC_HOST_TIMING") != nullptr), t(std::chrono::steady_clock::now()) {}
-  void mark(const char* what) {
-    if (!on) return;
-    const auto n = std::chrono::steady_clock::now();
-    fprintf(stderr, "bddc_setup host: %-28s %9.3f s\n", what, std::chrono::duration<double>(n - t).count());
-    t = n;
-  }
-};
 
 void set_err(char* err, size_t len, const std::string& msg) {
   if (!err || len == 0) return;
@@ -186,7 +174,10 @@ void build_plan(Ctx& c, const bddc_setup_desc* d) {
   // device copies
   FrontDev& fd = fp.d;
   // multifrontal update blocks share pages when the resident fronts would not fit (front_vmm.cu)
+  HostTimer ht0;
+  ht0.mark("plan: tree tables");
   if (!front_alias_layout(c)) fd.fronts = c.alloc<double>(fp.front_pool);
+  ht0.mark("plan: front memory / aliasing");
   fd.ualias = c.upload(fp.ualias.data(), N);
   fd.upd = c.alloc<double>(std::max<long long>(fp.upd_pool, 1));
   fd.sep_start = c.upload(fp.sep_start.data(), N);
@@ -211,6 +202,7 @@ void build_plan(Ctx& c, const bddc_setup_desc* d) {
     if (d->csr_col[e] >= fp.sep_size[nd]) throw ApiError{1, "coarse CSR entry outside its front's panel"};
     pos[e] = fp.front_off[nd] + d->csr_row[e] + (long long)d->csr_col[e] * fp.ld[nd];
   }
+  ht0.mark("plan: uploads + CSR positions");
   fp.csr_front_pos = c.upload(pos.data(), pos.size());
   fp.seg_ptr = c.upload(d->seg_ptr, d->nnz + 1);
   fp.ncontrib = d->ncontrib;

@@ -70,6 +70,8 @@ void build_level_schedule(Ctx& c) {
     }
     gptr.push_back(acc);
   }
+  HostTimer ht;
+  ht.mark("schedule: solve gather maps");
   ls.gat_ptr = c.upload<int>(gptr.data(), gptr.size());
   ls.gat_src = c.upload<int>(gsrc.data(), std::max<size_t>(gsrc.size(), 1));
 
@@ -253,7 +255,9 @@ void build_level_schedule(Ctx& c) {
     ls.df_ctr = c.alloc<int>(ls.n_ctr + 2);  // + queue head + error flag
     BDDC_CUDA(cudaMemset(ls.df_ctr, 0, sizeof(int) * (ls.n_ctr + 2)));
   }
+  ht.mark("schedule: solve tasks + queue");
   coop_build(c);
+  ht.mark("schedule: factor program (total)");
 }
 
 void coarse_assemble_and_factor(Ctx& c) {

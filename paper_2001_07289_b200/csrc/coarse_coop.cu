@@ -170,11 +170,13 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
                               1.0, 0.0, false, smem);
       break;
     }
-    case CT_SY: {  // trailing tile (a, b) of A22 -= L21 L21^T; tile (0,0) + lookahead:
+    case CT_SY: {  // tile (a, b) of the panel's trailing matrix INSIDE its group's block column
+      // (columns < group_k1) -= L21 L21^T; tile (0,0) + lookahead:
       const int k = t.arg * kTile, nb = min(kTile, s - k), rest = f - k - nb;
+      const int ncols = group_k1(t.arg / kGroup, s) - (k + nb);
       double* L21 = F + (k + nb) + (long long)k * ld;
       double* A22 = F + (k + nb) + (long long)(k + nb) * ld;
-      gemm_tile<false, true, kCoopStages>(L21, ld, L21, ld, A22, ld, rest, rest, nb, t.a * kTile, t.b * kTile,
+      gemm_tile<false, true, kCoopStages>(L21, ld, L21, ld, A22, ld, rest, ncols, nb, t.a * kTile, t.b * kTile,
                              -1.0, 1.0, true, smem);
       if (t.a == 0 && t.b == 0 && k + nb < s) {  // factor the next panel's diagonal tile now
         __syncthreads();
@@ -947,6 +949,8 @@ void coop_build(Ctx& c) {
       }
     }
     pool = std::max(pool, off);
+    HostTimer ht;
+    ht.mark("factor program: tasks");
     // Queue order = the start order of a simulated list schedule on grid_f CTAs: whenever a
     // CTA is free it takes the ready task of highest upward rank (its estimated cost plus the
     // longest chain of work depending on it). A task is only started after its producers
@@ -1030,6 +1034,7 @@ void coop_build(Ctx& c) {
             if (--ndep[w[wptr[cix]++].second] == 0) ready.push(w[wptr[cix] - 1].second);
         }
       }
+      ht.mark("factor program: list schedule");
       if (order.size() != n) throw std::runtime_error("coarse dataflow: program is not schedulable");
       std::vector<DfTask> sorted(n);
       for (size_t i = 0; i < n; ++i) sorted[i] = dt[order[i]];

@@ -22,6 +22,11 @@ from .partition import PartitionPair
 from .weights import ConstraintTable, WeightingOperator
 
 
+# coarse CSR pattern: the native statement (csrc/host_plan.cu); symbolic.coarse_csr is the
+# numpy statement it is checked against (tests/test_host_plan.py)
+COARSE_CSR = symbolic.coarse_csr_native
+
+
 def _round(x: int, m: int) -> int:
     return (x + m - 1) // m * m
 
@@ -190,7 +195,7 @@ def build_device_plan(pair: PartitionPair, cons: ConstraintTable,
     if n_con:
         plan = symbolic.analyze(n_con, con_owners, pc, tuple(subs), sub_con_ptr=sub_con_ptr,
                                 sub_con_ids=pair_con)
-        symbolic.coarse_csr(plan, sub_con_ptr, pair_con, nc_pad)
+        COARSE_CSR(plan, sub_con_ptr, pair_con, nc_pad)
         con_coarse[pair_sub, local_k] = plan.iperm[pair_con]
         # owners of each constraint (ascending) -> slot sub*nc_pad + k, rows in elimination order
         ks = np.where(pv, 0, -1).astype(np.int64)

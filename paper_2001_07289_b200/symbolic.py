@@ -234,3 +234,33 @@ def coarse_csr(plan: CoarsePlan, sub_con_ptr: np.ndarray, sub_con_ids: np.ndarra
     plan.csr_row, plan.csr_col, plan.csr_node = csr_row, csr_col, nd
     plan.csr_frow, plan.csr_fcol = frow, fcol
     plan.seg_ptr, plan.contrib = seg_ptr, contrib
+
+
+def coarse_csr_native(plan: CoarsePlan, sub_con_ptr: np.ndarray, sub_con_ids: np.ndarray,
+                      nc_pad: int) -> None:
+    """coarse_csr through the native library (csrc/host_plan.cu, bddc_coarse_pattern): the same
+    arrays, O(contributions) on the host threads instead of a global lexsort."""
+    import ctypes as C
+
+    from . import _capi
+
+    lib = _capi.load()
+    i64 = lambda a: np.ascontiguousarray(a, dtype=np.int64)  # noqa: E731
+    ptr, ids = i64(sub_con_ptr), i64(sub_con_ids)
+    m = np.diff(ptr)
+    cap = int(np.sum(m * (m + 1) // 2))
+    out = {k: np.empty(max(cap, 1), dtype=np.int64) for k in ("row", "col", "node", "frow", "fcol")}
+    seg = np.empty(cap + 1, dtype=np.int64)
+    contrib = np.empty(max(cap, 1), dtype=np.int32)
+    P = lambda a: _capi.ptr(a, C.c_longlong)  # noqa: E731
+    iperm, ss, sz = i64(plan.iperm), i64(plan.sep_start), i64(plan.sep_size)
+    bp, bi = i64(plan.bnd_ptr), i64(plan.bnd_idx)
+    nnz = lib.bddc_coarse_pattern(len(ptr) - 1, P(ptr), P(ids), P(iperm), plan.n, int(nc_pad), plan.nnodes,
+                                  P(ss), P(sz), P(bp), P(bi), P(out["row"]), P(out["col"]), P(out["node"]),
+                                  P(out["frow"]), P(out["fcol"]), P(seg), _capi.ptr(contrib, C.c_int))
+    if nnz < 0:
+        raise AssertionError("coarse entry outside its front")
+    plan.csr_row, plan.csr_col, plan.csr_node = out["row"][:nnz], out["col"][:nnz], out["node"][:nnz]
+    plan.csr_frow, plan.csr_fcol = out["frow"][:nnz], out["fcol"][:nnz]
+    plan.seg_ptr = seg[: nnz + 1]
+    plan.contrib = contrib[:cap].astype(np.int64)

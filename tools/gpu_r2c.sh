@@ -1,5 +1,5 @@
 # grouped coarse engine: tests + cfg2/cfg3/cfg5 bench lines
-OUT=gpurun_out/r2c; mkdir -p $OUT
+OUT=gpurun_out/${OUTD:-r2c}; mkdir -p $OUT
 timeout 1500 python -m pytest tests -q -m gpu -x -rxXs > $OUT/pytest_gpu.log 2>&1; echo "pytest exit $?"
 tail -5 $OUT/pytest_gpu.log
 for w in cfg2_L4h cfg3; do
