@@ -2,20 +2,24 @@
 """BDDC-SO setup + PCG solve throughput on B200 (BASELINE.json metric: Mdof/s, applies/s,
 fraction of roofline).
 
-Workload (BASELINE.json configs[1], the metric's config that fits one GPU): 2D Poisson,
-2048x2048 cells split into P1 triangles (4,190,209 dofs), 64x64 subdomains of 32x32 cells,
-subedges of L = 4h (split 8) + vertices between them ('ve'), cardinality weights,
+Default workload = the largest BASELINE config that fits one GPU: configs[4] (cfg5), 3D
+Poisson on 256^3 cells split into P1 tetrahedra (16,581,375 dofs), 32^3 subdomains of 8^3
+cells, subfaces / subedges of 4h + the vertices between them ('vef'), cardinality weights,
 f ~ U[-1,1] per dof (seed 0), PCG rtol 1e-8 from x0 = 0, FP64, reference coarse scaling.
+The other configs run with --workload (cfg1, cfg2_{LH,L16h,L4h,Lh}, cfg3, cfg4).
 
 One step = numeric BDDC-SO setup on device-resident inputs (local factorizations, coarse
 basis, coarse assembly + multifrontal factorization) + the PCG solve to rtol 1e-8.
 `value` = dofs solved per second over the timed steps (CUDA events on the library stream);
 `e2e` = the same through the C ABI with host buffers (bddc_solve_host: alpha and b uploaded
-from pinned memory, overlapped with the setup; x downloaded) every step. Host index tables / symbolic analysis are one-time prep
-(reported as prep_s). Inputs (factors ~3.5 GB) exceed the 126 MB L2 between steps.
+from pinned memory, overlapped with the setup; x downloaded) every step; `cold_e2e` = one
+solve from nothing (host index sets, build_bddc, pcg) through the Python API. Inputs (cfg5:
+factors 54 GB + fronts 75 GB) exceed the 126 MB L2 between steps.
 
---impl reference times the CPU oracle port (oracle/bddc_oracle.py: SuperLU factorizations,
-three-step apply, the reference algorithm) on a bounded sample of the same workload.
+`cpu_baseline` and --impl reference run ONE routine (cpu_measure): the reference algorithm
+(oracle/bddc_oracle.py, pinned to the reference by tests/golden: SuperLU factorizations,
+three-step apply) on bounded samples of the workload's local geometry, one process per host
+core with single-threaded BLAS, all processes timed together.
 """
 
 from __future__ import annotations
@@ -54,15 +58,15 @@ WORKLOADS = {
     "cfg5": (3, (256, 256, 256), (32, 32, 32), 2, "vef", "cardinality", "uniform", "one", "reference"),
     "cfg1": (2, (64, 64), (4, 4), 4, "ve", "cardinality", "one", "one", "reference"),
 }
-SAMPLE = {  # bounded CPU sample with the same local geometry (subdomain size, split, recipe)
-    "cfg2_L4h": (2, (128, 128), (4, 4), 8),
-    "cfg2_Lh": (2, (128, 128), (4, 4), 32),
-    "cfg2_L16h": (2, (128, 128), (4, 4), 2),
-    "cfg2_LH": (2, (128, 128), (4, 4), 1),
-    "cfg3": (3, (24, 24, 24), (3, 3, 3), 2),
-    "cfg4": (3, (24, 24, 24), (3, 3, 3), 2),
-    "cfg5": (3, (24, 24, 24), (3, 3, 3), 2),
-    "cfg1": (2, (64, 64), (4, 4), 4),
+SAMPLES = {  # bounded CPU samples with the workload's local geometry (subdomain size, split, recipe)
+    "cfg2_L4h": [(2, (128, 128), (4, 4), 8), (2, (256, 256), (8, 8), 8)],
+    "cfg2_Lh": [(2, (128, 128), (4, 4), 32), (2, (256, 256), (8, 8), 32)],
+    "cfg2_L16h": [(2, (128, 128), (4, 4), 2), (2, (256, 256), (8, 8), 2)],
+    "cfg2_LH": [(2, (128, 128), (4, 4), 1), (2, (256, 256), (8, 8), 1)],
+    "cfg3": [(3, (16, 16, 16), (2, 2, 2), 2), (3, (24, 24, 24), (3, 3, 3), 2), (3, (32, 32, 32), (4, 4, 4), 2)],
+    "cfg4": [(3, (16, 16, 16), (2, 2, 2), 2), (3, (24, 24, 24), (3, 3, 3), 2), (3, (32, 32, 32), (4, 4, 4), 2)],
+    "cfg5": [(3, (16, 16, 16), (2, 2, 2), 2), (3, (24, 24, 24), (3, 3, 3), 2), (3, (32, 32, 32), (4, 4, 4), 2)],
+    "cfg1": [(2, (64, 64), (4, 4), 4)],
 }
 DESCR = {
     "cfg2": "2D Poisson 2048^2 P1 (4,190,209 dofs), 64x64 subdomains of 32^2 cells, {L} subedges + "
@@ -333,6 +337,12 @@ def run_ours(args, rank, world, local_rank):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
+    # cold one-shot solve right after build_bddc (what experiments.run does once, with the
+    # host index sets and first setup before it): reported as cold_e2e
+    t1 = time.perf_counter()
+    res = op.pcg(b_dev, tol=tol, max_iters=maxit, x_out=x_dev)
+    torch.cuda.synchronize()
+    cold_solve_s = time.perf_counter() - t1
     for _ in range(args.warmup):
         res = step_device()
     iters = res[4]
@@ -544,8 +554,15 @@ def run_ours(args, rank, world, local_rank):
         "solve_ms": round(solve_ms / nsteps, 3),
         "applies_per_s": round(1000.0 / apply_ms, 1),
         "apply_ms": round(apply_ms, 4),
-        "prep_s": round(pb["prep"] + op.times.prep_s, 2),
+        "prep_s": round(pb["prep"] + op.times.prep_s, 2),  # + build_bddc host tables
         "first_setup_s": round(first_setup_s, 2),
+        "cold_e2e": {
+            "value": round(n / (pb["prep"] + first_setup_s + cold_solve_s) / 1e6, 4), "unit": "Mdof/s",
+            "prep_s": round(pb["prep"], 2), "first_setup_s": round(first_setup_s, 2),
+            "solve_s": round(cold_solve_s, 3),
+            "what": "one-shot through the Python API from nothing: mesh / partition / objects / weights "
+                    "(prep_s), build_bddc incl. its index tables, symbolic analysis and first numeric setup "
+                    "(first_setup_s), one pcg (solve_s)"},
         "phases": phase_out,
     }
     if rank == 0:
@@ -559,70 +576,134 @@ def _sample_alpha(cells, coef):
     return None if coef == "one" else orc.block_alpha(cells, 4, 0)
 
 
-def cpu_baseline(workload):
-    """Oracle port on a bounded sample with the workload's local geometry (one run)."""
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def _host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_worker(args):
+    """One CPU process of the baseline (spawned by cpu_measure with 1-thread BLAS): prep +
+    warm-up, then 'ready'; on 'go' it times --steps steps of build_bddc's numeric work
+    (oracle _build: per-subdomain SuperLU factorizations, Psi, coarse assembly + SuperLU;
+    bddc.py:393-523) + pcg to rtol 1e-8 (krylov.py:31-92) and prints one JSON line."""
     from oracle import bddc_oracle as orc
 
-    dim, cells, subs, split = SAMPLE[workload]
-    _, _, _, _, recipe, wmode, source, coef, scaling = WORKLOADS[workload]
-    # index sets (mesh, partition, objects, weights) are prep, as on the GPU side; the timed
-    # part is build_bddc's numeric work (oracle _build, bddc.py:393-523) + pcg
-    o = orc.Oracle(dim, cells, subs, split, recipe, wmode, "p1", _sample_alpha(cells, coef), scaling)
-    t0 = time.perf_counter()
-    o._build()
-    t_build = time.perf_counter() - t0
-    mesh = o.mesh
-    b = orc.load(mesh, orc.uniform_f(mesh.n_free, 0)) if source == "uniform" else orc.load(mesh, 1.0)
-    t1 = time.perf_counter()
-    x, rep = orc.pcg(o.matvec, o.apply, b, 1e-8, 2000)
-    t_pcg = time.perf_counter() - t1
-    n = mesh.n_free
-    return {"value": round(n / (t_build + t_pcg) / 1e6, 5), "unit": "Mdof/s",
-            "cores": os.cpu_count(), "kind": "port",
-            "sample": f"{dim}D {cells} P1, {subs} subdomains, split {split} (same local geometry), "
-                      f"{n} dofs: build {t_build:.2f} s + pcg {t_pcg:.2f} s ({rep['iterations']} its)"}
-
-
-def run_reference(args, rank, world):
-    if rank != 0:
-        return
-    from oracle import bddc_oracle as orc
-
-    dim, cells, subs, split = SAMPLE[args.workload]
+    dim, cells, subs, split = SAMPLES[args.workload][args.cpu_sample]
     _, _, _, _, recipe, wmode, source, coef, scaling = WORKLOADS[args.workload]
-    alpha = _sample_alpha(cells, coef)
-    # index sets are prep (untimed, as on the GPU side); each step = build_bddc's numeric work
-    # (oracle _build: per-subdomain SuperLU factorizations, Psi, coarse assembly + SuperLU)
-    # + the PCG solve
-    o = orc.Oracle(dim, cells, subs, split, recipe, wmode, "p1", alpha, scaling)
+    o = orc.Oracle(dim, cells, subs, split, recipe, wmode, "p1", _sample_alpha(cells, coef), scaling)
     mesh = o.mesh
     b = orc.load(mesh, orc.uniform_f(mesh.n_free, 0)) if source == "uniform" else orc.load(mesh, 1.0)
 
     def step():
+        t0 = time.perf_counter()
         o._build()
+        t1 = time.perf_counter()
         x, rep = orc.pcg(o.matvec, o.apply, b, 1e-8, 2000)
-        return mesh.n_free, rep["iterations"]
+        return t1 - t0, time.perf_counter() - t1, rep["iterations"]
 
     for _ in range(args.warmup):
         step()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        n, its = step()
-    el = time.perf_counter() - t0
-    value = n * args.steps / el / 1e6
-    sample = (f"{dim}D {cells} P1, {subs} subdomains, split {split} ({n} dofs, same local geometry "
-              f"as {args.workload}); oracle port of the reference (SuperLU), setup+pcg per step")
+    print("ready", flush=True)
+    sys.stdin.readline()
+    res = [step() for _ in range(args.steps)]
+    print(json.dumps({"n": int(mesh.n_free), "build": [r[0] for r in res], "pcg": [r[1] for r in res],
+                      "its": res[-1][2]}), flush=True)
+
+
+def cpu_measure(workload, sample, steps, warmup, procs=None):
+    """The reference algorithm (oracle port) on the host: `procs` concurrent processes (all
+    host cores by default), each with single-threaded BLAS (OpenBLAS threads on these small
+    SuperLU / BLAS calls are 5-8x slower than one thread: measured), each solving its own
+    copy of the bounded sample `sample` of `workload` for `steps` timed steps after `warmup`.
+    The processes start the timed steps together; value = dofs solved by all of them / wall
+    time. One routine for both the cpu_baseline field and --impl reference."""
+    procs = procs or _host_cores()
+    env = dict(os.environ, OPENBLAS_NUM_THREADS="1", OMP_NUM_THREADS="1", MKL_NUM_THREADS="1")
+    cmd = [sys.executable, os.path.abspath(__file__), "--cpu-worker", "--workload", workload,
+           "--cpu-sample", str(sample), "--steps", str(steps), "--warmup", str(warmup)]
+    ps = [subprocess.Popen(cmd, stdin=subprocess.PIPE, stdout=subprocess.PIPE, text=True, env=env)
+          for _ in range(procs)]
+    try:
+        for p in ps:
+            if p.stdout.readline().strip() != "ready":
+                raise RuntimeError("CPU baseline worker failed")
+        t0 = time.perf_counter()
+        for p in ps:
+            p.stdin.write("go\n")
+            p.stdin.flush()
+        outs = [json.loads(p.stdout.readline()) for p in ps]
+        wall = time.perf_counter() - t0
+    finally:
+        for p in ps:
+            try:
+                p.stdin.close()
+            except Exception:
+                pass
+            p.wait(timeout=60)
+    n = outs[0]["n"]
+    dim, cells, subs, split = SAMPLES[workload][sample]
+    build = statistics.median(t for o in outs for t in o["build"])
+    pcg = statistics.median(t for o in outs for t in o["pcg"])
+    return {"value": procs * n * steps / wall / 1e6, "dofs": n, "procs": procs, "wall_s": wall,
+            "build_s": build, "pcg_s": pcg, "its": outs[0]["its"],
+            "sample": f"{dim}D {cells} P1, {subs} subdomains of the workload's local geometry "
+                      f"(split {split}), {n} dofs"}
+
+
+def _cpu_line(m, trend=None):
+    cores = m["procs"]
+    d = {"value": round(m["value"], 5), "unit": "Mdof/s", "cores": cores, "kind": "port",
+         "cpu_model": _cpu_model(), "threads": f"{cores} processes x 1 BLAS thread (OPENBLAS_NUM_THREADS=1)",
+         "sample": (f"{m['sample']}; {cores} concurrent copies, each setup (build_bddc numeric) "
+                    f"{m['build_s']:.3f} s + pcg {m['pcg_s']:.3f} s ({m['its']} its), median over steps")}
+    if trend:
+        d["trend"] = trend
+    return d
+
+
+def cpu_baseline(workload):
+    """cpu_baseline field (rank 0, N=1): every bounded sample of the workload (smallest
+    first) so the per-dof trend toward the full config is visible; value = the largest."""
+    trend, last = [], None
+    for i in range(len(SAMPLES[workload])):
+        m = cpu_measure(workload, i, steps=2, warmup=1)
+        trend.append({"dofs": m["dofs"], "Mdof_s": round(m["value"], 5),
+                      "setup_s": round(m["build_s"], 4), "pcg_s": round(m["pcg_s"], 4)})
+        last = m
+    return _cpu_line(last, trend)
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU algorithm (oracle port, pinned to the reference
+    by tests/golden) on the host cores, same routine as cpu_baseline, largest sample."""
+    if rank != 0:
+        return
+    m = cpu_measure(args.workload, len(SAMPLES[args.workload]) - 1, args.steps, args.warmup)
+    value = m["value"]
+    cpu = _cpu_line(m)
     line = {
         "metric": "BDDC-SO setup+PCG solve throughput (Mdof/s)", "value": round(value, 5),
         "unit": "Mdof/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1000 * el / args.steps, 2), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "sample": sample}, "impl": "reference",
-        "cpu_baseline": {"value": round(value, 5), "unit": "Mdof/s", "cores": os.cpu_count(),
-                         "kind": "port", "sample": sample},
+        "ms_per_step": round(1000 * m["wall_s"] / args.steps, 2), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": describe(args.workload), "sample": cpu["sample"]}, "impl": "reference",
+        "cpu_baseline": cpu,
         "e2e": {"value": round(value, 5), "unit": "Mdof/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "iterations": its,
+        "iterations": m["its"],
     }
     print(json.dumps(line), flush=True)
 
@@ -633,11 +714,16 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--workload", default="cfg2_L4h", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="cfg5", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-worker", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--cpu-sample", type=int, default=0, help=argparse.SUPPRESS)
     ap.add_argument("--transport", default="nccl", choices=("nccl", "host"),
                     help="host: test-only gloo + host-staged exchanges with every rank on cuda:0")
     args = ap.parse_args()
+    if args.cpu_worker:
+        cpu_worker(args)
+        return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -170,6 +170,8 @@ bool front_alias_layout(Ctx& c) {
     }
   }
   upages = std::max(upages, 1LL);
+  HostTimer ht;
+  ht.mark("alias: page plan");
   // (3) physical memory: persistent pages (everything outside aliased update columns) + pool
   std::vector<char> aliased(vpages, 0);
   long long na = 0;
@@ -209,6 +211,7 @@ bool front_alias_layout(Ctx& c) {
     }
     p = q;
   }
+  ht.mark("alias: persistent runs");
   // pool: one allocation per page, mapped into the pool view and under every update block
   // the planner placed on it
   std::vector<CUmemGenericAllocationHandle> page(upages);
@@ -216,10 +219,19 @@ bool front_alias_layout(Ctx& c) {
     page[k] = create(PB);
     map(vm->uview + (size_t)k * PB, PB, page[k]);
   }
+  ht.mark("alias: pool pages");
   for (int i = 0; i < N; ++i) {
     long long vp = upage[i];
     for (auto& r : urun[i])
       for (long long k = 0; k < r.second; ++k, ++vp) map(vm->va + (size_t)vp * PB, PB, page[base[i] + r.first + k]);
+  }
+  ht.mark("alias: update-block maps");
+  if (ht.on) {
+    long long nal = 0, nmap = 0;
+    for (int i = 0; i < N; ++i) nal += u[i] > 0, nmap += u[i];
+    fprintf(stderr, "bddc_setup host: alias: page %lld MB, %lld virtual / %lld persistent / %lld pool pages, "
+            "%lld aliased fronts, %lld update-block page maps, %zu allocations\n", PG * 8 >> 20, vpages, ppages,
+            upages, nal, nmap, vm->handles.size());
   }
   CUmemAccessDesc acc{};
   acc.location = prop.location;
@@ -227,6 +239,7 @@ bool front_alias_layout(Ctx& c) {
   cu_check(d.access(vm->va, vm->va_bytes, &acc, 1), "cuMemSetAccess");
   cu_check(d.access(vm->pview, vm->p_bytes, &acc, 1), "cuMemSetAccess");
   cu_check(d.access(vm->uview, vm->u_bytes, &acc, 1), "cuMemSetAccess");
+  ht.mark("alias: access");
   fp.front_pool = vpages * PG;
   fp.alias = true;
   fp.alias_resident_bytes = (long long)(vm->p_bytes + vm->u_bytes);
