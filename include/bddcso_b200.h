@@ -172,6 +172,24 @@ long long bddc_coarse_pattern(int nsub, const long long* sub_con_ptr, const long
                               long long* csr_node, long long* frow, long long* fcol, long long* seg_ptr,
                               int* contrib);
 
+/* device index sets: membership, interface objects and counting /
+   cardinality weights of a partition pair on GPU `device`, bit-exact with the reference's
+   host code it replaces:
+     partition.py:117-131 (_node_membership), :75-83 (gamma dofs), :223-250 (classify_objects),
+     bddc.py:108-145 (compute_weights, counting and cardinality modes).
+   theta_hat [prod(cells)] subsubdomain per cell, parent [n_hat] subdomain per subsubdomain.
+   Results are held by the handle: sizes by name ("n_free", "n_gamma", "n_gamma_hat",
+   "n_obj", "width" = 2^dim), arrays copied out by name: "gamma_dofs", "gamma_hat_dofs",
+   "signature", "sig_len", "owners", "owner_len", "dof_ptr", "dof_list", "dof_obj",
+   "card_counts" (int64), "kind" (int8: 0 vertex, 1 edge, 2 face), "w_counting",
+   "w_cardinality" (float64, [n_obj * width]); count must equal the array length. */
+typedef struct bddc_index bddc_index;
+int bddc_index_build(int device, int dim, const int* cells, const int* theta_hat, const int* parent,
+                     int n_hat, bddc_index** out, char* err, size_t errlen);
+long long bddc_index_size(const bddc_index* ix, const char* what);
+int bddc_index_copy(const bddc_index* ix, const char* name, void* host, long long count);
+void bddc_index_free(bddc_index* ix);
+
 /* dense FP64 batched kernels (column-major, even leading dimensions, device pointers) */
 int bddc_dense_potrf(double* A, int n, int lda, long long stride, int count, int* info_host,
                      void* stream);

@@ -30,6 +30,7 @@ EXPORTS = (
     "bddc_nccl_unique_id", "bddc_comm_init_nccl", "bddc_comm_init_host", "bddc_partition_info",
     "bddc_dense_potrf", "bddc_dense_trsm", "bddc_dense_gemm", "bddc_check", "bddc_update_weights",
     "bddc_coarse_solve", "bddc_read_buffer", "bddc_coarse_pattern",
+    "bddc_index_build", "bddc_index_size", "bddc_index_copy", "bddc_index_free",
 )
 
 
@@ -108,6 +109,12 @@ def load(required: bool = True):
     lib.bddc_coarse_pattern.argtypes = [_i, _pll, _pll, _pll, _ll, _i, _i, _pll, _pll, _pll, _pll, _pll, _pll,
                                         _pll, _pll, _pll, _pll, _pi]
     lib.bddc_coarse_pattern.restype = _ll
+    lib.bddc_index_build.argtypes = [_i, _i, _pi, _pi, _pi, _i, C.POINTER(_vp), C.c_char_p, C.c_size_t]
+    lib.bddc_index_size.argtypes = [_vp, C.c_char_p]
+    lib.bddc_index_size.restype = _ll
+    lib.bddc_index_copy.argtypes = [_vp, C.c_char_p, _vp, _ll]
+    lib.bddc_index_free.argtypes = [_vp]
+    lib.bddc_index_free.restype = None
     lib.bddc_launch_count.argtypes = []
     lib.bddc_launch_count.restype = _ll
     lib.bddc_event_record.argtypes = [_vp, _i]

@@ -757,6 +757,7 @@ void coop_build(Ctx& c) {
   int max_children = 0;
   for (int nd = 0; nd < N; ++nd) max_children = std::max(max_children, fp.child_ptr[nd + 1] - fp.child_ptr[nd]);
   // ---- dataflow factorization program ----
+  HostTimer ht;
   {
     std::vector<DfTask> dt;
     int nctr = 0;
@@ -949,8 +950,8 @@ void coop_build(Ctx& c) {
       }
     }
     pool = std::max(pool, off);
-    HostTimer ht;
     ht.mark("factor program: tasks");
+    if (ht.on) fprintf(stderr, "bddc_setup host: factor program: %zu tasks, %d counters\n", dt.size(), nctr);
     // Queue order = the start order of a simulated list schedule on grid_f CTAs: whenever a
     // CTA is free it takes the ready task of highest upward rank (its estimated cost plus the
     // longest chain of work depending on it). A task is only started after its producers
@@ -994,13 +995,22 @@ void coop_build(Ctx& c) {
         for (int d = 0; d < kDeps; ++d)
           if (t.dep[d] >= 0) maxc[t.dep[d]] = std::max(maxc[t.dep[d]], rank[i]);
       }
-      // waiters per counter, by target
-      std::vector<std::vector<std::pair<int, int>>> wait(nctr);
-      std::vector<int> ndep(n, 0), cval(nctr, 0), wptr(nctr, 0);
+      // waiters per counter (CSR), each counter's list by target
+      std::vector<int> ndep(n, 0), cval(nctr, 0), wptr(nctr + 1, 0);
       for (size_t i = 0; i < n; ++i)
         for (int d = 0; d < kDeps; ++d)
-          if (dt[i].dep[d] >= 0) { wait[dt[i].dep[d]].push_back({dt[i].tgt[d], (int)i}); ndep[i]++; }
-      for (auto& w : wait) std::sort(w.begin(), w.end());
+          if (dt[i].dep[d] >= 0) { wptr[dt[i].dep[d] + 1]++; ndep[i]++; }
+      for (int q = 0; q < nctr; ++q) wptr[q + 1] += wptr[q];
+      std::vector<std::pair<int, int>> wlist(wptr[nctr]);
+      {
+        std::vector<int> fill(wptr.begin(), wptr.end() - 1);
+        for (size_t i = 0; i < n; ++i)
+          for (int d = 0; d < kDeps; ++d)
+            if (dt[i].dep[d] >= 0) wlist[fill[dt[i].dep[d]]++] = {dt[i].tgt[d], (int)i};
+      }
+      for (int q = 0; q < nctr; ++q)
+        if (wptr[q + 1] - wptr[q] > 1) std::sort(wlist.begin() + wptr[q], wlist.begin() + wptr[q + 1]);
+      std::vector<int> wpos(wptr.begin(), wptr.end() - 1);
       auto prio = [&](int a, int b) { return rank[a] < rank[b] || (rank[a] == rank[b] && a > b); };
       std::priority_queue<int, std::vector<int>, decltype(prio)> ready(prio);
       for (size_t i = 0; i < n; ++i)
@@ -1029,9 +1039,11 @@ void coop_build(Ctx& c) {
           const int cix = t.sig[q];
           if (cix < 0) continue;
           cval[cix] += t.sw[q];
-          auto& w = wait[cix];
-          while (wptr[cix] < (int)w.size() && w[wptr[cix]].first <= cval[cix])
-            if (--ndep[w[wptr[cix]++].second] == 0) ready.push(w[wptr[cix] - 1].second);
+          int& wp = wpos[cix];
+          while (wp < wptr[cix + 1] && wlist[wp].first <= cval[cix]) {
+            const int j = wlist[wp++].second;
+            if (--ndep[j] == 0) ready.push(j);
+          }
         }
       }
       ht.mark("factor program: list schedule");
@@ -1046,6 +1058,7 @@ void coop_build(Ctx& c) {
     }
     st.ndtasks = (int)dt.size();
     st.dtasks = c.upload(dt.data(), dt.size());
+    ht.mark("factor program: upload");
     st.nctr = nctr;
     st.ctr = c.alloc<int>(nctr + 2);  // + queue head + error flag
   }

@@ -109,58 +109,84 @@ bool front_alias_layout(Ctx& c) {
   prop.location.id = c.device;
   size_t g = 0;
   cu_check(d.gran(&g, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED), "granularity");
-  const long long PG = (long long)std::max<size_t>(g, 2 << 20) / 8;  // doubles per page
-  const char* te = getenv("BDDC_FRONT_ALIAS_MIN_MB");
-  const double thr = (te ? atof(te) : 2.0) * 1e6;
-  // (1) virtual layout: aliased fronts start so that their update columns are page aligned
-  std::vector<long long> u(N, 0), upage(N, -1);
-  long long off = 0;
-  for (int i = 0; i < N; ++i) {
-    const long long s = fp.sep_size[i], b = fp.bnd_size[i], f = s + b, ld = fp.ld[i];
-    if (b > 0 && 8.0 * (double)(ld * b) >= thr) {
-      const long long fo = round_up(off + s * ld, PG) - s * ld;
-      const long long ue = round_up(fo + f * ld, PG);
-      fp.front_off[i] = fo;
-      upage[i] = (fo + s * ld) / PG;
-      u[i] = ue / PG - upage[i];
-      off = ue;
-    } else {
-      fp.front_off[i] = off;
-      off = round_up(off + ld * f, 2);
-    }
-  }
-  const long long vpages = std::max<long long>(1, (off + PG - 1) / PG);
-  // (2) pool pages, bottom-up (nodes are in postorder): runs relative to the node's sub-pool
+  // Page size: every mapped page costs one cuMemMap + its share of cuMemSetAccess (~0.2 ms
+  // each, serialized in the driver: tools/vmm_probe.cu), while larger pages waste more of
+  // each aliased block's last page. Take the largest page (up to 32 MB) whose resident total
+  // stays within half of the free memory (the local factors come after this plan).
+  size_t free_b = 0, total_b = 0;
+  BDDC_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const char* pe = getenv("BDDC_FRONT_PAGE_MB");
+  const char* te = getenv("BDDC_FRONT_ALIAS_MIN_MB");  // aliasing threshold (default: one page)
+  std::vector<long long> cands;
+  if (pe) cands.push_back((long long)atoi(pe) << 20);
+  else for (long long mb = 32; mb >= 2; mb >>= 1) cands.push_back(mb << 20);
+  long long PG = 0, vpages = 0, upages = 0;
+  std::vector<long long> u, upage, need, choff, front_off;
   using Runs = std::vector<std::pair<long long, long long>>;  // (first page, count)
-  std::vector<Runs> urun(N);
-  std::vector<long long> need(N, 0), choff(N, 0);
-  for (int v = 0; v < N; ++v) {
-    long long sum_need = 0, sum_u = u[v];
-    Runs occ;
-    for (int k = fp.child_ptr[v]; k < fp.child_ptr[v + 1]; ++k) {
-      const int ch = fp.child_list[k];
-      choff[ch] = sum_need;
-      for (auto& r : urun[ch]) occ.push_back({r.first + sum_need, r.second});
-      sum_need += need[ch];
-      sum_u += u[ch];
-    }
-    need[v] = std::max(sum_need, sum_u);
-    std::sort(occ.begin(), occ.end());
-    long long want = u[v], p = 0;
-    for (size_t k = 0; k <= occ.size() && want > 0; ++k) {
-      const long long gap_end = k < occ.size() ? occ[k].first : need[v];
-      if (gap_end > p) {
-        const long long take = std::min(want, gap_end - p);
-        urun[v].push_back({p, take});
-        want -= take;
+  std::vector<Runs> urun;
+  for (size_t ci = 0; ci < cands.size(); ++ci) {
+    PG = std::max<long long>(cands[ci], (long long)g) / 8;  // doubles per page
+    const double thr = te ? atof(te) * 1e6 : 8.0 * (double)PG;
+    // (1) virtual layout: aliased fronts start so that their update columns are page aligned
+    u.assign(N, 0);
+    upage.assign(N, -1);
+    front_off.assign(N, 0);
+    long long off = 0;
+    for (int i = 0; i < N; ++i) {
+      const long long s = fp.sep_size[i], b = fp.bnd_size[i], f = s + b, ld = fp.ld[i];
+      if (b > 0 && 8.0 * (double)(ld * b) >= thr) {
+        const long long fo = round_up(off + s * ld, PG) - s * ld;
+        const long long ue = round_up(fo + f * ld, PG);
+        front_off[i] = fo;
+        upage[i] = (fo + s * ld) / PG;
+        u[i] = ue / PG - upage[i];
+        off = ue;
+      } else {
+        front_off[i] = off;
+        off = round_up(off + ld * f, 2);
       }
-      if (k < occ.size()) p = std::max(p, occ[k].first + occ[k].second);
     }
-    if (want > 0) throw CudaError("front alias planner: pool too small");
+    vpages = std::max<long long>(1, (off + PG - 1) / PG);
+    // (2) pool pages, bottom-up (nodes are in postorder): runs relative to the node's sub-pool
+    urun.assign(N, Runs());
+    need.assign(N, 0);
+    choff.assign(N, 0);
+    for (int v = 0; v < N; ++v) {
+      long long sum_need = 0, sum_u = u[v];
+      Runs occ;
+      for (int k = fp.child_ptr[v]; k < fp.child_ptr[v + 1]; ++k) {
+        const int ch = fp.child_list[k];
+        choff[ch] = sum_need;
+        for (auto& r : urun[ch]) occ.push_back({r.first + sum_need, r.second});
+        sum_need += need[ch];
+        sum_u += u[ch];
+      }
+      need[v] = std::max(sum_need, sum_u);
+      std::sort(occ.begin(), occ.end());
+      long long want = u[v], p = 0;
+      for (size_t k = 0; k <= occ.size() && want > 0; ++k) {
+        const long long gap_end = k < occ.size() ? occ[k].first : need[v];
+        if (gap_end > p) {
+          const long long take = std::min(want, gap_end - p);
+          urun[v].push_back({p, take});
+          want -= take;
+        }
+        if (k < occ.size()) p = std::max(p, occ[k].first + occ[k].second);
+      }
+      if (want > 0) throw CudaError("front alias planner: pool too small");
+    }
+    upages = 0;
+    for (int v = 0; v < N; ++v)
+      if (fp.parent[v] < 0) upages += need[v];
+    long long na = 0;
+    for (int i = 0; i < N; ++i) na += u[i];
+    const double resident = 8.0 * (double)PG * (double)(vpages - na + std::max(upages, 1LL));
+    if (resident <= 0.5 * (double)free_b || ci + 1 == cands.size()) break;
   }
+  for (int i = 0; i < N; ++i) fp.front_off[i] = front_off[i];
   // absolute pool positions, top-down (parents after children in index order)
   std::vector<long long> base(N, 0);
-  long long upages = 0;
+  upages = 0;
   for (int v = N - 1; v >= 0; --v) {
     if (fp.parent[v] < 0) {
       base[v] = upages;

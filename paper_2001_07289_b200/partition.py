@@ -235,20 +235,9 @@ class PartitionPair:
 
     @cached_property
     def membership(self) -> MembershipSets:
-        """partition.py:75-83 with _node_membership (117-131) as array work."""
-        cells = _node_cells(self.mesh)
-        th_rows, th_cnt = _sorted_unique_rows(self.theta[cells])
-        hat_rows, hat_cnt = _sorted_unique_rows(self.theta_hat[cells])
-        return MembershipSets(
-            on_gamma=_TupleView(th_rows, th_cnt),
-            on_gamma_hat=_TupleView(hat_rows, hat_cnt),
-            gamma_dofs=np.flatnonzero(th_cnt >= 2).astype(np.int64),
-            gamma_hat_dofs=np.flatnonzero(hat_cnt >= 2).astype(np.int64),
-            theta_rows=th_rows,
-            theta_counts=th_cnt,
-            hat_rows=hat_rows,
-            hat_counts=hat_cnt,
-        )
+        """partition.py:75-83 with _node_membership (117-131) as array work (host). After
+        ``classify_objects(pair, device=...)`` this is the device result (index_device.py)."""
+        return _host_membership(self)
 
     @cached_property
     def grounded_subdomains(self) -> np.ndarray:
@@ -262,6 +251,22 @@ class PartitionPair:
     def box_layout(self):
         """Uniform box structure of Θ if it has one: (subs_per_dim, block) else None."""
         return _uniform_box_layout(self.mesh, self.theta)
+
+
+def _host_membership(pair: "PartitionPair") -> MembershipSets:
+    cells = _node_cells(pair.mesh)
+    th_rows, th_cnt = _sorted_unique_rows(pair.theta[cells])
+    hat_rows, hat_cnt = _sorted_unique_rows(pair.theta_hat[cells])
+    return MembershipSets(
+        on_gamma=_TupleView(th_rows, th_cnt),
+        on_gamma_hat=_TupleView(hat_rows, hat_cnt),
+        gamma_dofs=np.flatnonzero(th_cnt >= 2).astype(np.int64),
+        gamma_hat_dofs=np.flatnonzero(hat_cnt >= 2).astype(np.int64),
+        theta_rows=th_rows,
+        theta_counts=th_cnt,
+        hat_rows=hat_rows,
+        hat_counts=hat_cnt,
+    )
 
 
 def _parent_map(theta, theta_hat, hat_count) -> np.ndarray:
@@ -414,12 +419,18 @@ def _lexsort_rows(rows: np.ndarray) -> np.ndarray:
     return np.lexsort(tuple(rows[:, k] for k in range(rows.shape[1] - 1, -1, -1)))
 
 
-def classify_objects(pair: PartitionPair) -> ObjectTable:
+def classify_objects(pair: PartitionPair, device: int | None = None) -> ObjectTable:
     """Group Γ dofs into objects by Θ̂-signature (partition.py:223-250).
 
     Returns an :class:`ObjectTable`, which indexes and iterates like the reference's
-    list of ``InterfaceObject``.
+    list of ``InterfaceObject``. ``device`` (a CUDA ordinal): membership, objects and the
+    counting / cardinality weights are computed by the sm_100a index-set kernels
+    (index_device.py, csrc/index_sets.cu), bit-identical to this host statement.
     """
+    if device is not None:
+        from .index_device import classify_objects_device
+
+        return classify_objects_device(pair, device)
     ms = pair.membership
     mesh = pair.mesh
     gamma = ms.gamma_dofs

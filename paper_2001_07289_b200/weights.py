@@ -161,6 +161,10 @@ def compute_weights(pair: PartitionPair, mode: str, coeff=None,
         alpha_hat = _constant_per_subsubdomain(pair, coeff)
     if objects is None:
         objects = classify_objects(pair)
+    dev = getattr(objects, "_device_weights", None)
+    if dev is not None and mode in dev:  # computed with the objects (index_device.py)
+        weights, counts = dev[mode]
+        return WeightingOperator(mode, ms.gamma_dofs, objects, weights, None, counts)
     W = objects.owners.shape[1]
     n_obj = len(objects)
     weights = np.zeros((n_obj, W))

@@ -62,8 +62,9 @@ def load_golden(name):
         return Golden({k: g[k] for k in g.files})
 
 
-def build_problem(g):
-    """Host problem (mesh, pair, objects, weights, constraints, system, rhs) of a fixture."""
+def build_problem(g, device=None):
+    """Host problem (mesh, pair, objects, weights, constraints, system, rhs) of a fixture;
+    ``device``: membership / objects / weights from the device index-set kernels."""
     import paper_2001_07289_b200 as P
 
     dim = int(g["dim"])
@@ -82,7 +83,7 @@ def build_problem(g):
         pair = P.refine_by_coefficient(mesh, theta, cf)
     else:
         pair = P.refine_uniform(mesh, theta, int(g["split"]), validate=False)
-    objs = P.classify_objects(pair)
+    objs = P.classify_objects(pair, device=device)
     w = P.compute_weights(pair, str(g["weighting"]), cf, objs)
     recipe = P.Recipe.full() if bool(g["full"]) else str(g["recipe"])
     system = P.assemble(mesh, cf)

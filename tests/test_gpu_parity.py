@@ -237,6 +237,8 @@ def test_aliased_front_memory(cuda_ok, case, monkeypatch):
     op.close()
     monkeypatch.setenv("BDDC_FRONT_ALIAS", "1")
     monkeypatch.setenv("BDDC_FRONT_ALIAS_MIN_MB", "0")
+    if case in ("cfg1_p1_ref", "cfg3a_p1_ref"):  # 2 MB pages (else the adaptive size, 32 MB here)
+        monkeypatch.setenv("BDDC_FRONT_PAGE_MB", "2")
     pb, op = _op(g)
     z = op.apply(g["r"])
     assert np.array_equal(z, z0)
