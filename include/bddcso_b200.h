@@ -70,6 +70,8 @@ typedef struct {
   const int* bnd_ptr;     /* [nnodes + 1] */
   const int* bnd_idx;     /* boundary dofs of each front (elimination order, ascending) */
   const int* rmap;        /* aligned with bnd_idx: position in the parent front */
+  /* coarse assembly pattern: contrib = NULL lets the setup build it on the device from
+     con_coarse (coarse_pattern.cu); otherwise the host statement's arrays: */
   long long nnz;          /* lower-triangular coarse CSR entries */
   const int* csr_node;    /* front receiving each entry */
   const int* csr_row;     /* row position in that front */
@@ -141,6 +143,13 @@ long long bddc_debug_copy(bddc_ctx* ctx, const char* name, double* host, long lo
 /* the same buffers, elements [offset, offset + count) (count 0 / host NULL: total length);
    backs the operator's lazy host views (.subdomains[i].coarse_basis, .coarse_matrix) */
 long long bddc_read_buffer(bddc_ctx* ctx, const char* name, long long offset, long long count, double* host);
+
+/* the coarse assembly pattern the setup built on the device (descriptor with contrib = NULL):
+   lower CSR of S_0 in elimination order (row, col), seg_ptr [nnz + 1] and contrib (local block
+   index per contribution, ascending subdomain inside an entry); all pointers NULL: returns nnz.
+   -1 if the pattern came from the descriptor or a capacity is too small. */
+long long bddc_coarse_csr(bddc_ctx* ctx, long long* row, long long* col, long long* seg_ptr, int* contrib,
+                          long long cap_nnz, long long cap_contrib);
 
 /* multi-GPU: one rank per GPU, each owning a slab of the subdomain lattice
    along the last axis (rows [r*R/world, (r+1)*R/world) of the R subdomain rows). Call one

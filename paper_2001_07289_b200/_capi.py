@@ -30,7 +30,7 @@ EXPORTS = (
     "bddc_nccl_unique_id", "bddc_comm_init_nccl", "bddc_comm_init_host", "bddc_partition_info",
     "bddc_dense_potrf", "bddc_dense_trsm", "bddc_dense_gemm", "bddc_check", "bddc_update_weights",
     "bddc_coarse_solve", "bddc_read_buffer", "bddc_coarse_pattern",
-    "bddc_index_build", "bddc_index_size", "bddc_index_copy", "bddc_index_free",
+    "bddc_index_build", "bddc_index_size", "bddc_index_copy", "bddc_index_free", "bddc_coarse_csr",
 )
 
 
@@ -115,6 +115,8 @@ def load(required: bool = True):
     lib.bddc_index_copy.argtypes = [_vp, C.c_char_p, _vp, _ll]
     lib.bddc_index_free.argtypes = [_vp]
     lib.bddc_index_free.restype = None
+    lib.bddc_coarse_csr.argtypes = [_vp, _pll, _pll, _pll, _pi, _ll, _ll]
+    lib.bddc_coarse_csr.restype = _ll
     lib.bddc_launch_count.argtypes = []
     lib.bddc_launch_count.restype = _ll
     lib.bddc_event_record.argtypes = [_vp, _i]

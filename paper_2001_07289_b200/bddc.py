@@ -181,13 +181,14 @@ class BddcOperator:
             d.bnd_ptr = _capi.ptr(keep("bnd_ptr", cp.bnd_ptr, np.int32), i32)
             d.bnd_idx = _capi.ptr(keep("bnd_idx", cp.bnd_idx, np.int32), i32)
             d.rmap = _capi.ptr(keep("rmap", cp.rmap, np.int32), i32)
-            d.nnz = len(cp.csr_row)
-            d.csr_node = _capi.ptr(keep("csr_node", cp.csr_node, np.int32), i32)
-            d.csr_row = _capi.ptr(keep("csr_frow", cp.csr_frow, np.int32), i32)
-            d.csr_col = _capi.ptr(keep("csr_fcol", cp.csr_fcol, np.int32), i32)
-            d.seg_ptr = _capi.ptr(keep("seg_ptr", cp.seg_ptr, np.int64), i64)
-            d.ncontrib = len(cp.contrib)
-            d.contrib = _capi.ptr(keep("contrib", cp.contrib, np.int32), i32)
+            if len(cp.contrib):  # host-built assembly pattern (else built on the device)
+                d.nnz = len(cp.csr_row)
+                d.csr_node = _capi.ptr(keep("csr_node", cp.csr_node, np.int32), i32)
+                d.csr_row = _capi.ptr(keep("csr_frow", cp.csr_frow, np.int32), i32)
+                d.csr_col = _capi.ptr(keep("csr_fcol", cp.csr_fcol, np.int32), i32)
+                d.seg_ptr = _capi.ptr(keep("seg_ptr", cp.seg_ptr, np.int64), i64)
+                d.ncontrib = len(cp.contrib)
+                d.contrib = _capi.ptr(keep("contrib", cp.contrib, np.int32), i32)
         self._desc_arrays = arrs
         self._desc = d
         return d
@@ -413,7 +414,10 @@ def build_bddc(system: AssembledSystem, pair: PartitionPair, objects: ObjectTabl
             "any refinement Θ̂ (refine_uniform, refine_by_coefficient) is supported on top of it")
     t0 = time.perf_counter()
     constraints = select_constraints(objects, recipe, pair)
-    plan = build_device_plan(pair, constraints, weights)
+    # the coarse assembly pattern is built by the setup on the device (coarse_pattern.cu);
+    # BDDC_HOST_PATTERN=1 passes the host statement's arrays instead
+    plan = build_device_plan(pair, constraints, weights,
+                             coarse_pattern="host" if os.environ.get("BDDC_HOST_PATTERN") == "1" else "device")
     prep = time.perf_counter() - t0
     op = BddcOperator(system, pair, weights, recipe, constraints, plan, coarse_scaling, device, comm)
     op.times.prep_s = prep

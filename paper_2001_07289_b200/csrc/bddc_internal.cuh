@@ -155,6 +155,8 @@ struct FrontPlan {
   long long* seg_ptr = nullptr;        // [nnz+1] contributions of each CSR entry
   int* contrib = nullptr;              // [ncontrib] index into local coarse blocks
   double* csr_val = nullptr;           // [nnz]
+  int* csr_row_dev = nullptr;          // [nnz] elimination positions (device-built pattern only)
+  int* csr_col_dev = nullptr;
   int* coarse_slots = nullptr;         // [n_coarse x W] (sub*nc_pad + k), -1 pad
   int W = 0;
   std::vector<int> level_list;         // nodes sorted by level (see level_ptr)
@@ -166,7 +168,7 @@ struct FrontPlan {
 // carries its front's metadata (no dependent loads before its first front read).
 struct CsTask {
   long long front_off;  // front base in the pool
-  long long w_off;      // dataflow factorization: W21 (boundary rows) offset in the scratch pool
+  long long w_off;      // W21 = L21 X (fronts with s <= the W limit) offset in the scratch pool
   long long gat_base;   // node's offset into gat_ptr (child-update gathers per position)
   long long upd_off;    // node's update-vector offset
   int node, r0, c0;
@@ -174,9 +176,12 @@ struct CsTask {
   int part;             // partial slot (np > 1)
   int red;              // global reduction index (arrival counter), -1 = none
   int np;               // tasks contributing to this task's reduction (1: write directly)
-  int mode;             // forward: 0 = 64 rows x 256 columns, 1 = 256 rows x all s <= 64 columns
+  int mode;             // forward: 0 = rows of [X; W21] (64 x cw), 1 = s <= 64 (256 rows x all s),
+                        // 4 = L21 rows x y_s (64 x cw); backward: 2 = -L21^T x_bnd into t,
+                        // 3 = rows of [X; W21]^T (y + t, -x_bnd); W21 fronts: ldw > 0
   int ldw;              // leading dimension of W21 (dataflow)
-  int span;             // forward mode 0: columns per task; backward: rows per task (256 or 64)
+  int span;             // forward mode 0/4: columns per task; backward: rows per task (256 or 64)
+  int rend;             // end of the task's rows (chunks never straddle the separator / boundary split)
 };
 // Dataflow coarse solve task: forward tasks (bottom-up) then backward tasks (top-down) in one
 // queue; dependencies are node counters of finalized chunks (coarse.cu builds them).
@@ -184,7 +189,7 @@ struct SdTask {
   CsTask t;
   int dir;         // 0 forward, 1 backward
   int dep, tgt;    // wait until ctr[dep] >= tgt (dep < 0: none)
-  int sig0, sig1;  // counters incremented when this task finalizes its chunk
+  int sig0, sig1, sig2;  // counters incremented when this task finalizes its chunk
 };
 
 struct CsRed {  // reduction over the partials of one row / column chunk
@@ -203,6 +208,7 @@ struct LevelSchedule {
   std::vector<int> n_fwd_t, n_bwd_t, n_fwd_r, n_bwd_r;
   double* partial = nullptr;
   double* ybuf = nullptr;     // forward-solve values of the separator rows (n)
+  double* tbuf = nullptr;     // backward: -L21^T x_bnd of the separator rows (n; 0 where b = 0)
   int* red_cnt = nullptr;     // arrival counters of the fused reductions (self-resetting)
   int* gat_ptr = nullptr;     // per node front position -> sources in the update pool
   int* gat_src = nullptr;
@@ -373,6 +379,7 @@ struct Ctx {
 void local_setup(Ctx& c, double* workspace, size_t ws_doubles);
 size_t local_setup_workspace(const Geometry& g, int chunk);
 // coarse_coop.cu: dataflow coarse factorization and its per-front scratch layout (inverse slots, Y partials, W21 = L21 X kept for the solve)
+int coarse_w21_max_sep();
 long long coarse_df_layout(const FrontPlan& fp, std::vector<long long>& inv, std::vector<long long>& Y,
                            std::vector<long long>& W, std::vector<int>& ldw);
 // coarse.cu
@@ -387,6 +394,8 @@ struct TvArgs {
   int n;
 };
 int coarse_solve_error(Ctx& c);  // 1 if the last coarse solve hit a dependency timeout (syncs)
+// coarse assembly pattern built on the device from the con_coarse table (coarse_pattern.cu)
+void device_coarse_pattern(Ctx& c, const int* con_coarse_host);
 void coarse_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s, const TvArgs* tv = nullptr);
 // apply.cu
 void apply_bddc(Ctx& c, const double* r, double* z, cudaStream_t s);

@@ -194,20 +194,27 @@ void build_plan(Ctx& c, const bddc_setup_desc* d) {
   fp.rmap_host.assign(d->rmap, d->rmap + fp.bnd_ptr[N]);
   fd.rmap_ptr = fd.bnd_ptr;
   fp.info = c.alloc<int>(N);
-  // CSR -> front positions
-  fp.nnz = d->nnz;
-  std::vector<long long> pos(d->nnz);
-  for (long long e = 0; e < d->nnz; ++e) {
-    const int nd = d->csr_node[e];
-    if (d->csr_col[e] >= fp.sep_size[nd]) throw ApiError{1, "coarse CSR entry outside its front's panel"};
-    pos[e] = fp.front_off[nd] + d->csr_row[e] + (long long)d->csr_col[e] * fp.ld[nd];
+  if (!d->contrib) {
+    // no host pattern in the descriptor: build it on the device (coarse_pattern.cu)
+    if (!d->con_coarse) throw ApiError{1, "coarse pattern: con_coarse is required"};
+    device_coarse_pattern(c, d->con_coarse);
+    ht0.mark("plan: uploads + device CSR pattern");
+  } else {
+    // CSR -> front positions
+    fp.nnz = d->nnz;
+    std::vector<long long> pos(d->nnz);
+    for (long long e = 0; e < d->nnz; ++e) {
+      const int nd = d->csr_node[e];
+      if (d->csr_col[e] >= fp.sep_size[nd]) throw ApiError{1, "coarse CSR entry outside its front's panel"};
+      pos[e] = fp.front_off[nd] + d->csr_row[e] + (long long)d->csr_col[e] * fp.ld[nd];
+    }
+    ht0.mark("plan: uploads + CSR positions");
+    fp.csr_front_pos = c.upload(pos.data(), pos.size());
+    fp.seg_ptr = c.upload(d->seg_ptr, d->nnz + 1);
+    fp.ncontrib = d->ncontrib;
+    fp.contrib = c.upload(d->contrib, d->ncontrib);
+    fp.csr_val = c.alloc<double>(d->nnz);
   }
-  ht0.mark("plan: uploads + CSR positions");
-  fp.csr_front_pos = c.upload(pos.data(), pos.size());
-  fp.seg_ptr = c.upload(d->seg_ptr, d->nnz + 1);
-  fp.ncontrib = d->ncontrib;
-  fp.contrib = c.upload(d->contrib, d->ncontrib);
-  fp.csr_val = c.alloc<double>(d->nnz);
   fp.coarse_slots = c.upload(d->coarse_slots, (size_t)d->n_coarse * fp.W);
   HostTimer ht;
   build_level_schedule(c);
@@ -808,6 +815,31 @@ int bddc_profile(bddc_ctx* h, int enable) {
 double bddc_profile_read(bddc_ctx* h, const char* phase, long long* count) {
   if (!h || !phase || !count) return -1.0;
   return h->c.prof.read(phase, count);
+}
+
+long long bddc_coarse_csr(bddc_ctx* h, long long* row, long long* col, long long* seg_ptr, int* contrib,
+                          long long cap_nnz, long long cap_contrib) {
+  if (!h) return -1;
+  const FrontPlan& fp = h->c.fp;
+  if (!fp.csr_row_dev && fp.nnz > 0) return -1;  // pattern came from the host descriptor
+  if (!row && !col && !seg_ptr && !contrib) return fp.nnz;
+  if (cap_nnz < fp.nnz || (contrib && cap_contrib < fp.ncontrib)) return -1;
+  if (cudaSetDevice(h->c.device) != cudaSuccess || cudaStreamSynchronize(h->c.stream) != cudaSuccess) return -1;
+  std::vector<int> tmp(std::max(fp.nnz, 1LL));
+  for (int which = 0; which < 2; ++which) {
+    long long* out = which ? col : row;
+    if (!out) continue;
+    if (fp.nnz && cudaMemcpy(tmp.data(), which ? fp.csr_col_dev : fp.csr_row_dev, sizeof(int) * fp.nnz,
+                             cudaMemcpyDeviceToHost) != cudaSuccess)
+      return -1;
+    for (long long e = 0; e < fp.nnz; ++e) out[e] = tmp[e];
+  }
+  if (seg_ptr && cudaMemcpy(seg_ptr, fp.seg_ptr, sizeof(long long) * (fp.nnz + 1), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -1;
+  if (contrib && fp.ncontrib &&
+      cudaMemcpy(contrib, fp.contrib, sizeof(int) * fp.ncontrib, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -1;
+  return fp.nnz;
 }
 
 long long bddc_read_buffer(bddc_ctx* h, const char* name, long long offset, long long count, double* host) {

@@ -35,14 +35,19 @@ __global__ void csr_to_front_kernel(long long nnz, const long long* __restrict__
 
 }  // namespace
 
-// Solve plan. Forward (per level, bottom-up): y_sep = X (rhs + child updates) and
-// upd = gathered - W21 (rhs + ...), as GEMV tasks over each front's partitioned inverse:
-//   * s <= 64 ("row" tasks): 256 rows x all separator columns, one thread per row, the row
-//     sums are complete inside the task (written directly);
-//   * otherwise 64 rows x 256 columns; the row chunk's partials are summed by the last task
-//     to arrive (fixed order).
-// Backward (top-down): x_sep = X^T y_sep - W21^T x_bnd, 256 rows x 64 columns per task,
-// partials over row chunks summed likewise (directly when a chunk has one task).
+// Solve plan. Every front holds [X; L21] (X = L11^{-1}, the partitioned inverse of the pivot
+// block); fronts with s <= coarse_w21_max_sep() also keep W21 = L21 X (scratch pool).
+// W21 fronts, one GEMV phase per direction:
+//   forward  y_s = X v, upd = gathered - W21 v  (v = rhs + child updates)
+//   backward x_s = X^T y_s - W21^T x_bnd
+//   * s <= 64 ("row" tasks, mode 1): 256 rows x all separator columns, one thread per row;
+//   * otherwise 64 rows x 64 (256) columns (mode 0 / 3); the row (column) chunk's partials
+//     are summed by the last task to arrive (fixed order).
+// L21 fronts (the top of the tree), two phases per direction with per-chunk dependencies:
+//   forward  y_s = X v (mode 0, rows < s), then upd = gathered - L21 y_s (mode 4: column chunk
+//            c0 waits for y_s chunk c0 only)
+//   backward t = -L21^T x_bnd (mode 2), then x_s = X^T (y_s + t) (mode 3: row chunk r0 waits
+//            for t chunk r0 only)
 void build_level_schedule(Ctx& c) {
   LevelSchedule& ls = c.sched;
   ls = LevelSchedule{};
@@ -82,10 +87,9 @@ void build_level_schedule(Ctx& c) {
   std::vector<CsRed> fr, br;
   std::vector<size_t> ft_off(L + 1), bt_off(L + 1), fr_off(L + 1), br_off(L + 1);
   int max_parts = 0;
-  // dataflow factorization: W21 (rows >= s of every front) stays in the scratch pool
   std::vector<long long> l_inv, l_y, l_w;
   std::vector<int> l_ldw;
-  coarse_df_layout(fp, l_inv, l_y, l_w, l_ldw);
+  coarse_df_layout(fp, l_inv, l_y, l_w, l_ldw);  // W21 fronts: l_ldw > 0
   auto base = [&](int nd) {
     CsTask t{};
     t.front_off = fp.front_off[nd];
@@ -105,16 +109,36 @@ void build_level_schedule(Ctx& c) {
   };
   // partial slots are unique over the whole solve (the dataflow solve overlaps levels)
   std::vector<int> nfch(fp.nnodes, 0), nbch(fp.nnodes, 0);  // finalized chunks per node
+  // L21 fronts: per-chunk counters of y_s (forward) and t (backward), chunk = 64 rows / columns
+  std::vector<int> ych(fp.nnodes, -1), tch(fp.nnodes, -1);
+  int nchunk_ctr = 0;
   int pf = 0, pb = 0;
+  // one reduction chunk: tasks [first, end) share partials (np > 1) or write directly
+  auto close_chunk = [](std::vector<CsTask>& v, std::vector<CsRed>& red, size_t first, int p0, int t0) {
+    const int cnt = (int)(v.size() - first);
+    for (size_t q = first; q < v.size(); ++q) {
+      v[q].np = cnt;
+      v[q].red = cnt > 1 ? (int)red.size() : -1;
+    }
+    if (cnt > 1) red.push_back(CsRed{t0, p0, cnt});
+    return cnt;
+  };
   for (int l = 0; l < L; ++l) {
     ft_off[l] = ft.size(); bt_off[l] = bt.size(); fr_off[l] = fr.size(); br_off[l] = br.size();
     for (int i = fp.level_ptr[l]; i < fp.level_ptr[l + 1]; ++i) {
       const int nd = fp.level_list[i];
       const int sz = fp.sep_size[nd], f = sz + fp.bnd_size[nd];
+      const bool wf = l_ldw[nd] > 0 || fp.bnd_size[nd] == 0;  // W21 front (or no boundary)
+      if (!wf) {
+        if (sz < 128) throw CudaError("coarse solve plan: L21 fronts need s >= 128");
+        ych[nd] = nchunk_ctr; nchunk_ctr += ceil_div(sz, 64);
+        tch[nd] = nchunk_ctr; nchunk_ctr += ceil_div(sz, 64);
+      }
       if (sz <= 64) {
         for (int r0 = 0; r0 < f; r0 += 256) {
           CsTask t = base(nd);
           t.r0 = r0;
+          t.rend = std::min(r0 + 256, f);
           t.mode = 1;
           ft.push_back(t);
           nfch[nd]++;
@@ -123,48 +147,45 @@ void build_level_schedule(Ctx& c) {
         // large separators (the top of the tree, where the level chain is the critical path):
         // narrow tasks whose front entries are all in flight before the dependency wait
         const int cw = sz >= 128 ? 64 : 256;
-        for (int r0 = 0; r0 < f; r0 += 64) {
-          const size_t first = ft.size();
-          const int p0 = pf;
-          for (int c0 = 0; c0 < sz; c0 += cw) {
-            // separator rows: L11^{-1} is lower triangular
-            if (r0 < sz && c0 > r0 + 63) break;
-            CsTask t = base(nd);
-            t.r0 = r0;
-            t.c0 = c0;
-            t.part = pf++;
-            t.mode = 0;
-            t.span = cw;
-            ft.push_back(t);
+        for (int pass = 0; pass < (wf ? 1 : 2); ++pass) {  // [X; W21] rows | X rows, then L21 rows
+          const int rbeg = pass ? sz : 0, rlim = (pass || wf) ? f : sz;
+          for (int r0 = rbeg; r0 < rlim; r0 += 64) {
+            const size_t first = ft.size();
+            const int p0 = pf;
+            const int rend = std::min(r0 + 64, rlim);
+            for (int c0 = 0; c0 < sz; c0 += cw) {
+              if (!pass && r0 < sz && c0 > std::min(rend, sz) - 1) break;  // X is lower triangular
+              CsTask t = base(nd);
+              t.r0 = r0;
+              t.rend = rend;
+              t.c0 = c0;
+              t.part = pf++;
+              t.mode = pass ? 4 : 0;
+              t.span = cw;
+              ft.push_back(t);
+            }
+            if (close_chunk(ft, fr, first, p0, r0) > 0) nfch[nd]++;
           }
-          const int cnt = (int)(ft.size() - first);
-          if (cnt > 0) nfch[nd]++;
-          for (size_t q = first; q < ft.size(); ++q) {
-            ft[q].np = cnt;
-            ft[q].red = cnt > 1 ? (int)fr.size() : -1;
-          }
-          if (cnt > 1) fr.push_back(CsRed{r0, p0, cnt});
         }
       }
       const int rw = sz >= 128 ? 64 : 256;
-      for (int c0 = 0; c0 < sz; c0 += 64) {
-        const size_t first = bt.size();
-        const int p0 = pb;
-        for (int r0 = (c0 / rw) * rw; r0 < f; r0 += rw) {
-          CsTask t = base(nd);
-          t.r0 = r0;
-          t.c0 = c0;
-          t.span = rw;
-          t.part = pb++;
-          bt.push_back(t);
+      for (int pass = (wf ? 1 : 0); pass < 2; ++pass) {  // (L21: t = -L21^T x_bnd), then x_s
+        for (int c0 = 0; c0 < sz; c0 += 64) {
+          const size_t first = bt.size();
+          const int p0 = pb;
+          const int rbeg = pass ? (c0 / rw) * rw : sz, rlim = (pass && !wf) ? sz : f;
+          for (int r0 = rbeg; r0 < rlim; r0 += rw) {
+            CsTask t = base(nd);
+            t.r0 = r0;
+            t.rend = std::min(r0 + rw, rlim);
+            t.c0 = c0;
+            t.span = rw;
+            t.part = pb++;
+            t.mode = pass ? 3 : 2;
+            bt.push_back(t);
+          }
+          if (close_chunk(bt, br, first, p0, c0) > 0 && pass) nbch[nd]++;
         }
-        const int cnt = (int)(bt.size() - first);
-        if (cnt > 0) nbch[nd]++;
-        for (size_t q = first; q < bt.size(); ++q) {
-          bt[q].np = cnt;
-          bt[q].red = cnt > 1 ? (int)br.size() : -1;
-        }
-        if (cnt > 1) br.push_back(CsRed{c0, p0, cnt});
       }
     }
   }
@@ -184,11 +205,14 @@ void build_level_schedule(Ctx& c) {
   }
   ls.partial = c.alloc<double>((size_t)std::max(max_parts, 1) * 64);
   ls.ybuf = c.alloc<double>((size_t)std::max(fp.n_coarse, 1));
+  ls.tbuf = c.alloc<double>((size_t)std::max(fp.n_coarse, 1));
+  BDDC_CUDA(cudaMemset(ls.tbuf, 0, sizeof(double) * std::max(fp.n_coarse, 1)));  // stays 0 where b = 0
   ls.red_cnt = c.alloc<int>(fr.size() + br.size() + 1);
   BDDC_CUDA(cudaMemset(ls.red_cnt, 0, sizeof(int) * (fr.size() + br.size() + 1)));
   {
     // dataflow solve queue. Counters: [0, N) finalized forward chunks of each node's children,
-    // [N, 2N) own forward chunks, [2N, 3N) own backward chunks.
+    // [N, 2N) own forward chunks, [2N, 3N) own x_s chunks, then per 64-chunk y_s / t counters
+    // of the L21 fronts.
     const int N = fp.nnodes;
     std::vector<int> need(N, 0);
     for (int nd = 0; nd < N; ++nd)
@@ -212,11 +236,12 @@ void build_level_schedule(Ctx& c) {
         SdTask d{};
         d.t.node = next_sub;
         d.dir = 2;
-        d.dep = d.sig0 = d.sig1 = -1;
+        d.dep = d.sig0 = d.sig1 = d.sig2 = -1;
         q.push_back(d);
         ls.n_tv++;
       }
     };
+    const int C0 = 3 * N;  // per-chunk counters of the L21 fronts start here
     for (int l = 0; l < L; ++l) {  // forward: level order, bottom-up
       if (l >= L - K) emit_tv(false);
       for (size_t i = ft_off[l]; i < ft_off[l + 1]; ++i) {
@@ -224,8 +249,15 @@ void build_level_schedule(Ctx& c) {
         SdTask d{};
         d.t = t;
         d.dir = 0;
-        d.dep = need[t.node] > 0 ? t.node : -1;
-        d.tgt = need[t.node];
+        d.sig2 = -1;
+        if (t.mode == 4) {  // L21 rows x y_s chunk c0 (cw = 64)
+          d.dep = C0 + ych[t.node] + t.c0 / 64;
+          d.tgt = 1;
+        } else {
+          d.dep = need[t.node] > 0 ? t.node : -1;
+          d.tgt = need[t.node];
+          if (ych[t.node] >= 0) d.sig2 = C0 + ych[t.node] + t.r0 / 64;  // y_s chunk final
+        }
         d.sig0 = fp.parent[t.node] >= 0 ? fp.parent[t.node] : -1;
         d.sig1 = N + t.node;
         q.push_back(d);
@@ -235,23 +267,29 @@ void build_level_schedule(Ctx& c) {
       if (l >= L - K) emit_tv(l == L - K);
       for (size_t i = bt_off[l]; i < bt_off[l + 1]; ++i) {
         const CsTask& t = bt[i];
-        int anc = fp.parent[t.node];
-        while (anc >= 0 && nbch[anc] == 0) anc = fp.parent[anc];
         SdTask d{};
         d.t = t;
         d.dir = 1;
-        d.dep = anc >= 0 ? 2 * N + anc : N + t.node;
-        d.tgt = anc >= 0 ? nbch[anc] : nfch[t.node];
-        if (d.tgt <= 0) d.dep = -1;
-        d.sig0 = 2 * N + t.node;
-        d.sig1 = -1;
+        d.sig1 = d.sig2 = -1;
+        if (t.mode == 3 && tch[t.node] >= 0) {  // X^T (y + t), rows r0: after t chunk r0 (rw = 64)
+          d.dep = C0 + tch[t.node] + t.r0 / 64;
+          d.tgt = 1;
+        } else {  // the nearest ancestor's x_s final (without one: the front's own forward)
+          int anc = fp.parent[t.node];
+          while (anc >= 0 && nbch[anc] == 0) anc = fp.parent[anc];
+          d.dep = anc >= 0 ? 2 * N + anc : N + t.node;
+          d.tgt = anc >= 0 ? nbch[anc] : nfch[t.node];
+          if (d.tgt <= 0) d.dep = -1;
+        }
+        if (t.mode == 3) d.sig0 = 2 * N + t.node;
+        else d.sig0 = C0 + tch[t.node] + t.c0 / 64;  // t chunk final
         q.push_back(d);
       }
     }
     emit_tv(true);  // (L == 0)
     ls.n_df = (int)q.size();
     ls.df_tasks = c.upload<SdTask>(q.data(), std::max<size_t>(q.size(), 1));
-    ls.n_ctr = 3 * N;
+    ls.n_ctr = 3 * N + nchunk_ctr;
     ls.df_ctr = c.alloc<int>(ls.n_ctr + 2);  // + queue head + error flag
     BDDC_CUDA(cudaMemset(ls.df_ctr, 0, sizeof(int) * (ls.n_ctr + 2)));
   }

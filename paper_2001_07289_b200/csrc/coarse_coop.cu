@@ -338,7 +338,8 @@ struct SolveProgram {
   const int* br_off;
   int nlevels;
   int nfr;  // number of forward reductions (offset of the backward counters)
-  const double* wpool;  // dataflow: W21 rows (r >= s) read from here (CsTask w_off / ldw)
+  const double* wpool;  // W21 rows (r >= s) of the W21 fronts (CsTask w_off / ldw)
+  double* tbuf;         // backward: t = -L21^T x_bnd per separator row of the L21 fronts
   int n;                // coarse size
 };
 
@@ -409,11 +410,16 @@ __device__ __forceinline__ double sum_partials_cta(const double* __restrict__ pa
   return tid < 64 ? ((red[o] + red[64 + o]) + (red[128 + o] + red[192 + o])) : 0.0;
 }
 
-// Forward task (bottom-up): y_sep = X (rhs + child updates), upd = gathered - W21 (..).
+// Forward task (bottom-up). A front holds [X; L21] (X = L11^{-1}); fronts with s up to the W
+// limit also keep W21 = L21 X in the scratch pool (t.ldw > 0). Modes:
+//   0: rows of [X; W21] times v = rhs + child updates: y_s (rows < s), upd = gathered - W21 v;
+//      for L21 fronts only rows < s (their chunks end at s)
+//   1: s <= 64 (W21 fronts): 256 rows x all separator columns, one thread per row
+//   4: L21 rows times the final y_s chunk: upd = gathered - L21 y_s
 // Everything that does not depend on other tasks (front entries, gather indices) is loaded
-// before wait() (the dataflow dependency wait; a no-op between grid barriers). Returns true
-// when this CTA wrote the chunk's final values (single task, or the last of the chunk's
-// tasks to arrive, which sums the partials in fixed order: deterministic).
+// before wait() (the dataflow dependency wait). Returns true when this CTA wrote the chunk's
+// final values (single task, or the last of the chunk's tasks to arrive, which sums the
+// partials in fixed order: deterministic).
 template <class Wait>
 __device__ bool solve_fwd_task(const CsTask& t, const FrontDev& fd, const LevelView& lv, const SolveProgram& sp,
                                const double* __restrict__ rhs, double* __restrict__ partial,
@@ -421,12 +427,13 @@ __device__ bool solve_fwd_task(const CsTask& t, const FrontDev& fd, const LevelV
   const int tid = threadIdx.x;
   const double* F = fd.fronts + t.front_off;
   const long long ld = t.ld;
-  const int s = t.s, f = t.f;
+  const int s = t.s;
+  const bool wf = t.ldw > 0;  // W21 front
   __syncthreads();
   if (t.mode == 1) {  // s <= 64: one thread per row, all separator columns
     const int r = t.r0 + tid;
-    const int ke = r < f ? (r < s ? r + 1 : s) : 0;
-    const bool wr = sp.wpool && r >= s;  // dataflow factorization: W21 rows from the scratch pool
+    const int ke = r < t.rend ? (r < s ? r + 1 : s) : 0;
+    const bool wr = r >= s;
     const double* Fr = wr ? sp.wpool + t.w_off + (r - s) : F + r;
     const long long lr = wr ? (long long)t.ldw : ld;
     double fv[16];
@@ -434,13 +441,13 @@ __device__ bool solve_fwd_task(const CsTask& t, const FrontDev& fd, const LevelV
     for (int u = 0; u < 16; ++u) fv[u] = u < ke ? __ldcs(Fr + (long long)u * lr) : 0.0;
     GatherPre gv, gr;
     gv.load(lv, t.gat_base, tid, tid < s);
-    gr.load(lv, t.gat_base, r, r >= s && r < f);
+    gr.load(lv, t.gat_base, r, r >= s && r < t.rend);
     const double rv = tid < s ? rhs[t.s0 + tid] : 0.0;
     wait();
     if (tid < s) sh.vs[tid] = rv + gv.value(lv, fd.upd);
     const double gu = gr.value(lv, fd.upd);
     __syncthreads();
-    if (r < f) {
+    if (r < t.rend) {
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
       for (int k0 = 0; k0 < ke; k0 += 16) {
         if (k0 > 0) {
@@ -456,13 +463,14 @@ __device__ bool solve_fwd_task(const CsTask& t, const FrontDev& fd, const LevelV
     }
     return true;
   }
+  const bool lrows = t.mode == 4;  // L21 rows x the final y_s
   const int rr = tid & 63, grp = tid >> 6;
   const int r = t.r0 + rr;
   const int cg = t.span >> 2;  // columns per thread group: 64, or 16 (one batch, before the wait)
   const int kb = t.c0 + grp * cg;
-  int ke = r < f ? min(kb + cg, s) : kb;
+  int ke = r < t.rend ? min(kb + cg, s) : kb;
   if (r < s) ke = min(ke, r + 1);
-  const bool wr = sp.wpool && r >= s;
+  const bool wr = wf && r >= s;
   const double* Fr = wr ? sp.wpool + t.w_off + (r - s) : F + r;
   const long long lr = wr ? (long long)t.ldw : ld;
   double fv[16];
@@ -471,11 +479,13 @@ __device__ bool solve_fwd_task(const CsTask& t, const FrontDev& fd, const LevelV
   const int kk = t.c0 + tid;
   const int rw = t.r0 + tid;  // row finalized by this thread (tid < 64)
   GatherPre gv, gr;
-  gv.load(lv, t.gat_base, kk, kk < s && tid < t.span);
-  gr.load(lv, t.gat_base, rw, tid < 64 && rw < f && rw >= s);
-  const double rv = kk < s ? rhs[t.s0 + kk] : 0.0;
+  gv.load(lv, t.gat_base, kk, !lrows && kk < s && tid < t.span);
+  gr.load(lv, t.gat_base, rw, tid < 64 && rw < t.rend && rw >= s);
+  const double rv = (!lrows && kk < s) ? rhs[t.s0 + kk] : 0.0;
   wait();
-  sh.vs[tid] = (kk < s && tid < t.span) ? rv + gv.value(lv, fd.upd) : 0.0;
+  double vin = 0.0;
+  if (kk < s && tid < t.span) vin = lrows ? __ldcg(ybuf + t.s0 + kk) : rv + gv.value(lv, fd.upd);
+  sh.vs[tid] = vin;
   __syncthreads();
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   for (int k0 = kb; k0 < ke; k0 += 16) {
@@ -493,7 +503,7 @@ __device__ bool solve_fwd_task(const CsTask& t, const FrontDev& fd, const LevelV
     else fd.upd[t.upd_off + (rw - s)] = gr.value(lv, fd.upd) - a;
   };
   if (t.np == 1) {
-    if (tid < 64 && rw < f) finish(sh.red[0][tid] + sh.red[1][tid] + sh.red[2][tid] + sh.red[3][tid]);
+    if (tid < 64 && rw < t.rend) finish(sh.red[0][tid] + sh.red[1][tid] + sh.red[2][tid] + sh.red[3][tid]);
     return true;
   }
   if (tid < 64) {
@@ -507,22 +517,26 @@ __device__ bool solve_fwd_task(const CsTask& t, const FrontDev& fd, const LevelV
   __threadfence();
   const CsRed R = sp.fr[t.red];
   const double a = sum_partials_cta(partial, R.p0, R.np, sh);
-  if (tid < 64 && rw < f) finish(a);
+  if (tid < 64 && rw < t.rend) finish(a);
   if (tid == 0) cnt_f[t.red] = 0;
   return true;
 }
 
-// Backward task (top-down): x_sep = X^T y_sep - W21^T x_bnd, 256 rows x 64 columns.
+// Backward task (top-down), rw rows x 64 columns. Mode 3: rows of [X; W21]^T:
+// x_s = X^T (y_s + t) - W21^T x_bnd (t = 0 and W21 rows on the W21 fronts; X rows only on the
+// L21 fronts); mode 2 (L21 fronts, rows >= s): t = -L21^T x_bnd.
 template <class Wait>
 __device__ bool solve_bwd_task(const CsTask& t, const FrontDev& fd, const SolveProgram& sp,
                                double* __restrict__ sol, double* __restrict__ partial,
                                const double* __restrict__ ybuf, int* __restrict__ cnt_b, SolveShared& sh,
                                Wait wait) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int s = t.s, f = t.f;
+  const int s = t.s;
   const long long ld = t.ld;
+  const bool wf = t.ldw > 0;
   const int* bidx = fd.bnd_idx + fd.bnd_ptr[t.node];
   const double* F = fd.fronts + t.front_off;
+  double* dst = t.mode == 2 ? sp.tbuf : sol;
   __syncthreads();
   // warp: 8 columns; lane: rows i = lane + 32 m; 16 loads in flight per batch
   const int kw = t.c0 + warp * 8;
@@ -531,28 +545,28 @@ __device__ bool solve_bwd_task(const CsTask& t, const FrontDev& fd, const SolveP
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int i = lane + 32 * (m + h), r = t.r0 + i;
-      const bool wr = sp.wpool && r >= s;
+      const bool wr = wf && r >= s;
       const double* Fr = wr ? sp.wpool + t.w_off + (r - s) : F + r;
       const long long lr = wr ? (long long)t.ldw : ld;
 #pragma unroll
       for (int cc = 0; cc < 8; ++cc) {
         const int k = kw + cc;
-        const bool ok = k < s && r < f && (r >= s || r >= k);
+        const bool ok = k < s && r < t.rend && (r >= s || r >= k);
         fv[h][cc] = ok ? __ldcs(Fr + (long long)k * lr) : 0.0;
       }
     }
   };
   load_rows(0);
   const int r = t.r0 + tid;
-  const bool mine = tid < t.span;
-  const int bi = (mine && r >= s && r < f) ? bidx[r - s] : -1;
+  const bool mine = tid < t.span && r < t.rend;
+  const int bi = (mine && r >= s) ? bidx[r - s] : -1;
   wait();
-  sh.vs[tid] = (mine && r < s) ? __ldcg(ybuf + t.s0 + r) : (bi >= 0 ? -__ldcg(sol + bi) : 0.0);
+  sh.vs[tid] = !mine ? 0.0 : (r >= s ? -__ldcg(sol + bi) : __ldcg(ybuf + t.s0 + r) + __ldcg(sp.tbuf + t.s0 + r));
   __syncthreads();
   double acc[8];
 #pragma unroll
   for (int cc = 0; cc < 8; ++cc) acc[cc] = 0.0;
-  const int mend = min(t.span >> 5, (f - t.r0 + 31) / 32);  // row batches that hold front rows
+  const int mend = min(t.span >> 5, (t.rend - t.r0 + 31) / 32);  // row batches that hold task rows
 #pragma unroll
   for (int m = 0; m < 8; m += 2) {
     if (m >= mend) break;
@@ -567,7 +581,7 @@ __device__ bool solve_bwd_task(const CsTask& t, const FrontDev& fd, const SolveP
     for (int cc = 0; cc < 8; ++cc) {
       const double v = warp_sum(acc[cc]);
       const int k = kw + cc;
-      if (lane == 0 && k < s) sol[t.s0 + k] = v;
+      if (lane == 0 && k < s) dst[t.s0 + k] = v;
     }
     return true;
   }
@@ -585,7 +599,7 @@ __device__ bool solve_bwd_task(const CsTask& t, const FrontDev& fd, const SolveP
   const CsRed R = sp.br[t.red];
   const int k = R.t0 + tid;
   const double a = sum_partials_cta(partial, R.p0, R.np, sh);
-  if (tid < 64 && k < s) sol[t.s0 + k] = a;
+  if (tid < 64 && k < s) dst[t.s0 + k] = a;
   if (tid == 0) cnt_b[t.red] = 0;
   return true;
 }
@@ -690,6 +704,7 @@ __global__ void __launch_bounds__(256, 3) coop_solve_df_kernel(FrontDev fd, Leve
       __threadfence();
       if (T.sig0 >= 0) atomicAdd(ctr + T.sig0, 1);
       if (T.sig1 >= 0) atomicAdd(ctr + T.sig1, 1);
+      if (T.sig2 >= 0) atomicAdd(ctr + T.sig2, 1);
     }
     if (tid < kWords && tn < ntasks) reinterpret_cast<int*>(&tsh[buf ^ 1])[tid] = nw;
     __syncthreads();
@@ -719,19 +734,30 @@ struct CoopState {
 
 static std::map<const Ctx*, CoopState> g_coop;
 
+// Fronts whose separator is at most this size keep W21 = L21 X for the solve (one GEMV phase
+// per front and direction); larger ones (the top of the tree: 78% of the W21 flops at cfg5 in
+// 15 fronts) solve with L21 in place and one more dependent GEMV phase (coarse.cu).
+int coarse_w21_max_sep() {  // (>= 127: L21 fronts have separators of two 64-chunks or more)
+  const char* e = getenv("BDDC_W21_MAX_SEP");
+  return e ? std::max(atoi(e), 127) : 2048;
+}
+
 long long coarse_df_layout(const FrontPlan& fp, std::vector<long long>& inv, std::vector<long long>& Y,
                            std::vector<long long>& W, std::vector<int>& ldw) {
   const int N = fp.nnodes;
-  inv.assign(N, 0); Y.assign(N, 0); W.assign(N, 0); ldw.assign(N, 2);
+  const int wmax = coarse_w21_max_sep();
+  inv.assign(N, 0); Y.assign(N, 0); W.assign(N, 0); ldw.assign(N, 0);
   long long off = 0;  // every front its own scratch (levels overlap in the dataflow program)
   for (int l = 0; l < fp.nlevels; ++l)
     for (int i = fp.level_ptr[l]; i < fp.level_ptr[l + 1]; ++i) {
       const int nd = fp.level_list[i];
       const int s = fp.sep_size[nd], b = fp.bnd_size[nd], np = ceil_div(s, kTile);
-      ldw[nd] = (int)round_up(std::max(b, 2), 2);
       inv[nd] = off; off += (long long)std::max(np, 1) * kTileInvStride;
       Y[nd] = off; off += 2 * round_up((long long)kTile * std::max(s, 1), 2) * ceil_div(std::max(s, 1), kX1Chunk);
-      W[nd] = off; off += round_up((long long)ldw[nd] * std::max(s, 1), 2);
+      if (s <= wmax) {  // W21 front (ldw > 0 marks it for the solve)
+        ldw[nd] = (int)round_up(std::max(b, 2), 2);
+        W[nd] = off; off += round_up((long long)ldw[nd] * std::max(s, 1), 2);
+      }
     }
   return std::max(off, 2LL);
 }
@@ -935,7 +961,7 @@ void coop_build(Ctx& c) {
           }
         }
         const int b = f - s;
-        if (b > 0) {
+        if (b > 0 && ldw[nd] > 0) {  // W21 = L21 X for the solve (coarse_w21_max_sep)
           for (int a = 0; a < ceil_div(b, kTile); ++a)
             for (int cc = 0; cc < np; ++cc) {
               DfTask t = mk(CT_W, nd, a, cc, 0);
@@ -946,7 +972,7 @@ void coop_build(Ctx& c) {
               tot_w[nd]++;
             }
         }
-        // W21 stays in the scratch pool for the solve; X is in place in the front
+        // X is in place in the front over L11; L21 stays; W21 (if any) in the scratch pool
       }
     }
     pool = std::max(pool, off);
@@ -1074,6 +1100,7 @@ void coop_build(Ctx& c) {
   st.sp.fr = ls.fwd_r[0];
   st.sp.br = ls.bwd_r[0];
   st.sp.nfr = nfr;
+  st.sp.tbuf = ls.tbuf;
   st.sp.wpool = st.pg.pool;
   st.sp.n = fp.n_coarse;
 }

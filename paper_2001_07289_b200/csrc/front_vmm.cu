@@ -109,17 +109,18 @@ bool front_alias_layout(Ctx& c) {
   prop.location.id = c.device;
   size_t g = 0;
   cu_check(d.gran(&g, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED), "granularity");
-  // Page size: every mapped page costs one cuMemMap + its share of cuMemSetAccess (~0.2 ms
-  // each, serialized in the driver: tools/vmm_probe.cu), while larger pages waste more of
-  // each aliased block's last page. Take the largest page (up to 32 MB) whose resident total
-  // stays within half of the free memory (the local factors come after this plan).
+  // Page size: every mapping costs a cuMemMap + its share of cuMemSetAccess (~0.2 ms each,
+  // serialized in the driver: tools/vmm_probe.cu), while larger pages waste more of each
+  // aliased block's last page (cfg5: 75.5 GB resident at 2 MB, 86 GB at 8 MB, and the local
+  // setup then runs in 4x more memory-bound chunks). Default 2 MB (BDDC_FRONT_PAGE_MB
+  // overrides); the mapping count is cut by merging pool runs below instead.
   size_t free_b = 0, total_b = 0;
   BDDC_CUDA(cudaMemGetInfo(&free_b, &total_b));
   const char* pe = getenv("BDDC_FRONT_PAGE_MB");
   const char* te = getenv("BDDC_FRONT_ALIAS_MIN_MB");  // aliasing threshold (default: one page)
   std::vector<long long> cands;
   if (pe) cands.push_back((long long)atoi(pe) << 20);
-  else for (long long mb = 32; mb >= 2; mb >>= 1) cands.push_back(mb << 20);
+  else cands.push_back(2LL << 20);
   long long PG = 0, vpages = 0, upages = 0;
   std::vector<long long> u, upage, need, choff, front_off;
   using Runs = std::vector<std::pair<long long, long long>>;  // (first page, count)
@@ -238,26 +239,41 @@ bool front_alias_layout(Ctx& c) {
     p = q;
   }
   ht.mark("alias: persistent runs");
-  // pool: one allocation per page, mapped into the pool view and under every update block
-  // the planner placed on it
-  std::vector<CUmemGenericAllocationHandle> page(upages);
-  for (long long k = 0; k < upages; ++k) {
-    page[k] = create(PB);
-    map(vm->uview + (size_t)k * PB, PB, page[k]);
-  }
-  ht.mark("alias: pool pages");
+  // pool: consecutive pages used by exactly the same update blocks at consecutive virtual
+  // pages form one allocation (every mapping costs a driver call: ~3.5x fewer at cfg5),
+  // mapped into the pool view and under each of those update blocks
+  std::vector<std::vector<std::pair<int, long long>>> users(upages);  // (front, virtual page)
   for (int i = 0; i < N; ++i) {
     long long vp = upage[i];
     for (auto& r : urun[i])
-      for (long long k = 0; k < r.second; ++k, ++vp) map(vm->va + (size_t)vp * PB, PB, page[base[i] + r.first + k]);
+      for (long long k = 0; k < r.second; ++k, ++vp) users[base[i] + r.first + k].push_back({i, vp});
   }
-  ht.mark("alias: update-block maps");
+  long long nruns = 0, nmaps = 0;
+  for (long long p0 = 0; p0 < upages;) {
+    long long p1 = p0 + 1;
+    auto same = [&](long long q) {
+      if (users[q].size() != users[p0].size()) return false;
+      for (size_t j = 0; j < users[q].size(); ++j)
+        if (users[q][j].first != users[p0][j].first || users[q][j].second != users[p0][j].second + (q - p0))
+          return false;
+      return true;
+    };
+    while (p1 < upages && same(p1)) ++p1;
+    const size_t bytes = (size_t)(p1 - p0) * PB;
+    const CUmemGenericAllocationHandle h = create(bytes);
+    map(vm->uview + (size_t)p0 * PB, bytes, h);
+    for (auto& us : users[p0]) map(vm->va + (size_t)us.second * PB, bytes, h);
+    ++nruns;
+    nmaps += 1 + (long long)users[p0].size();
+    p0 = p1;
+  }
+  ht.mark("alias: pool runs + update-block maps");
   if (ht.on) {
-    long long nal = 0, nmap = 0;
-    for (int i = 0; i < N; ++i) nal += u[i] > 0, nmap += u[i];
+    long long nal = 0;
+    for (int i = 0; i < N; ++i) nal += u[i] > 0;
     fprintf(stderr, "bddc_setup host: alias: page %lld MB, %lld virtual / %lld persistent / %lld pool pages, "
-            "%lld aliased fronts, %lld update-block page maps, %zu allocations\n", PG * 8 >> 20, vpages, ppages,
-            upages, nal, nmap, vm->handles.size());
+            "%lld aliased fronts, %lld pool runs, %lld pool mappings, %zu allocations\n", PG * 8 >> 20, vpages,
+            ppages, upages, nal, nruns, nmaps, vm->handles.size());
   }
   CUmemAccessDesc acc{};
   acc.location = prop.location;

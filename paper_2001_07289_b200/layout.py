@@ -99,7 +99,10 @@ class DevicePlan:
 
 
 def build_device_plan(pair: PartitionPair, cons: ConstraintTable,
-                      weights: WeightingOperator) -> DevicePlan:
+                      weights: WeightingOperator, coarse_pattern: str = "host") -> DevicePlan:
+    """``coarse_pattern``: "host" computes the coarse assembly pattern here (symbolic.py /
+    host_plan.cu); "device" leaves it to the setup, which builds it on the GPU from
+    ``con_coarse`` (coarse_pattern.cu)."""
     mesh = pair.mesh
     layout_info = pair.box_layout
     if layout_info is None:
@@ -195,7 +198,8 @@ def build_device_plan(pair: PartitionPair, cons: ConstraintTable,
     if n_con:
         plan = symbolic.analyze(n_con, con_owners, pc, tuple(subs), sub_con_ptr=sub_con_ptr,
                                 sub_con_ids=pair_con)
-        COARSE_CSR(plan, sub_con_ptr, pair_con, nc_pad)
+        if coarse_pattern == "host":
+            COARSE_CSR(plan, sub_con_ptr, pair_con, nc_pad)
         con_coarse[pair_sub, local_k] = plan.iperm[pair_con]
         # owners of each constraint (ascending) -> slot sub*nc_pad + k, rows in elimination order
         ks = np.where(pv, 0, -1).astype(np.int64)

@@ -193,15 +193,39 @@ class SubdomainList:
             yield self[i]
 
 
+def device_coarse_pattern(op):
+    """(row, col, seg_ptr, contrib) of the coarse assembly pattern the setup built on the
+    device (elimination order; bddc_coarse_csr)."""
+    import ctypes as C
+
+    lib = op._lib
+    nnz = lib.bddc_coarse_csr(op._ctx, None, None, None, None, 0, 0)
+    if nnz < 0:
+        raise RuntimeError("no device-built coarse pattern")
+    m = sum(int(k) * (int(k) + 1) // 2 for k in op.plan.n_con_local)
+    row = np.empty(nnz, np.int64)
+    col = np.empty(nnz, np.int64)
+    seg = np.empty(nnz + 1, np.int64)
+    con = np.empty(max(m, 1), np.int32)
+    P = lambda a: a.ctypes.data_as(C.POINTER(C.c_longlong))  # noqa: E731
+    got = lib.bddc_coarse_csr(op._ctx, P(row), P(col), P(seg), con.ctypes.data_as(C.POINTER(C.c_int)), nnz, m)
+    if got != nnz:
+        raise RuntimeError("bddc_coarse_csr failed")
+    return row, col, seg, con[:m].astype(np.int64)
+
+
 def coarse_matrix(op) -> SparseSym | None:
     """S_0 as the reference stores it: upper triangle in coarse-id order (bddc.py:494-505),
     values from the device's deterministic segmented assembly."""
     cp = op.plan.coarse
     if cp is None:
         return None
-    val = _read(op, "csr_val", 0, len(cp.csr_row))
-    r = cp.perm[cp.csr_row]
-    c = cp.perm[cp.csr_col]
+    row, col = cp.csr_row, cp.csr_col
+    if len(cp.contrib) == 0:  # pattern built on the device (coarse_pattern.cu)
+        row, col, _, _ = device_coarse_pattern(op)
+    val = _read(op, "csr_val", 0, len(row))
+    r = cp.perm[row]
+    c = cp.perm[col]
     return SparseSym.from_upper_triplets(cp.n, np.minimum(r, c), np.maximum(r, c), val)
 
 

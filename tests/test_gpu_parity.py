@@ -237,14 +237,31 @@ def test_aliased_front_memory(cuda_ok, case, monkeypatch):
     op.close()
     monkeypatch.setenv("BDDC_FRONT_ALIAS", "1")
     monkeypatch.setenv("BDDC_FRONT_ALIAS_MIN_MB", "0")
-    if case in ("cfg1_p1_ref", "cfg3a_p1_ref"):  # 2 MB pages (else the adaptive size, 32 MB here)
-        monkeypatch.setenv("BDDC_FRONT_PAGE_MB", "2")
+    if case in ("cfg2a_p1_L4h", "cfg4a_p1_spec"):  # 8 MB pages (else the default 2 MB)
+        monkeypatch.setenv("BDDC_FRONT_PAGE_MB", "8")
     pb, op = _op(g)
     z = op.apply(g["r"])
     assert np.array_equal(z, z0)
     op.refactor()
     op.refactor()
     assert np.array_equal(op.apply(g["r"]), z0)
+    x, rep = P.pcg(op.matvec, op.apply, g["b"], tol=float(g["tol"]), max_iters=2000)
+    assert abs(rep.iterations - int(g["iterations"])) <= 1
+    assert np.linalg.norm(x - g["x"]) <= 1e-10 * np.linalg.norm(g["x"])
+    op.close()
+
+
+@pytest.mark.parametrize("case", ["cfg2a_p1_L4h", "cfg3a_p1_ref", "cfg3c_p1_ref", "cfg4a_p1_spec"])
+def test_coarse_solve_l21_fronts(cuda_ok, case, monkeypatch):
+    """Every coarse front with a separator above 128 solved through L21 in place (two dependent
+    GEMV phases per direction, per-chunk dependencies) instead of W21 = L21 X (coarse.cu): the
+    apply and the PCG result match the reference as with the default split."""
+    g = load_golden(case)
+    monkeypatch.setenv("BDDC_W21_MAX_SEP", "128")
+    pb, op = _op(g)
+    z = op.apply(g["r"])
+    tol = 1e-9 if "cfg4" in case else 1e-12
+    assert np.abs(z - g["Br"]).max() <= tol * np.abs(g["Br"]).max()
     x, rep = P.pcg(op.matvec, op.apply, g["b"], tol=float(g["tol"]), max_iters=2000)
     assert abs(rep.iterations - int(g["iterations"])) <= 1
     assert np.linalg.norm(x - g["x"]) <= 1e-10 * np.linalg.norm(g["x"])

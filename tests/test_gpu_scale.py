@@ -176,3 +176,22 @@ def test_cfg4_reference_mode_iterations_pm1(cuda_ok):
     x, rep = P.pcg(op.matvec, op.apply, g["b"], tol=float(g["tol"]), max_iters=2000)
     op.close()
     assert abs(rep.iterations - int(g["iterations"])) <= 1
+
+
+@pytest.mark.parametrize("case", ["cfg1_p1_ref", "cfg2a_p1_L4h", "cfg2b_p1_Lh44", "cfg3a_p1_ref", "cfg3c_p1_ref",
+                                  "chan_q1_coeff"])
+def test_device_coarse_pattern_matches_host(cuda_ok, case):
+    """The coarse assembly pattern built by the setup on the device (coarse_pattern.cu) equals
+    the host statement (host_plan.cu / symbolic.coarse_csr): rows, columns, segments and the
+    ascending-subdomain contribution order (bddc.py:494-505)."""
+    from paper_2001_07289_b200.layout import build_device_plan
+    from paper_2001_07289_b200.operator_views import device_coarse_pattern
+
+    g = load_golden(case)
+    pb, op = _op(g)
+    assert len(op.plan.coarse.contrib) == 0  # the device built it
+    row, col, seg, con = device_coarse_pattern(op)
+    hp = build_device_plan(pb["pair"], op.constraints, pb["weights"], coarse_pattern="host").coarse
+    assert np.array_equal(row, hp.csr_row) and np.array_equal(col, hp.csr_col)
+    assert np.array_equal(seg, hp.seg_ptr) and np.array_equal(con, hp.contrib)
+    op.close()
