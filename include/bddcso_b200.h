@@ -199,6 +199,31 @@ long long bddc_index_size(const bddc_index* ix, const char* what);
 int bddc_index_copy(const bddc_index* ix, const char* name, void* host, long long count);
 void bddc_index_free(bddc_index* ix);
 
+/* host-only symbolic analysis of the coarse problem (no GPU): the nested-dissection tree over
+   the subdomain lattice, the elimination order, every front's boundary and the extend-add maps
+   (the numpy statement symbolic.analyze is the checker). owners [n * W] -1 padded owner
+   subdomains per coarse dof, sub_coords [nsub * dim], subs [dim], sub_con_ptr / sub_con_ids:
+   subdomain -> coarse ids. Sizes by name ("nnodes", "nbnd", "n"); int64 arrays by name
+   ("perm", "sep_start", "sep_size", "level", "parent", "bnd_ptr", "bnd_idx", "rmap"). */
+typedef struct bddc_nd bddc_nd;
+int bddc_nd_build(long long n, int W, const int* owners, int nsub, int dim, const int* sub_coords, const int* subs,
+                  const long long* sub_con_ptr, const long long* sub_con_ids, bddc_nd** out, char* err, size_t errlen);
+long long bddc_nd_size(const bddc_nd* h, const char* what);
+int bddc_nd_copy(const bddc_nd* h, const char* name, long long* host, long long count);
+void bddc_nd_free(bddc_nd* h);
+
+/* device per-subdomain slot tables of the operator (layout.py; bddc.py:420-490): for every
+   (subdomain, surface slot) the interface position, local constraint, coefficient and weight
+   [nsub * nG_pad], and for every interface dof its owners' slots [n_gamma * 2^dim]; inputs
+   are host arrays (slot coordinates of the local layout, per-free-dof constraint / coefficient
+   / object, object owners and weights, subdomain -> ascending constraint lists). */
+int bddc_layout_tables(int device, int dim, const int* cells, const int* subs, int nG, int nG_pad, int nloc,
+                       const int* slot_coords, const int* slot_of_node, long long n_free, const int* gamma,
+                       int n_gamma, const int* con_of, const double* coef_of, const int* dof_obj, int n_obj,
+                       const int* owners, const double* obj_w, const long long* sub_con_ptr, const int* sub_con,
+                       int* slot_gamma, int* slot_con, double* slot_coef, double* slot_w, int* gamma_slots,
+                       char* err, size_t errlen);
+
 /* dense FP64 batched kernels (column-major, even leading dimensions, device pointers) */
 int bddc_dense_potrf(double* A, int n, int lda, long long stride, int count, int* info_host,
                      void* stream);

@@ -31,6 +31,7 @@ EXPORTS = (
     "bddc_dense_potrf", "bddc_dense_trsm", "bddc_dense_gemm", "bddc_check", "bddc_update_weights",
     "bddc_coarse_solve", "bddc_read_buffer", "bddc_coarse_pattern",
     "bddc_index_build", "bddc_index_size", "bddc_index_copy", "bddc_index_free", "bddc_coarse_csr",
+    "bddc_layout_tables", "bddc_nd_build", "bddc_nd_size", "bddc_nd_copy", "bddc_nd_free",
 )
 
 
@@ -115,6 +116,14 @@ def load(required: bool = True):
     lib.bddc_index_copy.argtypes = [_vp, C.c_char_p, _vp, _ll]
     lib.bddc_index_free.argtypes = [_vp]
     lib.bddc_index_free.restype = None
+    lib.bddc_layout_tables.argtypes = [_i, _i, _pi, _pi, _i, _i, _i, _pi, _pi, _ll, _pi, _i, _pi, _pd, _pi, _i,
+                                       _pi, _pd, _pll, _pi, _pi, _pi, _pd, _pd, _pi, C.c_char_p, C.c_size_t]
+    lib.bddc_nd_build.argtypes = [_ll, _i, _pi, _i, _i, _pi, _pi, _pll, _pll, C.POINTER(_vp), C.c_char_p, C.c_size_t]
+    lib.bddc_nd_size.argtypes = [_vp, C.c_char_p]
+    lib.bddc_nd_size.restype = _ll
+    lib.bddc_nd_copy.argtypes = [_vp, C.c_char_p, _pll, _ll]
+    lib.bddc_nd_free.argtypes = [_vp]
+    lib.bddc_nd_free.restype = None
     lib.bddc_coarse_csr.argtypes = [_vp, _pll, _pll, _pll, _pi, _ll, _ll]
     lib.bddc_coarse_csr.restype = _ll
     lib.bddc_launch_count.argtypes = []

@@ -414,10 +414,11 @@ def build_bddc(system: AssembledSystem, pair: PartitionPair, objects: ObjectTabl
             "any refinement Θ̂ (refine_uniform, refine_by_coefficient) is supported on top of it")
     t0 = time.perf_counter()
     constraints = select_constraints(objects, recipe, pair)
-    # the coarse assembly pattern is built by the setup on the device (coarse_pattern.cu);
-    # BDDC_HOST_PATTERN=1 passes the host statement's arrays instead
-    plan = build_device_plan(pair, constraints, weights,
-                             coarse_pattern="host" if os.environ.get("BDDC_HOST_PATTERN") == "1" else "device")
+    # the slot tables come from the device kernels (index_sets.cu) and the coarse assembly
+    # pattern is built by the setup on the device (coarse_pattern.cu);
+    host = os.environ.get("BDDC_HOST_PLAN") == "1"  # the numpy / host statements (checkers)
+    plan = build_device_plan(pair, constraints, weights, coarse_pattern="host" if host else "device",
+                             device=None if host else device)
     prep = time.perf_counter() - t0
     op = BddcOperator(system, pair, weights, recipe, constraints, plan, coarse_scaling, device, comm)
     op.times.prep_s = prep

@@ -293,6 +293,7 @@ inline bool t_lower_only(const Geometry& G) { return G.nG_pad > 256 && G.nG_pad 
 struct Ctx;
 struct FrontVmm;
 void front_vmm_release(Ctx& c);
+void front_vmm_wait(Ctx& c);  // join the background mapping of the aliased fronts (rethrows)
 bool front_alias_layout(Ctx& c);
 void front_memset(Ctx& c, cudaStream_t s);
 

@@ -18,6 +18,8 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <exception>
+#include <thread>
 
 #include "bddc_internal.cuh"
 
@@ -70,11 +72,27 @@ struct FrontVmm {
   size_t va_bytes = 0, p_bytes = 0, u_bytes = 0;
   std::vector<CUmemGenericAllocationHandle> handles;  // each mapped whole (cuMemMap offset 0)
   std::vector<std::pair<size_t, size_t>> maps;  // (va, bytes) mapped ranges to unmap
+  // the driver calls that back the reserved ranges (create / map / access: seconds at cfg5)
+  // run on this thread while the setup builds its schedules; front_vmm_wait joins it
+  std::thread worker;
+  std::exception_ptr error;
 };
+
+void front_vmm_wait(Ctx& c) {
+  FrontVmm* v = c.vmm;
+  if (!v || !v->worker.joinable()) return;
+  v->worker.join();
+  if (v->error) {
+    std::exception_ptr e = v->error;
+    v->error = nullptr;
+    std::rethrow_exception(e);
+  }
+}
 
 void front_vmm_release(Ctx& c) {
   FrontVmm* v = c.vmm;
   if (!v) return;
+  if (v->worker.joinable()) v->worker.join();
   const Drv& d = drv();
   cudaDeviceSynchronize();
   for (auto& m : v->maps) d.unmap((CUdeviceptr)m.first, m.second);
@@ -214,86 +232,97 @@ bool front_alias_layout(Ctx& c) {
   cu_check(d.reserve(&vm->va, vm->va_bytes, PB, 0, 0), "reserve");
   cu_check(d.reserve(&vm->pview, vm->p_bytes, PB, 0, 0), "reserve");
   cu_check(d.reserve(&vm->uview, vm->u_bytes, PB, 0, 0), "reserve");
-  auto create = [&](size_t bytes) {
-    CUmemGenericAllocationHandle h;
-    cu_check(d.create(&h, bytes, &prop, 0), "cuMemCreate");
-    vm->handles.push_back(h);
-    return h;
-  };
-  auto map = [&](CUdeviceptr va, size_t bytes, CUmemGenericAllocationHandle h) {
-    cu_check(d.map(va, bytes, 0, h, 0), "cuMemMap");
-    vm->maps.push_back({(size_t)va, bytes});
-  };
-  // persistent runs: one allocation each, mapped in place and into the persistent view
-  long long pnext = 0;
-  for (long long p = 0; p < vpages;) {
-    long long q = p;
-    while (q < vpages && aliased[q] == aliased[p]) ++q;
-    if (!aliased[p]) {
-      const size_t bytes = (size_t)(q - p) * PB;
-      const CUmemGenericAllocationHandle h = create(bytes);
-      map(vm->va + (size_t)p * PB, bytes, h);
-      map(vm->pview + (size_t)pnext * PB, bytes, h);
-      pnext += q - p;
-    }
-    p = q;
-  }
-  ht.mark("alias: persistent runs");
-  // pool: consecutive pages used by exactly the same update blocks at consecutive virtual
-  // pages form one allocation (every mapping costs a driver call: ~3.5x fewer at cfg5),
-  // mapped into the pool view and under each of those update blocks
-  std::vector<std::vector<std::pair<int, long long>>> users(upages);  // (front, virtual page)
-  for (int i = 0; i < N; ++i) {
-    long long vp = upage[i];
-    for (auto& r : urun[i])
-      for (long long k = 0; k < r.second; ++k, ++vp) users[base[i] + r.first + k].push_back({i, vp});
-  }
-  long long nruns = 0, nmaps = 0;
-  for (long long p0 = 0; p0 < upages;) {
-    long long p1 = p0 + 1;
-    auto same = [&](long long q) {
-      if (users[q].size() != users[p0].size()) return false;
-      for (size_t j = 0; j < users[q].size(); ++j)
-        if (users[q][j].first != users[p0][j].first || users[q][j].second != users[p0][j].second + (q - p0))
-          return false;
-      return true;
-    };
-    while (p1 < upages && same(p1)) ++p1;
-    const size_t bytes = (size_t)(p1 - p0) * PB;
-    const CUmemGenericAllocationHandle h = create(bytes);
-    map(vm->uview + (size_t)p0 * PB, bytes, h);
-    for (auto& us : users[p0]) map(vm->va + (size_t)us.second * PB, bytes, h);
-    ++nruns;
-    nmaps += 1 + (long long)users[p0].size();
-    p0 = p1;
-  }
-  ht.mark("alias: pool runs + update-block maps");
-  if (ht.on) {
-    long long nal = 0;
-    for (int i = 0; i < N; ++i) nal += u[i] > 0;
-    fprintf(stderr, "bddc_setup host: alias: page %lld MB, %lld virtual / %lld persistent / %lld pool pages, "
-            "%lld aliased fronts, %lld pool runs, %lld pool mappings, %zu allocations\n", PG * 8 >> 20, vpages,
-            ppages, upages, nal, nruns, nmaps, vm->handles.size());
-  }
-  CUmemAccessDesc acc{};
-  acc.location = prop.location;
-  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-  cu_check(d.access(vm->va, vm->va_bytes, &acc, 1), "cuMemSetAccess");
-  cu_check(d.access(vm->pview, vm->p_bytes, &acc, 1), "cuMemSetAccess");
-  cu_check(d.access(vm->uview, vm->u_bytes, &acc, 1), "cuMemSetAccess");
-  ht.mark("alias: access");
   fp.front_pool = vpages * PG;
   fp.alias = true;
   fp.alias_resident_bytes = (long long)(vm->p_bytes + vm->u_bytes);
   fp.ualias.assign(N, 0);
   for (int i = 0; i < N; ++i) fp.ualias[i] = u[i] > 0;
   fp.d.fronts = (double*)vm->va;
+  const int dev = c.device;
+  long long nal = 0;
+  for (int i = 0; i < N; ++i) nal += u[i] > 0;
+  vm->worker = std::thread([vm, d, prop, PB, PG, vpages, ppages, upages, N, nal, dev, aliased = std::move(aliased),
+                            upage = std::move(upage), urun = std::move(urun), base = std::move(base)]() {
+    try {
+      BDDC_CUDA(cudaSetDevice(dev));
+      HostTimer ht;
+      auto create = [&](size_t bytes) {
+        CUmemGenericAllocationHandle h;
+        cu_check(d.create(&h, bytes, &prop, 0), "cuMemCreate");
+        vm->handles.push_back(h);
+        return h;
+      };
+      auto map = [&](CUdeviceptr va, size_t bytes, CUmemGenericAllocationHandle h) {
+        cu_check(d.map(va, bytes, 0, h, 0), "cuMemMap");
+        vm->maps.push_back({(size_t)va, bytes});
+      };
+      // persistent runs: one allocation each, mapped in place and into the persistent view
+      long long pnext = 0;
+      for (long long p = 0; p < vpages;) {
+        long long q = p;
+        while (q < vpages && aliased[q] == aliased[p]) ++q;
+        if (!aliased[p]) {
+          const size_t bytes = (size_t)(q - p) * PB;
+          const CUmemGenericAllocationHandle h = create(bytes);
+          map(vm->va + (size_t)p * PB, bytes, h);
+          map(vm->pview + (size_t)pnext * PB, bytes, h);
+          pnext += q - p;
+        }
+        p = q;
+      }
+      ht.mark("alias: persistent runs");
+      // pool: consecutive pages used by exactly the same update blocks at consecutive virtual
+      // pages form one allocation (every mapping costs a driver call: ~3.5x fewer at cfg5),
+      // mapped into the pool view and under each of those update blocks
+      std::vector<std::vector<std::pair<int, long long>>> users(upages);  // (front, virtual page)
+      for (int i = 0; i < N; ++i) {
+        long long vp = upage[i];
+        for (auto& r : urun[i])
+          for (long long k = 0; k < r.second; ++k, ++vp) users[base[i] + r.first + k].push_back({i, vp});
+      }
+      long long nruns = 0, nmaps = 0;
+      for (long long p0 = 0; p0 < upages;) {
+        long long p1 = p0 + 1;
+        auto same = [&](long long q) {
+          if (users[q].size() != users[p0].size()) return false;
+          for (size_t j = 0; j < users[q].size(); ++j)
+            if (users[q][j].first != users[p0][j].first || users[q][j].second != users[p0][j].second + (q - p0))
+              return false;
+          return true;
+        };
+        while (p1 < upages && same(p1)) ++p1;
+        const size_t bytes = (size_t)(p1 - p0) * PB;
+        const CUmemGenericAllocationHandle h = create(bytes);
+        map(vm->uview + (size_t)p0 * PB, bytes, h);
+        for (auto& us : users[p0]) map(vm->va + (size_t)us.second * PB, bytes, h);
+        ++nruns;
+        nmaps += 1 + (long long)users[p0].size();
+        p0 = p1;
+      }
+      ht.mark("alias: pool runs + update-block maps");
+      if (ht.on) {
+        fprintf(stderr, "bddc_setup host: alias: page %lld MB, %lld virtual / %lld persistent / %lld pool pages, "
+                "%lld aliased fronts, %lld pool runs, %lld pool mappings, %zu allocations\n", PG * 8 >> 20, vpages,
+                ppages, upages, nal, nruns, nmaps, vm->handles.size());
+      }
+      CUmemAccessDesc acc{};
+      acc.location = prop.location;
+      acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+      cu_check(d.access(vm->va, vm->va_bytes, &acc, 1), "cuMemSetAccess");
+      cu_check(d.access(vm->pview, vm->p_bytes, &acc, 1), "cuMemSetAccess");
+      cu_check(d.access(vm->uview, vm->u_bytes, &acc, 1), "cuMemSetAccess");
+      ht.mark("alias: access");
+    } catch (...) {
+      vm->error = std::current_exception();
+    }
+  });
   return true;
 }
 
 // Zero every front (setup start): the persistent pages and the pool, each through its own
 // contiguous view (the aliased virtual range would zero shared pages many times over).
 void front_memset(Ctx& c, cudaStream_t s) {
+  front_vmm_wait(c);  // the fronts' physical pages are mapped
   if (!c.vmm) {
     BDDC_CUDA(cudaMemsetAsync(c.fp.d.fronts, 0, sizeof(double) * c.fp.front_pool, s));
     return;

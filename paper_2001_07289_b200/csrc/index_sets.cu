@@ -20,6 +20,7 @@
 #include <cub/cub.cuh>
 
 #include <cstring>
+#include <type_traits>
 #include <string>
 #include <vector>
 
@@ -375,7 +376,186 @@ static void run_index(IndexResult& R, int device, int dim, const int* cells, con
   R.obj_ptr[nobj] = ng;
 }
 
+// ---- per-subdomain slot tables of the device operator (layout.py, bddc.py:420-490) ----
+namespace {
+
+struct LayGeom {
+  int dim, nsub, nG, nG_pad, W, nloc;
+  int subs[3], blk[3], cells[3], nf[3];
+};
+
+// one thread per (subdomain p, surface slot j): global free dof, interface position, local
+// constraint (binary search in p's ascending constraint list), coefficient, weight
+__global__ void slot_kernel(LayGeom g, const int* __restrict__ slot_coords, const int* __restrict__ gidx,
+                            const int* __restrict__ con_of, const double* __restrict__ coef_of,
+                            const int* __restrict__ dof_obj, const int* __restrict__ owners,
+                            const double* __restrict__ obj_w, const long long* __restrict__ sub_con_ptr,
+                            const int* __restrict__ sub_con, int* slot_gamma, int* slot_con, double* slot_coef,
+                            double* slot_w) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)g.nsub * g.nG_pad) return;
+  const int p = (int)(idx / g.nG_pad), j = (int)(idx % g.nG_pad);
+  int sg = -1, sc = -1;
+  double co = 0.0, w = 0.0;
+  if (j < g.nG) {
+    int rem = p;
+    long long fid = 0, st = 1;
+    bool dir = false;
+    for (int d = 0; d < g.dim; ++d) {
+      const int pc = rem % g.subs[d];
+      rem /= g.subs[d];
+      const int gc = pc * g.blk[d] + slot_coords[j * g.dim + d];
+      dir |= gc == 0 || gc == g.cells[d];
+      fid += (long long)(gc - 1) * st;
+      st *= g.nf[d];
+    }
+    if (!dir) {
+      sg = gidx[fid];
+      const int cn = con_of[fid];
+      if (cn >= 0) {
+        long long lo = sub_con_ptr[p], hi = sub_con_ptr[p + 1];
+        const long long a0 = lo;
+        while (lo < hi) {
+          const long long mid = (lo + hi) >> 1;
+          if (sub_con[mid] < cn) lo = mid + 1; else hi = mid;
+        }
+        sc = (int)(lo - a0);
+        co = coef_of[fid];
+      }
+      const int o = dof_obj[fid];
+      for (int k = 0; k < g.W; ++k)
+        if (owners[(long long)o * g.W + k] == p) w += obj_w[(long long)o * g.W + k];
+    }
+  }
+  slot_gamma[idx] = sg;
+  slot_con[idx] = sc;
+  slot_coef[idx] = co;
+  slot_w[idx] = w;
+}
+
+__global__ void gidx_kernel(int n, const int* __restrict__ gam, int* gidx) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) gidx[gam[i]] = i;
+}
+
+// one thread per (interface dof, owner k): the owner's slot of the dof, -1 padded
+__global__ void gamma_slot_kernel(LayGeom g, int n_gamma, const int* __restrict__ gamma, const int* __restrict__ dof_obj,
+                                  const int* __restrict__ owners, const int* __restrict__ slot_of_node, int* out) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)n_gamma * g.W) return;
+  const int gi = (int)(idx / g.W), k = (int)(idx % g.W);
+  const int dof = gamma[gi];
+  const int p = owners[(long long)dof_obj[dof] * g.W + k];
+  int v = -1;
+  if (p >= 0) {
+    int rem = dof, prem = p;
+    long long ln = 0, st = 1;
+    for (int d = 0; d < g.dim; ++d) {
+      const int gc = rem % g.nf[d] + 1;
+      rem /= g.nf[d];
+      const int pc = prem % g.subs[d];
+      prem /= g.subs[d];
+      ln += (long long)(gc - pc * g.blk[d]) * st;
+      st *= g.blk[d] + 1;
+    }
+    const int sl = (ln >= 0 && ln < g.nloc) ? slot_of_node[ln] : -1;
+    v = sl >= 0 ? p * g.nG_pad + sl : -2;  // -2: the dof is not a surface slot of its owner
+  }
+  out[idx] = v;
+}
+
+}  // namespace
 }  // namespace bddc
+
+extern "C" int bddc_layout_tables(int device, int dim, const int* cells, const int* subs, int nG, int nG_pad, int nloc,
+                                  const int* slot_coords, const int* slot_of_node, long long n_free,
+                                  const int* gamma, int n_gamma, const int* con_of, const double* coef_of,
+                                  const int* dof_obj, int n_obj, const int* owners, const double* obj_w,
+                                  const long long* sub_con_ptr, const int* sub_con, int* slot_gamma, int* slot_con,
+                                  double* slot_coef, double* slot_w, int* gamma_slots, char* err, size_t errlen) {
+  using namespace bddc;
+  try {
+    BDDC_CUDA(cudaSetDevice(device));
+    LayGeom g{};
+    g.dim = dim;
+    g.W = 1 << dim;
+    g.nG = nG;
+    g.nG_pad = nG_pad;
+    g.nloc = nloc;
+    g.nsub = 1;
+    for (int d = 0; d < dim; ++d) {
+      g.subs[d] = subs[d];
+      g.cells[d] = cells[d];
+      g.blk[d] = cells[d] / subs[d];
+      g.nf[d] = cells[d] - 1;
+      g.nsub *= subs[d];
+    }
+    cudaStream_t st;
+    BDDC_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct SG {
+      cudaStream_t s;
+      ~SG() { cudaStreamDestroy(s); }
+    } sgd{st};
+    DevBuf B;
+    auto up = [&](const auto* h, long long n) {
+      using T = std::remove_cv_t<std::remove_pointer_t<decltype(h)>>;
+      T* d = B.get<T>(n);
+      if (n) BDDC_CUDA(cudaMemcpyAsync(d, h, sizeof(T) * n, cudaMemcpyHostToDevice, st));
+      return d;
+    };
+    const long long nslots = (long long)g.nsub * nG_pad;
+    const long long ncon_pairs = sub_con_ptr[g.nsub];
+    int* d_sc = up(slot_coords, (long long)nG * dim);
+    int* d_son = up(slot_of_node, nloc);
+    int* d_gamma = up(gamma, n_gamma);
+    int* d_con = up(con_of, n_free);
+    double* d_coef = up(coef_of, n_free);
+    int* d_dobj = up(dof_obj, n_free);
+    int* d_own = up(owners, (long long)n_obj * g.W);
+    double* d_w = up(obj_w, (long long)n_obj * g.W);
+    long long* d_ptr = up(sub_con_ptr, g.nsub + 1);
+    int* d_scon = up(sub_con, ncon_pairs);
+    // interface position of every free dof
+    int* d_gidx = B.get<int>(n_free);
+    BDDC_CUDA(cudaMemsetAsync(d_gidx, 0xff, sizeof(int) * n_free, st));
+    if (n_gamma) {  // gidx[gamma[i]] = i
+      gidx_kernel<<<grid_of(n_gamma), 256, 0, st>>>(n_gamma, d_gamma, d_gidx);
+      BDDC_LAUNCH_CHECK();
+      BDDC_COUNT();
+    }
+    int* o_sg = B.get<int>(nslots);
+    int* o_sc = B.get<int>(nslots);
+    double* o_co = B.get<double>(nslots);
+    double* o_w = B.get<double>(nslots);
+    int* o_gs = B.get<int>((long long)n_gamma * g.W);
+    slot_kernel<<<grid_of(nslots), 256, 0, st>>>(g, d_sc, d_gidx, d_con, d_coef, d_dobj, d_own, d_w, d_ptr, d_scon,
+                                                 o_sg, o_sc, o_co, o_w);
+    BDDC_LAUNCH_CHECK();
+    BDDC_COUNT();
+    if (n_gamma) {
+      gamma_slot_kernel<<<grid_of((long long)n_gamma * g.W), 256, 0, st>>>(g, n_gamma, d_gamma, d_dobj, d_own, d_son,
+                                                                          o_gs);
+      BDDC_LAUNCH_CHECK();
+      BDDC_COUNT();
+    }
+    BDDC_CUDA(cudaMemcpyAsync(slot_gamma, o_sg, sizeof(int) * nslots, cudaMemcpyDeviceToHost, st));
+    BDDC_CUDA(cudaMemcpyAsync(slot_con, o_sc, sizeof(int) * nslots, cudaMemcpyDeviceToHost, st));
+    BDDC_CUDA(cudaMemcpyAsync(slot_coef, o_co, sizeof(double) * nslots, cudaMemcpyDeviceToHost, st));
+    BDDC_CUDA(cudaMemcpyAsync(slot_w, o_w, sizeof(double) * nslots, cudaMemcpyDeviceToHost, st));
+    if (n_gamma)
+      BDDC_CUDA(cudaMemcpyAsync(gamma_slots, o_gs, sizeof(int) * n_gamma * g.W, cudaMemcpyDeviceToHost, st));
+    BDDC_CUDA(cudaStreamSynchronize(st));
+  } catch (const std::exception& e) {
+    if (err && errlen) {
+      const std::string m = e.what();
+      const size_t n = std::min(errlen - 1, m.size());
+      memcpy(err, m.data(), n);
+      err[n] = 0;
+    }
+    return 6;
+  }
+  return 0;
+}
 
 struct bddc_index {
   bddc::IndexResult r;

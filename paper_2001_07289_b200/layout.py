@@ -25,6 +25,8 @@ from .weights import ConstraintTable, WeightingOperator
 # coarse CSR pattern: the native statement (csrc/host_plan.cu); symbolic.coarse_csr is the
 # numpy statement it is checked against (tests/test_host_plan.py)
 COARSE_CSR = symbolic.coarse_csr_native
+# ND analysis: the native statement (host_plan.cu); symbolic.analyze is its numpy checker
+ANALYZE = symbolic.analyze_native
 
 
 def _round(x: int, m: int) -> int:
@@ -99,10 +101,13 @@ class DevicePlan:
 
 
 def build_device_plan(pair: PartitionPair, cons: ConstraintTable,
-                      weights: WeightingOperator, coarse_pattern: str = "host") -> DevicePlan:
+                      weights: WeightingOperator, coarse_pattern: str = "host",
+                      device: int | None = None) -> DevicePlan:
     """``coarse_pattern``: "host" computes the coarse assembly pattern here (symbolic.py /
     host_plan.cu); "device" leaves it to the setup, which builds it on the GPU from
-    ``con_coarse`` (coarse_pattern.cu)."""
+    ``con_coarse`` (coarse_pattern.cu). ``device`` (CUDA ordinal): the per-subdomain slot
+    tables and the interface gather table come from the device kernels (index_sets.cu,
+    bddc_layout_tables), bit-identical to the numpy statement below."""
     mesh = pair.mesh
     layout_info = pair.box_layout
     if layout_info is None:
@@ -127,18 +132,19 @@ def build_device_plan(pair: PartitionPair, cons: ConstraintTable,
         pc[:, d] = rem % subs[d]
         rem //= subs[d]
 
-    # global free dof of every (sub, slot)
-    gcoords = pc[:, None, :] * np.asarray(blk)[None, None, :] + lay.slot_coords[None, :, :]
     cells = np.asarray(mesh.cells_per_dim)
-    dirichlet = np.any((gcoords == 0) | (gcoords == cells), axis=2)
     nf = cells - 1
-    fid = np.zeros(gcoords.shape[:2], dtype=np.int64)
-    st = 1
-    for d in range(dim):
-        fid += (gcoords[:, :, d] - 1) * st
-        st *= int(nf[d])
-    fid[dirichlet] = -1
     nG, nG_pad = lay.nG, lay.nG_pad
+    if device is None:
+        # global free dof of every (sub, slot)
+        gcoords = pc[:, None, :] * np.asarray(blk)[None, None, :] + lay.slot_coords[None, :, :]
+        dirichlet = np.any((gcoords == 0) | (gcoords == cells), axis=2)
+        fid = np.zeros(gcoords.shape[:2], dtype=np.int64)
+        st = 1
+        for d in range(dim):
+            fid += (gcoords[:, :, d] - 1) * st
+            st *= int(nf[d])
+        fid[dirichlet] = -1
 
     # constraint of each free dof
     n_con = len(cons)
@@ -167,36 +173,43 @@ def build_device_plan(pair: PartitionPair, cons: ConstraintTable,
         pos = np.searchsorted(pair_key, key)
         return local_k[pos]
 
-    valid = fid >= 0
-    slot_gamma = -np.ones((nsub, nG_pad), dtype=np.int32)
-    slot_w = np.zeros((nsub, nG_pad))
-    slot_con = -np.ones((nsub, nG_pad), dtype=np.int32)
-    slot_coef = np.zeros((nsub, nG_pad))
-    sub_idx = np.broadcast_to(pid[:, None], fid.shape)
-    fv = fid[valid]
-    sv = sub_idx[valid]
-    sg = slot_gamma[:, :nG]
-    sg[valid] = gidx[fv]
-    if np.any(gidx[fv] < 0):
-        raise AssertionError("a free surface node is not on the interface")
-    slot_gamma[:, :nG] = sg
-    cv = con_of[fv]
-    has = cv >= 0
-    sc = slot_con[:, :nG]
-    tmp = -np.ones(len(fv), dtype=np.int64)
-    tmp[has] = lookup_k(sv[has], cv[has])
-    sc[valid] = tmp
-    slot_con[:, :nG] = sc
-    sco = slot_coef[:, :nG]
-    sco[valid] = np.where(has, coef_of[fv], 0.0)
-    slot_coef[:, :nG] = sco
+    if device is not None:
+        dev_tables = _device_slot_tables(device, pair, lay, subs, nsub, nG_pad, gamma, con_of, coef_of,
+                                         objects, weights, sub_con_ptr, pair_con)
+    if device is None:
+        valid = fid >= 0
+        slot_gamma = -np.ones((nsub, nG_pad), dtype=np.int32)
+    if device is None:
+        slot_w = np.zeros((nsub, nG_pad))
+        slot_con = -np.ones((nsub, nG_pad), dtype=np.int32)
+        slot_coef = np.zeros((nsub, nG_pad))
+        sub_idx = np.broadcast_to(pid[:, None], fid.shape)
+        fv = fid[valid]
+        sv = sub_idx[valid]
+        sg = slot_gamma[:, :nG]
+        sg[valid] = gidx[fv]
+        if np.any(gidx[fv] < 0):
+            raise AssertionError("a free surface node is not on the interface")
+        slot_gamma[:, :nG] = sg
+        cv = con_of[fv]
+        has = cv >= 0
+        sc = slot_con[:, :nG]
+        tmp = -np.ones(len(fv), dtype=np.int64)
+        tmp[has] = lookup_k(sv[has], cv[has])
+        sc[valid] = tmp
+        slot_con[:, :nG] = sc
+        sco = slot_coef[:, :nG]
+        sco[valid] = np.where(has, coef_of[fv], 0.0)
+        slot_coef[:, :nG] = sco
+    else:
+        slot_gamma, slot_con, slot_coef, slot_w, gamma_slots_dev = dev_tables
 
     # coarse plan (elimination order) and the constraint maps
     plan = None
     con_coarse = -np.ones((nsub, nc_pad), dtype=np.int32)
     coarse_slots = -np.ones((max(n_con, 0), W), dtype=np.int32)
     if n_con:
-        plan = symbolic.analyze(n_con, con_owners, pc, tuple(subs), sub_con_ptr=sub_con_ptr,
+        plan = ANALYZE(n_con, con_owners, pc, tuple(subs), sub_con_ptr=sub_con_ptr,
                                 sub_con_ids=pair_con)
         if coarse_pattern == "host":
             COARSE_CSR(plan, sub_con_ptr, pair_con, nc_pad)
@@ -208,6 +221,10 @@ def build_device_plan(pair: PartitionPair, cons: ConstraintTable,
         coarse_slots = slots[plan.perm].astype(np.int32)
 
     # interface gather: owner slots of each gamma dof, ascending subdomain
+    if device is not None:
+        dp = DevicePlan(lay, nsub, nc_pad, slot_gamma, slot_w, slot_con, slot_coef, con_coarse,
+                        gamma.astype(np.int64), gamma_slots_dev, coarse_slots, plan, n_local)
+        return dp
     gobj = objects.dof_obj[gamma]
     gown = objects.owners[gobj]  # (n_gamma, W) ascending, −1 padded
     gv = gown >= 0
@@ -245,3 +262,45 @@ def slot_weights(plan: DevicePlan, weights: WeightingOperator) -> np.ndarray:
     out = np.zeros(sg.shape)
     out[valid] = weights.weights_for(sub, plan.gamma_dof[sg[valid]])
     return out
+
+
+def _device_slot_tables(device, pair, lay, subs, nsub, nG_pad, gamma, con_of, coef_of, objects, weights,
+                        sub_con_ptr, pair_con):
+    """slot_gamma / slot_con / slot_coef / slot_w [nsub, nG_pad] and gamma_slots [n_gamma, 2^d]
+    from the device kernels (bddc_layout_tables)."""
+    import ctypes as C
+
+    from . import _capi
+
+    lib = _capi.load()
+    mesh = pair.mesh
+    dim = mesh.dim
+    W = 2**dim
+    i32 = lambda a: np.ascontiguousarray(a, dtype=np.int32)  # noqa: E731
+    f64 = lambda a: np.ascontiguousarray(a, dtype=np.float64)  # noqa: E731
+    cells = i32(list(mesh.cells_per_dim) + [1] * (3 - dim))
+    subs3 = i32(list(subs) + [1] * (3 - dim))
+    slot_of_node = np.full(lay.nloc_nodes, -1, dtype=np.int32)
+    slot_of_node[lay.slot_node] = np.arange(lay.nG, dtype=np.int32)
+    args = dict(sc=i32(lay.slot_coords), son=slot_of_node, gamma=i32(gamma), con=i32(con_of), coef=f64(coef_of),
+                dobj=i32(objects.dof_obj), own=i32(objects.owners), w=f64(weights.obj_weights),
+                ptr=np.ascontiguousarray(sub_con_ptr, dtype=np.int64), scon=i32(pair_con))
+    out_sg = np.empty((nsub, nG_pad), np.int32)
+    out_sc = np.empty((nsub, nG_pad), np.int32)
+    out_co = np.empty((nsub, nG_pad), np.float64)
+    out_w = np.empty((nsub, nG_pad), np.float64)
+    out_gs = np.empty((len(gamma), W), np.int32)
+    pi, pd, pll = C.c_int, C.c_double, C.c_longlong
+    P = _capi.ptr
+    err = C.create_string_buffer(512)
+    rc = lib.bddc_layout_tables(int(device), dim, P(cells, pi), P(subs3, pi), lay.nG, nG_pad, lay.nloc_nodes,
+                                P(args["sc"], pi), P(args["son"], pi), mesh.free_count, P(args["gamma"], pi),
+                                len(gamma), P(args["con"], pi), P(args["coef"], pd), P(args["dobj"], pi),
+                                len(objects), P(args["own"], pi), P(args["w"], pd), P(args["ptr"], pll),
+                                P(args["scon"], pi), P(out_sg, pi), P(out_sc, pi), P(out_co, pd), P(out_w, pd),
+                                P(out_gs, pi), err, len(err))
+    if rc:
+        raise RuntimeError("device layout tables: " + err.value.decode(errors="replace"))
+    if np.any(out_gs == -2):
+        raise AssertionError("interface dof does not map to a surface slot")
+    return out_sg, out_sc, out_co, out_w, out_gs

@@ -23,6 +23,7 @@ from __future__ import annotations
 import itertools
 import math
 from dataclasses import dataclass, field
+from functools import cached_property
 from typing import Sequence
 
 import numpy as np
@@ -35,16 +36,17 @@ _SQRT3 = math.sqrt(3.0)
 
 @dataclass(frozen=True)
 class StructuredMesh:
-    """Tensor-product grid of the unit box (mesh.py:20-49)."""
+    """Tensor-product grid of the unit box (mesh.py:20-49).
+
+    ``cell_nodes`` (corner c has bit d <-> +1 on axis d), ``node_coords`` and
+    ``boundary_mask`` are the reference's fields; they are built on first access (the device
+    path never needs them; at cfg5 they are 1.2 GB of int64)."""
 
     dim: int
     cells_per_dim: tuple
     node_count: int
     cell_count: int
-    cell_nodes: np.ndarray  # (cell_count, 2**dim), corner c has bit d <-> +1 on axis d
-    node_coords: np.ndarray  # (node_count, dim)
     spacings: tuple
-    boundary_mask: np.ndarray
     free_nodes: np.ndarray
     node_to_free: np.ndarray
     element: str = "q1"
@@ -57,16 +59,47 @@ class StructuredMesh:
     def nodes_per_dim(self) -> tuple:
         return tuple(c + 1 for c in self.cells_per_dim)
 
+    def _grid(self, sizes):
+        """(prod(sizes), dim) x-fastest multi-indices."""
+        axes = np.meshgrid(*[np.arange(n, dtype=np.int64) for n in reversed(sizes)], indexing="ij")
+        return np.stack([a.ravel() for a in reversed(axes)], axis=1)
+
+    @cached_property
+    def node_coords(self) -> np.ndarray:
+        return self._grid(self.nodes_per_dim) * np.asarray(self.spacings)
+
+    @cached_property
+    def boundary_mask(self) -> np.ndarray:
+        mask = np.ones(self.node_count, dtype=bool)
+        mask[self.free_nodes] = False
+        return mask
+
+    @cached_property
+    def cell_nodes(self) -> np.ndarray:
+        npd = self.nodes_per_dim
+        strides = np.cumprod((1,) + npd[:-1]).astype(np.int64)
+        base = _axis_sum([np.arange(c, dtype=np.int64) * strides[d] for d, c in enumerate(self.cells_per_dim)])
+        corners = np.array([sum(((c >> d) & 1) * int(strides[d]) for d in range(self.dim))
+                            for c in range(2**self.dim)], dtype=np.int64)
+        return base[:, None] + corners[None, :]
+
+    @cached_property
+    def _cell_multi(self) -> np.ndarray:
+        return self._grid(self.cells_per_dim)
+
     def cell_multi_indices(self) -> np.ndarray:
-        ids = np.arange(self.cell_count)
-        out = np.empty((self.cell_count, self.dim), dtype=np.int64)
-        for d in range(self.dim):
-            out[:, d] = ids % self.cells_per_dim[d]
-            ids = ids // self.cells_per_dim[d]
-        return out
+        return self._cell_multi
 
     def cells_grid(self, values: np.ndarray) -> np.ndarray:
         return np.asarray(values).reshape(tuple(reversed(self.cells_per_dim)))
+
+
+def _axis_sum(parts) -> np.ndarray:
+    """x-fastest flattened outer sum: out[i0 + n0*(i1 + n1*i2)] = parts[0][i0] + parts[1][i1] + ..."""
+    out = parts[-1]
+    for p in reversed(parts[:-1]):
+        out = (out[:, None] + p[None, :]).ravel()
+    return out
 
 
 @dataclass(frozen=True)
@@ -125,30 +158,12 @@ def build_mesh(dim: int, cells_per_dim: Sequence[int], element: str = "q1") -> S
     node_count = int(np.prod(npd))
     cell_count = int(np.prod(cells))
     spacings = tuple(1.0 / c for c in cells)
-
-    # per-axis node grids broadcast into x-fastest order
-    axes = np.meshgrid(*[np.arange(n, dtype=np.int64) for n in reversed(npd)], indexing="ij")
-    grid = np.stack([a.ravel() for a in reversed(axes)], axis=1)
-    node_coords = grid * np.asarray(spacings)
-    boundary_mask = np.zeros(node_count, dtype=bool)
-    for d in range(dim):
-        boundary_mask |= (grid[:, d] == 0) | (grid[:, d] == cells[d])
-    free_nodes = np.flatnonzero(~boundary_mask)
+    # free nodes: interior grid points in increasing node id (mesh.py:97-102), as an outer sum
+    strides = np.cumprod((1,) + npd[:-1]).astype(np.int64)
+    free_nodes = _axis_sum([np.arange(1, c, dtype=np.int64) * strides[d] for d, c in enumerate(cells)])
     node_to_free = np.full(node_count, -1, dtype=np.int64)
     node_to_free[free_nodes] = np.arange(len(free_nodes))
-
-    strides = np.cumprod((1,) + npd[:-1]).astype(np.int64)
-    caxes = np.meshgrid(*[np.arange(c, dtype=np.int64) for c in reversed(cells)], indexing="ij")
-    base = np.zeros(cell_count, dtype=np.int64)
-    for d, a in enumerate(reversed(caxes)):
-        base += a.ravel() * strides[d]
-    corners = np.array(
-        [sum(((c >> d) & 1) * int(strides[d]) for d in range(dim)) for c in range(2**dim)],
-        dtype=np.int64,
-    )
-    cell_nodes = base[:, None] + corners[None, :]
-    return StructuredMesh(dim, cells, node_count, cell_count, cell_nodes, node_coords,
-                          spacings, boundary_mask, free_nodes, node_to_free, element)
+    return StructuredMesh(dim, cells, node_count, cell_count, spacings, free_nodes, node_to_free, element)
 
 
 def q1_element_box(lengths: Sequence[float]) -> np.ndarray:
@@ -259,9 +274,9 @@ def load_vector(mesh: StructuredMesh, f) -> np.ndarray:
     """
     vol = float(np.prod(mesh.spacings))
     if np.ndim(f) == 0:
-        counts = np.bincount(mesh.cell_nodes.ravel(), minlength=mesh.node_count)
-        load = float(f) * vol / (2**mesh.dim) * counts
-        return load[mesh.free_nodes]
+        # every free node lies in exactly 2^d cells: the same value as the reference's sum
+        # f·vol/2^d · count (count = 2^d), without the cell -> node incidence
+        return np.full(mesh.free_count, float(f) * vol / (2**mesh.dim) * (2**mesh.dim))
     f = np.asarray(f, dtype=float)
     if f.shape != (mesh.free_count,):
         raise ValueError(f"per-dof source has shape {f.shape}, expected ({mesh.free_count},)")

@@ -29,7 +29,7 @@ import numpy as np
 import scipy.sparse as sp
 from scipy.sparse.csgraph import connected_components
 
-from .mesh import CoefficientField, StructuredMesh
+from .mesh import CoefficientField, StructuredMesh, _axis_sum
 
 KINDS = ("vertex", "edge", "face")
 _KIND_CODE = {k: i for i, k in enumerate(KINDS)}
@@ -243,7 +243,10 @@ class PartitionPair:
     def grounded_subdomains(self) -> np.ndarray:
         """partition.py:85-91: subdomains whose closure meets the Dirichlet boundary."""
         touches = np.zeros(self.subdomain_count, dtype=bool)
-        cell_on_boundary = self.mesh.boundary_mask[self.mesh.cell_nodes].any(axis=1)
+        cells = self.mesh.cells_per_dim
+        # a cell meets the boundary iff one of its coordinates is 0 or cells - 1
+        edge = [np.isin(np.arange(c), (0, c - 1)).astype(np.int8) for c in cells]
+        cell_on_boundary = _axis_sum(edge) > 0
         touches[np.unique(self.theta[cell_on_boundary])] = True
         return touches
 
@@ -299,13 +302,9 @@ def partition_uniform(mesh: StructuredMesh, subdomains_per_dim: Sequence[int]) -
                 f"{subs[d]} subdomains do not divide {mesh.cells_per_dim[d]} cells on axis {d}"
             )
     blocks = [mesh.cells_per_dim[d] // subs[d] for d in range(mesh.dim)]
-    multi = mesh.cell_multi_indices()
-    theta = np.zeros(mesh.cell_count, dtype=np.int64)
-    stride = 1
-    for d in range(mesh.dim):
-        theta += (multi[:, d] // blocks[d]) * stride
-        stride *= subs[d]
-    return theta
+    strides = np.cumprod((1,) + subs[:-1]).astype(np.int64)
+    return _axis_sum([(np.arange(mesh.cells_per_dim[d], dtype=np.int64) // blocks[d]) * strides[d]
+                      for d in range(mesh.dim)])
 
 
 def _subdomain_boxes(mesh: StructuredMesh, theta: np.ndarray):
@@ -327,6 +326,18 @@ def _subdomain_boxes(mesh: StructuredMesh, theta: np.ndarray):
 
 def _uniform_box_layout(mesh: StructuredMesh, theta: np.ndarray):
     """(subs_per_dim, block) if Θ equals partition_uniform(mesh, subs_per_dim), else None."""
+    # candidate from the labels along each axis through cell 0, confirmed by an array compare
+    cells = mesh.cells_per_dim
+    cstr = np.cumprod((1,) + tuple(cells[:-1])).astype(np.int64)
+    block = []
+    for d in range(mesh.dim):
+        line = theta[np.arange(cells[d], dtype=np.int64) * cstr[d]]
+        ch = np.flatnonzero(line != line[0])
+        block.append(int(ch[0]) if len(ch) else cells[d])
+    if all(cells[d] % block[d] == 0 for d in range(mesh.dim)):
+        subs = tuple(cells[d] // block[d] for d in range(mesh.dim))
+        if np.array_equal(theta, partition_uniform(mesh, subs)):
+            return subs, tuple(block)
     try:
         lo, hi = _subdomain_boxes(mesh, theta)
     except ValueError:
@@ -351,6 +362,15 @@ def refine_uniform(mesh: StructuredMesh, theta: np.ndarray, split: int,
     theta = np.asarray(theta, dtype=np.int64)
     if split == 1:
         return PartitionPair(mesh, theta, theta.copy(), validate=validate)
+    lay = _uniform_box_layout(mesh, theta)
+    if lay is not None and all(b % split == 0 for b in lay[1]):
+        # uniform boxes: Θ̂ = Θ s^d + Σ_d ((i_d mod block_d) // (block_d / s)) s^d as an outer sum
+        blk = lay[1]
+        sub_id = _axis_sum([(np.arange(mesh.cells_per_dim[d], dtype=np.int64) % blk[d]) // (blk[d] // split)
+                            * split**d for d in range(mesh.dim)])
+        pair = PartitionPair(mesh, theta, theta * split**mesh.dim + sub_id, validate=validate)
+        pair.__dict__["box_layout"] = lay
+        return pair
     lo, hi = _subdomain_boxes(mesh, theta)
     size = hi - lo + 1
     bad = np.flatnonzero(np.any(size % split != 0, axis=1))

@@ -155,8 +155,10 @@ def test_device_inputs_are_validated(cuda_ok):
 def test_cfg4_reference_mode_documented_bound(cuda_ok):
     """cfg4 analogue in the reference's coarse scaling (κ ≈ 8e8): B·r, κ and x agree with
     the reference; the iteration count of this ill-conditioned Krylov run differs by more
-    than ±1 (reference 1397, ours 1366 on a B200: within 5%). Config 4 itself runs in spec
-    scaling, where the ±1 rule holds (cfg4a_p1_spec, cfg4b_p1_spec)."""
+    than ±1 (reference 1397, ours 1366 on a B200). The reference algorithm itself moves over
+    1378 .. 1441 when b is perturbed at rounding level (tests/test_oracle_sensitivity.py), so
+    the count is held to 5%. Config 4 itself runs in spec scaling, where the
+    ±1 rule holds (cfg4a_p1_spec, cfg4b_p1_spec)."""
     g = load_golden("cfg4a_p1_ref")
     pb, op = _op(g)
     z = op.apply(g["r"])

@@ -83,3 +83,23 @@ def test_device_index_sets_at_cfg3_size(cuda_ok):
     od = P.classify_objects(pd, device=0)
     _same_objects(oh, od)
     assert len(P.select_constraints(od, "vef", pd)) == P.count_coarse_dofs((16, 16, 16), 2, "vef") == 139455
+
+
+@pytest.mark.parametrize("case", golden_cases())
+def test_device_layout_tables_match_host(cuda_ok, case):
+    """Per-subdomain slot tables (interface position, local constraint, coefficient, weight)
+    and the interface gather table from the device kernels (bddc_layout_tables) equal the
+    numpy statement (layout.py; bddc.py:420-490)."""
+    from paper_2001_07289_b200.layout import build_device_plan
+
+    g = load_golden(case)
+    pb = build_problem(g)
+    if pb["pair"].box_layout is None:
+        pytest.skip("non-box partition")
+    cons = P.select_constraints(pb["objects"], pb["recipe"], pb["pair"])
+    h = build_device_plan(pb["pair"], cons, pb["weights"], coarse_pattern="device")
+    d = build_device_plan(pb["pair"], cons, pb["weights"], coarse_pattern="device", device=0)
+    for f in ("slot_gamma", "slot_con", "slot_coef", "slot_w", "gamma_slots", "con_coarse", "coarse_slots",
+              "gamma_dof", "n_con_local"):
+        a, b = getattr(h, f), getattr(d, f)
+        assert a.dtype == b.dtype and np.array_equal(a, b), f
