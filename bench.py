@@ -195,7 +195,9 @@ class ClockSampler:
                 "samples": len(sm), "source": source}
 
 
-def build_host_problem(name):
+def build_host_problem(name, device=None):
+    """The workload's mesh, partition pair, objects, weights, system and rhs; ``device``:
+    membership / objects / weights from the device index-set kernels (index_device.py)."""
     import paper_2001_07289_b200 as P
 
     dim, cells, subs, split, recipe, wmode, source, coef, scaling = WORKLOADS[name]
@@ -203,7 +205,7 @@ def build_host_problem(name):
     mesh = P.build_mesh(dim, cells, "p1")
     cf = P.make_constant(mesh, 1.0) if coef == "one" else P.make_blocks(mesh, 4, 0)
     pair = P.refine_uniform(mesh, P.partition_uniform(mesh, subs), split, validate=False)
-    objs = P.classify_objects(pair)
+    objs = P.classify_objects(pair, device=device)
     w = P.compute_weights(pair, wmode, cf, objs)
     system = P.assemble(mesh, cf)
     if source == "uniform":
@@ -305,7 +307,8 @@ def run_ours(args, rank, world, local_rank):
     from paper_2001_07289_b200 import _capi
 
     torch.cuda.set_device(local_rank)
-    pb = build_host_problem(args.workload)
+    torch.zeros(1, device="cuda")  # CUDA context outside the prep timing
+    pb = build_host_problem(args.workload, device=local_rank)
     P = pb["P"]
     t0 = time.perf_counter()
     # N > 1: one operator sharded over the ranks (slabs of subdomain rows, NCCL exchanges,
