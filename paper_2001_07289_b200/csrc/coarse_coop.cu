@@ -43,7 +43,10 @@ enum CoopType : int {
 // right-looking SY updates touch only the block column (K = 64); the trailing matrix beyond
 // it is updated ONCE per group (CT_SYG, K = 256), so every trailing tile is read and written
 // a quarter as often as with per-panel updates (the DRAM traffic of the large fronts).
-constexpr int kGroup = 4;
+#ifndef BDDC_KGROUP
+#define BDDC_KGROUP 4
+#endif
+constexpr int kGroup = BDDC_KGROUP;
 __host__ __device__ __forceinline__ int group_k0(int g) { return g * kGroup * kTile; }
 __host__ __device__ __forceinline__ int group_k1(int g, int s) { return min(s, (g + 1) * kGroup * kTile); }
 
@@ -342,14 +345,6 @@ struct SolveProgram {
   double* tbuf;         // backward: t = -L21^T x_bnd per separator row of the L21 fronts
   int n;                // coarse size
 };
-
-__device__ __forceinline__ double gather_at(const LevelView& lv, const double* __restrict__ upd, long long gbase,
-                                           int pos) {
-  const int* gp = lv.gat_ptr + gbase;
-  double acc = 0.0;
-  for (int q = gp[pos]; q < gp[pos + 1]; ++q) acc += __ldcg(upd + lv.gat_src[q]);  // other CTAs' results
-  return acc;
-}
 
 struct SolveShared {
   double vs[256];
