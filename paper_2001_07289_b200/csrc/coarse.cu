@@ -113,6 +113,8 @@ void build_level_schedule(Ctx& c) {
   std::vector<int> ych(fp.nnodes, -1), tch(fp.nnodes, -1);
   int nchunk_ctr = 0;
   int pf = 0, pb = 0;
+  const char* we = getenv("BDDC_SOLVE_WIDE_SEP");
+  const int wide_sep = we ? atoi(we) : 0;
   // one reduction chunk: tasks [first, end) share partials (np > 1) or write directly
   auto close_chunk = [](std::vector<CsTask>& v, std::vector<CsRed>& red, size_t first, int p0, int t0) {
     const int cnt = (int)(v.size() - first);
@@ -146,14 +148,17 @@ void build_level_schedule(Ctx& c) {
       } else {
         // large separators (the top of the tree, where the level chain is the critical path):
         // narrow tasks whose front entries are all in flight before the dependency wait
-        const int cw = sz >= 128 ? 64 : 256;
+        // wide (256-column) tasks for the X / W21 rows of very large fronts: fewer, longer
+        // streams where the dependency resolves long before the task starts (BDDC_SOLVE_WIDE_SEP)
+        const int cw = sz >= 128 ? (wide_sep > 0 && sz >= wide_sep ? 256 : 64) : 256;
         for (int pass = 0; pass < (wf ? 1 : 2); ++pass) {  // [X; W21] rows | X rows, then L21 rows
           const int rbeg = pass ? sz : 0, rlim = (pass || wf) ? f : sz;
           for (int r0 = rbeg; r0 < rlim; r0 += 64) {
             const size_t first = ft.size();
             const int p0 = pf;
             const int rend = std::min(r0 + 64, rlim);
-            for (int c0 = 0; c0 < sz; c0 += cw) {
+            const int cwp = pass ? 64 : cw;
+            for (int c0 = 0; c0 < sz; c0 += cwp) {
               if (!pass && r0 < sz && c0 > std::min(rend, sz) - 1) break;  // X is lower triangular
               CsTask t = base(nd);
               t.r0 = r0;
@@ -161,15 +166,16 @@ void build_level_schedule(Ctx& c) {
               t.c0 = c0;
               t.part = pf++;
               t.mode = pass ? 4 : 0;
-              t.span = cw;
+              t.span = pass ? 64 : cw;  // L21 rows wait for one 64-column y_s chunk
               ft.push_back(t);
             }
             if (close_chunk(ft, fr, first, p0, r0) > 0) nfch[nd]++;
           }
         }
       }
-      const int rw = sz >= 128 ? 64 : 256;
+      const int rw0 = sz >= 128 ? (wide_sep > 0 && sz >= wide_sep ? 256 : 64) : 256;
       for (int pass = (wf ? 1 : 0); pass < 2; ++pass) {  // (L21: t = -L21^T x_bnd), then x_s
+        const int rw = (pass && !wf) ? 64 : rw0;  // L21 fronts' x_s rows wait for one t chunk
         for (int c0 = 0; c0 < sz; c0 += 64) {
           const size_t first = bt.size();
           const int p0 = pb;

@@ -39,12 +39,12 @@ enum CoopType : int {
   CT_NTYPES = 9
 };
 
-// Panels are factored in groups of kGroup (a 256-column block column): inside the group the
+// Panels are factored in groups of kGroup (a 512-column block column): inside the group the
 // right-looking SY updates touch only the block column (K = 64); the trailing matrix beyond
 // it is updated ONCE per group (CT_SYG, K = 256), so every trailing tile is read and written
 // a quarter as often as with per-panel updates (the DRAM traffic of the large fronts).
 #ifndef BDDC_KGROUP
-#define BDDC_KGROUP 4
+#define BDDC_KGROUP 8
 #endif
 constexpr int kGroup = BDDC_KGROUP;
 __host__ __device__ __forceinline__ int group_k0(int g) { return g * kGroup * kTile; }
