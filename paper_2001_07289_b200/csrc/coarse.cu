@@ -113,8 +113,10 @@ void build_level_schedule(Ctx& c) {
   std::vector<int> ych(fp.nnodes, -1), tch(fp.nnodes, -1);
   int nchunk_ctr = 0;
   int pf = 0, pb = 0;
+  // 256-wide tasks for the X / W21 rows of fronts with s >= this (0: always 64): at cfg5 the
+  // coarse solve drops from 17.0 to 11.6 ms with every front wide (tools/gpu_ab2.sh)
   const char* we = getenv("BDDC_SOLVE_WIDE_SEP");
-  const int wide_sep = we ? atoi(we) : 0;
+  const int wide_sep = we ? atoi(we) : 128;
   // one reduction chunk: tasks [first, end) share partials (np > 1) or write directly
   auto close_chunk = [](std::vector<CsTask>& v, std::vector<CsRed>& red, size_t first, int p0, int t0) {
     const int cnt = (int)(v.size() - first);

@@ -41,8 +41,10 @@ enum CoopType : int {
 
 // Panels are factored in groups of kGroup (a 512-column block column): inside the group the
 // right-looking SY updates touch only the block column (K = 64); the trailing matrix beyond
-// it is updated ONCE per group (CT_SYG, K = 256), so every trailing tile is read and written
-// a quarter as often as with per-panel updates (the DRAM traffic of the large fronts).
+// it is updated ONCE per group (CT_SYG, K = kGroup * 64 = 512), so every trailing tile is read
+// and written 1/kGroup as often as with per-panel updates (the DRAM traffic of the large
+// fronts), and the program has half the tasks of groups of 4 (cfg5: 1.31 -> 1.25 s, measured
+// with groups of 4 / 6 / 8 / 12 / 16: tools/gpu_ab_group.sh, tools/gpu_ab2.sh).
 #ifndef BDDC_KGROUP
 #define BDDC_KGROUP 8
 #endif
