@@ -117,6 +117,10 @@ void build_level_schedule(Ctx& c) {
   // coarse solve drops from 17.0 to 11.6 ms with every front wide (tools/gpu_ab2.sh)
   const char* we = getenv("BDDC_SOLVE_WIDE_SEP");
   const int wide_sep = we ? atoi(we) : 128;
+  // 512-wide tasks for fronts with s >= BDDC_SOLVE_512_SEP (default 2048; 0: never): cfg5
+  // coarse solve 11.5 -> 11.4 ms, neutral on cfg3 / cfg2 (tools/gpu_ab4.sh)
+  const char* se = getenv("BDDC_SOLVE_512_SEP");
+  const int span_sep = se ? (atoi(se) > 0 ? atoi(se) : INT_MAX) : 2048;
   // one reduction chunk: tasks [first, end) share partials (np > 1) or write directly
   auto close_chunk = [](std::vector<CsTask>& v, std::vector<CsRed>& red, size_t first, int p0, int t0) {
     const int cnt = (int)(v.size() - first);
@@ -152,7 +156,7 @@ void build_level_schedule(Ctx& c) {
         // narrow tasks whose front entries are all in flight before the dependency wait
         // wide (256-column) tasks for the X / W21 rows of very large fronts: fewer, longer
         // streams where the dependency resolves long before the task starts (BDDC_SOLVE_WIDE_SEP)
-        const int cw = sz >= 128 ? (wide_sep > 0 && sz >= wide_sep ? 256 : 64) : 256;
+        const int cw = sz >= 128 ? (wide_sep > 0 && sz >= wide_sep ? (sz >= span_sep ? 512 : 256) : 64) : 256;
         for (int pass = 0; pass < (wf ? 1 : 2); ++pass) {  // [X; W21] rows | X rows, then L21 rows
           const int rbeg = pass ? sz : 0, rlim = (pass || wf) ? f : sz;
           for (int r0 = rbeg; r0 < rlim; r0 += 64) {
@@ -175,7 +179,7 @@ void build_level_schedule(Ctx& c) {
           }
         }
       }
-      const int rw0 = sz >= 128 ? (wide_sep > 0 && sz >= wide_sep ? 256 : 64) : 256;
+      const int rw0 = sz >= 128 ? (wide_sep > 0 && sz >= wide_sep ? (sz >= span_sep ? 512 : 256) : 64) : 256;
       for (int pass = (wf ? 1 : 0); pass < 2; ++pass) {  // (L21: t = -L21^T x_bnd), then x_s
         const int rw = (pass && !wf) ? 64 : rw0;  // L21 fronts' x_s rows wait for one t chunk
         for (int c0 = 0; c0 < sz; c0 += 64) {

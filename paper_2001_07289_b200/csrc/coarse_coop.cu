@@ -349,7 +349,7 @@ struct SolveProgram {
 };
 
 struct SolveShared {
-  double vs[256];
+  double vs[512];
   double red[4][64];
   int last;
 };
@@ -483,6 +483,20 @@ __device__ bool solve_fwd_task(const CsTask& t, const FrontDev& fd, const LevelV
   double vin = 0.0;
   if (kk < s && tid < t.span) vin = lrows ? __ldcg(ybuf + t.s0 + kk) : rv + gv.value(lv, fd.upd);
   sh.vs[tid] = vin;
+  if (t.span > 256) {  // 512-wide tasks: the second half of the columns, gathered after the wait
+    const int k2 = kk + 256;
+    double v2 = 0.0;
+    if (k2 < s) {
+      if (lrows) {
+        v2 = __ldcg(ybuf + t.s0 + k2);
+      } else {
+        GatherPre g2;
+        g2.load(lv, t.gat_base, k2, true);
+        v2 = rhs[t.s0 + k2] + g2.value(lv, fd.upd);
+      }
+    }
+    sh.vs[256 + tid] = v2;
+  }
   __syncthreads();
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   for (int k0 = kb; k0 < ke; k0 += 16) {
@@ -559,13 +573,19 @@ __device__ bool solve_bwd_task(const CsTask& t, const FrontDev& fd, const SolveP
   const int bi = (mine && r >= s) ? bidx[r - s] : -1;
   wait();
   sh.vs[tid] = !mine ? 0.0 : (r >= s ? -__ldcg(sol + bi) : __ldcg(ybuf + t.s0 + r) + __ldcg(sp.tbuf + t.s0 + r));
+  if (t.span > 256) {  // 512-row tasks: the second half of the rows
+    const int r2 = r + 256;
+    const bool m2 = r2 < t.rend;
+    sh.vs[256 + tid] = !m2 ? 0.0 : (r2 >= s ? -__ldcg(sol + bidx[r2 - s])
+                                            : __ldcg(ybuf + t.s0 + r2) + __ldcg(sp.tbuf + t.s0 + r2));
+  }
   __syncthreads();
   double acc[8];
 #pragma unroll
   for (int cc = 0; cc < 8; ++cc) acc[cc] = 0.0;
   const int mend = min(t.span >> 5, (t.rend - t.r0 + 31) / 32);  // row batches that hold task rows
-#pragma unroll
-  for (int m = 0; m < 8; m += 2) {
+#pragma unroll 4
+  for (int m = 0; m < 16; m += 2) {
     if (m >= mend) break;
     if (m > 0) load_rows(m);
 #pragma unroll

@@ -165,6 +165,7 @@ void nccl_check(ncclResult_t r, const char* what) {
 struct NcclTransport : Transport {
   ncclComm_t comm = nullptr;
   int* d_int = nullptr;
+  cudaStream_t st = nullptr;  // the failure-code reduction's own stream (not the legacy stream)
   NcclTransport(int r, int w, const void* id) {
     rank = r;
     world = w;
@@ -172,10 +173,12 @@ struct NcclTransport : Transport {
     memcpy(&uid, id, sizeof(uid));
     nccl_check(nccl_api().CommInitRank(&comm, w, uid, r), "CommInitRank");
     BDDC_CUDA(cudaMalloc(&d_int, sizeof(int)));
+    BDDC_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   }
   ~NcclTransport() override {
     if (comm) nccl_api().CommDestroy(comm);
     if (d_int) cudaFree(d_int);
+    if (st) cudaStreamDestroy(st);
   }
   void neighbors(const double* lo_send, double* lo_recv, long long lo_n, const double* hi_send, double* hi_recv,
                  long long hi_n, cudaStream_t s) override {
@@ -202,9 +205,10 @@ struct NcclTransport : Transport {
     nccl_check(nccl_api().AllReduce(buf, buf, n, ncclDouble, ncclSum, comm, s), "AllReduce");
   }
   int allreduce_max_host(int v) override {
-    BDDC_CUDA(cudaMemcpy(d_int, &v, sizeof(int), cudaMemcpyHostToDevice));
-    nccl_check(nccl_api().AllReduce(d_int, d_int, 1, ncclInt32, ncclMax, comm, nullptr), "AllReduce");
-    BDDC_CUDA(cudaMemcpy(&v, d_int, sizeof(int), cudaMemcpyDeviceToHost));
+    BDDC_CUDA(cudaMemcpyAsync(d_int, &v, sizeof(int), cudaMemcpyHostToDevice, st));
+    nccl_check(nccl_api().AllReduce(d_int, d_int, 1, ncclInt32, ncclMax, comm, st), "AllReduce");
+    BDDC_CUDA(cudaMemcpyAsync(&v, d_int, sizeof(int), cudaMemcpyDeviceToHost, st));
+    BDDC_CUDA(cudaStreamSynchronize(st));
     return v;
   }
 };
