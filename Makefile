@@ -7,8 +7,21 @@ HDR := $(wildcard paper_2001_07289_b200/csrc/*.cuh) include/bddcso_b200.h
 OBJDIR := paper_2001_07289_b200/build
 OBJ := $(patsubst paper_2001_07289_b200/csrc/%.cu,$(OBJDIR)/%.o,$(SRC))
 LIB := paper_2001_07289_b200/libbddcso_b200.so
+# checked build: device bounds checks on the index-driven gathers / scatters (BDDC_CHECK)
+CHKDIR := paper_2001_07289_b200/build_check
+CHKOBJ := $(patsubst paper_2001_07289_b200/csrc/%.cu,$(CHKDIR)/%.o,$(SRC))
+CHKLIB := paper_2001_07289_b200/libbddcso_b200_check.so
 
-all: $(LIB)
+all: $(LIB) $(CHKLIB)
+
+check: $(CHKLIB)
+
+$(CHKDIR)/%.o: paper_2001_07289_b200/csrc/%.cu $(HDR)
+	@mkdir -p $(CHKDIR)
+	$(NVCC) $(ARCH) $(FLAGS) -DBDDC_CHECKS -c -o $@ $<
+
+$(CHKLIB): $(CHKOBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(CHKOBJ)
 
 $(OBJDIR)/%.o: paper_2001_07289_b200/csrc/%.cu $(HDR)
 	@mkdir -p $(OBJDIR)
@@ -18,4 +31,4 @@ $(LIB): $(OBJ)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJ)
 
 clean:
-	rm -rf $(LIB) $(OBJDIR)
+	rm -rf $(LIB) $(OBJDIR) $(CHKLIB) $(CHKDIR)

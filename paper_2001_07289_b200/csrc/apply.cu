@@ -626,14 +626,16 @@ __global__ void __launch_bounds__(128) local_gamma2_kernel(Geometry G, SubTables
 // z[gamma dof] = sum over owner slots (ascending subdomain = reference summation order)
 __global__ void gamma_gather_kernel(int g_lo, int g_hi, int W, const long long* __restrict__ gdof,
                                     const int* __restrict__ gslots, const double* __restrict__ wloc,
-                                    double* __restrict__ z) {
+                                    double* __restrict__ z, long long nslots, long long n) {
   const int g = g_lo + blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= g_hi) return;
   double acc = 0.0;
   for (int w = 0; w < W; ++w) {
     const int s = gslots[(long long)g * W + w];
+    BDDC_CHECK(s < nslots);
     if (s >= 0) acc += wloc[s];
   }
+  BDDC_CHECK(gdof[g] >= 0 && gdof[g] < n);
   z[gdof[g]] = acc;
 }
 
@@ -746,7 +748,8 @@ void apply_bddc(Ctx& c, const double* r, double* z, cudaStream_t s) {
   BDDC_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * G.n, s));
   if (ng > 0) {
     { gamma_gather_kernel<<<ceil_div(ng, th), th, 0, s>>>(G.g_lo, G.g_hi, G.npe,
-                                                        c.gamma_dof, c.gamma_slots, c.wloc, z); BDDC_COUNT(); }
+                                                        c.gamma_dof, c.gamma_slots, c.wloc, z,
+                                                        (long long)G.nsub * G.nG_pad, G.n); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
   }
   // z_I = A_II^{-1} (r - A z_Gamma)_I

@@ -17,20 +17,26 @@ namespace {
 
 __global__ void csr_segsum_kernel(long long nnz, const long long* __restrict__ seg,
                                   const int* __restrict__ contrib, const double* __restrict__ Sloc,
-                                  double* __restrict__ val) {
+                                  double* __restrict__ val, long long nloc) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
        e += (long long)gridDim.x * blockDim.x) {
     double acc = 0.0;
-    for (long long k = seg[e]; k < seg[e + 1]; ++k) acc += Sloc[contrib[k]];
+    for (long long k = seg[e]; k < seg[e + 1]; ++k) {
+      BDDC_CHECK(contrib[k] >= 0 && contrib[k] < nloc);
+      acc += Sloc[contrib[k]];
+    }
     val[e] = acc;
   }
 }
 
 __global__ void csr_to_front_kernel(long long nnz, const long long* __restrict__ pos,
-                                    const double* __restrict__ val, double* __restrict__ fronts) {
+                                    const double* __restrict__ val, double* __restrict__ fronts,
+                                    long long pool) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
-       e += (long long)gridDim.x * blockDim.x)
+       e += (long long)gridDim.x * blockDim.x) {
+    BDDC_CHECK(pos[e] >= 0 && pos[e] < pool);
     fronts[pos[e]] = val[e];
+  }
 }
 
 }  // namespace
@@ -318,11 +324,12 @@ void coarse_assemble_and_factor(Ctx& c) {
   PhaseScope ps(c.prof, "setup.coarse", s);
   const int th = 256;
   { csr_segsum_kernel<<<std::min<long long>((fp.nnz + th - 1) / th, 148 * 16), th, 0, s>>>(
-      fp.nnz, fp.seg_ptr, fp.contrib, c.Sloc, fp.csr_val); BDDC_COUNT(); }
+      fp.nnz, fp.seg_ptr, fp.contrib, c.Sloc, fp.csr_val,
+      (long long)c.geo.nsub * c.geo.nc_pad * c.geo.nc_pad); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
   front_memset(c, s);
   { csr_to_front_kernel<<<std::min<long long>((fp.nnz + th - 1) / th, 148 * 16), th, 0, s>>>(
-      fp.nnz, fp.csr_front_pos, fp.csr_val, fd.fronts); BDDC_COUNT(); }
+      fp.nnz, fp.csr_front_pos, fp.csr_val, fd.fronts, fp.front_pool); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
   // multifrontal factorization + partitioned inverse: one cooperative launch
   coop_factor(c, s);

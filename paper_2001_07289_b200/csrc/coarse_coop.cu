@@ -132,6 +132,7 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
         for (int c = 0; c < 16; ++c) cof[c] = j0 + c < je ? (long long)rm[j0 + c] * ld : 0;
         for (int i = j0 + threadIdx.x; i < bc; i += blockDim.x) {
           const long long r = rm[i];
+          BDDC_CHECK(r >= 0 && r < f);  // extend-add row inside the parent front
           double u[16], fv[16];
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
@@ -367,6 +368,7 @@ struct GatherPre {
     q1 = gp[pos + 1];
     if (q1 > q0) i0 = lv.gat_src[q0];
     if (q1 > q0 + 1) i1 = lv.gat_src[q0 + 1];
+    BDDC_CHECK(q1 >= q0 && i0 >= -1 && i1 >= -1);
   }
   __device__ __forceinline__ double value(const LevelView& lv, const double* __restrict__ upd) const {
     double acc = 0.0;
@@ -571,6 +573,7 @@ __device__ bool solve_bwd_task(const CsTask& t, const FrontDev& fd, const SolveP
   const int r = t.r0 + tid;
   const bool mine = tid < t.span && r < t.rend;
   const int bi = (mine && r >= s) ? bidx[r - s] : -1;
+  BDDC_CHECK(bi < sp.n);
   wait();
   sh.vs[tid] = !mine ? 0.0 : (r >= s ? -__ldcg(sol + bi) : __ldcg(ybuf + t.s0 + r) + __ldcg(sp.tbuf + t.s0 + r));
   if (t.span > 256) {  // 512-row tasks: the second half of the rows

@@ -24,6 +24,26 @@ struct CudaError : std::runtime_error {
 
 #define BDDC_LAUNCH_CHECK() BDDC_CUDA(cudaGetLastError())
 
+// Device-side bounds checks of the index-driven gathers / scatters (extend-add maps, coarse
+// assembly positions, interface gathers, the coarse solve's gathers). Compiled in only for the
+// checked build (make check -> libbddcso_b200_check.so, -DBDDC_CHECKS): a failed check prints
+// its location and traps, so the launch fails loudly instead of corrupting memory. This is the
+// bounds evidence in place of compute-sanitizer, which is closed on this GPU pool.
+#ifdef BDDC_CHECKS
+#define BDDC_CHECK(cond)                                                                      \
+  do {                                                                                        \
+    if (!(cond)) {                                                                            \
+      printf("BDDC_CHECK failed at %s:%d: %s (block %d, thread %d)\n", __FILE__, __LINE__, #cond, \
+             (int)blockIdx.x, (int)threadIdx.x);                                              \
+      __trap();                                                                               \
+    }                                                                                         \
+  } while (0)
+#else
+#define BDDC_CHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 // Number of kernels this library has launched (reported by bench.py as gpu_launches).
 inline std::atomic<long long>& launch_counter() {
   static std::atomic<long long> c{0};
