@@ -535,7 +535,9 @@ def run_ours(args, rank, world, local_rank):
             "parallelism": "single GPU" if world == 1 else
                            f"sharded x{world}: slabs of subdomain rows along the last axis, "
                            + ("host-staged (gloo, ranks sharing one GPU: test transport)" if args.transport == "host"
-                              else "NCCL") + " halo / allgather exchanges, replicated coarse problem",
+                              else "NCCL") + " halo / allgather exchanges, "
+                           + ("replicated coarse problem" if os.environ.get("BDDC_DIST_COARSE") == "0" else
+                              "coarse ND subtrees per rank + replicated top (DESIGN.md §9.2)"),
             "l2": "inputs > L2 (factors %.1f GB + fronts %.2f GB vs 126 MB L2)" % (
                 st.factor_bytes / 1e9, st.front_bytes / 1e9),
         },

@@ -82,6 +82,29 @@ struct Transport {
   virtual int allreduce_max_host(int v) = 0;
 };
 
+// Distributed coarse factorization (sharded operators): the ND subtrees rooted
+// at depth `depth` are dealt to the ranks (root i -> rank i % world); each rank factors and
+// solves its subtrees only, the fronts above (`top`) are replicated. phase[nd]: 0 this
+// rank's subtrees, 1 top, -1 another rank's subtree.
+struct DistCoarse {
+  bool on = false;
+  int depth = 0;
+  std::vector<int> phase;      // per node
+  std::vector<int> roots;      // subtree roots (depth == depth), node order
+  std::vector<int> root_owner;
+  std::vector<int> sub_lo, sub_hi;  // per root: its subtree's node range [lo, hi] (postorder)
+  double* stage = nullptr;     // exchange staging (device)
+  long long stage_len = 0;
+};
+
+// one block of an exchange: `n` doubles at `ptr` (kind 0), or the lower triangle of the b x b
+// block at `ptr` with leading dimension ld (kind 1, packed column by column); owner's copy wins
+struct ExSeg {
+  double* ptr;
+  long long n;
+  int owner, kind, b, ld;
+};
+
 // Slab bookkeeping derived from the geometry (host).
 struct Slab {
   long long row_len = 0;  // free dofs per node row (2D) / plane (3D) of the last axis
@@ -215,6 +238,7 @@ struct LevelSchedule {
   // dataflow solve (default): one task queue, node counters [3 N] + queue head + error flag
   SdTask* df_tasks = nullptr;
   int n_df = 0;
+  std::vector<std::pair<SdTask*, int>> queues;  // 1 queue, or 3 (distributed coarse: coarse.cu)
   int n_tv = 0;               // of which v = T rho tasks of the apply's local Gamma phase (dir 2)
   int* df_ctr = nullptr;
   int n_ctr = 0;
@@ -349,6 +373,7 @@ struct Ctx {
   // multi-GPU: slab of this rank and the exchange transport (null: single rank)
   Slab slab;
   Transport* tp = nullptr;
+  DistCoarse dist;
   // timing of the last setup (ms) per phase
   float t_local_ms = 0, t_coarse_ms = 0, t_upload_ms = 0;
   std::vector<void*> allocations;
@@ -371,6 +396,8 @@ struct Ctx {
     front_vmm_release(*this);
     for (void* p : allocations) cudaFree(p);
     allocations.clear();
+    if (dist.stage) cudaFree(dist.stage);
+    dist = DistCoarse{};
   }
   LtArgs lt_defer{};      // local T deferred into the coarse factorization (on = 1)
   bool lt_fusable = false;  // the coarse factor program holds the T tasks
@@ -418,6 +445,8 @@ void slab_partition(Geometry& G, Slab& sl, int rank, int world, const long long*
 void exchange_dof_halo(Ctx& c, double* v, cudaStream_t s);        // rows next to the cut lines
 void exchange_boundary_rows(Ctx& c, double* per_sub, int stride, cudaStream_t s);  // nG_pad / sub
 void allgather_subs(Ctx& c, double* per_sub, long long stride, cudaStream_t s);   // [nsub x stride]
+// every rank gets every segment from its owner (staged in c.dist.stage, allgatherv)
+void allgather_segments(Ctx& c, const std::vector<ExSeg>& segs, cudaStream_t s);
 void allreduce_scalars(Ctx& c, double* d, int n, cudaStream_t s);
 Transport* make_nccl_transport(int rank, int world, const void* unique_id);
 Transport* make_host_transport(int rank, int world, bddc_host_exchange_fn fn, void* user);

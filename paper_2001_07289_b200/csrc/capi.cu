@@ -111,10 +111,55 @@ void numeric_setup(bddc_ctx* h) {
     BDDC_CUDA(cudaMemcpy(fi.data(), c.fp.info, sizeof(int) * c.fp.nnodes, cudaMemcpyDeviceToHost));
     int bad = kNoFail;
     for (int v : fi) bad = std::min(bad, v);
+    // distributed coarse factorization: a pivot failure in another rank's subtree
+    const int any4 = c.dist.on ? c.tp->allreduce_max_host(bad != kNoFail ? 4 : 0) : 0;
     if (bad != kNoFail)
       throw ApiError{4, "matrix not SPD: nonpositive pivot at index " + std::to_string(bad)};
+    if (any4) throw ApiError{4, "matrix not SPD (coarse pivot failure on another rank)"};
   }
   c.setup_done = true;
+}
+
+// Distributed coarse factorization of a sharded operator: the ND subtrees
+// rooted at the first depth with at least `world` nodes are dealt round-robin to the ranks;
+// the fronts above are replicated. BDDC_DIST_COARSE=0 keeps the replicated coarse problem.
+void build_dist(Ctx& c) {
+  DistCoarse& D = c.dist;
+  if (D.stage) cudaFree(D.stage);
+  D = DistCoarse{};
+  const FrontPlan& fp = c.fp;
+  const char* e = getenv("BDDC_DIST_COARSE");
+  if (!c.tp || c.tp->world < 2 || fp.nnodes == 0 || (e && atoi(e) == 0)) return;
+  const int N = fp.nnodes, world = c.tp->world, rank = c.tp->rank;
+  std::vector<int> depth(N, 0), size(N, 1);
+  for (int v = N - 1; v >= 0; --v) depth[v] = fp.parent[v] < 0 ? 0 : depth[fp.parent[v]] + 1;  // parents after children
+  for (int v = 0; v < N; ++v)
+    if (fp.parent[v] >= 0) size[fp.parent[v]] += size[v];
+  int maxd = 0;
+  for (int v = 0; v < N; ++v) maxd = std::max(maxd, depth[v]);
+  std::vector<int> cnt(maxd + 1, 0);
+  for (int v = 0; v < N; ++v) cnt[depth[v]]++;
+  int d = -1;
+  for (int k = 0; k <= maxd && d < 0; ++k)
+    if (cnt[k] >= world) d = k;
+  if (d < 0) return;  // tree too small to deal out: replicated
+  D.depth = d;
+  D.phase.assign(N, 1);
+  for (int v = 0; v < N; ++v)
+    if (depth[v] == d) {
+      const int owner = (int)D.roots.size() % world;
+      D.roots.push_back(v);
+      D.root_owner.push_back(owner);
+      D.sub_lo.push_back(v - size[v] + 1);  // postorder: a subtree is a contiguous node range
+      D.sub_hi.push_back(v);
+      for (int u = v - size[v] + 1; u <= v; ++u) {
+        int a = u;  // postorder check: u lies in v's subtree
+        while (a >= 0 && a != v) a = fp.parent[a];
+        if (a != v) throw CudaError("distributed coarse plan: subtree is not a contiguous node range");
+        D.phase[u] = owner == rank ? 0 : -1;
+      }
+    }
+  D.on = true;
 }
 
 void build_plan(Ctx& c, const bddc_setup_desc* d) {
@@ -216,6 +261,7 @@ void build_plan(Ctx& c, const bddc_setup_desc* d) {
     fp.csr_val = c.alloc<double>(d->nnz);
   }
   fp.coarse_slots = c.upload(d->coarse_slots, (size_t)d->n_coarse * fp.W);
+  build_dist(c);
   HostTimer ht;
   build_level_schedule(c);
   ht.mark("solve + factor schedules");

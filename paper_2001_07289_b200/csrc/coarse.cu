@@ -10,8 +10,8 @@
 namespace bddc {
 
 void coop_build(Ctx& c);
-void coop_factor(Ctx& c, cudaStream_t s);
-void coop_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s, const TvArgs* tv);
+void coop_factor(Ctx& c, cudaStream_t s, int prog);
+void coop_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s, const TvArgs* tv, int queue);
 
 namespace {
 
@@ -305,8 +305,41 @@ void build_level_schedule(Ctx& c) {
       }
     }
     emit_tv(true);  // (L == 0)
-    ls.n_df = (int)q.size();
-    ls.df_tasks = c.upload<SdTask>(q.data(), std::max<size_t>(q.size(), 1));
+    ls.queues.clear();
+    if (!c.dist.on) {
+      ls.queues.push_back({c.upload<SdTask>(q.data(), std::max<size_t>(q.size(), 1)), (int)q.size()});
+    } else {
+      // distributed: three launches with exchanges between them: this rank's
+      // subtrees forward (+ the v = T rho tasks), the replicated top forward + backward, this
+      // rank's subtrees backward. A dependency on a node of an earlier launch is dropped (its
+      // data is final and exchanged before the next launch); another rank's nodes are skipped.
+      const std::vector<int>& ph = c.dist.phase;
+      std::vector<int> need_d(N, 0);
+      for (int nd = 0; nd < N; ++nd)
+        if (fp.parent[nd] >= 0 && ph[nd] == ph[fp.parent[nd]]) need_d[fp.parent[nd]] += nfch[nd];
+      std::vector<SdTask> qq[3];
+      for (SdTask d : q) {
+        if (d.dir == 2) {
+          qq[0].push_back(d);
+          continue;
+        }
+        const int nd = d.t.node, p = ph[nd];
+        if (p < 0) continue;
+        const int qi = d.dir == 0 ? (p == 0 ? 0 : 1) : (p == 0 ? 2 : 1);
+        if (d.dir == 0 && d.t.mode != 4) {
+          d.dep = need_d[nd] > 0 ? nd : -1;
+          d.tgt = need_d[nd];
+        } else if (d.dir == 1 && !(d.t.mode == 3 && tch[nd] >= 0)) {
+          int anc = fp.parent[nd];
+          while (anc >= 0 && nbch[anc] == 0) anc = fp.parent[anc];
+          if (anc >= 0 ? ph[anc] != p : p == 0) d.dep = -1;
+        }
+        qq[qi].push_back(d);
+      }
+      for (auto& v : qq) ls.queues.push_back({c.upload<SdTask>(v.data(), std::max<size_t>(v.size(), 1)), (int)v.size()});
+    }
+    ls.df_tasks = ls.queues[0].first;
+    ls.n_df = ls.queues[0].second;
     ls.n_ctr = 3 * N + nchunk_ctr;
     ls.df_ctr = c.alloc<int>(ls.n_ctr + 2);  // + queue head + error flag
     BDDC_CUDA(cudaMemset(ls.df_ctr, 0, sizeof(int) * (ls.n_ctr + 2)));
@@ -332,11 +365,45 @@ void coarse_assemble_and_factor(Ctx& c) {
       fp.nnz, fp.csr_front_pos, fp.csr_val, fd.fronts, fp.front_pool); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
   // multifrontal factorization + partitioned inverse: one cooperative launch
-  coop_factor(c, s);
+  if (!c.dist.on) {
+    coop_factor(c, s, 0);
+    return;
+  }
+  // distributed: this rank's subtrees, the subtree roots' update blocks to
+  // every rank, then the replicated top of the tree
+  coop_factor(c, s, 0);
+  std::vector<ExSeg> segs;
+  const DistCoarse& D = c.dist;
+  for (size_t i = 0; i < D.roots.size(); ++i) {
+    const int r = D.roots[i], sz = fp.sep_size[r], b = fp.bnd_size[r], ld = fp.ld[r];
+    if (b > 0) segs.push_back(ExSeg{fd.fronts + fp.front_off[r] + sz + (long long)sz * ld, 0, D.root_owner[i], 1, b, ld});
+  }
+  allgather_segments(c, segs, s);
+  coop_factor(c, s, 1);
 }
 
 void coarse_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s, const TvArgs* tv) {
-  coop_solve(c, rhs, sol, s, tv);
+  if (!c.dist.on) {
+    coop_solve(c, rhs, sol, s, tv, 0);
+    return;
+  }
+  const FrontPlan& fp = c.fp;
+  const DistCoarse& D = c.dist;
+  coop_solve(c, rhs, sol, s, tv, 0);  // this rank's subtrees, forward
+  std::vector<ExSeg> segs;  // the subtree roots' update vectors
+  for (size_t i = 0; i < D.roots.size(); ++i) {
+    const int r = D.roots[i];
+    if (fp.bnd_size[r] > 0) segs.push_back(ExSeg{fp.d.upd + fp.upd_off[r], fp.bnd_size[r], D.root_owner[i], 0, 0, 0});
+  }
+  allgather_segments(c, segs, s);
+  coop_solve(c, rhs, sol, s, nullptr, 1);  // the top, forward + backward (replicated)
+  coop_solve(c, rhs, sol, s, nullptr, 2);  // this rank's subtrees, backward
+  segs.clear();  // every subtree's solution (a contiguous range of elimination positions)
+  for (size_t i = 0; i < D.roots.size(); ++i) {
+    const long long a = fp.sep_start[D.sub_lo[i]], e = fp.sep_start[D.sub_hi[i]] + fp.sep_size[D.sub_hi[i]];
+    if (e > a) segs.push_back(ExSeg{sol + a, e - a, D.root_owner[i], 0, 0, 0});
+  }
+  allgather_segments(c, segs, s);
 }
 
 }  // namespace bddc

@@ -745,8 +745,9 @@ struct CoopState {
   SolveProgram sp{};
   int grid_f = 0, grid_s = 0;
   size_t smem_f = 0;
-  DfTask* dtasks = nullptr;
+  DfTask* dtasks = nullptr;  // the program of the launch in flight (one of progs)
   int ndtasks = 0;
+  std::vector<std::pair<DfTask*, int>> progs;  // 1 program, or 2 (this rank's subtrees, top)
   int* ctr = nullptr;  // [nctr] dependency counters + queue head + error flag
   int nctr = 0;
   unsigned long long* prof = nullptr;  // BDDC_COOP_TIMING: per task type wait / run cycles
@@ -805,7 +806,6 @@ void coop_build(Ctx& c) {
   // ---- dataflow factorization program ----
   HostTimer ht;
   {
-    std::vector<DfTask> dt;
     int nctr = 0;
     auto newc = [&](int n) { const int b = nctr; nctr += n; return b; };
     // per node counter bases and totals
@@ -849,11 +849,14 @@ void coop_build(Ctx& c) {
         if (t.sig[q] < 0) { t.sig[q] = cix; t.sw[q] = (unsigned char)w; return; }
       throw std::runtime_error("coarse dataflow: too many signals");
     };
+    // one program over the active nodes `act` (with_lt: also the local T tiles)
+    auto gen = [&](const std::vector<char>& act, bool with_lt) {
+    std::vector<DfTask> dt;
     const long long off = coarse_df_layout(fp, inv, Y, W, ldw);  // X lives in the fronts
     // the local setup's T tiles (no dependencies): the simulated schedule places them in the
     // CTA time the critical path leaves idle
     c.lt_fusable = c.geo.nG_pad > 0 && c.geo.nG_pad % kTile == 0;
-    if (c.lt_fusable) {
+    if (c.lt_fusable && with_lt) {
       const int nt = c.geo.nG_pad / kTile;
       for (int sub = c.geo.s_lo; sub < c.geo.s_hi; ++sub)
         for (int I = 0; I < nt; ++I)
@@ -865,20 +868,21 @@ void coop_build(Ctx& c) {
       for (int k = 0; k < max_children; ++k) {
         long long cols = 0;
         for (int nd : nodes)
-          if (fp.child_ptr[nd + 1] - fp.child_ptr[nd] > k) cols += fp.bnd_size[fp.child_list[fp.child_ptr[nd] + k]];
+          if (act[nd] && fp.child_ptr[nd + 1] - fp.child_ptr[nd] > k) cols += fp.bnd_size[fp.child_list[fp.child_ptr[nd] + k]];
         int chunk = 64;
         while (chunk > 2 && cols / chunk < 2LL * grid_f) chunk >>= 1;
         for (int nd : nodes) {
-          if (fp.child_ptr[nd + 1] - fp.child_ptr[nd] <= k) continue;
+          if (!act[nd] || fp.child_ptr[nd + 1] - fp.child_ptr[nd] <= k) continue;
           const int ch = fp.child_list[fp.child_ptr[nd] + k];
           for (int q = 0; q < fp.bnd_size[ch]; q += chunk) {
             DfTask t = mk(CT_EA, nd, q, chunk, k);
-            dep(t, c_syall[ch], tot_sy[ch]);
+            // (a child outside this program was factored before its launch: no counter)
+            if (act[ch]) dep(t, c_syall[ch], tot_sy[ch]);
             // an aliased update block may share pages with grandchildren's: no write into it
             // before every child subtree is done (front_vmm.cu)
             if (fp.ualias[nd] && k == 0)
               for (int o = fp.child_ptr[nd] + 1; o < fp.child_ptr[nd + 1]; ++o)
-                dep(t, c_syall[fp.child_list[o]], tot_sy[fp.child_list[o]]);
+                if (act[fp.child_list[o]]) dep(t, c_syall[fp.child_list[o]], tot_sy[fp.child_list[o]]);
             if (k > 0) dep(t, c_ea[nd] + k - 1, nea[nd][k - 1]);
             sig(t, c_ea[nd] + k);
             dt.push_back(t);
@@ -889,7 +893,7 @@ void coop_build(Ctx& c) {
       for (int nd : nodes) {
         const int s = fp.sep_size[nd], f = s + fp.bnd_size[nd], np = nP[nd], T = nT[nd];
         const int nch = fp.child_ptr[nd + 1] - fp.child_ptr[nd];
-        if (s <= 0) continue;
+        if (s <= 0 || !act[nd]) continue;
         {
           DfTask t = mk(CT_PT, nd, 0, 0, 0);
           if (nch > 0) dep(t, c_ea[nd] + nch - 1, nea[nd][nch - 1]);
@@ -1102,8 +1106,20 @@ void coop_build(Ctx& c) {
         fprintf(stderr, "coarse dataflow: simulated makespan %.1f us on %d CTAs (critical path %.1f us)\n", now,
                 grid_f, *std::max_element(rank.begin(), rank.end()));
     }
-    st.ndtasks = (int)dt.size();
-    st.dtasks = c.upload(dt.data(), dt.size());
+    return dt;
+    };
+    std::vector<std::vector<DfTask>> programs;
+    if (c.dist.on) {  // this rank's subtrees, then the replicated top (capi.cu: build_dist)
+      std::vector<char> a0(N), a1(N);
+      for (int nd = 0; nd < N; ++nd) a0[nd] = c.dist.phase[nd] == 0, a1[nd] = c.dist.phase[nd] == 1;
+      programs.push_back(gen(a0, true));
+      programs.push_back(gen(a1, false));
+    } else {
+      programs.push_back(gen(std::vector<char>(N, 1), true));
+    }
+    for (auto& dt : programs) st.progs.push_back({c.upload(dt.data(), dt.size()), (int)dt.size()});
+    st.dtasks = st.progs[0].first;
+    st.ndtasks = st.progs[0].second;
     ht.mark("factor program: upload");
     st.nctr = nctr;
     st.ctr = c.alloc<int>(nctr + 2);  // + queue head + error flag
@@ -1127,8 +1143,10 @@ void coop_build(Ctx& c) {
 
 void coop_release(const Ctx& c) { g_coop.erase(&c); }
 
-void coop_factor(Ctx& c, cudaStream_t s) {
+void coop_factor(Ctx& c, cudaStream_t s, int prog) {
   CoopState& st = g_coop.at(&c);
+  st.dtasks = st.progs.at(prog).first;
+  st.ndtasks = st.progs.at(prog).second;
   FrontDev fd = c.fp.d;
   int* info = c.fp.info;
   BDDC_CUDA(cudaMemsetAsync(st.ctr, 0, sizeof(int) * (st.nctr + 2), s));
@@ -1195,7 +1213,7 @@ int coarse_solve_error(Ctx& c) {
   return e;
 }
 
-void coop_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s, const TvArgs* tva) {
+void coop_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s, const TvArgs* tva, int queue) {
   CoopState& st = g_coop.at(&c);
   FrontDev fd = c.fp.d;
   LevelView lv{c.sched.gat_ptr, c.sched.gat_src};
@@ -1206,8 +1224,8 @@ void coop_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s, const Tv
   int* ctr = ls.df_ctr;
   int* qhead = ctr + ls.n_ctr;
   int* err = qhead + 1;
-  const SdTask* tasks = ls.df_tasks;
-  int ntasks = ls.n_df;
+  const SdTask* tasks = ls.queues.at(queue).first;
+  int ntasks = ls.queues.at(queue).second;
   // counters, queue head and the error flag start at zero every launch (a timeout poisons
   // this launch's result only; pcg_solve / bddc_check report it)
   BDDC_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int) * (ls.n_ctr + 2), s));

@@ -102,6 +102,64 @@ void allgather_subs(Ctx& c, double* per_sub, long long stride, cudaStream_t s) {
   c.tp->allgatherv(per_sub, off.data(), cnt.data(), s);
 }
 
+namespace {
+// packed lower triangle of a b x b block (column j: rows j..b-1) <-> contiguous stage
+__global__ void lower_pack_kernel(double* blk, int b, int ld, double* packed, int dir) {
+  const long long tot = (long long)b * (b + 1) / 2;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < tot; q += (long long)gridDim.x * blockDim.x) {
+    // column j with off(j) = j b - j (j - 1) / 2 <= q
+    long long j = (long long)((2.0 * b + 1.0 - sqrt((2.0 * b + 1.0) * (2.0 * b + 1.0) - 8.0 * (double)q)) * 0.5);
+    if (j < 0) j = 0;
+    while (j > 0 && j * b - j * (j - 1) / 2 > q) --j;
+    while ((j + 1) * b - (j + 1) * j / 2 <= q) ++j;
+    const long long i = j + (q - (j * b - j * (j - 1) / 2));
+    double* e = blk + i + j * ld;
+    if (dir == 0) packed[q] = *e;
+    else *e = packed[q];
+  }
+}
+}  // namespace
+
+void allgather_segments(Ctx& c, const std::vector<ExSeg>& segs, cudaStream_t s) {
+  if (!c.tp || segs.empty()) return;
+  const int world = c.tp->world, rank = c.tp->rank;
+  std::vector<long long> len(segs.size()), off(world, 0), cnt(world, 0), pos(segs.size());
+  for (size_t k = 0; k < segs.size(); ++k) {
+    const ExSeg& g = segs[k];
+    len[k] = g.kind ? (long long)g.b * (g.b + 1) / 2 : g.n;
+    cnt[g.owner] += len[k];
+  }
+  for (int r = 1; r < world; ++r) off[r] = off[r - 1] + cnt[r - 1];
+  const long long tot = off[world - 1] + cnt[world - 1];
+  if (tot > c.dist.stage_len) {
+    if (c.dist.stage) cudaFree(c.dist.stage);
+    c.dist.stage = nullptr;
+    BDDC_CUDA(cudaMalloc(&c.dist.stage, sizeof(double) * std::max(tot, 1LL)));
+    c.dist.stage_len = tot;
+  }
+  double* st = c.dist.stage;
+  std::vector<long long> fill(off);
+  for (size_t k = 0; k < segs.size(); ++k) pos[k] = fill[segs[k].owner], fill[segs[k].owner] += len[k];
+  auto move = [&](size_t k, int dir) {  // dir 0: segment -> stage, 1: stage -> segment
+    const ExSeg& g = segs[k];
+    if (len[k] == 0) return;
+    if (g.kind == 0) {
+      if (dir == 0) BDDC_CUDA(cudaMemcpyAsync(st + pos[k], g.ptr, sizeof(double) * g.n, cudaMemcpyDeviceToDevice, s));
+      else BDDC_CUDA(cudaMemcpyAsync(g.ptr, st + pos[k], sizeof(double) * g.n, cudaMemcpyDeviceToDevice, s));
+    } else {
+      const int grid = (int)std::min<long long>((len[k] + 255) / 256, 148 * 8);
+      lower_pack_kernel<<<grid, 256, 0, s>>>(g.ptr, g.b, g.ld, st + pos[k], dir);
+      BDDC_LAUNCH_CHECK();
+      BDDC_COUNT();
+    }
+  };
+  for (size_t k = 0; k < segs.size(); ++k)
+    if (segs[k].owner == rank) move(k, 0);
+  c.tp->allgatherv(st, off.data(), cnt.data(), s);
+  for (size_t k = 0; k < segs.size(); ++k)
+    if (segs[k].owner != rank) move(k, 1);
+}
+
 void allreduce_scalars(Ctx& c, double* d, int n, cudaStream_t s) {
   if (c.tp) c.tp->allreduce_sum(d, n, s);
 }

@@ -48,8 +48,18 @@ def _worker(rank, world, port, case):
 
 
 @pytest.mark.parametrize("case,world", [("cfg1_p1_ref", 2), ("cfg3a_p1_ref", 2), ("cfg2a_p1_L4h", 3),
-                                        ("full_p1_2d", 4)])
+                                        ("full_p1_2d", 4), ("cfg3c_p1_ref", 2), ("cfg3c_p1_ref", 4),
+                                        ("cfg4a_p1_spec", 2)])
 def test_sharded_operator_matches_fixtures(cuda_ok, case, world):
+    """Distributed coarse factorization (each rank factors and solves its ND subtrees, the top
+    is replicated: DESIGN.md §9.2) on every case whose tree is deep enough."""
+    mp.spawn(_worker, args=(world, _free_port(), case), nprocs=world, join=True)
+
+
+@pytest.mark.parametrize("case,world", [("cfg3a_p1_ref", 2), ("cfg2a_p1_L4h", 3)])
+def test_sharded_operator_replicated_coarse(cuda_ok, case, world, monkeypatch):
+    """BDDC_DIST_COARSE=0: every rank factors the whole coarse problem (the round-1 path)."""
+    monkeypatch.setenv("BDDC_DIST_COARSE", "0")
     mp.spawn(_worker, args=(world, _free_port(), case), nprocs=world, join=True)
 
 
