@@ -320,6 +320,7 @@ void front_vmm_release(Ctx& c);
 void front_vmm_wait(Ctx& c);  // join the background mapping of the aliased fronts (rethrows)
 bool front_alias_layout(Ctx& c);
 void front_memset(Ctx& c, cudaStream_t s);
+void front_pool_mark_clean(Ctx& c);  // the factorization completed: the alias pool is zero
 
 struct Ctx {
   int device = 0;

@@ -367,6 +367,7 @@ void coarse_assemble_and_factor(Ctx& c) {
   // multifrontal factorization + partitioned inverse: one cooperative launch
   if (!c.dist.on) {
     coop_factor(c, s, 0);
+    front_pool_mark_clean(c);
     return;
   }
   // distributed: this rank's subtrees, the subtree roots' update blocks to
@@ -380,6 +381,7 @@ void coarse_assemble_and_factor(Ctx& c) {
   }
   allgather_segments(c, segs, s);
   coop_factor(c, s, 1);
+  front_pool_mark_clean(c);
 }
 
 void coarse_solve(Ctx& c, const double* rhs, double* sol, cudaStream_t s, const TvArgs* tv) {

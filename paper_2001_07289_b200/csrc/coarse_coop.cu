@@ -73,7 +73,10 @@ struct CoopProgram {
 // (counter >= target) and up to 3 counters it increments when done.
 constexpr int kDeps = 6;
 constexpr int kSigs = 6;
-constexpr int kDfCtasPerSm = 3;  // dataflow: no grid barrier, more CTAs hide tile latency
+#ifndef BDDC_DF_CTAS
+#define BDDC_DF_CTAS 3
+#endif
+constexpr int kDfCtasPerSm = BDDC_DF_CTAS;  // dataflow: no grid barrier, more CTAs hide tile latency
 struct DfTask {
   CoopTask t;
   int dep[kDeps], tgt[kDeps];
@@ -1061,10 +1064,12 @@ void coop_build(Ctx& c) {
       for (int q = 0; q < nctr; ++q)
         if (wptr[q + 1] - wptr[q] > 1) std::sort(wlist.begin() + wptr[q], wlist.begin() + wptr[q + 1]);
       std::vector<int> wpos(wptr.begin(), wptr.end() - 1);
-      auto prio = [&](int a, int b) { return rank[a] < rank[b] || (rank[a] == rank[b] && a > b); };
-      std::priority_queue<int, std::vector<int>, decltype(prio)> ready(prio);
+      // max-heap on (upward rank, then lower index), the keys stored in the heap entries
+      // (no indirect rank[] loads in the comparisons)
+      using Rk = std::pair<double, int>;  // (rank, -index)
+      std::priority_queue<Rk> ready;
       for (size_t i = 0; i < n; ++i)
-        if (!ndep[i]) ready.push((int)i);
+        if (!ndep[i]) ready.push({rank[i], -(int)i});
       using Ev = std::pair<double, int>;  // (finish time, task)
       std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> running;
       std::vector<int> order;
@@ -1073,7 +1078,7 @@ void coop_build(Ctx& c) {
       double now = 0.0;
       while (order.size() < n || !running.empty()) {
         while (free > 0 && !ready.empty()) {
-          const int i = ready.top();
+          const int i = -ready.top().second;
           ready.pop();
           order.push_back(i);
           running.push({now + cst[i], i});
@@ -1092,7 +1097,7 @@ void coop_build(Ctx& c) {
           int& wp = wpos[cix];
           while (wp < wptr[cix + 1] && wlist[wp].first <= cval[cix]) {
             const int j = wlist[wp++].second;
-            if (--ndep[j] == 0) ready.push(j);
+            if (--ndep[j] == 0) ready.push({rank[j], -j});
           }
         }
       }

@@ -76,7 +76,14 @@ struct FrontVmm {
   // run on this thread while the setup builds its schedules; front_vmm_wait joins it
   std::thread worker;
   std::exception_ptr error;
+  // every extend-add zeroes the update entries it consumes, so after a factorization that ran
+  // to completion the pool is all zero again and the next setup need not clear it
+  bool pool_clean = false;
 };
+
+void front_pool_mark_clean(Ctx& c) {
+  if (c.vmm) c.vmm->pool_clean = true;
+}
 
 void front_vmm_wait(Ctx& c) {
   FrontVmm* v = c.vmm;
@@ -319,8 +326,9 @@ bool front_alias_layout(Ctx& c) {
   return true;
 }
 
-// Zero every front (setup start): the persistent pages and the pool, each through its own
-// contiguous view (the aliased virtual range would zero shared pages many times over).
+// Zero every front (setup start): the persistent pages and (unless the last factorization left
+// it clean) the pool, each through its own contiguous view (the aliased virtual range would
+// zero shared pages many times over).
 void front_memset(Ctx& c, cudaStream_t s) {
   front_vmm_wait(c);  // the fronts' physical pages are mapped
   if (!c.vmm) {
@@ -328,7 +336,8 @@ void front_memset(Ctx& c, cudaStream_t s) {
     return;
   }
   BDDC_CUDA(cudaMemsetAsync((void*)c.vmm->pview, 0, c.vmm->p_bytes, s));
-  BDDC_CUDA(cudaMemsetAsync((void*)c.vmm->uview, 0, c.vmm->u_bytes, s));
+  if (!c.vmm->pool_clean) BDDC_CUDA(cudaMemsetAsync((void*)c.vmm->uview, 0, c.vmm->u_bytes, s));
+  c.vmm->pool_clean = false;  // dirty until the factorization completes (front_pool_mark_clean)
 }
 
 }  // namespace bddc
