@@ -49,6 +49,10 @@ enum CoopType : int {
 #define BDDC_KGROUP 8
 #endif
 constexpr int kGroup = BDDC_KGROUP;
+#ifndef BDDC_SYG_BK
+#define BDDC_SYG_BK 16
+#endif
+constexpr int kSygBK = BDDC_SYG_BK;  // K-slice width of the group trailing-update tiles
 __host__ __device__ __forceinline__ int group_k0(int g) { return g * kGroup * kTile; }
 __host__ __device__ __forceinline__ int group_k1(int g, int s) { return min(s, (g + 1) * kGroup * kTile); }
 
@@ -200,8 +204,8 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
       const int k0 = group_k0(t.arg), k1 = group_k1(t.arg, s), rest = f - k1;
       const double* L21 = F + k1 + (long long)k0 * ld;
       double* A22 = F + k1 + (long long)k1 * ld;
-      gemm_tile<false, true, kCoopStages>(L21, ld, L21, ld, A22, ld, rest, rest, k1 - k0, t.a * kTile, t.b * kTile,
-                                          -1.0, 1.0, true, smem);
+      gemm_tile<false, true, kCoopStages, kSygBK>(L21, ld, L21, ld, A22, ld, rest, rest, k1 - k0, t.a * kTile,
+                                                  t.b * kTile, -1.0, 1.0, true, smem);
       if (t.a == 0 && t.b == 0 && k1 < s) {  // the next group's first diagonal tile is final: factor it
         __syncthreads();
         const int p1 = k1 / kTile, nb1 = min(kTile, s - k1);
@@ -791,7 +795,8 @@ void coop_build(Ctx& c) {
   LevelSchedule& ls = c.sched;
   CoopState& st = g_coop[&c];
   st = CoopState{};
-  st.smem_f = sizeof(double) * std::max<int>(gemm_smem_doubles<kCoopStages>(), kFactSmemDoubles);
+  st.smem_f = sizeof(double) * std::max<int>(std::max(gemm_smem_doubles<kCoopStages>(), gemm_smem_doubles<kCoopStages, kSygBK>()),
+                                             kFactSmemDoubles);
   BDDC_CUDA(cudaFuncSetAttribute(coop_factor_df_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st.smem_f));
   int nsm = 0, per_f = 0, per_s = 0;
   BDDC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device));

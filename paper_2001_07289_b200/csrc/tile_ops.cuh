@@ -32,14 +32,15 @@ __device__ __forceinline__ void copy_pair(double* dst, const double* src, int va
   }
 }
 
-// Load a BM x BK slice of op(A) (rows m0.., k0..) into shared memory.
+// Load a BM x BKT slice of op(A) (rows m0.., k0..) into shared memory.
 //   !TA: A(m,k) = A[m + k*lda]  -> sm[k*LDW + m]
-//    TA: A(m,k) = A[k + m*lda]  -> sm[m*LDK + k]
-template <bool TA>
+//    TA: A(m,k) = A[k + m*lda]  -> sm[m*(BKT+4) + k]
+template <bool TA, int BKT = BK>
 __device__ __forceinline__ void load_a(double* sm, const double* A, int lda, int M, int K, int m0,
                                        int k0, int tid, bool al) {
+  constexpr int LDKT = BKT + 4, HK = BKT / 2;
 #pragma unroll
-  for (int it = 0; it < 4; ++it) {
+  for (int it = 0; it < BKT / 4; ++it) {
     int c = tid + it * 128;
     if (!TA) {
       int k = c >> 5, m = (c & 31) * 2;
@@ -48,30 +49,31 @@ __device__ __forceinline__ void load_a(double* sm, const double* A, int lda, int
       const double* src = valid ? A + gm + (long long)gk * lda : A;
       copy_pair(sm + k * LDW + m, src, valid, al);
     } else {
-      int m = c >> 3, k = (c & 7) * 2;
+      int m = c / HK, k = (c % HK) * 2;
       int gm = m0 + m, gk = k0 + k;
       int valid = (gm < M) ? max(0, min(2, K - gk)) : 0;
       const double* src = valid ? A + gk + (long long)gm * lda : A;
-      copy_pair(sm + m * LDK + k, src, valid, al);
+      copy_pair(sm + m * LDKT + k, src, valid, al);
     }
   }
 }
 
-// Load a BK x BN slice of op(B) (k0.., cols n0..).
-//   !TB: B(k,n) = B[k + n*ldb]  -> sm[n*LDK + k]
+// Load a BKT x BN slice of op(B) (k0.., cols n0..).
+//   !TB: B(k,n) = B[k + n*ldb]  -> sm[n*(BKT+4) + k]
 //    TB: B(k,n) = B[n + k*ldb]  -> sm[k*LDW + n]
-template <bool TB>
+template <bool TB, int BKT = BK>
 __device__ __forceinline__ void load_b(double* sm, const double* B, int ldb, int N, int K, int n0,
                                        int k0, int tid, bool al) {
+  constexpr int LDKT = BKT + 4, HK = BKT / 2;
 #pragma unroll
-  for (int it = 0; it < 4; ++it) {
+  for (int it = 0; it < BKT / 4; ++it) {
     int c = tid + it * 128;
     if (!TB) {
-      int n = c >> 3, k = (c & 7) * 2;
+      int n = c / HK, k = (c % HK) * 2;
       int gn = n0 + n, gk = k0 + k;
       int valid = (gn < N) ? max(0, min(2, K - gk)) : 0;
       const double* src = valid ? B + gk + (long long)gn * ldb : B;
-      copy_pair(sm + n * LDK + k, src, valid, al);
+      copy_pair(sm + n * LDKT + k, src, valid, al);
     } else {
       int k = c >> 5, n = (c & 31) * 2;
       int gn = n0 + n, gk = k0 + k;
@@ -82,10 +84,12 @@ __device__ __forceinline__ void load_b(double* sm, const double* B, int ldb, int
   }
 }
 
+template <int BKT>
+constexpr int tile_doubles() { return BKT * LDW > BM * (BKT + 4) ? BKT * LDW : BM * (BKT + 4); }
 
 constexpr int kGemmSmemDoubles = 4 * TILE_A;  // As[2] + Bs[2]
-template <int NS>
-constexpr int gemm_smem_doubles() { return 2 * NS * TILE_A; }
+template <int NS, int BKT = BK>
+constexpr int gemm_smem_doubles() { return 2 * NS * tile_doubles<BKT>(); }
 
 // One 64x64 output tile (rows m0.., cols n0..) of C = alpha op(A) op(B) + beta C over the
 // full K range; 128 threads (4 warps, 2x2), DMMA.8x8x4 accumulators, NS-stage cp.async
@@ -93,7 +97,7 @@ constexpr int gemm_smem_doubles() { return 2 * NS * TILE_A; }
 // lower: only entries with row >= col are written.
 // k_lo / k_hi (multiples of BK or K): the nonzero K range of this tile (triangular operands);
 // mirror (with lower): also write C(c, r) = C(r, c) (symmetric result).
-template <bool TA, bool TB, int NS = 2>
+template <bool TA, bool TB, int NS = 2, int BKT = BK>
 __device__ __forceinline__ void gemm_tile(const double* A, int lda, const double* B, int ldb,
                                           double* C, int ldc, int M, int N, int K, int m0, int n0,
                                           double alpha, double beta, bool lower, double* smem,
@@ -107,18 +111,19 @@ __device__ __forceinline__ void gemm_tile(const double* A, int lda, const double
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  const int kb0 = k_lo / BK;
-  const int nk = ((k_hi < 0 ? K : min(K, k_hi)) + BK - 1) / BK - kb0;
+  constexpr int LDKT = BKT + 4, TILE = tile_doubles<BKT>();
+  const int kb0 = k_lo / BKT;
+  const int nk = ((k_hi < 0 ? K : min(K, k_hi)) + BKT - 1) / BKT - kb0;
   const bool al_a = ((((unsigned long long)A) & 15) == 0) && ((lda & 1) == 0);
   const bool al_b = ((((unsigned long long)B) & 15) == 0) && ((ldb & 1) == 0);
-  auto As = [&](int st) { return smem + st * TILE_A; };
-  auto Bs = [&](int st) { return smem + (NS + st) * TILE_A; };
+  auto As = [&](int st) { return smem + st * TILE; };
+  auto Bs = [&](int st) { return smem + (NS + st) * TILE; };
   // prologue: slices 0 .. NS-2
 #pragma unroll
   for (int p = 0; p < NS - 1; ++p) {
     if (p < nk) {
-      load_a<TA>(As(p), A, lda, M, K, m0, (kb0 + p) * BK, tid, al_a);
-      load_b<TB>(Bs(p), B, ldb, N, K, n0, (kb0 + p) * BK, tid, al_b);
+      load_a<TA, BKT>(As(p), A, lda, M, K, m0, (kb0 + p) * BKT, tid, al_a);
+      load_b<TB, BKT>(Bs(p), B, ldb, N, K, n0, (kb0 + p) * BKT, tid, al_b);
     }
     cp_async_commit();  // empty groups keep the group count uniform
   }
@@ -126,8 +131,8 @@ __device__ __forceinline__ void gemm_tile(const double* A, int lda, const double
     const int st = kt % NS;
     const int pf = kt + NS - 1;  // slice to prefetch into the stage freed last iteration
     if (pf < nk) {
-      load_a<TA>(As(pf % NS), A, lda, M, K, m0, (kb0 + pf) * BK, tid, al_a);
-      load_b<TB>(Bs(pf % NS), B, ldb, N, K, n0, (kb0 + pf) * BK, tid, al_b);
+      load_a<TA, BKT>(As(pf % NS), A, lda, M, K, m0, (kb0 + pf) * BKT, tid, al_a);
+      load_b<TB, BKT>(Bs(pf % NS), B, ldb, N, K, n0, (kb0 + pf) * BKT, tid, al_b);
     }
     cp_async_commit();
     cp_async_wait<NS - 1>();  // slice kt has landed
@@ -135,17 +140,17 @@ __device__ __forceinline__ void gemm_tile(const double* A, int lda, const double
     const double* as = As(st);
     const double* bs = Bs(st);
 #pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
+    for (int kk = 0; kk < BKT; kk += 4) {
       double af[4], bf[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         int m = wm * 32 + i * 8 + g;
-        af[i] = TA ? as[m * LDK + kk + q] : as[(kk + q) * LDW + m];
+        af[i] = TA ? as[m * LDKT + kk + q] : as[(kk + q) * LDW + m];
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         int n = wn * 32 + j * 8 + g;
-        bf[j] = TB ? bs[(kk + q) * LDW + n] : bs[n * LDK + kk + q];
+        bf[j] = TB ? bs[(kk + q) * LDW + n] : bs[n * LDKT + kk + q];
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
