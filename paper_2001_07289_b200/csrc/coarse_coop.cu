@@ -29,7 +29,14 @@ namespace cg = cooperative_groups;
 
 namespace bddc {
 
-constexpr int kX1Chunk = 64;
+#ifndef BDDC_X1_CHUNK
+#define BDDC_X1_CHUNK 256
+#endif
+// K width of one X1 task (a multiple of 64): X[p, c] = -inv_pp sum_m L[p, m] X[m, c] is split
+// into chunks of kX1Chunk / 64 panel blocks m; X2 sums the chunk partials (fewer, longer X1
+// tasks: 4x less partial traffic than one panel block per task)
+constexpr int kX1Chunk = BDDC_X1_CHUNK;
+constexpr int kX1Blocks = kX1Chunk / 64;
 constexpr int kCoopStages = 2;  // cp.async depth of the engine GEMM tiles: 41 KB smem leaves more L1 (measured: 3 stages and 4 CTAs/SM are slower)
 
 enum CoopType : int {
@@ -969,21 +976,23 @@ void coop_build(Ctx& c) {
         // ---- X = L11^{-1} in place over L11, after the whole factorization of this front
         // (every TS / SY / SYG read of L11 is then done) ----
         for (int p = 0; p < np; ++p) {
+          int nx1 = 0;  // X1 tasks of row p
           for (int cc = 0; cc < p; ++cc)
-            for (int qq = 0; qq < p - cc; ++qq) {  // kX1Chunk = 64: chunk qq is column block m
-              const int m = cc + qq;
+            for (int qq = 0; qq * kX1Blocks < p - cc; ++qq) {  // chunk qq: panel blocks m0 .. m1 - 1
+              const int m0 = cc + qq * kX1Blocks, m1 = std::min(p, m0 + kX1Blocks);
               DfTask t = mk(CT_X1, nd, cc, qq, p);
-              dep(t, c_tsr[nd] + m * T + (p - m - 1), 1);
-              dep(t, c_x2[nd] + m * np + cc, 1);
+              for (int m = m0; m < m1; ++m) dep(t, c_tsr[nd] + m * T + (p - m - 1), 1);  // L[p, m] final
+              dep(t, c_x2col[nd] + cc, m1 - cc);  // X[m, cc] final for m < m1 (column cc finishes in m order)
               if (p >= 2) dep(t, c_x2row[nd] + p - 2, p - 1);
               sig(t, c_x1[nd] + p);
               dt.push_back(t);
+              ++nx1;
             }
           for (int cc = 0; cc <= p; ++cc) {
             DfTask t = mk(CT_X2, nd, cc, 0, p);
             dep(t, c_pt[nd] + p, 1);
             dep(t, c_syall[nd], tot_sy[nd]);
-            if (cc < p) dep(t, c_x1[nd] + p, p * (p + 1) / 2);  // every X1 of row p read L[p, .]
+            if (cc < p) dep(t, c_x1[nd] + p, nx1);  // every X1 of row p read L[p, .]
             sig(t, c_x2[nd] + p * np + cc);
             sig(t, c_x2row[nd] + p);
             sig(t, c_x2col[nd] + cc);
@@ -1025,7 +1034,7 @@ void coop_build(Ctx& c) {
           case CT_EA: return 2.5 + 0.15 * q.b;
           case CT_PT: return 15.0;
           case CT_TS: return 6.5;
-          case CT_X1: return 8.5;
+          case CT_X1: return 8.5 * kX1Blocks;
           case CT_SY: {
             const int k = q.arg * kTile;
             return (q.a == 0 && q.b == 0 && k + kTile < s) ? 10.7 + 15.0 : 10.7;  // + lookahead PT
