@@ -150,6 +150,7 @@ struct FrontDev {
   int* bnd_idx = nullptr;       // per node: boundary dofs (elimination order)
   int* bnd_ptr = nullptr;
   unsigned char* ualias = nullptr;  // per node: update columns on shared pool pages (front_vmm.cu)
+  int* grp = nullptr;               // per node: panels per group of the dataflow factorization
 };
 
 // Coarse multifrontal plan (device data + host schedule).

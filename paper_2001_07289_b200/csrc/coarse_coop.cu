@@ -60,8 +60,12 @@ constexpr int kGroup = BDDC_KGROUP;
 #define BDDC_SYG_BK 16
 #endif
 constexpr int kSygBK = BDDC_SYG_BK;  // K-slice width of the group trailing-update tiles
-__host__ __device__ __forceinline__ int group_k0(int g) { return g * kGroup * kTile; }
-__host__ __device__ __forceinline__ int group_k1(int g, int s) { return min(s, (g + 1) * kGroup * kTile); }
+// group size per front (FrontDev::grp): kGroup panels, or 1 (the per-panel right-looking update
+// with lookahead) for separators below BDDC_GROUP_MIN_SEP (default 0: groups everywhere; 512 /
+// 1024 / 2048 / 4096 measured slower on cfg5, cfg3 and cfg2 L=h, 4% faster on cfg2 L=4h only:
+// tools/gpu_ab8.sh)
+__host__ __device__ __forceinline__ int group_k0(int g, int G) { return g * G * kTile; }
+__host__ __device__ __forceinline__ int group_k1(int g, int G, int s) { return min(s, (g + 1) * G * kTile); }
 
 struct CoopTask {
   int type, node, a, b, arg;
@@ -193,7 +197,8 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
     case CT_SY: {  // tile (a, b) of the panel's trailing matrix INSIDE its group's block column
       // (columns < group_k1) -= L21 L21^T; tile (0,0) + lookahead:
       const int k = t.arg * kTile, nb = min(kTile, s - k), rest = f - k - nb;
-      const int ncols = group_k1(t.arg / kGroup, s) - (k + nb);
+      const int G = fd.grp[node];
+      const int ncols = group_k1(t.arg / G, G, s) - (k + nb);
       double* L21 = F + (k + nb) + (long long)k * ld;
       double* A22 = F + (k + nb) + (long long)(k + nb) * ld;
       gemm_tile<false, true, kCoopStages>(L21, ld, L21, ld, A22, ld, rest, ncols, nb, t.a * kTile, t.b * kTile,
@@ -208,7 +213,8 @@ __device__ void run_task(const CoopTask& t, const FrontDev& fd, const CoopProgra
       break;
     }
     case CT_SYG: {  // trailing tile (a, b) beyond group arg's block column -= L21 L21^T, K = group
-      const int k0 = group_k0(t.arg), k1 = group_k1(t.arg, s), rest = f - k1;
+      const int G = fd.grp[node];
+      const int k0 = group_k0(t.arg, G), k1 = group_k1(t.arg, G, s), rest = f - k1;
       const double* L21 = F + k1 + (long long)k0 * ld;
       double* A22 = F + k1 + (long long)k1 * ld;
       gemm_tile<false, true, kCoopStages, kSygBK>(L21, ld, L21, ld, A22, ld, rest, rest, k1 - k0, t.a * kTile,
@@ -818,6 +824,14 @@ void coop_build(Ctx& c) {
   long long pool = 2;
   int max_children = 0;
   for (int nd = 0; nd < N; ++nd) max_children = std::max(max_children, fp.child_ptr[nd + 1] - fp.child_ptr[nd]);
+  std::vector<int> grp(N, kGroup);
+  {
+    const char* e = getenv("BDDC_GROUP_MIN_SEP");
+    const int gmin = e ? atoi(e) : 0;
+    for (int nd = 0; nd < N; ++nd)
+      if (fp.sep_size[nd] < gmin) grp[nd] = 1;
+    c.fp.d.grp = c.upload(grp.data(), N);
+  }
   // ---- dataflow factorization program ----
   HostTimer ht;
   {
@@ -830,7 +844,7 @@ void coop_build(Ctx& c) {
     std::vector<std::vector<int>> nea(N);
     for (int nd = 0; nd < N; ++nd) {
       const int s = fp.sep_size[nd], f = s + fp.bnd_size[nd];
-      const int T = ceil_div(std::max(f, 1), kTile), np = ceil_div(s, kTile), ng = ceil_div(s, kGroup * kTile);
+      const int T = ceil_div(std::max(f, 1), kTile), np = ceil_div(s, kTile), ng = ceil_div(s, grp[nd] * kTile);
       nT[nd] = T; nP[nd] = np;
       c_ea[nd] = newc(std::max(1, fp.child_ptr[nd + 1] - fp.child_ptr[nd]));
       c_syall[nd] = newc(1); c_tsall[nd] = newc(1); c_w[nd] = newc(1); c_x2all[nd] = newc(1);
@@ -927,9 +941,10 @@ void coop_build(Ctx& c) {
               if (I >= J) dep(t, upd(nd, I, J), p);
         };
         // ---- factorization: panels in groups of kGroup ----
-        const int ng = ceil_div(s, kGroup * kTile);
+        const int Gn = grp[nd];
+        const int ng = ceil_div(s, Gn * kTile);
         for (int g = 0; g < ng; ++g) {
-          const int k0 = group_k0(g), k1 = group_k1(g, s), p0 = k0 / kTile, p1 = ceil_div(k1, kTile);
+          const int k0 = group_k0(g, Gn), k1 = group_k1(g, Gn, s), p0 = k0 / kTile, p1 = ceil_div(k1, kTile);
           int gts = 0;  // TS tasks of this group
           for (int p = p0; p < p1; ++p) {
             const int k = p * kTile, nb = std::min(kTile, s - k), rest = f - k - nb, nt = ceil_div(rest, kTile);
@@ -981,7 +996,10 @@ void coop_build(Ctx& c) {
             for (int qq = 0; qq * kX1Blocks < p - cc; ++qq) {  // chunk qq: panel blocks m0 .. m1 - 1
               const int m0 = cc + qq * kX1Blocks, m1 = std::min(p, m0 + kX1Blocks);
               DfTask t = mk(CT_X1, nd, cc, qq, p);
-              for (int m = m0; m < m1; ++m) dep(t, c_tsr[nd] + m * T + (p - m - 1), 1);  // L[p, m] final
+              if (kX1Blocks <= 4)
+                for (int m = m0; m < m1; ++m) dep(t, c_tsr[nd] + m * T + (p - m - 1), 1);  // L[p, m] final
+              else
+                dep(t, c_tsall[nd], tot_ts[nd]);  // (wider chunks: every L21 panel of the front final)
               dep(t, c_x2col[nd] + cc, m1 - cc);  // X[m, cc] final for m < m1 (column cc finishes in m order)
               if (p >= 2) dep(t, c_x2row[nd] + p - 2, p - 1);
               sig(t, c_x1[nd] + p);
@@ -1040,7 +1058,7 @@ void coop_build(Ctx& c) {
             return (q.a == 0 && q.b == 0 && k + kTile < s) ? 10.7 + 15.0 : 10.7;  // + lookahead PT
           }
           case CT_SYG: {
-            const int k0 = group_k0(q.arg), k1 = group_k1(q.arg, s);
+            const int k0 = group_k0(q.arg, grp[q.node]), k1 = group_k1(q.arg, grp[q.node], s);
             const double run = 4.0 + 6.7 * (k1 - k0) / 64.0;
             return (q.a == 0 && q.b == 0 && k1 < s) ? run + 15.0 : run;
           }
