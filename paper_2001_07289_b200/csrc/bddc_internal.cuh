@@ -370,6 +370,7 @@ struct Ctx {
   double *r = nullptr, *z = nullptr, *p = nullptr, *Ap = nullptr;
   double *bbuf = nullptr, *xbuf = nullptr;  // host-facing PCG staging
   double* red = nullptr;     // reduction partials
+  unsigned* redc = nullptr;  // arrival counter of the one-launch grid reductions (pcg.cu)
   double* scal = nullptr;    // device scalars
   double* h_scal = nullptr;  // pinned host mirror
   // multi-GPU: slab of this rank and the exchange transport (null: single rank)

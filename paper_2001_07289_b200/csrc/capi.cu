@@ -450,6 +450,8 @@ void do_setup(bddc_ctx* h, const bddc_setup_desc* d) {
   c.bbuf = c.alloc<double>(G.n);
   c.xbuf = c.alloc<double>(G.n);
   c.red = c.alloc<double>(4096);
+  c.redc = c.alloc<unsigned>(1);
+  BDDC_CUDA(cudaMemsetAsync(c.redc, 0, sizeof(unsigned), c.stream));
   c.scal = c.alloc<double>(16);
   BDDC_CUDA(cudaMemsetAsync(c.scal, 0, 16 * sizeof(double), c.stream));
   // setup workspace: all subdomains at once if it fits in ~60% of the free memory

@@ -1,6 +1,7 @@
 // Device PCG (krylov.py:31-92): x0 = 0, recurrence residual, stop at ||r|| <= tol ||b||.
-// SpMV is fused with <p, Ap>; the x / r update is fused with ||r||^2; all reductions are
-// two-pass over a fixed grid, hence deterministic. One host synchronisation per
+// SpMV is fused with <p, Ap>; the x / r update is fused with ||r||^2; every reduction is one
+// launch (block partials over a fixed grid, summed in fixed order by the last block to
+// finish), hence deterministic; rz <- rz_new rides on the p update. One host synchronisation per
 // iteration reads {rz, pAp, rr} for the stopping test, the SPD guards and the Lanczos
 // coefficients (alpha_k, beta_k).
 #include "stencil.cuh"
@@ -24,34 +25,49 @@ __device__ __forceinline__ void block_partial(double v, double* partial) {
   }
 }
 
+// The block partials of a grid reduction, then the grid total written by the LAST block to
+// finish (arrival counter, reset by that block): partial i summed by thread i mod 256 in index
+// order, then a fixed warp / block tree (deterministic), without a separate final launch.
+__device__ __forceinline__ void grid_total(double v, double* partial, unsigned* cnt, double* out) {
+  block_partial(v, partial);
+  __shared__ bool last;
+  __shared__ double red2[kRedThreads / 32];
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(cnt, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) acc += __ldcg(partial + i);
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red2[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < kRedThreads / 32; ++i) t += red2[i];
+    *out = t;
+    *cnt = 0u;
+  }
+}
+
 __global__ void __launch_bounds__(kRedThreads) dot_partial_kernel(const double* __restrict__ a,
                                                                   const double* __restrict__ b,
-                                                                  long long n, double* partial) {
+                                                                  long long n, double* partial, unsigned* cnt,
+                                                                  double* out) {
   double acc = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     acc += a[i] * b[i];
-  block_partial(acc, partial);
-}
-
-__global__ void reduce_final_kernel(const double* __restrict__ partial, int np, double* out) {
-  __shared__ double red[32];
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < np; i += blockDim.x) acc += partial[i];
-  acc = warp_sum(acc);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
-    *out = s;
-  }
+  grid_total(acc, partial, cnt, out);
 }
 
 template <int DIM>
 __global__ void __launch_bounds__(kRedThreads) spmv_dot_kernel(Geometry G, const double* __restrict__ alpha,
                                                                const double* __restrict__ p,
-                                                               double* __restrict__ Ap, double* partial) {
+                                                               double* __restrict__ Ap, double* partial,
+                                                               unsigned* cnt, double* out) {
   double acc = 0.0;
   for (long long f = G.f_lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; f < G.f_hi;
        f += (long long)gridDim.x * blockDim.x) {
@@ -61,7 +77,7 @@ __global__ void __launch_bounds__(kRedThreads) spmv_dot_kernel(Geometry G, const
     Ap[f] = v;
     if (f >= G.fo_lo) acc += p[f] * v;  // dot over owned rows (fo_hi == f_hi)
   }
-  block_partial(acc, partial);
+  grid_total(acc, partial, cnt, out);
 }
 
 // alpha = rz / pAp; x += alpha p; r -= alpha Ap; partial ||r||^2
@@ -70,7 +86,7 @@ __global__ void __launch_bounds__(kRedThreads) update_xr_kernel(double* __restri
                                                                 const double* __restrict__ Ap,
                                                                 const double* __restrict__ scal,
                                                                 long long lo, long long hi, long long own_lo,
-                                                                double* partial) {
+                                                                double* partial, unsigned* cnt, double* out) {
   const double a = scal[0] / scal[1];
   double acc = 0.0;
   for (long long i = lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < hi;
@@ -80,19 +96,25 @@ __global__ void __launch_bounds__(kRedThreads) update_xr_kernel(double* __restri
     r[i] = ri;
     if (i >= own_lo) acc += ri * ri;
   }
-  block_partial(acc, partial);
+  grid_total(acc, partial, cnt, out);
 }
 
-// beta = rz_new / rz; p = z + beta p
-__global__ void xpay_kernel(double* __restrict__ p, const double* __restrict__ z,
-                            const double* __restrict__ scal, long long lo, long long n) {
-  const double b = scal[3] / scal[0];
+// beta = rz_new / rz; p = z + beta p; then (last block) rz <- rz_new for the next iteration
+__global__ void xpay_kernel(double* __restrict__ p, const double* __restrict__ z, double* scal, long long lo,
+                            long long n, unsigned* cnt) {
+  const double b = scal[3] / scal[0];  // every block reads both before the last one rewrites scal[0]
   for (long long i = lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     p[i] = z[i] + b * p[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(cnt, 1u) == gridDim.x - 1) {
+      scal[0] = scal[3];
+      *cnt = 0u;
+    }
+  }
 }
-
-__global__ void copy_scalar_kernel(double* dst, const double* src) { *dst = *src; }
 
 }  // namespace
 
@@ -100,8 +122,8 @@ __global__ void copy_scalar_kernel(double* dst, const double* src) { *dst = *src
 double dot(Ctx& c, const double* a, const double* b, long long n, cudaStream_t s) {
   const Geometry& G = c.geo;
   (void)n;
-  { dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(a + G.fo_lo, b + G.fo_lo, G.fo_hi - G.fo_lo, c.red); BDDC_COUNT(); }
-  { reduce_final_kernel<<<1, 1024, 0, s>>>(c.red, kRedBlocks, c.scal + 7); BDDC_COUNT(); }
+  { dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(a + G.fo_lo, b + G.fo_lo, G.fo_hi - G.fo_lo, c.red, c.redc,
+                                                          c.scal + 7); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
   allreduce_scalars(c, c.scal + 7, 1, s);
   BDDC_CUDA(cudaMemcpyAsync(c.h_scal + 7, c.scal + 7, sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -112,8 +134,8 @@ double dot(Ctx& c, const double* a, const double* b, long long n, cudaStream_t s
 static void dot_to(Ctx& c, const double* a, const double* b, long long n, double* out, cudaStream_t s) {
   const Geometry& G = c.geo;
   (void)n;
-  { dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(a + G.fo_lo, b + G.fo_lo, G.fo_hi - G.fo_lo, c.red); BDDC_COUNT(); }
-  { reduce_final_kernel<<<1, 1024, 0, s>>>(c.red, kRedBlocks, out); BDDC_COUNT(); }
+  { dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(a + G.fo_lo, b + G.fo_lo, G.fo_hi - G.fo_lo, c.red, c.redc,
+                                                          out); BDDC_COUNT(); }
   BDDC_LAUNCH_CHECK();
 }
 
@@ -149,13 +171,12 @@ static PcgResult pcg_run(Ctx& c, const double* b, double* x, double tol, int max
   for (int it = 0; it < max_iters; ++it) {
     exchange_dof_halo(c, c.p, s);  // sharded: p on the rows next to the cut lines
     c.prof.begin("pcg.spmv_dot", s);
-    if (G.dim == 2) { spmv_dot_kernel<2><<<kRedBlocks, kRedThreads, 0, s>>>(G, c.alpha, c.p, c.Ap, c.red); BDDC_COUNT(); }
-    else { spmv_dot_kernel<3><<<kRedBlocks, kRedThreads, 0, s>>>(G, c.alpha, c.p, c.Ap, c.red); BDDC_COUNT(); }
-    { reduce_final_kernel<<<1, 1024, 0, s>>>(c.red, kRedBlocks, sc + 1); BDDC_COUNT(); }
+    if (G.dim == 2) { spmv_dot_kernel<2><<<kRedBlocks, kRedThreads, 0, s>>>(G, c.alpha, c.p, c.Ap, c.red, c.redc, sc + 1); BDDC_COUNT(); }
+    else { spmv_dot_kernel<3><<<kRedBlocks, kRedThreads, 0, s>>>(G, c.alpha, c.p, c.Ap, c.red, c.redc, sc + 1); BDDC_COUNT(); }
     c.prof.end("pcg.spmv_dot", s);
     allreduce_scalars(c, sc + 1, 1, s);
-    { update_xr_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(x, c.r, c.p, c.Ap, sc, G.f_lo, G.f_hi, G.fo_lo, c.red); BDDC_COUNT(); }
-    { reduce_final_kernel<<<1, 1024, 0, s>>>(c.red, kRedBlocks, sc + 2); BDDC_COUNT(); }
+    { update_xr_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(x, c.r, c.p, c.Ap, sc, G.f_lo, G.f_hi, G.fo_lo, c.red,
+                                                         c.redc, sc + 2); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
     allreduce_scalars(c, sc + 2, 1, s);
     BDDC_CUDA(cudaMemcpyAsync(hs, sc, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
@@ -199,8 +220,7 @@ static PcgResult pcg_run(Ctx& c, const double* b, double* x, double tol, int max
     apply_bddc(c, c.r, c.z, s);
     dot_to(c, c.r, c.z, n, sc + 3, s);
     allreduce_scalars(c, sc + 3, 1, s);
-    { xpay_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(c.p, c.z, sc, G.f_lo, G.f_hi); BDDC_COUNT(); }
-    { copy_scalar_kernel<<<1, 1, 0, s>>>(sc + 0, sc + 3); BDDC_COUNT(); }
+    { xpay_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(c.p, c.z, sc, G.f_lo, G.f_hi, c.redc); BDDC_COUNT(); }
     BDDC_LAUNCH_CHECK();
   }
   return res;
