@@ -68,6 +68,18 @@ def _trsm(torch, kind: int, L, n: int, ld: int, B, nrhs: int, ldb: int):
         raise RuntimeError(f"bddc_dense_trsm failed ({rc})")
 
 
+def _gemm(torch, tA: bool, tB: bool, M: int, N: int, K: int, alpha: float, A, lda: int, B, ldb: int,
+          beta: float, Cm, ldc: int):
+    """C = alpha op(A) op(B) + beta C on column-major device tensors (this library's DMMA GEMM)."""
+    lib = _capi.load()
+    stream = torch.cuda.current_stream().cuda_stream
+    rc = lib.bddc_dense_gemm(int(tA), int(tB), M, N, K, float(alpha), C.c_void_p(A.data_ptr()), lda, 0,
+                             C.c_void_p(B.data_ptr()), ldb, 0, float(beta), C.c_void_p(Cm.data_ptr()),
+                             ldc, 0, 1, C.c_void_p(stream))
+    if rc:
+        raise RuntimeError(f"bddc_dense_gemm failed ({rc})")
+
+
 class SpdFactorization:
     """Cholesky factor of an SPD matrix on the GPU (linalg.py:101-114)."""
 
@@ -114,8 +126,8 @@ class SaddleFactorization:
     """[[A, C^T], [C, 0]] through K = A + s C^T C and S = C K^{-1} C^T (linalg.py:145-172)."""
 
     def __init__(self, K: SpdFactorization, Cd: np.ndarray, s: float, S: SpdFactorization | None,
-                 Gt):
-        self._K, self._C, self._s, self._S, self._Gt = K, Cd, s, S, Gt
+                 G):
+        self._K, self._C, self._s, self._S, self._G = K, Cd, s, S, G
         self.n, self.m = K.n, Cd.shape[0]
 
     def solve(self, f: np.ndarray, g: np.ndarray):
@@ -135,16 +147,17 @@ class SaddleFactorization:
         # h = L^{-1} (f + s C^T g'), lambda = S^{-1} (G^T h - g'), u = L^{-T} (h - G lambda)
         H = _colmajor(torch, F + s * (Cd.T @ gp), self._K._ld)
         _trsm(torch, 0, self._K._L, self.n, self._K._ld, H, nrhs, self._K._ld)
-        Gt = self._Gt  # (m x n) = (L^{-1} C^T)^T on device
-        h = H[:nrhs, :self.n].T  # n x nrhs
-        rhs_l = (Gt @ h).cpu().numpy() - gp
+        G = self._G  # column-major n x m: L^{-1} C^T
+        ld, m, n = self._K._ld, self.m, self.n
+        ldm = m + (m & 1)
+        R = torch.zeros((nrhs, ldm), dtype=torch.float64, device="cuda")
+        _gemm(torch, True, False, m, nrhs, n, 1.0, G, ld, H, ld, 0.0, R, ldm)  # G^T h
+        rhs_l = R[:, :m].T.cpu().numpy() - gp
         lam_true = self._S.solve(rhs_l.reshape((self.m,) + g.shape[1:])).reshape(self.m, -1)
-        lt = torch.from_numpy(np.ascontiguousarray(lam_true)).cuda()
-        Y = (h - Gt.T @ lt).T.contiguous()  # nrhs x n (column-major n x nrhs)
-        Yb = torch.zeros((nrhs, self._K._ld), dtype=torch.float64, device="cuda")
-        Yb[:, :self.n] = Y
-        _trsm(torch, 1, self._K._L, self.n, self._K._ld, Yb, nrhs, self._K._ld)
-        u = Yb[:, :self.n].T.cpu().numpy().reshape(f.shape)
+        Lt = _colmajor(torch, lam_true, ldm)
+        _gemm(torch, False, False, n, nrhs, m, -1.0, G, ld, Lt, ldm, 1.0, H, ld)  # h - G lambda
+        _trsm(torch, 1, self._K._L, self.n, self._K._ld, H, nrhs, self._K._ld)
+        u = H[:nrhs, :self.n].T.cpu().numpy().reshape(f.shape)
         lam = (lam_true / (s * s)).reshape((self.m,) + g.shape[1:])
         return u, lam
 
@@ -169,13 +182,16 @@ def saddle_factor(A, C) -> SaddleFactorization:
         return SaddleFactorization(K, Cd, 1.0, None, None)
     G = _colmajor(torch, Cd.T, K._ld)  # C^T, n x m
     _trsm(torch, 0, K._L, n, K._ld, G, m, K._ld)
-    Gt = G[:m, :n]  # rows = columns of L^{-1} C^T
-    S = (Gt @ Gt.T).cpu().numpy()
+    ldm = m + (m & 1)
+    Sd = torch.zeros((m, ldm), dtype=torch.float64, device="cuda")
+    _gemm(torch, True, False, m, m, n, 1.0, G, K._ld, G, K._ld, 0.0, Sd, ldm)  # S = G^T G
+    S = Sd[:, :m].cpu().numpy()
+    S = 0.5 * (S + S.T)
     try:
         Sf = spd_factor(S)
     except NotSpdError as err:
         raise UnderconstrainedError(msg) from err
-    return SaddleFactorization(K, Cd, s, Sf, Gt.contiguous())
+    return SaddleFactorization(K, Cd, s, Sf, G)
 
 
 def saddle_solve(fact: SaddleFactorization, f: np.ndarray, g: np.ndarray):

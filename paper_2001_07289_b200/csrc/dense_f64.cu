@@ -30,7 +30,14 @@ __device__ __forceinline__ TaskView gemm_task(const GemmArgs& a, int b) {
                   a.lda,          a.ldb,          a.ldc};
 }
 
-constexpr int kGemmStages = 2;
+#ifndef BDDC_GEMM_STAGES
+#define BDDC_GEMM_STAGES 2
+#endif
+#ifndef BDDC_GEMM_PRED
+#define BDDC_GEMM_PRED 1
+#endif
+constexpr int kGemmStages = BDDC_GEMM_STAGES;
+constexpr bool kGemmPred = BDDC_GEMM_PRED != 0;
 
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(128) gemm_f64_kernel(GemmArgs args) {
@@ -51,7 +58,7 @@ __global__ void __launch_bounds__(128) gemm_f64_kernel(GemmArgs args) {
     default: break;
   }
   if (args.klo_on) k_lo = max(k_lo, args.klo[tm]);
-  gemm_tile<TA, TB, kGemmStages>(t.A, t.lda, t.B, t.ldb, t.C, t.ldc, t.M, t.N, t.K, m0, n0, args.alpha,
+  gemm_tile<TA, TB, kGemmStages, BK, kGemmPred>(t.A, t.lda, t.B, t.ldb, t.C, t.ldc, t.M, t.N, t.K, m0, n0, args.alpha,
                                  args.beta, args.lower != 0, smem, k_lo, k_hi, args.mirror != 0);
 }
 

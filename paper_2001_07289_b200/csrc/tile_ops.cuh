@@ -91,13 +91,41 @@ constexpr int kGemmSmemDoubles = 4 * TILE_A;  // As[2] + Bs[2]
 template <int NS, int BKT = BK>
 constexpr int gemm_smem_doubles() { return 2 * NS * tile_doubles<BKT>(); }
 
+// The DMMAs of one k-slice for the first NI x NJ accumulator blocks of a warp tile.
+template <int NI, int NJ, bool TA, bool TB, int BKT>
+__device__ __forceinline__ void mma_slice(double (&acc)[4][4][2], const double* as, const double* bs,
+                                          int wm, int wn, int g, int q) {
+  constexpr int LDKT = BKT + 4;
+#pragma unroll
+  for (int kk = 0; kk < BKT; kk += 4) {
+    double af[NI], bf[NJ];
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      int m = wm * 32 + i * 8 + g;
+      af[i] = TA ? as[m * LDKT + kk + q] : as[(kk + q) * LDW + m];
+    }
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      int n = wn * 32 + j * 8 + g;
+      bf[j] = TB ? bs[(kk + q) * LDW + n] : bs[n * LDKT + kk + q];
+    }
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+  }
+}
+
 // One 64x64 output tile (rows m0.., cols n0..) of C = alpha op(A) op(B) + beta C over the
 // full K range; 128 threads (4 warps, 2x2), DMMA.8x8x4 accumulators, NS-stage cp.async
 // pipeline (NS - 1 k-slices in flight ahead of the one being multiplied).
 // lower: only entries with row >= col are written.
 // k_lo / k_hi (multiples of BK or K): the nonzero K range of this tile (triangular operands);
 // mirror (with lower): also write C(c, r) = C(r, c) (symmetric result).
-template <bool TA, bool TB, int NS = 2, int BKT = BK>
+// PRED: a warp only issues the DMMAs of its 8-row / 8-column accumulator blocks that reach
+// below row M / column N (ragged sizes: 392 = 6.125 tiles), and none for a warp tile entirely
+// above the diagonal of a lower result.
+template <bool TA, bool TB, int NS = 2, int BKT = BK, bool PRED = false>
 __device__ __forceinline__ void gemm_tile(const double* A, int lda, const double* B, int ldb,
                                           double* C, int ldc, int M, int N, int K, int m0, int n0,
                                           double alpha, double beta, bool lower, double* smem,
@@ -111,6 +139,14 @@ __device__ __forceinline__ void gemm_tile(const double* A, int lda, const double
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  // PRED: number of this warp's 8-row / 8-column accumulator blocks that are written
+  int ni = 4, nj = 4;
+  if (PRED) {
+    ni = max(0, min(4, (M - m0 - wm * 32 + 7) >> 3));
+    nj = max(0, min(4, (N - n0 - wn * 32 + 7) >> 3));
+    if (lower && n0 + wn * 32 > m0 + wm * 32 + 31) ni = 0;  // warp tile above the diagonal
+    if (ni == 0 || nj == 0) ni = nj = 0;
+  }
   constexpr int LDKT = BKT + 4, TILE = tile_doubles<BKT>();
   const int kb0 = k_lo / BKT;
   const int nk = ((k_hi < 0 ? K : min(K, k_hi)) + BKT - 1) / BKT - kb0;
@@ -139,23 +175,18 @@ __device__ __forceinline__ void gemm_tile(const double* A, int lda, const double
     __syncthreads();
     const double* as = As(st);
     const double* bs = Bs(st);
-#pragma unroll
-    for (int kk = 0; kk < BKT; kk += 4) {
-      double af[4], bf[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        int m = wm * 32 + i * 8 + g;
-        af[i] = TA ? as[m * LDKT + kk + q] : as[(kk + q) * LDW + m];
+    if (!PRED) {
+      mma_slice<4, 4, TA, TB, BKT>(acc, as, bs, wm, wn, g, q);
+    } else {
+      switch (ni * 4 + nj - 5) {  // warp-uniform; every case keeps static accumulator indices
+#define BDDC_MMA_CASE(I, J) case (I) * 4 + (J) - 5: mma_slice<I, J, TA, TB, BKT>(acc, as, bs, wm, wn, g, q); break;
+        BDDC_MMA_CASE(1, 1) BDDC_MMA_CASE(1, 2) BDDC_MMA_CASE(1, 3) BDDC_MMA_CASE(1, 4)
+        BDDC_MMA_CASE(2, 1) BDDC_MMA_CASE(2, 2) BDDC_MMA_CASE(2, 3) BDDC_MMA_CASE(2, 4)
+        BDDC_MMA_CASE(3, 1) BDDC_MMA_CASE(3, 2) BDDC_MMA_CASE(3, 3) BDDC_MMA_CASE(3, 4)
+        BDDC_MMA_CASE(4, 1) BDDC_MMA_CASE(4, 2) BDDC_MMA_CASE(4, 3) BDDC_MMA_CASE(4, 4)
+#undef BDDC_MMA_CASE
+        default: break;  // nothing of this warp's tile is written
       }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        int n = wn * 32 + j * 8 + g;
-        bf[j] = TB ? bs[(kk + q) * LDW + n] : bs[n * LDKT + kk + q];
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
     __syncthreads();
   }
