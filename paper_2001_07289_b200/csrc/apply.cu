@@ -14,28 +14,30 @@ namespace bddc {
 
 namespace {
 
-template <int DIM>
-__global__ void spmv_kernel(Geometry G, const double* __restrict__ alpha, const double* __restrict__ x,
-                            double* __restrict__ y) {
-  for (long long f = G.f_lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; f < G.f_hi;
-       f += (long long)gridDim.x * blockDim.x) {
-    int g0, g1, g2;
-    free_coords(G, f, g0, g1, g2);
-    y[f] = stencil_row<DIM>(G, alpha, x, g0, g1, g2);
-  }
+template <int DIM, bool EDGE>
+__global__ void __launch_bounds__(256, (EDGE || DIM == 2) ? 3 : 1) spmv_kernel(Geometry G, const double* __restrict__ alpha,
+                                                   const double* __restrict__ x, double* __restrict__ y) {
+  stencil_sweep<DIM, EDGE>(G, alpha, x, [&](long long f, double v, double) { y[f] = v; });
 }
 
 // y = r - A x (all free dofs)
-template <int DIM>
-__global__ void residual_kernel(Geometry G, const double* __restrict__ alpha, const double* __restrict__ r,
-                                const double* __restrict__ x, double* __restrict__ y) {
-  for (long long f = G.f_lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; f < G.f_hi;
-       f += (long long)gridDim.x * blockDim.x) {
-    int g0, g1, g2;
-    free_coords(G, f, g0, g1, g2);
-    y[f] = r[f] - stencil_row<DIM>(G, alpha, x, g0, g1, g2);
-  }
+template <int DIM, bool EDGE>
+__global__ void __launch_bounds__(256, (EDGE || DIM == 2) ? 3 : 1) residual_kernel(Geometry G, const double* __restrict__ alpha,
+                                                       const double* __restrict__ r, const double* __restrict__ x,
+                                                       double* __restrict__ y) {
+  stencil_sweep<DIM, EDGE>(G, alpha, x, [&](long long f, double v, double) { y[f] = r[f] - v; });
 }
+
+// launch K<DIM, EDGE> over the sweep's work items (columns x row chunks of the active rows)
+#define BDDC_SWEEP_LAUNCH(K, G, s, ...)                                                            \
+  do {                                                                                             \
+    const int th_ = 256, gr_ = grid_for(sweep_items(G), th_);                                      \
+    const bool e_ = stencil_edge_only(G);                                                          \
+    if (G.dim == 2) { if (e_) K<2, true><<<gr_, th_, 0, s>>>(G, __VA_ARGS__); else K<2, false><<<gr_, th_, 0, s>>>(G, __VA_ARGS__); } \
+    else { if (e_) K<3, true><<<gr_, th_, 0, s>>>(G, __VA_ARGS__); else K<3, false><<<gr_, th_, 0, s>>>(G, __VA_ARGS__); } \
+    BDDC_COUNT();                                                                                  \
+    BDDC_LAUNCH_CHECK();                                                                           \
+  } while (0)
 
 // rpg[g] = r - (A u1) at interface dofs
 template <int DIM>
@@ -660,10 +662,7 @@ int grid_for(long long n, int threads) {
 
 void spmv(Ctx& c, const double* x, double* y, cudaStream_t s) {
   const Geometry& G = c.geo;
-  const int th = 256, gr = grid_for(G.f_hi - G.f_lo, th);
-  if (G.dim == 2) { spmv_kernel<2><<<gr, th, 0, s>>>(G, c.alpha, x, y); BDDC_COUNT(); }
-  else { spmv_kernel<3><<<gr, th, 0, s>>>(G, c.alpha, x, y); BDDC_COUNT(); }
-  BDDC_LAUNCH_CHECK();
+  BDDC_SWEEP_LAUNCH(spmv_kernel, G, s, c.alpha, x, y);
 }
 
 static void bt_solve(Ctx& c, const double* in, double* out, cudaStream_t s) {
@@ -691,10 +690,7 @@ static void bt_solve(Ctx& c, const double* in, double* out, cudaStream_t s) {
 // out holds g on Gamma and 0 on interiors; c.v1 must be zero.
 void harmonic_interior(Ctx& c, double* out, cudaStream_t s) {
   const Geometry& G = c.geo;
-  const int th = 256, gr = grid_for(G.f_hi - G.f_lo, th);
-  if (G.dim == 2) { residual_kernel<2><<<gr, th, 0, s>>>(G, c.alpha, c.v1, out, c.v2); BDDC_COUNT(); }
-  else { residual_kernel<3><<<gr, th, 0, s>>>(G, c.alpha, c.v1, out, c.v2); BDDC_COUNT(); }
-  BDDC_LAUNCH_CHECK();
+  BDDC_SWEEP_LAUNCH(residual_kernel, G, s, c.alpha, c.v1, out, c.v2);
   bt_solve(c, c.v2, out, s);
 }
 
@@ -753,10 +749,7 @@ void apply_bddc(Ctx& c, const double* r, double* z, cudaStream_t s) {
     BDDC_LAUNCH_CHECK();
   }
   // z_I = A_II^{-1} (r - A z_Gamma)_I
-  const int gr = grid_for(G.f_hi - G.f_lo, th);
-  if (G.dim == 2) { residual_kernel<2><<<gr, th, 0, s>>>(G, c.alpha, r, z, c.v2); BDDC_COUNT(); }
-  else { residual_kernel<3><<<gr, th, 0, s>>>(G, c.alpha, r, z, c.v2); BDDC_COUNT(); }
-  BDDC_LAUNCH_CHECK();
+  BDDC_SWEEP_LAUNCH(residual_kernel, G, s, c.alpha, r, z, c.v2);
   bt_solve(c, c.v2, z, s);
 }
 

@@ -63,20 +63,17 @@ __global__ void __launch_bounds__(kRedThreads) dot_partial_kernel(const double* 
   grid_total(acc, partial, cnt, out);
 }
 
-template <int DIM>
-__global__ void __launch_bounds__(kRedThreads) spmv_dot_kernel(Geometry G, const double* __restrict__ alpha,
+// one resident wave: every thread loops over the same number of sweep items (+-1)
+template <int DIM, bool EDGE>
+__global__ void __launch_bounds__(kRedThreads, (EDGE || DIM == 2) ? 3 : 1) spmv_dot_kernel(Geometry G, const double* __restrict__ alpha,
                                                                const double* __restrict__ p,
                                                                double* __restrict__ Ap, double* partial,
                                                                unsigned* cnt, double* out) {
   double acc = 0.0;
-  for (long long f = G.f_lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; f < G.f_hi;
-       f += (long long)gridDim.x * blockDim.x) {
-    int g0, g1, g2;
-    free_coords(G, f, g0, g1, g2);
-    const double v = stencil_row<DIM>(G, alpha, p, g0, g1, g2);
+  stencil_sweep<DIM, EDGE>(G, alpha, p, [&](long long f, double v, double pc) {
     Ap[f] = v;
-    if (f >= G.fo_lo) acc += p[f] * v;  // dot over owned rows (fo_hi == f_hi)
-  }
+    if (f >= G.fo_lo) acc += pc * v;  // dot over owned rows (fo_hi == f_hi)
+  });
   grid_total(acc, partial, cnt, out);
 }
 
@@ -168,11 +165,22 @@ static PcgResult pcg_run(Ctx& c, const double* b, double* x, double tol, int max
   }
   BDDC_CUDA(cudaMemcpyAsync(c.p, c.z, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   int nbeta = 0;
+  // the SpMV + dot kernel of this operator and a grid of exactly one resident wave
+  const bool edge = stencil_edge_only(G);
+  auto sd_kernel = G.dim == 2 ? (edge ? spmv_dot_kernel<2, true> : spmv_dot_kernel<2, false>)
+                              : (edge ? spmv_dot_kernel<3, true> : spmv_dot_kernel<3, false>);
+  int sd_per_sm = 1, sms = 148;
+  BDDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sd_per_sm, sd_kernel, kRedThreads, 0));
+  BDDC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+  const int sd_blocks = std::max(1, std::min(4096, sd_per_sm * sms));
+  auto sd_launch = [&](int grid, int threads, size_t smem, cudaStream_t st, auto... args) {
+    sd_kernel<<<grid, threads, smem, st>>>(args...);
+  };
   for (int it = 0; it < max_iters; ++it) {
     exchange_dof_halo(c, c.p, s);  // sharded: p on the rows next to the cut lines
     c.prof.begin("pcg.spmv_dot", s);
-    if (G.dim == 2) { spmv_dot_kernel<2><<<kRedBlocks, kRedThreads, 0, s>>>(G, c.alpha, c.p, c.Ap, c.red, c.redc, sc + 1); BDDC_COUNT(); }
-    else { spmv_dot_kernel<3><<<kRedBlocks, kRedThreads, 0, s>>>(G, c.alpha, c.p, c.Ap, c.red, c.redc, sc + 1); BDDC_COUNT(); }
+    sd_launch(sd_blocks, kRedThreads, 0, s, G, c.alpha, c.p, c.Ap, c.red, c.redc, sc + 1);
+    BDDC_COUNT();
     c.prof.end("pcg.spmv_dot", s);
     allreduce_scalars(c, sc + 1, 1, s);
     { update_xr_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(x, c.r, c.p, c.Ap, sc, G.f_lo, G.f_hi, G.fo_lo, c.red,

@@ -100,6 +100,120 @@ __device__ __forceinline__ double stencil_row(const Geometry& G, const double* _
   return acc;
 }
 
+// ---- plane-marching sweep of the operator over the rank's active rows --------------------
+// A thread owns one column of nodes (fixed g0 [, g1]) over kSweepChunk consecutive rows of the
+// last axis and keeps the 3^d window of x and the 2^d cell coefficients around its node in
+// registers: marching one row loads 3^(d-1) x values and 2^(d-1) coefficients (P1: only the
+// axis neighbours survive) instead of the 2^d (1 + nonzeros) loads of stencil_row. The row
+// value is accumulated in stencil_row's order (cells s ascending, nodes t ascending, zero
+// K entries and Dirichlet neighbours contributing exact zeros), so it is the same number.
+// EDGE: K(s, t) != 0 only for t = s or t an axis neighbour of s (P1 Kuhn; checked on the host).
+constexpr int kSweepChunk = 16;
+
+__host__ __device__ inline bool stencil_edge_only(const Geometry& G) {
+  for (int s = 0; s < G.npe; ++s)
+    for (int t = 0; t < G.npe; ++t) {
+      const int d = s ^ t;
+      if ((d & (d - 1)) != 0 && G.K[s * G.npe + t] != 0.0) return false;
+    }
+  return true;
+}
+
+// work items of a sweep over the rank's active rows
+inline long long sweep_items(const Geometry& G) {
+  const long long ncol = G.dim == 3 ? (long long)G.nfree[0] * G.nfree[1] : G.nfree[0];
+  const long long rows = (G.f_hi - G.f_lo) / ncol;
+  return ncol * ((rows + kSweepChunk - 1) / kSweepChunk);
+}
+
+// emit(f, v, xc): row f, v = (A x)[f], xc = x[f]
+template <int DIM, bool EDGE, class F>
+__device__ __forceinline__ void stencil_sweep(const Geometry& G, const double* __restrict__ alpha,
+                                              const double* __restrict__ x, F&& emit) {
+  constexpr int NPE = 1 << DIM;
+  constexpr int NY = DIM == 3 ? 3 : 1;   // window extent along axis 1 for DIM == 3
+  const int nf0 = G.nfree[0], c0n = G.cells[0];
+  const int nf1 = DIM == 3 ? G.nfree[1] : 1, c1n = G.cells[1];
+  const int ncol = nf0 * nf1;                      // nodes per row of the last axis
+  const int clast = G.cells[DIM - 1];
+  const int L_lo = (int)(G.f_lo / ncol), L_hi = (int)(G.f_hi / ncol);  // free rows [L_lo, L_hi)
+  const int nchunk = (L_hi - L_lo + kSweepChunk - 1) / kSweepChunk;
+  const long long items = (long long)ncol * nchunk;
+  const long long cstride = DIM == 3 ? (long long)c0n * c1n : c0n;  // cells per layer of the last axis
+  for (long long item = blockIdx.x * (long long)blockDim.x + threadIdx.x; item < items;
+       item += (long long)gridDim.x * blockDim.x) {
+    const int col = (int)(item % ncol), chunk = (int)(item / ncol);
+    const int g0 = col % nf0 + 1, g1 = DIM == 3 ? col / nf0 + 1 : 0;
+    const int za = L_lo + chunk * kSweepChunk, zb = min(za + kSweepChunk, L_hi);
+    const bool xok[3] = {g0 > 1, true, g0 < c0n - 1};
+    const bool yok[3] = {DIM == 3 ? g1 > 1 : true, true, DIM == 3 ? g1 < c1n - 1 : true};
+    // window: w[dl][dy][dx] = x(g + (dx-1, dy-1, dl-1)); a[sl][sy][sx] = alpha(cell g - s)
+    double w[3][NY][3], a[2][DIM == 3 ? 2 : 1][2];
+    auto load_row = [&](double (&dst)[NY][3], int z) {  // free row z of the last axis
+      const bool zok = z >= 0 && z + 1 < clast;
+      const double* xb = x + ((long long)z * ncol + col);
+#pragma unroll
+      for (int dy = 0; dy < NY; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) {
+          const int yy = DIM == 3 ? dy : 1;
+          const bool ok = zok && xok[dx] && yok[yy];
+          dst[dy][dx] = ok ? __ldg(xb + (dx - 1) + nf0 * (DIM == 3 ? dy - 1 : 0)) : 0.0;
+        }
+    };
+    auto load_cells = [&](double (&dst)[DIM == 3 ? 2 : 1][2], int cl) {  // cell layer cl of the last axis
+      const double* ab = alpha + (cl * cstride + (DIM == 3 ? (long long)g1 * c0n : 0) + g0);
+#pragma unroll
+      for (int sy = 0; sy < (DIM == 3 ? 2 : 1); ++sy)
+#pragma unroll
+        for (int sx = 0; sx < 2; ++sx) dst[sy][sx] = __ldg(ab - sx - (DIM == 3 ? sy * c0n : 0));
+    };
+    load_row(w[0], za - 1);
+    load_row(w[1], za);
+    load_cells(a[1], za);  // node coordinate = za + 1: the layer below it is cell layer za
+    load_row(w[2], za + 1);
+    load_cells(a[0], za + 1);
+    for (int z = za; z < zb; ++z) {
+      // the next row's upper neighbours and cells are requested before this row is computed
+      // (one row of loads in flight per thread: the sweep is bound by memory-level parallelism)
+      double nw[NY][3], na[DIM == 3 ? 2 : 1][2];
+      if (z + 1 < zb) {
+        load_row(nw, z + 2);
+        load_cells(na, z + 2);
+      }
+      double acc = 0.0;
+#pragma unroll
+      for (int s = 0; s < NPE; ++s) {
+        const int sx = s & 1, sy = DIM == 3 ? (s >> 1) & 1 : 0, sl = (s >> (DIM - 1)) & 1;
+        double part = 0.0;
+#pragma unroll
+        for (int t = 0; t < NPE; ++t) {
+          if (EDGE && ((s ^ t) & ((s ^ t) - 1)) != 0) continue;
+          const int tx = t & 1, ty = DIM == 3 ? (t >> 1) & 1 : 0, tl = (t >> (DIM - 1)) & 1;
+          part += G.K[s * NPE + t] * w[1 + tl - sl][DIM == 3 ? 1 + ty - sy : 0][1 + tx - sx];
+        }
+        acc += a[sl][sy][sx] * part;
+      }
+      emit((long long)z * ncol + col, acc, w[1][DIM == 3 ? 1 : 0][1]);
+#pragma unroll
+      for (int dy = 0; dy < NY; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) {
+          w[0][dy][dx] = w[1][dy][dx];
+          w[1][dy][dx] = w[2][dy][dx];
+          w[2][dy][dx] = nw[dy][dx];
+        }
+#pragma unroll
+      for (int sy = 0; sy < (DIM == 3 ? 2 : 1); ++sy)
+#pragma unroll
+        for (int sx = 0; sx < 2; ++sx) {
+          a[1][sy][sx] = a[0][sy][sx];
+          a[0][sy][sx] = na[sy][sx];
+        }
+    }
+  }
+}
+
 // Coefficient A_i(a, a + d) of subdomain p's local Neumann matrix (local node coords a),
 // summing only cells of the subdomain box (bddc.py:427 via assemble_cells).
 template <int DIM>

@@ -147,7 +147,7 @@ __device__ __forceinline__ void gemm_tile(const double* A, int lda, const double
     if (lower && n0 + wn * 32 > m0 + wm * 32 + 31) ni = 0;  // warp tile above the diagonal
     if (ni == 0 || nj == 0) ni = nj = 0;
   }
-  constexpr int LDKT = BKT + 4, TILE = tile_doubles<BKT>();
+  constexpr int TILE = tile_doubles<BKT>();
   const int kb0 = k_lo / BKT;
   const int nk = ((k_hi < 0 ? K : min(K, k_hi)) + BKT - 1) / BKT - kb0;
   const bool al_a = ((((unsigned long long)A) & 15) == 0) && ((lda & 1) == 0);
