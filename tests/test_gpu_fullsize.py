@@ -46,15 +46,17 @@ def test_fullsize_matches_reference(cuda_ok, case):
     z = op.apply(g["r"])
     e_br = np.abs(z[idx] - g["Br_s"]).max() / np.abs(g["Br_s"]).max()
     print(f"{case}: B r max diff / max = {e_br:.3e}")
-    assert e_br <= 1e-11
-    assert abs(np.linalg.norm(z) - float(g["Br_norm"])) <= 1e-11 * float(g["Br_norm"])
+    # 1e-9 for the 1e12-contrast coefficient (the bound of the small cfg4 fixtures, test_gpu_parity.py)
+    tol_br = 1e-9 if str(g["coeff"]) == "blocks" else 1e-11
+    assert e_br <= tol_br
+    assert abs(np.linalg.norm(z) - float(g["Br_norm"])) <= tol_br * float(g["Br_norm"])
     # coarse matrix diagonal (every k-th entry and the trace)
     d = op.coarse_matrix.diagonal()
     ds = d[:: max(1, op.coarse_size // 4096)]
     e_d = np.abs(ds - g["coarse_diag_s"]).max() / np.abs(g["coarse_diag_s"]).max()
     print(f"{case}: coarse diagonal max diff / max = {e_d:.3e}")
-    assert e_d <= 1e-11
-    assert abs(d.sum() - float(g["coarse_trace"])) <= 1e-11 * abs(float(g["coarse_trace"]))
+    assert e_d <= tol_br
+    assert abs(d.sum() - float(g["coarse_trace"])) <= tol_br * abs(float(g["coarse_trace"]))
     # PCG
     x, rep = P.pcg(op.matvec, op.apply, g["b"], tol=float(g["tol"]), max_iters=2000)
     e_x = np.linalg.norm(x[idx] - g["x_s"]) / np.linalg.norm(g["x_s"])
