@@ -37,7 +37,7 @@ namespace bddc {
 // tasks: 4x less partial traffic than one panel block per task)
 constexpr int kX1Chunk = BDDC_X1_CHUNK;
 constexpr int kX1Blocks = kX1Chunk / 64;
-constexpr int kCoopStages = 2;  // cp.async depth of the engine GEMM tiles: 41 KB smem leaves more L1 (measured: 3 stages and 4 CTAs/SM are slower)
+constexpr int kCoopStages = 2;  // cp.async depth of the engine GEMM tiles: 41 KB smem leaves more L1 (measured: 3 stages are slower)
 
 enum CoopType : int {
   CT_EA = 0, CT_PT = 1, CT_TS = 2, CT_X1 = 3, CT_SY = 4, CT_X2 = 5, CT_W = 6,
@@ -88,8 +88,11 @@ struct CoopProgram {
 // (counter >= target) and up to 3 counters it increments when done.
 constexpr int kDeps = 6;
 constexpr int kSigs = 6;
+// 4 CTAs per SM (128 registers) since the GEMM tile epilogue handles the C tile in two halves
+// (56 bytes of spills; the one-pass epilogue spilled 680): cfg5 coarse 1220.8 -> 1186.8 ms, cfg3
+// 30.07 -> 30.40 ms against 3 CTAs on the same box (profiles/r02/ab/ctas4)
 #ifndef BDDC_DF_CTAS
-#define BDDC_DF_CTAS 3
+#define BDDC_DF_CTAS 4
 #endif
 constexpr int kDfCtasPerSm = BDDC_DF_CTAS;  // dataflow: no grid barrier, more CTAs hide tile latency
 struct DfTask {

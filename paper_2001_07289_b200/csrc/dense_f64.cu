@@ -39,8 +39,13 @@ __device__ __forceinline__ TaskView gemm_task(const GemmArgs& a, int b) {
 constexpr int kGemmStages = BDDC_GEMM_STAGES;
 constexpr bool kGemmPred = BDDC_GEMM_PRED != 0;
 
+// 4 CTAs per SM (128 registers; the two-half epilogue of gemm_tile keeps the kernel spill-free):
+// cfg3 setup 70.24 -> 68.60 ms, cfg5 1547 -> 1535 ms against 3 CTAs (profiles/r02/ab/ctas4)
+#ifndef BDDC_GEMM_CTAS
+#define BDDC_GEMM_CTAS 4
+#endif
 template <bool TA, bool TB>
-__global__ void __launch_bounds__(128) gemm_f64_kernel(GemmArgs args) {
+__global__ void __launch_bounds__(128, BDDC_GEMM_CTAS) gemm_f64_kernel(GemmArgs args) {
   extern __shared__ __align__(16) double smem[];
   const TaskView t = gemm_task(args, blockIdx.y);
   const int tiles_m = (t.M + BM - 1) / BM;

@@ -166,6 +166,8 @@ __device__ __forceinline__ void gemm_tile(const double* A, int lda, const double
   for (int kt = 0; kt < nk; ++kt) {
     const int st = kt % NS;
     const int pf = kt + NS - 1;  // slice to prefetch into the stage freed last iteration
+    // (one barrier per slice, with the prefetch issued after it, measured 1-5% slower on the
+    // local GEMM phases and equal on the coarse engine: profiles/r02/ab/one_barrier)
     if (pf < nk) {
       load_a<TA, BKT>(As(pf % NS), A, lda, M, K, m0, (kb0 + pf) * BKT, tid, al_a);
       load_b<TB, BKT>(Bs(pf % NS), B, ldb, N, K, n0, (kb0 + pf) * BKT, tid, al_b);
@@ -191,36 +193,41 @@ __device__ __forceinline__ void gemm_tile(const double* A, int lda, const double
     __syncthreads();
   }
   cp_async_wait<0>();
-  // epilogue: all C reads issued before any store (no serial read-modify-write chain)
-  double cv[4][4][2];
-  if (beta != 0.0) {
+  // epilogue in two halves of the warp tile (accumulator block rows 0-1, then 2-3): the C reads
+  // of a half are all issued before its stores (no serial read-modify-write chain) while only
+  // 32 registers hold C values next to the 64 accumulator registers
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int row = m0 + wm * 32 + i * 8 + g;
+  for (int h = 0; h < 2; ++h) {
+    double cv[2][4][2];
+    if (beta != 0.0) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int i = 0; i < 2; ++i) {
+        const int row = m0 + wm * 32 + (2 * h + i) * 8 + g;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int col = n0 + wn * 32 + j * 8 + 2 * q + e;
+            const bool ok = row < M && col < N && !(lower && col > row);
+            cv[i][j][e] = ok ? __ldcg(C + row + (long long)col * ldc) : 0.0;
+          }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int row = m0 + wm * 32 + (2 * h + i) * 8 + g;
+      if (row >= M) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int col = n0 + wn * 32 + j * 8 + 2 * q + e;
-          const bool ok = row < M && col < N && !(lower && col > row);
-          cv[i][j][e] = ok ? __ldcg(C + row + (long long)col * ldc) : 0.0;
+          if (col >= N || (lower && col > row)) continue;
+          double v = alpha * acc[2 * h + i][j][e];
+          if (beta != 0.0) v += beta * cv[i][j][e];
+          C[row + (long long)col * ldc] = v;
+          if (mirror && row != col) C[col + (long long)row * ldc] = v;
         }
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int row = m0 + wm * 32 + i * 8 + g;
-    if (row >= M) continue;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int col = n0 + wn * 32 + j * 8 + 2 * q + e;
-        if (col >= N || (lower && col > row)) continue;
-        double v = alpha * acc[i][j][e];
-        if (beta != 0.0) v += beta * cv[i][j][e];
-        C[row + (long long)col * ldc] = v;
-        if (mirror && row != col) C[col + (long long)row * ldc] = v;
       }
     }
   }
