@@ -780,10 +780,13 @@ static std::map<const Ctx*, CoopState> g_coop;
 
 // Fronts whose separator is at most this size keep W21 = L21 X for the solve (one GEMV phase
 // per front and direction); larger ones (the top of the tree: 78% of the W21 flops at cfg5 in
-// 15 fronts) solve with L21 in place and one more dependent GEMV phase (coarse.cu).
+// 15 fronts) solve with L21 in place and one more dependent GEMV phase (coarse.cu). The
+// threshold trades setup for solve time: measured at 4 CTAs/SM (profiles/r02/ab/w21_ctas4), cfg5
+// coarse 1183 / 1163 / 1147 ms and coarse solve 11.5 / 11.9 / 13.7 ms per apply at 2048 / 1024 /
+// 512; 1024 wins below about 50 applies per setup (the BASELINE configs take 6-10).
 int coarse_w21_max_sep() {  // (>= 127: L21 fronts have separators of two 64-chunks or more)
   const char* e = getenv("BDDC_W21_MAX_SEP");
-  return e ? std::max(atoi(e), 127) : 2048;
+  return e ? std::max(atoi(e), 127) : 1024;
 }
 
 long long coarse_df_layout(const FrontPlan& fp, std::vector<long long>& inv, std::vector<long long>& Y,
