@@ -494,7 +494,9 @@ def run_ours(args, rank, world, local_rank):
     roof = None
     if dominant:
         d = phase_out[dominant]
-        roof = {"kernel": dominant, "bound": "hbm" if d.get("bound") == "hbm" else "fp64",
+        roof = {"kernel": dominant, "bound": "hbm" if d.get("bound") == "hbm" else "tensor",
+                "pipe": "HBM3e stream" if d.get("bound") == "hbm" else
+                "FP64 tensor pipe: DMMA.8x8x4 via mma.sync (tcgen05 has no f64 kind on sm_100a)",
                 "achieved": d.get("achieved"), "unit": d.get("unit"),
                 "peak": hbm if d.get("bound") == "hbm" else FP64_PEAK_TFLOPS,
                 "peak_source": hbm_src if d.get("bound") == "hbm" else

@@ -164,6 +164,10 @@ long long bddc_coarse_csr(bddc_ctx* ctx, long long* row, long long* col, long lo
 typedef int (*bddc_host_exchange_fn)(void* user, int op, double* a, double* b, long long n, int peer);
 int bddc_nccl_unique_id(void* out128);
 int bddc_comm_init_nccl(bddc_ctx* ctx, int rank, int world, const void* unique_id128);
+/* one-GPU self-test of the NCCL binding on `device`: a world-1 communicator runs every NCCL
+   call the transport makes (allreduce sum / max, grouped broadcast, grouped send/recv to
+   self). 0 ok, 2 wrong result, 6 NCCL / CUDA error (message on stderr) */
+int bddc_nccl_selftest(int device);
 int bddc_comm_init_host(bddc_ctx* ctx, int rank, int world, bddc_host_exchange_fn fn, void* user);
 /* host-only: slab of `rank` for a dim/cells/subs box; out[10] = s_lo, s_hi, f_lo, f_hi, fo_lo,
    fo_hi, halo_lo_send, halo_lo_recv, halo_hi_send, halo_hi_recv (free-dof offsets, -1 none) */

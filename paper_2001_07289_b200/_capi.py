@@ -27,7 +27,7 @@ EXPORTS = (
     "bddc_spmv", "bddc_pcg", "bddc_pcg_host", "bddc_solve_host", "bddc_get_stats", "bddc_sync",
     "bddc_kernel_launches_per_apply", "bddc_debug_copy", "bddc_launch_count",
     "bddc_event_record", "bddc_event_elapsed_ms", "bddc_profile", "bddc_profile_read",
-    "bddc_nccl_unique_id", "bddc_comm_init_nccl", "bddc_comm_init_host", "bddc_partition_info",
+    "bddc_nccl_unique_id", "bddc_nccl_selftest", "bddc_comm_init_nccl", "bddc_comm_init_host", "bddc_partition_info",
     "bddc_dense_potrf", "bddc_dense_trsm", "bddc_dense_gemm", "bddc_check", "bddc_update_weights",
     "bddc_coarse_solve", "bddc_read_buffer", "bddc_coarse_pattern",
     "bddc_index_build", "bddc_index_size", "bddc_index_copy", "bddc_index_free", "bddc_coarse_csr",
@@ -135,6 +135,7 @@ def load(required: bool = True):
     lib.bddc_profile_read.argtypes = [_vp, C.c_char_p, _pll]
     lib.bddc_profile_read.restype = _d
     lib.bddc_nccl_unique_id.argtypes = [_vp]
+    lib.bddc_nccl_selftest.argtypes = [_i]
     lib.bddc_comm_init_nccl.argtypes = [_vp, _i, _i, _vp]
     lib.bddc_comm_init_host.argtypes = [_vp, _i, _i, _vp, _vp]
     lib.bddc_partition_info.argtypes = [_i, _pi, _pi, _i, _i, _pll]

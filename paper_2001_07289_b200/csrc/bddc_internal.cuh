@@ -454,5 +454,6 @@ void allreduce_scalars(Ctx& c, double* d, int n, cudaStream_t s);
 Transport* make_nccl_transport(int rank, int world, const void* unique_id);
 Transport* make_host_transport(int rank, int world, bddc_host_exchange_fn fn, void* user);
 void nccl_unique_id(void* out);
+int nccl_selftest();  // world-1 run of every NCCL symbol the transport binds (0 = ok)
 
 }  // namespace bddc

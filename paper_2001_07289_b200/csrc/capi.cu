@@ -712,6 +712,16 @@ int bddc_nccl_unique_id(void* out) {
   }
 }
 
+int bddc_nccl_selftest(int device) {
+  try {
+    BDDC_CUDA(cudaSetDevice(device));
+    return nccl_selftest() ? 2 : 0;
+  } catch (const std::exception& e) {
+    fprintf(stderr, "bddc_nccl_selftest: %s\n", e.what());
+    return 6;
+  }
+}
+
 int bddc_comm_init_nccl(bddc_ctx* h, int rank, int world, const void* id) {
   if (!h || !id || world < 1 || rank < 0 || rank >= world) return 1;
   try {

@@ -341,6 +341,41 @@ Transport* make_host_transport(int rank, int world, bddc_host_exchange_fn fn, vo
   return new HostTransport(rank, world, fn, user);
 }
 
+// One-rank self-test of the NCCL binding on the current device: every symbol the transport
+// uses runs once on a communicator of world size 1 (sum-allreduce, max-allreduce, the grouped
+// broadcast of allgatherv, and a grouped send/recv to self standing in for the neighbour
+// exchange). Returns 0 when every result is the expected one.
+int nccl_selftest() {
+  ncclUniqueId id;
+  NcclApi& a = nccl_api();
+  if (!a.GetUniqueId || !a.GroupStart || !a.GroupEnd) throw std::runtime_error("NCCL symbols missing");
+  nccl_check(a.GetUniqueId(&id), "GetUniqueId");
+  NcclTransport t(0, 1, &id);
+  cudaStream_t s;
+  BDDC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  const int n = 1024;
+  std::vector<double> h(2 * n);
+  for (int i = 0; i < n; ++i) h[i] = 0.5 * i + 1.0;
+  double* d = nullptr;
+  BDDC_CUDA(cudaMalloc(&d, sizeof(double) * 2 * n));
+  BDDC_CUDA(cudaMemcpyAsync(d, h.data(), sizeof(double) * 2 * n, cudaMemcpyHostToDevice, s));
+  t.allreduce_sum(d, n, s);
+  const long long off[1] = {0}, cnt[1] = {n};
+  t.allgatherv(d, off, cnt, s);
+  nccl_check(a.GroupStart(), "GroupStart");  // self send/recv: [0, n) -> [n, 2n)
+  nccl_check(a.Send(d, n, ncclDouble, 0, t.comm, s), "Send");
+  nccl_check(a.Recv(d + n, n, ncclDouble, 0, t.comm, s), "Recv");
+  nccl_check(a.GroupEnd(), "GroupEnd");
+  BDDC_CUDA(cudaMemcpyAsync(h.data(), d, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, s));
+  BDDC_CUDA(cudaStreamSynchronize(s));
+  const int mx = t.allreduce_max_host(7);
+  cudaFree(d);
+  cudaStreamDestroy(s);
+  int bad = mx != 7;
+  for (int i = 0; i < n; ++i) bad |= (h[i] != 0.5 * i + 1.0) || (h[n + i] != h[i]);
+  return bad;
+}
+
 void nccl_unique_id(void* out) {
   ncclUniqueId id;
   NcclApi& a = nccl_api();

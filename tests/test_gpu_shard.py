@@ -99,3 +99,14 @@ def test_nccl_transport_two_gpus(cuda_ok, case):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
     mp.spawn(_nccl_worker, args=(2, _free_port(), case), nprocs=2, join=True)
+
+
+def test_nccl_binding_selftest_one_gpu(cuda_ok):
+    """Every NCCL symbol the transport binds (dlopen of the process's libnccl, CommInitRank,
+    AllReduce sum / max, grouped Broadcast, grouped Send/Recv) runs once on a world-1
+    communicator on this GPU: the one part of the NCCL path a one-GPU box can execute."""
+    import torch  # noqa: F401 - loads torch's NCCL first, as a sharded run does
+
+    from paper_2001_07289_b200 import _capi
+
+    assert _capi.load().bddc_nccl_selftest(0) == 0
