@@ -127,6 +127,14 @@ int bddc_update_weights(bddc_ctx* ctx, const double* slot_w_host, char* err, siz
 /* coarse solve S_0 x = rhs with the device factor (coarse_factor.solve, bddc.py:362-364);
    device vectors of n_coarse in the ELIMINATION order of the descriptor */
 int bddc_coarse_solve(bddc_ctx* ctx, const double* rhs_dev, double* sol_dev, void* stream);
+/* multilevel hook (the paper's outlook; not in the reference):
+   when set, bddc_apply / bddc_pcg call fn in place of the exact coarse solve, with device
+   vectors of n_coarse in elimination order and the stream the apply runs on (fn must order
+   its work on that stream); fn returns 0 on success. NULL restores the direct solve.
+   Single-rank operators only. */
+typedef int (*bddc_coarse_solver_fn)(void* user, const double* rhs_dev, double* sol_dev, long long n_coarse,
+                                     void* stream);
+int bddc_set_coarse_solver(bddc_ctx* ctx, bddc_coarse_solver_fn fn, void* user);
 int bddc_kernel_launches_per_apply(bddc_ctx* ctx);
 /* measurement: kernels launched by this library so far (process-wide); CUDA events on the
    context stream (slots 0..7); optional per-phase event timers ("apply.bt_solve",

@@ -22,6 +22,9 @@ _pll = C.POINTER(C.c_longlong)
 _pd = C.POINTER(C.c_double)
 _vp = C.c_void_p
 
+# coarse-solver hook of the multilevel operator: (user, rhs_dev, sol_dev, n_coarse, stream) -> rc
+COARSE_SOLVER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p)
+
 EXPORTS = (
     "bddc_create", "bddc_destroy", "bddc_setup", "bddc_refactor", "bddc_apply", "bddc_harmonic",
     "bddc_spmv", "bddc_pcg", "bddc_pcg_host", "bddc_solve_host", "bddc_get_stats", "bddc_sync",
@@ -29,7 +32,7 @@ EXPORTS = (
     "bddc_event_record", "bddc_event_elapsed_ms", "bddc_profile", "bddc_profile_read",
     "bddc_nccl_unique_id", "bddc_nccl_selftest", "bddc_comm_init_nccl", "bddc_comm_init_host", "bddc_partition_info",
     "bddc_dense_potrf", "bddc_dense_trsm", "bddc_dense_gemm", "bddc_check", "bddc_update_weights",
-    "bddc_coarse_solve", "bddc_read_buffer", "bddc_coarse_pattern",
+    "bddc_coarse_solve", "bddc_set_coarse_solver", "bddc_read_buffer", "bddc_coarse_pattern",
     "bddc_index_build", "bddc_index_size", "bddc_index_copy", "bddc_index_free", "bddc_coarse_csr",
     "bddc_layout_tables", "bddc_nd_build", "bddc_nd_size", "bddc_nd_copy", "bddc_nd_free",
 )
@@ -102,6 +105,7 @@ def load(required: bool = True):
     lib.bddc_check.argtypes = [_vp, C.c_char_p, C.c_size_t]
     lib.bddc_update_weights.argtypes = [_vp, _pd, C.c_char_p, C.c_size_t]
     lib.bddc_coarse_solve.argtypes = [_vp, _vp, _vp, _vp]
+    lib.bddc_set_coarse_solver.argtypes = [_vp, COARSE_SOLVER_FN, _vp]
     lib.bddc_kernel_launches_per_apply.argtypes = [_vp]
     lib.bddc_debug_copy.argtypes = [_vp, C.c_char_p, _pd, _ll]
     lib.bddc_debug_copy.restype = _ll

@@ -711,7 +711,7 @@ void apply_bddc(Ctx& c, const double* r, double* z, cudaStream_t s) {
     }
     const size_t smem1 = sizeof(double) * G.nG_pad;
     // v = T rho inside the coarse solve when its schedule holds those tasks (rho parked in wloc)
-    const bool tv_fused = c.fp.n_coarse > 0 && c.sched.n_tv > 0;
+    const bool tv_fused = c.fp.n_coarse > 0 && c.sched.n_tv > 0 && !c.coarse_cb;
     c.prof.begin("apply.gamma1", s);
     if (tv_fused) { local_gamma1_kernel<false><<<nl, 128, smem1, s>>>(G, c.st, c.LS, c.Phi, c.cscale, c.rpg, c.qloc, c.wloc); BDDC_COUNT(); }
     else if (t_lower_only(G)) {
@@ -732,7 +732,12 @@ void apply_bddc(Ctx& c, const double* r, double* z, cudaStream_t s) {
                                                                      c.fp.coarse_slots, c.qloc, c.crhs); BDDC_COUNT(); }
       BDDC_LAUNCH_CHECK();
       const TvArgs tv{c.LS, c.wloc, c.uloc, G.nG_pad};
-      coarse_solve(c, c.crhs, c.csol, s, tv_fused ? &tv : nullptr);
+      if (c.coarse_cb) {  // inexact coarse solve of a multilevel method, on this stream
+        if (c.coarse_cb(c.coarse_cb_user, c.crhs, c.csol, c.fp.n_coarse, (void*)s) != 0)
+          throw CudaError("coarse solver callback failed");
+      } else {
+        coarse_solve(c, c.crhs, c.csol, s, tv_fused ? &tv : nullptr);
+      }
     }
     c.prof.begin("apply.gamma2", s);
     { local_gamma2_kernel<<<nl, 128, 0, s>>>(G, c.st, c.Phi, c.cscale, c.csol, c.uloc,

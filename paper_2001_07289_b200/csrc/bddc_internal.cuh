@@ -377,6 +377,9 @@ struct Ctx {
   Slab slab;
   Transport* tp = nullptr;
   DistCoarse dist;
+  // three-level hook (bddc_set_coarse_solver): replaces the exact coarse solve of the apply
+  bddc_coarse_solver_fn coarse_cb = nullptr;
+  void* coarse_cb_user = nullptr;
   // timing of the last setup (ms) per phase
   float t_local_ms = 0, t_coarse_ms = 0, t_upload_ms = 0;
   std::vector<void*> allocations;

@@ -818,6 +818,14 @@ int bddc_coarse_solve(bddc_ctx* h, const double* rhs, double* sol, void* stream)
   });
 }
 
+int bddc_set_coarse_solver(bddc_ctx* h, bddc_coarse_solver_fn fn, void* user) {
+  if (!h) return 1;
+  if (fn && h->c.tp) return 1;  // single-rank operators only
+  h->c.coarse_cb = fn;
+  h->c.coarse_cb_user = user;
+  return 0;
+}
+
 int bddc_check(bddc_ctx* h, char* err, size_t errlen) {
   if (!h) return 1;
   return guarded(err, errlen, [&] {
