@@ -24,9 +24,11 @@ Tu (2007) / Mandel, Sousedík, Dohrmann (2008):
 hook ``bddc_set_coarse_solver``: the level-1 apply and the fused device PCG then call it in place
 of the multifrontal coarse solve, on the library's stream.
 
-Status: a prototype of the outlook, not a reference feature. The level-2 dense algebra runs
-through torch's batched Cholesky / matmul (library kernels) on the device; it is not hand-written
-and is not part of the benchmarked path. No reference exists to pin it: the tests check the
+Status: a prototype of the outlook, not a reference feature. On the GPU the level-2 setup's
+factorizations, multi-right-hand-side triangular solves and Schur-complement product run on this
+library's batched FP64 kernels (bddc_dense_potrf / trsm / gemm); the apply's single-vector solves
+and the gathers / scatters go through torch (library kernels). It is not part of the benchmarked
+path. On a CPU device the same formulas run through torch: that evaluation is the tests' checker. No reference exists to pin it: the tests check the
 properties the method guarantees (symmetry, positive definiteness, a bounded condition number of
 the preconditioned coarse problem, PCG convergence to the two-level solution).
 """
@@ -102,11 +104,12 @@ class Level2Bddc:
         nC = max((len(a) for a in O_of), default=0)
         self.shape = (nbox, nI, nG, nC)
 
-        idxI = np.full((nbox, max(nI, 1)), n0, dtype=np.int64)
-        idxG = np.full((nbox, max(nG, 1)), n0, dtype=np.int64)
-        idxC = np.full((nbox, max(nC, 1)), nobj, dtype=np.int64)
-        wG = np.zeros((nbox, max(nG, 1)))
-        Cm = np.zeros((nbox, max(nC, 1), max(nG, 1)))
+        r8 = lambda v: max(8, -(-v // 8) * 8)  # noqa: E731 - even leading dimensions for the dense kernels
+        idxI = np.full((nbox, r8(nI)), n0, dtype=np.int64)
+        idxG = np.full((nbox, r8(nG)), n0, dtype=np.int64)
+        idxC = np.full((nbox, r8(nC)), nobj, dtype=np.int64)
+        wG = np.zeros((nbox, r8(nG)))
+        Cm = np.zeros((nbox, r8(nC), r8(nG)))
         for J in range(nbox):
             idxI[J, :len(I_of[J])] = I_of[J]
             idxG[J, :len(G_of[J])] = G_of[J]
@@ -144,18 +147,39 @@ class Level2Bddc:
             padG = torch.arange(ng, nGp, device=dev)
             AGG[J, padG, padG] = 1.0
         AII = 0.5 * (AII + AII.transpose(1, 2))
-        self.LI = torch.linalg.cholesky(AII)
-        self.AIG = AIG
-        X = torch.cholesky_solve(AIG, self.LI)
-        S = AGG - AIG.transpose(1, 2) @ X
-        S = 0.5 * (S + S.transpose(1, 2))
         ngs = t(np.array([max(len(g), 1) for g in G_of]), torch.float64)
         validG = (self.idxG < n0).to(torch.float64)
-        s = (torch.diagonal(S, dim1=1, dim2=2) * validG).sum(1) / ngs  # mean diagonal per box
+        CtC = Cmat.transpose(1, 2) @ Cmat
+        if dev.type == "cuda":
+            # the O(n^3) work on this library's batched FP64 kernels (dense_f64.cu: DMMA tile
+            # Cholesky, tile-inverse triangular solves, GEMM). A symmetric batch is its own
+            # column-major image; potrf leaves L in the column-major lower triangle, which the
+            # torch view reads as the upper factor U = L^T (upper=True below).
+            self.upper = True
+            self.LI = _own_potrf(torch, AII.contiguous())
+            Xt = AIG.transpose(1, 2).contiguous()        # column-major n_I x n_G, one box each
+            _own_trsm(torch, 0, self.LI, Xt)             # L y = A_IG
+            _own_trsm(torch, 1, self.LI, Xt)             # L^T X = y
+            S = AGG.contiguous()                         # S = A_GG - A_IG^T X
+            _own_gemm(torch, True, False, -1.0, AIG.transpose(1, 2).contiguous(), Xt, 1.0, S)
+            S = 0.5 * (S + S.transpose(1, 2))
+            s = (torch.diagonal(S, dim1=1, dim2=2) * validG).sum(1) / ngs  # mean diagonal per box
+            self.LK = _own_potrf(torch, (S + s[:, None, None] * CtC).contiguous())
+            Yt = Cmat.clone()                            # column-major n_G x n_C = C^T
+            _own_trsm(torch, 0, self.LK, Yt)
+            _own_trsm(torch, 1, self.LK, Yt)
+            Y = Yt.transpose(1, 2).contiguous()          # K^{-1} C^T
+        else:  # CPU evaluation of the same formulas (the tests' checker of the device level 2)
+            self.upper = False
+            self.LI = torch.linalg.cholesky(AII)
+            X = torch.cholesky_solve(AIG, self.LI)
+            S = AGG - AIG.transpose(1, 2) @ X
+            S = 0.5 * (S + S.transpose(1, 2))
+            s = (torch.diagonal(S, dim1=1, dim2=2) * validG).sum(1) / ngs
+            self.LK = torch.linalg.cholesky(S + s[:, None, None] * CtC)
+            Y = torch.cholesky_solve(Cmat.transpose(1, 2).contiguous(), self.LK)  # K⁻¹Cᵀ
+        self.AIG = AIG
         self.s = s
-        K = S + s[:, None, None] * (Cmat.transpose(1, 2) @ Cmat)
-        self.LK = torch.linalg.cholesky(K)
-        Y = torch.cholesky_solve(Cmat.transpose(1, 2).contiguous(), self.LK)  # K⁻¹Cᵀ
         G = Cmat @ Y
         padC = (self.idxC >= nobj).to(torch.float64)
         G = G + torch.diag_embed(padC)
@@ -177,7 +201,7 @@ class Level2Bddc:
         zero = torch.zeros(1, dtype=torch.float64, device=self.device)
         rp = torch.cat([r, zero])
         # interior solves, interface residual
-        u1 = torch.cholesky_solve(rp[self.idxI].unsqueeze(2), self.LI)  # (B, nI, 1)
+        u1 = torch.cholesky_solve(rp[self.idxI].unsqueeze(2), self.LI, upper=self.upper)  # (B, nI, 1)
         tG = self.AIG.transpose(1, 2) @ u1
         rG = rp.clone()
         rG.index_add_(0, self.idxG.reshape(-1), -tG.reshape(-1))
@@ -191,13 +215,13 @@ class Level2Bddc:
         c = torch.zeros_like(r00)
         if nobj:
             c[:nobj] = torch.cholesky_solve(r00[:nobj].unsqueeze(1), self.L00).squeeze(1)
-        v = torch.cholesky_solve(rho, self.LK) - self.Phi @ (self.Y.transpose(1, 2) @ rho)
+        v = torch.cholesky_solve(rho, self.LK, upper=self.upper) - self.Phi @ (self.Y.transpose(1, 2) @ rho)
         w = self.wG.unsqueeze(2) * (v + self.Phi @ c[self.idxC].unsqueeze(2))
         zG = torch.zeros(n0 + 1, dtype=torch.float64, device=self.device)
         zG.index_add_(0, self.idxG.reshape(-1), w.reshape(-1))
         zG[n0] = 0.0
         # harmonic extension + interior correction
-        zI = u1 - torch.cholesky_solve(self.AIG @ zG[self.idxG].unsqueeze(2), self.LI)
+        zI = u1 - torch.cholesky_solve(self.AIG @ zG[self.idxG].unsqueeze(2), self.LI, upper=self.upper)
         zG.index_put_((self.idxI.reshape(-1),), zI.reshape(-1))
         return zG[:n0]
 
@@ -206,6 +230,48 @@ class Level2Bddc:
         torch = self._torch
         eye = torch.eye(self.n0, dtype=torch.float64, device=self.device)
         return torch.stack([self.solve(eye[i]) for i in range(self.n0)], dim=1)
+
+
+def _own_potrf(torch, A):
+    """In-place batched Cholesky of a contiguous symmetric (B, n, n) tensor on the library's
+    kernels (bddc_dense_potrf); returns A, whose torch view then holds U = L^T above the
+    diagonal."""
+    lib = _capi.load()
+    B, n, _ = A.shape
+    info = (C.c_int * B)()
+    rc = lib.bddc_dense_potrf(C.c_void_p(A.data_ptr()), n, n, n * n, B, info,
+                              C.c_void_p(torch.cuda.current_stream(A.device).cuda_stream))
+    if rc:
+        raise RuntimeError(f"bddc_dense_potrf failed ({rc})")
+    bad = [i for i in range(B) if info[i] >= 0]
+    if bad:
+        raise RuntimeError(f"level-2 matrix of box {bad[0]} is not positive definite (pivot {info[bad[0]]})")
+    return A
+
+
+def _own_trsm(torch, kind, L, Bt):
+    """In place on Bt (B, nrhs, n) = column-major n x nrhs: kind 0 solves L y = b, 1 L^T x = y."""
+    lib = _capi.load()
+    B, nrhs, n = Bt.shape
+    rc = lib.bddc_dense_trsm(kind, C.c_void_p(L.data_ptr()), n, n, n * n, C.c_void_p(Bt.data_ptr()), nrhs, n,
+                             n * nrhs, B, C.c_void_p(torch.cuda.current_stream(Bt.device).cuda_stream))
+    if rc:
+        raise RuntimeError(f"bddc_dense_trsm failed ({rc})")
+
+
+def _own_gemm(torch, tA, tB, alpha, At, Bt, beta, Ct):
+    """Ct = alpha op(A) op(B) + beta Ct, every operand a (B, cols, rows) tensor = column-major
+    rows x cols per box (bddc_dense_gemm)."""
+    lib = _capi.load()
+    nb = At.shape[0]
+    M, N = Ct.shape[2], Ct.shape[1]
+    K = At.shape[2] if tA else At.shape[1]
+    rc = lib.bddc_dense_gemm(int(tA), int(tB), M, N, K, float(alpha), C.c_void_p(At.data_ptr()), At.shape[2],
+                             At.shape[1] * At.shape[2], C.c_void_p(Bt.data_ptr()), Bt.shape[2],
+                             Bt.shape[1] * Bt.shape[2], float(beta), C.c_void_p(Ct.data_ptr()), Ct.shape[2],
+                             Ct.shape[1] * Ct.shape[2], nb, C.c_void_p(torch.cuda.current_stream(Ct.device).cuda_stream))
+    if rc:
+        raise RuntimeError(f"bddc_dense_gemm failed ({rc})")
 
 
 def box_of_subdomains(subs, coarsening) -> np.ndarray:
