@@ -681,7 +681,10 @@ __device__ void solve_tv_task(int sub, const TvArgs& tv, SolveShared& sh) {
   }
 }
 
-__global__ void __launch_bounds__(256, 3) coop_solve_df_kernel(FrontDev fd, LevelView lv, SolveProgram sp,
+#ifndef BDDC_SOLVE_CTAS
+#define BDDC_SOLVE_CTAS 3  // A/B compile switch: resident CTAs per SM of the coarse solve
+#endif
+__global__ void __launch_bounds__(256, BDDC_SOLVE_CTAS) coop_solve_df_kernel(FrontDev fd, LevelView lv, SolveProgram sp,
                                                             const SdTask* __restrict__ tasks, int ntasks,
                                                             int* ctr, int* qhead, int* err,
                                                             const double* __restrict__ rhs,
