@@ -131,10 +131,16 @@ int bddc_coarse_solve(bddc_ctx* ctx, const double* rhs_dev, double* sol_dev, voi
    when set, bddc_apply / bddc_pcg call fn in place of the exact coarse solve, with device
    vectors of n_coarse in elimination order and the stream the apply runs on (fn must order
    its work on that stream); fn returns 0 on success. NULL restores the direct solve.
-   Single-rank operators only. */
+   Single-rank operators only. While the hook is installed, bddc_refactor skips the coarse
+   assembly and factorization (3D path; the 2D path keeps it: its local T tiles run inside that
+   engine); after such a refactor and NULL, applies fail until the next bddc_refactor. */
 typedef int (*bddc_coarse_solver_fn)(void* user, const double* rhs_dev, double* sol_dev, long long n_coarse,
                                      void* stream);
 int bddc_set_coarse_solver(bddc_ctx* ctx, bddc_coarse_solver_fn fn, void* user);
+/* device pointer to the coarse element matrices S_0i = Psi_i^T A_i Psi_i of the last setup
+   (nsub blocks of nc_pad x nc_pad, symmetric; bddc.py:494-505 sums them into S_0); valid until
+   the next setup / refactor / destroy. The stream is synchronized first. */
+const double* bddc_coarse_elements(bddc_ctx* ctx, long long* count);
 int bddc_kernel_launches_per_apply(bddc_ctx* ctx);
 /* measurement: kernels launched by this library so far (process-wide); CUDA events on the
    context stream (slots 0..7); optional per-phase event timers ("apply.bt_solve",
@@ -244,6 +250,12 @@ int bddc_dense_trsm(int kind, const double* L, int n, int ldl, long long sL, dou
 int bddc_dense_gemm(int transA, int transB, int M, int N, int K, double alpha, const double* A,
                     int lda, long long sA, const double* B, int ldb, long long sB, double beta,
                     double* C, int ldc, long long sC, int count, void* stream);
+
+/* batched y = alpha A^T x + beta y: A column-major k x n (lda >= k even, 16-byte aligned, even
+   stride, finite padding), x of k and y of n doubles per batch entry; equivalently the row-major n x k matrix
+   times x. HBM-bound (each entry of A read once). Used by the three-level prototype's apply. */
+int bddc_dense_gemv_t(int k, int n, double alpha, const double* A, int lda, long long sA, const double* x,
+                      long long sx, double beta, double* y, long long sy, int count, void* stream);
 
 #ifdef __cplusplus
 }

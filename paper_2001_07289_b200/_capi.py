@@ -31,8 +31,8 @@ EXPORTS = (
     "bddc_kernel_launches_per_apply", "bddc_debug_copy", "bddc_launch_count",
     "bddc_event_record", "bddc_event_elapsed_ms", "bddc_profile", "bddc_profile_read",
     "bddc_nccl_unique_id", "bddc_nccl_selftest", "bddc_comm_init_nccl", "bddc_comm_init_host", "bddc_partition_info",
-    "bddc_dense_potrf", "bddc_dense_trsm", "bddc_dense_gemm", "bddc_check", "bddc_update_weights",
-    "bddc_coarse_solve", "bddc_set_coarse_solver", "bddc_read_buffer", "bddc_coarse_pattern",
+    "bddc_dense_potrf", "bddc_dense_trsm", "bddc_dense_gemm", "bddc_dense_gemv_t", "bddc_check", "bddc_update_weights",
+    "bddc_coarse_solve", "bddc_set_coarse_solver", "bddc_coarse_elements", "bddc_read_buffer", "bddc_coarse_pattern",
     "bddc_index_build", "bddc_index_size", "bddc_index_copy", "bddc_index_free", "bddc_coarse_csr",
     "bddc_layout_tables", "bddc_nd_build", "bddc_nd_size", "bddc_nd_copy", "bddc_nd_free",
 )
@@ -106,6 +106,8 @@ def load(required: bool = True):
     lib.bddc_update_weights.argtypes = [_vp, _pd, C.c_char_p, C.c_size_t]
     lib.bddc_coarse_solve.argtypes = [_vp, _vp, _vp, _vp]
     lib.bddc_set_coarse_solver.argtypes = [_vp, COARSE_SOLVER_FN, _vp]
+    lib.bddc_coarse_elements.argtypes = [_vp, _pll]
+    lib.bddc_coarse_elements.restype = C.c_void_p
     lib.bddc_kernel_launches_per_apply.argtypes = [_vp]
     lib.bddc_debug_copy.argtypes = [_vp, C.c_char_p, _pd, _ll]
     lib.bddc_debug_copy.restype = _ll
@@ -147,6 +149,7 @@ def load(required: bool = True):
     lib.bddc_dense_trsm.argtypes = [_i, _vp, _i, _i, _ll, _vp, _i, _i, _ll, _i, _vp]
     lib.bddc_dense_gemm.argtypes = [_i, _i, _i, _i, _i, _d, _vp, _i, _ll, _vp, _i, _ll, _d, _vp,
                                     _i, _ll, _i, _vp]
+    lib.bddc_dense_gemv_t.argtypes = [_i, _i, _d, _vp, _i, _ll, _vp, _ll, _d, _vp, _ll, _i, _vp]
     _lib = lib
     return lib
 

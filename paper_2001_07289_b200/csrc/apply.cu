@@ -736,6 +736,8 @@ void apply_bddc(Ctx& c, const double* r, double* z, cudaStream_t s) {
         if (c.coarse_cb(c.coarse_cb_user, c.crhs, c.csol, c.fp.n_coarse, (void*)s) != 0)
           throw CudaError("coarse solver callback failed");
       } else {
+        if (!c.coarse_factor_valid)
+          throw CudaError("no exact coarse factor: the last refactor ran under the coarse-solver hook (refactor again)");
         coarse_solve(c, c.crhs, c.csol, s, tv_fused ? &tv : nullptr);
       }
     }

@@ -79,7 +79,11 @@ void numeric_setup(bddc_ctx* h) {
   // sharded: every rank assembles the replicated coarse matrix from all local blocks
   allgather_subs(c, c.Sloc, (long long)c.geo.nc_pad * c.geo.nc_pad, s);
   BDDC_CUDA(cudaEventRecord(e1, s));
-  coarse_assemble_and_factor(c);
+  // three-level hook installed (bddc_set_coarse_solver): the exact coarse factor is never used,
+  // so a re-setup skips its assembly and factorization, unless the local T tiles are
+  // deferred into that engine (lt_defer: the 2D path)
+  c.coarse_factor_valid = !(c.coarse_cb && !c.lt_defer.on && c.setup_done);
+  if (c.coarse_factor_valid) coarse_assemble_and_factor(c);
   BDDC_CUDA(cudaEventRecord(e2, s));
   BDDC_CUDA(cudaEventSynchronize(e2));
   BDDC_CUDA(cudaEventElapsedTime(&c.t_local_ms, e0, e1));
@@ -814,6 +818,7 @@ int bddc_coarse_solve(bddc_ctx* h, const double* rhs, double* sol, void* stream)
   return guarded(nullptr, 0, [&] {
     BDDC_CUDA(cudaSetDevice(h->c.device));
     if (h->c.fp.n_coarse == 0) return;
+    if (!h->c.coarse_factor_valid) throw ApiError{1, "the exact coarse factor was skipped under the coarse-solver hook"};
     on_stream(h, stream, [&](cudaStream_t s) { coarse_solve(h->c, rhs, sol, s, nullptr); });
   });
 }
@@ -908,6 +913,13 @@ long long bddc_coarse_csr(bddc_ctx* h, long long* row, long long* col, long long
   return fp.nnz;
 }
 
+const double* bddc_coarse_elements(bddc_ctx* h, long long* count) {
+  if (!h || !h->c.setup_done || !h->c.Sloc) return nullptr;
+  if (cudaSetDevice(h->c.device) != cudaSuccess || cudaStreamSynchronize(h->c.stream) != cudaSuccess) return nullptr;
+  if (count) *count = (long long)h->c.geo.nsub * h->c.geo.nc_pad * h->c.geo.nc_pad;
+  return h->c.Sloc;
+}
+
 long long bddc_read_buffer(bddc_ctx* h, const char* name, long long offset, long long count, double* host) {
   if (!h || !name) return -1;
   const Ctx& c = h->c;
@@ -992,6 +1004,14 @@ int bddc_dense_gemm(int tA, int tB, int M, int N, int K, double alpha, const dou
   return guarded(nullptr, 0, [&] {
     gemm_batched(tA != 0, tB != 0, M, N, K, alpha, BMat{(double*)A, sA, lda}, BMat{(double*)B, sB, ldb},
                  beta, BMat{C, sC, ldc}, count, (cudaStream_t)stream);
+  });
+}
+
+int bddc_dense_gemv_t(int k, int n, double alpha, const double* A, int lda, long long sA, const double* x,
+                      long long sx, double beta, double* y, long long sy, int count, void* stream) {
+  if (!A || !x || !y || k <= 0 || lda < k || (lda & 1) || (sA & 1) || ((uintptr_t)A & 15)) return 1;
+  return guarded(nullptr, 0, [&] {
+    gemv_t_batched(k, n, alpha, BMat{(double*)A, sA, lda}, x, sx, beta, y, sy, count, (cudaStream_t)stream);
   });
 }
 

@@ -408,4 +408,64 @@ void trsm_batched(TrsmKind kind, BMat L, int n, BMat B, int nother, int count, d
   }
 }
 
+// Batched y = alpha A^T x + beta y for column-major k x n operands (lda >= k, even): every
+// output entry is a dot product over one contiguous column of A, i.e. over one row of the
+// row-major n x k matrix a torch tensor holds. HBM-bound: each entry of A is read once with
+// 16-byte loads (lda even, 16-byte aligned bases), x of the batch entry sits in shared memory,
+// one warp per output entry, kGemvRows entries per CTA, fixed summation order.
+namespace {
+constexpr int kGemvWarps = 8, kGemvRows = 32;
+__global__ void __launch_bounds__(32 * kGemvWarps) gemv_t_kernel(int k, int n, double alpha,
+                                                                 const double* __restrict__ A, int lda,
+                                                                 long long sA, const double* __restrict__ x,
+                                                                 long long sx, double beta,
+                                                                 double* __restrict__ y, long long sy) {
+  extern __shared__ double xs[];
+  const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* xb = x + (long long)b * sx;
+  for (int i = tid; i < k; i += blockDim.x) xs[i] = xb[i];
+  if (tid == 0 && (k & 1)) xs[k] = 0.0;
+  __syncthreads();
+  const double* Ab = A + (long long)b * sA;
+  double* yb = y + (long long)b * sy;
+  const int j0 = blockIdx.x * kGemvRows;
+  const int k2 = (k + 1) >> 1;  // pairs; a column's padding element (lda even) meets xs[k] = 0
+  for (int jj = warp; jj < kGemvRows; jj += kGemvWarps) {
+    const int j = j0 + jj;
+    if (j >= n) break;
+    const double2* col = reinterpret_cast<const double2*>(Ab + (long long)j * lda);
+    double a0 = 0.0, a1 = 0.0;
+    int p = lane;
+    for (; p + 32 < k2; p += 64) {
+      const double2 u = __ldcs(col + p), v = __ldcs(col + p + 32);
+      a0 += u.x * xs[2 * p] + u.y * xs[2 * p + 1];
+      a1 += v.x * xs[2 * p + 64] + v.y * xs[2 * p + 65];
+    }
+    if (p < k2) {
+      const double2 u = __ldcs(col + p);
+      const double ux = u.x, uy = (2 * p + 1 < k) ? u.y : 0.0;
+      a0 += ux * xs[2 * p] + uy * xs[2 * p + 1];
+    }
+    double acc = a0 + a1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) yb[j] = beta == 0.0 ? alpha * acc : alpha * acc + beta * yb[j];
+  }
+}
+}  // namespace
+
+void gemv_t_batched(int k, int n, double alpha, BMat A, const double* x, long long sx, double beta, double* y,
+                    long long sy, int count, cudaStream_t s) {
+  if (n <= 0 || count <= 0) return;
+  const size_t smem = sizeof(double) * (size_t)(k + 2);
+  if (smem > 200 * 1024) throw CudaError("gemv_t_batched: x does not fit shared memory");
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr))
+    BDDC_CUDA(cudaFuncSetAttribute(gemv_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  dim3 grid(ceil_div(n, kGemvRows), count);
+  gemv_t_kernel<<<grid, 32 * kGemvWarps, smem, s>>>(k, n, alpha, A.p, A.ld, A.stride, x, sx, beta, y, sy);
+  BDDC_LAUNCH_CHECK();
+  BDDC_COUNT();
+}
+
 }  // namespace bddc

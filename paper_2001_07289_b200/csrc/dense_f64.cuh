@@ -95,6 +95,9 @@ void trsm_batched(TrsmKind kind, BMat L, int n, BMat B, int nother, int count, d
 size_t trsm_scratch_doubles(int n, int count);
 // C = alpha op(A) op(B) + beta C over a strided batch.
 // klo (optional, ceil(M/64) <= 16 entries): first nonzero K of op(A)'s 64-row tile i.
+// y = alpha A^T x + beta y, A column-major k x n per batch entry (dot products over contiguous columns)
+void gemv_t_batched(int k, int n, double alpha, BMat A, const double* x, long long sx, double beta, double* y,
+                    long long sy, int count, cudaStream_t s);
 void gemm_batched(bool tA, bool tB, int M, int N, int K, double alpha, BMat A, BMat B,
                   double beta, BMat C, int count, cudaStream_t s, bool lower = false, int tri = 0,
                   bool mirror = false, const int* klo = nullptr);

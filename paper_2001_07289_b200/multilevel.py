@@ -123,52 +123,83 @@ class Level2Bddc:
         Cmat = t(Cm, torch.float64)
         nIp, nGp, nCp = idxI.shape[1], idxG.shape[1], idxC.shape[1]
 
-        # ---- numeric: assemble each box, Schur complement on Γ₂, constrained solves ----
-        AII = torch.zeros((nbox, nIp, nIp), dtype=torch.float64, device=dev)
-        AIG = torch.zeros((nbox, nIp, nGp), dtype=torch.float64, device=dev)
-        AGG = torch.zeros((nbox, nGp, nGp), dtype=torch.float64, device=dev)
-        eorder = np.argsort(box_of_elem, kind="stable")
-        eptr = np.concatenate([[0], np.cumsum(np.bincount(box_of_elem, minlength=nbox))])
-        pos = np.empty(n0 + 1, dtype=np.int64)
+        # ---- numeric: assemble every box at once, Schur complement on Γ₂, constrained solves ----
+        # local position of each (dof, box) incidence: interior dofs first, then the interface
+        nJ = nIp + nGp
+        inc_pos = np.empty(len(key), dtype=np.int64)
         for J in range(nbox):
-            ni, ng = len(I_of[J]), len(G_of[J])
-            nJ = nIp + nGp
-            pos[:] = nJ  # dummy row / column for padding
-            pos[I_of[J]] = np.arange(ni)
-            pos[G_of[J]] = nIp + np.arange(ng)
-            el = eorder[eptr[J]:eptr[J + 1]]
-            loc = t(pos[np.where(ids[el] >= 0, ids[el], n0)])  # (m, ncp)
-            A = torch.zeros((nJ + 1, nJ + 1), dtype=torch.float64, device=dev)
-            A.index_put_((loc[:, :, None].expand(-1, -1, ncp), loc[:, None, :].expand(-1, ncp, -1)),
-                         mats[t(el)], accumulate=True)
-            AII[J], AIG[J], AGG[J] = A[:nIp, :nIp], A[:nIp, nIp:nJ], A[nIp:nJ, nIp:nJ]
-            padI = torch.arange(ni, nIp, device=dev)
-            AII[J, padI, padI] = 1.0
-            padG = torch.arange(ng, nGp, device=dev)
-            AGG[J, padG, padG] = 1.0
+            sl = order[bptr[J]:bptr[J + 1]]
+            isl = inter[sl]
+            inc_pos[sl[~isl]] = np.arange(int((~isl).sum()))
+            inc_pos[sl[isl]] = nIp + np.arange(int(isl.sum()))
+        ekey = np.where(valid, ids * nbox + ebox, -1)
+        loc = np.where(valid, inc_pos[np.searchsorted(key, np.maximum(ekey, 0))], nJ)  # (E, ncp); padding -> dummy
+        flat = (box_of_elem[:, None, None] * (nJ + 1) + loc[:, :, None]) * (nJ + 1) + loc[:, None, :]
+        self._flat = t(flat.reshape(-1))
+        del flat
+        self._Cmat = Cmat
+        self._ngs = t(np.array([max(len(g), 1) for g in G_of]), torch.float64)
+        self._dims = (nbox, nIp, nGp, nCp, nJ, nobj, E, ncp)
+        self.refactor(mats)
+
+    def refactor(self, elem_mats):
+        """Numeric setup for new element matrices on the same elements / boxes (the symbolic
+        part above is kept)."""
+        torch = self._torch
+        dev, n0 = self.device, self.n0
+        nbox, nIp, nGp, nCp, nJ, nobj, E, ncp = self._dims
+        mats = torch.as_tensor(elem_mats, dtype=torch.float64).to(dev)
+        if mats.shape != (E, ncp, ncp):
+            raise ValueError(f"element matrices have shape {tuple(mats.shape)}, expected {(E, ncp, ncp)}")
+        Cmat, ngs = self._Cmat, self._ngs
+        Aall = torch.zeros(nbox * (nJ + 1) * (nJ + 1), dtype=torch.float64, device=dev)
+        Aall.index_add_(0, self._flat, mats.reshape(-1))
+        Aall = Aall.view(nbox, nJ + 1, nJ + 1)
+        AII = Aall[:, :nIp, :nIp].clone()
+        AIG = Aall[:, :nIp, nIp:nJ].clone()
+        AGG = Aall[:, nIp:nJ, nIp:nJ].clone()
+        del Aall
+        AII += torch.diag_embed((self.idxI >= n0).to(torch.float64))  # identity on the padding
+        AGG += torch.diag_embed((self.idxG >= n0).to(torch.float64))
         AII = 0.5 * (AII + AII.transpose(1, 2))
-        ngs = t(np.array([max(len(g), 1) for g in G_of]), torch.float64)
         validG = (self.idxG < n0).to(torch.float64)
-        CtC = Cmat.transpose(1, 2) @ Cmat
         if dev.type == "cuda":
             # the O(n^3) work on this library's batched FP64 kernels (dense_f64.cu: DMMA tile
             # Cholesky, tile-inverse triangular solves, GEMM). A symmetric batch is its own
             # column-major image; potrf leaves L in the column-major lower triangle, which the
             # torch view reads as the upper factor U = L^T (upper=True below).
             self.upper = True
-            self.LI = _own_potrf(torch, AII.contiguous())
-            Xt = AIG.transpose(1, 2).contiguous()        # column-major n_I x n_G, one box each
-            _own_trsm(torch, 0, self.LI, Xt)             # L y = A_IG
-            _own_trsm(torch, 1, self.LI, Xt)             # L^T X = y
-            S = AGG.contiguous()                         # S = A_GG - A_IG^T X
-            _own_gemm(torch, True, False, -1.0, AIG.transpose(1, 2).contiguous(), Xt, 1.0, S)
-            S = 0.5 * (S + S.transpose(1, 2))
+            AGI = AIG.transpose(1, 2).contiguous()       # column-major n_I x n_G, one box each
+            LI = _own_potrf(torch, AII)                  # in place
+            Xt = AGI.clone()
+            _own_trsm(torch, 0, LI, Xt)                  # L y = A_IG
+            _own_trsm(torch, 1, LI, Xt)                  # L^T X = y
+            S = AGG                                      # S = A_GG - A_IG^T X, in place
+            _own_gemm(torch, True, False, -1.0, AGI, Xt, 1.0, S)
+            del Xt
+            S.add_(S.transpose(1, 2).clone()).mul_(0.5)
             s = (torch.diagonal(S, dim1=1, dim2=2) * validG).sum(1) / ngs  # mean diagonal per box
-            self.LK = _own_potrf(torch, (S + s[:, None, None] * CtC).contiguous())
+            Cs = Cmat * torch.sqrt(s)[:, None, None]
+            S.baddbmm_(Cs.transpose(1, 2), Cs)           # K = S + s C^T C, in place
+            del Cs
+            LK = _own_potrf(torch, S)
             Yt = Cmat.clone()                            # column-major n_G x n_C = C^T
-            _own_trsm(torch, 0, self.LK, Yt)
-            _own_trsm(torch, 1, self.LK, Yt)
+            _own_trsm(torch, 0, LK, Yt)
+            _own_trsm(torch, 1, LK, Yt)
             Y = Yt.transpose(1, 2).contiguous()          # K^{-1} C^T
+            del Yt
+            # explicit symmetric inverses, so that the apply is batched matrix-vector products
+            eyeI = torch.eye(nIp, dtype=torch.float64, device=dev).expand(nbox, -1, -1).contiguous()
+            _own_trsm(torch, 0, LI, eyeI)
+            _own_trsm(torch, 1, LI, eyeI)
+            del LI, AII
+            self.AIIinv = eyeI.add_(eyeI.transpose(1, 2).clone()).mul_(0.5)
+            eyeG = torch.eye(nGp, dtype=torch.float64, device=dev).expand(nbox, -1, -1).contiguous()
+            _own_trsm(torch, 0, LK, eyeG)
+            _own_trsm(torch, 1, LK, eyeG)
+            del LK, S, AGG
+            self.Kinv = eyeG
+            self.AGI = AGI
         else:  # CPU evaluation of the same formulas (the tests' checker of the device level 2)
             self.upper = False
             self.LI = torch.linalg.cholesky(AII)
@@ -176,7 +207,7 @@ class Level2Bddc:
             S = AGG - AIG.transpose(1, 2) @ X
             S = 0.5 * (S + S.transpose(1, 2))
             s = (torch.diagonal(S, dim1=1, dim2=2) * validG).sum(1) / ngs
-            self.LK = torch.linalg.cholesky(S + s[:, None, None] * CtC)
+            self.LK = torch.linalg.cholesky(S + s[:, None, None] * (Cmat.transpose(1, 2) @ Cmat))
             Y = torch.cholesky_solve(Cmat.transpose(1, 2).contiguous(), self.LK)  # K⁻¹Cᵀ
         self.AIG = AIG
         self.s = s
@@ -186,6 +217,11 @@ class Level2Bddc:
         Ginv = torch.linalg.inv(0.5 * (G + G.transpose(1, 2)))
         self.Y = Y
         self.Phi = Y @ Ginv
+        if dev.type == "cuda":  # T2 = K^{-1} - Phi Y^T: the constrained local solve as one matrix
+            T2 = self.Kinv.baddbmm_(self.Phi, Y.transpose(1, 2), alpha=-1.0)
+            del self.Kinv
+            self.T2 = T2.add_(T2.transpose(1, 2).clone()).mul_(0.5)
+            self.PhiT = self.Phi.transpose(1, 2).contiguous()
         Ecoarse = Ginv - s[:, None, None] * torch.eye(nCp, dtype=torch.float64, device=dev)
         S00 = torch.zeros((nobj + 1, nobj + 1), dtype=torch.float64, device=dev)
         S00.index_put_((self.idxC[:, :, None].expand(-1, -1, nCp), self.idxC[:, None, :].expand(-1, nCp, -1)),
@@ -193,6 +229,12 @@ class Level2Bddc:
         S00 = S00[:nobj, :nobj]
         self.S00 = 0.5 * (S00 + S00.T)
         self.L00 = torch.linalg.cholesky(self.S00) if nobj else None
+        self.S00inv = None
+        if dev.type == "cuda" and 0 < nobj <= 8192:  # explicit inverse: the level-2 coarse solve is one GEMV
+            n8 = -(-nobj // 8) * 8
+            inv = torch.cholesky_inverse(self.L00)
+            self.S00inv = torch.zeros((1, n8, n8), dtype=torch.float64, device=dev)
+            self.S00inv[0, :nobj, :nobj] = 0.5 * (inv + inv.T)
 
     def solve(self, r):
         """z ≈ S_0⁻¹ r (torch vector of n0 on ``device``)."""
@@ -200,6 +242,8 @@ class Level2Bddc:
         n0 = self.n0
         zero = torch.zeros(1, dtype=torch.float64, device=self.device)
         rp = torch.cat([r, zero])
+        if self.device.type == "cuda":
+            return self._solve_gemv(rp)
         # interior solves, interface residual
         u1 = torch.cholesky_solve(rp[self.idxI].unsqueeze(2), self.LI, upper=self.upper)  # (B, nI, 1)
         tG = self.AIG.transpose(1, 2) @ u1
@@ -225,6 +269,36 @@ class Level2Bddc:
         zG.index_put_((self.idxI.reshape(-1),), zI.reshape(-1))
         return zG[:n0]
 
+    def _solve_gemv(self, rp):
+        """The same apply with explicit inverses: every large product is one launch of the
+        library's batched GEMV (bddc_dense_gemv_t); torch only gathers and scatters."""
+        torch = self._torch
+        n0, nobj = self.n0, self.n_coarse2
+        mv = lambda M, x: _own_gemv(torch, M, x)  # noqa: E731
+        u1 = mv(self.AIIinv, rp[self.idxI].contiguous())                 # (B, nI)
+        rG = rp.clone()
+        rG.index_add_(0, self.idxG.reshape(-1), -mv(self.AGI, u1).reshape(-1))
+        rG[n0] = 0.0
+        rho = (self.wG * rG[self.idxG]).contiguous()                       # (B, nG)
+        q = mv(self.PhiT, rho)                                             # (B, nC)
+        r00 = torch.zeros(nobj + 1, dtype=torch.float64, device=self.device)
+        r00.index_add_(0, self.idxC.reshape(-1), q.reshape(-1))
+        c = torch.zeros_like(r00)
+        if nobj and self.S00inv is not None:
+            n8 = self.S00inv.shape[1]
+            rr = torch.zeros((1, n8), dtype=torch.float64, device=self.device)
+            rr[0, :nobj] = r00[:nobj]
+            c[:nobj] = mv(self.S00inv, rr)[0, :nobj]
+        elif nobj:  # large level-2 coarse problems: triangular solves with the dense factor
+            c[:nobj] = torch.cholesky_solve(r00[:nobj].unsqueeze(1), self.L00).squeeze(1)
+        w = self.wG * (mv(self.T2, rho) + mv(self.Phi, c[self.idxC].contiguous()))
+        zG = torch.zeros(n0 + 1, dtype=torch.float64, device=self.device)
+        zG.index_add_(0, self.idxG.reshape(-1), w.reshape(-1))
+        zG[n0] = 0.0
+        zI = u1 - mv(self.AIIinv, mv(self.AIG, zG[self.idxG].contiguous()))
+        zG.index_put_((self.idxI.reshape(-1),), zI.reshape(-1))
+        return zG[:n0]
+
     def dense(self):
         """The operator as an explicit matrix (tests, small n0)."""
         torch = self._torch
@@ -247,6 +321,20 @@ def _own_potrf(torch, A):
     if bad:
         raise RuntimeError(f"level-2 matrix of box {bad[0]} is not positive definite (pivot {info[bad[0]]})")
     return A
+
+
+def _own_gemv(torch, M, x):
+    """y[b] = M[b] @ x[b] for a contiguous (B, n, k) tensor and x (B, k): the library's batched
+    GEMV (each row of M is a contiguous column of the column-major k x n operand)."""
+    lib = _capi.load()
+    B, n, k = M.shape
+    y = torch.empty((B, n), dtype=torch.float64, device=M.device)
+    rc = lib.bddc_dense_gemv_t(k, n, 1.0, C.c_void_p(M.data_ptr()), k, n * k, C.c_void_p(x.data_ptr()), k, 0.0,
+                               C.c_void_p(y.data_ptr()), n, B,
+                               C.c_void_p(torch.cuda.current_stream(M.device).cuda_stream))
+    if rc:
+        raise RuntimeError(f"bddc_dense_gemv_t failed ({rc})")
+    return y
 
 
 def _own_trsm(torch, kind, L, Bt):
@@ -318,18 +406,34 @@ class ThreeLevelOperator:
         nsub, ncp = plan.nsub, plan.nc_pad
         n0 = plan.coarse.n
         dev = torch.device(f"cuda:{op.device}")
-        sloc = np.empty(nsub * ncp * ncp)
-        got = op._lib.bddc_read_buffer(op._ctx, b"Sloc", 0, sloc.size, _capi.ptr(sloc, C.c_double))
-        if got != sloc.size:
-            raise RuntimeError("reading the coarse element matrices failed")
-        self.level2 = Level2Bddc(plan.con_coarse, torch.from_numpy(sloc.reshape(nsub, ncp, ncp)),
-                                 box_of_subdomains(subs, coarsening), n0, device=dev)
+        self.level2 = Level2Bddc(plan.con_coarse, self._element_matrices(), box_of_subdomains(subs, coarsening),
+                                 n0, device=dev)
         self.calls = 0
         self._error = None
         self._fn = _capi.COARSE_SOLVER_FN(self._solve)  # keep the thunk alive
         rc = op._lib.bddc_set_coarse_solver(op._ctx, self._fn, None)
         if rc:
             raise RuntimeError("bddc_set_coarse_solver failed (sharded operators are not supported)")
+
+    def _element_matrices(self):
+        """S_0i of every subdomain, a zero-copy view of the device setup's blocks
+        (bddc_coarse_elements: nsub x nc_pad x nc_pad)."""
+        import torch
+
+        plan = self.op.plan
+        cnt = C.c_longlong(0)
+        ptr = self.op._lib.bddc_coarse_elements(self.op._ctx, C.byref(cnt))
+        if not ptr or cnt.value != plan.nsub * plan.nc_pad * plan.nc_pad:
+            raise RuntimeError("the coarse element matrices are not available")
+        v = torch.as_tensor(_DevVec(ptr, cnt.value, False), device=torch.device(f"cuda:{self.op.device}"))
+        return v.view(plan.nsub, plan.nc_pad, plan.nc_pad)
+
+    def refactor(self, alpha=None):
+        """New coefficient on the same partition: the level-1 numeric setup, then the level-2
+        numeric setup from the new coarse element matrices (both symbolic parts are kept)."""
+        self.op.refactor(alpha)  # under the hook the 3D path skips the exact coarse factorization
+        self._refactored = True
+        self.level2.refactor(self._element_matrices())
 
     def _solve(self, user, rhs, sol, n, stream):
         try:
@@ -347,11 +451,17 @@ class ThreeLevelOperator:
             return 1
 
     def restore(self):
+        """Back to the two-level operator (the exact coarse factor is rebuilt if a refactor under
+        the hook skipped it)."""
         if self.op is not None and getattr(self.op, "_ctx", None):
             self.op._lib.bddc_set_coarse_solver(self.op._ctx, _capi.COARSE_SOLVER_FN(), None)  # NULL: direct solve
+            if getattr(self, "_refactored", False):
+                self._refactored = False
+                self.op.refactor()
 
     def close(self):
-        self.restore()
+        if getattr(self.op, "_ctx", None):
+            self.op._lib.bddc_set_coarse_solver(self.op._ctx, _capi.COARSE_SOLVER_FN(), None)
         self.op.close()
 
     def __getattr__(self, name):  # apply, matvec, pcg, n, … of the wrapped operator

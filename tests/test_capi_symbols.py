@@ -11,7 +11,7 @@ from conftest import ROOT
 
 def _declared():
     hdr = open(os.path.join(ROOT, "include", "bddcso_b200.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|void|long long|double)\s+(bddc_\w+)\s*\(", hdr, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|void|long long|double|const double\s*\*)\s*(bddc_\w+)\s*\(", hdr, re.M)))
 
 
 def test_header_lists_entry_points():

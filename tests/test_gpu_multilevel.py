@@ -61,6 +61,11 @@ def test_three_level_operator(cuda_ok, case, k, extra):
     b = cpu.solve(r0)
     assert float((a - b).abs().max()) <= 1e-9 * float(b.abs().max())
 
+    # numeric-only refactor on the same symbolic data reproduces the operator
+    t.refactor()
+    a2 = L2.solve(r0.to(L2.device)).cpu()
+    assert float((a2 - a).abs().max()) <= 1e-11 * float(a.abs().max())
+
     t.restore()
     assert np.array_equal(op.apply(r), z2)
     op.close()
