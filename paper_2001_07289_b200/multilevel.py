@@ -24,13 +24,13 @@ Tu (2007) / Mandel, Sousedík, Dohrmann (2008):
 hook ``bddc_set_coarse_solver``: the level-1 apply and the fused device PCG then call it in place
 of the multifrontal coarse solve, on the library's stream.
 
-Status: a prototype of the outlook, not a reference feature. On the GPU the level-2 setup's
-factorizations, multi-right-hand-side triangular solves and Schur-complement product run on this
-library's batched FP64 kernels (bddc_dense_potrf / trsm / gemm); the apply's single-vector solves
-and the gathers / scatters go through torch (library kernels). It is not part of the benchmarked
-path. On a CPU device the same formulas run through torch: that evaluation is the tests' checker. No reference exists to pin it: the tests check the
-properties the method guarantees (symmetry, positive definiteness, a bounded condition number of
-the preconditioned coarse problem, PCG convergence to the two-level solution).
+Status: a prototype of the outlook, not a reference feature and not on the benchmarked path.
+On the GPU the level-2 numeric setup (batched Cholesky, triangular solves, Schur complement,
+explicit inverses) and the apply's matrix-vector products run on this library's own batched FP64
+kernels (bddc_dense_potrf / trsm / gemm / gemv_t); torch does the gathers / scatters and the
+dense factorization of the small level-2 coarse matrix. While the hook is installed, a re-setup
+of the 3D path skips the exact coarse factorization (DESIGN.md §10a has the measurements). On a
+CPU device the same formulas run through torch: that evaluation is the tests' checker.
 """
 
 from __future__ import annotations
