@@ -133,7 +133,9 @@ int bddc_coarse_solve(bddc_ctx* ctx, const double* rhs_dev, double* sol_dev, voi
    its work on that stream); fn returns 0 on success. NULL restores the direct solve.
    Single-rank operators only. While the hook is installed, bddc_refactor skips the coarse
    assembly and factorization (3D path; the 2D path keeps it: its local T tiles run inside that
-   engine); after such a refactor and NULL, applies fail until the next bddc_refactor. */
+   engine); after such a refactor and NULL, applies fail until the next bddc_refactor.
+   Installed BEFORE bddc_setup, the setup builds no coarse plan at all (no front memory, no
+   schedules, no factorization): such a context can only apply through the hook. */
 typedef int (*bddc_coarse_solver_fn)(void* user, const double* rhs_dev, double* sol_dev, long long n_coarse,
                                      void* stream);
 int bddc_set_coarse_solver(bddc_ctx* ctx, bddc_coarse_solver_fn fn, void* user);

@@ -380,6 +380,7 @@ struct Ctx {
   // three-level hook (bddc_set_coarse_solver): replaces the exact coarse solve of the apply
   bddc_coarse_solver_fn coarse_cb = nullptr;
   void* coarse_cb_user = nullptr;
+  bool coarse_lean = false;          // set up under the hook: no coarse plan, fronts or factor exist
   bool coarse_factor_valid = true;  // false after a re-setup under the hook skipped the factorization
   // timing of the last setup (ms) per phase
   float t_local_ms = 0, t_coarse_ms = 0, t_upload_ms = 0;

@@ -82,7 +82,7 @@ void numeric_setup(bddc_ctx* h) {
   // three-level hook installed (bddc_set_coarse_solver): the exact coarse factor is never used,
   // so a re-setup skips its assembly and factorization, unless the local T tiles are
   // deferred into that engine (lt_defer: the 2D path)
-  c.coarse_factor_valid = !(c.coarse_cb && !c.lt_defer.on && c.setup_done);
+  c.coarse_factor_valid = !(c.coarse_lean || (c.coarse_cb && !c.lt_defer.on && c.setup_done));
   if (c.coarse_factor_valid) coarse_assemble_and_factor(c);
   BDDC_CUDA(cudaEventRecord(e2, s));
   BDDC_CUDA(cudaEventSynchronize(e2));
@@ -172,6 +172,19 @@ void build_plan(Ctx& c, const bddc_setup_desc* d) {
   fp.nnodes = d->nnodes;
   fp.W = c.geo.npe;
   if (fp.n_coarse == 0) return;
+  // three-level operators (hook installed before the setup): the coarse problem is never
+  // factored, so no front memory, schedules or assembly pattern are built; the apply only
+  // needs the gather of the coarse right-hand side
+  c.coarse_lean = c.coarse_cb != nullptr;
+  if (c.coarse_lean) {
+    if (c.tp) throw ApiError{1, "three-level operators are single-rank"};
+    fp.nnodes = 0;
+    fp.nlevels = 0;
+    c.lt_fusable = false;
+    c.sched = LevelSchedule{};
+    fp.coarse_slots = c.upload(d->coarse_slots, (size_t)d->n_coarse * fp.W);
+    return;
+  }
   const int N = fp.nnodes;
   fp.sep_start.assign(d->node_sep_start, d->node_sep_start + N);
   fp.sep_size.assign(d->node_sep_size, d->node_sep_size + N);
@@ -463,6 +476,9 @@ void do_setup(bddc_ctx* h, const bddc_setup_desc* d) {
   BDDC_CUDA(cudaMemGetInfo(&free_b, &total_b));
   const size_t per = local_setup_workspace(G, 1);
   size_t want = per * nl;
+  // three-level operators leave the memory to the level 2 (chunks of 4,096 subdomains run the
+  // local chain at the same rate: cfg3 is one such chunk)
+  if (c.coarse_lean) want = std::min(want, per * (size_t)4096);
   size_t cap = (size_t)(0.6 * free_b) / sizeof(double);
   size_t use = std::min(want, std::max(cap - cap % per, per));
   h->ws = c.alloc<double>(use);

@@ -393,27 +393,58 @@ class ThreeLevelOperator:
     ``close()`` (or ``restore()``) puts the direct solve back.
     """
 
-    def __init__(self, op, coarsening=2):
-        import torch
-
+    def __init__(self, op, coarsening=2, _setup_under_hook=False):
         self.op = op
-        plan = op.plan
-        if plan.coarse is None:
+        self.coarsening = coarsening
+        self.lean = bool(_setup_under_hook)
+        self.calls = 0
+        self._error = None
+        self.level2 = None
+        if op.plan.coarse is None:
             raise ValueError("the operator has no coarse problem")
         if op.pair.box_layout is None:
             raise ValueError("three-level BDDC-SO needs a uniform box partition Θ")
-        subs = op.pair.box_layout[0]
-        nsub, ncp = plan.nsub, plan.nc_pad
-        n0 = plan.coarse.n
-        dev = torch.device(f"cuda:{op.device}")
-        self.level2 = Level2Bddc(plan.con_coarse, self._element_matrices(), box_of_subdomains(subs, coarsening),
-                                 n0, device=dev)
-        self.calls = 0
-        self._error = None
         self._fn = _capi.COARSE_SOLVER_FN(self._solve)  # keep the thunk alive
-        rc = op._lib.bddc_set_coarse_solver(op._ctx, self._fn, None)
+        if _setup_under_hook:  # hook first: the setup then builds no coarse plan, fronts or factor
+            self._install()
+            op._setup()
+            self._build_level2()
+        else:                  # an operator that is already set up (it keeps its exact factor)
+            self._build_level2()
+            self._install()
+
+    @classmethod
+    def build(cls, system, pair, objects, recipe, weights, coarsening=2, coarse_scaling="reference", device=0):
+        """Three-level operator from nothing (the arguments of ``build_bddc``): the hook is
+        installed before the setup, so the coarse problem is never planned, allocated or
+        factored; only the level-1 local setup and the level 2 run."""
+        from . import bddc as _b
+        from .layout import build_device_plan
+        from .weights import Recipe, select_constraints
+
+        if isinstance(recipe, str):
+            recipe = Recipe.parse(recipe)
+        if coarse_scaling not in _b.COARSE_SCALINGS:
+            raise ValueError(f"unknown coarse_scaling {coarse_scaling!r}; expected {_b.COARSE_SCALINGS}")
+        if pair.box_layout is None:
+            raise ValueError("three-level BDDC-SO needs a uniform box partition Θ")
+        constraints = select_constraints(objects, recipe, pair)
+        plan = build_device_plan(pair, constraints, weights, coarse_pattern="device", device=device)
+        op = _b.BddcOperator(system, pair, weights, recipe, constraints, plan, coarse_scaling, device, None)
+        return cls(op, coarsening, _setup_under_hook=True)
+
+    def _install(self):
+        rc = self.op._lib.bddc_set_coarse_solver(self.op._ctx, self._fn, None)
         if rc:
             raise RuntimeError("bddc_set_coarse_solver failed (sharded operators are not supported)")
+
+    def _build_level2(self):
+        import torch
+
+        op, plan = self.op, self.op.plan
+        self.level2 = Level2Bddc(plan.con_coarse, self._element_matrices(),
+                                 box_of_subdomains(op.pair.box_layout[0], self.coarsening), plan.coarse.n,
+                                 device=torch.device(f"cuda:{op.device}"))
 
     def _element_matrices(self):
         """S_0i of every subdomain, a zero-copy view of the device setup's blocks
@@ -453,6 +484,8 @@ class ThreeLevelOperator:
     def restore(self):
         """Back to the two-level operator (the exact coarse factor is rebuilt if a refactor under
         the hook skipped it)."""
+        if self.lean:
+            raise RuntimeError("this operator was set up under the hook: it has no exact coarse factor to restore")
         if self.op is not None and getattr(self.op, "_ctx", None):
             self.op._lib.bddc_set_coarse_solver(self.op._ctx, _capi.COARSE_SOLVER_FN(), None)  # NULL: direct solve
             if getattr(self, "_refactored", False):

@@ -87,3 +87,27 @@ def test_three_level_iteration_report(cuda_ok, capsys):
         for r in rows:
             print("three-level: %s k=%d n0=%d boxes/nI/nG/nC=%s n00=%d | two-level its %d kappa %.4f | "
                   "three-level its %d kappa %.4f" % r)
+
+
+@pytest.mark.parametrize("case,k", [("cfg3c_p1_ref", 2), ("cfg2c_p1_L4h", 4), ("cfg5a_p1_ref", 3)])
+def test_three_level_built_under_hook(cuda_ok, case, k):
+    """ThreeLevelOperator.build: the hook is installed before the setup, so no coarse plan,
+    front memory or factorization exists; same iterates as wrapping a two-level operator."""
+    g = load_golden(case)
+    pb, op = _op(g)
+    tw = P.ThreeLevelOperator(op, coarsening=k)
+    xw, repw = P.pcg(tw.matvec, tw.apply, g["b"], tol=float(g["tol"]), max_iters=2000)
+    tw.close()
+    t = P.ThreeLevelOperator.build(pb["system"], pb["pair"], pb["objects"], pb["recipe"], pb["weights"],
+                                   coarsening=k, coarse_scaling=pb["mode"])
+    assert t.lean and t.op.stats().t_coarse_ms == 0.0
+    x, rep = P.pcg(t.matvec, t.apply, g["b"], tol=float(g["tol"]), max_iters=2000)
+    assert rep.converged and rep.iterations == repw.iterations
+    assert np.linalg.norm(x - xw) <= 1e-9 * np.linalg.norm(xw)
+    assert np.linalg.norm(x - g["x"]) <= 1e-5 * np.linalg.norm(g["x"])
+    t.refactor()
+    x2, rep2 = P.pcg(t.matvec, t.apply, g["b"], tol=float(g["tol"]), max_iters=2000)
+    assert rep2.iterations == rep.iterations and np.linalg.norm(x2 - x) <= 1e-9 * np.linalg.norm(x)
+    with pytest.raises(RuntimeError):
+        t.restore()
+    t.close()
