@@ -572,9 +572,43 @@ def run_ours(args, rank, world, local_rank):
                     "(first_setup_s), one pcg (solve_s)"},
         "phases": phase_out,
     }
+    op.close()
+    if rank == 0 and world == 1 and args.workload == "cfg5" and not args.no_three_level:
+        line["three_level"] = three_level_extra(args.workload)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    op.close()
+
+
+def three_level_extra(workload):
+    """Extra field of the cfg5 line: the three-level BDDC-SO prototype on the same
+    workload, run by tools/three_level_bench.py in a child process after this process released
+    its operator (a failure there cannot touch the line). It is the paper's outlook, NOT the
+    reference's method (more iterations, another preconditioner), so it is excluded from
+    value / e2e / roofline and only reported next to them."""
+    import subprocess
+
+    import torch
+
+    try:
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        env = dict(os.environ, PYTORCH_CUDA_ALLOC_CONF="expandable_segments:True")
+        p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "three_level_bench.py"), "--workload",
+                            workload, "--coarsening", "2", "--lean"], capture_output=True, text=True,
+                           timeout=420, env=env)
+        if p.returncode:
+            return {"unavailable": ("exit %d: " % p.returncode) + p.stderr.strip().splitlines()[-1][:200]}
+        d = json.loads(p.stdout.strip().splitlines()[-1])
+        return {"note": "three-level BDDC-SO prototype (paper's outlook; not the reference's method: excluded "
+                        "from value / e2e / roofline), one re-setup + PCG to the same rtol, set up without a "
+                        "coarse factorization",
+                "value": d["Mdof_s"], "unit": "Mdof/s", "ms_per_step": d["step_ms"],
+                "setup_ms": d["refactor_ms"], "solve_ms": d["pcg_ms"], "iterations": d["iterations"],
+                "kappa": d["kappa"], "true_residual_rel": d["true_residual_rel"],
+                "level2": d["level2"], "cold_build_s": d["cold_build_s"],
+                "gpu_memory_used_gb": d["gpu_memory_used_gb"]}
+    except Exception as e:  # noqa: BLE001 - an optional extra must never cost the line
+        return {"unavailable": str(e)[:200]}
 
 
 def _sample_alpha(cells, coef):
@@ -723,6 +757,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--workload", default="cfg5", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-three-level", action="store_true",
+                    help="skip the three-level extra field of the cfg5 line (DESIGN.md §10a)")
     ap.add_argument("--cpu-worker", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--cpu-sample", type=int, default=0, help=argparse.SUPPRESS)
     ap.add_argument("--transport", default="nccl", choices=("nccl", "host"),
