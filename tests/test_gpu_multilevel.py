@@ -100,7 +100,7 @@ def test_three_level_built_under_hook(cuda_ok, case, k):
     tw.close()
     t = P.ThreeLevelOperator.build(pb["system"], pb["pair"], pb["objects"], pb["recipe"], pb["weights"],
                                    coarsening=k, coarse_scaling=pb["mode"])
-    assert t.lean and t.op.stats().t_coarse_ms == 0.0
+    assert t.lean and t.op.stats().t_coarse_ms < 0.1  # nothing runs between the two events
     x, rep = P.pcg(t.matvec, t.apply, g["b"], tol=float(g["tol"]), max_iters=2000)
     assert rep.converged and rep.iterations == repw.iterations
     assert np.linalg.norm(x - xw) <= 1e-9 * np.linalg.norm(xw)
