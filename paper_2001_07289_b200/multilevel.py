@@ -144,8 +144,21 @@ class Level2Bddc:
 
     def refactor(self, elem_mats):
         """Numeric setup for new element matrices on the same elements / boxes (the symbolic
-        part above is kept)."""
+        part above is kept). BDDC_L2_TIMING=1 prints the time of each stage (synchronising)."""
         torch = self._torch
+        import os
+        import sys
+        import time
+
+        timing = os.environ.get("BDDC_L2_TIMING") == "1" and self.device.type == "cuda"
+        tprev = [time.perf_counter()]
+
+        def mark(name):
+            if timing:
+                torch.cuda.synchronize(self.device)
+                now = time.perf_counter()
+                print(f"level-2 numeric: {name:<34s}{(now - tprev[0]) * 1e3:9.2f} ms", file=sys.stderr)
+                tprev[0] = now
         dev, n0 = self.device, self.n0
         nbox, nIp, nGp, nCp, nJ, nobj, E, ncp = self._dims
         mats = torch.as_tensor(elem_mats, dtype=torch.float64).to(dev)
@@ -161,6 +174,7 @@ class Level2Bddc:
         del Aall
         AII += torch.diag_embed((self.idxI >= n0).to(torch.float64))  # identity on the padding
         AGG += torch.diag_embed((self.idxG >= n0).to(torch.float64))
+        mark("assemble boxes")
         AII = 0.5 * (AII + AII.transpose(1, 2))
         validG = (self.idxG < n0).to(torch.float64)
         if dev.type == "cuda":
@@ -171,11 +185,14 @@ class Level2Bddc:
             self.upper = True
             AGI = AIG.transpose(1, 2).contiguous()       # column-major n_I x n_G, one box each
             LI = _own_potrf(torch, AII)                  # in place
+            mark("potrf A_II")
             Xt = AGI.clone()
             _own_trsm(torch, 0, LI, Xt)                  # L y = A_IG
             _own_trsm(torch, 1, LI, Xt)                  # L^T X = y
+            mark("X = A_II^-1 A_IG")
             S = AGG                                      # S = A_GG - A_IG^T X, in place
             _own_gemm(torch, True, False, -1.0, AGI, Xt, 1.0, S)
+            mark("Schur complement")
             del Xt
             S.add_(S.transpose(1, 2).clone()).mul_(0.5)
             s = (torch.diagonal(S, dim1=1, dim2=2) * validG).sum(1) / ngs  # mean diagonal per box
@@ -183,6 +200,7 @@ class Level2Bddc:
             S.baddbmm_(Cs.transpose(1, 2), Cs)           # K = S + s C^T C, in place
             del Cs
             LK = _own_potrf(torch, S)
+            mark("K = S + s C^T C, potrf")
             Yt = Cmat.clone()                            # column-major n_G x n_C = C^T
             _own_trsm(torch, 0, LK, Yt)
             _own_trsm(torch, 1, LK, Yt)
@@ -194,11 +212,13 @@ class Level2Bddc:
             _own_trsm(torch, 1, LI, eyeI)
             del LI, AII
             self.AIIinv = eyeI.add_(eyeI.transpose(1, 2).clone()).mul_(0.5)
+            mark("explicit A_II^-1 (and Y)")
             eyeG = torch.eye(nGp, dtype=torch.float64, device=dev).expand(nbox, -1, -1).contiguous()
             _own_trsm(torch, 0, LK, eyeG)
             _own_trsm(torch, 1, LK, eyeG)
             del LK, S, AGG
             self.Kinv = eyeG
+            mark("explicit K^-1")
             self.AGI = AGI
         else:  # CPU evaluation of the same formulas (the tests' checker of the device level 2)
             self.upper = False
@@ -222,13 +242,23 @@ class Level2Bddc:
             del self.Kinv
             self.T2 = T2.add_(T2.transpose(1, 2).clone()).mul_(0.5)
             self.PhiT = self.Phi.transpose(1, 2).contiguous()
+            mark("Phi, T2")
         Ecoarse = Ginv - s[:, None, None] * torch.eye(nCp, dtype=torch.float64, device=dev)
-        S00 = torch.zeros((nobj + 1, nobj + 1), dtype=torch.float64, device=dev)
-        S00.index_put_((self.idxC[:, :, None].expand(-1, -1, nCp), self.idxC[:, None, :].expand(-1, nCp, -1)),
-                       Ecoarse, accumulate=True)
-        S00 = S00[:nobj, :nobj]
-        self.S00 = 0.5 * (S00 + S00.T)
+        # only the valid (constraint, constraint) pairs of each box are scattered (the padded slots
+        # would all hit one address); S00 is exactly n00 x n00 and contiguous. Only the lower
+        # triangle is read by the factorization, so no symmetrisation pass is needed.
+        if getattr(self, "_s00_lin", None) is None:
+            okC = self.idxC < nobj
+            pair_ok = okC[:, :, None] & okC[:, None, :]
+            lin = self.idxC[:, :, None] * max(nobj, 1) + self.idxC[:, None, :]
+            self._s00_mask, self._s00_lin = pair_ok, lin[pair_ok]
+        S00 = torch.zeros(max(nobj, 1) * max(nobj, 1), dtype=torch.float64, device=dev)
+        S00.index_add_(0, self._s00_lin, Ecoarse[self._s00_mask])
+        S00 = S00.view(max(nobj, 1), max(nobj, 1))
+        self.S00 = S00
+        mark("assemble S00")
         self.L00 = torch.linalg.cholesky(self.S00) if nobj else None
+        mark("Cholesky of S00")
         self.S00inv = None
         if dev.type == "cuda" and 0 < nobj <= 8192:  # explicit inverse: the level-2 coarse solve is one GEMV
             n8 = -(-nobj // 8) * 8
