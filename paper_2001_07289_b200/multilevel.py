@@ -528,4 +528,6 @@ class ThreeLevelOperator:
         self.op.close()
 
     def __getattr__(self, name):  # apply, matvec, pcg, n, … of the wrapped operator
+        if name in ("op", "level2", "_fn"):  # not set yet: no recursion through self.op
+            raise AttributeError(name)
         return getattr(self.op, name)
