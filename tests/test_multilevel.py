@@ -84,3 +84,23 @@ def test_box_of_subdomains():
     assert b.tolist() == [0, 0, 1, 1, 0, 0, 1, 1]
     b3 = box_of_subdomains((2, 2, 4), (2, 2, 2))
     assert b3.tolist() == [0] * 8 + [1] * 8
+
+
+def test_stiffness_weights_are_a_partition_of_unity():
+    case = CASES[0]
+    orc = O.Oracle(case["dim"], case["cells"], case["subs"], case["split"], element=case["element"],
+                   coarse_scaling=case["mode"])
+    ids, mats = _coarse_elements(orc)
+    M = Level2Bddc(ids, torch.from_numpy(mats), box_of_subdomains(case["subs"], case["k"]), orc.n_coarse,
+                   weights="stiffness")
+    tot = torch.zeros(M.n0 + 1, dtype=torch.float64)
+    tot.index_add_(0, M.idxG.reshape(-1), M.wG.reshape(-1))
+    on_g2 = torch.unique(M.idxG[M.idxG < M.n0])
+    assert float((tot[on_g2] - 1.0).abs().max()) <= 1e-12
+    B = M.dense().numpy()
+    assert np.abs(B - B.T).max() <= 1e-10 * np.abs(B).max()
+    lam = np.linalg.eigvals(0.5 * (B + B.T) @ orc.coarse.toarray()).real
+    assert lam.min() >= 1.0 - 1e-8
+    with pytest.raises(ValueError):
+        Level2Bddc(ids, torch.from_numpy(mats), box_of_subdomains(case["subs"], case["k"]), orc.n_coarse,
+                   weights="nope")
