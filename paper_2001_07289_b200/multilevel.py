@@ -48,10 +48,12 @@ class Level2Bddc:
 
     ``elem_ids`` (E, ncp) int: global unknowns of each element, −1 padded. ``elem_mats``
     (E, ncp, ncp): dense symmetric element matrices (torch tensor or array; padding ignored).
-    ``box_of_elem`` (E,): level-2 subdomain of each element. Works on any torch device in FP64.
+    ``box_of_elem`` (E,): level-2 subdomain of each element. Runs on a CUDA device; ``checker=True``
+    allows the CPU evaluation of the same formulas, which only the tests use.
     """
 
-    def __init__(self, elem_ids, elem_mats, box_of_elem, n0: int, device=None, weights: str = "cardinality"):
+    def __init__(self, elem_ids, elem_mats, box_of_elem, n0: int, device=None, weights: str = "cardinality",
+                 checker: bool = False):
         import torch
 
         if weights not in ("cardinality", "stiffness"):
@@ -67,6 +69,9 @@ class Level2Bddc:
         mats = mats.to(dev)
         if mats.shape != (E, ncp, ncp):
             raise ValueError(f"element matrices have shape {tuple(mats.shape)}, expected {(E, ncp, ncp)}")
+        if dev.type != "cuda" and not checker:
+            raise RuntimeError("Level2Bddc runs on a CUDA device with this library's kernels (no CPU fallback); "
+                               "the CPU evaluation exists for the tests only (checker=True)")
         self.n0, self.device = int(n0), dev
         nbox = int(box_of_elem.max()) + 1 if E else 0
         self.n_boxes = nbox

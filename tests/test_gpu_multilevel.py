@@ -55,7 +55,7 @@ def test_three_level_operator(cuda_ok, case, k, extra):
     sloc = np.empty(nsub * ncp * ncp)
     assert op._lib.bddc_read_buffer(op._ctx, b"Sloc", 0, sloc.size, _capi.ptr(sloc, C.c_double)) == sloc.size
     cpu = P.Level2Bddc(plan.con_coarse, torch.from_numpy(sloc.reshape(nsub, ncp, ncp)),
-                       P.box_of_subdomains(pb["pair"].box_layout[0], k), L2.n0)
+                       P.box_of_subdomains(pb["pair"].box_layout[0], k), L2.n0, checker=True)
     r0 = torch.from_numpy(np.random.default_rng(3).standard_normal(L2.n0))
     a = L2.solve(r0.to(L2.device)).cpu()
     b = cpu.solve(r0)

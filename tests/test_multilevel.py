@@ -39,7 +39,7 @@ def test_level2_is_spd_and_bounded(case):
     ids, mats = _coarse_elements(orc)
     box = box_of_subdomains(case["subs"], case["k"])
     n0 = orc.n_coarse
-    M = Level2Bddc(ids, torch.from_numpy(mats), box, n0)
+    M = Level2Bddc(ids, torch.from_numpy(mats), box, n0, checker=True)
     assert M.n_boxes == np.prod([s // case["k"] for s in case["subs"]])
     assert M.n_coarse2 < n0 and M.n_gamma2 < n0
     B = M.dense().numpy()
@@ -65,7 +65,7 @@ def test_three_level_pcg_matches_two_level():
     b = O.uniform_f(orc.mesh.n_free, 0)
     x2, rep2 = O.pcg(orc.matvec, orc.apply, b, tol=1e-8)
     ids, mats = _coarse_elements(orc)
-    M = Level2Bddc(ids, torch.from_numpy(mats), box_of_subdomains(case["subs"], case["k"]), orc.n_coarse)
+    M = Level2Bddc(ids, torch.from_numpy(mats), box_of_subdomains(case["subs"], case["k"]), orc.n_coarse, checker=True)
 
     class Fac:
         def solve(self, r):
@@ -92,7 +92,7 @@ def test_stiffness_weights_are_a_partition_of_unity():
                    coarse_scaling=case["mode"])
     ids, mats = _coarse_elements(orc)
     M = Level2Bddc(ids, torch.from_numpy(mats), box_of_subdomains(case["subs"], case["k"]), orc.n_coarse,
-                   weights="stiffness")
+                   weights="stiffness", checker=True)
     tot = torch.zeros(M.n0 + 1, dtype=torch.float64)
     tot.index_add_(0, M.idxG.reshape(-1), M.wG.reshape(-1))
     on_g2 = torch.unique(M.idxG[M.idxG < M.n0])
@@ -103,4 +103,11 @@ def test_stiffness_weights_are_a_partition_of_unity():
     assert lam.min() >= 1.0 - 1e-8
     with pytest.raises(ValueError):
         Level2Bddc(ids, torch.from_numpy(mats), box_of_subdomains(case["subs"], case["k"]), orc.n_coarse,
-                   weights="nope")
+                   weights="nope", checker=True)
+
+
+def test_level2_refuses_cpu_without_checker_flag():
+    ids = np.array([[0, 1], [1, 2]])
+    mats = np.tile(np.array([[1.0, -1.0], [-1.0, 1.0]]) + np.eye(2), (2, 1, 1))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        Level2Bddc(ids, torch.from_numpy(mats), np.array([0, 1]), 3)
